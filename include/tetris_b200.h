@@ -1,0 +1,167 @@
+/*
+ * tetris_b200.h — C-ABI boundary of the B200-native RNS-CKKS evaluator.
+ *
+ * This is the thin layer the C++ host API (include/tetris_b200/*.hpp, the
+ * drop-in for the reference's proj/include/tetris/ evaluation path) calls into.
+ * Plain pointers, sizes and opaque handles only; no C++ or torch types.
+ *
+ * Data model (mirrors the reference's Poly, ring.hpp:204-374):
+ *   a "poly" is rows x N uint64 residues, row-major, rows = level+1+nspecial;
+ *   row r is reduced mod moduli[r <= level ? r : q_count + (r-level-1)]
+ *   (ring.hpp:227-229). nspecial is 0 or the ring's special count. Every
+ *   residue stored at the boundary is canonical in [0, q).
+ *   Batched entry points take `npolys` polys of identical shape laid out
+ *   back to back (stride rows*N words).
+ *
+ * All device pointers are device-global memory allocated with tg_alloc (or
+ * any cudaMalloc'd memory). `stream` is a cudaStream_t (NULL = legacy
+ * default stream). Every call is asynchronous on `stream` unless stated.
+ *
+ * Errors: every function returns 0 on success or a negative TG_E* code; the
+ * message is available from tg_last_error() (thread-local). Contract errors
+ * mirror the reference's TetrisError messages ("ring"/"rlwe"/"ckks" tags).
+ */
+#ifndef TETRIS_B200_H
+#define TETRIS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TG_OK 0
+#define TG_E_ARG (-1)     /* contract violation (shape/form/level)          */
+#define TG_E_CUDA (-2)    /* CUDA runtime error                              */
+#define TG_E_NOMEM (-3)   /* device allocation failed                        */
+#define TG_E_STATE (-4)   /* no device / context unusable                    */
+
+#define TG_FORM_COEFF 0   /* Form::coeff (ring.hpp:202) */
+#define TG_FORM_EVAL 1    /* Form::eval                 */
+
+typedef struct tg_context tg_context; /* RingParams + its NTT tables on device */
+typedef struct tg_gadget tg_gadget;   /* GadgetPlan + ModDown constants        */
+
+/* ---- library / errors -------------------------------------------------- */
+const char* tg_last_error(void);
+/* Number of CUDA devices visible (0 on a host without GPU). Never fails. */
+int tg_device_count(void);
+/* Library build string (arch, version). */
+const char* tg_build_info(void);
+
+/* ---- context: replaces RingParams (ring.hpp:116-195) ------------------- */
+/* Uploads the host-built NTT tables verbatim, so psi choice and the
+ * bit-reversed evaluation order are exactly the reference's
+ * (NttTables::init ring.hpp:25-51, build_eval_order_map ring.hpp:165-186).
+ *   tables:   4*nmod*N words: per modulus i, [w | w_shoup | winv | winv_shoup]
+ *   n_inv:    2*nmod words:   per modulus i, [n_inv, n_inv_shoup]
+ *   eval_exp: N entries; slot_of_exp: 2N entries.
+ * Rescale constants (ring.hpp:505-508) are derived from `moduli` here. */
+int tg_context_create(tg_context** out, int device, uint32_t degree, const uint64_t* moduli,
+                      uint32_t nmod, uint32_t special_count, const uint64_t* tables,
+                      const uint64_t* n_inv, const uint32_t* eval_exp,
+                      const uint32_t* slot_of_exp);
+void tg_context_destroy(tg_context* ctx);
+uint32_t tg_context_degree(const tg_context* ctx);
+
+/* ---- memory ------------------------------------------------------------- */
+/* Stream-ordered allocation from the context device's memory pool. */
+int tg_alloc(tg_context* ctx, void** ptr, size_t bytes, void* stream);
+int tg_free(tg_context* ctx, void* ptr, void* stream);
+int tg_memcpy_h2d(tg_context* ctx, void* dst, const void* src, size_t bytes, void* stream);
+int tg_memcpy_d2h(tg_context* ctx, void* dst, const void* src, size_t bytes, void* stream);
+int tg_memcpy_d2d(tg_context* ctx, void* dst, const void* src, size_t bytes, void* stream);
+int tg_memset0(tg_context* ctx, void* dst, size_t bytes, void* stream);
+int tg_stream_sync(tg_context* ctx, void* stream);
+/* A non-blocking stream on the context's device (*stream = cudaStream_t). */
+int tg_stream_create(tg_context* ctx, void** stream);
+int tg_stream_destroy(tg_context* ctx, void* stream);
+/* Device index the context lives on. */
+int tg_context_device(const tg_context* ctx);
+
+/* ---- ring layer --------------------------------------------------------- */
+/* Poly::ntt_forward / NttTables::forward (ring.hpp:64-80, :234-239), in place.
+ * Negacyclic CT, natural -> bit-reversed evaluation order. */
+int tg_ntt_forward(tg_context* ctx, uint64_t* data, int level, int nspecial, uint32_t npolys,
+                   void* stream);
+/* Poly::ntt_inverse / NttTables::inverse (ring.hpp:82-101, :241-246), in place. */
+int tg_ntt_inverse(tg_context* ctx, uint64_t* data, int level, int nspecial, uint32_t npolys,
+                   void* stream);
+/* Out-of-place variants: out receives the transform of in (in unchanged;
+ * out may equal in). */
+int tg_ntt_forward_oop(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, int nspecial,
+                       uint32_t npolys, void* stream);
+int tg_ntt_inverse_oop(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, int nspecial,
+                       uint32_t npolys, void* stream);
+/* Poly::add_inplace / sub_inplace / negate_inplace (ring.hpp:250-276).
+ * out may alias a or b. For neg, b is ignored. op: 0 add, 1 sub, 2 neg. */
+int tg_poly_addsub(tg_context* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int op,
+                   int level, int nspecial, uint32_t npolys, void* stream);
+/* Poly::mul_pointwise_inplace (ring.hpp:278-288): out = a*b mod q (eval form). */
+int tg_poly_mul(tg_context* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int level,
+                int nspecial, uint32_t npolys, void* stream);
+/* Poly::mul_acc_pointwise (ring.hpp:290-304): out += a*b mod q. */
+int tg_poly_mul_acc(tg_context* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b,
+                    int level, int nspecial, uint32_t npolys, void* stream);
+/* Poly::mul_scalar_inplace (ring.hpp:307-315): scalar given per MODULUS INDEX
+ * (nmod words, host memory); each is reduced mod its row modulus first. */
+int tg_poly_mul_scalar(tg_context* ctx, uint64_t* out, const uint64_t* a,
+                       const uint64_t* scalar_per_modulus, int level, int nspecial,
+                       uint32_t npolys, void* stream);
+/* Evaluator::add_scalar's residue update (ckks.hpp:296-313): adds
+ * add_per_modulus[m] to every entry (eval form) or to index 0 (coeff form). */
+int tg_poly_add_scalar(tg_context* ctx, uint64_t* out, const uint64_t* a,
+                       const uint64_t* add_per_modulus, int form, int level, int nspecial,
+                       uint32_t npolys, void* stream);
+/* automorphism_apply (ring.hpp:410-436): X -> X^g, g odd; coeff form is a
+ * signed scatter, eval form a slot gather. out must not alias in. */
+int tg_automorphism(tg_context* ctx, uint64_t* out, const uint64_t* in, uint64_t exponent,
+                    int form, int level, int nspecial, uint32_t npolys, void* stream);
+/* rescale_round (ring.hpp:493-518): coeff form, level -> level-1 rows.
+ * out (level rows) must not alias in (level+1 rows). */
+int tg_rescale(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, uint32_t npolys,
+               void* stream);
+
+/* ---- CKKS products ------------------------------------------------------ */
+/* Evaluator::mul tensor step (ckks.hpp:229-237), eval form inputs:
+ * p0 = x0*y0, p1 = x0*y1 + x1*y0, p2 = x1*y1. Outputs must not alias inputs. */
+int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const uint64_t* x0,
+              const uint64_t* x1, const uint64_t* y0, const uint64_t* y1, int level,
+              uint32_t npolys, void* stream);
+/* Evaluator::mul_plain residue step (ckks.hpp:257-265): every part row r
+ * (modulus index m) times plain row m; plain holds >= level+1 rows. */
+int tg_mul_plain(tg_context* ctx, uint64_t* out, const uint64_t* ct_part, const uint64_t* plain,
+                 int level, uint32_t nparts, void* stream);
+
+/* ---- key switching ------------------------------------------------------ */
+/* GadgetPlan (rlwe.hpp:28-206) for this ring: RNS digit groups of group_size
+ * primes (base2_bits must be 0: base-2 refinement is not on the device path)
+ * and the ModDown constants of mod_down_p (rlwe.hpp:555-579). */
+int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group_size, uint32_t base2_bits);
+void tg_gadget_destroy(tg_gadget* g);
+/* GadgetPlan::digit_count (rlwe.hpp:54-61). */
+uint32_t tg_gadget_digit_count(const tg_gadget* g, int level);
+
+/* GadgetPlan::decompose = ModUp (rlwe.hpp:65-139): d (coeff, level, no
+ * specials) -> digit_count(level) digit polys of level+1+K rows each, in EVAL
+ * form, written back to back at `digits`. Uncorrected fast base conversion. */
+int tg_modup(tg_gadget* g, uint64_t* digits, const uint64_t* d, int level, void* stream);
+/* KeyContext::ks_inner (rlwe.hpp:501-540): acc_{0,1} = sum_i digit_i * key_{b,a}[i]
+ * over key rows (key_row map rlwe.hpp:517-518), then iNTT and mod_down_p.
+ * key: digits x 2 x (max_level+1+K) x N words, [digit][b|a][row][N].
+ * out0/out1: coeff form, level+1 rows. */
+int tg_ks_inner(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* digits,
+                uint32_t ndigits, const uint64_t* key, uint32_t key_digits, int level,
+                void* stream);
+/* KeyContext::mod_down_p (rlwe.hpp:547-592): in (coeff, level+1+K rows) ->
+ * out (coeff, level+1 rows), centered fast base conversion of the specials. */
+int tg_mod_down(tg_gadget* g, uint64_t* out, const uint64_t* in, int level, void* stream);
+/* KeyContext::switch_key_apply (rlwe.hpp:542-544) = ks_inner(decompose(d)). */
+int tg_switch_key_apply(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
+                        const uint64_t* key, uint32_t key_digits, int level, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TETRIS_B200_H */

@@ -1,0 +1,131 @@
+// tetris_b200 CKKS layer: encoder (host), evaluation keys, Evaluator,
+// Chebyshev evaluation, slot sum and the private threshold. Drop-in for the
+// reference ckks.hpp:24-370, :515-615 and threshold.hpp:13-157.
+//
+// The Evaluator keeps the reference's per-ciphertext, by-value API; scale
+// bookkeeping, rounding of host constants and every contract check follow
+// the reference's expression order exactly, so outputs are bit-identical.
+#pragma once
+
+#include <complex>
+#include <functional>
+#include <map>
+
+#include "tetris_b200/keys.hpp"
+
+namespace tetris_b200 {
+
+using cplx = std::complex<double>;
+
+// Canonical-embedding encoder (ckks.hpp:24-148); O(n^2) special DFT on the
+// host, parallelised over output indices (per-index summation order kept).
+class Encoder {
+public:
+    Encoder(const RingParams& ring, u32 nslots);
+    const RingParams& ring() const { return *ring_; }
+    u32 slots() const { return n_; }
+    std::vector<cplx> dft(const std::vector<cplx>& w) const;
+    std::vector<cplx> dft_inv(const std::vector<cplx>& v) const;
+    Poly encode_slots(const std::vector<cplx>& v, double scale, int level) const;
+    std::vector<cplx> decode_slots(const Poly& poly, double scale) const;
+    Poly encode_coeffs(const std::vector<double>& v, double scale, int level) const;
+    std::vector<double> decode_coeffs(const Poly& poly, double scale, std::size_t count) const;
+    // host residues of encode_slots (no device needed)
+    std::vector<u64> encode_slots_host(const std::vector<cplx>& v, double scale, int level) const;
+    std::vector<cplx> decode_slots_host(const u64* rows01, int level, double scale) const;
+
+private:
+    const RingParams* ring_;
+    u32 n_;
+    std::vector<cplx> psi_;
+    std::vector<u32> rot5_;
+};
+
+struct EvalKeys {
+    SwitchingKey relin;
+    std::map<u64, SwitchingKey> galois;
+    const SwitchingKey& galois_key(u64 exponent) const;
+    bool has(u64 exponent) const { return galois.count(exponent) != 0; }
+};
+
+u64 rotation_exponent(const RingParams& ring, u32 k);
+u64 conjugation_exponent(const RingParams& ring);
+
+class Evaluator {
+public:
+    explicit Evaluator(const KeyContext& ctx) : ctx_(&ctx) {}
+    const KeyContext& key_context() const { return *ctx_; }
+    const RingParams& ring() const { return ctx_->ring(); }
+
+    static void check_scales_match(double a, double b);
+    void align_levels(Ciphertext& a, Ciphertext& b) const;
+    Ciphertext add(const Ciphertext& a, const Ciphertext& b) const;
+    Ciphertext sub(const Ciphertext& a, const Ciphertext& b) const;
+    Ciphertext mul(const Ciphertext& a, const Ciphertext& b) const;
+    Ciphertext mul_relin(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys) const;
+    Ciphertext mul_plain(const Ciphertext& ct, const Poly& plain_eval, double plain_scale) const;
+    Ciphertext mul_scalar(const Ciphertext& ct, double c, double scalar_scale) const;
+    static u64 scaled_residue(double value, u64 q);
+    Ciphertext add_scalar(const Ciphertext& ct, double c) const;
+    Ciphertext rescale(const Ciphertext& ct) const;
+    Ciphertext rotate(const Ciphertext& ct, u32 k, const EvalKeys& keys) const;
+    Ciphertext conjugate(const Ciphertext& ct, const EvalKeys& keys) const;
+
+private:
+    const KeyContext* ctx_;
+};
+
+// Chebyshev ladder evaluation (ckks.hpp:515-579), bit-exact with the reference.
+Ciphertext eval_chebyshev(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
+                          const EvalKeys& keys);
+std::vector<double> power_to_chebyshev(const std::vector<double>& pow_coeffs);
+// log2(n) rotate-and-add (ckks.hpp:605-615).
+Ciphertext inner_sum(const Evaluator& ev, const Ciphertext& ct, u32 n, const EvalKeys& keys);
+
+// ---------------------------------------------------------------------------
+// Threshold (threshold.hpp)
+// ---------------------------------------------------------------------------
+struct ThresholdParams {
+    u32 alpha = 8;
+    u32 beta = 12;
+    std::vector<u32> degrees;
+    double epsilon = 1.0;
+};
+
+struct ChainStage {
+    u32 degree = 0;
+    double gamma = 0, upper = 1;
+    std::vector<double> cheb;
+    double error = 0;
+};
+
+struct MinimaxChain {
+    ThresholdParams params;
+    std::vector<ChainStage> stages;
+    double sign_error = 0;
+    double achieved_beta = 0;
+    bool meets_target() const { return achieved_beta >= double(params.beta); }
+    std::vector<double> eval_coeffs(std::size_t i) const;
+    double eval_step(double x) const;
+    u32 levels_required() const;
+};
+
+// Remez minimax of sign on [-U,-gamma] u [gamma,U] (remez.hpp:101-231).
+struct MinimaxResult {
+    u32 degree = 0;
+    long double gamma = 0, upper = 1;
+    std::vector<long double> odd_coeffs;
+    long double error = 0;
+    std::vector<long double> nodes;
+    u32 iterations = 0;
+    long double eval(long double x) const;
+};
+MinimaxResult remez_minimax(long double gamma, long double upper, u32 degree, u32 max_iters = 64);
+MinimaxChain build_chain(const ThresholdParams& params);
+
+Ciphertext eval_private_threshold(const Evaluator& ev, const Ciphertext& ct_scores, const Ciphertext& ct_t,
+                                  const Ciphertext& ct_norm, const MinimaxChain& chain, const EvalKeys& keys);
+Ciphertext eval_private_threshold_plain_norm(const Evaluator& ev, const Ciphertext& ct_scores, const Ciphertext& ct_t,
+                                             double norm, const MinimaxChain& chain, const EvalKeys& keys);
+
+}  // namespace tetris_b200

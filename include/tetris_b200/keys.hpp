@@ -1,0 +1,145 @@
+// tetris_b200 RLWE layer: gadget decomposition, keys, encryption, key
+// switching, relinearisation and Galois automorphisms. Drop-in for the
+// reference rlwe.hpp evaluation path (keygen/encrypt/decrypt included so a
+// caller can switch wholesale). Key material is sampled on the host from the
+// reference's RNG streams and resident in HBM in the layout the key-switch
+// kernels read: [digit][b|a][max_level+1+K rows][N].
+#pragma once
+
+#include <map>
+#include <utility>
+
+#include "tetris_b200/core.hpp"
+
+namespace tetris_b200 {
+
+struct GadgetVector {
+    u32 group_size = 1;
+    u32 base2_bits = 0;  // base-2 refinement (rlwe.hpp:103-135); host-only, not on the device path
+    u32 sub_digits(u64 q) const;
+};
+
+// Replaces GadgetPlan (rlwe.hpp:28-206). The device tables (src_scale,
+// conv_w, ModDown constants) live in a tg_gadget.
+class GadgetPlan {
+public:
+    GadgetPlan() = default;
+    GadgetPlan(const RingParams& ring, GadgetVector cfg);
+    ~GadgetPlan();
+    GadgetPlan(const GadgetPlan&) = delete;
+    GadgetPlan& operator=(const GadgetPlan&) = delete;
+
+    const RingParams& ring() const { return *ring_; }
+    const GadgetVector& config() const { return cfg_; }
+    u32 group_count(int level) const { return (u32(level) + cfg_.group_size) / cfg_.group_size; }
+    u32 digit_count(int level) const;
+    // ModUp: digits in eval form, each level+1+K rows (rlwe.hpp:65-139).
+    std::vector<Poly> decompose(const Poly& d) const;
+    // w_digit * P mod q_t per digit (rlwe.hpp:142-165), host.
+    std::vector<std::vector<u64>> key_scalars() const;
+    tg_gadget* dev() const;
+
+private:
+    const RingParams* ring_ = nullptr;
+    GadgetVector cfg_;
+    mutable std::once_flag once_;
+    mutable tg_gadget* dev_ = nullptr;
+};
+
+class SecretKey {
+public:
+    SecretKey() = default;
+    SecretKey(const RingParams& ring, const NoiseParams& noise, Rng& rng);
+    SecretKey(const RingParams& ring, std::vector<i64> coeffs, u64 id);
+
+    const RingParams& ring() const { return *ring_; }
+    u32 hamming_weight() const { return hamming_weight_; }
+    u64 id() const { return id_; }
+    const std::vector<i64>& coeffs() const { return coeffs_; }
+    // eval-form rows for (level, nspecial), extracted from the full key
+    Poly shaped(int level, int nspecial) const;
+
+private:
+    const RingParams* ring_ = nullptr;
+    u32 hamming_weight_ = 0;
+    u64 id_ = 0;
+    std::vector<i64> coeffs_;
+    Poly eval_full_;
+};
+
+struct PublicKey {
+    Poly b, a;
+    u64 sk_id = 0;
+};
+
+enum class Domain { coeffs, slots };
+
+// Replaces reference Ciphertext (rlwe.hpp:275-317).
+struct Ciphertext {
+    std::vector<Poly> parts;
+    double scale = 1.0;
+    Domain domain = Domain::coeffs;
+    u64 sk_id = 0;
+    double noise_bound = 0.0;
+
+    const RingParams& ring() const { return parts.at(0).ring(); }
+    int level() const { return parts.at(0).level(); }
+    Form form() const { return parts.at(0).form(); }
+    int degree() const { return int(parts.size()) - 1; }
+    void to_coeff();
+    void to_eval();
+    void drop_to_level(int new_level);
+    void add_inplace(const Ciphertext& o);
+    void sub_inplace(const Ciphertext& o);
+    void negate_inplace();
+};
+
+// Switching key (rlwe.hpp:325-333). b[i]/a[i] are views into one HBM block.
+struct SwitchingKey {
+    GadgetVector gadget;
+    u64 from_id = 0, to_id = 0;
+    u64 a_seed = 0;
+    std::vector<Poly> b, a;
+    std::shared_ptr<DeviceBuffer> block;  // [digit][b|a][rows][N]
+    const RingParams& ring() const { return b.at(0).ring(); }
+    u32 digits() const { return u32(b.size()); }
+    const u64* device_data() const { return block ? block->data() : nullptr; }
+};
+
+// Replaces KeyContext (rlwe.hpp:335-682).
+class KeyContext {
+public:
+    KeyContext(const RingParams& ring, NoiseParams noise, GadgetVector gadget);
+
+    const RingParams& ring() const { return *ring_; }
+    const NoiseParams& noise() const { return noise_; }
+    const GadgetPlan& plan() const { return *plan_; }
+
+    std::pair<SecretKey, PublicKey> keygen(Rng& rng) const;
+    PublicKey make_public(const SecretKey& sk, Rng& rng) const;
+    Ciphertext encrypt(const SecretKey& sk, const Poly& m, double scale, Rng& rng,
+                       Domain domain = Domain::coeffs) const;
+    Ciphertext encrypt_pk(const PublicKey& pk, const Poly& m, double scale, Rng& rng,
+                          Domain domain = Domain::coeffs) const;
+    Poly decrypt(const SecretKey& sk, const Ciphertext& ct) const;
+    Ciphertext zero_ciphertext(int level, double scale, u64 sk_id, Domain domain = Domain::coeffs) const;
+
+    SwitchingKey switch_key_gen(const SecretKey& from, const SecretKey& to, Rng& rng) const;
+    std::pair<Poly, Poly> ks_inner(const std::vector<Poly>& digits, const SwitchingKey& swk) const;
+    std::pair<Poly, Poly> switch_key_apply(const Poly& d, const SwitchingKey& swk) const;
+    Poly mod_down_p(const Poly& x) const;
+
+    SwitchingKey relin_key_gen(const SecretKey& sk, Rng& rng) const;
+    Ciphertext relinearize(const Ciphertext& ct, const SwitchingKey& rlk) const;
+    SwitchingKey galois_key_gen(const SecretKey& sk, u64 exponent, Rng& rng) const;
+    Ciphertext apply_galois(const Ciphertext& ct, u64 exponent, const SwitchingKey& swk) const;
+    double ks_noise_estimate() const;
+    SecretKey square_secret(const SecretKey& sk) const;
+
+private:
+    const RingParams* ring_;
+    NoiseParams noise_;
+    std::shared_ptr<GadgetPlan> plan_;
+};
+
+}  // namespace tetris_b200

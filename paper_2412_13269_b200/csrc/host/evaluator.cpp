@@ -1,0 +1,452 @@
+// CKKS layer on the device: Encoder (host DFT), Evaluator, eval_chebyshev,
+// inner_sum (reference ckks.hpp:24-615). Every ciphertext op runs on the GPU;
+// host work is limited to scale bookkeeping and exact integer constants, in
+// the reference's expression order.
+#include <algorithm>
+#include <cmath>
+#include <thread>
+
+#include "internal.hpp"
+#include "tetris_b200/evaluator.hpp"
+
+namespace tetris_b200 {
+
+using detail::contiguous;
+using detail::exclusively_owned;
+using detail::fresh_parts;
+using detail::tg_form;
+
+// ---------------------------------------------------------------------------
+// Encoder (ckks.hpp:24-148)
+// ---------------------------------------------------------------------------
+Encoder::Encoder(const RingParams& ring, u32 nslots) : ring_(&ring), n_(nslots) {
+    if (n_ < 2 || (n_ & (n_ - 1)) != 0 || n_ > ring.degree() / 2)
+        throw TetrisError("ckks", "slot count must be a power of two <= N/2");
+    const u32 m = 4 * n_;
+    psi_.resize(m);
+    for (u32 t = 0; t < m; ++t) {
+        const double ang = M_PI * double(t) / double(2 * n_);
+        psi_[t] = cplx(std::cos(ang), std::sin(ang));
+    }
+    rot5_.resize(n_);
+    u64 g = 1;
+    for (u32 j = 0; j < n_; ++j) {
+        rot5_[j] = u32(g);
+        g = (g * 5) % m;
+    }
+}
+
+// Runs body(lo, hi) over [0, n) on up to hardware_concurrency threads. Each
+// output index is computed by exactly one thread with the sequential inner
+// summation order, so the result does not depend on the thread count.
+template <class F>
+static void parallel_for(u32 n, F body) {
+    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    unsigned nt = std::min<unsigned>(hw, std::max<u32>(1, n / 256));
+    if (nt <= 1) {
+        body(0u, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const u32 per = (n + nt - 1) / nt;
+    for (unsigned i = 0; i < nt; ++i) {
+        const u32 lo = i * per, hi = std::min(n, lo + per);
+        if (lo < hi) th.emplace_back(body, lo, hi);
+    }
+    for (auto& t : th) t.join();
+}
+
+std::vector<cplx> Encoder::dft(const std::vector<cplx>& w) const {
+    std::vector<cplx> out(n_);
+    const u64 mask = 4 * u64(n_);
+    parallel_for(n_, [&](u32 lo, u32 hi) {
+        for (u32 j = lo; j < hi; ++j) {
+            cplx acc{0, 0};
+            for (u32 t = 0; t < n_; ++t) acc += w[t] * psi_[u32((u64(t) * rot5_[j]) % mask)];
+            out[j] = acc;
+        }
+    });
+    return out;
+}
+
+std::vector<cplx> Encoder::dft_inv(const std::vector<cplx>& v) const {
+    std::vector<cplx> out(n_);
+    const u64 mask = 4 * u64(n_);
+    parallel_for(n_, [&](u32 lo, u32 hi) {
+        for (u32 t = lo; t < hi; ++t) {
+            cplx acc{0, 0};
+            for (u32 j = 0; j < n_; ++j) acc += v[j] * std::conj(psi_[u32((u64(t) * rot5_[j]) % mask)]);
+            out[t] = acc / double(n_);
+        }
+    });
+    return out;
+}
+
+std::vector<u64> Encoder::encode_slots_host(const std::vector<cplx>& v, double scale, int level) const {
+    if (v.size() != n_) throw TetrisError("ckks", "slot vector length mismatch");
+    const std::vector<cplx> w = dft_inv(v);
+    const u32 N = ring_->degree(), stride = N / (2 * n_);
+    double bound = 0;
+    for (const cplx& c : w) bound = std::max({bound, std::abs(c.real()), std::abs(c.imag())});
+    if (level == 0 && bound * scale * 2 >= double(ring_->modulus(0)))
+        throw TetrisError("ckks", "plaintext overflows the level-0 modulus");
+    std::vector<u64> res(std::size_t(level + 1) * N, 0);
+    for (u32 t = 0; t < n_; ++t) {
+        const i64 re = round_half_away(w[t].real() * scale);
+        const i64 im = round_half_away(w[t].imag() * scale);
+        for (int r = 0; r <= level; ++r) {
+            const u64 q = ring_->modulus(r);
+            res[std::size_t(r) * N + std::size_t(t) * stride] = from_centered(re, q);
+            res[std::size_t(r) * N + std::size_t(n_ + t) * stride] = from_centered(im, q);
+        }
+    }
+    return res;
+}
+
+Poly Encoder::encode_slots(const std::vector<cplx>& v, double scale, int level) const {
+    if (level < 0 || level > ring_->max_level()) throw TetrisError("ring", "poly level out of range");
+    return Poly::from_host(*ring_, encode_slots_host(v, scale, level), level, Form::coeff);
+}
+
+// Exact centered value from rows 0 and 1 (ckks.hpp:123-134).
+static i128 centered_from_rows(const RingParams& ring, int level, u64 r0, u64 r1) {
+    if (level == 0) return to_centered(r0, ring.modulus(0));
+    const u64 q0 = ring.modulus(0), q1 = ring.modulus(1);
+    const u64 d = sub_mod(r1 % q1, r0 % q1, q1);
+    const u64 t = mul_mod(d, inv_mod(q0 % q1, q1), q1);
+    i128 x = i128(r0) + i128(q0) * i128(t);
+    const i128 q = i128(q0) * i128(q1);
+    if (x > q / 2) x -= q;
+    return x;
+}
+
+std::vector<cplx> Encoder::decode_slots_host(const u64* rows01, int level, double scale) const {
+    const u32 N = ring_->degree(), stride = N / (2 * n_);
+    const u64* row1 = level == 0 ? rows01 : rows01 + N;
+    std::vector<cplx> w(n_);
+    for (u32 t = 0; t < n_; ++t) {
+        const std::size_t i0 = std::size_t(t) * stride, i1 = std::size_t(n_ + t) * stride;
+        const double re = double(centered_from_rows(*ring_, level, rows01[i0], row1[i0])) / scale;
+        const double im = double(centered_from_rows(*ring_, level, rows01[i1], row1[i1])) / scale;
+        w[t] = cplx(re, im);
+    }
+    return dft(w);
+}
+
+static std::vector<u64> download_rows01(const Poly& p) {
+    const u32 N = p.ring().degree();
+    const int nrows = p.level() == 0 ? 1 : 2;
+    std::vector<u64> h(std::size_t(nrows) * N);
+    check_tg(tg_memcpy_d2h(p.ring().dev(), h.data(), p.data(), h.size() * 8, p.ring().stream()));
+    p.ring().synchronize();
+    return h;
+}
+
+// Reads rows 0/1 as stored (the reference does not convert forms either).
+std::vector<cplx> Encoder::decode_slots(const Poly& poly, double scale) const {
+    const std::vector<u64> h = download_rows01(poly);
+    return decode_slots_host(h.data(), poly.level(), scale);
+}
+
+Poly Encoder::encode_coeffs(const std::vector<double>& v, double scale, int level) const {
+    const u32 N = ring_->degree();
+    if (v.size() > N) throw TetrisError("ckks", "coeff vector too long");
+    const u32 stride = N / u32(v.size());
+    std::vector<u64> res(std::size_t(level + 1) * N, 0);
+    for (std::size_t t = 0; t < v.size(); ++t) {
+        const i64 c = round_half_away(v[t] * scale);
+        if (std::abs(double(c)) * 2 >= double(ring_->modulus(0)) && level == 0)
+            throw TetrisError("ckks", "plaintext overflows the level-0 modulus");
+        for (int r = 0; r <= level; ++r) res[std::size_t(r) * N + t * stride] = from_centered(c, ring_->modulus(r));
+    }
+    return Poly::from_host(*ring_, res, level, Form::coeff);
+}
+
+std::vector<double> Encoder::decode_coeffs(const Poly& poly, double scale, std::size_t count) const {
+    const Poly& c = poly;
+    const std::vector<u64> h = download_rows01(c);
+    const u32 N = ring_->degree(), stride = N / u32(count);
+    const u64* row1 = c.level() == 0 ? h.data() : h.data() + N;
+    std::vector<double> v(count);
+    for (std::size_t t = 0; t < count; ++t)
+        v[t] = double(centered_from_rows(*ring_, c.level(), h[t * stride], row1[t * stride])) / scale;
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// EvalKeys / exponents (ckks.hpp:155-173)
+// ---------------------------------------------------------------------------
+const SwitchingKey& EvalKeys::galois_key(u64 exponent) const {
+    auto it = galois.find(exponent);
+    if (it == galois.end()) throw TetrisError("ckks", "missing rotation key for exponent " + std::to_string(exponent));
+    return it->second;
+}
+
+u64 rotation_exponent(const RingParams& ring, u32 k) { return pow_mod(5, k, 2 * u64(ring.degree())); }
+u64 conjugation_exponent(const RingParams& ring) { return 2 * u64(ring.degree()) - 1; }
+
+// ---------------------------------------------------------------------------
+// Evaluator (ckks.hpp:181-335)
+// ---------------------------------------------------------------------------
+void Evaluator::check_scales_match(double a, double b) {
+    if (std::abs(a / b - 1.0) > 1e-4) throw TetrisError("ckks", "scaling factors diverged beyond tolerance");
+}
+
+void Evaluator::align_levels(Ciphertext& a, Ciphertext& b) const {
+    const int lvl = std::min(a.level(), b.level());
+    if (a.level() != lvl) {
+        a.to_coeff();
+        a.drop_to_level(lvl);
+    }
+    if (b.level() != lvl) {
+        b.to_coeff();
+        b.drop_to_level(lvl);
+    }
+}
+
+Ciphertext Evaluator::add(const Ciphertext& a, const Ciphertext& b) const {
+    Ciphertext x = a, y = b;
+    align_levels(x, y);
+    check_scales_match(x.scale, y.scale);
+    if (x.form() != y.form()) {
+        x.to_coeff();
+        y.to_coeff();
+    }
+    x.add_inplace(y);
+    return x;
+}
+
+Ciphertext Evaluator::sub(const Ciphertext& a, const Ciphertext& b) const {
+    Ciphertext x = a, y = b;
+    align_levels(x, y);
+    check_scales_match(x.scale, y.scale);
+    if (x.form() != y.form()) {
+        x.to_coeff();
+        y.to_coeff();
+    }
+    x.sub_inplace(y);
+    return x;
+}
+
+// Tensor product (ckks.hpp:220-245): one fused kernel for the 4 products.
+Ciphertext Evaluator::mul(const Ciphertext& a, const Ciphertext& b) const {
+    if (a.domain != b.domain) throw TetrisError("ckks", "domain tag mismatch in mul");
+    if (a.degree() != 1 || b.degree() != 1) throw TetrisError("ckks", "mul expects degree-1 operands");
+    Ciphertext x = a, y = b;
+    align_levels(x, y);
+    if (x.level() == 0) throw TetrisError("ckks", "exhausted ciphertext: no level left to rescale");
+    x.to_eval();
+    y.to_eval();
+    const RingParams& R = ring();
+    const int lvl = x.level();
+    std::vector<Poly> p = fresh_parts(R, 3, lvl, Form::eval);
+    check_tg(tg_tensor(R.dev(), const_cast<u64*>(p[0].data()), const_cast<u64*>(p[1].data()),
+                       const_cast<u64*>(p[2].data()), x.parts[0].data(), x.parts[1].data(), y.parts[0].data(),
+                       y.parts[1].data(), lvl, 1, R.stream()));
+    Ciphertext out;
+    out.parts = std::move(p);
+    out.scale = x.scale * y.scale;
+    out.domain = x.domain;
+    out.sk_id = x.sk_id;
+    out.noise_bound = x.noise_bound * y.scale + y.noise_bound * x.scale;
+    return out;
+}
+
+Ciphertext Evaluator::mul_relin(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys) const {
+    return ctx_->relinearize(mul(a, b), keys.relin);
+}
+
+Ciphertext Evaluator::mul_plain(const Ciphertext& ct, const Poly& plain_eval, double plain_scale) const {
+    Ciphertext out = ct;
+    out.to_eval();
+    const RingParams& R = ring();
+    const int lvl = out.level();
+    if (plain_eval.level() < lvl || plain_eval.nspecial() != 0)
+        throw TetrisError("ckks", "plaintext has fewer rows than the ciphertext");
+    const std::size_t np = out.parts.size();
+    std::vector<Poly> dst = fresh_parts(R, int(np), lvl, Form::eval);
+    if (contiguous(out.parts, 0, np)) {
+        check_tg(tg_mul_plain(R.dev(), const_cast<u64*>(dst[0].data()), out.parts[0].data(), plain_eval.data(), lvl,
+                              u32(np), R.stream()));
+    } else {
+        for (std::size_t i = 0; i < np; ++i)
+            check_tg(tg_mul_plain(R.dev(), const_cast<u64*>(dst[i].data()), out.parts[i].data(), plain_eval.data(),
+                                  lvl, 1, R.stream()));
+    }
+    out.parts = std::move(dst);
+    out.scale = ct.scale * plain_scale;
+    out.noise_bound = ct.noise_bound * plain_scale;
+    return out;
+}
+
+// Applies a per-modulus Shoup scalar to every part, batched when contiguous.
+static void scale_parts(Ciphertext& out, const std::vector<u64>& per_mod) {
+    const std::size_t np = out.parts.size();
+    const Poly& p0 = out.parts[0];
+    const RingParams& R = p0.ring();
+    if (contiguous(out.parts, 0, np)) {
+        std::vector<Poly> dst = fresh_parts(R, int(np), p0.level(), p0.form(), p0.nspecial());
+        check_tg(tg_poly_mul_scalar(R.dev(), const_cast<u64*>(dst[0].data()), p0.data(), per_mod.data(), p0.level(),
+                                    p0.nspecial(), u32(np), R.stream()));
+        out.parts = std::move(dst);
+        return;
+    }
+    for (auto& part : out.parts) part.mul_scalar_inplace(per_mod);
+}
+
+Ciphertext Evaluator::mul_scalar(const Ciphertext& ct, double c, double scalar_scale) const {
+    if (std::abs(c) * scalar_scale >= 9.0e18) throw TetrisError("ckks", "scalar multiplier exceeds the integer range");
+    const i64 v = round_half_away(c * scalar_scale);
+    Ciphertext out = ct;
+    std::vector<u64> per_mod(ring().moduli().size());
+    for (std::size_t i = 0; i < per_mod.size(); ++i) per_mod[i] = from_centered(v, ring().moduli()[i]);
+    scale_parts(out, per_mod);
+    out.scale = ct.scale * scalar_scale;
+    return out;
+}
+
+u64 Evaluator::scaled_residue(double value, u64 q) {
+    if (std::abs(value) < 9.0e18) return from_centered(round_half_away(value), q);
+    const long double r = std::fmod((long double)value, (long double)q);
+    return from_centered((i64)llroundl(r), q);
+}
+
+Ciphertext Evaluator::add_scalar(const Ciphertext& ct, double c) const {
+    Ciphertext out = ct;
+    const Poly& p0 = ct.parts[0];
+    const RingParams& R = ring();
+    std::vector<u64> add(R.moduli().size(), 0);
+    for (int r = 0; r < p0.rows(); ++r) add[p0.modulus_index(r)] = scaled_residue(c * ct.scale, p0.row_modulus(r));
+    std::vector<Poly> dst = fresh_parts(R, 1, p0.level(), p0.form(), p0.nspecial());
+    check_tg(tg_poly_add_scalar(R.dev(), const_cast<u64*>(dst[0].data()), p0.data(), add.data(), tg_form(p0.form()),
+                                p0.level(), p0.nspecial(), 1, R.stream()));
+    out.parts[0] = dst[0];
+    return out;
+}
+
+Ciphertext Evaluator::rescale(const Ciphertext& ct) const {
+    if (ct.level() == 0) throw TetrisError("ckks", "cannot rescale at level 0");
+    Ciphertext out = ct;
+    out.to_coeff();
+    const u64 ql = ring().modulus(u32(ct.level()));
+    const std::size_t np = out.parts.size();
+    if (contiguous(out.parts, 0, np)) {
+        const RingParams& R = ring();
+        const int lvl = out.level();
+        std::vector<Poly> dst = fresh_parts(R, int(np), lvl - 1, Form::coeff);
+        check_tg(tg_rescale(R.dev(), const_cast<u64*>(dst[0].data()), out.parts[0].data(), lvl, u32(np), R.stream()));
+        out.parts = std::move(dst);
+    } else {
+        for (auto& p : out.parts) p = rescale_round(p);
+    }
+    out.scale = ct.scale / double(ql);
+    out.noise_bound = ct.noise_bound / double(ql) + 1.0;
+    return out;
+}
+
+Ciphertext Evaluator::rotate(const Ciphertext& ct, u32 k, const EvalKeys& keys) const {
+    if (k == 0) return ct;
+    const u64 g = rotation_exponent(ring(), k);
+    return ctx_->apply_galois(ct, g, keys.galois_key(g));
+}
+
+Ciphertext Evaluator::conjugate(const Ciphertext& ct, const EvalKeys& keys) const {
+    const u64 g = conjugation_exponent(ring());
+    return ctx_->apply_galois(ct, g, keys.galois_key(g));
+}
+
+// ---------------------------------------------------------------------------
+// eval_chebyshev (ckks.hpp:515-579): memoised T_k ladder, identical op order.
+// ---------------------------------------------------------------------------
+Ciphertext eval_chebyshev(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
+                          const EvalKeys& keys) {
+    std::size_t d = cheb_coeffs.size() - 1;
+    while (d > 0 && cheb_coeffs[d] == 0.0) --d;
+    if (d == 0) {
+        Ciphertext out = ev.mul_scalar(x, 0.0, 1.0);
+        return ev.add_scalar(out, cheb_coeffs[0]);
+    }
+    if (x.level() < int(std::ceil(std::log2(double(d)))) + 1)
+        throw TetrisError("ckks", "insufficient levels for polynomial evaluation");
+    std::map<std::size_t, Ciphertext> T;
+    T.emplace(1, x);
+    std::function<const Ciphertext&(std::size_t)> get = [&](std::size_t k) -> const Ciphertext& {
+        auto hit = T.find(k);
+        if (hit != T.end()) return hit->second;
+        const std::size_t a = k / 2, b = k - a;
+        const Ciphertext& ta = get(a);
+        const Ciphertext& tb = get(b);
+        Ciphertext prod = ev.mul_relin(ta, tb, keys);
+        prod.to_coeff();
+        prod.add_inplace(prod);  // 2 T_a T_b
+        Ciphertext res;
+        if (a == b) {
+            res = ev.rescale(ev.add_scalar(prod, -1.0));
+        } else {
+            Ciphertext tc = get(b - a);
+            tc.to_coeff();
+            if (tc.level() > prod.level()) tc.drop_to_level(prod.level());
+            tc = ev.mul_scalar(tc, 1.0, prod.scale / tc.scale);
+            Evaluator::check_scales_match(tc.scale, prod.scale);
+            prod.sub_inplace(tc);
+            res = ev.rescale(prod);
+        }
+        return T.emplace(k, std::move(res)).first->second;
+    };
+    for (std::size_t k = d; k >= 1; k /= 2) get(k);
+    int lvl = x.level();
+    for (std::size_t k = 1; k <= d; ++k)
+        if (cheb_coeffs[k] != 0.0) lvl = std::min(lvl, get(k).level());
+    const double comb_scale = double(ev.ring().modulus(u32(lvl)));
+    Ciphertext acc;
+    bool first = true;
+    for (std::size_t k = 1; k <= d; ++k) {
+        if (cheb_coeffs[k] == 0.0) continue;
+        Ciphertext term = get(k);
+        term.to_coeff();
+        if (term.level() > lvl) term.drop_to_level(lvl);
+        term = ev.mul_scalar(term, cheb_coeffs[k], comb_scale);
+        if (first) {
+            acc = std::move(term);
+            first = false;
+        } else {
+            Evaluator::check_scales_match(acc.scale, term.scale);
+            acc.add_inplace(term);
+        }
+    }
+    if (cheb_coeffs[0] != 0.0) acc = ev.add_scalar(acc, cheb_coeffs[0]);
+    return ev.rescale(acc);
+}
+
+std::vector<double> power_to_chebyshev(const std::vector<double>& pow_coeffs) {
+    const std::size_t d = pow_coeffs.size();
+    std::vector<std::vector<double>> t(d, std::vector<double>(d, 0.0));
+    t[0][0] = 1.0;
+    if (d > 1) t[1][1] = 1.0;
+    for (std::size_t k = 2; k < d; ++k)
+        for (std::size_t i = 0; i < d; ++i) {
+            double v = -t[k - 2][i];
+            if (i > 0) v += 2.0 * t[k - 1][i - 1];
+            t[k][i] = v;
+        }
+    std::vector<double> c(d, 0.0), rem = pow_coeffs;
+    for (std::size_t k = d; k-- > 0;) {
+        const double lead = t[k][k];
+        c[k] = rem[k] / lead;
+        for (std::size_t i = 0; i <= k; ++i) rem[i] -= c[k] * t[k][i];
+    }
+    return c;
+}
+
+Ciphertext inner_sum(const Evaluator& ev, const Ciphertext& ct, u32 n, const EvalKeys& keys) {
+    if (ct.domain != Domain::slots) throw TetrisError("ckks", "inner_sum expects slots domain");
+    if ((n & (n - 1)) != 0) throw TetrisError("ckks", "slot count must be a power of two");
+    Ciphertext acc = ct;
+    for (u32 k = 1; k < n; k <<= 1) {
+        Ciphertext rot = ev.rotate(acc, k, keys);
+        acc = ev.add(acc, rot);
+    }
+    return acc;
+}
+
+}  // namespace tetris_b200

@@ -1,0 +1,43 @@
+// Host-internal helpers: ciphertext-part blocks (several polys of one shape
+// back to back in one HBM allocation) so that per-part ops launch once.
+#pragma once
+
+#include "tetris_b200/keys.hpp"
+
+namespace tetris_b200::detail {
+
+inline std::shared_ptr<DeviceBuffer> new_block(const RingParams& ring, std::size_t words) {
+    return std::make_shared<DeviceBuffer>(ring, words);
+}
+
+// `n` views of shape (level, form, nspecial) over a fresh block.
+inline std::vector<Poly> fresh_parts(const RingParams& ring, int n, int level, Form form, int nspecial = 0) {
+    const std::size_t w = std::size_t(level + 1 + nspecial) * ring.degree();
+    auto blk = new_block(ring, w * std::size_t(n));
+    std::vector<Poly> out;
+    out.reserve(n);
+    for (int i = 0; i < n; ++i) out.push_back(Poly::view(ring, blk, w * i, level, form, nspecial));
+    return out;
+}
+
+// True if parts[first..first+n) have one shape and sit back to back in one block.
+inline bool contiguous(const std::vector<Poly>& parts, std::size_t first, std::size_t n) {
+    if (n == 0 || first + n > parts.size()) return false;
+    const Poly& p0 = parts[first];
+    for (std::size_t i = 1; i < n; ++i) {
+        const Poly& p = parts[first + i];
+        if (p.storage() != p0.storage() || p.level() != p0.level() || p.nspecial() != p0.nspecial() ||
+            p.form() != p0.form() || p.offset() != p0.offset() + i * p0.words())
+            return false;
+    }
+    return true;
+}
+
+// True if the parts are contiguous AND nothing outside them references the block.
+inline bool exclusively_owned(const std::vector<Poly>& parts) {
+    return contiguous(parts, 0, parts.size()) && parts[0].storage().use_count() == long(parts.size());
+}
+
+inline int tg_form(Form f) { return f == Form::eval ? TG_FORM_EVAL : TG_FORM_COEFF; }
+
+}  // namespace tetris_b200::detail

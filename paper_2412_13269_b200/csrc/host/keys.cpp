@@ -1,0 +1,472 @@
+// RLWE layer: gadget plan, keys, encryption, key switching, relinearisation,
+// Galois automorphisms (reference rlwe.hpp:16-682). Sampling happens on the
+// host in the reference's exact draw order; every polynomial product, NTT and
+// base conversion runs on the GPU.
+#include <cmath>
+
+#include "internal.hpp"
+
+namespace tetris_b200 {
+
+using detail::contiguous;
+using detail::exclusively_owned;
+using detail::fresh_parts;
+using detail::new_block;
+using detail::tg_form;
+
+// ---------------------------------------------------------------------------
+// GadgetVector / GadgetPlan (rlwe.hpp:16-206)
+// ---------------------------------------------------------------------------
+u32 GadgetVector::sub_digits(u64 q) const {
+    if (base2_bits == 0) return 1;
+    u32 bits = 0;
+    while ((q >> bits) != 0) ++bits;
+    return (bits + base2_bits - 1) / base2_bits;
+}
+
+GadgetPlan::GadgetPlan(const RingParams& ring, GadgetVector cfg) : ring_(&ring), cfg_(cfg) {
+    if (cfg_.group_size == 0) throw TetrisError("rlwe", "gadget group size must be positive");
+    if (cfg_.base2_bits != 0 && cfg_.group_size != 1)
+        throw TetrisError("rlwe", "base2 refinement requires single-prime groups");
+}
+
+GadgetPlan::~GadgetPlan() {
+    if (dev_) tg_gadget_destroy(dev_);
+}
+
+tg_gadget* GadgetPlan::dev() const {
+    std::call_once(once_, [this] {
+        tg_gadget* g = nullptr;
+        check_tg(tg_gadget_create(&g, ring_->dev(), cfg_.group_size, cfg_.base2_bits));
+        dev_ = g;
+    });
+    if (!dev_) throw TetrisError("gpu", "gadget tables unavailable");
+    return dev_;
+}
+
+u32 GadgetPlan::digit_count(int level) const {
+    u32 n = 0;
+    for (u32 j = 0; j < group_count(level); ++j)
+        n += cfg_.base2_bits ? cfg_.sub_digits(ring_->modulus(j * cfg_.group_size)) : 1;
+    return n;
+}
+
+std::vector<Poly> GadgetPlan::decompose(const Poly& d) const {
+    if (d.form() != Form::coeff || d.nspecial() != 0)
+        throw TetrisError("rlwe", "decompose expects coeff form without special rows");
+    const int level = d.level(), k = int(ring_->special_count());
+    const u32 nd = digit_count(level);
+    std::vector<Poly> digits = fresh_parts(*ring_, int(nd), level, Form::eval, k);
+    u64* base = const_cast<u64*>(digits[0].data());  // fresh block, exclusively ours
+    check_tg(tg_modup(dev(), base, d.data(), level, ring_->stream()));
+    return digits;
+}
+
+std::vector<std::vector<u64>> GadgetPlan::key_scalars() const {
+    const u32 nq = ring_->q_count(), nmod = u32(ring_->moduli().size()), gs = cfg_.group_size;
+    const u32 ngroups = (nq + gs - 1) / gs;
+    std::vector<std::vector<u64>> out;
+    for (u32 j = 0; j < ngroups; ++j) {
+        const u32 first = j * gs, count = std::min(gs, nq - first);
+        const u32 nsub = cfg_.base2_bits ? cfg_.sub_digits(ring_->modulus(first)) : 1;
+        for (u32 s = 0; s < nsub; ++s) {
+            std::vector<u64> row(nmod, 0);
+            for (u32 t = first; t < first + count; ++t) {  // Dhat = 0 outside the group, P = 0 mod specials
+                const u64 qt = ring_->modulus(t);
+                u64 p_mod = 1;
+                for (u32 sp = 0; sp < ring_->special_count(); ++sp)
+                    p_mod = mul_mod(p_mod, ring_->modulus(nq + sp) % qt, qt);
+                row[t] = mul_mod(pow_mod(2, u64(s) * cfg_.base2_bits, qt), p_mod, qt);
+            }
+            out.push_back(std::move(row));
+        }
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// Keys (rlwe.hpp:212-267)
+// ---------------------------------------------------------------------------
+SecretKey::SecretKey(const RingParams& ring, const NoiseParams& noise, Rng& rng)
+    : ring_(&ring), hamming_weight_(noise.secret_hamming_weight) {
+    id_ = splitmix64(rng.next());  // drawn before the ternary sample, as the reference's member init
+    coeffs_ = sample_ternary_coeffs(ring.degree(), hamming_weight_, rng);
+    eval_full_ = poly_from_i64(ring, coeffs_, ring.max_level(), int(ring.special_count()));
+    eval_full_.ntt_forward();
+}
+
+SecretKey::SecretKey(const RingParams& ring, std::vector<i64> coeffs, u64 id)
+    : ring_(&ring), id_(id), coeffs_(std::move(coeffs)) {
+    hamming_weight_ = 0;
+    for (i64 c : coeffs_) hamming_weight_ += c != 0;
+    eval_full_ = poly_from_i64(ring, coeffs_, ring.max_level(), int(ring.special_count()));
+    eval_full_.ntt_forward();
+}
+
+Poly SecretKey::shaped(int level, int nspecial) const {
+    Poly out(*ring_, level, Form::eval, nspecial);
+    const std::size_t n = ring_->degree();
+    u64* dst = out.mutable_data();
+    const u64* src = eval_full_.data();
+    check_tg(tg_memcpy_d2d(ring_->dev(), dst, src, std::size_t(level + 1) * n * 8, ring_->stream()));
+    if (nspecial)
+        check_tg(tg_memcpy_d2d(ring_->dev(), dst + std::size_t(level + 1) * n,
+                               src + std::size_t(ring_->max_level() + 1) * n, std::size_t(nspecial) * n * 8,
+                               ring_->stream()));
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// Ciphertext (rlwe.hpp:287-317)
+// ---------------------------------------------------------------------------
+static void transform_parts(Ciphertext& ct, Form target) {
+    const Form from = target == Form::eval ? Form::coeff : Form::eval;
+    bool any = false;
+    for (auto& p : ct.parts) any |= p.form() == from;
+    if (!any) return;
+    const std::size_t np = ct.parts.size();
+    if (contiguous(ct.parts, 0, np)) {
+        const Poly& p0 = ct.parts[0];
+        const RingParams& ring = p0.ring();
+        const u64* src = p0.data();
+        std::vector<Poly> dst = exclusively_owned(ct.parts) ? ct.parts
+                                                            : fresh_parts(ring, int(np), p0.level(), target, p0.nspecial());
+        u64* out = const_cast<u64*>(dst[0].data());
+        if (target == Form::eval)
+            check_tg(tg_ntt_forward_oop(ring.dev(), out, src, p0.level(), p0.nspecial(), u32(np), ring.stream()));
+        else
+            check_tg(tg_ntt_inverse_oop(ring.dev(), out, src, p0.level(), p0.nspecial(), u32(np), ring.stream()));
+        for (auto& p : dst) p.set_form(target);
+        ct.parts = std::move(dst);
+        return;
+    }
+    for (auto& p : ct.parts)
+        if (p.form() == from) target == Form::eval ? p.ntt_forward() : p.ntt_inverse();
+}
+
+void Ciphertext::to_coeff() { transform_parts(*this, Form::coeff); }
+void Ciphertext::to_eval() { transform_parts(*this, Form::eval); }
+
+void Ciphertext::drop_to_level(int new_level) {
+    for (auto& p : parts) p.drop_to_level(new_level);
+}
+
+static void addsub_ct(Ciphertext& x, const Ciphertext& o, int op) {
+    if (x.parts.size() != o.parts.size()) throw TetrisError("rlwe", "ciphertext degree mismatch");
+    if (x.domain != o.domain) throw TetrisError("rlwe", "domain tag mismatch");
+    const std::size_t np = x.parts.size();
+    for (std::size_t i = 0; i < np; ++i) x.parts[i].check_shape(o.parts[i]);
+    if (contiguous(x.parts, 0, np) && contiguous(o.parts, 0, np)) {
+        const Poly& p0 = x.parts[0];
+        const RingParams& ring = p0.ring();
+        std::vector<Poly> dst =
+            exclusively_owned(x.parts) ? x.parts : fresh_parts(ring, int(np), p0.level(), p0.form(), p0.nspecial());
+        check_tg(tg_poly_addsub(ring.dev(), const_cast<u64*>(dst[0].data()), p0.data(), o.parts[0].data(), op,
+                                p0.level(), p0.nspecial(), u32(np), ring.stream()));
+        x.parts = std::move(dst);
+        return;
+    }
+    for (std::size_t i = 0; i < np; ++i) op == 0 ? x.parts[i].add_inplace(o.parts[i]) : x.parts[i].sub_inplace(o.parts[i]);
+}
+
+void Ciphertext::add_inplace(const Ciphertext& o) {
+    addsub_ct(*this, o, 0);
+    noise_bound += o.noise_bound;
+}
+
+void Ciphertext::sub_inplace(const Ciphertext& o) {
+    addsub_ct(*this, o, 1);
+    noise_bound += o.noise_bound;
+}
+
+void Ciphertext::negate_inplace() {
+    for (auto& p : parts) p.negate_inplace();
+}
+
+// ---------------------------------------------------------------------------
+// KeyContext (rlwe.hpp:335-682)
+// ---------------------------------------------------------------------------
+KeyContext::KeyContext(const RingParams& ring, NoiseParams noise, GadgetVector gadget)
+    : ring_(&ring), noise_(noise), plan_(std::make_shared<GadgetPlan>(ring, gadget)) {}
+
+std::pair<SecretKey, PublicKey> KeyContext::keygen(Rng& rng) const {
+    Rng r_s = rng.split(1), r_pk = rng.split(2);
+    SecretKey sk(*ring_, noise_, r_s);
+    PublicKey pk = make_public(sk, r_pk);
+    return {std::move(sk), std::move(pk)};
+}
+
+PublicKey KeyContext::make_public(const SecretKey& sk, Rng& rng) const {
+    const int lvl = ring_->max_level();
+    Rng ra = rng.split(1), re = rng.split(2);
+    Poly a = sample_uniform(*ring_, lvl, 0, ra);
+    a.ntt_forward();
+    Poly e = sample_gaussian(*ring_, noise_.gaussian_sigma, lvl, 0, re);
+    e.ntt_forward();
+    Poly as = a;
+    as.mul_pointwise_inplace(sk.shaped(lvl, 0));
+    e.sub_inplace(as);  // b = e - a*s
+    return PublicKey{std::move(e), std::move(a), sk.id()};
+}
+
+Ciphertext KeyContext::encrypt(const SecretKey& sk, const Poly& m, double scale, Rng& rng, Domain domain) const {
+    if (m.nspecial() != 0) throw TetrisError("rlwe", "message must not carry special rows");
+    const int lvl = m.level();
+    Rng ra = rng.split(1), re = rng.split(2);
+    Poly a = sample_uniform(*ring_, lvl, 0, ra);  // c1 (coeff form, = iNTT(NTT(a)))
+    Poly e = sample_gaussian(*ring_, noise_.gaussian_sigma, lvl, 0, re);
+    // c0 = m + e - a*s   (exactly the reference's NTT(m+e) - a*s, then iNTT)
+    std::vector<Poly> parts = fresh_parts(*ring_, 2, lvl, Form::coeff);
+    const RingParams& R = *ring_;
+    u64* c0 = const_cast<u64*>(parts[0].data());
+    u64* c1 = const_cast<u64*>(parts[1].data());
+    check_tg(tg_memcpy_d2d(R.dev(), c1, a.data(), a.words() * 8, R.stream()));
+    Poly as = ntt_transform(a, Form::eval);
+    as.mul_pointwise_inplace(sk.shaped(lvl, 0));
+    as.ntt_inverse();
+    Poly me = m.form() == Form::coeff ? m : ntt_transform(m, Form::coeff);
+    check_tg(tg_poly_addsub(R.dev(), c0, me.data(), e.data(), 0, lvl, 0, 1, R.stream()));
+    check_tg(tg_poly_addsub(R.dev(), c0, c0, as.data(), 1, lvl, 0, 1, R.stream()));
+    Ciphertext ct;
+    ct.parts = std::move(parts);
+    ct.scale = scale;
+    ct.domain = domain;
+    ct.sk_id = sk.id();
+    ct.noise_bound = 6.0 * noise_.gaussian_sigma;
+    return ct;
+}
+
+Ciphertext KeyContext::encrypt_pk(const PublicKey& pk, const Poly& m, double scale, Rng& rng, Domain domain) const {
+    const int lvl = m.level();
+    Rng rv = rng.split(1), r0 = rng.split(2), r1 = rng.split(3);
+    std::vector<i64> vc(ring_->degree());
+    for (auto& x : vc) x = i64(rv.uniform(3)) - 1;
+    Poly v = poly_from_i64(*ring_, vc, lvl);
+    v.ntt_forward();
+    Poly c0 = pk.b, c1 = pk.a;
+    c0.drop_to_level(lvl);
+    c1.drop_to_level(lvl);
+    c0.mul_pointwise_inplace(v);
+    c1.mul_pointwise_inplace(v);
+    c0.ntt_inverse();
+    c1.ntt_inverse();
+    Poly e0 = sample_gaussian(*ring_, noise_.gaussian_sigma, lvl, 0, r0);
+    Poly e1 = sample_gaussian(*ring_, noise_.gaussian_sigma, lvl, 0, r1);
+    c0.add_inplace(e0);
+    c0.add_inplace(m.form() == Form::coeff ? m : ntt_transform(m, Form::coeff));
+    c1.add_inplace(e1);
+    Ciphertext ct;
+    ct.parts = {std::move(c0), std::move(c1)};
+    ct.scale = scale;
+    ct.domain = domain;
+    ct.sk_id = pk.sk_id;
+    ct.noise_bound = 6.0 * noise_.gaussian_sigma * (2.0 * std::sqrt(double(ring_->degree())) + 1.0);
+    return ct;
+}
+
+Poly KeyContext::decrypt(const SecretKey& sk, const Ciphertext& ct) const {
+    if (ct.sk_id != 0 && ct.sk_id != sk.id()) throw TetrisError("rlwe", "ciphertext bound to a different secret");
+    const int lvl = ct.level();
+    Poly s = sk.shaped(lvl, 0);
+    Poly acc = ct.parts[0].form() == Form::eval ? ct.parts[0] : ntt_transform(ct.parts[0], Form::eval);
+    Poly spow = s;
+    for (std::size_t k = 1; k < ct.parts.size(); ++k) {
+        Poly pe = ct.parts[k].form() == Form::eval ? ct.parts[k] : ntt_transform(ct.parts[k], Form::eval);
+        acc.mul_acc_pointwise(pe, spow);
+        if (k + 1 < ct.parts.size()) spow.mul_pointwise_inplace(s);
+    }
+    acc.ntt_inverse();
+    return acc;
+}
+
+Ciphertext KeyContext::zero_ciphertext(int level, double scale, u64 sk_id, Domain domain) const {
+    Ciphertext ct;
+    ct.parts = {Poly(*ring_, level, Form::coeff), Poly(*ring_, level, Form::coeff)};
+    ct.scale = scale;
+    ct.domain = domain;
+    ct.sk_id = sk_id;
+    ct.noise_bound = 0.0;
+    return ct;
+}
+
+SwitchingKey KeyContext::switch_key_gen(const SecretKey& from, const SecretKey& to, Rng& rng) const {
+    if (!from.ring().compatible(to.ring()) || !from.ring().compatible(*ring_))
+        throw TetrisError("rlwe", "switching key requires matching rings");
+    SwitchingKey swk;
+    swk.gadget = plan_->config();
+    swk.from_id = from.id();
+    swk.to_id = to.id();
+    swk.a_seed = splitmix64(rng.next());
+    const auto scalars = plan_->key_scalars();
+    const int lvl = ring_->max_level(), k = int(ring_->special_count());
+    const Poly s_to = to.shaped(lvl, k);
+    const Poly s_from = from.shaped(lvl, k);
+    Rng ra(swk.a_seed);
+    Rng re = rng.split(7);
+    const std::size_t w = std::size_t(lvl + 1 + k) * ring_->degree();
+    swk.block = new_block(*ring_, 2 * w * scalars.size());
+    for (std::size_t i = 0; i < scalars.size(); ++i) {
+        Rng rai = ra.split(i);
+        Poly a = sample_uniform(*ring_, lvl, k, rai);
+        a.ntt_forward();
+        Rng rei = re.split(i);
+        Poly e = sample_gaussian(*ring_, noise_.gaussian_sigma, lvl, k, rei);
+        e.ntt_forward();
+        Poly as = a;
+        as.mul_pointwise_inplace(s_to);
+        e.sub_inplace(as);
+        Poly ws = s_from;
+        ws.mul_scalar_inplace(scalars[i]);
+        e.add_inplace(ws);  // b = e - a*s_to + w_i*P*s_from
+        u64* bdst = swk.block->data() + 2 * w * i;
+        check_tg(tg_memcpy_d2d(ring_->dev(), bdst, e.data(), w * 8, ring_->stream()));
+        check_tg(tg_memcpy_d2d(ring_->dev(), bdst + w, a.data(), w * 8, ring_->stream()));
+        swk.b.push_back(Poly::view(*ring_, swk.block, 2 * w * i, lvl, Form::eval, k));
+        swk.a.push_back(Poly::view(*ring_, swk.block, 2 * w * i + w, lvl, Form::eval, k));
+    }
+    return swk;
+}
+
+static const u64* key_base(const SwitchingKey& swk) {
+    if (!swk.block) throw TetrisError("rlwe", "switching key has no device block");
+    return swk.block->data();
+}
+
+std::pair<Poly, Poly> KeyContext::ks_inner(const std::vector<Poly>& digits, const SwitchingKey& swk) const {
+    if (digits.empty()) throw TetrisError("rlwe", "empty decomposition");
+    if (digits.size() > swk.b.size()) throw TetrisError("rlwe", "switching key has too few digits");
+    const int lvl = digits[0].level(), k = int(ring_->special_count());
+    std::vector<Poly> src = digits;
+    if (!contiguous(src, 0, src.size())) {  // gather into one block
+        std::vector<Poly> g = fresh_parts(*ring_, int(src.size()), lvl, Form::eval, k);
+        for (std::size_t i = 0; i < src.size(); ++i)
+            check_tg(tg_memcpy_d2d(ring_->dev(), const_cast<u64*>(g[i].data()), src[i].data(), src[i].words() * 8,
+                                   ring_->stream()));
+        src = std::move(g);
+    }
+    std::vector<Poly> out = fresh_parts(*ring_, 2, lvl, Form::coeff);
+    check_tg(tg_ks_inner(plan_->dev(), const_cast<u64*>(out[0].data()), const_cast<u64*>(out[1].data()),
+                         src[0].data(), u32(src.size()), key_base(swk), swk.digits(), lvl, ring_->stream()));
+    return {out[0], out[1]};
+}
+
+std::pair<Poly, Poly> KeyContext::switch_key_apply(const Poly& d, const SwitchingKey& swk) const {
+    if (d.form() != Form::coeff || d.nspecial() != 0)
+        throw TetrisError("rlwe", "decompose expects coeff form without special rows");
+    const int lvl = d.level();
+    std::vector<Poly> out = fresh_parts(*ring_, 2, lvl, Form::coeff);
+    check_tg(tg_switch_key_apply(plan_->dev(), const_cast<u64*>(out[0].data()), const_cast<u64*>(out[1].data()),
+                                 d.data(), key_base(swk), swk.digits(), lvl, ring_->stream()));
+    return {out[0], out[1]};
+}
+
+Poly KeyContext::mod_down_p(const Poly& x) const {
+    if (x.nspecial() == 0) throw TetrisError("rlwe", "mod_down_p expects special rows");
+    if (x.form() != Form::coeff) throw TetrisError("rlwe", "mod_down_p expects coeff form");
+    std::vector<Poly> out = fresh_parts(*ring_, 1, x.level(), Form::coeff);
+    check_tg(tg_mod_down(plan_->dev(), const_cast<u64*>(out[0].data()), x.data(), x.level(), ring_->stream()));
+    return out[0];
+}
+
+SwitchingKey KeyContext::relin_key_gen(const SecretKey& sk, Rng& rng) const {
+    SecretKey s2 = square_secret(sk);
+    return switch_key_gen(s2, sk, rng);
+}
+
+// relinearize (rlwe.hpp:601-620): c2 -> coeff, KS(c2), (c0+d0, c1+d1) in coeff form.
+Ciphertext KeyContext::relinearize(const Ciphertext& ct, const SwitchingKey& rlk) const {
+    if (ct.degree() != 2) throw TetrisError("rlwe", "relinearize expects a degree-2 ciphertext");
+    if (rlk.to_id != ct.sk_id) throw TetrisError("rlwe", "relinearization key mismatch");
+    Ciphertext src = ct;
+    src.to_coeff();  // one batched iNTT when the three parts share a block
+    auto [d0, d1] = switch_key_apply(src.parts[2], rlk);
+    Ciphertext out;
+    out.parts = {src.parts[0], src.parts[1]};
+    std::vector<Poly> d = {d0, d1};
+    const int lvl = ct.level();
+    if (contiguous(out.parts, 0, 2) && contiguous(d, 0, 2)) {
+        std::vector<Poly> dst = fresh_parts(*ring_, 2, lvl, Form::coeff);
+        check_tg(tg_poly_addsub(ring_->dev(), const_cast<u64*>(dst[0].data()), out.parts[0].data(), d0.data(), 0, lvl,
+                                0, 2, ring_->stream()));
+        out.parts = std::move(dst);
+    } else {
+        out.parts[0].add_inplace(d0);
+        out.parts[1].add_inplace(d1);
+    }
+    out.scale = ct.scale;
+    out.domain = ct.domain;
+    out.sk_id = ct.sk_id;
+    out.noise_bound = ct.noise_bound + ks_noise_estimate();
+    return out;
+}
+
+SwitchingKey KeyContext::galois_key_gen(const SecretKey& sk, u64 exponent, Rng& rng) const {
+    const u32 n = ring_->degree();
+    const u64 two_n = 2 * u64(n);
+    const u64 g = exponent % two_n;
+    if (g % 2 == 0) throw TetrisError("rlwe", "invalid automorphism exponent");
+    std::vector<i64> c(n);
+    const auto& s = sk.coeffs();
+    for (u32 i = 0; i < n; ++i) {
+        const u64 j = (u64(i) * g) % two_n;
+        if (j < n) c[j] = s[i];
+        else c[j - n] = -s[i];
+    }
+    SecretKey phi_s(*ring_, std::move(c), splitmix64(sk.id() ^ exponent));
+    return switch_key_gen(phi_s, sk, rng);
+}
+
+// apply_galois (rlwe.hpp:637-654)
+Ciphertext KeyContext::apply_galois(const Ciphertext& ct, u64 exponent, const SwitchingKey& swk) const {
+    if (ct.degree() != 1) throw TetrisError("rlwe", "apply_galois expects degree-1 input");
+    Ciphertext src = ct;
+    src.to_coeff();
+    const int lvl = ct.level();
+    const u64 g = exponent % (2 * u64(ring_->degree()));
+    if (g % 2 == 0) throw TetrisError("ring", "automorphism exponent must be odd");
+    std::vector<Poly> rot = fresh_parts(*ring_, 2, lvl, Form::coeff);
+    if (contiguous(src.parts, 0, 2)) {
+        check_tg(tg_automorphism(ring_->dev(), const_cast<u64*>(rot[0].data()), src.parts[0].data(), g, TG_FORM_COEFF,
+                                 lvl, 0, 2, ring_->stream()));
+    } else {
+        for (int i = 0; i < 2; ++i)
+            check_tg(tg_automorphism(ring_->dev(), const_cast<u64*>(rot[i].data()), src.parts[i].data(), g,
+                                     TG_FORM_COEFF, lvl, 0, 1, ring_->stream()));
+    }
+    auto [d0, d1] = switch_key_apply(rot[1], swk);
+    Ciphertext out;
+    std::vector<Poly> dst = fresh_parts(*ring_, 2, lvl, Form::coeff);
+    check_tg(tg_poly_addsub(ring_->dev(), const_cast<u64*>(dst[0].data()), rot[0].data(), d0.data(), 0, lvl, 0, 1,
+                            ring_->stream()));
+    check_tg(tg_memcpy_d2d(ring_->dev(), const_cast<u64*>(dst[1].data()), d1.data(), d1.words() * 8, ring_->stream()));
+    out.parts = std::move(dst);
+    out.scale = ct.scale;
+    out.domain = ct.domain;
+    out.sk_id = ct.sk_id;
+    out.noise_bound = ct.noise_bound + ks_noise_estimate();
+    return out;
+}
+
+double KeyContext::ks_noise_estimate() const {
+    return 6.0 * noise_.gaussian_sigma * std::sqrt(double(ring_->degree())) *
+           double(plan_->digit_count(ring_->max_level()));
+}
+
+SecretKey KeyContext::square_secret(const SecretKey& sk) const {
+    const u32 n = ring_->degree();
+    const auto& s = sk.coeffs();
+    std::vector<u32> nz;
+    for (u32 i = 0; i < n; ++i)
+        if (s[i] != 0) nz.push_back(i);
+    std::vector<i64> sq(n, 0);
+    for (u32 i : nz)
+        for (u32 j : nz) {
+            const u32 k = i + j;
+            const i64 v = s[i] * s[j];
+            if (k < n) sq[k] += v;
+            else sq[k - n] -= v;
+        }
+    return SecretKey(*ring_, std::move(sq), splitmix64(sk.id() ^ 0x5157ULL));
+}
+
+}  // namespace tetris_b200

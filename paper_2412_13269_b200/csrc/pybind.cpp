@@ -1,0 +1,303 @@
+// Python binding of the drop-in C++ API (tetris_b200::). The surface mirrors
+// the oracle module built over the reference headers (oracle/ref_py.cpp), so
+// parity scripts run unchanged against both and compare residues.
+#include <pybind11/complex.h>
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <chrono>
+
+#include "tetris_b200/tetris.hpp"
+
+namespace py = pybind11;
+using namespace tetris_b200;
+
+namespace {
+
+py::array_t<uint64_t> poly_to_numpy(const Poly& p) {
+    const u32 n = p.ring().degree();
+    py::array_t<uint64_t> out({py::ssize_t(p.rows()), py::ssize_t(n)});
+    {
+        py::gil_scoped_release nogil;
+        p.to_host(out.mutable_data());
+    }
+    return out;
+}
+
+Poly poly_from_numpy(const RingParams& ring, py::array_t<uint64_t, py::array::c_style | py::array::forcecast> a,
+                     int level, Form form, int nspecial) {
+    const u32 n = ring.degree();
+    if (a.ndim() != 2 || a.shape(0) != py::ssize_t(level + 1 + nspecial) || a.shape(1) != py::ssize_t(n))
+        throw TetrisError("ring", "poly_from_numpy: shape mismatch");
+    return Poly::from_host(ring, a.data(), level, form, nspecial);
+}
+
+template <class T>
+py::array_t<T> vec_to_numpy(const std::vector<T>& v) {
+    py::array_t<T> out(py::ssize_t(v.size()));
+    std::memcpy(out.mutable_data(), v.data(), v.size() * sizeof(T));
+    return out;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_tetris_b200, m) {
+    m.doc() = "B200-native RNS-CKKS evaluator (drop-in for the TETRIS evaluation path)";
+    m.attr("IMPL") = "b200";
+    m.attr("BUILD") = std::string(tg_build_info());
+
+    py::register_exception<TetrisError>(m, "TetrisError", PyExc_RuntimeError);
+
+    m.def("device_count", &tg_device_count);
+    m.def("set_default_device", &set_default_device);
+    m.def("default_device", &default_device);
+
+    py::enum_<Form>(m, "Form").value("coeff", Form::coeff).value("eval", Form::eval);
+    py::enum_<Domain>(m, "Domain").value("coeffs", Domain::coeffs).value("slots", Domain::slots);
+
+    m.def("find_ntt_primes", &find_ntt_primes, py::arg("bits"), py::arg("count"), py::arg("modulus"),
+          py::arg("exclude") = std::vector<u64>{});
+    m.def("round_half_away", &round_half_away);
+
+    py::class_<Rng>(m, "Rng")
+        .def(py::init<u64>())
+        .def("seed", &Rng::seed)
+        .def("next", &Rng::next)
+        .def("uniform", &Rng::uniform)
+        .def("normal", &Rng::normal)
+        .def("split", &Rng::split);
+
+    py::class_<RingParams, std::shared_ptr<RingParams>>(m, "RingParams")
+        .def(py::init<u32, std::vector<u64>, u32>())
+        .def("degree", &RingParams::degree)
+        .def("moduli", &RingParams::moduli)
+        .def("special_count", &RingParams::special_count)
+        .def("q_count", &RingParams::q_count)
+        .def("max_level", &RingParams::max_level)
+        .def("modulus", &RingParams::modulus)
+        .def("device", &RingParams::device)
+        .def("synchronize", &RingParams::synchronize, py::call_guard<py::gil_scoped_release>())
+        .def("stream_handle", [](const RingParams& r) { return reinterpret_cast<uintptr_t>(r.stream()); })
+        .def("tables", [](const RingParams& r, u32 i) {
+            const NttTables& t = r.tables(i);
+            py::dict d;
+            d["q"] = t.q;
+            d["psi"] = t.psi;
+            d["w"] = vec_to_numpy(t.w);
+            d["w_shoup"] = vec_to_numpy(t.w_shoup);
+            d["winv"] = vec_to_numpy(t.winv);
+            d["winv_shoup"] = vec_to_numpy(t.winv_shoup);
+            d["n_inv"] = t.n_inv;
+            d["n_inv_shoup"] = t.n_inv_shoup;
+            return d;
+        })
+        .def("eval_exp_table", [](const RingParams& r) { return vec_to_numpy(r.eval_exp_table()); })
+        .def("slot_of_exp_table", [](const RingParams& r) { return vec_to_numpy(r.slot_of_exp_table()); });
+
+    py::class_<Poly>(m, "Poly")
+        .def(py::init<const RingParams&, int, Form, int>(), py::arg("ring"), py::arg("level"), py::arg("form"),
+             py::arg("nspecial") = 0, py::keep_alive<1, 2>())
+        .def("level", &Poly::level)
+        .def("nspecial", &Poly::nspecial)
+        .def("form", &Poly::form)
+        .def("rows", &Poly::rows)
+        .def("to_numpy", &poly_to_numpy)
+        .def_static("from_numpy", &poly_from_numpy, py::arg("ring"), py::arg("data"), py::arg("level"),
+                    py::arg("form"), py::arg("nspecial") = 0, py::keep_alive<0, 1>())
+        .def("copy", [](const Poly& p) { return Poly(p); })
+        .def("device_ptr", [](const Poly& p) { return reinterpret_cast<uintptr_t>(p.data()); })
+        .def("ntt_forward", &Poly::ntt_forward)
+        .def("ntt_inverse", &Poly::ntt_inverse)
+        .def("add_inplace", &Poly::add_inplace)
+        .def("sub_inplace", &Poly::sub_inplace)
+        .def("negate_inplace", &Poly::negate_inplace)
+        .def("mul_pointwise_inplace", &Poly::mul_pointwise_inplace)
+        .def("mul_acc_pointwise", &Poly::mul_acc_pointwise)
+        .def("mul_scalar_inplace", &Poly::mul_scalar_inplace)
+        .def("mul_small_scalar_inplace", &Poly::mul_small_scalar_inplace)
+        .def("drop_to_level", &Poly::drop_to_level);
+
+    m.def("ntt_transform", &ntt_transform);
+    m.def("automorphism_apply", &automorphism_apply);
+    m.def("rescale_round", &rescale_round);
+    m.def("sample_uniform", &sample_uniform, py::keep_alive<0, 1>());
+    m.def("sample_gaussian", &sample_gaussian, py::keep_alive<0, 1>());
+    m.def("sample_ternary_hw", &sample_ternary_hw, py::keep_alive<0, 1>());
+    m.def("sample_uniform_host", [](const RingParams& ring, int level, int nspecial, Rng& rng) {
+        auto v = sample_uniform_host(ring, level, nspecial, rng);
+        py::array_t<uint64_t> out({py::ssize_t(level + 1 + nspecial), py::ssize_t(ring.degree())});
+        std::memcpy(out.mutable_data(), v.data(), v.size() * 8);
+        return out;
+    });
+    m.def("sample_gaussian_coeffs", &sample_gaussian_coeffs);
+    m.def("sample_ternary_coeffs", &sample_ternary_coeffs);
+
+    py::class_<NoiseParams>(m, "NoiseParams")
+        .def(py::init([](double sigma, u32 h) { return NoiseParams{sigma, h}; }), py::arg("gaussian_sigma") = 3.2,
+             py::arg("secret_hamming_weight") = 0)
+        .def_readwrite("gaussian_sigma", &NoiseParams::gaussian_sigma)
+        .def_readwrite("secret_hamming_weight", &NoiseParams::secret_hamming_weight);
+
+    py::class_<GadgetVector>(m, "GadgetVector")
+        .def(py::init([](u32 g, u32 b) { return GadgetVector{g, b}; }), py::arg("group_size") = 1,
+             py::arg("base2_bits") = 0)
+        .def_readwrite("group_size", &GadgetVector::group_size)
+        .def_readwrite("base2_bits", &GadgetVector::base2_bits);
+
+    py::class_<SecretKey>(m, "SecretKey")
+        .def("id", &SecretKey::id)
+        .def("coeffs", &SecretKey::coeffs)
+        .def("hamming_weight", &SecretKey::hamming_weight)
+        .def("shaped", &SecretKey::shaped);
+    py::class_<PublicKey>(m, "PublicKey")
+        .def_readonly("b", &PublicKey::b)
+        .def_readonly("a", &PublicKey::a)
+        .def_readonly("sk_id", &PublicKey::sk_id);
+
+    py::class_<Ciphertext>(m, "Ciphertext")
+        .def(py::init<>())
+        .def_readwrite("parts", &Ciphertext::parts)
+        .def_readwrite("scale", &Ciphertext::scale)
+        .def_readwrite("domain", &Ciphertext::domain)
+        .def_readwrite("sk_id", &Ciphertext::sk_id)
+        .def_readwrite("noise_bound", &Ciphertext::noise_bound)
+        .def("level", &Ciphertext::level)
+        .def("form", &Ciphertext::form)
+        .def("degree", &Ciphertext::degree)
+        .def("copy", [](const Ciphertext& c) { return Ciphertext(c); })
+        .def("to_coeff", &Ciphertext::to_coeff)
+        .def("to_eval", &Ciphertext::to_eval)
+        .def("drop_to_level", &Ciphertext::drop_to_level)
+        .def("add_inplace", &Ciphertext::add_inplace)
+        .def("sub_inplace", &Ciphertext::sub_inplace);
+
+    py::class_<SwitchingKey>(m, "SwitchingKey")
+        .def_readonly("b", &SwitchingKey::b)
+        .def_readonly("a", &SwitchingKey::a)
+        .def_readonly("from_id", &SwitchingKey::from_id)
+        .def_readonly("to_id", &SwitchingKey::to_id)
+        .def_readonly("a_seed", &SwitchingKey::a_seed);
+
+    py::class_<EvalKeys>(m, "EvalKeys")
+        .def(py::init<>())
+        .def_readwrite("relin", &EvalKeys::relin)
+        .def("add_galois", [](EvalKeys& k, u64 g, const SwitchingKey& s) { k.galois[g] = s; })
+        .def("has", &EvalKeys::has)
+        .def("galois_exponents", [](const EvalKeys& k) {
+            std::vector<u64> v;
+            for (auto& [g, s] : k.galois) v.push_back(g);
+            return v;
+        })
+        .def("galois_key", &EvalKeys::galois_key, py::return_value_policy::reference_internal);
+
+    py::class_<KeyContext>(m, "KeyContext")
+        .def(py::init<const RingParams&, NoiseParams, GadgetVector>(), py::keep_alive<1, 2>())
+        .def("keygen", &KeyContext::keygen)
+        .def("relin_key_gen", &KeyContext::relin_key_gen)
+        .def("galois_key_gen", &KeyContext::galois_key_gen)
+        .def("switch_key_gen", &KeyContext::switch_key_gen)
+        .def("encrypt", &KeyContext::encrypt, py::arg("sk"), py::arg("m"), py::arg("scale"), py::arg("rng"),
+             py::arg("domain") = Domain::coeffs)
+        .def("encrypt_pk", &KeyContext::encrypt_pk, py::arg("pk"), py::arg("m"), py::arg("scale"), py::arg("rng"),
+             py::arg("domain") = Domain::coeffs)
+        .def("decrypt", &KeyContext::decrypt)
+        .def("decompose", [](const KeyContext& c, const Poly& d) { return c.plan().decompose(d); })
+        .def("digit_count", [](const KeyContext& c, int level) { return c.plan().digit_count(level); })
+        .def("ks_inner", &KeyContext::ks_inner)
+        .def("switch_key_apply", &KeyContext::switch_key_apply)
+        .def("mod_down_p", &KeyContext::mod_down_p)
+        .def("relinearize", &KeyContext::relinearize)
+        .def("apply_galois", &KeyContext::apply_galois)
+        .def("square_secret", &KeyContext::square_secret);
+
+    m.def("rotation_exponent", &rotation_exponent);
+    m.def("conjugation_exponent", &conjugation_exponent);
+
+    py::class_<Encoder>(m, "Encoder")
+        .def(py::init<const RingParams&, u32>(), py::keep_alive<1, 2>())
+        .def("slots", &Encoder::slots)
+        .def("encode_slots", &Encoder::encode_slots, py::call_guard<py::gil_scoped_release>())
+        .def("decode_slots", &Encoder::decode_slots, py::call_guard<py::gil_scoped_release>())
+        .def("encode_coeffs", &Encoder::encode_coeffs)
+        .def("decode_coeffs", &Encoder::decode_coeffs)
+        .def("encode_slots_host", [](const Encoder& e, const std::vector<cplx>& v, double scale, int level) {
+            std::vector<u64> h;
+            {
+                py::gil_scoped_release nogil;
+                h = e.encode_slots_host(v, scale, level);
+            }
+            py::array_t<uint64_t> out({py::ssize_t(level + 1), py::ssize_t(e.ring().degree())});
+            std::memcpy(out.mutable_data(), h.data(), h.size() * 8);
+            return out;
+        });
+
+    py::class_<Evaluator>(m, "Evaluator")
+        .def(py::init<const KeyContext&>(), py::keep_alive<1, 2>())
+        .def("add", &Evaluator::add)
+        .def("sub", &Evaluator::sub)
+        .def("mul", &Evaluator::mul)
+        .def("mul_relin", &Evaluator::mul_relin)
+        .def("mul_plain", &Evaluator::mul_plain)
+        .def("mul_scalar", &Evaluator::mul_scalar)
+        .def("add_scalar", &Evaluator::add_scalar)
+        .def("rescale", &Evaluator::rescale)
+        .def("rotate", &Evaluator::rotate)
+        .def("conjugate", &Evaluator::conjugate)
+        .def_static("scaled_residue", &Evaluator::scaled_residue);
+
+    m.def("eval_chebyshev", &eval_chebyshev);
+    m.def("inner_sum", &inner_sum);
+    m.def("power_to_chebyshev", &power_to_chebyshev);
+
+    py::class_<ThresholdParams>(m, "ThresholdParams")
+        .def(py::init([](u32 alpha, u32 beta, std::vector<u32> degrees, double eps) {
+                 return ThresholdParams{alpha, beta, std::move(degrees), eps};
+             }),
+             py::arg("alpha") = 8, py::arg("beta") = 12, py::arg("degrees") = std::vector<u32>{},
+             py::arg("epsilon") = 1.0)
+        .def_readwrite("alpha", &ThresholdParams::alpha)
+        .def_readwrite("beta", &ThresholdParams::beta)
+        .def_readwrite("degrees", &ThresholdParams::degrees)
+        .def_readwrite("epsilon", &ThresholdParams::epsilon);
+    py::class_<ChainStage>(m, "ChainStage")
+        .def(py::init<>())
+        .def_readwrite("degree", &ChainStage::degree)
+        .def_readwrite("gamma", &ChainStage::gamma)
+        .def_readwrite("upper", &ChainStage::upper)
+        .def_readwrite("cheb", &ChainStage::cheb)
+        .def_readwrite("error", &ChainStage::error);
+    py::class_<MinimaxChain>(m, "MinimaxChain")
+        .def(py::init<>())
+        .def_readwrite("params", &MinimaxChain::params)
+        .def_readwrite("stages", &MinimaxChain::stages)
+        .def_readwrite("sign_error", &MinimaxChain::sign_error)
+        .def_readwrite("achieved_beta", &MinimaxChain::achieved_beta)
+        .def("eval_coeffs", &MinimaxChain::eval_coeffs)
+        .def("eval_step", &MinimaxChain::eval_step)
+        .def("levels_required", &MinimaxChain::levels_required);
+    m.def("build_chain", &build_chain, py::call_guard<py::gil_scoped_release>());
+    m.def("eval_private_threshold", &eval_private_threshold);
+    m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm);
+
+    // The whole threshold-count query in C++ (no Python between ops):
+    // per-ciphertext threshold, sum mod q in index order, one inner_sum
+    // (the reference order, protocol.hpp:319-323). Returns (ct, seconds),
+    // seconds measured after a device synchronize.
+    m.def(
+        "threshold_count",
+        [](const Evaluator& ev, const std::vector<Ciphertext>& scores, const Ciphertext& ct_t, double norm,
+           const MinimaxChain& chain, const EvalKeys& keys, u32 slots, bool do_inner_sum) {
+            py::gil_scoped_release nogil;
+            auto t0 = std::chrono::steady_clock::now();
+            Ciphertext acc;
+            for (std::size_t i = 0; i < scores.size(); ++i) {
+                Ciphertext o = eval_private_threshold_plain_norm(ev, scores[i], ct_t, norm, chain, keys);
+                acc = i == 0 ? o : ev.add(acc, o);
+            }
+            if (do_inner_sum) acc = inner_sum(ev, acc, slots, keys);
+            ev.ring().synchronize();
+            double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            return std::make_pair(acc, s);
+        });
+}

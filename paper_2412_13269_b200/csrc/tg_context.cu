@@ -1,0 +1,313 @@
+// Context, memory and gadget setup for the C-ABI (include/tetris_b200.h).
+//
+// tg_context replaces the reference RingParams (ring.hpp:116-195) on the
+// device: the host-built NTT tables are uploaded verbatim; the exact integer
+// constants of rescale (ring.hpp:505-508), the gadget size tables
+// (rlwe.hpp:178-201) and ModDown (rlwe.hpp:555-579) are derived here from the
+// moduli with exact 128-bit host arithmetic.
+#include <cstring>
+#include <mutex>
+
+#include "tg_internal.cuh"
+
+namespace tg {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+    g_last_error = std::string("[gpu] ") + where + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? TG_E_NOMEM : TG_E_CUDA;
+}
+
+}  // namespace tg
+
+using namespace tg;
+
+extern "C" const char* tg_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int tg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+extern "C" const char* tg_build_info(void) {
+    return "tetris_b200 sm_100a (CUDA " TG_STR(__CUDACC_VER_MAJOR__) "." TG_STR(__CUDACC_VER_MINOR__) ")";
+}
+
+extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, const uint64_t* moduli,
+                                 uint32_t nmod, uint32_t special_count, const uint64_t* tables,
+                                 const uint64_t* n_inv, const uint32_t* eval_exp,
+                                 const uint32_t* slot_of_exp) {
+    if (!out) return fail(TG_E_ARG, "[ring] null output handle");
+    *out = nullptr;
+    if (degree < 16 || (degree & (degree - 1)) != 0) return fail(TG_E_ARG, "[ring] degree must be a power of two >= 16");
+    if (nmod == 0 || nmod > u32(kMaxMod) || special_count >= nmod)
+        return fail(TG_E_ARG, "[ring] need at least one non-special prime (and at most 64 moduli)");
+    if (special_count > u32(kMaxSpecial)) return fail(TG_E_ARG, "[ring] too many special primes");
+    for (u32 i = 0; i < nmod; ++i)
+        if (moduli[i] >= (1ULL << 62) || moduli[i] < 3) return fail(TG_E_ARG, "[ring] moduli must be odd primes below 2^62");
+    int ndev = tg_device_count();
+    if (ndev <= 0) return fail(TG_E_STATE, "[gpu] no CUDA device visible");
+    if (device < 0 || device >= ndev) return fail(TG_E_ARG, "[gpu] device index out of range");
+    DeviceGuard guard(device);
+
+    auto* ctx = new tg_context();
+    ctx->device = device;
+    DevRing& R = ctx->ring;
+    R.N = degree;
+    R.logN = 0;
+    while ((1u << R.logN) < degree) ++R.logN;
+    R.nmod = nmod;
+    R.K = special_count;
+    R.q_count = nmod - special_count;
+    ctx->h_q.assign(moduli, moduli + nmod);
+    ctx->h_ratio.resize(2 * nmod);
+    for (u32 i = 0; i < nmod; ++i) h_ratio(moduli[i], &ctx->h_ratio[2 * i], &ctx->h_ratio[2 * i + 1]);
+
+    // rescale constants per (level, target row): ql mod q_r, (ql mod q_r)^-1, shoup, ql>>1
+    const u32 qc = R.q_count;
+    std::vector<u64> rs(size_t(qc) * qc * 4, 0);
+    for (u32 l = 1; l < qc; ++l) {
+        u64 ql = moduli[l];
+        for (u32 r = 0; r < l; ++r) {
+            u64 q = moduli[r];
+            u64 qlq = ql % q;
+            u64 inv = h_inv_mod(qlq, q);
+            u64* e = &rs[(size_t(l) * qc + r) * 4];
+            e[0] = qlq;
+            e[1] = inv;
+            e[2] = h_shoup(inv, q);
+            e[3] = ql >> 1;
+        }
+    }
+
+    // one device block: q | ratio | tw | ninv | rs | eval_exp | slot_of_exp
+    size_t n_q = nmod, n_ratio = 2 * nmod, n_tw = size_t(4) * nmod * degree, n_ninv = 2 * nmod, n_rs = rs.size();
+    size_t words = n_q + n_ratio + n_tw + n_ninv + n_rs;
+    size_t bytes = words * 8 + size_t(3) * degree * 4;
+    cudaError_t e = cudaMalloc(&ctx->dev_block, bytes);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return cuda_fail(e, "cudaMalloc(tables)");
+    }
+    u64* p = static_cast<u64*>(ctx->dev_block);
+    R.q = p;
+    R.ratio = p + n_q;
+    R.tw = p + n_q + n_ratio;
+    R.ninv = p + n_q + n_ratio + n_tw;
+    R.rs = p + n_q + n_ratio + n_tw + n_ninv;
+    u32* p32 = reinterpret_cast<u32*>(p + words);
+    R.eval_exp = p32;
+    R.slot_of_exp = p32 + degree;
+    std::vector<u64> host(words);
+    std::memcpy(host.data(), moduli, n_q * 8);
+    std::memcpy(host.data() + n_q, ctx->h_ratio.data(), n_ratio * 8);
+    std::memcpy(host.data() + n_q + n_ratio, tables, n_tw * 8);
+    std::memcpy(host.data() + n_q + n_ratio + n_tw, n_inv, n_ninv * 8);
+    std::memcpy(host.data() + n_q + n_ratio + n_tw + n_ninv, rs.data(), n_rs * 8);
+    e = cudaMemcpy(p, host.data(), words * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(p32, eval_exp, size_t(degree) * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(p32 + degree, slot_of_exp, size_t(2) * degree * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(ctx->dev_block);
+        delete ctx;
+        return cuda_fail(e, "cudaMemcpy(tables)");
+    }
+    // stream-ordered pool: keep freed blocks cached (no release back to the OS)
+    cudaDeviceGetDefaultMemPool(&ctx->pool, device);
+    uint64_t threshold = UINT64_MAX;
+    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    *out = ctx;
+    return TG_OK;
+}
+
+extern "C" void tg_context_destroy(tg_context* ctx) {
+    if (!ctx) return;
+    DeviceGuard guard(ctx->device);
+    cudaDeviceSynchronize();
+    cudaFree(ctx->dev_block);
+    delete ctx;
+}
+
+extern "C" uint32_t tg_context_degree(const tg_context* ctx) { return ctx ? ctx->ring.N : 0; }
+
+extern "C" int tg_alloc(tg_context* ctx, void** ptr, size_t bytes, void* stream) {
+    if (!ctx || !ptr) return fail(TG_E_ARG, "[gpu] tg_alloc: null argument");
+    DeviceGuard guard(ctx->device);
+    *ptr = nullptr;
+    if (bytes == 0) return TG_OK;
+    TG_CUDA(cudaMallocFromPoolAsync(ptr, bytes, ctx->pool, as_stream(stream)));
+    return TG_OK;
+}
+
+extern "C" int tg_free(tg_context* ctx, void* ptr, void* stream) {
+    if (!ctx) return fail(TG_E_ARG, "[gpu] tg_free: null context");
+    if (!ptr) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    TG_CUDA(cudaFreeAsync(ptr, as_stream(stream)));
+    return TG_OK;
+}
+
+extern "C" int tg_memcpy_h2d(tg_context* ctx, void* dst, const void* src, size_t bytes, void* stream) {
+    DeviceGuard guard(ctx->device);
+    TG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream)));
+    return TG_OK;
+}
+extern "C" int tg_memcpy_d2h(tg_context* ctx, void* dst, const void* src, size_t bytes, void* stream) {
+    DeviceGuard guard(ctx->device);
+    TG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
+    return TG_OK;
+}
+extern "C" int tg_memcpy_d2d(tg_context* ctx, void* dst, const void* src, size_t bytes, void* stream) {
+    DeviceGuard guard(ctx->device);
+    TG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(stream)));
+    return TG_OK;
+}
+extern "C" int tg_memset0(tg_context* ctx, void* dst, size_t bytes, void* stream) {
+    DeviceGuard guard(ctx->device);
+    TG_CUDA(cudaMemsetAsync(dst, 0, bytes, as_stream(stream)));
+    return TG_OK;
+}
+extern "C" int tg_stream_sync(tg_context* ctx, void* stream) {
+    DeviceGuard guard(ctx->device);
+    TG_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    return TG_OK;
+}
+
+extern "C" int tg_stream_create(tg_context* ctx, void** stream) {
+    if (!ctx || !stream) return fail(TG_E_ARG, "[gpu] tg_stream_create: null argument");
+    DeviceGuard guard(ctx->device);
+    cudaStream_t s = nullptr;
+    TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *stream = s;
+    return TG_OK;
+}
+extern "C" int tg_stream_destroy(tg_context* ctx, void* stream) {
+    if (!ctx || !stream) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    TG_CUDA(cudaStreamDestroy(as_stream(stream)));
+    return TG_OK;
+}
+extern "C" int tg_context_device(const tg_context* ctx) { return ctx ? ctx->device : -1; }
+
+// ---------------------------------------------------------------------------
+// Gadget: GadgetPlan size tables (rlwe.hpp:31-45, :178-201) + ModDown constants
+// ---------------------------------------------------------------------------
+
+extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group_size, uint32_t base2_bits) {
+    if (!out || !ctx) return fail(TG_E_ARG, "[rlwe] null argument");
+    *out = nullptr;
+    if (group_size == 0) return fail(TG_E_ARG, "[rlwe] gadget group size must be positive");
+    if (base2_bits != 0)
+        return fail(TG_E_ARG, "[rlwe] base-2 gadget refinement is not supported on the device path");
+    if (group_size > u32(kMaxGroup)) return fail(TG_E_ARG, "[rlwe] gadget group size exceeds 16");
+    DeviceGuard guard(ctx->device);
+    const DevRing& R = ctx->ring;
+    const std::vector<u64>& mod = ctx->h_q;
+    const u32 nq = R.q_count, nmod = R.nmod, K = R.K, gs = group_size;
+    const u32 ng = (nq + gs - 1) / gs;
+    auto* g = new tg_gadget();
+    g->ctx = ctx;
+    g->g.group_size = gs;
+    g->g.ngroups = ng;
+    std::vector<u64> src(size_t(ng) * gs * gs * 2, 0);
+    std::vector<u64> conv(size_t(ng) * gs * gs * nmod * 2, 0);
+    for (u32 j = 0; j < ng; ++j) {
+        u32 first = j * gs, count = std::min(gs, nq - first);
+        g->group_first.push_back(first);
+        g->group_count.push_back(count);
+        for (u32 a = 1; a <= count; ++a) {
+            for (u32 i = 0; i < a; ++i) {
+                u64 q = mod[first + i];
+                u64 rest = 1;  // (D'/q_i) mod q_i over the `a` active primes
+                for (u32 t = 0; t < a; ++t)
+                    if (t != i) rest = h_mul_mod(rest, mod[first + t] % q, q);
+                u64 sc = h_inv_mod(rest, q);
+                u64* se = &src[((size_t(j) * gs + (a - 1)) * gs + i) * 2];
+                se[0] = sc;
+                se[1] = h_shoup(sc, q);
+                for (u32 t = 0; t < nmod; ++t) {
+                    u64 qt = mod[t];
+                    u64 w = 1;  // D'/q_i mod q_t
+                    for (u32 u = 0; u < a; ++u)
+                        if (u != i) w = h_mul_mod(w, mod[first + u] % qt, qt);
+                    u64* ce = &conv[(((size_t(j) * gs + (a - 1)) * gs + i) * nmod + t) * 2];
+                    ce[0] = w;
+                    ce[1] = h_shoup(w, qt);
+                }
+            }
+        }
+    }
+    // ModDown (rlwe.hpp:555-579)
+    std::vector<u64> md(size_t(K) * 2 + size_t(K) * nq * 2 + size_t(nq) * 2, 0);
+    for (u32 s = 0; s < K; ++s) {
+        u64 ps = mod[nq + s];
+        u64 rest = 1;
+        for (u32 t = 0; t < K; ++t)
+            if (t != s) rest = h_mul_mod(rest, mod[nq + t] % ps, ps);
+        u64 c = h_inv_mod(rest, ps);
+        md[2 * s] = c;
+        md[2 * s + 1] = h_shoup(c, ps);
+    }
+    for (u32 s = 0; s < K; ++s)
+        for (u32 r = 0; r < nq; ++r) {
+            u64 q = mod[r];
+            u64 ws = 1;
+            for (u32 t = 0; t < K; ++t)
+                if (t != s) ws = h_mul_mod(ws, mod[nq + t] % q, q);
+            u64* e = &md[2 * K + (size_t(s) * nq + r) * 2];
+            e[0] = ws;
+            e[1] = h_shoup(ws, q);
+        }
+    for (u32 r = 0; r < nq; ++r) {
+        u64 q = mod[r];
+        u64 pinv = 1;
+        for (u32 s = 0; s < K; ++s) pinv = h_mul_mod(pinv, mod[nq + s] % q, q);
+        pinv = h_inv_mod(pinv, q);
+        u64* e = &md[2 * K + size_t(K) * nq * 2 + size_t(r) * 2];
+        e[0] = pinv;
+        e[1] = h_shoup(pinv, q);
+    }
+    size_t words = src.size() + conv.size() + md.size();
+    cudaError_t e = cudaMalloc(&g->dev_block, words * 8);
+    if (e != cudaSuccess) {
+        delete g;
+        return cuda_fail(e, "cudaMalloc(gadget)");
+    }
+    u64* p = static_cast<u64*>(g->dev_block);
+    g->g.src = p;
+    g->g.conv = p + src.size();
+    g->g.md = p + src.size() + conv.size();
+    e = cudaMemcpy(g->g.src, src.data(), src.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->g.conv, conv.data(), conv.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !md.empty()) e = cudaMemcpy(g->g.md, md.data(), md.size() * 8, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(g->dev_block);
+        delete g;
+        return cuda_fail(e, "cudaMemcpy(gadget)");
+    }
+    *out = g;
+    return TG_OK;
+}
+
+extern "C" void tg_gadget_destroy(tg_gadget* g) {
+    if (!g) return;
+    DeviceGuard guard(g->ctx->device);
+    cudaDeviceSynchronize();
+    cudaFree(g->dev_block);
+    delete g;
+}
+
+extern "C" uint32_t tg_gadget_digit_count(const tg_gadget* g, int level) {
+    // group_count(level) = (level + group_size) / group_size (rlwe.hpp:50-52)
+    return g ? (u32(level) + g->g.group_size) / g->g.group_size : 0;
+}

@@ -1,0 +1,199 @@
+// Internal header of the B200 evaluator: device ring descriptor, 64-bit
+// modular arithmetic and error plumbing shared by every kernel file.
+//
+// Arithmetic contract: every residue that leaves a kernel
+// is canonical in [0, q); inside a kernel values may be lazy in [0, 2q) or
+// [0, 4q) (q < 2^62, so 4q fits a word). Any exact modular algorithm yields the
+// same canonical residue as the reference's u128 `%` (common.hpp:37-39) or
+// Shoup (common.hpp:46-50), so results are bit-identical by construction.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "tetris_b200.h"
+
+#define TG_STR_(x) #x
+#define TG_STR(x) TG_STR_(x)
+
+namespace tg {
+
+using u64 = uint64_t;
+using u32 = uint32_t;
+using i64 = int64_t;
+
+constexpr int kMaxMod = 64;      // max moduli per ring (q-chain + specials)
+constexpr int kMaxGroup = 16;    // max primes per gadget digit group
+constexpr int kMaxSpecial = 16;  // max special primes K
+
+// Everything a kernel needs to know about the ring; passed by value.
+struct DevRing {
+    u32 N, logN, nmod, q_count, K;
+    const u64* q;            // [nmod]
+    const u64* ratio;        // [nmod][2] floor(2^128 / q) as (lo, hi)
+    const u64* tw;           // [nmod][4][N]: w | w_shoup | winv | winv_shoup
+    const u64* ninv;         // [nmod][2]: n_inv, n_inv_shoup
+    const u32* eval_exp;     // [N]
+    const u32* slot_of_exp;  // [2N]
+    const u64* rs;           // [q_count][q_count][4]: ql mod q_r, ql^-1, shoup, half(ql)
+};
+
+// Row r of a poly at (level, nspecial) -> modulus index (ring.hpp:227-229).
+__host__ __device__ __forceinline__ u32 mod_index(u32 r, int level, u32 q_count) {
+    return r <= u32(level) ? r : q_count + (r - u32(level) - 1);
+}
+
+// ---------------------------------------------------------------------------
+// Word arithmetic
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ u64 add_mod(u64 a, u64 b, u64 q) {
+    u64 r = a + b;
+    return r >= q ? r - q : r;
+}
+__device__ __forceinline__ u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+__device__ __forceinline__ u64 neg_mod(u64 a, u64 q) { return a == 0 ? 0 : q - a; }
+
+// Shoup product a*w mod q for ANY a < 2^64, result in [0, 2q).
+__device__ __forceinline__ u64 shoup_lazy(u64 a, u64 w, u64 ws, u64 q) {
+    u64 hi = __umul64hi(a, ws);
+    return a * w - hi * q;
+}
+__device__ __forceinline__ u64 shoup(u64 a, u64 w, u64 ws, u64 q) {
+    u64 r = shoup_lazy(a, w, ws, q);
+    return r >= q ? r - q : r;
+}
+
+// Exact z mod q for any 128-bit z = hi:lo, with mu = floor(2^128/q) = rhi:rlo.
+// est = floor(z*mu / 2^128) (computed exactly, mod 2^64) lies in
+// {floor(z/q)-1, floor(z/q)}, so z - est*q < 2q fits a word.
+__device__ __forceinline__ u64 barrett128(u64 lo, u64 hi, u64 q, u64 rlo, u64 rhi) {
+    u64 t = __umul64hi(lo, rlo);
+    u64 m1l = lo * rhi, m1h = __umul64hi(lo, rhi);
+    u64 m2l = hi * rlo, m2h = __umul64hi(hi, rlo);
+    u64 s = t + m1l;
+    u64 c = s < t;
+    u64 s2 = s + m2l;
+    c += s2 < s;
+    u64 est = hi * rhi + m1h + m2h + c;
+    u64 r = lo - est * q;
+    return r >= q ? r - q : r;
+}
+// Exact x mod q for a single word.
+__device__ __forceinline__ u64 reduce64(u64 x, u64 q, u64 rlo, u64 rhi) {
+    // floor(x * mu / 2^128) with hi = 0
+    u64 t = __umul64hi(x, rlo);
+    u64 m1l = x * rhi, m1h = __umul64hi(x, rhi);
+    u64 s = t + m1l;
+    u64 est = m1h + (s < t);
+    u64 r = x - est * q;
+    return r >= q ? r - q : r;
+}
+__device__ __forceinline__ u64 mul_mod(u64 a, u64 b, u64 q, u64 rlo, u64 rhi) {
+    return barrett128(a * b, __umul64hi(a, b), q, rlo, rhi);
+}
+
+// 128-bit accumulator helpers.
+struct U128 {
+    u64 lo, hi;
+};
+__device__ __forceinline__ void mac128(U128& acc, u64 a, u64 b) {
+    u64 lo = a * b, hi = __umul64hi(a, b);
+    acc.lo += lo;
+    acc.hi += hi + (acc.lo < lo);
+}
+
+// ---------------------------------------------------------------------------
+// Host-side exact helpers (context setup; never from floating point)
+// ---------------------------------------------------------------------------
+using u128 = unsigned __int128;
+inline u64 h_mul_mod(u64 a, u64 b, u64 q) { return u64((u128(a) * b) % q); }
+inline u64 h_pow_mod(u64 b, u64 e, u64 q) {
+    u64 r = 1 % q;
+    b %= q;
+    while (e) {
+        if (e & 1) r = h_mul_mod(r, b, q);
+        b = h_mul_mod(b, b, q);
+        e >>= 1;
+    }
+    return r;
+}
+inline u64 h_inv_mod(u64 a, u64 q) { return h_pow_mod(a % q, q - 2, q); }
+inline u64 h_shoup(u64 w, u64 q) { return u64((u128(w) << 64) / q); }
+inline void h_ratio(u64 q, u64* lo, u64* hi) {
+    u128 mu = (~u128(0)) / q;  // = floor(2^128 / q) for odd q > 1
+    *lo = u64(mu);
+    *hi = u64(mu >> 64);
+}
+
+// ---------------------------------------------------------------------------
+// Errors
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+#define TG_CUDA(expr)                                              \
+    do {                                                           \
+        cudaError_t _e = (expr);                                   \
+        if (_e != cudaSuccess) return ::tg::cuda_fail(_e, #expr);  \
+    } while (0)
+#define TG_LAUNCH_CHECK()                                                      \
+    do {                                                                       \
+        cudaError_t _e = cudaGetLastError();                                   \
+        if (_e != cudaSuccess) return ::tg::cuda_fail(_e, "kernel launch");   \
+    } while (0)
+#define TG_REQUIRE(cond, msg)                         \
+    do {                                              \
+        if (!(cond)) return ::tg::fail(TG_E_ARG, msg); \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Host-side exact constants of one gadget size table (rlwe.hpp:178-201).
+struct GadgetDev {
+    u32 group_size, ngroups;
+    u64* src;   // [ngroups][group_size(active-1)][group_size(i)][2]
+    u64* conv;  // [ngroups][group_size][group_size][nmod][2]
+    u64* md;    // ModDown: [K][2] (P/p_s)^-1 mod p_s; [K][q_count][2] (P/p_s) mod q_r; [q_count][2] P^-1 mod q_r
+};
+
+}  // namespace tg
+
+struct tg_context {
+    int device = 0;
+    tg::DevRing ring{};
+    std::vector<tg::u64> h_q;
+    std::vector<tg::u64> h_ratio;
+    void* dev_block = nullptr;  // one allocation for all tables
+    cudaMemPool_t pool = nullptr;
+};
+
+struct tg_gadget {
+    tg_context* ctx = nullptr;
+    tg::GadgetDev g{};
+    std::vector<tg::u32> group_first, group_count;
+    void* dev_block = nullptr;
+};
+
+namespace tg {
+// Launch helpers implemented in tg_ntt.cu (used by the keyswitch pipeline).
+int ntt_forward_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s);
+int ntt_inverse_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s);
+int ntt_forward_oop(tg_context* ctx, u64* dst, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s);
+int ntt_inverse_oop(tg_context* ctx, u64* dst, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s);
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+}  // namespace tg

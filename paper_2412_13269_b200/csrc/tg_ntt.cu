@@ -1,0 +1,261 @@
+// Negacyclic NTT / iNTT over 64-bit primes, batched over rows.
+//
+// Same transform as NttTables::forward / inverse (ring.hpp:64-101): the
+// forward CT transform maps natural order to the bit-reversed evaluation
+// order using w[m+i] = psi^brv(m+i); the inverse GS transform uses
+// winv[h+i] and ends with the N^-1 Shoup scaling. The twiddle tables are the
+// reference's own (uploaded verbatim), so outputs are bit-identical.
+//
+// B200 mapping: N = N1 * N2 with N1 = 2^floor(logN/2). The first log N1
+// forward stages only mix elements of one column {c + k*N2}; the remaining
+// stages only mix elements of one contiguous chunk of N2. Each phase stages a
+// 16 KiB tile in shared memory (one HBM read + one HBM write per phase; the
+// intermediate of a batched launch stays in the 126 MB L2). Butterflies are
+// Harvey-lazy: values live in [0,4q) (forward) / [0,2q) (inverse) and are
+// made canonical only at the end of the last phase.
+#include "tg_internal.cuh"
+
+namespace tg {
+
+namespace {
+
+constexpr u32 kThreads = 256;
+constexpr u32 kLogTile = 11;  // 2048 words = 16 KiB of shared memory per block
+
+struct Plan {
+    u32 logN1, logN2, logC, logCpb;
+};
+
+Plan make_plan(u32 logN) {
+    Plan p;
+    p.logN1 = logN / 2;
+    p.logN2 = logN - p.logN1;
+    // columns per phase-1 block, chunks per phase-2 block
+    p.logC = std::min(p.logN2, kLogTile > p.logN1 ? kLogTile - p.logN1 : 0u);
+    p.logCpb = std::min(p.logN1, kLogTile > p.logN2 ? kLogTile - p.logN2 : 0u);
+    return p;
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rows_per_poly, int level, u32 logN1, u32 logC) {
+    extern __shared__ u64 sm[];
+    const u32 N = R.N, C = 1u << logC, N2 = N >> logN1;
+    const u32 row = row_base + blockIdx.y;
+    const u32 mi = mod_index(row % rows_per_poly, level, R.q_count);
+    const u64 q = R.q[mi], q2 = 2 * q;
+    const u64* __restrict__ w = R.tw + size_t(mi) * 4 * N;
+    const u64* __restrict__ ws = w + N;
+    u64* x = data + size_t(row) * N + size_t(blockIdx.x) * C;
+    const u64* xs = src + size_t(row) * N + size_t(blockIdx.x) * C;
+    const u32 tile = 1u << (logN1 + logC);
+    for (u32 e = threadIdx.x; e < tile; e += kThreads) sm[e] = xs[size_t(e >> logC) * N2 + (e & (C - 1))];
+    __syncthreads();
+    for (u32 s = 0; s < logN1; ++s) {
+        const u32 logt = logN1 - 1 - s;
+        for (u32 b = threadIdx.x; b < (tile >> 1); b += kThreads) {
+            const u32 cc = b & (C - 1), bb = b >> logC;
+            const u32 i = bb >> logt, j = bb & ((1u << logt) - 1);
+            const u32 a0 = ((((i << 1) << logt) + j) << logC) + cc;
+            const u32 a1 = a0 + (1u << (logt + logC));
+            const u32 widx = (1u << s) + i;
+            u64 u = sm[a0], v = sm[a1];
+            if (u >= q2) u -= q2;
+            v = shoup_lazy(v, w[widx], ws[widx], q);
+            sm[a0] = u + v;
+            sm[a1] = u - v + q2;
+        }
+        __syncthreads();
+    }
+    for (u32 e = threadIdx.x; e < tile; e += kThreads) x[size_t(e >> logC) * N2 + (e & (C - 1))] = sm[e];
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_fwd_chunks(DevRing R, u64* __restrict__ data, u32 row_base, u32 rows_per_poly, int level, u32 logN1, u32 logCpb) {
+    extern __shared__ u64 sm[];
+    const u32 N = R.N, logN = R.logN, logN2 = logN - logN1;
+    const u32 row = row_base + blockIdx.y;
+    const u32 mi = mod_index(row % rows_per_poly, level, R.q_count);
+    const u64 q = R.q[mi], q2 = 2 * q;
+    const u64* __restrict__ w = R.tw + size_t(mi) * 4 * N;
+    const u64* __restrict__ ws = w + N;
+    const u32 chunk0 = blockIdx.x << logCpb;
+    const u32 tile = 1u << (logN2 + logCpb);
+    u64* x = data + size_t(row) * N + (size_t(chunk0) << logN2);
+    for (u32 e = threadIdx.x; e < tile; e += kThreads) sm[e] = x[e];
+    __syncthreads();
+    for (u32 s = logN1; s < logN; ++s) {
+        const u32 logt = logN - 1 - s;
+        for (u32 b = threadIdx.x; b < (tile >> 1); b += kThreads) {
+            const u32 cl = b >> (logN2 - 1), bb = b & ((1u << (logN2 - 1)) - 1);
+            const u32 il = bb >> logt, j = bb & ((1u << logt) - 1);
+            const u32 a0 = (cl << logN2) + ((il << 1) << logt) + j;
+            const u32 a1 = a0 + (1u << logt);
+            const u32 widx = (1u << s) + ((chunk0 + cl) << (s - logN1)) + il;
+            u64 u = sm[a0], v = sm[a1];
+            if (u >= q2) u -= q2;
+            v = shoup_lazy(v, w[widx], ws[widx], q);
+            sm[a0] = u + v;
+            sm[a1] = u - v + q2;
+        }
+        __syncthreads();
+    }
+    for (u32 e = threadIdx.x; e < tile; e += kThreads) {
+        u64 v = sm[e];
+        if (v >= q2) v -= q2;
+        if (v >= q) v -= q;
+        x[e] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_inv_chunks(DevRing R, u64* data, const u64* src, u32 row_base, u32 rows_per_poly, int level, u32 logN1, u32 logCpb) {
+    extern __shared__ u64 sm[];
+    const u32 N = R.N, logN = R.logN, logN2 = logN - logN1;
+    const u32 row = row_base + blockIdx.y;
+    const u32 mi = mod_index(row % rows_per_poly, level, R.q_count);
+    const u64 q = R.q[mi], q2 = 2 * q;
+    const u64* __restrict__ w = R.tw + size_t(mi) * 4 * N + 2 * size_t(N);  // winv
+    const u64* __restrict__ ws = w + N;
+    const u32 chunk0 = blockIdx.x << logCpb;
+    const u32 tile = 1u << (logN2 + logCpb);
+    u64* x = data + size_t(row) * N + (size_t(chunk0) << logN2);
+    const u64* xs = src + size_t(row) * N + (size_t(chunk0) << logN2);
+    for (u32 e = threadIdx.x; e < tile; e += kThreads) sm[e] = xs[e];
+    __syncthreads();
+    // h = 2^lh from N/2 down to N1: t = N/(2h) < N2 (chunk-local)
+    for (int lh = int(logN) - 1; lh >= int(logN1); --lh) {
+        const u32 logt = logN - 1 - u32(lh);
+        for (u32 b = threadIdx.x; b < (tile >> 1); b += kThreads) {
+            const u32 cl = b >> (logN2 - 1), bb = b & ((1u << (logN2 - 1)) - 1);
+            const u32 il = bb >> logt, j = bb & ((1u << logt) - 1);
+            const u32 a0 = (cl << logN2) + ((il << 1) << logt) + j;
+            const u32 a1 = a0 + (1u << logt);
+            const u32 widx = (1u << lh) + ((chunk0 + cl) << (u32(lh) - logN1)) + il;
+            u64 u = sm[a0], v = sm[a1];
+            u64 s0 = u + v;
+            if (s0 >= q2) s0 -= q2;
+            sm[a0] = s0;
+            sm[a1] = shoup_lazy(u - v + q2, w[widx], ws[widx], q);
+        }
+        __syncthreads();
+    }
+    for (u32 e = threadIdx.x; e < tile; e += kThreads) x[e] = sm[e];
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_inv_cols(DevRing R, u64* __restrict__ data, u32 row_base, u32 rows_per_poly, int level, u32 logN1, u32 logC) {
+    extern __shared__ u64 sm[];
+    const u32 N = R.N, C = 1u << logC, N2 = N >> logN1;
+    const u32 row = row_base + blockIdx.y;
+    const u32 mi = mod_index(row % rows_per_poly, level, R.q_count);
+    const u64 q = R.q[mi], q2 = 2 * q;
+    const u64* __restrict__ w = R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
+    const u64* __restrict__ ws = w + N;
+    const u64 ninv = R.ninv[2 * mi], ninv_s = R.ninv[2 * mi + 1];
+    u64* x = data + size_t(row) * N + size_t(blockIdx.x) * C;
+    const u32 tile = 1u << (logN1 + logC);
+    for (u32 e = threadIdx.x; e < tile; e += kThreads) sm[e] = x[size_t(e >> logC) * N2 + (e & (C - 1))];
+    __syncthreads();
+    // h = 2^lh from N1/2 down to 1: column stride t' = N1/(2h)
+    for (int lh = int(logN1) - 1; lh >= 0; --lh) {
+        const u32 logt = logN1 - 1 - u32(lh);
+        for (u32 b = threadIdx.x; b < (tile >> 1); b += kThreads) {
+            const u32 cc = b & (C - 1), bb = b >> logC;
+            const u32 i = bb >> logt, j = bb & ((1u << logt) - 1);
+            const u32 a0 = ((((i << 1) << logt) + j) << logC) + cc;
+            const u32 a1 = a0 + (1u << (logt + logC));
+            const u32 widx = (1u << lh) + i;
+            u64 u = sm[a0], v = sm[a1];
+            u64 s0 = u + v;
+            if (s0 >= q2) s0 -= q2;
+            sm[a0] = s0;
+            sm[a1] = shoup_lazy(u - v + q2, w[widx], ws[widx], q);
+        }
+        __syncthreads();
+    }
+    for (u32 e = threadIdx.x; e < tile; e += kThreads)
+        x[size_t(e >> logC) * N2 + (e & (C - 1))] = shoup(sm[e], ninv, ninv_s, q);
+}
+
+}  // namespace
+
+int ntt_forward_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s) {
+    return ntt_forward_oop(ctx, data, data, level, nspecial, npolys, s);
+}
+
+int ntt_inverse_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s) {
+    return ntt_inverse_oop(ctx, data, data, level, nspecial, npolys, s);
+}
+
+int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s) {
+    const DevRing& R = ctx->ring;
+    const Plan p = make_plan(R.logN);
+    const u32 rpp = u32(level + 1 + nspecial);
+    const u32 total = rpp * npolys;
+    const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
+    for (u32 base = 0; base < total; base += 65535) {
+        const u32 rows = std::min(65535u, total - base);
+        dim3 g1((R.N >> p.logN1) >> p.logC, rows), g2((1u << p.logN1) >> p.logCpb, rows);
+        k_fwd_cols<<<g1, kThreads, sm1, s>>>(R, data, src, base, rpp, level, p.logN1, p.logC);
+        k_fwd_chunks<<<g2, kThreads, sm2, s>>>(R, data, base, rpp, level, p.logN1, p.logCpb);
+    }
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+int ntt_inverse_oop(tg_context* ctx, u64* data, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s) {
+    const DevRing& R = ctx->ring;
+    const Plan p = make_plan(R.logN);
+    const u32 rpp = u32(level + 1 + nspecial);
+    const u32 total = rpp * npolys;
+    const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
+    for (u32 base = 0; base < total; base += 65535) {
+        const u32 rows = std::min(65535u, total - base);
+        dim3 g1((R.N >> p.logN1) >> p.logC, rows), g2((1u << p.logN1) >> p.logCpb, rows);
+        k_inv_chunks<<<g2, kThreads, sm2, s>>>(R, data, src, base, rpp, level, p.logN1, p.logCpb);
+        k_inv_cols<<<g1, kThreads, sm1, s>>>(R, data, base, rpp, level, p.logN1, p.logC);
+    }
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+}  // namespace tg
+
+using namespace tg;
+
+static int check_shape(tg_context* ctx, int level, int nspecial) {
+    if (!ctx) return fail(TG_E_ARG, "[ring] null context");
+    if (level < 0 || u32(level) >= ctx->ring.q_count) return fail(TG_E_ARG, "[ring] poly level out of range");
+    if (nspecial != 0 && u32(nspecial) != ctx->ring.K) return fail(TG_E_ARG, "[ring] special rows must be all-or-none");
+    return TG_OK;
+}
+
+extern "C" int tg_ntt_forward(tg_context* ctx, uint64_t* data, int level, int nspecial, uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    return ntt_forward_rows(ctx, data, level, nspecial, npolys, as_stream(stream));
+}
+
+extern "C" int tg_ntt_inverse(tg_context* ctx, uint64_t* data, int level, int nspecial, uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    return ntt_inverse_rows(ctx, data, level, nspecial, npolys, as_stream(stream));
+}
+
+extern "C" int tg_ntt_forward_oop(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, int nspecial,
+                                  uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    return ntt_forward_oop(ctx, out, in, level, nspecial, npolys, as_stream(stream));
+}
+
+extern "C" int tg_ntt_inverse_oop(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, int nspecial,
+                                  uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    return ntt_inverse_oop(ctx, out, in, level, nspecial, npolys, as_stream(stream));
+}

@@ -1,0 +1,291 @@
+// Element-wise ring and CKKS residue kernels (HBM-bound, coalesced, one
+// grid-stride pass per op). Each kernel cites the reference loop it replaces.
+#include "tg_internal.cuh"
+
+namespace tg {
+namespace {
+
+constexpr u32 kThreads = 256;
+
+inline u32 grid_for(size_t work) {
+    // 148 SMs x 8 resident 256-thread blocks; grid-stride beyond that
+    size_t b = (work + kThreads - 1) / kThreads;
+    return u32(std::min<size_t>(b, size_t(148) * 8 * 4));
+}
+
+struct Shape {
+    u32 rpp;  // rows per poly
+    int level;
+    u64 words;  // total words
+};
+
+__device__ __forceinline__ u32 row_mod(const DevRing& R, const Shape& S, u64 idx) {
+    const u32 row = u32(idx >> R.logN);
+    return mod_index(row % S.rpp, S.level, R.q_count);
+}
+
+// Poly::add_inplace / sub_inplace / negate_inplace (ring.hpp:250-276)
+__global__ void k_addsub(DevRing R, Shape S, u64* out, const u64* a, const u64* b, int op) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u64 q = R.q[row_mod(R, S, i)];
+        const u64 x = a[i];
+        u64 r;
+        if (op == 0) r = add_mod(x, b[i], q);
+        else if (op == 1) r = sub_mod(x, b[i], q);
+        else r = neg_mod(x, q);
+        out[i] = r;
+    }
+}
+
+// Poly::mul_pointwise_inplace (ring.hpp:278-288) and mul_acc_pointwise (:290-304)
+__global__ void k_mul(DevRing R, Shape S, u64* out, const u64* a, const u64* b, int acc) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u32 m = row_mod(R, S, i);
+        const u64 q = R.q[m];
+        u64 r = mul_mod(a[i], b[i], q, R.ratio[2 * m], R.ratio[2 * m + 1]);
+        if (acc) r = add_mod(out[i], r, q);
+        out[i] = r;
+    }
+}
+
+struct Scalars {
+    u64 s[kMaxMod];
+    u64 ss[kMaxMod];
+};
+
+// Poly::mul_scalar_inplace (ring.hpp:307-315): Shoup with per-modulus scalar
+__global__ void k_mul_scalar(DevRing R, Shape S, u64* out, const u64* a, Scalars sc) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u32 m = row_mod(R, S, i);
+        out[i] = shoup(a[i], sc.s[m], sc.ss[m], R.q[m]);
+    }
+}
+
+// Evaluator::add_scalar residue update (ckks.hpp:299-311)
+__global__ void k_add_scalar(DevRing R, Shape S, u64* out, const u64* a, Scalars sc, int eval_form) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u32 m = row_mod(R, S, i);
+        u64 v = a[i];
+        if (eval_form || (i & (R.N - 1)) == 0) v = add_mod(v, sc.s[m], R.q[m]);
+        out[i] = v;
+    }
+}
+
+// automorphism_apply, coefficient form (ring.hpp:417-427): signed scatter
+__global__ void k_auto_coeff(DevRing R, Shape S, u64* out, const u64* in, u64 g) {
+    const u64 two_n = 2 * u64(R.N);
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u64 row_off = i & ~u64(R.N - 1);
+        const u64 c = i & (R.N - 1);
+        const u64 j = (c * g) % two_n;
+        const u64 v = in[i];
+        if (j < R.N) out[row_off + j] = v;
+        else out[row_off + j - R.N] = neg_mod(v, R.q[row_mod(R, S, i)]);
+    }
+}
+
+// automorphism_apply, evaluation form (ring.hpp:428-434): slot gather
+__global__ void k_auto_eval(DevRing R, Shape S, u64* out, const u64* in, u64 g) {
+    const u64 two_n = 2 * u64(R.N);
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u64 row_off = i & ~u64(R.N - 1);
+        const u32 j = u32(i & (R.N - 1));
+        const u32 src = R.slot_of_exp[u32((u64(R.eval_exp[j]) * g) % two_n)];
+        out[i] = in[row_off + src];
+    }
+}
+
+// rescale_round (ring.hpp:493-518): thread per coefficient, loop over targets
+__global__ void k_rescale(DevRing R, u64* out, const u64* in, int level, u32 npolys) {
+    const u32 N = R.N, lvl = u32(level);
+    const u64 total = u64(npolys) * N;
+    const u64 ql = R.q[lvl];
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
+        const u64 p = i >> R.logN, c = i & (N - 1);
+        const u64* src = in + p * (lvl + 1) * N;
+        u64* dst = out + p * lvl * N;
+        const u64 last = src[size_t(lvl) * N + c];
+        for (u32 r = 0; r < lvl; ++r) {
+            const u64 q = R.q[r];
+            const u64* e = R.rs + (size_t(lvl) * R.q_count + r) * 4;
+            u64 t = last < q ? last : reduce64(last, q, R.ratio[2 * r], R.ratio[2 * r + 1]);
+            if (last > e[3]) t = sub_mod(t, e[0], q);  // centered remainder
+            dst[size_t(r) * N + c] = shoup(sub_mod(src[size_t(r) * N + c], t, q), e[1], e[2], q);
+        }
+        (void)ql;
+    }
+}
+
+// Evaluator::mul tensor (ckks.hpp:229-237)
+__global__ void k_tensor(DevRing R, Shape S, u64* p0, u64* p1, u64* p2, const u64* x0, const u64* x1,
+                         const u64* y0, const u64* y1) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u32 m = row_mod(R, S, i);
+        const u64 q = R.q[m], rl = R.ratio[2 * m], rh = R.ratio[2 * m + 1];
+        const u64 a0 = x0[i], a1 = x1[i], b0 = y0[i], b1 = y1[i];
+        p0[i] = mul_mod(a0, b0, q, rl, rh);
+        // x0*y1 + x1*y0 as one 128-bit sum (< 2^125), one reduction
+        U128 acc{0, 0};
+        mac128(acc, a0, b1);
+        mac128(acc, a1, b0);
+        p1[i] = barrett128(acc.lo, acc.hi, q, rl, rh);
+        p2[i] = mul_mod(a1, b1, q, rl, rh);
+    }
+}
+
+// Evaluator::mul_plain (ckks.hpp:257-265): part row r x plain row m (= r here)
+__global__ void k_mul_plain(DevRing R, u64* out, const u64* ct, const u64* plain, int level, u32 nparts) {
+    const u32 N = R.N, rows = u32(level) + 1;
+    const u64 per = u64(rows) * N, total = per * nparts;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
+        const u64 w = i % per;
+        const u32 m = u32(w >> R.logN);
+        out[i] = mul_mod(ct[i], plain[w], R.q[m], R.ratio[2 * m], R.ratio[2 * m + 1]);
+    }
+}
+
+}  // namespace
+}  // namespace tg
+
+using namespace tg;
+
+static int check_shape(tg_context* ctx, int level, int nspecial) {
+    if (!ctx) return fail(TG_E_ARG, "[ring] null context");
+    if (level < 0 || u32(level) >= ctx->ring.q_count) return fail(TG_E_ARG, "[ring] poly level out of range");
+    if (nspecial != 0 && u32(nspecial) != ctx->ring.K) return fail(TG_E_ARG, "[ring] special rows must be all-or-none");
+    return TG_OK;
+}
+
+static Shape shape_of(tg_context* ctx, int level, int nspecial, u32 npolys) {
+    Shape S;
+    S.rpp = u32(level + 1 + nspecial);
+    S.level = level;
+    S.words = u64(S.rpp) * npolys * ctx->ring.N;
+    return S;
+}
+
+extern "C" int tg_poly_addsub(tg_context* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int op, int level,
+                              int nspecial, uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    TG_REQUIRE(op >= 0 && op <= 2, "[ring] addsub op must be 0 (add), 1 (sub) or 2 (neg)");
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, nspecial, npolys);
+    k_addsub<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, a, b, op);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_poly_mul(tg_context* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int level,
+                           int nspecial, uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, nspecial, npolys);
+    k_mul<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, a, b, 0);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_poly_mul_acc(tg_context* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int level,
+                               int nspecial, uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, nspecial, npolys);
+    k_mul<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, a, b, 1);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+static Scalars make_scalars(tg_context* ctx, const uint64_t* per_mod, bool shoup_pre) {
+    Scalars sc{};
+    for (u32 m = 0; m < ctx->ring.nmod; ++m) {
+        u64 q = ctx->h_q[m];
+        u64 s = per_mod[m] % q;
+        sc.s[m] = s;
+        sc.ss[m] = shoup_pre ? h_shoup(s, q) : 0;
+    }
+    return sc;
+}
+
+extern "C" int tg_poly_mul_scalar(tg_context* ctx, uint64_t* out, const uint64_t* a,
+                                  const uint64_t* scalar_per_modulus, int level, int nspecial, uint32_t npolys,
+                                  void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    TG_REQUIRE(scalar_per_modulus, "[ring] null scalar table");
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, nspecial, npolys);
+    k_mul_scalar<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, a,
+                                                                        make_scalars(ctx, scalar_per_modulus, true));
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_poly_add_scalar(tg_context* ctx, uint64_t* out, const uint64_t* a, const uint64_t* add_per_modulus,
+                                  int form, int level, int nspecial, uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    TG_REQUIRE(add_per_modulus, "[ring] null scalar table");
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, nspecial, npolys);
+    k_add_scalar<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(
+        ctx->ring, S, out, a, make_scalars(ctx, add_per_modulus, false), form == TG_FORM_EVAL ? 1 : 0);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_automorphism(tg_context* ctx, uint64_t* out, const uint64_t* in, uint64_t exponent, int form,
+                               int level, int nspecial, uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    const u64 two_n = 2 * u64(ctx->ring.N);
+    const u64 g = exponent % two_n;
+    TG_REQUIRE(g % 2 == 1, "[ring] automorphism exponent must be odd");
+    TG_REQUIRE(out != in, "[ring] automorphism output must not alias its input");
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, nspecial, npolys);
+    if (form == TG_FORM_COEFF)
+        k_auto_coeff<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, in, g);
+    else
+        k_auto_eval<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, in, g);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_rescale(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, uint32_t npolys,
+                          void* stream) {
+    if (int rc = check_shape(ctx, level, 0)) return rc;
+    TG_REQUIRE(level >= 1, "[ring] cannot rescale at level 0");
+    TG_REQUIRE(out != in, "[ring] rescale output must not alias its input");
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    k_rescale<<<grid_for(size_t(npolys) * ctx->ring.N), kThreads, 0, as_stream(stream)>>>(ctx->ring, out, in, level,
+                                                                                          npolys);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const uint64_t* x0,
+                         const uint64_t* x1, const uint64_t* y0, const uint64_t* y1, int level, uint32_t npolys,
+                         void* stream) {
+    if (int rc = check_shape(ctx, level, 0)) return rc;
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, 0, npolys);
+    k_tensor<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, p0, p1, p2, x0, x1, y0, y1);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_mul_plain(tg_context* ctx, uint64_t* out, const uint64_t* ct_part, const uint64_t* plain, int level,
+                            uint32_t nparts, void* stream) {
+    if (int rc = check_shape(ctx, level, 0)) return rc;
+    if (nparts == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    size_t words = size_t(level + 1) * ctx->ring.N * nparts;
+    k_mul_plain<<<grid_for(words), kThreads, 0, as_stream(stream)>>>(ctx->ring, out, ct_part, plain, level, nparts);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
