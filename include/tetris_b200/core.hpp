@@ -112,6 +112,17 @@ struct NttTables {
     void init(u64 modulus, u32 degree, Rng& rng);
 };
 
+// Device context + stream of one ring. Shared by the ring and every device
+// buffer allocated on it, so buffers may safely outlive their RingParams.
+struct DeviceState {
+    tg_context* ctx = nullptr;
+    void* stream = nullptr;
+    DeviceState() = default;
+    DeviceState(const DeviceState&) = delete;
+    DeviceState& operator=(const DeviceState&) = delete;
+    ~DeviceState();
+};
+
 // Per-process default CUDA device for new contexts (torchrun: LOCAL_RANK).
 void set_default_device(int device);
 int default_device();
@@ -144,6 +155,7 @@ public:
     // Device side (lazy).
     tg_context* dev() const;
     void* stream() const;  // cudaStream_t of this ring's work
+    const std::shared_ptr<DeviceState>& device_state() const;
     void synchronize() const;
     int device() const { return device_; }
 
@@ -156,8 +168,7 @@ private:
     std::vector<u32> eval_exp_, slot_of_exp_;
     int device_;
     mutable std::once_flag dev_once_;
-    mutable tg_context* dev_ = nullptr;
-    mutable void* stream_ = nullptr;
+    mutable std::shared_ptr<DeviceState> dev_;
 };
 
 // Device buffer (stream-ordered pool allocation on the ring's stream).
@@ -171,7 +182,7 @@ public:
     std::size_t words() const { return words_; }
 
 private:
-    const RingParams* ring_;
+    std::shared_ptr<DeviceState> dev_;
     u64* ptr_ = nullptr;
     std::size_t words_ = 0;
 };

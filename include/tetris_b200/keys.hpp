@@ -43,6 +43,7 @@ private:
     const RingParams* ring_ = nullptr;
     GadgetVector cfg_;
     mutable std::once_flag once_;
+    mutable std::shared_ptr<DeviceState> devstate_;  // keeps the context alive past the ring
     mutable tg_gadget* dev_ = nullptr;
 };
 

@@ -208,7 +208,15 @@ double RingParams::total_log2_q(int level) const {
     return s;
 }
 
-tg_context* RingParams::dev() const {
+DeviceState::~DeviceState() {
+    if (ctx) {
+        tg_stream_sync(ctx, stream);
+        tg_stream_destroy(ctx, stream);
+        tg_context_destroy(ctx);
+    }
+}
+
+const std::shared_ptr<DeviceState>& RingParams::device_state() const {
     std::call_once(dev_once_, [this] {
         const u32 nmod = u32(moduli_.size());
         std::vector<u64> tw(size_t(4) * nmod * degree_);
@@ -223,48 +231,35 @@ tg_context* RingParams::dev() const {
             ninv[2 * i] = t.n_inv;
             ninv[2 * i + 1] = t.n_inv_shoup;
         }
-        tg_context* c = nullptr;
-        check_tg(tg_context_create(&c, device_, degree_, moduli_.data(), nmod, special_count_, tw.data(), ninv.data(),
-                                   eval_exp_.data(), slot_of_exp_.data()));
-        void* s = nullptr;
-        int rc = tg_stream_create(c, &s);
-        if (rc != TG_OK) {
-            tg_context_destroy(c);
-            check_tg(rc);
-        }
-        stream_ = s;
-        dev_ = c;
+        auto st = std::make_shared<DeviceState>();
+        check_tg(tg_context_create(&st->ctx, device_, degree_, moduli_.data(), nmod, special_count_, tw.data(),
+                                   ninv.data(), eval_exp_.data(), slot_of_exp_.data()));
+        check_tg(tg_stream_create(st->ctx, &st->stream));
+        dev_ = std::move(st);
     });
     if (!dev_) throw TetrisError("gpu", "device context unavailable");
     return dev_;
 }
 
-void* RingParams::stream() const {
-    dev();
-    return stream_;
-}
+tg_context* RingParams::dev() const { return device_state()->ctx; }
+
+void* RingParams::stream() const { return device_state()->stream; }
 
 void RingParams::synchronize() const { check_tg(tg_stream_sync(dev(), stream())); }
 
-RingParams::~RingParams() {
-    if (dev_) {
-        tg_stream_sync(dev_, stream_);
-        tg_stream_destroy(dev_, stream_);
-        tg_context_destroy(dev_);
-    }
-}
+RingParams::~RingParams() = default;
 
 // ---------------------------------------------------------------------------
 // Device storage and Poly
 // ---------------------------------------------------------------------------
-DeviceBuffer::DeviceBuffer(const RingParams& ring, std::size_t words) : ring_(&ring), words_(words) {
+DeviceBuffer::DeviceBuffer(const RingParams& ring, std::size_t words) : dev_(ring.device_state()), words_(words) {
     void* p = nullptr;
-    check_tg(tg_alloc(ring.dev(), &p, words * 8, ring.stream()));
+    check_tg(tg_alloc(dev_->ctx, &p, words * 8, dev_->stream));
     ptr_ = static_cast<u64*>(p);
 }
 
 DeviceBuffer::~DeviceBuffer() {
-    if (ptr_) tg_free(ring_->dev(), ptr_, ring_->stream());
+    if (ptr_) tg_free(dev_->ctx, ptr_, dev_->stream);
 }
 
 Poly::Poly(const RingParams& ring, int level, Form form, int nspecial)

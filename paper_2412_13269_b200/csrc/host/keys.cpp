@@ -37,7 +37,8 @@ GadgetPlan::~GadgetPlan() {
 tg_gadget* GadgetPlan::dev() const {
     std::call_once(once_, [this] {
         tg_gadget* g = nullptr;
-        check_tg(tg_gadget_create(&g, ring_->dev(), cfg_.group_size, cfg_.base2_bits));
+        devstate_ = ring_->device_state();
+        check_tg(tg_gadget_create(&g, devstate_->ctx, cfg_.group_size, cfg_.base2_bits));
         dev_ = g;
     });
     if (!dev_) throw TetrisError("gpu", "gadget tables unavailable");

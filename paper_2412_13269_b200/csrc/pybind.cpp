@@ -118,9 +118,9 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("mul_small_scalar_inplace", &Poly::mul_small_scalar_inplace)
         .def("drop_to_level", &Poly::drop_to_level);
 
-    m.def("ntt_transform", &ntt_transform);
-    m.def("automorphism_apply", &automorphism_apply);
-    m.def("rescale_round", &rescale_round);
+    m.def("ntt_transform", &ntt_transform, py::keep_alive<0, 1>());
+    m.def("automorphism_apply", &automorphism_apply, py::keep_alive<0, 1>());
+    m.def("rescale_round", &rescale_round, py::keep_alive<0, 1>());
     m.def("sample_uniform", &sample_uniform, py::keep_alive<0, 1>());
     m.def("sample_gaussian", &sample_gaussian, py::keep_alive<0, 1>());
     m.def("sample_ternary_hw", &sample_ternary_hw, py::keep_alive<0, 1>());
@@ -194,22 +194,22 @@ PYBIND11_MODULE(_tetris_b200, m) {
     py::class_<KeyContext>(m, "KeyContext")
         .def(py::init<const RingParams&, NoiseParams, GadgetVector>(), py::keep_alive<1, 2>())
         .def("keygen", &KeyContext::keygen)
-        .def("relin_key_gen", &KeyContext::relin_key_gen)
-        .def("galois_key_gen", &KeyContext::galois_key_gen)
-        .def("switch_key_gen", &KeyContext::switch_key_gen)
-        .def("encrypt", &KeyContext::encrypt, py::arg("sk"), py::arg("m"), py::arg("scale"), py::arg("rng"),
+        .def("relin_key_gen", &KeyContext::relin_key_gen, py::keep_alive<0, 1>())
+        .def("galois_key_gen", &KeyContext::galois_key_gen, py::keep_alive<0, 1>())
+        .def("switch_key_gen", &KeyContext::switch_key_gen, py::keep_alive<0, 1>())
+        .def("encrypt", &KeyContext::encrypt, py::keep_alive<0, 1>(), py::arg("sk"), py::arg("m"), py::arg("scale"), py::arg("rng"),
              py::arg("domain") = Domain::coeffs)
-        .def("encrypt_pk", &KeyContext::encrypt_pk, py::arg("pk"), py::arg("m"), py::arg("scale"), py::arg("rng"),
+        .def("encrypt_pk", &KeyContext::encrypt_pk, py::keep_alive<0, 1>(), py::arg("pk"), py::arg("m"), py::arg("scale"), py::arg("rng"),
              py::arg("domain") = Domain::coeffs)
-        .def("decrypt", &KeyContext::decrypt)
+        .def("decrypt", &KeyContext::decrypt, py::keep_alive<0, 1>())
         .def("decompose", [](const KeyContext& c, const Poly& d) { return c.plan().decompose(d); })
         .def("digit_count", [](const KeyContext& c, int level) { return c.plan().digit_count(level); })
         .def("ks_inner", &KeyContext::ks_inner)
         .def("switch_key_apply", &KeyContext::switch_key_apply)
-        .def("mod_down_p", &KeyContext::mod_down_p)
-        .def("relinearize", &KeyContext::relinearize)
-        .def("apply_galois", &KeyContext::apply_galois)
-        .def("square_secret", &KeyContext::square_secret);
+        .def("mod_down_p", &KeyContext::mod_down_p, py::keep_alive<0, 1>())
+        .def("relinearize", &KeyContext::relinearize, py::keep_alive<0, 1>())
+        .def("apply_galois", &KeyContext::apply_galois, py::keep_alive<0, 1>())
+        .def("square_secret", &KeyContext::square_secret, py::keep_alive<0, 1>());
 
     m.def("rotation_exponent", &rotation_exponent);
     m.def("conjugation_exponent", &conjugation_exponent);
@@ -217,7 +217,7 @@ PYBIND11_MODULE(_tetris_b200, m) {
     py::class_<Encoder>(m, "Encoder")
         .def(py::init<const RingParams&, u32>(), py::keep_alive<1, 2>())
         .def("slots", &Encoder::slots)
-        .def("encode_slots", &Encoder::encode_slots, py::call_guard<py::gil_scoped_release>())
+        .def("encode_slots", &Encoder::encode_slots, py::keep_alive<0, 1>())
         .def("decode_slots", &Encoder::decode_slots, py::call_guard<py::gil_scoped_release>())
         .def("encode_coeffs", &Encoder::encode_coeffs)
         .def("decode_coeffs", &Encoder::decode_coeffs)
@@ -234,20 +234,20 @@ PYBIND11_MODULE(_tetris_b200, m) {
 
     py::class_<Evaluator>(m, "Evaluator")
         .def(py::init<const KeyContext&>(), py::keep_alive<1, 2>())
-        .def("add", &Evaluator::add)
-        .def("sub", &Evaluator::sub)
-        .def("mul", &Evaluator::mul)
-        .def("mul_relin", &Evaluator::mul_relin)
-        .def("mul_plain", &Evaluator::mul_plain)
-        .def("mul_scalar", &Evaluator::mul_scalar)
-        .def("add_scalar", &Evaluator::add_scalar)
-        .def("rescale", &Evaluator::rescale)
-        .def("rotate", &Evaluator::rotate)
-        .def("conjugate", &Evaluator::conjugate)
+        .def("add", &Evaluator::add, py::keep_alive<0, 1>())
+        .def("sub", &Evaluator::sub, py::keep_alive<0, 1>())
+        .def("mul", &Evaluator::mul, py::keep_alive<0, 1>())
+        .def("mul_relin", &Evaluator::mul_relin, py::keep_alive<0, 1>())
+        .def("mul_plain", &Evaluator::mul_plain, py::keep_alive<0, 1>())
+        .def("mul_scalar", &Evaluator::mul_scalar, py::keep_alive<0, 1>())
+        .def("add_scalar", &Evaluator::add_scalar, py::keep_alive<0, 1>())
+        .def("rescale", &Evaluator::rescale, py::keep_alive<0, 1>())
+        .def("rotate", &Evaluator::rotate, py::keep_alive<0, 1>())
+        .def("conjugate", &Evaluator::conjugate, py::keep_alive<0, 1>())
         .def_static("scaled_residue", &Evaluator::scaled_residue);
 
-    m.def("eval_chebyshev", &eval_chebyshev);
-    m.def("inner_sum", &inner_sum);
+    m.def("eval_chebyshev", &eval_chebyshev, py::keep_alive<0, 1>());
+    m.def("inner_sum", &inner_sum, py::keep_alive<0, 1>());
     m.def("power_to_chebyshev", &power_to_chebyshev);
 
     py::class_<ThresholdParams>(m, "ThresholdParams")
@@ -277,8 +277,8 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("eval_step", &MinimaxChain::eval_step)
         .def("levels_required", &MinimaxChain::levels_required);
     m.def("build_chain", &build_chain, py::call_guard<py::gil_scoped_release>());
-    m.def("eval_private_threshold", &eval_private_threshold);
-    m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm);
+    m.def("eval_private_threshold", &eval_private_threshold, py::keep_alive<0, 1>());
+    m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm, py::keep_alive<0, 1>());
 
     // The whole threshold-count query in C++ (no Python between ops):
     // per-ciphertext threshold, sum mod q in index order, one inner_sum
