@@ -80,7 +80,42 @@ int tg_stream_destroy(tg_context* ctx, void* stream);
 /* Device index the context lives on. */
 int tg_context_device(const tg_context* ctx);
 
+/* Page-locked host memory (end-to-end H2D/D2H staging). */
+int tg_host_alloc_pinned(void** ptr, size_t bytes);
+int tg_host_free_pinned(void* ptr);
+
+/* ---- kernel timing -------------------------------------------------------
+ * When enabled, every kernel launch of the context is bracketed by CUDA
+ * events on its stream and attributed to an op class together with its
+ * ALGORITHMIC bytes (inputs read once + outputs written once + key bytes,
+ * SURVEY 8(d)). tg_profile_read synchronizes, accumulates per class and
+ * clears: ms[i], launches[i], bytes[i] for i < TG_OP_COUNT. */
+enum {
+    TG_OP_NTT_FWD = 0,
+    TG_OP_NTT_INV,
+    TG_OP_ADDSUB,
+    TG_OP_MUL,
+    TG_OP_SCALAR,
+    TG_OP_AUTOMORPHISM,
+    TG_OP_RESCALE,
+    TG_OP_TENSOR,
+    TG_OP_MUL_PLAIN,
+    TG_OP_MODUP,
+    TG_OP_KEY_INNER,
+    TG_OP_MOD_DOWN,
+    TG_OP_REDUCE,
+    TG_OP_COUNT
+};
+int tg_profile_enable(tg_context* ctx, int on);
+int tg_profile_read(tg_context* ctx, double* ms, uint64_t* launches, double* bytes);
+const char* tg_profile_op_name(int op);
+
 /* ---- ring layer --------------------------------------------------------- */
+/* Reduces arbitrary words mod their row modulus, in place: the fix-up after
+ * an NCCL integer sum of per-rank partial ciphertexts (exact while
+ * ranks * max q < 2^64). */
+int tg_poly_reduce(tg_context* ctx, uint64_t* data, int level, int nspecial, uint32_t npolys,
+                   void* stream);
 /* Poly::ntt_forward / NttTables::forward (ring.hpp:64-80, :234-239), in place.
  * Negacyclic CT, natural -> bit-reversed evaluation order. */
 int tg_ntt_forward(tg_context* ctx, uint64_t* data, int level, int nspecial, uint32_t npolys,

@@ -204,6 +204,8 @@ PYBIND11_MODULE(tetris_ref, m) {
         .def("encrypt_pk", &KeyContext::encrypt_pk, py::arg("pk"), py::arg("m"), py::arg("scale"),
              py::arg("rng"), py::arg("domain") = Domain::coeffs)
         .def("decrypt", &KeyContext::decrypt)
+        .def("zero_ciphertext", &KeyContext::zero_ciphertext, py::arg("level"), py::arg("scale"),
+             py::arg("sk_id"), py::arg("domain") = Domain::coeffs)
         .def("decompose", [](const KeyContext& c, const Poly& d) { return c.plan().decompose(d); })
         .def("digit_count", [](const KeyContext& c, int level) { return c.plan().digit_count(level); })
         .def("ks_inner", &KeyContext::ks_inner)

@@ -202,6 +202,8 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("encrypt_pk", &KeyContext::encrypt_pk, py::keep_alive<0, 1>(), py::arg("pk"), py::arg("m"), py::arg("scale"), py::arg("rng"),
              py::arg("domain") = Domain::coeffs)
         .def("decrypt", &KeyContext::decrypt, py::keep_alive<0, 1>())
+        .def("zero_ciphertext", &KeyContext::zero_ciphertext, py::keep_alive<0, 1>(), py::arg("level"),
+             py::arg("scale"), py::arg("sk_id"), py::arg("domain") = Domain::coeffs)
         .def("decompose", [](const KeyContext& c, const Poly& d) { return c.plan().decompose(d); })
         .def("digit_count", [](const KeyContext& c, int level) { return c.plan().digit_count(level); })
         .def("ks_inner", &KeyContext::ks_inner)
@@ -279,6 +281,69 @@ PYBIND11_MODULE(_tetris_b200, m) {
     m.def("build_chain", &build_chain, py::call_guard<py::gil_scoped_release>());
     m.def("eval_private_threshold", &eval_private_threshold, py::keep_alive<0, 1>());
     m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm, py::keep_alive<0, 1>());
+
+    // ---- kernel timing, end-to-end transfer helpers --------------------------
+    m.def("profile_enable", [](const RingParams& r, bool on) { check_tg(tg_profile_enable(r.dev(), on ? 1 : 0)); });
+    m.def("profile_read", [](const RingParams& r) {
+        std::vector<double> ms(TG_OP_COUNT), bytes(TG_OP_COUNT);
+        std::vector<uint64_t> n(TG_OP_COUNT);
+        {
+            py::gil_scoped_release nogil;
+            check_tg(tg_profile_read(r.dev(), ms.data(), n.data(), bytes.data()));
+        }
+        py::dict d;
+        for (int i = 0; i < TG_OP_COUNT; ++i)
+            if (n[i]) d[tg_profile_op_name(i)] = py::make_tuple(ms[i], n[i], bytes[i]);
+        return d;
+    });
+    m.def("pinned_empty", [](std::vector<py::ssize_t> shape) {
+        py::ssize_t count = 1;
+        for (auto s : shape) count *= s;
+        void* p = nullptr;
+        check_tg(tg_host_alloc_pinned(&p, std::max<py::ssize_t>(count, 1) * 8));
+        py::capsule owner(p, [](void* q) { tg_host_free_pinned(q); });
+        return py::array_t<uint64_t>(shape, static_cast<uint64_t*>(p), owner);
+    });
+    // Ciphertext <-> host array of shape (parts, rows, N): one H2D / D2H copy
+    // per call on the ring's stream (pinned memory makes it a DMA copy).
+    m.def(
+        "ciphertext_from_numpy",
+        [](const RingParams& ring, py::array_t<uint64_t, py::array::c_style> a, int level, Form form, double scale,
+           Domain domain, u64 sk_id) {
+            if (a.ndim() != 3 || a.shape(1) != level + 1 || a.shape(2) != py::ssize_t(ring.degree()))
+                throw TetrisError("ckks", "ciphertext_from_numpy: shape mismatch");
+            const int np = int(a.shape(0));
+            const std::size_t w = std::size_t(level + 1) * ring.degree();
+            auto blk = std::make_shared<DeviceBuffer>(ring, w * np);
+            {
+                py::gil_scoped_release nogil;
+                check_tg(tg_memcpy_h2d(ring.dev(), blk->data(), a.data(), w * np * 8, ring.stream()));
+                ring.synchronize();
+            }
+            Ciphertext ct;
+            for (int i = 0; i < np; ++i) ct.parts.push_back(Poly::view(ring, blk, w * i, level, form, 0));
+            ct.scale = scale;
+            ct.domain = domain;
+            ct.sk_id = sk_id;
+            return ct;
+        },
+        py::keep_alive<0, 1>());
+    m.def("ciphertext_to_numpy", [](const Ciphertext& ct, py::array_t<uint64_t, py::array::c_style> out) {
+        const RingParams& ring = ct.ring();
+        const std::size_t w = ct.parts[0].words();
+        if (std::size_t(out.size()) != w * ct.parts.size())
+            throw TetrisError("ckks", "ciphertext_to_numpy: size mismatch");
+        uint64_t* dst = out.mutable_data();
+        py::gil_scoped_release nogil;
+        for (std::size_t i = 0; i < ct.parts.size(); ++i)
+            check_tg(tg_memcpy_d2h(ring.dev(), dst + w * i, ct.parts[i].data(), w * 8, ring.stream()));
+        ring.synchronize();
+    });
+    // Post-NCCL fix-up of a summed partial ciphertext (see tg_poly_reduce).
+    m.def("ciphertext_reduce_inplace", [](Ciphertext& ct) {
+        for (auto& p : ct.parts)
+            check_tg(tg_poly_reduce(p.ring().dev(), p.mutable_data(), p.level(), p.nspecial(), 1, p.ring().stream()));
+    });
 
     // The whole threshold-count query in C++ (no Python between ops):
     // per-ciphertext threshold, sum mod q in index order, one inner_sum

@@ -134,6 +134,11 @@ extern "C" void tg_context_destroy(tg_context* ctx) {
     if (!ctx) return;
     DeviceGuard guard(ctx->device);
     cudaDeviceSynchronize();
+    for (auto& r : ctx->prof_recs) {
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+    }
+    for (auto e : ctx->prof_free) cudaEventDestroy(e);
     cudaFree(ctx->dev_block);
     delete ctx;
 }
@@ -181,6 +186,51 @@ extern "C" int tg_stream_sync(tg_context* ctx, void* stream) {
     DeviceGuard guard(ctx->device);
     TG_CUDA(cudaStreamSynchronize(as_stream(stream)));
     return TG_OK;
+}
+
+extern "C" int tg_host_alloc_pinned(void** ptr, size_t bytes) {
+    if (!ptr) return fail(TG_E_ARG, "[gpu] null argument");
+    TG_CUDA(cudaHostAlloc(ptr, bytes, cudaHostAllocDefault));
+    return TG_OK;
+}
+extern "C" int tg_host_free_pinned(void* ptr) {
+    if (ptr) TG_CUDA(cudaFreeHost(ptr));
+    return TG_OK;
+}
+
+extern "C" int tg_profile_enable(tg_context* ctx, int on) {
+    if (!ctx) return fail(TG_E_ARG, "[gpu] null context");
+    ctx->prof_on = on != 0;
+    return TG_OK;
+}
+
+extern "C" int tg_profile_read(tg_context* ctx, double* ms, uint64_t* launches, double* bytes) {
+    if (!ctx) return fail(TG_E_ARG, "[gpu] null context");
+    DeviceGuard guard(ctx->device);
+    for (int i = 0; i < TG_OP_COUNT; ++i) {
+        if (ms) ms[i] = 0;
+        if (launches) launches[i] = 0;
+        if (bytes) bytes[i] = 0;
+    }
+    for (auto& r : ctx->prof_recs) {
+        TG_CUDA(cudaEventSynchronize(r.stop));
+        float t = 0;
+        TG_CUDA(cudaEventElapsedTime(&t, r.start, r.stop));
+        if (ms) ms[r.op] += t;
+        if (launches) launches[r.op] += 1;
+        if (bytes) bytes[r.op] += r.bytes;
+        ctx->prof_free.push_back(r.start);
+        ctx->prof_free.push_back(r.stop);
+    }
+    ctx->prof_recs.clear();
+    return TG_OK;
+}
+
+extern "C" const char* tg_profile_op_name(int op) {
+    static const char* names[TG_OP_COUNT] = {"ntt_fwd", "ntt_inv",  "addsub", "mul_pointwise", "mul_scalar",
+                                             "automorphism", "rescale", "tensor", "mul_plain", "modup_baseconv",
+                                             "key_inner", "mod_down", "reduce"};
+    return op >= 0 && op < TG_OP_COUNT ? names[op] : "?";
 }
 
 extern "C" int tg_stream_create(tg_context* ctx, void** stream) {

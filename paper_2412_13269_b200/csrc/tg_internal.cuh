@@ -162,6 +162,14 @@ struct GadgetDev {
 
 }  // namespace tg
 
+namespace tg {
+struct ProfRecord {
+    int op;
+    double bytes;
+    cudaEvent_t start, stop;
+};
+}  // namespace tg
+
 struct tg_context {
     int device = 0;
     tg::DevRing ring{};
@@ -169,7 +177,45 @@ struct tg_context {
     std::vector<tg::u64> h_ratio;
     void* dev_block = nullptr;  // one allocation for all tables
     cudaMemPool_t pool = nullptr;
+    // kernel timing (tg_profile_*)
+    bool prof_on = false;
+    std::vector<tg::ProfRecord> prof_recs;
+    std::vector<cudaEvent_t> prof_free;
 };
+
+namespace tg {
+// Brackets the launches of its scope with CUDA events when profiling is on.
+struct ProfScope {
+    tg_context* ctx;
+    ProfRecord rec{};
+    bool on;
+    ProfScope(tg_context* c, int op, double bytes, cudaStream_t s) : ctx(c), on(c && c->prof_on) {
+        if (!on) return;
+        rec.op = op;
+        rec.bytes = bytes;
+        rec.start = take_event();
+        rec.stop = take_event();
+        stream = s;
+        cudaEventRecord(rec.start, s);
+    }
+    ~ProfScope() {
+        if (!on) return;
+        cudaEventRecord(rec.stop, stream);
+        ctx->prof_recs.push_back(rec);
+    }
+    cudaEvent_t take_event() {
+        if (!ctx->prof_free.empty()) {
+            cudaEvent_t e = ctx->prof_free.back();
+            ctx->prof_free.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    cudaStream_t stream = nullptr;
+};
+}  // namespace tg
 
 struct tg_gadget {
     tg_context* ctx = nullptr;

@@ -141,13 +141,17 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s) {
     const DevRing& R = ctx->ring;
     const u32 nd = tg_gadget_digit_count(g, level);
     dim3 grid(std::max(1u, std::min(R.N / kThreads, 1024u)), nd);
-    k_modup<<<grid, kThreads, 0, s>>>(R, g->g, digits, d, level);
+    {
+        ProfScope prof(ctx, TG_OP_MODUP, 8.0 * R.N * (double(level + 1) + double(nd) * (level + 1 + R.K)), s);
+        k_modup<<<grid, kThreads, 0, s>>>(R, g->g, digits, d, level);
+    }
     TG_LAUNCH_CHECK();
     return ntt_forward_rows(ctx, digits, level, int(R.K), nd, s);
 }
 
 int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaStream_t s) {
     const DevRing& R = g->ctx->ring;
+    ProfScope prof(g->ctx, TG_OP_MOD_DOWN, 8.0 * R.N * npolys * (2.0 * (level + 1) + R.K), s);
     k_mod_down<<<grid_for(size_t(npolys) * R.N), kThreads, 0, s>>>(R, g->g, out, in, level, npolys);
     TG_LAUNCH_CHECK();
     return TG_OK;
@@ -159,7 +163,11 @@ int ks_inner(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd, cons
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const size_t words = size_t(level + 1 + R.K) * R.N;
+    {
+    // digits + both key halves read once, two accumulators written
+    ProfScope prof(ctx, TG_OP_KEY_INNER, 8.0 * words * (3.0 * nd + 2.0), s);
     k_key_inner<<<grid_for(words), kThreads, 0, s>>>(R, acc, acc + words, digits, nd, key, level);
+    }
     TG_LAUNCH_CHECK();
     if (int rc = ntt_inverse_rows(ctx, acc, level, int(R.K), 2, s)) return rc;
     if (out1 == out0 + size_t(level + 1) * R.N) return mod_down(g, out0, acc, level, 2, s);

@@ -193,6 +193,7 @@ int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     const u32 rpp = u32(level + 1 + nspecial);
     const u32 total = rpp * npolys;
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
+    ProfScope prof(ctx, TG_OP_NTT_FWD, 16.0 * total * R.N, s);
     for (u32 base = 0; base < total; base += 65535) {
         const u32 rows = std::min(65535u, total - base);
         dim3 g1((R.N >> p.logN1) >> p.logC, rows), g2((1u << p.logN1) >> p.logCpb, rows);
@@ -209,6 +210,7 @@ int ntt_inverse_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     const u32 rpp = u32(level + 1 + nspecial);
     const u32 total = rpp * npolys;
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
+    ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * total * R.N, s);
     for (u32 base = 0; base < total; base += 65535) {
         const u32 rows = std::min(65535u, total - base);
         dim3 g1((R.N >> p.logN1) >> p.logC, rows), g2((1u << p.logN1) >> p.logCpb, rows);

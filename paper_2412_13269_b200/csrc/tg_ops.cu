@@ -144,6 +144,14 @@ __global__ void k_mul_plain(DevRing R, u64* out, const u64* ct, const u64* plain
     }
 }
 
+// Post-NCCL fix-up: arbitrary word -> canonical residue of its row modulus.
+__global__ void k_reduce(DevRing R, Shape S, u64* data) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u32 m = row_mod(R, S, i);
+        data[i] = reduce64(data[i], R.q[m], R.ratio[2 * m], R.ratio[2 * m + 1]);
+    }
+}
+
 }  // namespace
 }  // namespace tg
 
@@ -164,6 +172,8 @@ static Shape shape_of(tg_context* ctx, int level, int nspecial, u32 npolys) {
     return S;
 }
 
+#define PROF(op, bytes) ProfScope prof_(ctx, op, double(bytes), as_stream(stream))
+
 extern "C" int tg_poly_addsub(tg_context* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int op, int level,
                               int nspecial, uint32_t npolys, void* stream) {
     if (int rc = check_shape(ctx, level, nspecial)) return rc;
@@ -171,6 +181,7 @@ extern "C" int tg_poly_addsub(tg_context* ctx, uint64_t* out, const uint64_t* a,
     if (npolys == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     Shape S = shape_of(ctx, level, nspecial, npolys);
+    PROF(TG_OP_ADDSUB, (op == 2 ? 16 : 24) * S.words);
     k_addsub<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, a, b, op);
     TG_LAUNCH_CHECK();
     return TG_OK;
@@ -182,6 +193,7 @@ extern "C" int tg_poly_mul(tg_context* ctx, uint64_t* out, const uint64_t* a, co
     if (npolys == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     Shape S = shape_of(ctx, level, nspecial, npolys);
+    PROF(TG_OP_MUL, 24 * S.words);
     k_mul<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, a, b, 0);
     TG_LAUNCH_CHECK();
     return TG_OK;
@@ -193,6 +205,7 @@ extern "C" int tg_poly_mul_acc(tg_context* ctx, uint64_t* out, const uint64_t* a
     if (npolys == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     Shape S = shape_of(ctx, level, nspecial, npolys);
+    PROF(TG_OP_MUL, 32 * S.words);
     k_mul<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, a, b, 1);
     TG_LAUNCH_CHECK();
     return TG_OK;
@@ -217,6 +230,7 @@ extern "C" int tg_poly_mul_scalar(tg_context* ctx, uint64_t* out, const uint64_t
     if (npolys == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     Shape S = shape_of(ctx, level, nspecial, npolys);
+    PROF(TG_OP_SCALAR, 16 * S.words);
     k_mul_scalar<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, a,
                                                                         make_scalars(ctx, scalar_per_modulus, true));
     TG_LAUNCH_CHECK();
@@ -230,6 +244,7 @@ extern "C" int tg_poly_add_scalar(tg_context* ctx, uint64_t* out, const uint64_t
     if (npolys == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     Shape S = shape_of(ctx, level, nspecial, npolys);
+    PROF(TG_OP_SCALAR, 16 * S.words);
     k_add_scalar<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(
         ctx->ring, S, out, a, make_scalars(ctx, add_per_modulus, false), form == TG_FORM_EVAL ? 1 : 0);
     TG_LAUNCH_CHECK();
@@ -246,6 +261,7 @@ extern "C" int tg_automorphism(tg_context* ctx, uint64_t* out, const uint64_t* i
     if (npolys == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     Shape S = shape_of(ctx, level, nspecial, npolys);
+    PROF(TG_OP_AUTOMORPHISM, 16 * S.words);
     if (form == TG_FORM_COEFF)
         k_auto_coeff<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, in, g);
     else
@@ -261,6 +277,7 @@ extern "C" int tg_rescale(tg_context* ctx, uint64_t* out, const uint64_t* in, in
     TG_REQUIRE(out != in, "[ring] rescale output must not alias its input");
     if (npolys == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
+    PROF(TG_OP_RESCALE, 8.0 * npolys * ctx->ring.N * (2 * level + 1));
     k_rescale<<<grid_for(size_t(npolys) * ctx->ring.N), kThreads, 0, as_stream(stream)>>>(ctx->ring, out, in, level,
                                                                                           npolys);
     TG_LAUNCH_CHECK();
@@ -274,6 +291,7 @@ extern "C" int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* 
     if (npolys == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     Shape S = shape_of(ctx, level, 0, npolys);
+    PROF(TG_OP_TENSOR, 56 * S.words);
     k_tensor<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, p0, p1, p2, x0, x1, y0, y1);
     TG_LAUNCH_CHECK();
     return TG_OK;
@@ -285,7 +303,20 @@ extern "C" int tg_mul_plain(tg_context* ctx, uint64_t* out, const uint64_t* ct_p
     if (nparts == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     size_t words = size_t(level + 1) * ctx->ring.N * nparts;
+    PROF(TG_OP_MUL_PLAIN, 16.0 * words + 8.0 * words / nparts);
     k_mul_plain<<<grid_for(words), kThreads, 0, as_stream(stream)>>>(ctx->ring, out, ct_part, plain, level, nparts);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_poly_reduce(tg_context* ctx, uint64_t* data, int level, int nspecial, uint32_t npolys,
+                              void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, nspecial, npolys);
+    PROF(TG_OP_REDUCE, 16 * S.words);
+    k_reduce<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, data);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
