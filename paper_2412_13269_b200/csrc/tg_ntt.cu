@@ -177,6 +177,8 @@ k_inv_cols(DevRing R, u64* __restrict__ data, u32 row_base, u32 rows_per_poly, i
         x[size_t(e >> logC) * N2 + (e & (C - 1))] = shoup(sm[e], ninv, ninv_s, q);
 }
 
+#include "tg_ntt_warp.cuh"
+
 }  // namespace
 
 int ntt_forward_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s) {
@@ -194,6 +196,17 @@ int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     const u32 total = rpp * npolys;
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
     ProfScope prof(ctx, TG_OP_NTT_FWD, 16.0 * total * R.N, s);
+    int e1 = 0, e2 = 0;
+    if (warp_plan(R.logN, e1, e2)) {
+        for (u32 base = 0; base < total; base += 65535) {
+            const u32 rows = std::min(65535u, total - base);
+            if (e1 == 8) launch_fwd_w<8, 8>(R, data, src, base, rows, rpp, level, s);
+            else if (e2 == 8) launch_fwd_w<4, 8>(R, data, src, base, rows, rpp, level, s);
+            else launch_fwd_w<4, 4>(R, data, src, base, rows, rpp, level, s);
+        }
+        TG_LAUNCH_CHECK();
+        return TG_OK;
+    }
     for (u32 base = 0; base < total; base += 65535) {
         const u32 rows = std::min(65535u, total - base);
         dim3 g1((R.N >> p.logN1) >> p.logC, rows), g2((1u << p.logN1) >> p.logCpb, rows);
@@ -211,6 +224,17 @@ int ntt_inverse_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     const u32 total = rpp * npolys;
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
     ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * total * R.N, s);
+    int e1 = 0, e2 = 0;
+    if (warp_plan(R.logN, e1, e2)) {
+        for (u32 base = 0; base < total; base += 65535) {
+            const u32 rows = std::min(65535u, total - base);
+            if (e1 == 8) launch_inv_w<8, 8>(R, data, src, base, rows, rpp, level, s);
+            else if (e2 == 8) launch_inv_w<4, 8>(R, data, src, base, rows, rpp, level, s);
+            else launch_inv_w<4, 4>(R, data, src, base, rows, rpp, level, s);
+        }
+        TG_LAUNCH_CHECK();
+        return TG_OK;
+    }
     for (u32 base = 0; base < total; base += 65535) {
         const u32 rows = std::min(65535u, total - base);
         dim3 g1((R.N >> p.logN1) >> p.logC, rows), g2((1u << p.logN1) >> p.logCpb, rows);

@@ -1,0 +1,357 @@
+// Warp-level NTT for N = 2^14 .. 2^16 (included by tg_ntt.cu, inside the
+// anonymous namespace).
+//
+// One warp owns one M-point sub-transform (M = 32*E, E = 4 or 8 residues per
+// lane). Radix-E stages run in registers; between stage blocks the warp
+// re-distributes its M residues through a private, padded shared-memory
+// column (__syncwarp only). A block is 8 warps = 8 columns (phase 1) or 8
+// consecutive chunks (phase 2). Every twiddle the block needs is staged in
+// shared memory at kernel start with coalesced loads that overlap the data
+// load, so no stage waits on an L2 round trip.
+//
+// Layout `lo`: lane l, register j hold element k = ins(l, j, lo), i.e. the
+// register index supplies bits [lo, lo+LOGE) of k.
+//
+// Twiddle index algebra (reference tables, ring.hpp:64-101):
+//   forward, phase-2 chunk r, local stage s: w[2^(logN1+s) + r*2^s + i]
+//   inverse, phase-A chunk r, u = LOGM-1-p:  winv[2^(logN1+u) + r*2^u + i]
+//   both column phases: table[2^u + i]  (u = stage, i = group)
+// so a block of 8 consecutive chunks needs, per u, one contiguous run of
+// 8*2^u entries starting at 2^(logN1+u) + 8*bx*2^u, and a column block needs
+// table[1 .. M1).
+
+template <int E>
+struct WGeo {
+    static constexpr int LOGE = E == 8 ? 3 : 2;
+    static constexpr int M = 32 * E;
+    static constexpr int LOGM = 5 + LOGE;
+    static constexpr int CS = M + M / 8 + 2;  // padded column stride (words)
+    static constexpr int TW_CHUNK = 8 * (M - 1);  // staged twiddles of 8 chunks
+    static constexpr int TW_COL = M;              // staged twiddles of a column block
+};
+
+__device__ __forceinline__ u32 wpad(u32 k) { return k + (k >> 3); }
+
+template <int LOGE>
+__device__ __forceinline__ u32 wins(u32 lane, u32 j, u32 lo) {
+    return ((lane >> lo) << (lo + LOGE)) | (j << lo) | (lane & ((1u << lo) - 1));
+}
+
+__device__ __forceinline__ void ct_bfly(u64& a, u64& b, u64 w, u64 ws, u64 q) {
+    const u64 q2 = 2 * q;
+    if (a >= q2) a -= q2;
+    const u64 t = shoup_lazy(b, w, ws, q);
+    b = a - t + q2;
+    a = a + t;
+}
+
+__device__ __forceinline__ void gs_bfly(u64& a, u64& b, u64 w, u64 ws, u64 q) {
+    const u64 q2 = 2 * q;
+    u64 s = a + b;
+    if (s >= q2) s -= q2;
+    const u64 d = a - b + q2;
+    b = shoup_lazy(d, w, ws, q);
+    a = s;
+}
+
+// Staged-twiddle index for group i of stage-unit u: CHUNK blocks use the
+// per-u runs (8 chunks, this warp's chunk c), column blocks the raw index.
+template <bool CHUNK>
+__device__ __forceinline__ u32 tw_slot(u32 u, u32 c, u32 i) {
+    if constexpr (CHUNK) return 8 * ((1u << u) - 1) + (c << u) + i;
+    else return (1u << u) + i;
+}
+
+// Forward (CT) stages on bits HI..LO (descending) of layout LAY; stage s = LOGM-1-p.
+template <int E, bool CHUNK, int LAY, int HI, int LO>
+__device__ __forceinline__ void wfwd(u64 (&v)[E], u32 lane, const u64* sw, const u64* sws, u64 q, u32 c) {
+    constexpr int LOGE = WGeo<E>::LOGE, LOGM = WGeo<E>::LOGM;
+#pragma unroll
+    for (int p = HI; p >= LO; --p) {
+        const int b = p - LAY;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            if (j & (1 << b)) continue;
+            const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
+            const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
+            ct_bfly(v[j], v[j | (1 << b)], sw[t], sws[t], q);
+        }
+    }
+}
+
+// Inverse (GS) stages on bits LO..HI (ascending) of layout LAY; unit u = LOGM-1-p.
+template <int E, bool CHUNK, int LAY, int LO, int HI>
+__device__ __forceinline__ void winv(u64 (&v)[E], u32 lane, const u64* sw, const u64* sws, u64 q, u32 c) {
+    constexpr int LOGE = WGeo<E>::LOGE, LOGM = WGeo<E>::LOGM;
+#pragma unroll
+    for (int p = LO; p <= HI; ++p) {
+        const int b = p - LAY;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            if (j & (1 << b)) continue;
+            const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
+            const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
+            gs_bfly(v[j], v[j | (1 << b)], sw[t], sws[t], q);
+        }
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void wxchg(u64 (&v)[E], u64* col, u32 lane, u32 lo_from, u32 lo_to) {
+    constexpr int LOGE = WGeo<E>::LOGE;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < E; ++j) col[wpad(wins<LOGE>(lane, u32(j), lo_from))] = v[j];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = col[wpad(wins<LOGE>(lane, u32(j), lo_to))];
+}
+
+// Full forward sub-transform: layout 5 (k = lane + 32 j) -> layout 0.
+template <int E, bool CHUNK>
+__device__ __forceinline__ void wfwd_all(u64 (&v)[E], u64* col, u32 lane, const u64* sw, const u64* sws, u64 q, u32 c) {
+    if constexpr (E == 8) {
+        wfwd<8, CHUNK, 5, 7, 5>(v, lane, sw, sws, q, c);
+        wxchg<8>(v, col, lane, 5, 2);
+        wfwd<8, CHUNK, 2, 4, 2>(v, lane, sw, sws, q, c);
+        wxchg<8>(v, col, lane, 2, 0);
+        wfwd<8, CHUNK, 0, 1, 0>(v, lane, sw, sws, q, c);
+    } else {
+        wfwd<4, CHUNK, 5, 6, 5>(v, lane, sw, sws, q, c);
+        wxchg<4>(v, col, lane, 5, 3);
+        wfwd<4, CHUNK, 3, 4, 3>(v, lane, sw, sws, q, c);
+        wxchg<4>(v, col, lane, 3, 1);
+        wfwd<4, CHUNK, 1, 2, 1>(v, lane, sw, sws, q, c);
+        wxchg<4>(v, col, lane, 1, 0);
+        wfwd<4, CHUNK, 0, 0, 0>(v, lane, sw, sws, q, c);
+    }
+}
+
+// Full inverse sub-transform: layout 0 -> layout 5.
+template <int E, bool CHUNK>
+__device__ __forceinline__ void winv_all(u64 (&v)[E], u64* col, u32 lane, const u64* sw, const u64* sws, u64 q, u32 c) {
+    if constexpr (E == 8) {
+        winv<8, CHUNK, 0, 0, 2>(v, lane, sw, sws, q, c);
+        wxchg<8>(v, col, lane, 0, 3);
+        winv<8, CHUNK, 3, 3, 5>(v, lane, sw, sws, q, c);
+        wxchg<8>(v, col, lane, 3, 5);
+        winv<8, CHUNK, 5, 6, 7>(v, lane, sw, sws, q, c);
+    } else {
+        winv<4, CHUNK, 0, 0, 1>(v, lane, sw, sws, q, c);
+        wxchg<4>(v, col, lane, 0, 2);
+        winv<4, CHUNK, 2, 2, 3>(v, lane, sw, sws, q, c);
+        wxchg<4>(v, col, lane, 2, 4);
+        winv<4, CHUNK, 4, 4, 5>(v, lane, sw, sws, q, c);
+        wxchg<4>(v, col, lane, 4, 5);
+        winv<4, CHUNK, 5, 6, 6>(v, lane, sw, sws, q, c);
+    }
+}
+
+// Stage the 8-chunk twiddle runs of block bx: for u < LOGM,
+// sw[8(2^u-1) + t] = tab[2^(logN1+u) + 8 bx 2^u + t], t < 8*2^u.
+template <int E>
+__device__ __forceinline__ void stage_chunk_twiddles(u64* sw, u64* sws, const u64* __restrict__ w,
+                                                     const u64* __restrict__ ws, u32 logN1, u32 bx) {
+    constexpr int LOGM = WGeo<E>::LOGM;
+#pragma unroll
+    for (int u = 0; u < LOGM; ++u) {
+        const u32 n = 8u << u, dst = 8 * ((1u << u) - 1), src = (1u << (logN1 + u)) + ((8 * bx) << u);
+        for (u32 t = threadIdx.x; t < n; t += 256) {
+            sw[dst + t] = __ldg(w + src + t);
+            sws[dst + t] = __ldg(ws + src + t);
+        }
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void stage_col_twiddles(u64* sw, u64* sws, const u64* __restrict__ w,
+                                                   const u64* __restrict__ ws) {
+    for (u32 t = threadIdx.x; t < u32(WGeo<E>::M); t += 256) {
+        sw[t] = __ldg(w + t);
+        sws[t] = __ldg(ws + t);
+    }
+}
+
+template <int E>
+constexpr size_t col_smem() {
+    return size_t(8) * (8 * WGeo<E>::CS + 2 * WGeo<E>::TW_COL);
+}
+template <int E>
+constexpr size_t chunk_smem() {
+    return size_t(8) * (8 * WGeo<E>::CS + 2 * WGeo<E>::TW_CHUNK);
+}
+
+// Phase 1 forward: 8 columns x M1 rows, stages 0 .. log M1 - 1.
+template <int E>
+__global__ void __launch_bounds__(256)
+kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int level) {
+    using Gm = WGeo<E>;
+    extern __shared__ u64 dyn[];
+    u64* sm = dyn;
+    u64* sw = dyn + 8 * Gm::CS;
+    u64* sws = sw + Gm::TW_COL;
+    const u32 N = R.N, N2 = N >> Gm::LOGM;
+    const u32 row = row_base + blockIdx.y;
+    const u32 mi = mod_index(row % rpp, level, R.q_count);
+    const u64 q = R.q[mi];
+    const u64* w = R.tw + size_t(mi) * 4 * N;
+    const u32 c0 = blockIdx.x * 8;
+    const u64* xs = src + size_t(row) * N + c0;
+    u64* xd = data + size_t(row) * N + c0;
+    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
+        sm[(e & 7) * Gm::CS + wpad(e >> 3)] = xs[size_t(e >> 3) * N2 + (e & 7)];
+    stage_col_twiddles<E>(sw, sws, w, w + N);
+    __syncthreads();
+    const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    u64* col = sm + warp * Gm::CS;
+    u64 v[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = col[wpad(lane + 32 * j)];
+    wfwd_all<E, false>(v, col, lane, sw, sws, q, 0);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < E; ++j) col[wpad((lane << Gm::LOGE) | j)] = v[j];
+    __syncthreads();
+    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
+        xd[size_t(e >> 3) * N2 + (e & 7)] = sm[(e & 7) * Gm::CS + wpad(e >> 3)];
+}
+
+// Phase 2 forward: one warp per contiguous chunk of M2, final canonical reduce.
+template <int E>
+__global__ void __launch_bounds__(256)
+kw_fwd_chunks(DevRing R, u64* data, u32 row_base, u32 rpp, int level, u32 logN1) {
+    using Gm = WGeo<E>;
+    extern __shared__ u64 dyn[];
+    u64* sm = dyn;
+    u64* sw = dyn + 8 * Gm::CS;
+    u64* sws = sw + Gm::TW_CHUNK;
+    const u32 N = R.N;
+    const u32 row = row_base + blockIdx.y;
+    const u32 mi = mod_index(row % rpp, level, R.q_count);
+    const u64 q = R.q[mi];
+    const u64* w = R.tw + size_t(mi) * 4 * N;
+    const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const u32 chunk = blockIdx.x * 8 + warp;
+    u64* x = data + size_t(row) * N + size_t(chunk) * Gm::M;
+    u64 v[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = x[lane + 32 * j];
+    stage_chunk_twiddles<E>(sw, sws, w, w + N, logN1, blockIdx.x);
+    __syncthreads();
+    wfwd_all<E, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+    const u64 q2 = 2 * q;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        u64 t = v[j];
+        if (t >= q2) t -= q2;
+        if (t >= q) t -= q;
+        v[j] = t;
+    }
+    ulonglong2* x2 = reinterpret_cast<ulonglong2*>(x + (lane << Gm::LOGE));
+#pragma unroll
+    for (int j = 0; j < E / 2; ++j) x2[j] = make_ulonglong2(v[2 * j], v[2 * j + 1]);
+}
+
+// Phase A inverse: one warp per contiguous chunk (stages t = 1 .. M2/2).
+template <int E>
+__global__ void __launch_bounds__(256)
+kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int level, u32 logN1) {
+    using Gm = WGeo<E>;
+    extern __shared__ u64 dyn[];
+    u64* sm = dyn;
+    u64* sw = dyn + 8 * Gm::CS;
+    u64* sws = sw + Gm::TW_CHUNK;
+    const u32 N = R.N;
+    const u32 row = row_base + blockIdx.y;
+    const u32 mi = mod_index(row % rpp, level, R.q_count);
+    const u64 q = R.q[mi];
+    const u64* w = R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
+    const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const u32 chunk = blockIdx.x * 8 + warp;
+    const ulonglong2* xs2 =
+        reinterpret_cast<const ulonglong2*>(src + size_t(row) * N + size_t(chunk) * Gm::M + (lane << Gm::LOGE));
+    u64* x = data + size_t(row) * N + size_t(chunk) * Gm::M;
+    u64 v[E];
+#pragma unroll
+    for (int j = 0; j < E / 2; ++j) {
+        const ulonglong2 t = xs2[j];
+        v[2 * j] = t.x;
+        v[2 * j + 1] = t.y;
+    }
+    stage_chunk_twiddles<E>(sw, sws, w, w + N, logN1, blockIdx.x);
+    __syncthreads();
+    winv_all<E, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+#pragma unroll
+    for (int j = 0; j < E; ++j) x[lane + 32 * j] = v[j];
+}
+
+// Phase B inverse: 8 columns x M1 rows, then the N^-1 scaling.
+template <int E>
+__global__ void __launch_bounds__(256)
+kw_inv_cols(DevRing R, u64* data, u32 row_base, u32 rpp, int level) {
+    using Gm = WGeo<E>;
+    extern __shared__ u64 dyn[];
+    u64* sm = dyn;
+    u64* sw = dyn + 8 * Gm::CS;
+    u64* sws = sw + Gm::TW_COL;
+    const u32 N = R.N, N2 = N >> Gm::LOGM;
+    const u32 row = row_base + blockIdx.y;
+    const u32 mi = mod_index(row % rpp, level, R.q_count);
+    const u64 q = R.q[mi];
+    const u64* w = R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
+    const u64 ninv = R.ninv[2 * mi], ninv_s = R.ninv[2 * mi + 1];
+    u64* x = data + size_t(row) * N + blockIdx.x * 8;
+    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
+        sm[(e & 7) * Gm::CS + wpad(e >> 3)] = x[size_t(e >> 3) * N2 + (e & 7)];
+    stage_col_twiddles<E>(sw, sws, w, w + N);
+    __syncthreads();
+    const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    u64* col = sm + warp * Gm::CS;
+    u64 v[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = col[wpad((lane << Gm::LOGE) | j)];
+    winv_all<E, false>(v, col, lane, sw, sws, q, 0);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = shoup(v[j], ninv, ninv_s, q);
+    __syncthreads();
+    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
+        x[size_t(e >> 3) * N2 + (e & 7)] = sm[(e & 7) * Gm::CS + wpad(e >> 3)];
+}
+
+// (E1, E2) for N = M1 * M2 handled by the warp kernels.
+inline bool warp_plan(u32 logN, int& e1, int& e2) {
+    switch (logN) {
+        case 16: e1 = 8; e2 = 8; return true;
+        case 15: e1 = 4; e2 = 8; return true;
+        case 14: e1 = 4; e2 = 4; return true;
+        default: return false;
+    }
+}
+
+template <int E1, int E2>
+void set_smem_attrs() {
+    static bool done = false;  // per device is enough for this process model
+    if (done) return;
+    cudaFuncSetAttribute(kw_fwd_cols<E1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
+    cudaFuncSetAttribute(kw_inv_cols<E1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
+    cudaFuncSetAttribute(kw_fwd_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
+    cudaFuncSetAttribute(kw_inv_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
+    done = true;
+}
+
+template <int E1, int E2>
+void launch_fwd_w(const DevRing& R, u64* data, const u64* src, u32 base, u32 rows, u32 rpp, int level, cudaStream_t s) {
+    set_smem_attrs<E1, E2>();
+    const u32 M1 = 32 * E1, M2 = 32 * E2;
+    kw_fwd_cols<E1><<<dim3(M2 / 8, rows), 256, col_smem<E1>(), s>>>(R, data, src, base, rpp, level);
+    kw_fwd_chunks<E2><<<dim3(M1 / 8, rows), 256, chunk_smem<E2>(), s>>>(R, data, base, rpp, level, WGeo<E1>::LOGM);
+}
+
+template <int E1, int E2>
+void launch_inv_w(const DevRing& R, u64* data, const u64* src, u32 base, u32 rows, u32 rpp, int level, cudaStream_t s) {
+    set_smem_attrs<E1, E2>();
+    const u32 M1 = 32 * E1, M2 = 32 * E2;
+    kw_inv_chunks<E2><<<dim3(M1 / 8, rows), 256, chunk_smem<E2>(), s>>>(R, data, src, base, rpp, level, WGeo<E1>::LOGM);
+    kw_inv_cols<E1><<<dim3(M2 / 8, rows), 256, col_smem<E1>(), s>>>(R, data, base, rpp, level);
+}

@@ -1,0 +1,87 @@
+#!/usr/bin/env python3
+"""Kernel microbenchmarks through the C-ABI-backed module (device time via
+CUDA events on the ring's stream). Used for ncu captures and roofline
+iteration on single ops: NTT fwd/inv, tensor, ModUp, key inner product,
+ModDown, rescale at config-3 shapes.
+
+  python tools/kbench.py [--rows 21] [--reps 50] [--ops ntt,modup,...]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    import torch
+
+    from paper_2412_13269_b200 import tetris as G
+    from paper_2412_13269_b200 import workloads as W
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--levels", default="20,10")
+    ap.add_argument("--batch", type=int, default=1, help="polys per NTT launch")
+    ap.add_argument("--ops", default="ntt,intt,relin,rescale")
+    a = ap.parse_args()
+    spec = W.CONFIGS[3]
+    S = W.make_context(G, spec)
+    ring = S.ring
+    ext = torch.cuda.ExternalStream(ring.stream_handle())
+    res = {}
+
+    def timeit(name, fn, nbytes=None):
+        for _ in range(3):
+            fn()
+        ring.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        for _ in range(a.reps):
+            fn()
+        e1.record(ext)
+        ring.synchronize()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.reps
+        res[name] = {"us": round(ms * 1e3, 2)}
+        if nbytes:
+            res[name]["GBps"] = round(nbytes / (ms / 1e3) / 1e9, 1)
+        print(name, res[name], flush=True)
+
+    G.profile_enable(ring, False)
+    for lvl in (int(x) for x in a.levels.split(",")):
+        K = spec.K
+        rows = lvl + 1 + K
+        p = G.sample_uniform(ring, lvl, K, G.Rng(1))
+        pe = G.ntt_transform(p, G.Form.eval)
+        if "ntt" in a.ops:
+            timeit(f"ntt_fwd_l{lvl}_rows{rows}", lambda: G.ntt_transform(p, G.Form.eval), 16 * rows * spec.N)
+        if "intt" in a.ops:
+            timeit(f"ntt_inv_l{lvl}_rows{rows}", lambda: G.ntt_transform(pe, G.Form.coeff), 16 * rows * spec.N)
+        rng = G.Rng(2)
+        x = G.Ciphertext()
+        x.parts = [G.sample_uniform(ring, lvl, 0, rng.split(i)) for i in range(2)]
+        x.scale, x.domain, x.sk_id = spec.delta, G.Domain.slots, S.sk.id()
+        if "relin" in a.ops:
+            timeit(f"mul_relin_l{lvl}", lambda: S.ev.mul_relin(x, x, S.keys))
+        if "rescale" in a.ops:
+            timeit(f"rescale_l{lvl}", lambda: S.ev.rescale(x), 8 * spec.N * 2 * (2 * lvl + 1))
+        if "prof" in a.ops:
+            G.profile_enable(ring, True)
+            for _ in range(5):
+                S.ev.mul_relin(x, x, S.keys)
+            ring.synchronize()
+            pr = G.profile_read(ring)
+            G.profile_enable(ring, False)
+            for k, v in sorted(pr.items(), key=lambda kv: -kv[1][0]):
+                print(f"  relin l{lvl} {k}: {v[0] / 5 * 1e3:.1f} us/call-set, launches {v[1] // 5}, "
+                      f"{v[2] / v[1] / (v[0] / v[1] / 1e3) / 1e9:.0f} GB/s", flush=True)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
