@@ -171,9 +171,12 @@ def run_b200(args):
     flush = torch.empty(64 << 22, dtype=torch.int32, device="cuda")  # 1 GiB > 126 MB L2
 
     def query(local_cts, t_ct):
+        # per-ciphertext thresholds run concurrently (one host thread + CUDA
+        # stream each); outputs are summed in index order on the main stream
         acc = None
-        for c in local_cts:
-            o = G.eval_private_threshold_plain_norm(S.ev, c, t_ct, spec.norm, chain, S.keys)
+        outs = G.eval_private_threshold_plain_norm_many(S.ev, local_cts, t_ct, spec.norm, chain, S.keys,
+                                                        args.streams) if local_cts else []
+        for o in outs:
             acc = o if acc is None else S.ev.add(acc, o)
         if acc is None:  # rank without ciphertexts contributes zero
             acc = S.ctx.zero_ciphertext(t_ct.level() - chain.levels_required(), 1.0, S.sk.id(), G.Domain.slots)
@@ -414,6 +417,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=4, help="concurrent ciphertext pipelines per GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     if args.impl == "reference":

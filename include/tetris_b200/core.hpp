@@ -117,10 +117,30 @@ struct NttTables {
 struct DeviceState {
     tg_context* ctx = nullptr;
     void* stream = nullptr;
+    std::mutex mu;
+    std::vector<void*> workers;  // extra streams for concurrent pipelines
     DeviceState() = default;
     DeviceState(const DeviceState&) = delete;
     DeviceState& operator=(const DeviceState&) = delete;
     ~DeviceState();
+    void* worker_stream(std::size_t i);
+};
+
+// Routes every device call the current host thread makes on `ring` to
+// `stream` for the scope's lifetime (one stream per host thread when
+// independent ciphertexts run concurrently, the reference's thread-pool
+// granularity, protocol.hpp:297-311).
+class RingParams;
+class StreamScope {
+public:
+    StreamScope(const RingParams& ring, void* stream);
+    ~StreamScope();
+    StreamScope(const StreamScope&) = delete;
+    StreamScope& operator=(const StreamScope&) = delete;
+
+private:
+    const void* prev_state_;
+    void* prev_stream_;
 };
 
 // Per-process default CUDA device for new contexts (torchrun: LOCAL_RANK).
@@ -183,6 +203,7 @@ public:
 
 private:
     std::shared_ptr<DeviceState> dev_;
+    void* stream_ = nullptr;  // allocation stream; the buffer is freed there
     u64* ptr_ = nullptr;
     std::size_t words_ = 0;
 };

@@ -128,4 +128,14 @@ Ciphertext eval_private_threshold(const Evaluator& ev, const Ciphertext& ct_scor
 Ciphertext eval_private_threshold_plain_norm(const Evaluator& ev, const Ciphertext& ct_scores, const Ciphertext& ct_t,
                                              double norm, const MinimaxChain& chain, const EvalKeys& keys);
 
+// Independent ciphertexts through eval_private_threshold_plain_norm
+// concurrently: one host thread + one CUDA stream per ciphertext (up to
+// max_streams), the reference's per-ciphertext thread pool
+// (protocol.hpp:297-311). Each output is bit-identical to the single call.
+std::vector<Ciphertext> eval_private_threshold_plain_norm_many(const Evaluator& ev,
+                                                               const std::vector<Ciphertext>& scores,
+                                                               const Ciphertext& ct_t, double norm,
+                                                               const MinimaxChain& chain, const EvalKeys& keys,
+                                                               int max_streams = 8);
+
 }  // namespace tetris_b200

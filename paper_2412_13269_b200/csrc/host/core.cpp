@@ -210,10 +210,40 @@ double RingParams::total_log2_q(int level) const {
 
 DeviceState::~DeviceState() {
     if (ctx) {
+        for (void* s : workers) {
+            tg_stream_sync(ctx, s);
+            tg_stream_destroy(ctx, s);
+        }
         tg_stream_sync(ctx, stream);
         tg_stream_destroy(ctx, stream);
         tg_context_destroy(ctx);
     }
+}
+
+void* DeviceState::worker_stream(std::size_t i) {
+    std::lock_guard<std::mutex> g(mu);
+    while (workers.size() <= i) {
+        void* s = nullptr;
+        check_tg(tg_stream_create(ctx, &s));
+        workers.push_back(s);
+    }
+    return workers[i];
+}
+
+namespace {
+thread_local const void* t_override_state = nullptr;
+thread_local void* t_override_stream = nullptr;
+}  // namespace
+
+StreamScope::StreamScope(const RingParams& ring, void* stream)
+    : prev_state_(t_override_state), prev_stream_(t_override_stream) {
+    t_override_state = ring.device_state().get();
+    t_override_stream = stream;
+}
+
+StreamScope::~StreamScope() {
+    t_override_state = prev_state_;
+    t_override_stream = prev_stream_;
 }
 
 const std::shared_ptr<DeviceState>& RingParams::device_state() const {
@@ -243,7 +273,10 @@ const std::shared_ptr<DeviceState>& RingParams::device_state() const {
 
 tg_context* RingParams::dev() const { return device_state()->ctx; }
 
-void* RingParams::stream() const { return device_state()->stream; }
+void* RingParams::stream() const {
+    const auto& st = device_state();
+    return t_override_state == st.get() ? t_override_stream : st->stream;
+}
 
 void RingParams::synchronize() const { check_tg(tg_stream_sync(dev(), stream())); }
 
@@ -252,14 +285,20 @@ RingParams::~RingParams() = default;
 // ---------------------------------------------------------------------------
 // Device storage and Poly
 // ---------------------------------------------------------------------------
-DeviceBuffer::DeviceBuffer(const RingParams& ring, std::size_t words) : dev_(ring.device_state()), words_(words) {
+DeviceBuffer::DeviceBuffer(const RingParams& ring, std::size_t words)
+    : dev_(ring.device_state()), stream_(ring.stream()), words_(words) {
     void* p = nullptr;
-    check_tg(tg_alloc(dev_->ctx, &p, words * 8, dev_->stream));
+    check_tg(tg_alloc(dev_->ctx, &p, words * 8, stream_));
     ptr_ = static_cast<u64*>(p);
 }
 
+// Freed on the destroying thread's current stream: ordered after that
+// thread's uses; buffers crossing threads are handed over only after the
+// producing stream was synchronized (see eval_private_threshold_many).
 DeviceBuffer::~DeviceBuffer() {
-    if (ptr_) tg_free(dev_->ctx, ptr_, dev_->stream);
+    if (!ptr_) return;
+    void* s = t_override_state == dev_.get() ? t_override_stream : dev_->stream;
+    tg_free(dev_->ctx, ptr_, s);
 }
 
 Poly::Poly(const RingParams& ring, int level, Form form, int nspecial)

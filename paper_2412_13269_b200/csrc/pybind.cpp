@@ -349,20 +349,24 @@ PYBIND11_MODULE(_tetris_b200, m) {
     // per-ciphertext threshold, sum mod q in index order, one inner_sum
     // (the reference order, protocol.hpp:319-323). Returns (ct, seconds),
     // seconds measured after a device synchronize.
+    m.def("eval_private_threshold_plain_norm_many", &eval_private_threshold_plain_norm_many,
+          py::call_guard<py::gil_scoped_release>(), py::arg("ev"), py::arg("scores"), py::arg("ct_t"),
+          py::arg("norm"), py::arg("chain"), py::arg("keys"), py::arg("max_streams") = 8);
     m.def(
         "threshold_count",
         [](const Evaluator& ev, const std::vector<Ciphertext>& scores, const Ciphertext& ct_t, double norm,
-           const MinimaxChain& chain, const EvalKeys& keys, u32 slots, bool do_inner_sum) {
+           const MinimaxChain& chain, const EvalKeys& keys, u32 slots, bool do_inner_sum, int streams) {
             py::gil_scoped_release nogil;
             auto t0 = std::chrono::steady_clock::now();
             Ciphertext acc;
-            for (std::size_t i = 0; i < scores.size(); ++i) {
-                Ciphertext o = eval_private_threshold_plain_norm(ev, scores[i], ct_t, norm, chain, keys);
-                acc = i == 0 ? o : ev.add(acc, o);
-            }
+            std::vector<Ciphertext> outs =
+                eval_private_threshold_plain_norm_many(ev, scores, ct_t, norm, chain, keys, streams);
+            for (std::size_t i = 0; i < outs.size(); ++i) acc = i == 0 ? outs[i] : ev.add(acc, outs[i]);
             if (do_inner_sum) acc = inner_sum(ev, acc, slots, keys);
             ev.ring().synchronize();
             double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             return std::make_pair(acc, s);
-        });
+        },
+        py::arg("ev"), py::arg("scores"), py::arg("ct_t"), py::arg("norm"), py::arg("chain"), py::arg("keys"),
+        py::arg("slots"), py::arg("do_inner_sum") = true, py::arg("streams") = 8);
 }

@@ -207,6 +207,7 @@ extern "C" int tg_profile_enable(tg_context* ctx, int on) {
 extern "C" int tg_profile_read(tg_context* ctx, double* ms, uint64_t* launches, double* bytes) {
     if (!ctx) return fail(TG_E_ARG, "[gpu] null context");
     DeviceGuard guard(ctx->device);
+    std::lock_guard<std::mutex> lock(ctx->prof_mu);
     for (int i = 0; i < TG_OP_COUNT; ++i) {
         if (ms) ms[i] = 0;
         if (launches) launches[i] = 0;

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "tetris_b200.h"
@@ -177,7 +178,8 @@ struct tg_context {
     std::vector<tg::u64> h_ratio;
     void* dev_block = nullptr;  // one allocation for all tables
     cudaMemPool_t pool = nullptr;
-    // kernel timing (tg_profile_*)
+    // kernel timing (tg_profile_*); launches may come from several host threads
+    std::mutex prof_mu;
     bool prof_on = false;
     std::vector<tg::ProfRecord> prof_recs;
     std::vector<cudaEvent_t> prof_free;
@@ -193,14 +195,18 @@ struct ProfScope {
         if (!on) return;
         rec.op = op;
         rec.bytes = bytes;
-        rec.start = take_event();
-        rec.stop = take_event();
+        {
+            std::lock_guard<std::mutex> g(ctx->prof_mu);
+            rec.start = take_event();
+            rec.stop = take_event();
+        }
         stream = s;
         cudaEventRecord(rec.start, s);
     }
     ~ProfScope() {
         if (!on) return;
         cudaEventRecord(rec.stop, stream);
+        std::lock_guard<std::mutex> g(ctx->prof_mu);
         ctx->prof_recs.push_back(rec);
     }
     cudaEvent_t take_event() {

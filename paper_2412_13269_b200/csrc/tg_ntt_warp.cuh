@@ -20,6 +20,10 @@
 // 8*2^u entries starting at 2^(logN1+u) + 8*bx*2^u, and a column block needs
 // table[1 .. M1).
 
+#ifndef NTT_MIN_BLOCKS
+#define NTT_MIN_BLOCKS 6
+#endif
+
 template <int E>
 struct WGeo {
     static constexpr int LOGE = E == 8 ? 3 : 2;
@@ -74,7 +78,8 @@ __device__ __forceinline__ void wfwd(u64 (&v)[E], u32 lane, const u64* sw, const
             if (j & (1 << b)) continue;
             const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
             const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
-            ct_bfly(v[j], v[j | (1 << b)], sw[t], sws[t], q);
+            const ulonglong2 tw = reinterpret_cast<const ulonglong2*>(sw)[t];
+            ct_bfly(v[j], v[j | (1 << b)], tw.x, tw.y, q);
         }
     }
 }
@@ -91,7 +96,8 @@ __device__ __forceinline__ void winv(u64 (&v)[E], u32 lane, const u64* sw, const
             if (j & (1 << b)) continue;
             const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
             const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
-            gs_bfly(v[j], v[j | (1 << b)], sw[t], sws[t], q);
+            const ulonglong2 tw = reinterpret_cast<const ulonglong2*>(sw)[t];
+            gs_bfly(v[j], v[j | (1 << b)], tw.x, tw.y, q);
         }
     }
 }
@@ -156,20 +162,16 @@ __device__ __forceinline__ void stage_chunk_twiddles(u64* sw, u64* sws, const u6
 #pragma unroll
     for (int u = 0; u < LOGM; ++u) {
         const u32 n = 8u << u, dst = 8 * ((1u << u) - 1), src = (1u << (logN1 + u)) + ((8 * bx) << u);
-        for (u32 t = threadIdx.x; t < n; t += 256) {
-            sw[dst + t] = __ldg(w + src + t);
-            sws[dst + t] = __ldg(ws + src + t);
-        }
+        for (u32 t = threadIdx.x; t < n; t += 256)
+            reinterpret_cast<ulonglong2*>(sw)[dst + t] = make_ulonglong2(__ldg(w + src + t), __ldg(ws + src + t));
     }
 }
 
 template <int E>
 __device__ __forceinline__ void stage_col_twiddles(u64* sw, u64* sws, const u64* __restrict__ w,
                                                    const u64* __restrict__ ws) {
-    for (u32 t = threadIdx.x; t < u32(WGeo<E>::M); t += 256) {
-        sw[t] = __ldg(w + t);
-        sws[t] = __ldg(ws + t);
-    }
+    for (u32 t = threadIdx.x; t < u32(WGeo<E>::M); t += 256)
+        reinterpret_cast<ulonglong2*>(sw)[t] = make_ulonglong2(__ldg(w + t), __ldg(ws + t));
 }
 
 template <int E>
@@ -183,7 +185,7 @@ constexpr size_t chunk_smem() {
 
 // Phase 1 forward: 8 columns x M1 rows, stages 0 .. log M1 - 1.
 template <int E>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
 kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int level) {
     using Gm = WGeo<E>;
     extern __shared__ u64 dyn[];
@@ -218,7 +220,7 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int lev
 
 // Phase 2 forward: one warp per contiguous chunk of M2, final canonical reduce.
 template <int E>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
 kw_fwd_chunks(DevRing R, u64* data, u32 row_base, u32 rpp, int level, u32 logN1) {
     using Gm = WGeo<E>;
     extern __shared__ u64 dyn[];
@@ -254,7 +256,7 @@ kw_fwd_chunks(DevRing R, u64* data, u32 row_base, u32 rpp, int level, u32 logN1)
 
 // Phase A inverse: one warp per contiguous chunk (stages t = 1 .. M2/2).
 template <int E>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
 kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int level, u32 logN1) {
     using Gm = WGeo<E>;
     extern __shared__ u64 dyn[];
@@ -287,7 +289,7 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int l
 
 // Phase B inverse: 8 columns x M1 rows, then the N^-1 scaling.
 template <int E>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
 kw_inv_cols(DevRing R, u64* data, u32 row_base, u32 rpp, int level) {
     using Gm = WGeo<E>;
     extern __shared__ u64 dyn[];
@@ -331,13 +333,15 @@ inline bool warp_plan(u32 logN, int& e1, int& e2) {
 
 template <int E1, int E2>
 void set_smem_attrs() {
-    static bool done = false;  // per device is enough for this process model
-    if (done) return;
-    cudaFuncSetAttribute(kw_fwd_cols<E1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
-    cudaFuncSetAttribute(kw_inv_cols<E1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
-    cudaFuncSetAttribute(kw_fwd_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
-    cudaFuncSetAttribute(kw_inv_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
-    done = true;
+    // thread-safe one-time init (one process drives one device)
+    static const bool done = [] {
+        cudaFuncSetAttribute(kw_fwd_cols<E1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
+        cudaFuncSetAttribute(kw_inv_cols<E1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
+        cudaFuncSetAttribute(kw_fwd_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
+        cudaFuncSetAttribute(kw_inv_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
+        return true;
+    }();
+    (void)done;
 }
 
 template <int E1, int E2>
