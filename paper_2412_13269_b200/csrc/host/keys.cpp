@@ -374,26 +374,23 @@ SwitchingKey KeyContext::relin_key_gen(const SecretKey& sk, Rng& rng) const {
     return switch_key_gen(s2, sk, rng);
 }
 
-// relinearize (rlwe.hpp:601-620): c2 -> coeff, KS(c2), (c0+d0, c1+d1) in coeff form.
+// relinearize (rlwe.hpp:601-620): c2 -> coeff, KS(c2), (c0+d0, c1+d1) in
+// coeff form; the final adds are fused into ModDown (tg_keyswitch_add).
 Ciphertext KeyContext::relinearize(const Ciphertext& ct, const SwitchingKey& rlk) const {
     if (ct.degree() != 2) throw TetrisError("rlwe", "relinearize expects a degree-2 ciphertext");
     if (rlk.to_id != ct.sk_id) throw TetrisError("rlwe", "relinearization key mismatch");
     Ciphertext src = ct;
     src.to_coeff();  // one batched iNTT when the three parts share a block
-    auto [d0, d1] = switch_key_apply(src.parts[2], rlk);
-    Ciphertext out;
-    out.parts = {src.parts[0], src.parts[1]};
-    std::vector<Poly> d = {d0, d1};
     const int lvl = ct.level();
-    if (contiguous(out.parts, 0, 2) && contiguous(d, 0, 2)) {
-        std::vector<Poly> dst = fresh_parts(*ring_, 2, lvl, Form::coeff);
-        check_tg(tg_poly_addsub(ring_->dev(), const_cast<u64*>(dst[0].data()), out.parts[0].data(), d0.data(), 0, lvl,
-                                0, 2, ring_->stream()));
-        out.parts = std::move(dst);
-    } else {
-        out.parts[0].add_inplace(d0);
-        out.parts[1].add_inplace(d1);
-    }
+    const Poly& c2 = src.parts[2];
+    if (c2.form() != Form::coeff || c2.nspecial() != 0)
+        throw TetrisError("rlwe", "decompose expects coeff form without special rows");
+    std::vector<Poly> dst = fresh_parts(*ring_, 2, lvl, Form::coeff);
+    check_tg(tg_keyswitch_add(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[1].data()),
+                              c2.data(), key_base(rlk), rlk.digits(), lvl, src.parts[0].data(), src.parts[1].data(),
+                              ring_->stream()));
+    Ciphertext out;
+    out.parts = std::move(dst);
     out.scale = ct.scale;
     out.domain = ct.domain;
     out.sk_id = ct.sk_id;
@@ -434,12 +431,12 @@ Ciphertext KeyContext::apply_galois(const Ciphertext& ct, u64 exponent, const Sw
             check_tg(tg_automorphism(ring_->dev(), const_cast<u64*>(rot[i].data()), src.parts[i].data(), g,
                                      TG_FORM_COEFF, lvl, 0, 1, ring_->stream()));
     }
-    auto [d0, d1] = switch_key_apply(rot[1], swk);
+    // (phi(c0) + d0, d1): the add fused into ModDown
     Ciphertext out;
     std::vector<Poly> dst = fresh_parts(*ring_, 2, lvl, Form::coeff);
-    check_tg(tg_poly_addsub(ring_->dev(), const_cast<u64*>(dst[0].data()), rot[0].data(), d0.data(), 0, lvl, 0, 1,
-                            ring_->stream()));
-    check_tg(tg_memcpy_d2d(ring_->dev(), const_cast<u64*>(dst[1].data()), d1.data(), d1.words() * 8, ring_->stream()));
+    check_tg(tg_keyswitch_add(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[1].data()),
+                              rot[1].data(), key_base(swk), swk.digits(), lvl, rot[0].data(), nullptr,
+                              ring_->stream()));
     out.parts = std::move(dst);
     out.scale = ct.scale;
     out.domain = ct.domain;

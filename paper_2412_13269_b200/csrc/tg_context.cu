@@ -92,7 +92,7 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
 
     // one device block: q | ratio | tw | ninv | rs | eval_exp | slot_of_exp
     size_t n_q = nmod, n_ratio = 2 * nmod, n_tw = size_t(4) * nmod * degree, n_ninv = 2 * nmod, n_rs = rs.size();
-    size_t words = n_q + n_ratio + n_tw + n_ninv + n_rs;
+    size_t words = n_q + n_ratio + n_tw + n_ninv + n_rs + nmod;  // + one_shoup
     size_t bytes = words * 8 + size_t(3) * degree * 4;
     cudaError_t e = cudaMalloc(&ctx->dev_block, bytes);
     if (e != cudaSuccess) {
@@ -105,6 +105,7 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
     R.tw = p + n_q + n_ratio;
     R.ninv = p + n_q + n_ratio + n_tw;
     R.rs = p + n_q + n_ratio + n_tw + n_ninv;
+    R.one_shoup = p + n_q + n_ratio + n_tw + n_ninv + n_rs;
     u32* p32 = reinterpret_cast<u32*>(p + words);
     R.eval_exp = p32;
     R.slot_of_exp = p32 + degree;
@@ -114,6 +115,7 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
     std::memcpy(host.data() + n_q + n_ratio, tables, n_tw * 8);
     std::memcpy(host.data() + n_q + n_ratio + n_tw, n_inv, n_ninv * 8);
     std::memcpy(host.data() + n_q + n_ratio + n_tw + n_ninv, rs.data(), n_rs * 8);
+    for (u32 i = 0; i < nmod; ++i) host[n_q + n_ratio + n_tw + n_ninv + n_rs + i] = h_shoup(1, moduli[i]);
     e = cudaMemcpy(p, host.data(), words * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(p32, eval_exp, size_t(degree) * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(p32 + degree, slot_of_exp, size_t(2) * degree * 4, cudaMemcpyHostToDevice);
@@ -298,8 +300,11 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
             }
         }
     }
-    // ModDown (rlwe.hpp:555-579)
-    std::vector<u64> md(size_t(K) * 2 + size_t(K) * nq * 2 + size_t(nq) * 2, 0);
+    // ModDown (rlwe.hpp:555-579). Layout: [K][2] (P/p_s)^-1 mod p_s + Shoup;
+    // [K][nq][4] (P/p_s) mod q_r, Shoup, its negation q_r - w, Shoup (so a
+    // centered y_s < 0 multiplies |y_s| by -w: no per-term reduction);
+    // [nq][2] P^-1 mod q_r + Shoup.
+    std::vector<u64> md(size_t(K) * 2 + size_t(K) * nq * 4 + size_t(nq) * 2, 0);
     for (u32 s = 0; s < K; ++s) {
         u64 ps = mod[nq + s];
         u64 rest = 1;
@@ -315,18 +320,28 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
             u64 ws = 1;
             for (u32 t = 0; t < K; ++t)
                 if (t != s) ws = h_mul_mod(ws, mod[nq + t] % q, q);
-            u64* e = &md[2 * K + (size_t(s) * nq + r) * 2];
+            u64* e = &md[2 * K + (size_t(s) * nq + r) * 4];
             e[0] = ws;
             e[1] = h_shoup(ws, q);
+            e[2] = ws ? q - ws : 0;
+            e[3] = h_shoup(e[2], q);
         }
     for (u32 r = 0; r < nq; ++r) {
         u64 q = mod[r];
         u64 pinv = 1;
         for (u32 s = 0; s < K; ++s) pinv = h_mul_mod(pinv, mod[nq + s] % q, q);
         pinv = h_inv_mod(pinv, q);
-        u64* e = &md[2 * K + size_t(K) * nq * 2 + size_t(r) * 2];
+        u64* e = &md[2 * K + size_t(K) * nq * 4 + size_t(r) * 2];
         e[0] = pinv;
         e[1] = h_shoup(pinv, q);
+    }
+    // lazy-sum safety: 2*K*q_max + q_max < 2^64 for ModDown, 2*group*q < 2^64 for ModUp
+    {
+        u128 qmax = 0, allmax = 0;
+        for (u32 r = 0; r < nq; ++r) qmax = std::max<u128>(qmax, mod[r]);
+        for (u32 r = 0; r < nmod; ++r) allmax = std::max<u128>(allmax, mod[r]);
+        g->g.lazy_moddown = (u128(2 * K + 1) * qmax) < (u128(1) << 64);
+        g->g.lazy_modup = (u128(2 * gs) * allmax) < (u128(1) << 64);
     }
     size_t words = src.size() + conv.size() + md.size();
     cudaError_t e = cudaMalloc(&g->dev_block, words * 8);

@@ -39,6 +39,7 @@ struct DevRing {
     const u32* eval_exp;     // [N]
     const u32* slot_of_exp;  // [2N]
     const u64* rs;           // [q_count][q_count][4]: ql mod q_r, ql^-1, shoup, half(ql)
+    const u64* one_shoup;    // [nmod]: floor(2^64 / q) (Shoup companion of 1: word -> [0,2q))
 };
 
 // Row r of a poly at (level, nspecial) -> modulus index (ring.hpp:227-229).
@@ -158,7 +159,8 @@ struct GadgetDev {
     u32 group_size, ngroups;
     u64* src;   // [ngroups][group_size(active-1)][group_size(i)][2]
     u64* conv;  // [ngroups][group_size][group_size][nmod][2]
-    u64* md;    // ModDown: [K][2] (P/p_s)^-1 mod p_s; [K][q_count][2] (P/p_s) mod q_r; [q_count][2] P^-1 mod q_r
+    u64* md;    // ModDown: [K][2] (P/p_s)^-1 mod p_s; [K][q_count][4] +-(P/p_s) mod q_r; [q_count][2] P^-1 mod q_r
+    bool lazy_modup, lazy_moddown;  // lazy sums provably fit a word (checked on the host)
 };
 
 }  // namespace tg

@@ -22,8 +22,16 @@ inline u32 grid_for(size_t work) {
     return u32(std::min<size_t>(b, size_t(148) * 8 * 4));
 }
 
-// ModUp base conversion for all digits of one level. grid.y = digit.
-__global__ void __launch_bounds__(kThreads)
+// ModUp base conversion for all digits of one level. grid.y = digit,
+// one thread per coefficient. The uncorrected conversion reproduces the
+// digit's own-group rows exactly (rlwe.hpp:78-100: conv_w[i][t] = 0 for
+// t != i inside the group and y_i * D'/q_i = x_i), so those rows are copied
+// and only the other rows are computed, 4 at a time for ILP. Terms are
+// accumulated lazily (Shoup outputs in [0,2q), sum < 2*active*q < 2^64,
+// checked on the host) and reduced once per output.
+constexpr u32 kMUThreads = 128;
+
+__global__ void __launch_bounds__(kMUThreads)
 k_modup(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict__ d, int level) {
     const u32 N = R.N, lvl = u32(level), K = R.K;
     const u32 j = blockIdx.y;
@@ -34,28 +42,52 @@ k_modup(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict_
     const u64* src_tb = G.src + ((size_t(j) * gs + (active - 1)) * gs) * 2;
     const u64* conv_tb = G.conv + ((size_t(j) * gs + (active - 1)) * gs) * R.nmod * 2;
     u64* out = digits + size_t(j) * rows_out * N;
-    for (u32 c = blockIdx.x * kThreads + threadIdx.x; c < N; c += gridDim.x * kThreads) {
-        u64 y[kMaxGroup];
+    const u32 c = blockIdx.x * kMUThreads + threadIdx.x;
+    if (c >= N) return;
+    u64 y[kMaxGroup];
 #pragma unroll
-        for (u32 i = 0; i < u32(kMaxGroup); ++i) {
-            if (i < active) {
-                const u32 s = first + i;
-                y[i] = shoup(d[size_t(s) * N + c], src_tb[2 * i], src_tb[2 * i + 1], R.q[s]);
-            }
+    for (u32 i = 0; i < u32(kMaxGroup); ++i) {
+        if (i < active) {
+            const u32 s = first + i;
+            const u64 x = d[size_t(s) * N + c];
+            out[size_t(s) * N + c] = x;  // own-group row: exact copy
+            y[i] = shoup(x, src_tb[2 * i], src_tb[2 * i + 1], R.q[s]);
         }
-        for (u32 r = 0; r < rows_out; ++r) {
-            const u32 t = mod_index(r, level, R.q_count);
-            const u64 qt = R.q[t];
-            u64 acc = 0;
+    }
+    const u32 nrest = rows_out - active;
+    for (u32 v0 = 0; v0 < nrest; v0 += 4) {
+        u64 acc[4] = {0, 0, 0, 0};
+        u32 t[4], r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const u32 v = min(v0 + k, nrest - 1);
+            r[k] = v < first ? v : v + active;
+            t[k] = mod_index(r[k], level, R.q_count);
+        }
+        if (G.lazy_modup) {
 #pragma unroll
             for (u32 i = 0; i < u32(kMaxGroup); ++i) {
                 if (i < active) {
-                    const u64* cw = conv_tb + (size_t(i) * R.nmod + t) * 2;
-                    acc = add_mod(acc, shoup(y[i], cw[0], cw[1], qt), qt);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const u64* cw = conv_tb + (size_t(i) * R.nmod + t[k]) * 2;
+                        acc[k] += shoup_lazy(y[i], cw[0], cw[1], R.q[t[k]]);
+                    }
                 }
             }
-            out[size_t(r) * N + c] = acc;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] = shoup(acc[k], 1, R.one_shoup[t[k]], R.q[t[k]]);
+        } else {
+            for (u32 i = 0; i < active; ++i)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const u64* cw = conv_tb + (size_t(i) * R.nmod + t[k]) * 2;
+                    acc[k] = add_mod(acc[k], shoup(y[i], cw[0], cw[1], R.q[t[k]]), R.q[t[k]]);
+                }
         }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (v0 + k < nrest) out[size_t(r[k]) * N + c] = acc[k];
     }
 }
 
@@ -92,44 +124,64 @@ k_key_inner(DevRing R, u64* __restrict__ acc0, u64* __restrict__ acc1, const u64
     }
 }
 
-// ModDown of npolys polys (each level+1+K rows, coeff) -> level+1 rows.
-__global__ void __launch_bounds__(kThreads)
-k_mod_down(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict__ in, int level, u32 npolys) {
+// ModDown of npolys polys (each level+1+K rows, coeff) -> level+1 rows,
+// optionally added to `addend` (out = addend + ModDown(in); the relinearise
+// / Galois epilogue, rlwe.hpp:612-613, :647). Centered y_s = |y_s| * sign
+// multiplies |y_s| by +-(P/p_s) mod q (host-negated tables), so no per-term
+// reduction of from_centered(y_s, q) is needed; terms are summed lazily
+// (< 2Kq) and (x + 2Kq - sum) * P^-1 is one Shoup product.
+__global__ void __launch_bounds__(256)
+k_mod_down(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict__ in, int level, u32 npolys,
+           const u64* __restrict__ addend) {
     const u32 N = R.N, K = R.K, nq = R.q_count, lvl = u32(level);
     const u32 rin = lvl + 1 + K, rout = lvl + 1;
-    const u64* c_s = G.md;                    // [K][2]
-    const u64* w_sr = G.md + 2 * K;           // [K][nq][2]
-    const u64* pinv = w_sr + size_t(K) * nq * 2;  // [nq][2]
+    const u64* c_s = G.md;                            // [K][2]
+    const u64* w_sr = G.md + 2 * K;                   // [K][nq][4]
+    const u64* pinv = w_sr + size_t(K) * nq * 4;      // [nq][2]
     const u64 total = u64(npolys) * N;
-    for (u64 idx = blockIdx.x * u64(kThreads) + threadIdx.x; idx < total; idx += u64(gridDim.x) * kThreads) {
+    for (u64 idx = blockIdx.x * u64(blockDim.x) + threadIdx.x; idx < total; idx += u64(gridDim.x) * blockDim.x) {
         const u64 p = idx >> R.logN;
         const u32 c = u32(idx & (N - 1));
         const u64* src = in + p * rin * N;
         u64* dst = out + p * rout * N;
-        i64 y[kMaxSpecial];
+        const u64* add = addend ? addend + p * rout * N : nullptr;
+        u64 mag[kMaxSpecial];
+        u32 sel[kMaxSpecial];
 #pragma unroll
         for (u32 s = 0; s < u32(kMaxSpecial); ++s) {
             if (s < K) {
                 const u64 ps = R.q[nq + s];
                 const u64 v = shoup(src[size_t(lvl + 1 + s) * N + c], c_s[2 * s], c_s[2 * s + 1], ps);
-                y[s] = v > ps / 2 ? i64(v) - i64(ps) : i64(v);  // to_centered (common.hpp:84-86)
+                const bool neg = v > ps / 2;  // to_centered (common.hpp:84-86)
+                mag[s] = neg ? ps - v : v;
+                sel[s] = neg ? 2 : 0;
             }
         }
-        for (u32 r = 0; r < rout; ++r) {
-            const u64 q = R.q[r], rl = R.ratio[2 * r], rh = R.ratio[2 * r + 1];
-            u64 conv = 0;
+        for (u32 r0 = 0; r0 < rout; r0 += 4) {
+            u64 acc[4] = {0, 0, 0, 0};
 #pragma unroll
             for (u32 s = 0; s < u32(kMaxSpecial); ++s) {
                 if (s < K) {
-                    // from_centered(y_s, q) (common.hpp:88-92)
-                    const u64 mag = y[s] < 0 ? u64(-y[s]) : u64(y[s]);
-                    u64 ys = mag < q ? mag : reduce64(mag, q, rl, rh);
-                    if (y[s] < 0) ys = neg_mod(ys, q);
-                    const u64* w = w_sr + (size_t(s) * nq + r) * 2;
-                    conv = add_mod(conv, shoup(ys, w[0], w[1], q), q);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const u32 r = min(r0 + k, rout - 1);
+                        const u64* w = w_sr + (size_t(s) * nq + r) * 4 + sel[s];
+                        if (G.lazy_moddown) acc[k] += shoup_lazy(mag[s], w[0], w[1], R.q[r]);
+                        else acc[k] = add_mod(acc[k], shoup(mag[s], w[0], w[1], R.q[r]), R.q[r]);
+                    }
                 }
             }
-            dst[size_t(r) * N + c] = shoup(sub_mod(src[size_t(r) * N + c], conv, q), pinv[2 * r], pinv[2 * r + 1], q);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const u32 r = r0 + k;
+                if (r >= rout) break;
+                const u64 q = R.q[r];
+                const u64 x = src[size_t(r) * N + c];
+                const u64 val = G.lazy_moddown ? x + 2 * K * q - acc[k] : sub_mod(x, acc[k], q);
+                u64 o = shoup(val, pinv[2 * r], pinv[2 * r + 1], q);
+                if (add) o = add_mod(o, add[size_t(r) * N + c], q);
+                dst[size_t(r) * N + c] = o;
+            }
         }
     }
 }
@@ -140,26 +192,27 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const u32 nd = tg_gadget_digit_count(g, level);
-    dim3 grid(std::max(1u, std::min(R.N / kThreads, 1024u)), nd);
+    dim3 grid((R.N + kMUThreads - 1) / kMUThreads, nd);
     {
         ProfScope prof(ctx, TG_OP_MODUP, 8.0 * R.N * (double(level + 1) + double(nd) * (level + 1 + R.K)), s);
-        k_modup<<<grid, kThreads, 0, s>>>(R, g->g, digits, d, level);
+        k_modup<<<grid, kMUThreads, 0, s>>>(R, g->g, digits, d, level);
     }
     TG_LAUNCH_CHECK();
     return ntt_forward_rows(ctx, digits, level, int(R.K), nd, s);
 }
 
-int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaStream_t s) {
+int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaStream_t s,
+             const u64* addend = nullptr) {
     const DevRing& R = g->ctx->ring;
-    ProfScope prof(g->ctx, TG_OP_MOD_DOWN, 8.0 * R.N * npolys * (2.0 * (level + 1) + R.K), s);
-    k_mod_down<<<grid_for(size_t(npolys) * R.N), kThreads, 0, s>>>(R, g->g, out, in, level, npolys);
+    ProfScope prof(g->ctx, TG_OP_MOD_DOWN, 8.0 * R.N * npolys * (2.0 * (level + 1) + R.K + (addend ? level + 1 : 0)), s);
+    k_mod_down<<<grid_for(size_t(npolys) * R.N), kThreads, 0, s>>>(R, g->g, out, in, level, npolys, addend);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
 
 // acc buffer holds 2 polys (level+1+K rows each) back to back.
 int ks_inner(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd, const u64* key, int level, u64* acc,
-             cudaStream_t s) {
+             cudaStream_t s, const u64* add0 = nullptr, const u64* add1 = nullptr) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const size_t words = size_t(level + 1 + R.K) * R.N;
@@ -170,9 +223,11 @@ int ks_inner(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd, cons
     }
     TG_LAUNCH_CHECK();
     if (int rc = ntt_inverse_rows(ctx, acc, level, int(R.K), 2, s)) return rc;
-    if (out1 == out0 + size_t(level + 1) * R.N) return mod_down(g, out0, acc, level, 2, s);
-    if (int rc = mod_down(g, out0, acc, level, 1, s)) return rc;
-    return mod_down(g, out1, acc + words, level, 1, s);
+    const size_t ow = size_t(level + 1) * R.N;
+    if (out1 == out0 + ow && ((!add0 && !add1) || (add0 && add1 == add0 + ow)))
+        return mod_down(g, out0, acc, level, 2, s, add0);
+    if (int rc = mod_down(g, out0, acc, level, 1, s, add0)) return rc;
+    return mod_down(g, out1, acc + words, level, 1, s, add1);
 }
 
 }  // namespace tg
@@ -216,6 +271,12 @@ extern "C" int tg_ks_inner(tg_gadget* g, uint64_t* out0, uint64_t* out1, const u
 
 extern "C" int tg_switch_key_apply(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
                                    const uint64_t* key, uint32_t key_digits, int level, void* stream) {
+    return tg_keyswitch_add(g, out0, out1, d, key, key_digits, level, nullptr, nullptr, stream);
+}
+
+extern "C" int tg_keyswitch_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d, const uint64_t* key,
+                                uint32_t key_digits, int level, const uint64_t* add0, const uint64_t* add1,
+                                void* stream) {
     if (int rc = check_ks(g, level)) return rc;
     tg_context* ctx = g->ctx;
     const u32 nd = tg_gadget_digit_count(g, level);
@@ -227,7 +288,7 @@ extern "C" int tg_switch_key_apply(tg_gadget* g, uint64_t* out0, uint64_t* out1,
     TG_CUDA(cudaMallocFromPoolAsync(&scratch, (nd + 2) * words * 8, ctx->pool, s));
     u64* digits = static_cast<u64*>(scratch);
     int rc = modup(g, digits, d, level, s);
-    if (rc == TG_OK) rc = ks_inner(g, out0, out1, digits, nd, key, level, digits + size_t(nd) * words, s);
+    if (rc == TG_OK) rc = ks_inner(g, out0, out1, digits, nd, key, level, digits + size_t(nd) * words, s, add0, add1);
     cudaFreeAsync(scratch, s);
     return rc;
 }
