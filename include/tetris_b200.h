@@ -198,10 +198,12 @@ int tg_switch_key_apply(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint
 /* Key switch with the epilogue add fused into ModDown: out_i = add_i +
  * switch_key_apply(d)_i (add_i may be NULL). This is relinearize's
  * (c0+d0, c1+d1) (rlwe.hpp:607-613) and apply_galois' (phi(c0)+d0, d1)
- * (rlwe.hpp:646-648) in one pass. */
+ * (rlwe.hpp:646-648) in one pass. d_eval (may be NULL) is the eval form of d:
+ * when given, each digit's own-group rows (equal to d's rows, rlwe.hpp:78-100)
+ * are copied from it instead of being forward-transformed. */
 int tg_keyswitch_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
-                     const uint64_t* key, uint32_t key_digits, int level, const uint64_t* add0,
-                     const uint64_t* add1, void* stream);
+                     const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
+                     const uint64_t* add0, const uint64_t* add1, void* stream);
 
 #ifdef __cplusplus
 }

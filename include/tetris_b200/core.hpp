@@ -201,9 +201,25 @@ public:
     u64* data() const { return ptr_; }
     std::size_t words() const { return words_; }
 
+    // Memoised forward transforms of (immutable, shared) contents: the eval
+    // form of the `nparts` polys of shape (level, nspecial) starting at `off`.
+    // Ladder operands are multiplied several times (and squared), so each is
+    // transformed once. Bit-exact: the NTT is deterministic.
+    struct EvalCache {
+        std::size_t off;
+        int level, nspecial, nparts;
+        void* stream;
+        std::shared_ptr<DeviceBuffer> buf;
+    };
+    std::shared_ptr<DeviceBuffer> find_eval(std::size_t off, int level, int nspecial, int nparts, void* stream) const;
+    void put_eval(std::size_t off, int level, int nspecial, int nparts, void* stream,
+                  std::shared_ptr<DeviceBuffer> buf) const;
+
 private:
     std::shared_ptr<DeviceState> dev_;
-    void* stream_ = nullptr;  // allocation stream; the buffer is freed there
+    void* stream_ = nullptr;  // allocation stream
+    mutable std::mutex cache_mu_;
+    mutable std::vector<EvalCache> cache_;
     u64* ptr_ = nullptr;
     std::size_t words_ = 0;
 };

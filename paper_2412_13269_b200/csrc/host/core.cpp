@@ -292,6 +292,22 @@ DeviceBuffer::DeviceBuffer(const RingParams& ring, std::size_t words)
     ptr_ = static_cast<u64*>(p);
 }
 
+std::shared_ptr<DeviceBuffer> DeviceBuffer::find_eval(std::size_t off, int level, int nspecial, int nparts,
+                                                      void* stream) const {
+    std::lock_guard<std::mutex> g(cache_mu_);
+    for (const auto& e : cache_)
+        if (e.off == off && e.level == level && e.nspecial == nspecial && e.nparts == nparts && e.stream == stream)
+            return e.buf;
+    return nullptr;
+}
+
+void DeviceBuffer::put_eval(std::size_t off, int level, int nspecial, int nparts, void* stream,
+                            std::shared_ptr<DeviceBuffer> buf) const {
+    std::lock_guard<std::mutex> g(cache_mu_);
+    if (cache_.size() >= 4) cache_.erase(cache_.begin());
+    cache_.push_back(EvalCache{off, level, nspecial, nparts, stream, std::move(buf)});
+}
+
 // Freed on the destroying thread's current stream: ordered after that
 // thread's uses; buffers crossing threads are handed over only after the
 // producing stream was synchronized (see eval_private_threshold_many).

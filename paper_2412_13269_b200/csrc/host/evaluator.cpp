@@ -284,14 +284,11 @@ static void scale_parts(Ciphertext& out, const std::vector<u64>& per_mod) {
     const std::size_t np = out.parts.size();
     const Poly& p0 = out.parts[0];
     const RingParams& R = p0.ring();
-    if (contiguous(out.parts, 0, np)) {
-        std::vector<Poly> dst = fresh_parts(R, int(np), p0.level(), p0.form(), p0.nspecial());
-        check_tg(tg_poly_mul_scalar(R.dev(), const_cast<u64*>(dst[0].data()), p0.data(), per_mod.data(), p0.level(),
-                                    p0.nspecial(), u32(np), R.stream()));
-        out.parts = std::move(dst);
-        return;
-    }
-    for (auto& part : out.parts) part.mul_scalar_inplace(per_mod);
+    (void)np;
+    const int lvl = p0.level(), ns = p0.nspecial();
+    out.parts = detail::map_parts(out.parts, lvl, p0.form(), [&](u64* d, const u64* s, u32 n) {
+        check_tg(tg_poly_mul_scalar(R.dev(), d, s, per_mod.data(), lvl, ns, n, R.stream()));
+    });
 }
 
 Ciphertext Evaluator::mul_scalar(const Ciphertext& ct, double c, double scalar_scale) const {
@@ -317,10 +314,20 @@ Ciphertext Evaluator::add_scalar(const Ciphertext& ct, double c) const {
     const RingParams& R = ring();
     std::vector<u64> add(R.moduli().size(), 0);
     for (int r = 0; r < p0.rows(); ++r) add[p0.modulus_index(r)] = scaled_residue(c * ct.scale, p0.row_modulus(r));
-    std::vector<Poly> dst = fresh_parts(R, 1, p0.level(), p0.form(), p0.nspecial());
+    // keep all parts in one block (batched launches downstream)
+    const std::size_t np = ct.parts.size();
+    std::vector<Poly> dst = fresh_parts(R, int(np), p0.level(), p0.form(), p0.nspecial());
     check_tg(tg_poly_add_scalar(R.dev(), const_cast<u64*>(dst[0].data()), p0.data(), add.data(), tg_form(p0.form()),
                                 p0.level(), p0.nspecial(), 1, R.stream()));
-    out.parts[0] = dst[0];
+    for (std::size_t i = 1; i < np; ++i) {
+        if (ct.parts[i].level() != p0.level() || ct.parts[i].form() != p0.form()) {  // irregular: keep as is
+            out.parts[0] = dst[0];
+            return out;
+        }
+        check_tg(tg_memcpy_d2d(R.dev(), const_cast<u64*>(dst[i].data()), ct.parts[i].data(), dst[i].words() * 8,
+                               R.stream()));
+    }
+    out.parts = std::move(dst);
     return out;
 }
 
@@ -329,16 +336,13 @@ Ciphertext Evaluator::rescale(const Ciphertext& ct) const {
     Ciphertext out = ct;
     out.to_coeff();
     const u64 ql = ring().modulus(u32(ct.level()));
-    const std::size_t np = out.parts.size();
-    if (contiguous(out.parts, 0, np)) {
-        const RingParams& R = ring();
-        const int lvl = out.level();
-        std::vector<Poly> dst = fresh_parts(R, int(np), lvl - 1, Form::coeff);
-        check_tg(tg_rescale(R.dev(), const_cast<u64*>(dst[0].data()), out.parts[0].data(), lvl, u32(np), R.stream()));
-        out.parts = std::move(dst);
-    } else {
-        for (auto& p : out.parts) p = rescale_round(p);
-    }
+    const RingParams& R = ring();
+    const int lvl = out.level();
+    for (const auto& p : out.parts)
+        if (p.nspecial() != 0) throw TetrisError("ring", "rescale with special rows");
+    out.parts = detail::map_parts(out.parts, lvl - 1, Form::coeff, [&](u64* d, const u64* s, u32 n) {
+        check_tg(tg_rescale(R.dev(), d, s, lvl, n, R.stream()));
+    });
     out.scale = ct.scale / double(ql);
     out.noise_bound = ct.noise_bound / double(ql) + 1.0;
     return out;

@@ -40,4 +40,37 @@ inline bool exclusively_owned(const std::vector<Poly>& parts) {
 
 inline int tg_form(Form f) { return f == Form::eval ? TG_FORM_EVAL : TG_FORM_COEFF; }
 
+// Applies a per-part kernel `fn(dst, src, npolys)` to all parts, writing one
+// fresh contiguous block of shape (out_level, out_form): a single batched
+// launch when the sources are contiguous, one launch per part otherwise.
+// Keeping outputs contiguous keeps every downstream op batched.
+template <class F>
+std::vector<Poly> map_parts(const std::vector<Poly>& src, int out_level, Form out_form, F fn) {
+    const Poly& p0 = src[0];
+    const RingParams& ring = p0.ring();
+    const std::size_t np = src.size();
+    std::vector<Poly> dst = fresh_parts(ring, int(np), out_level, out_form, p0.nspecial());
+    if (contiguous(src, 0, np)) {
+        fn(const_cast<u64*>(dst[0].data()), p0.data(), u32(np));
+    } else {
+        for (std::size_t i = 0; i < np; ++i) fn(const_cast<u64*>(dst[i].data()), src[i].data(), 1u);
+    }
+    return dst;
+}
+
+// Binary variant: fn(dst, a, b, npolys).
+template <class F>
+std::vector<Poly> map_parts2(const std::vector<Poly>& a, const std::vector<Poly>& b, F fn) {
+    const Poly& p0 = a[0];
+    const RingParams& ring = p0.ring();
+    const std::size_t np = a.size();
+    std::vector<Poly> dst = fresh_parts(ring, int(np), p0.level(), p0.form(), p0.nspecial());
+    if (contiguous(a, 0, np) && contiguous(b, 0, np)) {
+        fn(const_cast<u64*>(dst[0].data()), p0.data(), b[0].data(), u32(np));
+    } else {
+        for (std::size_t i = 0; i < np; ++i) fn(const_cast<u64*>(dst[i].data()), a[i].data(), b[i].data(), 1u);
+    }
+    return dst;
+}
+
 }  // namespace tetris_b200::detail

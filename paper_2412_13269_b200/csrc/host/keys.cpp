@@ -120,25 +120,67 @@ Poly SecretKey::shaped(int level, int nspecial) const {
 // ---------------------------------------------------------------------------
 // Ciphertext (rlwe.hpp:287-317)
 // ---------------------------------------------------------------------------
+// Parts that share one block at a uniform stride S (a contiguous block, or
+// one whose level was dropped: each part is then a row prefix of an S-word
+// poly). Returns S in words, 0 if the parts are not laid out that way.
+static std::size_t uniform_stride(const std::vector<Poly>& parts) {
+    const Poly& p0 = parts[0];
+    const std::size_t n = p0.ring().degree();
+    std::size_t S = p0.words();
+    if (parts.size() > 1) S = parts[1].offset() - p0.offset();
+    if (S < p0.words() || S % n != 0) return 0;
+    for (std::size_t i = 0; i < parts.size(); ++i) {
+        const Poly& p = parts[i];
+        if (p.storage() != p0.storage() || p.level() != p0.level() || p.nspecial() != p0.nspecial() ||
+            p.form() != p0.form() || p.offset() != p0.offset() + i * S)
+            return 0;
+    }
+    if (p0.offset() + parts.size() * S > p0.storage()->words()) return 0;
+    return S;
+}
+
+// Transforms all parts in as few launches as possible. Parts on a uniform
+// stride are transformed as full S-word polys (rows beyond a dropped level
+// included: the NTT is row-wise, so the prefix rows are exactly the dropped
+// poly's transform). A shared block's forward transform is memoised on the
+// block, so ladder operands used several times (squares included) are
+// transformed once.
 static void transform_parts(Ciphertext& ct, Form target) {
     const Form from = target == Form::eval ? Form::coeff : Form::eval;
     bool any = false;
     for (auto& p : ct.parts) any |= p.form() == from;
     if (!any) return;
     const std::size_t np = ct.parts.size();
-    if (contiguous(ct.parts, 0, np)) {
+    const std::size_t S = uniform_stride(ct.parts);
+    if (S) {
         const Poly& p0 = ct.parts[0];
         const RingParams& ring = p0.ring();
-        const u64* src = p0.data();
-        std::vector<Poly> dst = exclusively_owned(ct.parts) ? ct.parts
-                                                            : fresh_parts(ring, int(np), p0.level(), target, p0.nspecial());
-        u64* out = const_cast<u64*>(dst[0].data());
-        if (target == Form::eval)
-            check_tg(tg_ntt_forward_oop(ring.dev(), out, src, p0.level(), p0.nspecial(), u32(np), ring.stream()));
-        else
-            check_tg(tg_ntt_inverse_oop(ring.dev(), out, src, p0.level(), p0.nspecial(), u32(np), ring.stream()));
-        for (auto& p : dst) p.set_form(target);
-        ct.parts = std::move(dst);
+        const int ns = p0.nspecial(), lvl = p0.level();
+        const int full_level = int(S / ring.degree()) - 1 - ns;
+        const bool own = p0.storage().use_count() == long(np);
+        std::shared_ptr<DeviceBuffer> out_blk;
+        std::size_t out_off = 0;
+        if (!own && target == Form::eval)
+            out_blk = p0.storage()->find_eval(p0.offset(), full_level, ns, int(np), ring.stream());
+        if (!out_blk) {
+            if (own) {
+                out_blk = p0.storage();
+                out_off = p0.offset();
+            } else {
+                out_blk = detail::new_block(ring, S * np);
+            }
+            u64* dst = out_blk->data() + out_off;
+            if (target == Form::eval)
+                check_tg(tg_ntt_forward_oop(ring.dev(), dst, p0.data(), full_level, ns, u32(np), ring.stream()));
+            else
+                check_tg(tg_ntt_inverse_oop(ring.dev(), dst, p0.data(), full_level, ns, u32(np), ring.stream()));
+            if (!own && target == Form::eval)
+                p0.storage()->put_eval(p0.offset(), full_level, ns, int(np), ring.stream(), out_blk);
+        }
+        std::vector<Poly> v;
+        v.reserve(np);
+        for (std::size_t i = 0; i < np; ++i) v.push_back(Poly::view(ring, out_blk, out_off + S * i, lvl, target, ns));
+        ct.parts = std::move(v);
         return;
     }
     for (auto& p : ct.parts)
@@ -167,7 +209,12 @@ static void addsub_ct(Ciphertext& x, const Ciphertext& o, int op) {
         x.parts = std::move(dst);
         return;
     }
-    for (std::size_t i = 0; i < np; ++i) op == 0 ? x.parts[i].add_inplace(o.parts[i]) : x.parts[i].sub_inplace(o.parts[i]);
+    const Poly& p0 = x.parts[0];
+    const RingParams& ring = p0.ring();
+    const int lvl = p0.level(), ns = p0.nspecial();
+    x.parts = detail::map_parts2(x.parts, o.parts, [&](u64* d, const u64* a, const u64* b, u32 n) {
+        check_tg(tg_poly_addsub(ring.dev(), d, a, b, op, lvl, ns, n, ring.stream()));
+    });
 }
 
 void Ciphertext::add_inplace(const Ciphertext& o) {
@@ -379,6 +426,10 @@ SwitchingKey KeyContext::relin_key_gen(const SecretKey& sk, Rng& rng) const {
 Ciphertext KeyContext::relinearize(const Ciphertext& ct, const SwitchingKey& rlk) const {
     if (ct.degree() != 2) throw TetrisError("rlwe", "relinearize expects a degree-2 ciphertext");
     if (rlk.to_id != ct.sk_id) throw TetrisError("rlwe", "relinearization key mismatch");
+    // keep the eval form of c2 (the tensor output): the digits' own-group rows
+    // are its rows, so ModUp copies them instead of re-transforming
+    Poly c2_eval;
+    if (ct.parts[2].form() == Form::eval && ct.parts[2].nspecial() == 0) c2_eval = ct.parts[2];
     Ciphertext src = ct;
     src.to_coeff();  // one batched iNTT when the three parts share a block
     const int lvl = ct.level();
@@ -387,8 +438,8 @@ Ciphertext KeyContext::relinearize(const Ciphertext& ct, const SwitchingKey& rlk
         throw TetrisError("rlwe", "decompose expects coeff form without special rows");
     std::vector<Poly> dst = fresh_parts(*ring_, 2, lvl, Form::coeff);
     check_tg(tg_keyswitch_add(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[1].data()),
-                              c2.data(), key_base(rlk), rlk.digits(), lvl, src.parts[0].data(), src.parts[1].data(),
-                              ring_->stream()));
+                              c2.data(), c2_eval.empty() ? nullptr : c2_eval.data(), key_base(rlk), rlk.digits(),
+                              lvl, src.parts[0].data(), src.parts[1].data(), ring_->stream()));
     Ciphertext out;
     out.parts = std::move(dst);
     out.scale = ct.scale;
@@ -435,7 +486,7 @@ Ciphertext KeyContext::apply_galois(const Ciphertext& ct, u64 exponent, const Sw
     Ciphertext out;
     std::vector<Poly> dst = fresh_parts(*ring_, 2, lvl, Form::coeff);
     check_tg(tg_keyswitch_add(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[1].data()),
-                              rot[1].data(), key_base(swk), swk.digits(), lvl, rot[0].data(), nullptr,
+                              rot[1].data(), nullptr, key_base(swk), swk.digits(), lvl, rot[0].data(), nullptr,
                               ring_->stream()));
     out.parts = std::move(dst);
     out.scale = ct.scale;

@@ -236,7 +236,8 @@ namespace tg {
 // Launch helpers implemented in tg_ntt.cu (used by the keyswitch pipeline).
 int ntt_forward_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s);
 int ntt_inverse_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s);
-int ntt_forward_oop(tg_context* ctx, u64* dst, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s);
+int ntt_forward_oop(tg_context* ctx, u64* dst, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s,
+                    u32 skip_gs = 0);
 int ntt_inverse_oop(tg_context* ctx, u64* dst, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s);
 struct DeviceGuard {
     int prev = -1;

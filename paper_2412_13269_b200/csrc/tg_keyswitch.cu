@@ -32,7 +32,8 @@ inline u32 grid_for(size_t work) {
 constexpr u32 kMUThreads = 128;
 
 __global__ void __launch_bounds__(kMUThreads)
-k_modup(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict__ d, int level) {
+k_modup(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict__ d, int level,
+        const u64* __restrict__ d_eval) {
     const u32 N = R.N, lvl = u32(level), K = R.K;
     const u32 j = blockIdx.y;
     const u32 gs = G.group_size;
@@ -50,7 +51,9 @@ k_modup(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict_
         if (i < active) {
             const u32 s = first + i;
             const u64 x = d[size_t(s) * N + c];
-            out[size_t(s) * N + c] = x;  // own-group row: exact copy
+            // own-group row: exact copy (already transformed when the caller
+            // holds the eval form of d; the digit NTT then skips this row)
+            out[size_t(s) * N + c] = d_eval ? d_eval[size_t(s) * N + c] : x;
             y[i] = shoup(x, src_tb[2 * i], src_tb[2 * i + 1], R.q[s]);
         }
     }
@@ -188,17 +191,17 @@ k_mod_down(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict_
 
 }  // namespace
 
-int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s) {
+int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, const u64* d_eval = nullptr) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const u32 nd = tg_gadget_digit_count(g, level);
     dim3 grid((R.N + kMUThreads - 1) / kMUThreads, nd);
     {
         ProfScope prof(ctx, TG_OP_MODUP, 8.0 * R.N * (double(level + 1) + double(nd) * (level + 1 + R.K)), s);
-        k_modup<<<grid, kMUThreads, 0, s>>>(R, g->g, digits, d, level);
+        k_modup<<<grid, kMUThreads, 0, s>>>(R, g->g, digits, d, level, d_eval);
     }
     TG_LAUNCH_CHECK();
-    return ntt_forward_rows(ctx, digits, level, int(R.K), nd, s);
+    return ntt_forward_oop(ctx, digits, digits, level, int(R.K), nd, s, d_eval ? g->g.group_size : 0);
 }
 
 int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaStream_t s,
@@ -271,10 +274,11 @@ extern "C" int tg_ks_inner(tg_gadget* g, uint64_t* out0, uint64_t* out1, const u
 
 extern "C" int tg_switch_key_apply(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
                                    const uint64_t* key, uint32_t key_digits, int level, void* stream) {
-    return tg_keyswitch_add(g, out0, out1, d, key, key_digits, level, nullptr, nullptr, stream);
+    return tg_keyswitch_add(g, out0, out1, d, nullptr, key, key_digits, level, nullptr, nullptr, stream);
 }
 
-extern "C" int tg_keyswitch_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d, const uint64_t* key,
+extern "C" int tg_keyswitch_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
+                                const uint64_t* d_eval, const uint64_t* key,
                                 uint32_t key_digits, int level, const uint64_t* add0, const uint64_t* add1,
                                 void* stream) {
     if (int rc = check_ks(g, level)) return rc;
@@ -287,7 +291,7 @@ extern "C" int tg_keyswitch_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, co
     void* scratch = nullptr;
     TG_CUDA(cudaMallocFromPoolAsync(&scratch, (nd + 2) * words * 8, ctx->pool, s));
     u64* digits = static_cast<u64*>(scratch);
-    int rc = modup(g, digits, d, level, s);
+    int rc = modup(g, digits, d, level, s, d_eval);
     if (rc == TG_OK) rc = ks_inner(g, out0, out1, digits, nd, key, level, digits + size_t(nd) * words, s, add0, add1);
     cudaFreeAsync(scratch, s);
     return rc;

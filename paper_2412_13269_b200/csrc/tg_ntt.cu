@@ -20,7 +20,15 @@ namespace tg {
 namespace {
 
 constexpr u32 kThreads = 256;
-constexpr u32 kLogTile = 11;  // 2048 words = 16 KiB of shared memory per block
+constexpr u32 kLogTile = 11;
+
+// Row-skip rule of ModUp digit transforms: poly p = digit p, whose own-group
+// rows (r <= level, r / group_size == p) were copied already in eval form.
+__device__ __forceinline__ bool ntt_row_skipped(u32 row, u32 rpp, int level, u32 skip_gs) {
+    if (!skip_gs) return false;
+    const u32 r = row % rpp, p = row / rpp;
+    return r <= u32(level) && r / skip_gs == p;
+}  // 2048 words = 16 KiB of shared memory per block
 
 struct Plan {
     u32 logN1, logN2, logC, logCpb;
@@ -37,8 +45,10 @@ Plan make_plan(u32 logN) {
 }
 
 __global__ void __launch_bounds__(kThreads)
-k_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rows_per_poly, int level, u32 logN1, u32 logC) {
+k_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rows_per_poly, int level, u32 logN1, u32 logC,
+           u32 skip_gs) {
     extern __shared__ u64 sm[];
+    if (ntt_row_skipped(row_base + blockIdx.y, rows_per_poly, level, skip_gs)) return;
     const u32 N = R.N, C = 1u << logC, N2 = N >> logN1;
     const u32 row = row_base + blockIdx.y;
     const u32 mi = mod_index(row % rows_per_poly, level, R.q_count);
@@ -70,8 +80,10 @@ k_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rows_per_poly
 }
 
 __global__ void __launch_bounds__(kThreads)
-k_fwd_chunks(DevRing R, u64* __restrict__ data, u32 row_base, u32 rows_per_poly, int level, u32 logN1, u32 logCpb) {
+k_fwd_chunks(DevRing R, u64* __restrict__ data, u32 row_base, u32 rows_per_poly, int level, u32 logN1, u32 logCpb,
+             u32 skip_gs) {
     extern __shared__ u64 sm[];
+    if (ntt_row_skipped(row_base + blockIdx.y, rows_per_poly, level, skip_gs)) return;
     const u32 N = R.N, logN = R.logN, logN2 = logN - logN1;
     const u32 row = row_base + blockIdx.y;
     const u32 mi = mod_index(row % rows_per_poly, level, R.q_count);
@@ -189,7 +201,8 @@ int ntt_inverse_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 np
     return ntt_inverse_oop(ctx, data, data, level, nspecial, npolys, s);
 }
 
-int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s) {
+int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s,
+                    u32 skip_gs) {
     const DevRing& R = ctx->ring;
     const Plan p = make_plan(R.logN);
     const u32 rpp = u32(level + 1 + nspecial);
@@ -200,9 +213,9 @@ int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     if (warp_plan(R.logN, e1, e2)) {
         for (u32 base = 0; base < total; base += 65535) {
             const u32 rows = std::min(65535u, total - base);
-            if (e1 == 8) launch_fwd_w<8, 8>(R, data, src, base, rows, rpp, level, s);
-            else if (e2 == 8) launch_fwd_w<4, 8>(R, data, src, base, rows, rpp, level, s);
-            else launch_fwd_w<4, 4>(R, data, src, base, rows, rpp, level, s);
+            if (e1 == 8) launch_fwd_w<8, 8>(R, data, src, base, rows, rpp, level, s, skip_gs);
+            else if (e2 == 8) launch_fwd_w<4, 8>(R, data, src, base, rows, rpp, level, s, skip_gs);
+            else launch_fwd_w<4, 4>(R, data, src, base, rows, rpp, level, s, skip_gs);
         }
         TG_LAUNCH_CHECK();
         return TG_OK;
@@ -210,8 +223,8 @@ int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     for (u32 base = 0; base < total; base += 65535) {
         const u32 rows = std::min(65535u, total - base);
         dim3 g1((R.N >> p.logN1) >> p.logC, rows), g2((1u << p.logN1) >> p.logCpb, rows);
-        k_fwd_cols<<<g1, kThreads, sm1, s>>>(R, data, src, base, rpp, level, p.logN1, p.logC);
-        k_fwd_chunks<<<g2, kThreads, sm2, s>>>(R, data, base, rpp, level, p.logN1, p.logCpb);
+        k_fwd_cols<<<g1, kThreads, sm1, s>>>(R, data, src, base, rpp, level, p.logN1, p.logC, skip_gs);
+        k_fwd_chunks<<<g2, kThreads, sm2, s>>>(R, data, base, rpp, level, p.logN1, p.logCpb, skip_gs);
     }
     TG_LAUNCH_CHECK();
     return TG_OK;

@@ -186,8 +186,9 @@ constexpr size_t chunk_smem() {
 // Phase 1 forward: 8 columns x M1 rows, stages 0 .. log M1 - 1.
 template <int E>
 __global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
-kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int level) {
+kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int level, u32 skip_gs) {
     using Gm = WGeo<E>;
+    if (ntt_row_skipped(row_base + blockIdx.y, rpp, level, skip_gs)) return;
     extern __shared__ u64 dyn[];
     u64* sm = dyn;
     u64* sw = dyn + 8 * Gm::CS;
@@ -221,8 +222,9 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int lev
 // Phase 2 forward: one warp per contiguous chunk of M2, final canonical reduce.
 template <int E>
 __global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
-kw_fwd_chunks(DevRing R, u64* data, u32 row_base, u32 rpp, int level, u32 logN1) {
+kw_fwd_chunks(DevRing R, u64* data, u32 row_base, u32 rpp, int level, u32 logN1, u32 skip_gs) {
     using Gm = WGeo<E>;
+    if (ntt_row_skipped(row_base + blockIdx.y, rpp, level, skip_gs)) return;
     extern __shared__ u64 dyn[];
     u64* sm = dyn;
     u64* sw = dyn + 8 * Gm::CS;
@@ -345,11 +347,13 @@ void set_smem_attrs() {
 }
 
 template <int E1, int E2>
-void launch_fwd_w(const DevRing& R, u64* data, const u64* src, u32 base, u32 rows, u32 rpp, int level, cudaStream_t s) {
+void launch_fwd_w(const DevRing& R, u64* data, const u64* src, u32 base, u32 rows, u32 rpp, int level, cudaStream_t s,
+                  u32 skip_gs) {
     set_smem_attrs<E1, E2>();
     const u32 M1 = 32 * E1, M2 = 32 * E2;
-    kw_fwd_cols<E1><<<dim3(M2 / 8, rows), 256, col_smem<E1>(), s>>>(R, data, src, base, rpp, level);
-    kw_fwd_chunks<E2><<<dim3(M1 / 8, rows), 256, chunk_smem<E2>(), s>>>(R, data, base, rpp, level, WGeo<E1>::LOGM);
+    kw_fwd_cols<E1><<<dim3(M2 / 8, rows), 256, col_smem<E1>(), s>>>(R, data, src, base, rpp, level, skip_gs);
+    kw_fwd_chunks<E2><<<dim3(M1 / 8, rows), 256, chunk_smem<E2>(), s>>>(R, data, base, rpp, level, WGeo<E1>::LOGM,
+                                                                          skip_gs);
 }
 
 template <int E1, int E2>
