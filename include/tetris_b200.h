@@ -104,6 +104,7 @@ enum {
     TG_OP_KEY_INNER,
     TG_OP_MOD_DOWN,
     TG_OP_REDUCE,
+    TG_OP_LINCOMB,
     TG_OP_COUNT
 };
 int tg_profile_enable(tg_context* ctx, int on);
@@ -157,6 +158,23 @@ int tg_automorphism(tg_context* ctx, uint64_t* out, const uint64_t* in, uint64_t
  * out (level rows) must not alias in (level+1 rows). */
 int tg_rescale(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, uint32_t npolys,
                void* stream);
+
+/* ---- fused residue expressions ------------------------------------------ */
+#define TG_LINCOMB_MAX_TERMS 32
+#define TG_LINCOMB_MAX_ROWS 32
+/* out = [rescale_round]( sum_t coeffs[t][r] * term_t  (+ add_per_row[r]) ) mod q_r
+ * over `nparts` parts of `level`+1 rows (no specials). Term t part p row r
+ * is read at terms[t] + p*part_strides[t] + r*N (level-dropped views allowed).
+ * coeffs: nterms x (level+1) host words (one integer per row modulus).
+ * add_per_row (host, may be NULL) is added to part 0 only: to every
+ * coefficient if add_all (eval form) else to coefficient 0 (coeff form).
+ * With rescale, out has `level` rows (rescale_round, ring.hpp:493-518) and
+ * the input must be coefficient form. One pass replaces the ladder /
+ * combination chains of eval_chebyshev (ckks.hpp:538-578): add_inplace,
+ * mul_scalar, sub_inplace, add_scalar, rescale. out must not alias a term. */
+int tg_lincomb(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* terms,
+               const uint64_t* part_strides, const uint64_t* coeffs, const uint64_t* add_per_row,
+               int add_all, int level, uint32_t nparts, int rescale, void* stream);
 
 /* ---- CKKS products ------------------------------------------------------ */
 /* Evaluator::mul tensor step (ckks.hpp:229-237), eval form inputs:

@@ -1,0 +1,110 @@
+// Fused linear combination (+ constant, + rescale) of ciphertext parts.
+//
+// The Chebyshev ladder (ckks.hpp:538-551) and its coefficient combination
+// (ckks.hpp:558-578), and the threshold normalisation (threshold.hpp:152-155),
+// are chains of Poly ops: doubling (add_inplace), mul_scalar (Shoup by a
+// per-modulus integer), sub_inplace, add_scalar, rescale_round. Every link is
+// exact arithmetic mod q, so the whole chain equals ONE residue expression
+//     out = rescale( sum_t c_t * term_t  +  const )        (mod q)
+// evaluated here in one pass: each input word read once, each output word
+// written once, no intermediate polys. Results are bit-identical to the
+// sequential reference ops (canonical residues of the same integers).
+#include "tg_internal.cuh"
+
+namespace tg {
+namespace {
+
+constexpr u32 kThreads = 256;
+
+inline u32 grid_for(size_t work) {
+    size_t b = (work + kThreads - 1) / kThreads;
+    return u32(std::min<size_t>(b, size_t(148) * 8 * 4));
+}
+
+struct LinComb {
+    u32 nterms, nparts, rescale, add_all;
+    int level;
+    const u64* ptr[TG_LINCOMB_MAX_TERMS];
+    u64 pstride[TG_LINCOMB_MAX_TERMS];
+    u64 c[TG_LINCOMB_MAX_TERMS][TG_LINCOMB_MAX_ROWS];
+    u64 cs[TG_LINCOMB_MAX_TERMS][TG_LINCOMB_MAX_ROWS];
+    u64 add[TG_LINCOMB_MAX_ROWS];
+};
+
+// sum_t c_t * term_t[p][r][c] (+ const) mod q_r, canonical
+__device__ __forceinline__ u64 lc_row(const DevRing& R, const LinComb& L, u32 p, u32 r, u32 c, bool add_here) {
+    const u64 q = R.q[r], one = R.one_shoup[r];
+    u64 acc = add_here ? L.add[r] : 0;
+    for (u32 t = 0; t < L.nterms; ++t) {
+        const u64 x = L.ptr[t][p * L.pstride[t] + size_t(r) * R.N + c];
+        acc += shoup_lazy(x, L.c[t][r], L.cs[t][r], q);
+        if ((t & 7) == 7) acc = shoup_lazy(acc, 1, one, q);  // keep the lazy sum < 16q < 2^64
+    }
+    return shoup(acc, 1, one, q);
+}
+
+__global__ void __launch_bounds__(kThreads) k_lincomb(DevRing R, LinComb L, u64* __restrict__ out) {
+    const u32 N = R.N, lvl = u32(L.level);
+    const u32 rout = L.rescale ? lvl : lvl + 1;
+    const u64 total = u64(L.nparts) * N;
+    for (u64 i = blockIdx.x * u64(kThreads) + threadIdx.x; i < total; i += u64(gridDim.x) * kThreads) {
+        const u32 p = u32(i >> R.logN), c = u32(i & (N - 1));
+        const bool add_here = p == 0 && (L.add_all || c == 0);
+        u64* dst = out + size_t(p) * rout * N;
+        if (!L.rescale) {
+            for (u32 r = 0; r <= lvl; ++r) dst[size_t(r) * N + c] = lc_row(R, L, p, r, c, add_here);
+            continue;
+        }
+        // rescale_round (ring.hpp:493-518) of the combined poly
+        const u64 last = lc_row(R, L, p, lvl, c, add_here);
+        for (u32 r = 0; r < lvl; ++r) {
+            const u64 q = R.q[r];
+            const u64* e = R.rs + (size_t(lvl) * R.q_count + r) * 4;
+            u64 t = last < q ? last : reduce64(last, q, R.ratio[2 * r], R.ratio[2 * r + 1]);
+            if (last > e[3]) t = sub_mod(t, e[0], q);
+            const u64 v = lc_row(R, L, p, r, c, add_here);
+            dst[size_t(r) * N + c] = shoup(sub_mod(v, t, q), e[1], e[2], q);
+        }
+    }
+}
+
+}  // namespace
+}  // namespace tg
+
+using namespace tg;
+
+extern "C" int tg_lincomb(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* terms,
+                          const uint64_t* part_strides, const uint64_t* coeffs, const uint64_t* add_per_row,
+                          int add_all, int level, uint32_t nparts, int rescale, void* stream) {
+    if (!ctx) return fail(TG_E_ARG, "[ring] null context");
+    const DevRing& R = ctx->ring;
+    if (level < 0 || u32(level) >= R.q_count) return fail(TG_E_ARG, "[ring] poly level out of range");
+    if (rescale && level < 1) return fail(TG_E_ARG, "[ring] cannot rescale at level 0");
+    if (nterms == 0 || nterms > TG_LINCOMB_MAX_TERMS) return fail(TG_E_ARG, "[ring] lincomb: 1..32 terms");
+    if (u32(level) + 1 > TG_LINCOMB_MAX_ROWS) return fail(TG_E_ARG, "[ring] lincomb: too many rows");
+    if (nparts == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    LinComb L{};
+    L.nterms = nterms;
+    L.nparts = nparts;
+    L.rescale = rescale ? 1 : 0;
+    L.add_all = add_all ? 1 : 0;
+    L.level = level;
+    for (u32 t = 0; t < nterms; ++t) {
+        L.ptr[t] = terms[t];
+        L.pstride[t] = part_strides[t];
+        for (int r = 0; r <= level; ++r) {
+            const u64 q = ctx->h_q[r];
+            const u64 v = coeffs[size_t(t) * (level + 1) + r] % q;
+            L.c[t][r] = v;
+            L.cs[t][r] = h_shoup(v, q);
+        }
+    }
+    for (int r = 0; r <= level; ++r) L.add[r] = add_per_row ? add_per_row[r] % ctx->h_q[r] : 0;
+    const double rows = double(level + 1);
+    ProfScope prof(ctx, TG_OP_LINCOMB, 8.0 * nparts * R.N * (rows * nterms + (rescale ? rows - 1 : rows)),
+                   as_stream(stream));
+    k_lincomb<<<grid_for(size_t(nparts) * R.N), kThreads, 0, as_stream(stream)>>>(R, L, out);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
