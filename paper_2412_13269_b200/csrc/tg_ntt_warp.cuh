@@ -20,8 +20,10 @@
 // 8*2^u entries starting at 2^(logN1+u) + 8*bx*2^u, and a column block needs
 // table[1 .. M1).
 
+constexpr u64 kSmallQ = u64(1) << 55;  // lazy-bound threshold of the SQ path
+
 #ifndef NTT_MIN_BLOCKS
-#define NTT_MIN_BLOCKS 6
+#define NTT_MIN_BLOCKS 4
 #endif
 
 template <int E>
@@ -41,19 +43,31 @@ __device__ __forceinline__ u32 wins(u32 lane, u32 j, u32 lo) {
     return ((lane >> lo) << (lo + LOGE)) | (j << lo) | (lane & ((1u << lo) - 1));
 }
 
+// Small-modulus variants (SQ, q < 2^55, i.e. every q-chain prime here):
+// no Harvey corrections inside a phase. Forward: values grow by < 2q per
+// stage, < 33q after both phases (< 2^64). Inverse: with B_p = 2q << p a
+// bound on the inputs of stage p, a+b < 2 B_p and a - b + B_p in (0, 2 B_p);
+// after a phase (<= 8 stages) values are < 512q < 2^64 and are brought back
+// to [0, 2q) once. 60-bit special primes take the corrected path.
+template <bool SQ>
 __device__ __forceinline__ void ct_bfly(u64& a, u64& b, u64 w, u64 ws, u64 q) {
     const u64 q2 = 2 * q;
-    if (a >= q2) a -= q2;
+    if constexpr (!SQ) {
+        if (a >= q2) a -= q2;
+    }
     const u64 t = shoup_lazy(b, w, ws, q);
     b = a - t + q2;
     a = a + t;
 }
 
-__device__ __forceinline__ void gs_bfly(u64& a, u64& b, u64 w, u64 ws, u64 q) {
+template <bool SQ>
+__device__ __forceinline__ void gs_bfly(u64& a, u64& b, u64 w, u64 ws, u64 q, u64 bound) {
     const u64 q2 = 2 * q;
     u64 s = a + b;
-    if (s >= q2) s -= q2;
-    const u64 d = a - b + q2;
+    if constexpr (!SQ) {
+        if (s >= q2) s -= q2;
+    }
+    const u64 d = a - b + (SQ ? bound : q2);
     b = shoup_lazy(d, w, ws, q);
     a = s;
 }
@@ -67,7 +81,7 @@ __device__ __forceinline__ u32 tw_slot(u32 u, u32 c, u32 i) {
 }
 
 // Forward (CT) stages on bits HI..LO (descending) of layout LAY; stage s = LOGM-1-p.
-template <int E, bool CHUNK, int LAY, int HI, int LO>
+template <int E, bool CHUNK, bool SQ, int LAY, int HI, int LO>
 __device__ __forceinline__ void wfwd(u64 (&v)[E], u32 lane, const u64* sw, const u64* sws, u64 q, u32 c) {
     constexpr int LOGE = WGeo<E>::LOGE, LOGM = WGeo<E>::LOGM;
 #pragma unroll
@@ -79,13 +93,13 @@ __device__ __forceinline__ void wfwd(u64 (&v)[E], u32 lane, const u64* sw, const
             const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
             const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
             const ulonglong2 tw = reinterpret_cast<const ulonglong2*>(sw)[t];
-            ct_bfly(v[j], v[j | (1 << b)], tw.x, tw.y, q);
+            ct_bfly<SQ>(v[j], v[j | (1 << b)], tw.x, tw.y, q);
         }
     }
 }
 
 // Inverse (GS) stages on bits LO..HI (ascending) of layout LAY; unit u = LOGM-1-p.
-template <int E, bool CHUNK, int LAY, int LO, int HI>
+template <int E, bool CHUNK, bool SQ, int LAY, int LO, int HI>
 __device__ __forceinline__ void winv(u64 (&v)[E], u32 lane, const u64* sw, const u64* sws, u64 q, u32 c) {
     constexpr int LOGE = WGeo<E>::LOGE, LOGM = WGeo<E>::LOGM;
 #pragma unroll
@@ -97,7 +111,7 @@ __device__ __forceinline__ void winv(u64 (&v)[E], u32 lane, const u64* sw, const
             const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
             const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
             const ulonglong2 tw = reinterpret_cast<const ulonglong2*>(sw)[t];
-            gs_bfly(v[j], v[j | (1 << b)], tw.x, tw.y, q);
+            gs_bfly<SQ>(v[j], v[j | (1 << b)], tw.x, tw.y, q, (2 * q) << p);
         }
     }
 }
@@ -114,42 +128,42 @@ __device__ __forceinline__ void wxchg(u64 (&v)[E], u64* col, u32 lane, u32 lo_fr
 }
 
 // Full forward sub-transform: layout 5 (k = lane + 32 j) -> layout 0.
-template <int E, bool CHUNK>
+template <int E, bool CHUNK, bool SQ>
 __device__ __forceinline__ void wfwd_all(u64 (&v)[E], u64* col, u32 lane, const u64* sw, const u64* sws, u64 q, u32 c) {
     if constexpr (E == 8) {
-        wfwd<8, CHUNK, 5, 7, 5>(v, lane, sw, sws, q, c);
+        wfwd<8, CHUNK, SQ, 5, 7, 5>(v, lane, sw, sws, q, c);
         wxchg<8>(v, col, lane, 5, 2);
-        wfwd<8, CHUNK, 2, 4, 2>(v, lane, sw, sws, q, c);
+        wfwd<8, CHUNK, SQ, 2, 4, 2>(v, lane, sw, sws, q, c);
         wxchg<8>(v, col, lane, 2, 0);
-        wfwd<8, CHUNK, 0, 1, 0>(v, lane, sw, sws, q, c);
+        wfwd<8, CHUNK, SQ, 0, 1, 0>(v, lane, sw, sws, q, c);
     } else {
-        wfwd<4, CHUNK, 5, 6, 5>(v, lane, sw, sws, q, c);
+        wfwd<4, CHUNK, SQ, 5, 6, 5>(v, lane, sw, sws, q, c);
         wxchg<4>(v, col, lane, 5, 3);
-        wfwd<4, CHUNK, 3, 4, 3>(v, lane, sw, sws, q, c);
+        wfwd<4, CHUNK, SQ, 3, 4, 3>(v, lane, sw, sws, q, c);
         wxchg<4>(v, col, lane, 3, 1);
-        wfwd<4, CHUNK, 1, 2, 1>(v, lane, sw, sws, q, c);
+        wfwd<4, CHUNK, SQ, 1, 2, 1>(v, lane, sw, sws, q, c);
         wxchg<4>(v, col, lane, 1, 0);
-        wfwd<4, CHUNK, 0, 0, 0>(v, lane, sw, sws, q, c);
+        wfwd<4, CHUNK, SQ, 0, 0, 0>(v, lane, sw, sws, q, c);
     }
 }
 
 // Full inverse sub-transform: layout 0 -> layout 5.
-template <int E, bool CHUNK>
+template <int E, bool CHUNK, bool SQ>
 __device__ __forceinline__ void winv_all(u64 (&v)[E], u64* col, u32 lane, const u64* sw, const u64* sws, u64 q, u32 c) {
     if constexpr (E == 8) {
-        winv<8, CHUNK, 0, 0, 2>(v, lane, sw, sws, q, c);
+        winv<8, CHUNK, SQ, 0, 0, 2>(v, lane, sw, sws, q, c);
         wxchg<8>(v, col, lane, 0, 3);
-        winv<8, CHUNK, 3, 3, 5>(v, lane, sw, sws, q, c);
+        winv<8, CHUNK, SQ, 3, 3, 5>(v, lane, sw, sws, q, c);
         wxchg<8>(v, col, lane, 3, 5);
-        winv<8, CHUNK, 5, 6, 7>(v, lane, sw, sws, q, c);
+        winv<8, CHUNK, SQ, 5, 6, 7>(v, lane, sw, sws, q, c);
     } else {
-        winv<4, CHUNK, 0, 0, 1>(v, lane, sw, sws, q, c);
+        winv<4, CHUNK, SQ, 0, 0, 1>(v, lane, sw, sws, q, c);
         wxchg<4>(v, col, lane, 0, 2);
-        winv<4, CHUNK, 2, 2, 3>(v, lane, sw, sws, q, c);
+        winv<4, CHUNK, SQ, 2, 2, 3>(v, lane, sw, sws, q, c);
         wxchg<4>(v, col, lane, 2, 4);
-        winv<4, CHUNK, 4, 4, 5>(v, lane, sw, sws, q, c);
+        winv<4, CHUNK, SQ, 4, 4, 5>(v, lane, sw, sws, q, c);
         wxchg<4>(v, col, lane, 4, 5);
-        winv<4, CHUNK, 5, 6, 6>(v, lane, sw, sws, q, c);
+        winv<4, CHUNK, SQ, 5, 6, 6>(v, lane, sw, sws, q, c);
     }
 }
 
@@ -158,13 +172,26 @@ __device__ __forceinline__ void winv_all(u64 (&v)[E], u64* col, u32 lane, const 
 template <int E>
 __device__ __forceinline__ void stage_chunk_twiddles(u64* sw, u64* sws, const u64* __restrict__ w,
                                                      const u64* __restrict__ ws, u32 logN1, u32 bx) {
-    constexpr int LOGM = WGeo<E>::LOGM;
+    // flattened slot e -> (u, t): all of a thread's loads are issued before
+    // any store, so the staging costs one memory latency, not LOGM of them
+    constexpr int TOT = WGeo<E>::TW_CHUNK;
+    constexpr int PER = (TOT + 255) / 256;
+    u64 a[PER], b[PER];
+    u32 d[PER];
 #pragma unroll
-    for (int u = 0; u < LOGM; ++u) {
-        const u32 n = 8u << u, dst = 8 * ((1u << u) - 1), src = (1u << (logN1 + u)) + ((8 * bx) << u);
-        for (u32 t = threadIdx.x; t < n; t += 256)
-            reinterpret_cast<ulonglong2*>(sw)[dst + t] = make_ulonglong2(__ldg(w + src + t), __ldg(ws + src + t));
+    for (int k = 0; k < PER; ++k) {
+        const u32 e = threadIdx.x + 256u * k;
+        d[k] = e;
+        if (e < u32(TOT)) {
+            const u32 u = 31 - __clz((e >> 3) + 1);  // e in [8(2^u - 1), 8(2^(u+1) - 1))
+            const u32 src = (1u << (logN1 + u)) + ((8 * bx) << u) + (e - 8 * ((1u << u) - 1));
+            a[k] = __ldg(w + src);
+            b[k] = __ldg(ws + src);
+        }
     }
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+        if (d[k] < u32(TOT)) reinterpret_cast<ulonglong2*>(sw)[d[k]] = make_ulonglong2(a[k], b[k]);
 }
 
 template <int E>
@@ -210,7 +237,8 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int lev
     u64 v[E];
 #pragma unroll
     for (int j = 0; j < E; ++j) v[j] = col[wpad(lane + 32 * j)];
-    wfwd_all<E, false>(v, col, lane, sw, sws, q, 0);
+    if (q < kSmallQ) wfwd_all<E, false, true>(v, col, lane, sw, sws, q, 0);
+    else wfwd_all<E, false, false>(v, col, lane, sw, sws, q, 0);
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < E; ++j) col[wpad((lane << Gm::LOGE) | j)] = v[j];
@@ -242,14 +270,21 @@ kw_fwd_chunks(DevRing R, u64* data, u32 row_base, u32 rpp, int level, u32 logN1,
     for (int j = 0; j < E; ++j) v[j] = x[lane + 32 * j];
     stage_chunk_twiddles<E>(sw, sws, w, w + N, logN1, blockIdx.x);
     __syncthreads();
-    wfwd_all<E, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
-    const u64 q2 = 2 * q;
+    if (q < kSmallQ) {
+        wfwd_all<E, true, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+        const u64 one = R.one_shoup[mi];
 #pragma unroll
-    for (int j = 0; j < E; ++j) {
-        u64 t = v[j];
-        if (t >= q2) t -= q2;
-        if (t >= q) t -= q;
-        v[j] = t;
+        for (int j = 0; j < E; ++j) v[j] = shoup(v[j], 1, one, q);  // < 33q -> canonical
+    } else {
+        wfwd_all<E, true, false>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+        const u64 q2 = 2 * q;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            u64 t = v[j];
+            if (t >= q2) t -= q2;
+            if (t >= q) t -= q;
+            v[j] = t;
+        }
     }
     ulonglong2* x2 = reinterpret_cast<ulonglong2*>(x + (lane << Gm::LOGE));
 #pragma unroll
@@ -284,7 +319,14 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int l
     }
     stage_chunk_twiddles<E>(sw, sws, w, w + N, logN1, blockIdx.x);
     __syncthreads();
-    winv_all<E, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+    if (q < kSmallQ) {
+        winv_all<E, true, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+        const u64 one = R.one_shoup[mi];
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = shoup_lazy(v[j], 1, one, q);  // < 512q -> [0, 2q)
+    } else {
+        winv_all<E, true, false>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+    }
 #pragma unroll
     for (int j = 0; j < E; ++j) x[lane + 32 * j] = v[j];
 }
@@ -314,7 +356,8 @@ kw_inv_cols(DevRing R, u64* data, u32 row_base, u32 rpp, int level) {
     u64 v[E];
 #pragma unroll
     for (int j = 0; j < E; ++j) v[j] = col[wpad((lane << Gm::LOGE) | j)];
-    winv_all<E, false>(v, col, lane, sw, sws, q, 0);
+    if (q < kSmallQ) winv_all<E, false, true>(v, col, lane, sw, sws, q, 0);
+    else winv_all<E, false, false>(v, col, lane, sw, sws, q, 0);
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = shoup(v[j], ninv, ninv_s, q);

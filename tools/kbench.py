@@ -53,7 +53,19 @@ def main():
         print(name, res[name], flush=True)
 
     G.profile_enable(ring, False)
-    for lvl in (int(x) for x in a.levels.split(",")):
+    if "batch" in a.ops:  # NTT launch cost vs rows: P polys x 21 rows in one launch
+        import numpy as np
+        lvl = ring.max_level()
+        for P in (1, 2, 4, 8, 16, 32):
+            arr = np.random.default_rng(P).integers(0, 1 << 40, size=(P, lvl + 1, spec.N), dtype=np.uint64)
+            ct = G.ciphertext_from_numpy(ring, arr, lvl, G.Form.coeff, 1.0, G.Domain.slots, 0)
+
+            def f():  # fresh exclusively-owned block (no memoised transform), then in-place NTT
+                c = S.ev.mul_scalar(ct, 1.0, 1.0)
+                c.to_eval()
+            timeit(f"scalar+ntt_fwd_batch{P}_rows{P * (lvl + 1)}", f, 16 * P * (lvl + 1) * spec.N)
+            timeit(f"scalar_only_batch{P}", lambda: S.ev.mul_scalar(ct, 1.0, 1.0), 16 * P * (lvl + 1) * spec.N)
+    for lvl in (int(x) for x in a.levels.split(",") if x):
         K = spec.K
         rows = lvl + 1 + K
         p = G.sample_uniform(ring, lvl, K, G.Rng(1))
