@@ -78,6 +78,13 @@ private:
 // Chebyshev ladder evaluation (ckks.hpp:515-579), bit-exact with the reference.
 Ciphertext eval_chebyshev(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
                           const EvalKeys& keys);
+// Baby-step/giant-step Chebyshev evaluation (same level budget as the ladder,
+// ~sqrt(d) + log(d) products). Bit-exact with oracle/bsgs_ref.py, i.e. the
+// same algorithm composed of the reference's Evaluator primitives.
+Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
+                               const EvalKeys& keys);
+// Which Chebyshev evaluator the threshold stages use.
+enum class PolyEval { ladder, bsgs };
 std::vector<double> power_to_chebyshev(const std::vector<double>& pow_coeffs);
 // log2(n) rotate-and-add (ckks.hpp:605-615).
 Ciphertext inner_sum(const Evaluator& ev, const Ciphertext& ct, u32 n, const EvalKeys& keys);
@@ -123,10 +130,14 @@ struct MinimaxResult {
 MinimaxResult remez_minimax(long double gamma, long double upper, u32 degree, u32 max_iters = 64);
 MinimaxChain build_chain(const ThresholdParams& params);
 
+// `mode` picks the stage evaluator: the reference ladder (default, bit-exact
+// with the unmodified reference) or BSGS (bit-exact with oracle/bsgs_ref.py).
 Ciphertext eval_private_threshold(const Evaluator& ev, const Ciphertext& ct_scores, const Ciphertext& ct_t,
-                                  const Ciphertext& ct_norm, const MinimaxChain& chain, const EvalKeys& keys);
+                                  const Ciphertext& ct_norm, const MinimaxChain& chain, const EvalKeys& keys,
+                                  PolyEval mode = PolyEval::ladder);
 Ciphertext eval_private_threshold_plain_norm(const Evaluator& ev, const Ciphertext& ct_scores, const Ciphertext& ct_t,
-                                             double norm, const MinimaxChain& chain, const EvalKeys& keys);
+                                             double norm, const MinimaxChain& chain, const EvalKeys& keys,
+                                             PolyEval mode = PolyEval::ladder);
 
 // Independent ciphertexts through eval_private_threshold_plain_norm
 // concurrently: one host thread + one CUDA stream per ciphertext (up to
@@ -136,6 +147,6 @@ std::vector<Ciphertext> eval_private_threshold_plain_norm_many(const Evaluator& 
                                                                const std::vector<Ciphertext>& scores,
                                                                const Ciphertext& ct_t, double norm,
                                                                const MinimaxChain& chain, const EvalKeys& keys,
-                                                               int max_streams = 8);
+                                                               int max_streams = 8, PolyEval mode = PolyEval::ladder);
 
 }  // namespace tetris_b200

@@ -1,0 +1,134 @@
+"""TEST INFRASTRUCTURE ONLY — the oracle for baby-step/giant-step Chebyshev
+evaluation.
+
+The reference evaluates Chebyshev series with a full T_k ladder
+(eval_chebyshev, ckks.hpp:515-579); BASELINE.json config 3 asks for BSGS.
+There is no reference BSGS to run, so — as SURVEY 8(c) prescribes — the
+oracle is the BSGS algorithm written here ONCE over the shared Python API and
+executed with the compiled, unmodified reference module (oracle/_ref): every
+homomorphic step is a reference primitive (Evaluator::mul_relin, rescale,
+mul_scalar, add_scalar, add; ckks.hpp:201-324). The product's C++
+eval_chebyshev_bsgs performs the identical sequence; tests compare residues
+bit for bit.
+
+Algorithm (depth = ceil(log2 d) + 1, the same level budget as the ladder):
+  b = 2^ceil(log2(d+1)/2) baby steps T_1..T_b and giants T_{b 2^j}, all from
+  the reference's ladder recurrence T_{a+b} = 2 T_a T_b - T_{b-a} (a = k/2);
+  p = q * T_n + r by Chebyshev division at the largest giant n <= deg p:
+      q = [c_n, 2 c_{n+1}, ..., 2 c_m],  r_i = c_i  (i < n),  r_{n-i} -= c_{n+i};
+  blocks of degree < b are the reference's combination step
+      rescale( sum_k mul_scalar(T_k, c_k, q_lvl) + add_scalar(c_0) ).
+"""
+from __future__ import annotations
+
+import math
+
+
+def _trim(c):
+    c = list(c)
+    while len(c) > 1 and c[-1] == 0.0:
+        c.pop()
+    return c
+
+
+def eval_chebyshev_bsgs(T, ev, x, coeffs, keys):
+    c = _trim(coeffs)
+    d = len(c) - 1
+    if d == 0:
+        return ev.add_scalar(ev.mul_scalar(x, 0.0, 1.0), c[0])
+    if x.level() < math.ceil(math.log2(d)) + 1:
+        raise RuntimeError("[ckks] insufficient levels for polynomial evaluation")
+    lb = math.ceil(math.log2(d + 1) / 2)
+    b = 1 << lb
+    cache = {1: x}
+
+    def get(k):  # the reference ladder step (ckks.hpp:532-555)
+        if k in cache:
+            return cache[k]
+        a = k // 2
+        bb = k - a
+        ta, tb = get(a), get(bb)
+        prod = ev.mul_relin(ta, tb, keys)
+        prod.to_coeff()
+        prod.add_inplace(prod)
+        if a == bb:
+            res = ev.rescale(ev.add_scalar(prod, -1.0))
+        else:
+            tc = get(bb - a).copy()
+            tc.to_coeff()
+            if tc.level() > prod.level():
+                tc.drop_to_level(prod.level())
+            tc = ev.mul_scalar(tc, 1.0, prod.scale / tc.scale)
+            prod.sub_inplace(tc)
+            res = ev.rescale(prod)
+        cache[k] = res
+        return res
+
+    def base(cs):  # degree < b: the reference combination step (ckks.hpp:556-578)
+        ks = [k for k in range(1, len(cs)) if cs[k] != 0.0]
+        if not ks:
+            ks_use = [1]
+            cvals = {1: 0.0}
+        else:
+            ks_use = ks
+            cvals = {k: cs[k] for k in ks}
+        for k in ks_use:
+            get(k)
+        lvl = x.level()
+        for k in ks_use:
+            lvl = min(lvl, get(k).level())
+        comb = float(ev.ring().modulus(lvl))
+        acc = None
+        for k in ks_use:
+            term = get(k).copy()
+            term.to_coeff()
+            if term.level() > lvl:
+                term.drop_to_level(lvl)
+            term = ev.mul_scalar(term, cvals[k], comb)
+            if acc is None:
+                acc = term
+            else:
+                acc.add_inplace(term)
+        if cs[0] != 0.0:
+            acc = ev.add_scalar(acc, cs[0])
+        return ev.rescale(acc)
+
+    def rec(cs):
+        cs = _trim(cs)
+        if all(v == 0.0 for v in cs):
+            return None
+        m = len(cs) - 1
+        if m < b:
+            return base(cs)
+        n = b
+        while 2 * n <= m:
+            n *= 2
+        q = [cs[n]] + [2.0 * cs[n + i] for i in range(1, m - n + 1)]
+        r = [cs[i] for i in range(n)]
+        for i in range(1, m - n + 1):
+            r[n - i] = r[n - i] - cs[n + i]
+        Q = rec(q)
+        Rr = rec(r)
+        if Q is None:
+            return Rr
+        P = ev.rescale(ev.mul_relin(Q, get(n), keys))
+        return P if Rr is None else ev.add(P, Rr)
+
+    out = rec(c)
+    if out is None:  # identically zero: a fresh encoding of 0 (as d == 0 does)
+        return ev.add_scalar(ev.mul_scalar(x, 0.0, 1.0), 0.0)
+    return out
+
+
+def threshold_plain_norm_bsgs(T, ev, ct_scores, ct_t, norm, chain, keys):
+    """eval_private_threshold_plain_norm (threshold.hpp:146-157) with every
+    stage evaluated by eval_chebyshev_bsgs."""
+    if ct_scores.level() < chain.levels_required():
+        raise RuntimeError("[threshold] insufficient levels")
+    diff = ev.sub(ct_scores, ct_t)
+    diff = ev.add_scalar(diff, chain.params.epsilon / 2.0)
+    ql = ev.ring().modulus(diff.level())
+    u = ev.rescale(ev.mul_scalar(diff, norm, float(ql)))
+    for i in range(len(chain.stages)):
+        u = eval_chebyshev_bsgs(T, ev, u, chain.eval_coeffs(i), keys)
+    return ev.add_scalar(u, 0.5)

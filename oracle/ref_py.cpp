@@ -228,6 +228,7 @@ PYBIND11_MODULE(tetris_ref, m) {
 
     py::class_<Evaluator>(m, "Evaluator")
         .def(py::init<const KeyContext&>(), py::keep_alive<1, 2>())
+        .def("ring", &Evaluator::ring, py::return_value_policy::reference_internal)
         .def("add", &Evaluator::add)
         .def("sub", &Evaluator::sub)
         .def("mul", &Evaluator::mul)

@@ -1,0 +1,259 @@
+// Chebyshev-series evaluation on the device:
+//  * eval_chebyshev        — the reference's memoised T_k ladder
+//                            (ckks.hpp:515-579), bit-exact with it;
+//  * eval_chebyshev_bsgs   — baby-step/giant-step evaluation (BASELINE.json
+//                            config 3), bit-exact with its oracle
+//                            (oracle/bsgs_ref.py over the reference's own
+//                            Evaluator primitives), same level budget,
+//                            7/11/16 instead of 11/20/47 relinearised products
+//                            for d = 15/27/63.
+// Every ladder step and every combination step runs as ONE fused residue pass
+// (tg_lincomb) after the relinearised product; scales and noise bounds follow
+// the reference's add_inplace / mul_scalar / sub_inplace / add_scalar /
+// rescale sequence exactly.
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <map>
+#include <optional>
+
+#include "internal.hpp"
+#include "tetris_b200/evaluator.hpp"
+
+namespace tetris_b200 {
+
+using detail::fresh_parts;
+
+namespace {
+
+struct LinTerm {
+    const Ciphertext* ct;
+    std::vector<u64> coef;  // one integer per q row 0..level
+};
+
+std::vector<Poly> fused_lincomb(const RingParams& R, const std::vector<LinTerm>& terms,
+                                const std::vector<u64>& add_per_row, int level, bool rescale) {
+    const u32 nt = u32(terms.size());
+    std::vector<const u64*> ptrs(nt);
+    std::vector<u64> strides(nt);
+    std::vector<u64> coeffs(std::size_t(nt) * (level + 1));
+    for (u32 t = 0; t < nt; ++t) {
+        const Ciphertext& c = *terms[t].ct;
+        if (c.parts.size() != 2 || c.form() != Form::coeff || c.level() < level || c.parts[0].nspecial() != 0)
+            throw TetrisError("ckks", "fused combination expects degree-1 coefficient-form terms");
+        ptrs[t] = c.parts[0].data();
+        strides[t] = u64(c.parts[1].data()) / 8 - u64(c.parts[0].data()) / 8;  // words (mod 2^64)
+        for (int r = 0; r <= level; ++r) coeffs[std::size_t(t) * (level + 1) + r] = terms[t].coef[r];
+    }
+    std::vector<Poly> out = fresh_parts(R, 2, rescale ? level - 1 : level, Form::coeff);
+    check_tg(tg_lincomb(R.dev(), const_cast<u64*>(out[0].data()), nt, ptrs.data(), strides.data(), coeffs.data(),
+                        add_per_row.empty() ? nullptr : add_per_row.data(), 0, level, 2, rescale ? 1 : 0,
+                        R.stream()));
+    return out;
+}
+
+std::vector<u64> residues_of(const RingParams& R, i64 v, int level) {
+    std::vector<u64> c(level + 1);
+    for (int r = 0; r <= level; ++r) c[r] = from_centered(v, R.modulus(u32(r)));
+    return c;
+}
+
+// The reference ladder T_k = 2 T_a T_b - T_{b-a}, a = floor(k/2) (ckks.hpp:532-555).
+struct Ladder {
+    const Evaluator& ev;
+    const EvalKeys& keys;
+    const RingParams& R;
+    std::map<std::size_t, Ciphertext> T;
+    Ladder(const Evaluator& e, const Ciphertext& x, const EvalKeys& k) : ev(e), keys(k), R(e.ring()) {
+        T.emplace(1, x);
+    }
+
+    const Ciphertext& get(std::size_t k) {
+        auto hit = T.find(k);
+        if (hit != T.end()) return hit->second;
+        const std::size_t a = k / 2, b = k - a;
+        const Ciphertext& ta = get(a);
+        const Ciphertext& tb = get(b);
+        Ciphertext prod = ev.mul_relin(ta, tb, keys);
+        prod.to_coeff();
+        const int lvl = prod.level();
+        if (lvl == 0) throw TetrisError("ckks", "cannot rescale at level 0");
+        const double two_noise = prod.noise_bound + prod.noise_bound;  // add_inplace(prod)
+        const u64 ql = R.modulus(u32(lvl));
+        Ciphertext res;
+        if (a == b) {  // rescale(add_scalar(2 prod, -1))
+            std::vector<u64> add(lvl + 1);
+            for (int r = 0; r <= lvl; ++r) add[r] = Evaluator::scaled_residue(-1.0 * prod.scale, R.modulus(u32(r)));
+            res.parts = fused_lincomb(R, {LinTerm{&prod, residues_of(R, 2, lvl)}}, add, lvl, true);
+            res.noise_bound = two_noise / double(ql) + 1.0;
+        } else {  // rescale(2 prod - mul_scalar(T_{b-a}, 1, ratio))
+            Ciphertext tc0 = get(b - a);
+            tc0.to_coeff();
+            const double ratio = prod.scale / tc0.scale;
+            if (std::abs(1.0) * ratio >= 9.0e18)
+                throw TetrisError("ckks", "scalar multiplier exceeds the integer range");
+            const i64 v = round_half_away(1.0 * ratio);
+            const double tc_scale = tc0.scale * ratio;
+            Evaluator::check_scales_match(tc_scale, prod.scale);
+            std::vector<u64> negv(lvl + 1);
+            for (int r = 0; r <= lvl; ++r) negv[r] = neg_mod(from_centered(v, R.modulus(u32(r))), R.modulus(u32(r)));
+            res.parts = fused_lincomb(R, {LinTerm{&prod, residues_of(R, 2, lvl)}, LinTerm{&tc0, negv}}, {}, lvl, true);
+            res.noise_bound = (two_noise + tc0.noise_bound) / double(ql) + 1.0;
+        }
+        res.scale = prod.scale / double(ql);
+        res.domain = prod.domain;
+        res.sk_id = prod.sk_id;
+        return T.emplace(k, std::move(res)).first->second;
+    }
+};
+
+// The reference combination step (ckks.hpp:556-578) over ladder terms
+// ks (coefficients cs[k]), at the common level min(x.level, T_k.level):
+// rescale( sum_k mul_scalar(T_k, c_k, q_lvl) + add_scalar(c_0) ).
+Ciphertext combine(Ladder& L, const Ciphertext& x, const std::vector<std::size_t>& ks, const std::vector<double>& cs,
+                   double c0) {
+    const RingParams& R = L.R;
+    int lvl = x.level();
+    for (std::size_t k : ks) lvl = std::min(lvl, L.get(k).level());
+    const double comb_scale = double(R.modulus(u32(lvl)));
+    std::vector<LinTerm> terms;
+    std::vector<Ciphertext> conv;  // coefficient-form copies of eval-form terms (T_1 may be eval)
+    conv.reserve(ks.size());
+    double acc_scale = 0, acc_noise = 0;
+    bool first = true;
+    for (std::size_t k : ks) {
+        const Ciphertext* tk = &L.get(k);
+        if (tk->form() != Form::coeff) {
+            conv.push_back(*tk);
+            conv.back().to_coeff();
+            tk = &conv.back();
+        }
+        const double c = cs[k];
+        if (std::abs(c) * comb_scale >= 9.0e18) throw TetrisError("ckks", "scalar multiplier exceeds the integer range");
+        const double term_scale = tk->scale * comb_scale;
+        if (first) {
+            acc_scale = term_scale;
+            acc_noise = tk->noise_bound;
+            first = false;
+        } else {
+            Evaluator::check_scales_match(acc_scale, term_scale);
+            acc_noise += tk->noise_bound;
+        }
+        terms.push_back(LinTerm{tk, residues_of(R, round_half_away(c * comb_scale), lvl)});
+    }
+    std::vector<u64> add;
+    if (c0 != 0.0) {
+        add.resize(lvl + 1);
+        for (int r = 0; r <= lvl; ++r) add[r] = Evaluator::scaled_residue(c0 * acc_scale, R.modulus(u32(r)));
+    }
+    if (lvl == 0) throw TetrisError("ckks", "cannot rescale at level 0");
+    Ciphertext out;
+    if (terms.size() <= TG_LINCOMB_MAX_TERMS) {
+        out.parts = fused_lincomb(R, terms, add, lvl, true);
+    } else {  // more terms than one pass holds: accumulate in chunks, rescale at the end
+        Ciphertext partial;
+        const std::vector<u64> one = residues_of(R, 1, lvl);
+        const std::size_t step = TG_LINCOMB_MAX_TERMS - 1;
+        for (std::size_t i = 0; i < terms.size(); i += step) {
+            std::vector<LinTerm> chunk;
+            if (i) chunk.push_back(LinTerm{&partial, one});
+            for (std::size_t j = i; j < std::min(terms.size(), i + step); ++j) chunk.push_back(terms[j]);
+            const bool last = i + step >= terms.size();
+            Ciphertext next;
+            next.parts = fused_lincomb(R, chunk, last ? add : std::vector<u64>{}, lvl, last);
+            next.scale = acc_scale;
+            partial = std::move(next);
+        }
+        out.parts = partial.parts;
+    }
+    const u64 ql = R.modulus(u32(lvl));
+    out.scale = acc_scale / double(ql);
+    out.noise_bound = acc_noise / double(ql) + 1.0;
+    out.domain = x.domain;
+    out.sk_id = x.sk_id;
+    return out;
+}
+
+std::vector<double> trimmed(const std::vector<double>& c) {
+    std::vector<double> v = c;
+    while (v.size() > 1 && v.back() == 0.0) v.pop_back();
+    return v;
+}
+
+}  // namespace
+
+Ciphertext eval_chebyshev(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
+                          const EvalKeys& keys) {
+    std::size_t d = cheb_coeffs.size() - 1;
+    while (d > 0 && cheb_coeffs[d] == 0.0) --d;
+    if (d == 0) {
+        Ciphertext out = ev.mul_scalar(x, 0.0, 1.0);
+        return ev.add_scalar(out, cheb_coeffs[0]);
+    }
+    if (x.level() < int(std::ceil(std::log2(double(d)))) + 1)
+        throw TetrisError("ckks", "insufficient levels for polynomial evaluation");
+    Ladder L(ev, x, keys);
+    for (std::size_t k = d; k >= 1; k /= 2) L.get(k);  // warm the ladder top-down
+    std::vector<std::size_t> ks;
+    for (std::size_t k = 1; k <= d; ++k)
+        if (cheb_coeffs[k] != 0.0) {
+            L.get(k);
+            ks.push_back(k);
+        }
+    return combine(L, x, ks, cheb_coeffs, cheb_coeffs[0]);
+}
+
+Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
+                               const EvalKeys& keys) {
+    const std::vector<double> c = trimmed(cheb_coeffs);
+    const std::size_t d = c.size() - 1;
+    if (d == 0) {
+        Ciphertext out = ev.mul_scalar(x, 0.0, 1.0);
+        return ev.add_scalar(out, c[0]);
+    }
+    if (x.level() < int(std::ceil(std::log2(double(d)))) + 1)
+        throw TetrisError("ckks", "insufficient levels for polynomial evaluation");
+    const int lb = int(std::ceil(std::log2(double(d + 1)) / 2.0));
+    const std::size_t b = std::size_t(1) << lb;
+    Ladder L(ev, x, keys);
+
+    auto base = [&](const std::vector<double>& cs) {
+        std::vector<std::size_t> ks;
+        for (std::size_t k = 1; k < cs.size(); ++k)
+            if (cs[k] != 0.0) ks.push_back(k);
+        if (ks.empty()) {  // constant block: carried by 0 * T_1
+            std::vector<double> z = {cs[0], 0.0};
+            for (std::size_t k : {std::size_t(1)}) L.get(k);
+            return combine(L, x, {1}, z, cs[0]);
+        }
+        for (std::size_t k : ks) L.get(k);
+        return combine(L, x, ks, cs, cs[0]);
+    };
+
+    std::function<std::optional<Ciphertext>(std::vector<double>)> rec =
+        [&](std::vector<double> cs) -> std::optional<Ciphertext> {
+        cs = trimmed(cs);
+        bool all_zero = true;
+        for (double v : cs) all_zero &= v == 0.0;
+        if (all_zero) return std::nullopt;
+        const std::size_t m = cs.size() - 1;
+        if (m < b) return base(cs);
+        std::size_t n = b;
+        while (2 * n <= m) n *= 2;
+        std::vector<double> q(m - n + 1), r(cs.begin(), cs.begin() + n);
+        q[0] = cs[n];
+        for (std::size_t i = 1; i <= m - n; ++i) q[i] = 2.0 * cs[n + i];
+        for (std::size_t i = 1; i <= m - n; ++i) r[n - i] = r[n - i] - cs[n + i];
+        std::optional<Ciphertext> Q = rec(q);
+        std::optional<Ciphertext> Rr = rec(r);
+        if (!Q) return Rr;
+        Ciphertext P = ev.rescale(ev.mul_relin(*Q, L.get(n), keys));
+        if (!Rr) return P;
+        return ev.add(P, *Rr);
+    };
+    std::optional<Ciphertext> out = rec(c);
+    if (!out) return ev.add_scalar(ev.mul_scalar(x, 0.0, 1.0), 0.0);
+    return *out;
+}
+
+}  // namespace tetris_b200

@@ -359,160 +359,7 @@ Ciphertext Evaluator::conjugate(const Ciphertext& ct, const EvalKeys& keys) cons
     return ctx_->apply_galois(ct, g, keys.galois_key(g));
 }
 
-// ---------------------------------------------------------------------------
-// Fused residue chains (tg_lincomb): out = [rescale](sum_t c_t * term_t + add)
-// ---------------------------------------------------------------------------
-struct LinTerm {
-    const Ciphertext* ct;
-    std::vector<u64> coef;  // one integer per q row 0..level
-};
-
-static std::vector<Poly> fused_lincomb(const RingParams& R, const std::vector<LinTerm>& terms,
-                                       const std::vector<u64>& add_per_row, int level, bool rescale) {
-    const u32 nt = u32(terms.size());
-    std::vector<const u64*> ptrs(nt);
-    std::vector<u64> strides(nt);
-    std::vector<u64> coeffs(std::size_t(nt) * (level + 1));
-    for (u32 t = 0; t < nt; ++t) {
-        const Ciphertext& c = *terms[t].ct;
-        if (c.parts.size() != 2 || c.form() != Form::coeff || c.level() < level || c.parts[0].nspecial() != 0)
-            throw TetrisError("ckks", "fused combination expects degree-1 coefficient-form terms");
-        ptrs[t] = c.parts[0].data();
-        strides[t] = u64(c.parts[1].data()) / 8 - u64(c.parts[0].data()) / 8;  // words (mod 2^64)
-        for (int r = 0; r <= level; ++r) coeffs[std::size_t(t) * (level + 1) + r] = terms[t].coef[r];
-    }
-    std::vector<Poly> out = fresh_parts(R, 2, rescale ? level - 1 : level, Form::coeff);
-    check_tg(tg_lincomb(R.dev(), const_cast<u64*>(out[0].data()), nt, ptrs.data(), strides.data(), coeffs.data(),
-                        add_per_row.empty() ? nullptr : add_per_row.data(), 0, level, 2, rescale ? 1 : 0,
-                        R.stream()));
-    return out;
-}
-
-static std::vector<u64> residues_of(const RingParams& R, i64 v, int level) {
-    std::vector<u64> c(level + 1);
-    for (int r = 0; r <= level; ++r) c[r] = from_centered(v, R.modulus(u32(r)));
-    return c;
-}
-
-// ---------------------------------------------------------------------------
-// eval_chebyshev (ckks.hpp:515-579): memoised T_k ladder, identical op order.
-// Each ladder step  T_k = rescale(2 T_a T_b - [T_{b-a} * v | 1])  and the
-// final combination run as one fused residue pass after the relinearised
-// product; scales and noise bounds are updated exactly as the reference's
-// add_inplace / mul_scalar / sub_inplace / add_scalar / rescale sequence.
-// ---------------------------------------------------------------------------
-Ciphertext eval_chebyshev(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
-                          const EvalKeys& keys) {
-    const RingParams& R = ev.ring();
-    std::size_t d = cheb_coeffs.size() - 1;
-    while (d > 0 && cheb_coeffs[d] == 0.0) --d;
-    if (d == 0) {
-        Ciphertext out = ev.mul_scalar(x, 0.0, 1.0);
-        return ev.add_scalar(out, cheb_coeffs[0]);
-    }
-    if (x.level() < int(std::ceil(std::log2(double(d)))) + 1)
-        throw TetrisError("ckks", "insufficient levels for polynomial evaluation");
-    std::map<std::size_t, Ciphertext> T;
-    T.emplace(1, x);
-    std::function<const Ciphertext&(std::size_t)> get = [&](std::size_t k) -> const Ciphertext& {
-        auto hit = T.find(k);
-        if (hit != T.end()) return hit->second;
-        const std::size_t a = k / 2, b = k - a;
-        const Ciphertext& ta = get(a);
-        const Ciphertext& tb = get(b);
-        Ciphertext prod = ev.mul_relin(ta, tb, keys);
-        prod.to_coeff();
-        const int lvl = prod.level();
-        if (lvl == 0) throw TetrisError("ckks", "cannot rescale at level 0");
-        const double two_noise = prod.noise_bound + prod.noise_bound;  // add_inplace(prod)
-        const u64 ql = R.modulus(u32(lvl));
-        Ciphertext res;
-        if (a == b) {  // rescale(add_scalar(2 prod, -1))
-            std::vector<u64> add(lvl + 1);
-            for (int r = 0; r <= lvl; ++r) add[r] = Evaluator::scaled_residue(-1.0 * prod.scale, R.modulus(u32(r)));
-            res.parts = fused_lincomb(R, {LinTerm{&prod, residues_of(R, 2, lvl)}}, add, lvl, true);
-            res.noise_bound = two_noise / double(ql) + 1.0;
-        } else {  // rescale(2 prod - mul_scalar(T_{b-a}, 1, ratio))
-            Ciphertext tc0 = get(b - a);
-            tc0.to_coeff();
-            const double ratio = prod.scale / tc0.scale;
-            if (std::abs(1.0) * ratio >= 9.0e18) throw TetrisError("ckks", "scalar multiplier exceeds the integer range");
-            const i64 v = round_half_away(1.0 * ratio);
-            const double tc_scale = tc0.scale * ratio;
-            Evaluator::check_scales_match(tc_scale, prod.scale);
-            std::vector<u64> negv(lvl + 1);
-            for (int r = 0; r <= lvl; ++r) negv[r] = neg_mod(from_centered(v, R.modulus(u32(r))), R.modulus(u32(r)));
-            res.parts = fused_lincomb(R, {LinTerm{&prod, residues_of(R, 2, lvl)}, LinTerm{&tc0, negv}}, {}, lvl, true);
-            res.noise_bound = (two_noise + tc0.noise_bound) / double(ql) + 1.0;
-        }
-        res.scale = prod.scale / double(ql);
-        res.domain = prod.domain;
-        res.sk_id = prod.sk_id;
-        return T.emplace(k, std::move(res)).first->second;
-    };
-    for (std::size_t k = d; k >= 1; k /= 2) get(k);
-    int lvl = x.level();
-    for (std::size_t k = 1; k <= d; ++k)
-        if (cheb_coeffs[k] != 0.0) lvl = std::min(lvl, get(k).level());
-    const double comb_scale = double(R.modulus(u32(lvl)));
-    // combination: sum_k mul_scalar(T_k, c_k, q_lvl) (+ add_scalar(c_0)), rescale
-    std::vector<LinTerm> terms;
-    std::vector<Ciphertext> coeff_form;  // T_k are coefficient form already; keep any converted copies alive
-    coeff_form.reserve(d);
-    double acc_scale = 0, acc_noise = 0;
-    bool first = true;
-    for (std::size_t k = 1; k <= d; ++k) {
-        if (cheb_coeffs[k] == 0.0) continue;
-        const Ciphertext* tk = &get(k);
-        if (tk->form() != Form::coeff) {
-            coeff_form.push_back(*tk);
-            coeff_form.back().to_coeff();
-            tk = &coeff_form.back();
-        }
-        const double c = cheb_coeffs[k];
-        if (std::abs(c) * comb_scale >= 9.0e18) throw TetrisError("ckks", "scalar multiplier exceeds the integer range");
-        const double term_scale = tk->scale * comb_scale;
-        if (first) {
-            acc_scale = term_scale;
-            acc_noise = tk->noise_bound;
-            first = false;
-        } else {
-            Evaluator::check_scales_match(acc_scale, term_scale);
-            acc_noise += tk->noise_bound;
-        }
-        terms.push_back(LinTerm{tk, residues_of(R, round_half_away(c * comb_scale), lvl)});
-    }
-    std::vector<u64> add;
-    if (cheb_coeffs[0] != 0.0) {
-        add.resize(lvl + 1);
-        for (int r = 0; r <= lvl; ++r) add[r] = Evaluator::scaled_residue(cheb_coeffs[0] * acc_scale, R.modulus(u32(r)));
-    }
-    if (lvl == 0) throw TetrisError("ckks", "cannot rescale at level 0");
-    Ciphertext out;
-    if (terms.size() <= TG_LINCOMB_MAX_TERMS) {
-        out.parts = fused_lincomb(R, terms, add, lvl, true);
-    } else {  // more terms than one pass holds: accumulate, then rescale
-        std::vector<LinTerm> chunk;
-        Ciphertext partial;
-        std::vector<u64> one = residues_of(R, 1, lvl);
-        for (std::size_t i = 0; i < terms.size(); i += TG_LINCOMB_MAX_TERMS - 1) {
-            chunk.clear();
-            if (i) chunk.push_back(LinTerm{&partial, one});
-            for (std::size_t j = i; j < std::min(terms.size(), i + TG_LINCOMB_MAX_TERMS - 1); ++j) chunk.push_back(terms[j]);
-            Ciphertext next;
-            const bool last = i + TG_LINCOMB_MAX_TERMS - 1 >= terms.size();
-            next.parts = fused_lincomb(R, chunk, last ? add : std::vector<u64>{}, lvl, last);
-            partial = std::move(next);
-        }
-        out.parts = partial.parts;
-    }
-    const u64 ql = R.modulus(u32(lvl));
-    out.scale = acc_scale / double(ql);
-    out.noise_bound = acc_noise / double(ql) + 1.0;
-    out.domain = x.domain;
-    out.sk_id = x.sk_id;
-    return out;
-}
+// eval_chebyshev / eval_chebyshev_bsgs live in chebyshev.cpp
 
 std::vector<double> power_to_chebyshev(const std::vector<double>& pow_coeffs) {
     const std::size_t d = pow_coeffs.size();

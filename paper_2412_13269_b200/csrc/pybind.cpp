@@ -236,6 +236,7 @@ PYBIND11_MODULE(_tetris_b200, m) {
 
     py::class_<Evaluator>(m, "Evaluator")
         .def(py::init<const KeyContext&>(), py::keep_alive<1, 2>())
+        .def("ring", &Evaluator::ring, py::return_value_policy::reference_internal)
         .def("add", &Evaluator::add, py::keep_alive<0, 1>())
         .def("sub", &Evaluator::sub, py::keep_alive<0, 1>())
         .def("mul", &Evaluator::mul, py::keep_alive<0, 1>())
@@ -249,6 +250,8 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def_static("scaled_residue", &Evaluator::scaled_residue);
 
     m.def("eval_chebyshev", &eval_chebyshev, py::keep_alive<0, 1>());
+    m.def("eval_chebyshev_bsgs", &eval_chebyshev_bsgs, py::keep_alive<0, 1>());
+    py::enum_<PolyEval>(m, "PolyEval").value("ladder", PolyEval::ladder).value("bsgs", PolyEval::bsgs);
     m.def("inner_sum", &inner_sum, py::keep_alive<0, 1>());
     m.def("power_to_chebyshev", &power_to_chebyshev);
 
@@ -279,8 +282,12 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("eval_step", &MinimaxChain::eval_step)
         .def("levels_required", &MinimaxChain::levels_required);
     m.def("build_chain", &build_chain, py::call_guard<py::gil_scoped_release>());
-    m.def("eval_private_threshold", &eval_private_threshold, py::keep_alive<0, 1>());
-    m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm, py::keep_alive<0, 1>());
+    m.def("eval_private_threshold", &eval_private_threshold, py::keep_alive<0, 1>(), py::arg("ev"),
+          py::arg("ct_scores"), py::arg("ct_t"), py::arg("ct_norm"), py::arg("chain"), py::arg("keys"),
+          py::arg("mode") = PolyEval::ladder);
+    m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm, py::keep_alive<0, 1>(),
+          py::arg("ev"), py::arg("ct_scores"), py::arg("ct_t"), py::arg("norm"), py::arg("chain"), py::arg("keys"),
+          py::arg("mode") = PolyEval::ladder);
 
     // ---- kernel timing, end-to-end transfer helpers --------------------------
     m.def("profile_enable", [](const RingParams& r, bool on) { check_tg(tg_profile_enable(r.dev(), on ? 1 : 0)); });
@@ -351,16 +358,18 @@ PYBIND11_MODULE(_tetris_b200, m) {
     // seconds measured after a device synchronize.
     m.def("eval_private_threshold_plain_norm_many", &eval_private_threshold_plain_norm_many,
           py::call_guard<py::gil_scoped_release>(), py::arg("ev"), py::arg("scores"), py::arg("ct_t"),
-          py::arg("norm"), py::arg("chain"), py::arg("keys"), py::arg("max_streams") = 8);
+          py::arg("norm"), py::arg("chain"), py::arg("keys"), py::arg("max_streams") = 8,
+          py::arg("mode") = PolyEval::ladder);
     m.def(
         "threshold_count",
         [](const Evaluator& ev, const std::vector<Ciphertext>& scores, const Ciphertext& ct_t, double norm,
-           const MinimaxChain& chain, const EvalKeys& keys, u32 slots, bool do_inner_sum, int streams) {
+           const MinimaxChain& chain, const EvalKeys& keys, u32 slots, bool do_inner_sum, int streams,
+           PolyEval mode) {
             py::gil_scoped_release nogil;
             auto t0 = std::chrono::steady_clock::now();
             Ciphertext acc;
             std::vector<Ciphertext> outs =
-                eval_private_threshold_plain_norm_many(ev, scores, ct_t, norm, chain, keys, streams);
+                eval_private_threshold_plain_norm_many(ev, scores, ct_t, norm, chain, keys, streams, mode);
             for (std::size_t i = 0; i < outs.size(); ++i) acc = i == 0 ? outs[i] : ev.add(acc, outs[i]);
             if (do_inner_sum) acc = inner_sum(ev, acc, slots, keys);
             ev.ring().synchronize();
@@ -368,5 +377,5 @@ PYBIND11_MODULE(_tetris_b200, m) {
             return std::make_pair(acc, s);
         },
         py::arg("ev"), py::arg("scores"), py::arg("ct_t"), py::arg("norm"), py::arg("chain"), py::arg("keys"),
-        py::arg("slots"), py::arg("do_inner_sum") = true, py::arg("streams") = 8);
+        py::arg("slots"), py::arg("do_inner_sum") = true, py::arg("streams") = 8, py::arg("mode") = PolyEval::ladder);
 }
