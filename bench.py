@@ -163,7 +163,10 @@ def run_b200(args):
     S = W.make_context(G, spec, rotations=rot)
     chain = W.config3_chain(G, spec)
     scores, thr, _, _ = W.linear_scores(spec)
-    mine = [b for b in range(spec.n_cts) if b % world == rank]
+    from paper_2412_13269_b200 import distributed as D
+
+    mine = D.shard(spec.n_cts, world, rank)
+    D.check_exact(world, S.primes)
     cts, ct_t, _, _ = W.config3_inputs(S, ct_indices=mine, scores=scores, t=thr)
     S.ring.synchronize()
     log(f"[rank {rank}] setup {time.time() - t0:.1f}s: N={spec.N} L={spec.nq - 1} K={spec.K} cts={mine}")
@@ -171,12 +174,13 @@ def run_b200(args):
     ext = torch.cuda.ExternalStream(S.ring.stream_handle(), device=torch.device("cuda", local))
     flush = torch.empty(64 << 22, dtype=torch.int32, device="cuda")  # 1 GiB > 126 MB L2
 
-    def query(local_cts, t_ct):
+    def query(local_cts, t_ct, streams=None):
+        streams = streams or args.streams
         # per-ciphertext thresholds run concurrently (one host thread + CUDA
         # stream each); outputs are summed in index order on the main stream
         acc = None
         outs = G.eval_private_threshold_plain_norm_many(S.ev, local_cts, t_ct, spec.norm, chain, S.keys,
-                                                        args.streams, mode) if local_cts else []
+                                                        streams, mode) if local_cts else []
         for o in outs:
             acc = o if acc is None else S.ev.add(acc, o)
         if acc is None:  # rank without ciphertexts contributes zero
@@ -228,7 +232,9 @@ def run_b200(args):
     # profiled replay of the same steps: per-kernel-class CUDA-event times
     G.profile_enable(S.ring, True)
     barrier()
-    _, _ = timed(lambda: query(cts, ct_t), args.steps)
+    # one stream here, so every kernel's event-bracketed duration is its own
+    # (concurrent streams would time-share the SMs inside the brackets)
+    _, _ = timed(lambda: query(cts, ct_t, streams=1), args.steps)
     prof = G.profile_read(S.ring)
     G.profile_enable(S.ring, False)
 
