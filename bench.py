@@ -217,9 +217,14 @@ def run_b200(args):
         res = query(cts, ct_t)
     barrier()
     # timed region (device-resident inputs)
+    prof_region = os.environ.get("TG_PROFILE_REGION") == "1"  # ncu --profile-from-start off
     with ClockSampler(local) as clocks:
         barrier()
+        if prof_region:
+            torch.cuda.cudart().cudaProfilerStart()
         ms_list, res = timed(lambda: query(cts, ct_t), args.steps)
+        if prof_region:
+            torch.cuda.cudart().cudaProfilerStop()
         barrier()
     ms_step = sum(ms_list) / len(ms_list)
     if world > 1:
