@@ -124,6 +124,39 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
         delete ctx;
         return cuda_fail(e, "cudaMemcpy(tables)");
     }
+    // FP64 NTT tables: w, fl(w/q), winv, fl(winv/q) per modulus (exact w as a
+    // double when q < 2^50.5, the only moduli that take the FP64 path) and
+    // q, fl(1/q), n_inv, fl(n_inv/q).
+    {
+        const size_t nt = size_t(4) * nmod * degree, nq4 = size_t(4) * nmod;
+        std::vector<double> fp(nt + nq4);
+        for (u32 i = 0; i < nmod; ++i) {
+            const double qd = double(moduli[i]);
+            const u64* t = tables + size_t(4) * i * degree;
+            double* o = fp.data() + size_t(4) * i * degree;
+            for (u32 j = 0; j < degree; ++j) {
+                o[j] = double(t[j]);
+                o[degree + j] = double(t[j]) / qd;
+                o[2 * size_t(degree) + j] = double(t[2 * size_t(degree) + j]);
+                o[3 * size_t(degree) + j] = double(t[2 * size_t(degree) + j]) / qd;
+            }
+            double* s = fp.data() + nt + 4 * size_t(i);
+            s[0] = qd;
+            s[1] = 1.0 / qd;
+            s[2] = double(n_inv[2 * i]);
+            s[3] = double(n_inv[2 * i]) / qd;
+        }
+        e = cudaMalloc(&ctx->dev_fp, fp.size() * sizeof(double));
+        if (e == cudaSuccess) e = cudaMemcpy(ctx->dev_fp, fp.data(), fp.size() * sizeof(double), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(ctx->dev_block);
+            if (ctx->dev_fp) cudaFree(ctx->dev_fp);
+            delete ctx;
+            return cuda_fail(e, "cudaMemcpy(fp tables)");
+        }
+        R.twd = static_cast<const double*>(ctx->dev_fp);
+        R.qd = R.twd + nt;
+    }
     // stream-ordered pool: keep freed blocks cached (no release back to the OS)
     cudaDeviceGetDefaultMemPool(&ctx->pool, device);
     uint64_t threshold = UINT64_MAX;
@@ -142,6 +175,7 @@ extern "C" void tg_context_destroy(tg_context* ctx) {
     }
     for (auto e : ctx->prof_free) cudaEventDestroy(e);
     cudaFree(ctx->dev_block);
+    if (ctx->dev_fp) cudaFree(ctx->dev_fp);
     delete ctx;
 }
 

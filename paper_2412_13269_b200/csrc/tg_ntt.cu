@@ -14,6 +14,7 @@
 // Harvey-lazy: values live in [0,4q) (forward) / [0,2q) (inverse) and are
 // made canonical only at the end of the last phase.
 #include "tg_internal.cuh"
+#include "tg_fp64.cuh"
 
 namespace tg {
 

@@ -116,15 +116,102 @@ __device__ __forceinline__ void winv(u64 (&v)[E], u32 lane, const u64* sw, const
     }
 }
 
-template <int E>
-__device__ __forceinline__ void wxchg(u64 (&v)[E], u64* col, u32 lane, u32 lo_from, u32 lo_to) {
+template <int E, class T>
+__device__ __forceinline__ void wxchg(T (&v)[E], u64* colw, u32 lane, u32 lo_from, u32 lo_to) {
     constexpr int LOGE = WGeo<E>::LOGE;
+    T* col = reinterpret_cast<T*>(colw);
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < E; ++j) col[wpad(wins<LOGE>(lane, u32(j), lo_from))] = v[j];
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < E; ++j) v[j] = col[wpad(wins<LOGE>(lane, u32(j), lo_to))];
+}
+
+// ---- FP64 path (q < 2^50.5; tg_fp64.cuh) ---------------------------------
+// Staged twiddle pairs are (w, fl(w/q)) doubles. Forward blocks hold at most
+// 3 stages: from |v| <= q each stage adds |t| <= 1.5q, so |v| <= 5.5q < 2^53,
+// then every value is reduced to |v| <= q/2 + 1. Inverse butterflies reduce
+// a+b every stage (|a|,|b| <= 1.5q => |a-b| <= 3q, |a+b| reduced).
+template <int E, bool CHUNK, int LAY, int HI, int LO>
+__device__ __forceinline__ void wfwd_fp(double (&v)[E], u32 lane, const u64* sw, double q, double qi, u32 c) {
+    constexpr int LOGE = WGeo<E>::LOGE, LOGM = WGeo<E>::LOGM;
+#pragma unroll
+    for (int p = HI; p >= LO; --p) {
+        const int b = p - LAY;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            if (j & (1 << b)) continue;
+            const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
+            const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
+            const double2 tw = reinterpret_cast<const double2*>(sw)[t];
+            const double x = fp_mulmod(v[j | (1 << b)], tw.x, tw.y, q);
+            const double a = v[j];
+            v[j] = __dadd_rn(a, x);
+            v[j | (1 << b)] = __dsub_rn(a, x);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = fp_reduce(v[j], q, qi);
+}
+
+template <int E, bool CHUNK, int LAY, int LO, int HI>
+__device__ __forceinline__ void winv_fp(double (&v)[E], u32 lane, const u64* sw, double q, double qi, u32 c) {
+    constexpr int LOGE = WGeo<E>::LOGE, LOGM = WGeo<E>::LOGM;
+#pragma unroll
+    for (int p = LO; p <= HI; ++p) {
+        const int b = p - LAY;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            if (j & (1 << b)) continue;
+            const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
+            const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
+            const double2 tw = reinterpret_cast<const double2*>(sw)[t];
+            const double a = v[j], bb = v[j | (1 << b)];
+            v[j] = fp_reduce(__dadd_rn(a, bb), q, qi);
+            v[j | (1 << b)] = fp_mulmod(__dsub_rn(a, bb), tw.x, tw.y, q);
+        }
+    }
+}
+
+template <int E, bool CHUNK>
+__device__ __forceinline__ void wfwd_all_fp(double (&v)[E], u64* col, u32 lane, const u64* sw, double q, double qi,
+                                            u32 c) {
+    if constexpr (E == 8) {
+        wfwd_fp<8, CHUNK, 5, 7, 5>(v, lane, sw, q, qi, c);
+        wxchg<8>(v, col, lane, 5, 2);
+        wfwd_fp<8, CHUNK, 2, 4, 2>(v, lane, sw, q, qi, c);
+        wxchg<8>(v, col, lane, 2, 0);
+        wfwd_fp<8, CHUNK, 0, 1, 0>(v, lane, sw, q, qi, c);
+    } else {
+        wfwd_fp<4, CHUNK, 5, 6, 5>(v, lane, sw, q, qi, c);
+        wxchg<4>(v, col, lane, 5, 3);
+        wfwd_fp<4, CHUNK, 3, 4, 3>(v, lane, sw, q, qi, c);
+        wxchg<4>(v, col, lane, 3, 1);
+        wfwd_fp<4, CHUNK, 1, 2, 1>(v, lane, sw, q, qi, c);
+        wxchg<4>(v, col, lane, 1, 0);
+        wfwd_fp<4, CHUNK, 0, 0, 0>(v, lane, sw, q, qi, c);
+    }
+}
+
+template <int E, bool CHUNK>
+__device__ __forceinline__ void winv_all_fp(double (&v)[E], u64* col, u32 lane, const u64* sw, double q, double qi,
+                                            u32 c) {
+    if constexpr (E == 8) {
+        winv_fp<8, CHUNK, 0, 0, 2>(v, lane, sw, q, qi, c);
+        wxchg<8>(v, col, lane, 0, 3);
+        winv_fp<8, CHUNK, 3, 3, 5>(v, lane, sw, q, qi, c);
+        wxchg<8>(v, col, lane, 3, 5);
+        winv_fp<8, CHUNK, 5, 6, 7>(v, lane, sw, q, qi, c);
+    } else {
+        winv_fp<4, CHUNK, 0, 0, 1>(v, lane, sw, q, qi, c);
+        wxchg<4>(v, col, lane, 0, 2);
+        winv_fp<4, CHUNK, 2, 2, 3>(v, lane, sw, q, qi, c);
+        wxchg<4>(v, col, lane, 2, 4);
+        winv_fp<4, CHUNK, 4, 4, 5>(v, lane, sw, q, qi, c);
+        wxchg<4>(v, col, lane, 4, 5);
+        winv_fp<4, CHUNK, 5, 6, 6>(v, lane, sw, q, qi, c);
+    }
 }
 
 // Full forward sub-transform: layout 5 (k = lane + 32 j) -> layout 0.
@@ -224,7 +311,8 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int lev
     const u32 row = row_base + blockIdx.y;
     const u32 mi = mod_index(row % rpp, level, R.q_count);
     const u64 q = R.q[mi];
-    const u64* w = R.tw + size_t(mi) * 4 * N;
+    const bool fp = q < kFpMaxQ;  // FP64 path; the phase-2 kernel makes the same choice
+    const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N) : R.tw + size_t(mi) * 4 * N;
     const u32 c0 = blockIdx.x * 8;
     const u64* xs = src + size_t(row) * N + c0;
     u64* xd = data + size_t(row) * N + c0;
@@ -234,14 +322,26 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int lev
     __syncthreads();
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     u64* col = sm + warp * Gm::CS;
-    u64 v[E];
+    if (fp) {  // canonical u64 in, doubles (|v| <= q/2 + 1, raw bits) out to phase 2
+        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+        double v[E];
 #pragma unroll
-    for (int j = 0; j < E; ++j) v[j] = col[wpad(lane + 32 * j)];
-    if (q < kSmallQ) wfwd_all<E, false, true>(v, col, lane, sw, sws, q, 0);
-    else wfwd_all<E, false, false>(v, col, lane, sw, sws, q, 0);
-    __syncwarp();
+        for (int j = 0; j < E; ++j) v[j] = u2d(col[wpad(lane + 32 * j)]);
+        wfwd_all_fp<E, false>(v, col, lane, sw, qd, qi, 0);
+        __syncwarp();
+        double* cold = reinterpret_cast<double*>(col);
 #pragma unroll
-    for (int j = 0; j < E; ++j) col[wpad((lane << Gm::LOGE) | j)] = v[j];
+        for (int j = 0; j < E; ++j) cold[wpad((lane << Gm::LOGE) | j)] = v[j];
+    } else {
+        u64 v[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = col[wpad(lane + 32 * j)];
+        if (q < kSmallQ) wfwd_all<E, false, true>(v, col, lane, sw, sws, q, 0);
+        else wfwd_all<E, false, false>(v, col, lane, sw, sws, q, 0);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < E; ++j) col[wpad((lane << Gm::LOGE) | j)] = v[j];
+    }
     __syncthreads();
     for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
         xd[size_t(e >> 3) * N2 + (e & 7)] = sm[(e & 7) * Gm::CS + wpad(e >> 3)];
@@ -261,7 +361,8 @@ kw_fwd_chunks(DevRing R, u64* data, u32 row_base, u32 rpp, int level, u32 logN1,
     const u32 row = row_base + blockIdx.y;
     const u32 mi = mod_index(row % rpp, level, R.q_count);
     const u64 q = R.q[mi];
-    const u64* w = R.tw + size_t(mi) * 4 * N;
+    const bool fp = q < kFpMaxQ;
+    const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N) : R.tw + size_t(mi) * 4 * N;
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const u32 chunk = blockIdx.x * 8 + warp;
     u64* x = data + size_t(row) * N + size_t(chunk) * Gm::M;
@@ -270,7 +371,15 @@ kw_fwd_chunks(DevRing R, u64* data, u32 row_base, u32 rpp, int level, u32 logN1,
     for (int j = 0; j < E; ++j) v[j] = x[lane + 32 * j];
     stage_chunk_twiddles<E>(sw, sws, w, w + N, logN1, blockIdx.x);
     __syncthreads();
-    if (q < kSmallQ) {
+    if (fp) {  // phase-1 doubles in, canonical u64 out
+        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+        double vd[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) vd[j] = __longlong_as_double(static_cast<long long>(v[j]));
+        wfwd_all_fp<E, true>(vd, sm + warp * Gm::CS, lane, sw, qd, qi, warp);
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = fp_canonical(vd[j], qd);
+    } else if (q < kSmallQ) {
         wfwd_all<E, true, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
         const u64 one = R.one_shoup[mi];
 #pragma unroll
@@ -304,7 +413,9 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int l
     const u32 row = row_base + blockIdx.y;
     const u32 mi = mod_index(row % rpp, level, R.q_count);
     const u64 q = R.q[mi];
-    const u64* w = R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
+    const bool fp = q < kFpMaxQ;
+    const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N + 2 * size_t(N))
+                      : R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const u32 chunk = blockIdx.x * 8 + warp;
     const ulonglong2* xs2 =
@@ -319,7 +430,15 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int l
     }
     stage_chunk_twiddles<E>(sw, sws, w, w + N, logN1, blockIdx.x);
     __syncthreads();
-    if (q < kSmallQ) {
+    if (fp) {  // canonical u64 in, doubles (|v| <= 1.5q, raw bits) out to phase B
+        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+        double vd[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) vd[j] = u2d(v[j]);
+        winv_all_fp<E, true>(vd, sm + warp * Gm::CS, lane, sw, qd, qi, warp);
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = static_cast<u64>(__double_as_longlong(vd[j]));
+    } else if (q < kSmallQ) {
         winv_all<E, true, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
         const u64 one = R.one_shoup[mi];
 #pragma unroll
@@ -344,7 +463,9 @@ kw_inv_cols(DevRing R, u64* data, u32 row_base, u32 rpp, int level) {
     const u32 row = row_base + blockIdx.y;
     const u32 mi = mod_index(row % rpp, level, R.q_count);
     const u64 q = R.q[mi];
-    const u64* w = R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
+    const bool fp = q < kFpMaxQ;
+    const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N + 2 * size_t(N))
+                      : R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
     const u64 ninv = R.ninv[2 * mi], ninv_s = R.ninv[2 * mi + 1];
     u64* x = data + size_t(row) * N + blockIdx.x * 8;
     for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
@@ -353,14 +474,26 @@ kw_inv_cols(DevRing R, u64* data, u32 row_base, u32 rpp, int level) {
     __syncthreads();
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     u64* col = sm + warp * Gm::CS;
-    u64 v[E];
+    if (fp) {  // phase-A doubles in, canonical u64 out (N^-1 applied in FP64)
+        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1], nd = R.qd[4 * mi + 2], ndq = R.qd[4 * mi + 3];
+        const double* cold = reinterpret_cast<const double*>(col);
+        double v[E];
 #pragma unroll
-    for (int j = 0; j < E; ++j) v[j] = col[wpad((lane << Gm::LOGE) | j)];
-    if (q < kSmallQ) winv_all<E, false, true>(v, col, lane, sw, sws, q, 0);
-    else winv_all<E, false, false>(v, col, lane, sw, sws, q, 0);
-    __syncwarp();
+        for (int j = 0; j < E; ++j) v[j] = cold[wpad((lane << Gm::LOGE) | j)];
+        winv_all_fp<E, false>(v, col, lane, sw, qd, qi, 0);
+        __syncwarp();
 #pragma unroll
-    for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = shoup(v[j], ninv, ninv_s, q);
+        for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canonical(fp_mulmod(v[j], nd, ndq, qd), qd);
+    } else {
+        u64 v[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = col[wpad((lane << Gm::LOGE) | j)];
+        if (q < kSmallQ) winv_all<E, false, true>(v, col, lane, sw, sws, q, 0);
+        else winv_all<E, false, false>(v, col, lane, sw, sws, q, 0);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = shoup(v[j], ninv, ninv_s, q);
+    }
     __syncthreads();
     for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
         x[size_t(e >> 3) * N2 + (e & 7)] = sm[(e & 7) * Gm::CS + wpad(e >> 3)];
