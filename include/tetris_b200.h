@@ -105,6 +105,7 @@ enum {
     TG_OP_MOD_DOWN,
     TG_OP_REDUCE,
     TG_OP_LINCOMB,
+    TG_OP_ENCODE,
     TG_OP_COUNT
 };
 int tg_profile_enable(tg_context* ctx, int on);
@@ -186,6 +187,21 @@ int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const u
  * (modulus index m) times plain row m; plain holds >= level+1 rows. */
 int tg_mul_plain(tg_context* ctx, uint64_t* out, const uint64_t* ct_part, const uint64_t* plain,
                  int level, uint32_t nparts, void* stream);
+
+/* ---- slot encoder ------------------------------------------------------- */
+/* Encoder::encode_slots (ckks.hpp:59-86) for `batch` slot vectors of n slots:
+ * the reference's O(n^2) inverse DFT replayed per output in the same
+ * sequential order and IEEE operations, round_half_away(w * scale) and
+ * from_centered per row, so residues are bit-identical to the reference.
+ * v: [batch][n] complex as (re, im) doubles; psi: [4n] complex table of the
+ * reference encoder (ckks.hpp:28-34, host-computed); rot5: [n] powers of 5
+ * mod 4n (ckks.hpp:35-40); all device pointers. out: [batch][level+1][N]
+ * coeff-form rows (fully written). max_abs_bits (device u64, may be NULL)
+ * receives max(|Re w|, |Im w|) as double bits via atomicMax (must be zeroed
+ * by the caller), for check_encoding_bound (ckks.hpp:137-142). */
+int tg_encode_slots(tg_context* ctx, uint64_t* out, const double* v, uint32_t batch, uint32_t n,
+                    const double* psi, const uint32_t* rot5, double scale, int level,
+                    uint64_t* max_abs_bits, void* stream);
 
 /* ---- key switching ------------------------------------------------------ */
 /* GadgetPlan (rlwe.hpp:28-206) for this ring: RNS digit groups of group_size

@@ -26,7 +26,10 @@ public:
     u32 slots() const { return n_; }
     std::vector<cplx> dft(const std::vector<cplx>& w) const;
     std::vector<cplx> dft_inv(const std::vector<cplx>& v) const;
+    // on the device (tg_encode_slots), bit-identical to the reference's host DFT
     Poly encode_slots(const std::vector<cplx>& v, double scale, int level) const;
+    // several slot vectors in one launch; the polys share one HBM block
+    std::vector<Poly> encode_slots_many(const std::vector<std::vector<cplx>>& vs, double scale, int level) const;
     std::vector<cplx> decode_slots(const Poly& poly, double scale) const;
     Poly encode_coeffs(const std::vector<double>& v, double scale, int level) const;
     std::vector<double> decode_coeffs(const Poly& poly, double scale, std::size_t count) const;
@@ -39,6 +42,10 @@ private:
     u32 n_;
     std::vector<cplx> psi_;
     std::vector<u32> rot5_;
+    // device copies of psi_ ([4n] complex) and rot5_ ([n] u32), uploaded once
+    const DeviceBuffer& device_tables() const;
+    mutable std::shared_ptr<DeviceBuffer> dtab_;
+    std::shared_ptr<std::mutex> dtab_mu_ = std::make_shared<std::mutex>();
 };
 
 struct EvalKeys {

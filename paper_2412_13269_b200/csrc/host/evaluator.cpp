@@ -103,9 +103,56 @@ std::vector<u64> Encoder::encode_slots_host(const std::vector<cplx>& v, double s
     return res;
 }
 
+const DeviceBuffer& Encoder::device_tables() const {
+    std::lock_guard<std::mutex> g(*dtab_mu_);
+    if (!dtab_) {
+        static_assert(sizeof(cplx) == 16, "std::complex<double> layout");
+        const std::size_t psi_words = 2 * psi_.size(), rot_words = (rot5_.size() + 1) / 2;
+        auto buf = std::make_shared<DeviceBuffer>(*ring_, psi_words + rot_words);
+        tg_context* c = ring_->dev();
+        check_tg(tg_memcpy_h2d(c, buf->data(), psi_.data(), psi_words * 8, ring_->stream()));
+        check_tg(tg_memcpy_h2d(c, buf->data() + psi_words, rot5_.data(), rot5_.size() * 4, ring_->stream()));
+        ring_->synchronize();  // the tables are read from every stream afterwards
+        dtab_ = std::move(buf);
+    }
+    return *dtab_;
+}
+
+std::vector<Poly> Encoder::encode_slots_many(const std::vector<std::vector<cplx>>& vs, double scale,
+                                             int level) const {
+    if (level < 0 || level > ring_->max_level()) throw TetrisError("ring", "poly level out of range");
+    for (const auto& v : vs)
+        if (v.size() != n_) throw TetrisError("ckks", "slot vector length mismatch");
+    if (vs.empty()) return {};
+    const DeviceBuffer& tab = device_tables();
+    const std::size_t B = vs.size(), vw = 2 * std::size_t(n_);
+    std::vector<double> h(B * vw + 1, 0.0);  // slot vectors + the bound word (zero)
+    for (std::size_t b = 0; b < B; ++b) std::memcpy(h.data() + b * vw, vs[b].data(), vw * 8);
+    DeviceBuffer in(*ring_, h.size());
+    tg_context* c = ring_->dev();
+    void* s = ring_->stream();
+    check_tg(tg_memcpy_h2d(c, in.data(), h.data(), h.size() * 8, s));
+    std::vector<Poly> out = detail::fresh_parts(*ring_, int(B), level, Form::coeff);
+    u64* bound = level == 0 ? in.data() + B * vw : nullptr;
+    check_tg(tg_encode_slots(c, const_cast<u64*>(out[0].data()), reinterpret_cast<const double*>(in.data()), u32(B),
+                             n_, reinterpret_cast<const double*>(tab.data()),
+                             reinterpret_cast<const u32*>(tab.data() + 2 * psi_.size()), scale, level, bound, s));
+    if (bound) {  // check_encoding_bound (ckks.hpp:137-142)
+        u64 bits = 0;
+        check_tg(tg_memcpy_d2h(c, &bits, bound, 8, s));
+        ring_->synchronize();
+        double b;
+        std::memcpy(&b, &bits, 8);
+        if (b * scale * 2 >= double(ring_->modulus(0)))
+            throw TetrisError("ckks", "plaintext overflows the level-0 modulus");
+    }
+    return out;
+}
+
 Poly Encoder::encode_slots(const std::vector<cplx>& v, double scale, int level) const {
     if (level < 0 || level > ring_->max_level()) throw TetrisError("ring", "poly level out of range");
-    return Poly::from_host(*ring_, encode_slots_host(v, scale, level), level, Form::coeff);
+    if (v.size() != n_) throw TetrisError("ckks", "slot vector length mismatch");
+    return encode_slots_many({v}, scale, level)[0];
 }
 
 // Exact centered value from rows 0 and 1 (ckks.hpp:123-134).

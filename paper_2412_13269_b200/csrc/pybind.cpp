@@ -220,6 +220,15 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def(py::init<const RingParams&, u32>(), py::keep_alive<1, 2>())
         .def("slots", &Encoder::slots)
         .def("encode_slots", &Encoder::encode_slots, py::keep_alive<0, 1>())
+        .def("encode_slots_many",
+             [](const Encoder& e, py::array_t<cplx, py::array::c_style | py::array::forcecast> a, double scale,
+                int level) {
+                 if (a.ndim() != 2) throw TetrisError("ckks", "encode_slots_many expects a [batch][slots] array");
+                 std::vector<std::vector<cplx>> vs(a.shape(0));
+                 for (py::ssize_t b = 0; b < a.shape(0); ++b) vs[b].assign(a.data(b, 0), a.data(b, 0) + a.shape(1));
+                 py::gil_scoped_release nogil;
+                 return e.encode_slots_many(vs, scale, level);
+             })
         .def("decode_slots", &Encoder::decode_slots, py::call_guard<py::gil_scoped_release>())
         .def("encode_coeffs", &Encoder::encode_coeffs)
         .def("decode_coeffs", &Encoder::decode_coeffs)

@@ -266,7 +266,7 @@ extern "C" int tg_profile_read(tg_context* ctx, double* ms, uint64_t* launches, 
 extern "C" const char* tg_profile_op_name(int op) {
     static const char* names[TG_OP_COUNT] = {"ntt_fwd", "ntt_inv",  "addsub", "mul_pointwise", "mul_scalar",
                                              "automorphism", "rescale", "tensor", "mul_plain", "modup_baseconv",
-                                             "key_inner", "mod_down", "reduce", "lincomb"};
+                                             "key_inner", "mod_down", "reduce", "lincomb", "encode"};
     return op >= 0 && op < TG_OP_COUNT ? names[op] : "?";
 }
 
