@@ -246,22 +246,22 @@ PYBIND11_MODULE(_tetris_b200, m) {
     py::class_<Evaluator>(m, "Evaluator")
         .def(py::init<const KeyContext&>(), py::keep_alive<1, 2>())
         .def("ring", &Evaluator::ring, py::return_value_policy::reference_internal)
-        .def("add", &Evaluator::add, py::keep_alive<0, 1>())
-        .def("sub", &Evaluator::sub, py::keep_alive<0, 1>())
-        .def("mul", &Evaluator::mul, py::keep_alive<0, 1>())
-        .def("mul_relin", &Evaluator::mul_relin, py::keep_alive<0, 1>())
-        .def("mul_plain", &Evaluator::mul_plain, py::keep_alive<0, 1>())
-        .def("mul_scalar", &Evaluator::mul_scalar, py::keep_alive<0, 1>())
-        .def("add_scalar", &Evaluator::add_scalar, py::keep_alive<0, 1>())
-        .def("rescale", &Evaluator::rescale, py::keep_alive<0, 1>())
-        .def("rotate", &Evaluator::rotate, py::keep_alive<0, 1>())
-        .def("conjugate", &Evaluator::conjugate, py::keep_alive<0, 1>())
+        .def("add", &Evaluator::add, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("sub", &Evaluator::sub, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("mul", &Evaluator::mul, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("mul_relin", &Evaluator::mul_relin, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("mul_plain", &Evaluator::mul_plain, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("mul_scalar", &Evaluator::mul_scalar, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("add_scalar", &Evaluator::add_scalar, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("rescale", &Evaluator::rescale, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("rotate", &Evaluator::rotate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("conjugate", &Evaluator::conjugate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def_static("scaled_residue", &Evaluator::scaled_residue);
 
-    m.def("eval_chebyshev", &eval_chebyshev, py::keep_alive<0, 1>());
-    m.def("eval_chebyshev_bsgs", &eval_chebyshev_bsgs, py::keep_alive<0, 1>());
+    m.def("eval_chebyshev", &eval_chebyshev, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>());
+    m.def("eval_chebyshev_bsgs", &eval_chebyshev_bsgs, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>());
     py::enum_<PolyEval>(m, "PolyEval").value("ladder", PolyEval::ladder).value("bsgs", PolyEval::bsgs);
-    m.def("inner_sum", &inner_sum, py::keep_alive<0, 1>());
+    m.def("inner_sum", &inner_sum, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>());
     m.def("power_to_chebyshev", &power_to_chebyshev);
 
     py::class_<ThresholdParams>(m, "ThresholdParams")
@@ -291,12 +291,33 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("eval_step", &MinimaxChain::eval_step)
         .def("levels_required", &MinimaxChain::levels_required);
     m.def("build_chain", &build_chain, py::call_guard<py::gil_scoped_release>());
-    m.def("eval_private_threshold", &eval_private_threshold, py::keep_alive<0, 1>(), py::arg("ev"),
+    m.def("eval_private_threshold", &eval_private_threshold, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>(), py::arg("ev"),
           py::arg("ct_scores"), py::arg("ct_t"), py::arg("ct_norm"), py::arg("chain"), py::arg("keys"),
           py::arg("mode") = PolyEval::ladder);
-    m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm, py::keep_alive<0, 1>(),
+    m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>(),
           py::arg("ev"), py::arg("ct_scores"), py::arg("ct_t"), py::arg("norm"), py::arg("chain"), py::arg("keys"),
           py::arg("mode") = PolyEval::ladder);
+
+    // Python threads: `with stream_scope(ring, i):` runs the ops of this
+    // thread on the ring's i-th worker stream (thread-local, like the C++
+    // StreamScope). Call ring.synchronize() inside the scope before handing
+    // results to another thread.
+    struct PyStreamScope {
+        const RingParams* ring;
+        std::size_t index;
+        std::unique_ptr<StreamScope> scope;
+    };
+    py::class_<PyStreamScope>(m, "StreamScope")
+        .def("__enter__",
+             [](PyStreamScope& s) {
+                 s.scope = std::make_unique<StreamScope>(*s.ring, s.ring->device_state()->worker_stream(s.index));
+                 return &s;
+             },
+             py::return_value_policy::reference)
+        .def("__exit__", [](PyStreamScope& s, py::args) { s.scope.reset(); });
+    m.def(
+        "stream_scope", [](const RingParams& ring, std::size_t i) { return PyStreamScope{&ring, i, nullptr}; },
+        py::keep_alive<0, 1>());
 
     // ---- kernel timing, end-to-end transfer helpers --------------------------
     m.def("profile_enable", [](const RingParams& r, bool on) { check_tg(tg_profile_enable(r.dev(), on ? 1 : 0)); });

@@ -57,6 +57,21 @@ CONFIGS = {
     3: Spec("config3-threshold-count", N=1 << 16, nq=21, q_bits=50, K=6, sp_bits=60, group=7, h=192,
             delta_log2=50, degrees=(15, 15, 27), alpha=8, epsilon=0.0, norm=1.0, n_cts=4, records=1 << 17,
             seed=0xC0F3),
+    # configs[3]: full TETRIS statement, 2^18 records: three private thresholds
+    # (blood sugar, blood pressure, 8-attribute encrypted linear risk score),
+    # AND by products, plaintext disorder flag, slot-sum. Levels: the
+    # thresholds take 17 from L (risk score: from L-1 after its rescale), two
+    # AND products + the flag product take 3 more -> count at level L-20 = 1
+    # (two limbs for decoding, ckks.hpp:121-134) with L = 21.
+    4: Spec("config4-tetris-statement", N=1 << 16, nq=22, q_bits=50, K=6, sp_bits=60, group=7, h=192,
+            delta_log2=50, degrees=(15, 15, 27), alpha=8, epsilon=0.0, norm=1.0, n_cts=8, records=1 << 18,
+            seed=0xC0F4),
+    # configs[4]: scale-out stress, 2^20 records (32 record blocks), three
+    # degree-63 stages (levels_required 22), L = 28, dnum = 3 (group 10:
+    # 10 x 50-bit digits under P = 9 x 60-bit specials). Count at level 3.
+    5: Spec("config5-stress", N=1 << 16, nq=29, q_bits=50, K=9, sp_bits=60, group=10, h=192,
+            delta_log2=50, degrees=(63, 63, 63), alpha=13, epsilon=0.0, norm=1.0, n_cts=32, records=1 << 20,
+            seed=0xC0F5),
 }
 
 
@@ -88,7 +103,19 @@ def make_context(T, spec: Spec, rotations=(), relin=True):
         g = T.rotation_exponent(ring, k)
         if not keys.has(g):
             keys.add_galois(g, ctx.galois_key_gen(sk, g, krng))
-    return SimpleNamespace(T=T, spec=spec, ring=ring, ctx=ctx, ev=ev, sk=sk, pk=pk, keys=keys, primes=qs, sp=sp)
+    return SimpleNamespace(T=T, spec=spec, ring=ring, ctx=ctx, ev=ev, sk=sk, pk=pk, keys=keys, primes=qs, sp=sp,
+                           encode=encode_slots_batch)
+
+
+def encode_slots_batch(S, arr, scale, level):
+    """Encoder::encode_slots of every row of `arr` ([batch][slots] complex):
+    one device launch on the B200 module, the per-vector host DFT elsewhere.
+    Parity harnesses may replace S.encode to feed the reference the device
+    encoder's (bit-identical) residues instead of re-running its O(n^2) DFT."""
+    enc = S.T.Encoder(S.ring, S.spec.slots)
+    if hasattr(enc, "encode_slots_many"):
+        return list(enc.encode_slots_many(arr, scale, level))
+    return [enc.encode_slots(list(v), scale, level) for v in arr]
 
 
 def inner_sum_rotations(slots: int):
@@ -159,4 +186,191 @@ def config3_query(S, chain, cts, ct_t, do_inner_sum=True):
         acc = o if acc is None else ev.add(acc, o)
     if do_inner_sum:
         acc = T.inner_sum(ev, acc, S.spec.slots, S.keys)
+    return acc
+
+
+def run_concurrent(T, ring, fn, items, streams):
+    """fn(item) for every item; with the B200 module and streams > 1 the items
+    are spread round-robin over `streams` host threads, each issuing on its
+    own CUDA stream (stream_scope) and synchronising it before returning its
+    results. Results come back in item order, so every later reduction runs
+    in the reference's order."""
+    items = list(items)
+    if streams <= 1 or len(items) <= 1 or not hasattr(T, "stream_scope"):
+        return [fn(x) for x in items]
+    import threading
+    out = [None] * len(items)
+    errs = []
+    k = min(streams, len(items))
+
+    def worker(w):
+        try:
+            with T.stream_scope(ring, w):
+                for i in range(w, len(items), k):
+                    out[i] = fn(items[i])
+                ring.synchronize()
+        except BaseException as e:  # surfaced on the caller's thread
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(w,)) for w in range(k)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Config 2: encrypted linear score (pt x ct multiply-accumulate)
+# ---------------------------------------------------------------------------
+
+ATTR_NORM = 8 * 255.0  # folds the [0,255] attribute range and the 8-term sum into [-1, 1]
+
+
+def linear_score_data(spec: Spec, seed_offset: int = 0):
+    """Server records (8 integer attributes in [0,255]) and the scientist's
+    weights w_j ~ U[-1,1]."""
+    g = np.random.Generator(np.random.PCG64(spec.seed + seed_offset))
+    attrs = g.integers(0, 256, size=(spec.records, 8)).astype(np.float64)
+    w = g.uniform(-1.0, 1.0, size=8)
+    return attrs, w
+
+
+def encode_plaintexts(S, columns, level, to_eval=True):
+    """Server-side plaintexts: each row of `columns` (a slot vector) encoded at
+    scale q_level (the mul_scalar convention, so a following rescale restores
+    the ciphertext scale) and transformed to eval form for mul_plain
+    (ckks.hpp:253-269). The B200 module encodes the batch in one device launch."""
+    scale = float(S.ring.modulus(level))
+    arr = np.asarray(columns, dtype=np.complex128).reshape(-1, S.spec.slots)
+    pts = S.encode(S, arr, scale, level)
+    if to_eval:
+        for p in pts:
+            p.ntt_forward()
+    return pts, scale
+
+
+def encrypt_many(S, vectors, level, labels):
+    """Scientist-side encryption (KeyContext::encrypt, secret key) of slot
+    vectors at scale Delta, randomness Rng(seed).split(label)."""
+    T = S.T
+    arr = np.asarray(vectors, dtype=np.complex128).reshape(-1, S.spec.slots)
+    ms = S.encode(S, arr, S.spec.delta, level)
+    return [S.ctx.encrypt(S.sk, m, S.spec.delta, T.Rng(S.spec.seed).split(lab), T.Domain.slots)
+            for m, lab in zip(ms, labels)]
+
+
+def linear_score(S, ct_w, pts, plain_scale):
+    """score = rescale(sum_j mul_plain(ct_w_j, pt_j)), summed in j order
+    (config 2's pt x ct MAC)."""
+    ev = S.ev
+    acc = None
+    for cw, p in zip(ct_w, pts):
+        t = ev.mul_plain(cw, p, plain_scale)
+        acc = t if acc is None else ev.add(acc, t)
+    return ev.rescale(acc)
+
+
+def config2_inputs(S, attrs=None, w=None):
+    spec = S.spec
+    if attrs is None:
+        attrs, w = linear_score_data(spec)
+    n, L = spec.slots, S.ring.max_level()
+    ct_w = encrypt_many(S, [[wj] * n for wj in w], L, [400 + j for j in range(8)])
+    cols = [attrs[b * n:(b + 1) * n, j] / ATTR_NORM for b in range(spec.n_cts) for j in range(8)]
+    pts, pscale = encode_plaintexts(S, cols, L)
+    blocks = [pts[8 * b:8 * b + 8] for b in range(spec.n_cts)]
+    return SimpleNamespace(ct_w=ct_w, blocks=blocks, plain_scale=pscale, attrs=attrs, w=w)
+
+
+def config2_query(S, inp, streams=1):
+    return run_concurrent(S.T, S.ring, lambda pts: linear_score(S, inp.ct_w, pts, inp.plain_scale),
+                          inp.blocks, streams)
+
+
+# ---------------------------------------------------------------------------
+# Configs 4-5: the full TETRIS statement
+# ---------------------------------------------------------------------------
+
+RISK_NORM = 0.5  # |risk - t| <= 1.05 for risk in [-1,1], |t| <= 0.05
+
+
+def statement_data(spec: Spec, seed_offset: int = 0):
+    """Synthetic records with BASELINE.json's distributions, each attribute
+    normalised by its clip range, plus the scientist's statement:
+    sugar >= 126 mg/dL AND pressure >= 140 mmHg AND risk >= t_risk AND flag."""
+    g = np.random.Generator(np.random.PCG64(spec.seed + seed_offset))
+    n = spec.records
+    sugar = np.clip(g.normal(100.0, 25.0, n), 40.0, 300.0)
+    bp = np.clip(g.normal(120.0, 15.0, n), 70.0, 220.0)
+    flag = (g.random(n) < 0.1).astype(np.float64)
+    attrs = g.integers(0, 256, size=(n, 8)).astype(np.float64)
+    w = g.uniform(-1.0, 1.0, size=8)
+    t = ((126.0 - 40.0) / 260.0, (140.0 - 70.0) / 150.0, float(g.uniform(-0.05, 0.05)))
+    return SimpleNamespace(sugar=(sugar - 40.0) / 260.0, bp=(bp - 70.0) / 150.0, flag=flag,
+                           attrs=attrs / ATTR_NORM, w=w, t=t)
+
+
+def statement_plain_count(d):
+    """Plaintext comparator (informational; the exact check is against the
+    oracle's decrypted count, SURVEY 8(d) config 3 note)."""
+    risk = d.attrs @ d.w
+    return int(((d.sugar >= d.t[0]) & (d.bp >= d.t[1]) & (risk >= d.t[2]) & (d.flag > 0)).sum())
+
+
+def statement_query_inputs(S, d):
+    """The scientist's encrypted statement: 8 risk weights and 3 thresholds."""
+    n, L = S.spec.slots, S.ring.max_level()
+    vecs = [[wj] * n for wj in d.w] + [[tk] * n for tk in d.t]
+    cts = encrypt_many(S, vecs, L, [400 + j for j in range(8)] + [90, 91, 92])
+    return SimpleNamespace(ct_w=cts[:8], ct_t=cts[8:])
+
+
+def statement_block_inputs(S, d, b):
+    """Record block b: encrypted sugar/pressure columns, plaintext risk
+    attributes and plaintext flag (eval form, level L, scale q_L). The flag
+    multiplies the AND output, whose level depends on the polynomial
+    evaluator (BSGS saves a level on degree 27); a level-L plaintext serves
+    any level (mul_plain reads rows by modulus index, ckks.hpp:257-265), and
+    the tracked scale absorbs q_L / q_level after the rescale."""
+    n = S.spec.slots
+    L = S.ring.max_level()
+    sl = slice(b * n, (b + 1) * n)
+    cts = encrypt_many(S, [d.sugar[sl], d.bp[sl]], L, [200 + b, 300 + b])
+    pts, ascale = encode_plaintexts(S, [d.attrs[sl, j] for j in range(8)] + [d.flag[sl]], L)
+    flag, fscale = pts[8:], ascale
+    pts = pts[:8]
+    return SimpleNamespace(ct_sugar=cts[0], ct_bp=cts[1], pt_attr=pts, attr_scale=ascale,
+                           pt_flag=flag[0], flag_scale=fscale)
+
+
+def statement_block(S, q, blk, threshold):
+    """One block of the statement in the reference API's op order:
+    linear risk score, three private thresholds (threshold(x, t, norm)),
+    AND = rescale(mul_relin(b1, b2)) then x b3, then the flag product."""
+    ev, keys = S.ev, S.keys
+    risk = linear_score(S, q.ct_w, blk.pt_attr, blk.attr_scale)
+    b1 = threshold(blk.ct_sugar, q.ct_t[0], 1.0)
+    b2 = threshold(blk.ct_bp, q.ct_t[1], 1.0)
+    b3 = threshold(risk, q.ct_t[2], RISK_NORM)
+    a = ev.rescale(ev.mul_relin(b1, b2, keys))
+    a = ev.rescale(ev.mul_relin(a, b3, keys))
+    return ev.rescale(ev.mul_plain(a, blk.pt_flag, blk.flag_scale))
+
+
+def threshold_fn(S, chain, mode=None):
+    T = S.T
+    if mode is None:
+        return lambda x, t, norm: T.eval_private_threshold_plain_norm(S.ev, x, t, norm, chain, S.keys)
+    return lambda x, t, norm: T.eval_private_threshold_plain_norm(S.ev, x, t, norm, chain, S.keys, mode)
+
+
+def statement_partial(S, q, blocks, threshold, streams=1):
+    """Sum (mod q, block order) of the per-block statements on this shard."""
+    outs = run_concurrent(S.T, S.ring, lambda blk: statement_block(S, q, blk, threshold), blocks, streams)
+    acc = None
+    for o in outs:
+        acc = o if acc is None else S.ev.add(acc, o)
     return acc

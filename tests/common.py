@@ -96,3 +96,31 @@ def enc_slots(S, values, delta, rng, level=None, nslots=None):
 def dec_slots(S, ct, nslots):
     enc = S.T.Encoder(S.ring, nslots)
     return np.array(enc.decode_slots(S.ctx.decrypt(S.sk, ct), ct.scale))
+
+
+def mirror_encoder(S_gpu, R):
+    """S.encode for the reference side of a parity run: slot vectors are
+    encoded once on the device (bit-identical to the reference Encoder,
+    tests/test_gpu_encoder.py) and the residues handed to the reference, which
+    skips its O(n^2) host DFT. Everything downstream runs in the reference."""
+    def encode(SR, arr, scale, level):
+        polys = S_gpu.encode(S_gpu, arr, scale, level)
+        return [R.Poly.from_numpy(SR.ring, p.to_numpy(), level, R.Form.coeff, 0) for p in polys]
+    return encode
+
+
+def copy_chain(T, chain):
+    """The same MinimaxChain in module T (build_chain is bit-exact across the
+    two modules, test_host_cpu::test_remez_chain_bit_exact; degree-63 chains
+    take ~20 s to build, so parity runs build them once)."""
+    c = T.MinimaxChain()
+    c.params = T.ThresholdParams(chain.params.alpha, chain.params.beta, list(chain.params.degrees),
+                                 chain.params.epsilon)
+    stages = []
+    for s in chain.stages:
+        t = T.ChainStage()
+        t.degree, t.gamma, t.upper, t.cheb, t.error = s.degree, s.gamma, s.upper, list(s.cheb), s.error
+        stages.append(t)
+    c.stages = stages
+    c.sign_error, c.achieved_beta = chain.sign_error, chain.achieved_beta
+    return c
