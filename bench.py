@@ -1,21 +1,29 @@
 #!/usr/bin/env python3
-"""Benchmark of the B200 RNS-CKKS threshold-count query (BASELINE.json metric:
+"""Benchmark of the B200 RNS-CKKS TETRIS query (BASELINE.json metric:
 encrypted records/s & amortized us/record per TETRIS query).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--config 4|3|5] [--poly-eval bsgs|ladder] [--streams S]
 
-One step = one full query over the workload: per-ciphertext private
-threshold (composite minimax sign chain), sum of the per-ciphertext outputs,
-and the log2(slots) rotate-and-add slot sum into an encrypted count.
-N>1 (torchrun): ciphertexts are sharded round-robin over ranks; each rank
-sums its outputs, the partial ciphertexts are NCCL-reduced to rank 0
-(integer sum + mod-q fix-up kernel) and rank 0 runs the one inner_sum — the
-reference's order (sum, then InnerSum; protocol.hpp:319-323), so the result
-is bit-identical at every GPU count.
+Default workload: config 4, the full TETRIS statement over 2^18 records
+(N=2^16, L=21): per record block (2^15 records per ciphertext) an encrypted
+8-attribute linear risk score (8 pt x ct MACs + rescale), three private
+thresholds (composite minimax sign chain (15,15,27), BSGS), the AND as
+products of indicators, the plaintext disorder flag, the sum over blocks and
+the log2(slots) rotate-and-add slot sum into one encrypted count.
+Config 3 (threshold count, 2^17 records) and config 5 (2^20 records,
+degree-63 chain, L=28, dnum=3) run with --config.
+
+One step = one full query. N>1 (torchrun): record blocks are sharded
+round-robin over ranks; each rank sums its block outputs, the partial
+ciphertexts are NCCL-reduced to rank 0 (integer sum + mod-q fix-up kernel)
+and rank 0 runs the one inner_sum - the reference's order (sum, then
+InnerSum; protocol.hpp:319-323), so the count is bit-identical at every GPU
+count.
 
 `--impl reference` times the reference's own CPU implementation (the
-unmodified headers compiled into oracle/_ref) on the box's host cores with a
-std::thread pool over ciphertexts (protocol.hpp:297-311); rank 0 only.
+unmodified headers compiled into oracle/_ref) on the box's host cores with
+threads over blocks and thresholds (protocol.hpp:297-311); rank 0 only.
 """
 from __future__ import annotations
 
@@ -137,6 +145,140 @@ def reduce_partial_to_root(G, torch, dist, ct, ext_stream, N):
 
 
 # ---------------------------------------------------------------------------
+# Workloads: per-query client ciphertexts (uploaded by the e2e leg), resident
+# server data, and the per-rank partial result before the NCCL reduce.
+# ---------------------------------------------------------------------------
+class ThresholdCount:
+    """Config 3: private threshold of every encrypted score block against an
+    encrypted threshold (plain norm), summed."""
+    metric = "encrypted records/sec per TETRIS threshold-count query (amortized us/record in config)"
+
+    def __init__(self, G, W, spec, rank=0, world=1, rotations=True, device=True):
+        from paper_2412_13269_b200 import distributed as D
+        self.G, self.W, self.spec = G, W, spec
+        self.scores, self.thr, _, _ = W.linear_scores(spec)
+        if not device:  # inputs only (the CPU reference arm)
+            return
+        rot = W.inner_sum_rotations(spec.slots) if rotations else []
+        self.S = W.make_context(G, spec, rotations=rot)
+        self.chain = W.config3_chain(G, spec)
+        self.mine = D.shard(spec.n_cts, world, rank)
+        cts, ct_t, _, _ = W.config3_inputs(self.S, ct_indices=self.mine, scores=self.scores, t=self.thr)
+        self.client = cts + [ct_t]
+
+    def partial(self, client, streams, mode):
+        cts, ct_t = client[:-1], client[-1]
+        if not cts:
+            return None
+        outs = self.G.eval_private_threshold_plain_norm_many(self.S.ev, cts, ct_t, self.spec.norm, self.chain,
+                                                             self.S.keys, streams, mode)
+        acc = outs[0]
+        for o in outs[1:]:
+            acc = self.S.ev.add(acc, o)
+        return acc
+
+    def plain_count(self):
+        return int((self.scores >= self.thr).sum())
+
+    def ref_inputs(self, R, SR, chain_r, host_encode, blocks):
+        n = self.spec.slots
+        cts = [host_encode(self.scores[b * n:(b + 1) * n], 100 + b) for b in blocks]
+        return cts, host_encode([self.thr] * n, 99)
+
+    def ref_step(self, R, SR, chain_r, inp, threads):
+        cts, ct_t = inp
+        return R.threshold_count_pool(SR.ev, cts, ct_t, self.spec.norm, chain_r, SR.keys, self.spec.slots,
+                                      threads, False)[0]
+
+    def gpu_ladder(self, blocks):
+        cts = [self.client[self.mine.index(b)] for b in blocks]
+        return self.partial(cts + [self.client[-1]], len(cts), self.G.PolyEval.ladder)
+
+
+class Statement:
+    """Configs 4/5: the full TETRIS statement per record block (linear risk
+    score, three private thresholds, AND, plaintext flag), summed."""
+    metric = "encrypted records/sec per TETRIS query (full statement; amortized us/record in config)"
+
+    def __init__(self, G, W, spec, rank=0, world=1, rotations=True, device=True):
+        from paper_2412_13269_b200 import distributed as D
+        self.G, self.W, self.spec = G, W, spec
+        self.d = W.statement_data(spec)
+        if not device:  # inputs only (the CPU reference arm)
+            return
+        rot = W.inner_sum_rotations(spec.slots) if rotations else []
+        self.S = W.make_context(G, spec, rotations=rot)
+        self.chain = W.config3_chain(G, spec)
+        self.mine = D.shard(spec.n_cts, world, rank)
+        q = W.statement_query_inputs(self.S, self.d)
+        self.blocks = [W.statement_block_inputs(self.S, self.d, b) for b in self.mine]
+        self.client = q.ct_w + q.ct_t + [c for blk in self.blocks for c in (blk.ct_sugar, blk.ct_bp)]
+
+    def _bind(self, client, blocks):
+        from types import SimpleNamespace as NS
+        q = NS(ct_w=client[:8], ct_t=client[8:11])
+        bl = [NS(ct_sugar=client[11 + 2 * i], ct_bp=client[12 + 2 * i], pt_attr=b.pt_attr,
+                 attr_scale=b.attr_scale, pt_flag=b.pt_flag, flag_scale=b.flag_scale)
+              for i, b in enumerate(blocks)]
+        return q, bl
+
+    def partial(self, client, streams, mode):
+        if not self.blocks:
+            return None
+        q, bl = self._bind(client, self.blocks)
+        return self.W.statement_partial(self.S, q, bl, self.W.threshold_fn(self.S, self.chain, mode), streams)
+
+    def plain_count(self):
+        return self.W.statement_plain_count(self.d)
+
+    def ref_inputs(self, R, SR, chain_r, host_encode, blocks):
+        from types import SimpleNamespace as NS
+        W, d, n, L = self.W, self.d, self.spec.slots, SR.ring.max_level()
+        ct_w = [host_encode([wj] * n, 400 + j) for j, wj in enumerate(d.w)]
+        ct_t = [host_encode([tk] * n, 90 + k) for k, tk in enumerate(d.t)]
+        out = []
+        for b in blocks:
+            sl = slice(b * n, (b + 1) * n)
+            pts, sc = W.encode_plaintexts(SR, [d.attrs[sl, j] for j in range(8)] + [d.flag[sl]], L)
+            out.append(NS(ct_sugar=host_encode(d.sugar[sl], 200 + b), ct_bp=host_encode(d.bp[sl], 300 + b),
+                          pt_attr=pts[:8], attr_scale=sc, pt_flag=pts[8], flag_scale=sc))
+        return NS(ct_w=ct_w, ct_t=ct_t), out
+
+    def ref_step(self, R, SR, chain_r, inp, threads):
+        """The reference's own code path, threads over blocks x thresholds;
+        per block the same ops as workloads.statement_block."""
+        from concurrent.futures import ThreadPoolExecutor
+        W, ev, keys = self.W, SR.ev, SR.keys
+        q, blocks = inp
+
+        def thr(x, t, norm):
+            return R.eval_private_threshold_plain_norm(ev, x, t, norm, chain_r, keys)
+
+        with ThreadPoolExecutor(max(1, threads)) as ex:
+            risks = list(ex.map(lambda b: W.linear_score(SR, q.ct_w, b.pt_attr, b.attr_scale), blocks))
+            futs = [(ex.submit(thr, b.ct_sugar, q.ct_t[0], 1.0), ex.submit(thr, b.ct_bp, q.ct_t[1], 1.0),
+                     ex.submit(thr, r, q.ct_t[2], W.RISK_NORM)) for b, r in zip(blocks, risks)]
+            outs = []
+            for b, (f1, f2, f3) in zip(blocks, futs):
+                a = ev.rescale(ev.mul_relin(f1.result(), f2.result(), keys))
+                a = ev.rescale(ev.mul_relin(a, f3.result(), keys))
+                outs.append(ev.rescale(ev.mul_plain(a, b.pt_flag, b.flag_scale)))
+        acc = outs[0]
+        for o in outs[1:]:
+            acc = ev.add(acc, o)
+        return acc
+
+    def gpu_ladder(self, blocks):
+        q, bl = self._bind(self.client, self.blocks)
+        sel = [bl[self.mine.index(b)] for b in blocks]
+        return self.W.statement_partial(self.S, q, sel, self.W.threshold_fn(self.S, self.chain,
+                                                                              self.G.PolyEval.ladder), len(sel))
+
+
+WORKLOADS = {3: ThresholdCount, 4: Statement, 5: Statement}
+
+
+# ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
 def run_b200(args):
@@ -157,35 +299,32 @@ def run_b200(args):
         raise SystemExit("bench.py: no CUDA device visible (the B200 arm has no CPU fallback)")
     G.set_default_device(local)
 
-    spec = W.CONFIGS[3]
+    spec = W.CONFIGS[args.config]
     t0 = time.time()
-    rot = W.inner_sum_rotations(spec.slots) if rank == 0 else []
-    S = W.make_context(G, spec, rotations=rot)
-    chain = W.config3_chain(G, spec)
-    scores, thr, _, _ = W.linear_scores(spec)
     from paper_2412_13269_b200 import distributed as D
-
-    mine = D.shard(spec.n_cts, world, rank)
+    wl = WORKLOADS[args.config](G, W, spec, rank, world, rotations=(rank == 0))
+    S, chain = wl.S, wl.chain
     D.check_exact(world, S.primes)
-    cts, ct_t, _, _ = W.config3_inputs(S, ct_indices=mine, scores=scores, t=thr)
     S.ring.synchronize()
-    log(f"[rank {rank}] setup {time.time() - t0:.1f}s: N={spec.N} L={spec.nq - 1} K={spec.K} cts={mine}")
+    log(f"[rank {rank}] setup {time.time() - t0:.1f}s: {spec.name} N={spec.N} L={spec.nq - 1} K={spec.K} "
+        f"blocks={wl.mine}")
     mode = G.PolyEval.bsgs if args.poly_eval == "bsgs" else G.PolyEval.ladder
     ext = torch.cuda.ExternalStream(S.ring.stream_handle(), device=torch.device("cuda", local))
     flush = torch.empty(64 << 22, dtype=torch.int32, device="cuda")  # 1 GiB > 126 MB L2
+    out_meta = {}
 
-    def query(local_cts, t_ct, streams=None):
+    def query(client, streams=None):
         streams = streams or args.streams
-        # per-ciphertext thresholds run concurrently (one host thread + CUDA
-        # stream each); outputs are summed in index order on the main stream
-        acc = None
-        outs = G.eval_private_threshold_plain_norm_many(S.ev, local_cts, t_ct, spec.norm, chain, S.keys,
-                                                        streams, mode) if local_cts else []
-        for o in outs:
-            acc = o if acc is None else S.ev.add(acc, o)
-        if acc is None:  # rank without ciphertexts contributes zero
-            acc = S.ctx.zero_ciphertext(t_ct.level() - chain.levels_required(), 1.0, S.sk.id(), G.Domain.slots)
+        # record blocks run concurrently (one host thread + CUDA stream each);
+        # outputs are summed in block order
+        acc = wl.partial(client, streams, mode)
         if world > 1:
+            if "level" not in out_meta:  # ranks without blocks learn the output level once
+                lv = torch.tensor([acc.level() if acc is not None else -1], device="cuda", dtype=torch.int64)
+                dist.all_reduce(lv, op=dist.ReduceOp.MAX)
+                out_meta["level"] = int(lv.item())
+            if acc is None:  # contributes zero
+                acc = S.ctx.zero_ciphertext(out_meta["level"], 1.0, S.sk.id(), G.Domain.slots)
             reduce_partial_to_root(G, torch, dist, acc, ext, spec.N)
         if rank == 0:
             acc = G.inner_sum(S.ev, acc, spec.slots, S.keys)
@@ -214,7 +353,7 @@ def run_b200(args):
 
     # warm-up
     for _ in range(args.warmup):
-        res = query(cts, ct_t)
+        res = query(wl.client)
     barrier()
     # timed region (device-resident inputs)
     prof_region = os.environ.get("TG_PROFILE_REGION") == "1"  # ncu --profile-from-start off
@@ -222,7 +361,7 @@ def run_b200(args):
         barrier()
         if prof_region:
             torch.cuda.cudart().cudaProfilerStart()
-        ms_list, res = timed(lambda: query(cts, ct_t), args.steps)
+        ms_list, res = timed(lambda: query(wl.client), args.steps)
         if prof_region:
             torch.cuda.cudart().cudaProfilerStop()
         barrier()
@@ -239,24 +378,24 @@ def run_b200(args):
     barrier()
     # one stream here, so every kernel's event-bracketed duration is its own
     # (concurrent streams would time-share the SMs inside the brackets)
-    _, _ = timed(lambda: query(cts, ct_t, streams=1), args.steps)
+    _, _ = timed(lambda: query(wl.client, streams=1), args.steps)
     prof = G.profile_read(S.ring)
     G.profile_enable(S.ring, False)
 
-    # end to end through the public API: host (pinned) ciphertexts in, count out
+    # end to end through the public API: the query's client ciphertexts come
+    # from pinned host memory every step, the count goes back to the host
     host_in = []
-    for c in cts + [ct_t]:
-        arr = G.pinned_empty([2, c.level() + 1, spec.N])
+    for c in wl.client:
+        arr = G.pinned_empty([len(c.parts), c.level() + 1, spec.N])
         G.ciphertext_to_numpy(c, arr)
-        host_in.append((arr, c.scale, c.sk_id))
-    lvl_in = ct_t.level()
+        host_in.append((arr, c.level(), c.scale, c.sk_id))
     out_lvl = res.level() if rank == 0 else 0
     host_out = G.pinned_empty([2, out_lvl + 1, spec.N])
 
     def e2e_step():
-        ups = [G.ciphertext_from_numpy(S.ring, a, lvl_in, G.Form.coeff, sc, G.Domain.slots, sid)
-               for (a, sc, sid) in host_in]
-        r = query(ups[:-1], ups[-1])
+        ups = [G.ciphertext_from_numpy(S.ring, a, lv, G.Form.coeff, sc, G.Domain.slots, sid)
+               for (a, lv, sc, sid) in host_in]
+        r = query(ups)
         if rank == 0:
             G.ciphertext_to_numpy(r, host_out)
         return r
@@ -270,7 +409,7 @@ def run_b200(args):
         tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    h2d = sum(a.nbytes for a, _, _ in host_in)
+    h2d = sum(a.nbytes for a, _, _, _ in host_in)
     d2h = host_out.nbytes if rank == 0 else 0
 
     # decrypt + check the count (rank 0)
@@ -278,9 +417,8 @@ def run_b200(args):
     if rank == 0:
         enc = G.Encoder(S.ring, spec.slots)
         dec = np.array(enc.decode_slots(S.ctx.decrypt(S.sk, res), res.scale))
-        count = float(dec[0].real)
-        want = int((scores >= thr).sum())
-        check = {"decrypted_count": round(count, 3), "plaintext_comparator_count": want}
+        check = {"decrypted_count": round(float(dec[0].real), 3), "plaintext_comparator_count": wl.plain_count(),
+                 "count_level": res.level()}
 
     if rank != 0:
         if dist is not None:
@@ -294,7 +432,7 @@ def run_b200(args):
     per_launch_ms = dms / dn
     achieved = (dbytes / dn) / (per_launch_ms / 1e3) / 1e9
     total_prof_ms = sum(v[0] for v in prof.values())
-    launches = sum(v[1] * (2 if k.startswith("ntt") else 1) for k, v in prof.items())
+    launches = sum(v[1] * (2 if k.startswith("ntt") else 1) for k, v in prof.items()) // args.steps * args.steps
     roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
                 "bytes_per_launch": dbytes / dn, "ms_per_launch": per_launch_ms,
@@ -306,34 +444,27 @@ def run_b200(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            # full-size parity: the GPU ladder query vs the unmodified CPU reference
-            ladder = G.eval_private_threshold_plain_norm_many(S.ev, cts, ct_t, spec.norm, chain, S.keys,
-                                                              args.streams, G.PolyEval.ladder)
-            lad = ladder[0]
-            for o in ladder[1:]:
-                lad = S.ev.add(lad, o)
-            lad = G.inner_sum(S.ev, lad, spec.slots, S.keys)
-            cpu = cpu_baseline(G, W, spec, S, chain, scores, thr, lad)
+            cpu = cpu_baseline(G, W, spec, wl)
         except Exception as e:  # the baseline is reported, never the product
-            cpu = {"value": None, "error": str(e)[:200]}
+            cpu = {"value": None, "error": str(e)[:300]}
 
     clk = clocks.summary()
     line = {
-        "metric": "encrypted records/sec per TETRIS threshold-count query (amortized us/record in config)",
+        "metric": wl.metric,
         "value": round(value, 1), "unit": "records/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u64 (mod-q RNS residues)", "data": "synthetic",
         "config": {"workload": spec.name, "records": records, "N": spec.N, "levels": spec.nq - 1,
-                   "q_bits": spec.q_bits, "special_primes": f"{spec.K}x{spec.sp_bits}b", "dnum": -(-spec.nq // spec.group),
-                   "chain_degrees": list(spec.degrees), "alpha": spec.alpha, "epsilon": spec.epsilon,
-                   "poly_eval": args.poly_eval, "streams": args.streams,
-                   "ciphertexts": spec.n_cts, "slots": spec.slots, "secret_hw": spec.h,
+                   "q_bits": spec.q_bits, "special_primes": f"{spec.K}x{spec.sp_bits}b",
+                   "dnum": -(-spec.nq // spec.group), "chain_degrees": list(spec.degrees), "alpha": spec.alpha,
+                   "epsilon": spec.epsilon, "poly_eval": args.poly_eval, "streams": args.streams,
+                   "record_blocks": spec.n_cts, "slots": spec.slots, "secret_hw": spec.h,
                    "amortized_us_per_record": round(ms_step * 1e3 / records, 4),
-                   "l2": "1 GiB buffer written between timed steps; working set (keys) ~1.4 GB > 126 MB L2",
-                   "parallelism": f"ct-shard x{world}", **check},
+                   "l2": "1 GiB buffer written between timed steps; working set (keys, blocks) > 126 MB L2",
+                   "parallelism": f"block-shard x{world}", **check},
         "e2e": {"value": round(records / (e2e_ms / 1e3), 1), "unit": "records/s", "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": int(launches),
+        "gpu_launches": int(launches // args.steps),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clk,
@@ -344,7 +475,7 @@ def run_b200(args):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the compiled, unmodified reference (oracle/_ref)
+# CPU reference: the compiled, unmodified reference (oracle/_ref)
 # ---------------------------------------------------------------------------
 def _ref_module():
     sys.path.insert(0, str(ROOT / "tests"))
@@ -352,43 +483,60 @@ def _ref_module():
     return load_ref()
 
 
-def _ref_setup(G, W, spec, scores, thr):
-    """Reference context + the same inputs (bit-identical by construction;
-    slot vectors encoded once with the product's multi-threaded host encoder,
-    which produces the reference encoder's exact residues)."""
+def _ref_setup(G, W, spec, wl, blocks, rotations=False):
+    """Reference context + the workload's inputs for `blocks`, bit-identical to
+    the B200 arm's (same keys/randomness streams; slot vectors encoded with the
+    product's multi-threaded HOST encoder, which reproduces the reference
+    Encoder's residues exactly - tests/test_host_cpu.py - instead of its
+    single-threaded O(n^2) DFT)."""
     R = _ref_module()
     if R is None:
         raise RuntimeError("oracle/_ref not built")
-    rot = W.inner_sum_rotations(spec.slots)
-    SR = W.make_context(R, spec, rotations=rot)
-    chain = W.config3_chain(R, spec)
+    SR = W.make_context(R, spec, rotations=W.inner_sum_rotations(spec.slots) if rotations else [])
+    sys.path.insert(0, str(ROOT / "tests"))
+    from common import copy_chain
+    # the B200 arm's chain when present (bit-identical, saves the host Remez
+    # time of degree-63 chains), else the reference's own build_chain
+    chain_r = copy_chain(R, wl.chain) if hasattr(wl, "chain") else W.config3_chain(R, spec)
     ringG = G.RingParams(spec.N, SR.primes + SR.sp, spec.K)
     encG = G.Encoder(ringG, spec.slots)
-    lvl = SR.ring.max_level()
-    n = spec.slots
 
-    def enc(values, label):
-        host = encG.encode_slots_host([complex(v) for v in values], spec.delta, lvl)
-        m = R.Poly.from_numpy(SR.ring, host, lvl, R.Form.coeff, 0)
+    def encode_host(SR_, arr, scale, level):
+        return [R.Poly.from_numpy(SR_.ring, encG.encode_slots_host([complex(x) for x in v], scale, level), level,
+                                  R.Form.coeff, 0) for v in arr]
+
+    SR.encode = encode_host
+    lvl = SR.ring.max_level()
+
+    def host_encode(values, label):
+        m = encode_host(SR, [values], spec.delta, lvl)[0]
         return SR.ctx.encrypt(SR.sk, m, spec.delta, R.Rng(spec.seed).split(label), R.Domain.slots)
 
-    cts = [enc(scores[b * n:(b + 1) * n], 100 + b) for b in range(spec.n_cts)]
-    ct_t = enc([thr] * n, 99)
-    return R, SR, chain, cts, ct_t
+    return R, SR, chain_r, wl.ref_inputs(R, SR, chain_r, host_encode, blocks)
 
 
-def cpu_baseline(G, W, spec, S, chain, scores, thr, gpu_result):
-    R, SR, chain_r, cts, ct_t = _ref_setup(G, W, spec, scores, thr)
-    threads = min(spec.n_cts, os.cpu_count() or 1)
-    res, secs = R.threshold_count_pool(SR.ev, cts, ct_t, spec.norm, chain_r, SR.keys, spec.slots, threads, True)
-    same = all(np.array_equal(a.to_numpy(), b.to_numpy()) for a, b in zip(res.parts, gpu_result.parts)) \
-        and res.scale == gpu_result.scale and res.level() == gpu_result.level()
-    return {"value": round(spec.records / secs, 2), "unit": "records/s", "cores": threads, "kind": "reference",
-            "sample": f"full query: {spec.n_cts} cts x threshold on a {threads}-thread pool + sum + inner_sum "
-                      f"(unmodified reference headers, g++ -O2), {secs:.1f} s",
+def cpu_baseline(G, W, spec, wl):
+    """Bounded sample (~10-30 s of CPU work): the reference on one record
+    block (config 3: all blocks, one thread each), compared residue for
+    residue with the GPU ladder run of the same block(s)."""
+    blocks = list(range(spec.n_cts)) if isinstance(wl, ThresholdCount) else [0]
+    R, SR, chain_r, inp = _ref_setup(G, W, spec, wl, blocks)
+    threads = min(len(blocks) * (3 if isinstance(wl, Statement) else 1), os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    res = wl.ref_step(R, SR, chain_r, inp, threads)
+    secs = time.perf_counter() - t0
+    lad = wl.gpu_ladder(blocks)
+    same = all(np.array_equal(a.to_numpy(), b.to_numpy()) for a, b in zip(res.parts, lad.parts)) \
+        and res.scale == lad.scale and res.level() == lad.level()
+    recs = len(blocks) * spec.slots
+    return {"value": round(recs / secs, 2), "unit": "records/s", "cores": threads, "kind": "reference",
+            "sample": f"{len(blocks)} record block(s) x {spec.slots} records through the reference's own "
+                      f"{'threshold' if isinstance(wl, ThresholdCount) else 'statement ops'} on {threads} threads "
+                      f"(unmodified headers, g++ -O2), {secs:.1f} s; slot-sum not in the sample",
             "seconds": round(secs, 2), "bit_exact_vs_gpu_ladder": bool(same),
-            "note": "reference = its own T_k-ladder implementation; the GPU ladder query's output ciphertext "
-                    "is compared residue for residue (BSGS parity vs its oracle is in tests/test_gpu_bsgs.py)"}
+            "note": "reference = its own T_k-ladder polynomial evaluator; the GPU ladder run of the same blocks is "
+                    "compared residue for residue (BSGS parity vs its oracle: tests/test_gpu_bsgs.py, "
+                    "tests/test_gpu_statement.py)"}
 
 
 def run_reference(args):
@@ -398,34 +546,43 @@ def run_reference(args):
     from paper_2412_13269_b200 import tetris as G
     from paper_2412_13269_b200 import workloads as W
 
-    spec = W.CONFIGS[3]
-    R = _ref_module()
-    if R is None:
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
+    spec = W.CONFIGS[args.config]
+    if _ref_module() is None:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
         return
-    scores, thr, _, _ = W.linear_scores(spec)
+    cores = os.cpu_count() or 1
+    per_block = 3 if WORKLOADS[args.config] is Statement else 1
+    nblk = max(1, min(spec.n_cts, cores // per_block))
+    blocks = list(range(nblk))
     t0 = time.time()
-    R, SR, chain, cts, ct_t = _ref_setup(G, W, spec, scores, thr)
-    log(f"[reference] setup {time.time() - t0:.1f}s")
-    threads = min(spec.n_cts, os.cpu_count() or 1)
+
+    wl = WORKLOADS[args.config](G, W, spec, device=False)
+    R, SR, chain, inp = _ref_setup(G, W, spec, wl, blocks)
+    log(f"[reference] setup {time.time() - t0:.1f}s, sample {nblk} blocks on {nblk * per_block} threads")
+    threads = nblk * per_block
 
     def step():
-        return R.threshold_count_pool(SR.ev, cts, ct_t, spec.norm, chain, SR.keys, spec.slots, threads, True)[1]
+        t = time.perf_counter()
+        wl.ref_step(R, SR, chain, inp, threads)
+        return time.perf_counter() - t
 
     for _ in range(args.warmup):
         step()
     secs = [step() for _ in range(args.steps)]
     s = sum(secs) / len(secs)
-    value = spec.records / s
-    sample = (f"each step = the full query ({spec.n_cts} cts x private threshold on a {threads}-thread pool "
-              f"+ sum + inner_sum), unmodified reference headers compiled g++ -O2")
+    recs = nblk * spec.slots
+    value = recs / s
+    sample = (f"each step = {nblk} of {spec.n_cts} record blocks ({recs} records) through the reference's own "
+              f"code path on {threads} threads (unmodified headers, g++ -O2); per-record work is identical across "
+              f"blocks; the once-per-query slot-sum is not in the sample")
     print(json.dumps({
-        "impl": "reference", "metric": "encrypted records/sec per TETRIS threshold-count query (amortized us/record in config)",
+        "impl": "reference", "metric": WORKLOADS[args.config].metric,
         "value": round(value, 2), "unit": "records/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(s * 1e3, 1), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u64 (mod-q RNS residues)", "data": "synthetic",
         "config": {"workload": spec.name, "records": spec.records, "N": spec.N, "levels": spec.nq - 1,
-                   "amortized_us_per_record": round(s * 1e6 / spec.records, 2)},
+                   "sample_records": recs, "amortized_us_per_record": round(s * 1e6 / recs, 2)},
         "cpu_baseline": {"value": round(value, 2), "unit": "records/s", "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": round(value, 2), "unit": "records/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -441,7 +598,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=4, help="concurrent ciphertext pipelines per GPU")
     ap.add_argument("--poly-eval", choices=["bsgs", "ladder"], default="bsgs",
-                    help="Chebyshev evaluator of the sign stages (config 3 specifies BSGS)")
+                    help="Chebyshev evaluator of the sign stages (BASELINE configs specify BSGS)")
+    ap.add_argument("--config", type=int, choices=[3, 4, 5], default=4,
+                    help="BASELINE.json workload: 4 = full TETRIS statement (default), 3 = threshold count, "
+                         "5 = scale-out stress")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     if args.impl == "reference":

@@ -229,20 +229,20 @@ PYBIND11_MODULE(tetris_ref, m) {
     py::class_<Evaluator>(m, "Evaluator")
         .def(py::init<const KeyContext&>(), py::keep_alive<1, 2>())
         .def("ring", &Evaluator::ring, py::return_value_policy::reference_internal)
-        .def("add", &Evaluator::add)
-        .def("sub", &Evaluator::sub)
-        .def("mul", &Evaluator::mul)
-        .def("mul_relin", &Evaluator::mul_relin)
-        .def("mul_plain", &Evaluator::mul_plain)
-        .def("mul_scalar", &Evaluator::mul_scalar)
-        .def("add_scalar", &Evaluator::add_scalar)
-        .def("rescale", &Evaluator::rescale)
-        .def("rotate", &Evaluator::rotate)
-        .def("conjugate", &Evaluator::conjugate)
+        .def("add", &Evaluator::add, py::call_guard<py::gil_scoped_release>())
+        .def("sub", &Evaluator::sub, py::call_guard<py::gil_scoped_release>())
+        .def("mul", &Evaluator::mul, py::call_guard<py::gil_scoped_release>())
+        .def("mul_relin", &Evaluator::mul_relin, py::call_guard<py::gil_scoped_release>())
+        .def("mul_plain", &Evaluator::mul_plain, py::call_guard<py::gil_scoped_release>())
+        .def("mul_scalar", &Evaluator::mul_scalar, py::call_guard<py::gil_scoped_release>())
+        .def("add_scalar", &Evaluator::add_scalar, py::call_guard<py::gil_scoped_release>())
+        .def("rescale", &Evaluator::rescale, py::call_guard<py::gil_scoped_release>())
+        .def("rotate", &Evaluator::rotate, py::call_guard<py::gil_scoped_release>())
+        .def("conjugate", &Evaluator::conjugate, py::call_guard<py::gil_scoped_release>())
         .def_static("scaled_residue", &Evaluator::scaled_residue);
 
-    m.def("eval_chebyshev", &eval_chebyshev);
-    m.def("inner_sum", &inner_sum);
+    m.def("eval_chebyshev", &eval_chebyshev, py::call_guard<py::gil_scoped_release>());
+    m.def("inner_sum", &inner_sum, py::call_guard<py::gil_scoped_release>());
     m.def("power_to_chebyshev", &power_to_chebyshev);
 
     py::class_<ThresholdParams>(m, "ThresholdParams")
@@ -271,9 +271,9 @@ PYBIND11_MODULE(tetris_ref, m) {
         .def("eval_coeffs", &MinimaxChain::eval_coeffs)
         .def("eval_step", &MinimaxChain::eval_step)
         .def("levels_required", &MinimaxChain::levels_required);
-    m.def("build_chain", &build_chain);
-    m.def("eval_private_threshold", &eval_private_threshold);
-    m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm);
+    m.def("build_chain", &build_chain, py::call_guard<py::gil_scoped_release>());
+    m.def("eval_private_threshold", &eval_private_threshold, py::call_guard<py::gil_scoped_release>());
+    m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm, py::call_guard<py::gil_scoped_release>());
 
     // Multi-threaded driver for the CPU baseline: evaluates the threshold on
     // each ciphertext with a std::thread pool (the reference's own granularity,

@@ -72,12 +72,45 @@ __device__ __forceinline__ void gs_bfly(u64& a, u64& b, u64 w, u64 ws, u64 q, u6
     a = s;
 }
 
+// Bank-conflict-free twiddle runs. In stage p of a stage block with layout
+// lo, lane l / register j reads group i = k0 >> (p+1): the low nj bits of i
+// come from j and the rest from the lane's high bits, so consecutive lanes
+// read entries 2^nj apart (64 B strides for nj = 2: 16 wavefronts per
+// LDS.128 instead of 4). Each staged run of 2^u entries is therefore
+// stored transposed, pos(i) = (i mod 2^nj) * 2^(u-nj) + (i >> nj), which puts
+// one register's entries for consecutive lanes in consecutive slots.
+template <int E, bool FWD>
+__host__ __device__ constexpr int stage_lo(int p) {
+    if constexpr (E == 8) return FWD ? (p >= 5 ? 5 : p >= 2 ? 2 : 0) : (p <= 2 ? 0 : p <= 5 ? 3 : 5);
+    else return FWD ? (p >= 5 ? 5 : p >= 3 ? 3 : p >= 1 ? 1 : 0) : (p <= 1 ? 0 : p <= 3 ? 2 : p <= 5 ? 4 : 5);
+}
+template <int E, bool FWD>
+__host__ __device__ constexpr int tw_nj(int u) {
+    constexpr int LOGE = WGeo<E>::LOGE, LOGM = WGeo<E>::LOGM;
+    const int p = LOGM - 1 - u, lo = stage_lo<E, FWD>(p);
+    return LOGM - lo - LOGE > 0 ? lo + LOGE - p - 1 : 0;  // no lane-high bits: broadcast, keep order
+}
+template <int E, bool FWD>
+__host__ __device__ constexpr u32 tw_nj_mask() {
+    u32 m = 0;
+    for (int u = 0; u < WGeo<E>::LOGM; ++u) m |= u32(tw_nj<E, FWD>(u)) << (2 * u);
+    return m;
+}
+__device__ __forceinline__ u32 tw_pos(u32 u, u32 nj, u32 i) {
+    return ((i & ((1u << nj) - 1)) << (u - nj)) | (i >> nj);
+}
+// inverse of tw_pos: the group index stored at position pl
+__device__ __forceinline__ u32 tw_src(u32 u, u32 nj, u32 pl) {
+    return ((pl & ((1u << (u - nj)) - 1)) << nj) | (pl >> (u - nj));
+}
+
 // Staged-twiddle index for group i of stage-unit u: CHUNK blocks use the
 // per-u runs (8 chunks, this warp's chunk c), column blocks the raw index.
-template <bool CHUNK>
+template <int E, bool FWD, bool CHUNK>
 __device__ __forceinline__ u32 tw_slot(u32 u, u32 c, u32 i) {
-    if constexpr (CHUNK) return 8 * ((1u << u) - 1) + (c << u) + i;
-    else return (1u << u) + i;
+    const u32 pi = tw_pos(u, u32(tw_nj<E, FWD>(int(u))), i);
+    if constexpr (CHUNK) return 8 * ((1u << u) - 1) + (c << u) + pi;
+    else return (1u << u) + pi;
 }
 
 // Forward (CT) stages on bits HI..LO (descending) of layout LAY; stage s = LOGM-1-p.
@@ -91,7 +124,7 @@ __device__ __forceinline__ void wfwd(u64 (&v)[E], u32 lane, const u64* sw, const
         for (int j = 0; j < E; ++j) {
             if (j & (1 << b)) continue;
             const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
-            const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
+            const u32 t = tw_slot<E, true, CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
             const ulonglong2 tw = reinterpret_cast<const ulonglong2*>(sw)[t];
             ct_bfly<SQ>(v[j], v[j | (1 << b)], tw.x, tw.y, q);
         }
@@ -109,7 +142,7 @@ __device__ __forceinline__ void winv(u64 (&v)[E], u32 lane, const u64* sw, const
         for (int j = 0; j < E; ++j) {
             if (j & (1 << b)) continue;
             const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
-            const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
+            const u32 t = tw_slot<E, false, CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
             const ulonglong2 tw = reinterpret_cast<const ulonglong2*>(sw)[t];
             gs_bfly<SQ>(v[j], v[j | (1 << b)], tw.x, tw.y, q, (2 * q) << p);
         }
@@ -143,7 +176,7 @@ __device__ __forceinline__ void wfwd_fp(double (&v)[E], u32 lane, const u64* sw,
         for (int j = 0; j < E; ++j) {
             if (j & (1 << b)) continue;
             const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
-            const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
+            const u32 t = tw_slot<E, true, CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
             const double2 tw = reinterpret_cast<const double2*>(sw)[t];
             const double x = fp_mulmod(v[j | (1 << b)], tw.x, tw.y, q);
             const double a = v[j];
@@ -165,7 +198,7 @@ __device__ __forceinline__ void winv_fp(double (&v)[E], u32 lane, const u64* sw,
         for (int j = 0; j < E; ++j) {
             if (j & (1 << b)) continue;
             const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
-            const u32 t = tw_slot<CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
+            const u32 t = tw_slot<E, false, CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
             const double2 tw = reinterpret_cast<const double2*>(sw)[t];
             const double a = v[j], bb = v[j | (1 << b)];
             v[j] = fp_reduce(__dadd_rn(a, bb), q, qi);
@@ -256,7 +289,7 @@ __device__ __forceinline__ void winv_all(u64 (&v)[E], u64* col, u32 lane, const 
 
 // Stage the 8-chunk twiddle runs of block bx: for u < LOGM,
 // sw[8(2^u-1) + t] = tab[2^(logN1+u) + 8 bx 2^u + t], t < 8*2^u.
-template <int E>
+template <int E, bool FWD>
 __device__ __forceinline__ void stage_chunk_twiddles(u64* sw, u64* sws, const u64* __restrict__ w,
                                                      const u64* __restrict__ ws, u32 logN1, u32 bx) {
     // flattened slot e -> (u, t): all of a thread's loads are issued before
@@ -265,15 +298,20 @@ __device__ __forceinline__ void stage_chunk_twiddles(u64* sw, u64* sws, const u6
     constexpr int PER = (TOT + 255) / 256;
     u64 a[PER], b[PER];
     u32 d[PER];
+    constexpr u32 NJ = tw_nj_mask<E, FWD>();
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
         const u32 e = threadIdx.x + 256u * k;
-        d[k] = e;
+        d[k] = u32(TOT);
         if (e < u32(TOT)) {
             const u32 u = 31 - __clz((e >> 3) + 1);  // e in [8(2^u - 1), 8(2^(u+1) - 1))
-            const u32 src = (1u << (logN1 + u)) + ((8 * bx) << u) + (e - 8 * ((1u << u) - 1));
+            // thread e fills slot e (conflict-free stores) from the group
+            // index whose transposed position it is
+            const u32 t = e - 8 * ((1u << u) - 1), pl = t & ((1u << u) - 1);
+            const u32 src = (1u << (logN1 + u)) + ((8 * bx) << u) + (t - pl) + tw_src(u, (NJ >> (2 * u)) & 3, pl);
             a[k] = __ldg(w + src);
             b[k] = __ldg(ws + src);
+            d[k] = e;
         }
     }
 #pragma unroll
@@ -281,11 +319,18 @@ __device__ __forceinline__ void stage_chunk_twiddles(u64* sw, u64* sws, const u6
         if (d[k] < u32(TOT)) reinterpret_cast<ulonglong2*>(sw)[d[k]] = make_ulonglong2(a[k], b[k]);
 }
 
-template <int E>
+template <int E, bool FWD>
 __device__ __forceinline__ void stage_col_twiddles(u64* sw, u64* sws, const u64* __restrict__ w,
                                                    const u64* __restrict__ ws) {
-    for (u32 t = threadIdx.x; t < u32(WGeo<E>::M); t += 256)
-        reinterpret_cast<ulonglong2*>(sw)[t] = make_ulonglong2(__ldg(w + t), __ldg(ws + t));
+    constexpr u32 NJ = tw_nj_mask<E, FWD>();
+    for (u32 d = threadIdx.x; d < u32(WGeo<E>::M); d += 256) {
+        u32 t = 0;
+        if (d > 0) {
+            const u32 u = 31 - __clz(d);
+            t = (1u << u) + tw_src(u, (NJ >> (2 * u)) & 3, d - (1u << u));
+        }
+        reinterpret_cast<ulonglong2*>(sw)[d] = make_ulonglong2(__ldg(w + t), __ldg(ws + t));
+    }
 }
 
 template <int E>
@@ -318,7 +363,7 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int lev
     u64* xd = data + size_t(row) * N + c0;
     for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
         sm[(e & 7) * Gm::CS + wpad(e >> 3)] = xs[size_t(e >> 3) * N2 + (e & 7)];
-    stage_col_twiddles<E>(sw, sws, w, w + N);
+    stage_col_twiddles<E, true>(sw, sws, w, w + N);
     __syncthreads();
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     u64* col = sm + warp * Gm::CS;
@@ -369,7 +414,7 @@ kw_fwd_chunks(DevRing R, u64* data, u32 row_base, u32 rpp, int level, u32 logN1,
     u64 v[E];
 #pragma unroll
     for (int j = 0; j < E; ++j) v[j] = x[lane + 32 * j];
-    stage_chunk_twiddles<E>(sw, sws, w, w + N, logN1, blockIdx.x);
+    stage_chunk_twiddles<E, true>(sw, sws, w, w + N, logN1, blockIdx.x);
     __syncthreads();
     if (fp) {  // phase-1 doubles in, canonical u64 out
         const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
@@ -428,7 +473,7 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int l
         v[2 * j] = t.x;
         v[2 * j + 1] = t.y;
     }
-    stage_chunk_twiddles<E>(sw, sws, w, w + N, logN1, blockIdx.x);
+    stage_chunk_twiddles<E, false>(sw, sws, w, w + N, logN1, blockIdx.x);
     __syncthreads();
     if (fp) {  // canonical u64 in, doubles (|v| <= 1.5q, raw bits) out to phase B
         const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
@@ -470,7 +515,7 @@ kw_inv_cols(DevRing R, u64* data, u32 row_base, u32 rpp, int level) {
     u64* x = data + size_t(row) * N + blockIdx.x * 8;
     for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
         sm[(e & 7) * Gm::CS + wpad(e >> 3)] = x[size_t(e >> 3) * N2 + (e & 7)];
-    stage_col_twiddles<E>(sw, sws, w, w + N);
+    stage_col_twiddles<E, false>(sw, sws, w, w + N);
     __syncthreads();
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     u64* col = sm + warp * Gm::CS;

@@ -196,19 +196,22 @@ def run_concurrent(T, ring, fn, items, streams):
     results. Results come back in item order, so every later reduction runs
     in the reference's order."""
     items = list(items)
-    if streams <= 1 or len(items) <= 1 or not hasattr(T, "stream_scope"):
+    if streams <= 1 or len(items) <= 1:
         return [fn(x) for x in items]
+    import contextlib
     import threading
     out = [None] * len(items)
     errs = []
     k = min(streams, len(items))
+    scoped = hasattr(T, "stream_scope")  # the CPU reference: plain threads (protocol.hpp:297-311)
 
     def worker(w):
         try:
-            with T.stream_scope(ring, w):
+            with (T.stream_scope(ring, w) if scoped else contextlib.nullcontext()):
                 for i in range(w, len(items), k):
                     out[i] = fn(items[i])
-                ring.synchronize()
+                if scoped:
+                    ring.synchronize()
         except BaseException as e:  # surfaced on the caller's thread
             errs.append(e)
 
