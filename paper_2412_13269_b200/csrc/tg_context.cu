@@ -62,6 +62,8 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
 
     auto* ctx = new tg_context();
     ctx->device = device;
+    if (cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || ctx->sms <= 0)
+        ctx->sms = 148;
     DevRing& R = ctx->ring;
     R.N = degree;
     R.logN = 0;

@@ -179,6 +179,7 @@ struct ProfRecord {
 
 struct tg_context {
     int device = 0;
+    int sms = 148;  // multiprocessor count (grid sizing)
     tg::DevRing ring{};
     std::vector<tg::u64> h_q;
     std::vector<tg::u64> h_ratio;

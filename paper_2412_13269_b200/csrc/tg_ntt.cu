@@ -211,13 +211,10 @@ int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
     ProfScope prof(ctx, TG_OP_NTT_FWD, 16.0 * total * R.N, s);
     int e1 = 0, e2 = 0;
-    if (warp_plan(R.logN, e1, e2)) {
-        for (u32 base = 0; base < total; base += 65535) {
-            const u32 rows = std::min(65535u, total - base);
-            if (e1 == 8) launch_fwd_w<8, 8>(R, data, src, base, rows, rpp, level, s, skip_gs);
-            else if (e2 == 8) launch_fwd_w<4, 8>(R, data, src, base, rows, rpp, level, s, skip_gs);
-            else launch_fwd_w<4, 4>(R, data, src, base, rows, rpp, level, s, skip_gs);
-        }
+    if (warp_plan(R.logN, e1, e2) && npolys <= 65535) {
+        if (e1 == 8) launch_fwd_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs);
+        else if (e2 == 8) launch_fwd_w<4, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs);
+        else launch_fwd_w<4, 4>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs);
         TG_LAUNCH_CHECK();
         return TG_OK;
     }
@@ -239,13 +236,10 @@ int ntt_inverse_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
     ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * total * R.N, s);
     int e1 = 0, e2 = 0;
-    if (warp_plan(R.logN, e1, e2)) {
-        for (u32 base = 0; base < total; base += 65535) {
-            const u32 rows = std::min(65535u, total - base);
-            if (e1 == 8) launch_inv_w<8, 8>(R, data, src, base, rows, rpp, level, s);
-            else if (e2 == 8) launch_inv_w<4, 8>(R, data, src, base, rows, rpp, level, s);
-            else launch_inv_w<4, 4>(R, data, src, base, rows, rpp, level, s);
-        }
+    if (warp_plan(R.logN, e1, e2) && npolys <= 65535) {
+        if (e1 == 8) launch_inv_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s);
+        else if (e2 == 8) launch_inv_w<4, 8>(R, ctx->sms, data, src, rpp, npolys, level, s);
+        else launch_inv_w<4, 4>(R, ctx->sms, data, src, rpp, npolys, level, s);
         TG_LAUNCH_CHECK();
         return TG_OK;
     }

@@ -25,6 +25,9 @@ constexpr u64 kSmallQ = u64(1) << 55;  // lazy-bound threshold of the SQ path
 #ifndef NTT_MIN_BLOCKS
 #define NTT_MIN_BLOCKS 4
 #endif
+#ifndef NTT_CHUNK_MIN_BLOCKS
+#define NTT_CHUNK_MIN_BLOCKS 3  // room for the next poly's chunk in registers
+#endif
 
 template <int E>
 struct WGeo {
@@ -333,215 +336,303 @@ __device__ __forceinline__ void stage_col_twiddles(u64* sw, u64* sws, const u64*
     }
 }
 
+// ---- poly loop ------------------------------------------------------------
+// Grid: x = column / chunk block, y = row r of a poly (modulus), z = group of
+// `ppb` polys. A block transforms row r of each of its polys in turn: the
+// staged twiddles (modulus r) are reused for every poly, and the next poly's
+// input is fetched while the current one is computed (cp.async into a second
+// tile for the column phase; registers for the chunk phase).
+__device__ __forceinline__ u32 next_poly(u32 p, u32 pend, u32 r, u32 rpp, int level, u32 skip_gs) {
+    while (p < pend && ntt_row_skipped(p * rpp + r, rpp, level, skip_gs)) ++p;
+    return p;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const u32 a = static_cast<u32>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
+}
+
 template <int E>
-constexpr size_t col_smem() {
-    return size_t(8) * (8 * WGeo<E>::CS + 2 * WGeo<E>::TW_COL);
+constexpr size_t col_smem() {  // two tiles + twiddles
+    return size_t(8) * (16 * WGeo<E>::CS + 2 * WGeo<E>::TW_COL);
 }
 template <int E>
 constexpr size_t chunk_smem() {
     return size_t(8) * (8 * WGeo<E>::CS + 2 * WGeo<E>::TW_CHUNK);
 }
 
+// Column tile of row `row` (8 columns x M1, element (m, c) at c*CS + wpad(m)).
+template <int E>
+__device__ __forceinline__ void issue_col_tile(u64* tile, const u64* src, u32 row, u32 c0, u32 N) {
+    using Gm = WGeo<E>;
+    const u32 N2 = N >> Gm::LOGM;
+    const u64* xs = src + size_t(row) * N + c0;
+    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
+        cp_async8(&tile[(e & 7) * Gm::CS + wpad(e >> 3)], xs + size_t(e >> 3) * N2 + (e & 7));
+    cp_async_commit();
+}
+template <int E>
+__device__ __forceinline__ void store_col_tile(const u64* tile, u64* dst, u32 row, u32 c0, u32 N) {
+    using Gm = WGeo<E>;
+    const u32 N2 = N >> Gm::LOGM;
+    u64* xd = dst + size_t(row) * N + c0;
+    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
+        xd[size_t(e >> 3) * N2 + (e & 7)] = tile[(e & 7) * Gm::CS + wpad(e >> 3)];
+}
+
 // Phase 1 forward: 8 columns x M1 rows, stages 0 .. log M1 - 1.
 template <int E>
 __global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
-kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int level, u32 skip_gs) {
+kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, int level, u32 skip_gs) {
     using Gm = WGeo<E>;
-    if (ntt_row_skipped(row_base + blockIdx.y, rpp, level, skip_gs)) return;
+    const u32 r = blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
+    u32 p = next_poly(blockIdx.z * ppb, pend, r, rpp, level, skip_gs);
+    if (p >= pend) return;
     extern __shared__ u64 dyn[];
-    u64* sm = dyn;
-    u64* sw = dyn + 8 * Gm::CS;
+    u64* tiles = dyn;
+    u64* sw = dyn + 16 * Gm::CS;
     u64* sws = sw + Gm::TW_COL;
-    const u32 N = R.N, N2 = N >> Gm::LOGM;
-    const u32 row = row_base + blockIdx.y;
-    const u32 mi = mod_index(row % rpp, level, R.q_count);
+    const u32 N = R.N;
+    const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
     const bool fp = q < kFpMaxQ;  // FP64 path; the phase-2 kernel makes the same choice
     const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N) : R.tw + size_t(mi) * 4 * N;
     const u32 c0 = blockIdx.x * 8;
-    const u64* xs = src + size_t(row) * N + c0;
-    u64* xd = data + size_t(row) * N + c0;
-    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
-        sm[(e & 7) * Gm::CS + wpad(e >> 3)] = xs[size_t(e >> 3) * N2 + (e & 7)];
+    issue_col_tile<E>(tiles, src, p * rpp + r, c0, N);
     stage_col_twiddles<E, true>(sw, sws, w, w + N);
-    __syncthreads();
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    u64* col = sm + warp * Gm::CS;
-    if (fp) {  // canonical u64 in, doubles (|v| <= q/2 + 1, raw bits) out to phase 2
-        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
-        double v[E];
+    u32 cur = 0;
+    while (p < pend) {
+        const u32 pn = next_poly(p + 1, pend, r, rpp, level, skip_gs);
+        if (pn < pend) {
+            issue_col_tile<E>(tiles + (cur ^ 1) * 8 * Gm::CS, src, pn * rpp + r, c0, N);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        u64* tile = tiles + cur * 8 * Gm::CS;
+        u64* col = tile + warp * Gm::CS;
+        if (fp) {  // canonical u64 in, doubles (|v| <= q/2 + 1, raw bits) out to phase 2
+            const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+            double v[E];
 #pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = u2d(col[wpad(lane + 32 * j)]);
-        wfwd_all_fp<E, false>(v, col, lane, sw, qd, qi, 0);
-        __syncwarp();
-        double* cold = reinterpret_cast<double*>(col);
+            for (int j = 0; j < E; ++j) v[j] = u2d(col[wpad(lane + 32 * j)]);
+            wfwd_all_fp<E, false>(v, col, lane, sw, qd, qi, 0);
+            __syncwarp();
+            double* cold = reinterpret_cast<double*>(col);
 #pragma unroll
-        for (int j = 0; j < E; ++j) cold[wpad((lane << Gm::LOGE) | j)] = v[j];
-    } else {
-        u64 v[E];
+            for (int j = 0; j < E; ++j) cold[wpad((lane << Gm::LOGE) | j)] = v[j];
+        } else {
+            u64 v[E];
 #pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = col[wpad(lane + 32 * j)];
-        if (q < kSmallQ) wfwd_all<E, false, true>(v, col, lane, sw, sws, q, 0);
-        else wfwd_all<E, false, false>(v, col, lane, sw, sws, q, 0);
-        __syncwarp();
+            for (int j = 0; j < E; ++j) v[j] = col[wpad(lane + 32 * j)];
+            if (q < kSmallQ) wfwd_all<E, false, true>(v, col, lane, sw, sws, q, 0);
+            else wfwd_all<E, false, false>(v, col, lane, sw, sws, q, 0);
+            __syncwarp();
 #pragma unroll
-        for (int j = 0; j < E; ++j) col[wpad((lane << Gm::LOGE) | j)] = v[j];
+            for (int j = 0; j < E; ++j) col[wpad((lane << Gm::LOGE) | j)] = v[j];
+        }
+        __syncthreads();
+        store_col_tile<E>(tile, data, p * rpp + r, c0, N);
+        __syncthreads();  // the tile is the next prefetch target
+        p = pn;
+        cur ^= 1;
     }
-    __syncthreads();
-    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
-        xd[size_t(e >> 3) * N2 + (e & 7)] = sm[(e & 7) * Gm::CS + wpad(e >> 3)];
 }
 
 // Phase 2 forward: one warp per contiguous chunk of M2, final canonical reduce.
 template <int E>
-__global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
-kw_fwd_chunks(DevRing R, u64* data, u32 row_base, u32 rpp, int level, u32 logN1, u32 skip_gs) {
+__global__ void __launch_bounds__(256, NTT_CHUNK_MIN_BLOCKS)
+kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 logN1, u32 skip_gs) {
     using Gm = WGeo<E>;
-    if (ntt_row_skipped(row_base + blockIdx.y, rpp, level, skip_gs)) return;
+    const u32 r = blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
+    u32 p = next_poly(blockIdx.z * ppb, pend, r, rpp, level, skip_gs);
+    if (p >= pend) return;
     extern __shared__ u64 dyn[];
     u64* sm = dyn;
     u64* sw = dyn + 8 * Gm::CS;
     u64* sws = sw + Gm::TW_CHUNK;
     const u32 N = R.N;
-    const u32 row = row_base + blockIdx.y;
-    const u32 mi = mod_index(row % rpp, level, R.q_count);
+    const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
     const bool fp = q < kFpMaxQ;
     const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N) : R.tw + size_t(mi) * 4 * N;
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const u32 chunk = blockIdx.x * 8 + warp;
-    u64* x = data + size_t(row) * N + size_t(chunk) * Gm::M;
-    u64 v[E];
+    const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
+    u64 v[E], nx[E];
+    {
+        const u64* x = data + size_t(p * rpp + r) * N + off;
 #pragma unroll
-    for (int j = 0; j < E; ++j) v[j] = x[lane + 32 * j];
+        for (int j = 0; j < E; ++j) v[j] = x[lane + 32 * j];
+    }
     stage_chunk_twiddles<E, true>(sw, sws, w, w + N, logN1, blockIdx.x);
     __syncthreads();
-    if (fp) {  // phase-1 doubles in, canonical u64 out
-        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
-        double vd[E];
+    while (p < pend) {
+        const u32 pn = next_poly(p + 1, pend, r, rpp, level, skip_gs);
+        if (pn < pend) {  // next poly's chunk in flight during this one's stages
+            const u64* x = data + size_t(pn * rpp + r) * N + off;
 #pragma unroll
-        for (int j = 0; j < E; ++j) vd[j] = __longlong_as_double(static_cast<long long>(v[j]));
-        wfwd_all_fp<E, true>(vd, sm + warp * Gm::CS, lane, sw, qd, qi, warp);
-#pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = fp_canonical(vd[j], qd);
-    } else if (q < kSmallQ) {
-        wfwd_all<E, true, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
-        const u64 one = R.one_shoup[mi];
-#pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = shoup(v[j], 1, one, q);  // < 33q -> canonical
-    } else {
-        wfwd_all<E, true, false>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
-        const u64 q2 = 2 * q;
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-            u64 t = v[j];
-            if (t >= q2) t -= q2;
-            if (t >= q) t -= q;
-            v[j] = t;
+            for (int j = 0; j < E; ++j) nx[j] = x[lane + 32 * j];
         }
-    }
-    ulonglong2* x2 = reinterpret_cast<ulonglong2*>(x + (lane << Gm::LOGE));
+        if (fp) {  // phase-1 doubles in, canonical u64 out
+            const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+            double vd[E];
 #pragma unroll
-    for (int j = 0; j < E / 2; ++j) x2[j] = make_ulonglong2(v[2 * j], v[2 * j + 1]);
+            for (int j = 0; j < E; ++j) vd[j] = __longlong_as_double(static_cast<long long>(v[j]));
+            wfwd_all_fp<E, true>(vd, sm + warp * Gm::CS, lane, sw, qd, qi, warp);
+#pragma unroll
+            for (int j = 0; j < E; ++j) v[j] = fp_canonical(vd[j], qd);
+        } else if (q < kSmallQ) {
+            wfwd_all<E, true, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+            const u64 one = R.one_shoup[mi];
+#pragma unroll
+            for (int j = 0; j < E; ++j) v[j] = shoup(v[j], 1, one, q);  // < 33q -> canonical
+        } else {
+            wfwd_all<E, true, false>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+            const u64 q2 = 2 * q;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                u64 t = v[j];
+                if (t >= q2) t -= q2;
+                if (t >= q) t -= q;
+                v[j] = t;
+            }
+        }
+        ulonglong2* x2 =
+            reinterpret_cast<ulonglong2*>(data + size_t(p * rpp + r) * N + off + (lane << Gm::LOGE));
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) x2[j] = make_ulonglong2(v[2 * j], v[2 * j + 1]);
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = nx[j];
+        p = pn;
+    }
 }
 
 // Phase A inverse: one warp per contiguous chunk (stages t = 1 .. M2/2).
 template <int E>
-__global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
-kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 row_base, u32 rpp, int level, u32 logN1) {
+__global__ void __launch_bounds__(256, NTT_CHUNK_MIN_BLOCKS)
+kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, int level, u32 logN1) {
     using Gm = WGeo<E>;
+    const u32 r = blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
+    u32 p = blockIdx.z * ppb;
+    if (p >= pend) return;
     extern __shared__ u64 dyn[];
     u64* sm = dyn;
     u64* sw = dyn + 8 * Gm::CS;
     u64* sws = sw + Gm::TW_CHUNK;
     const u32 N = R.N;
-    const u32 row = row_base + blockIdx.y;
-    const u32 mi = mod_index(row % rpp, level, R.q_count);
+    const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
     const bool fp = q < kFpMaxQ;
     const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N + 2 * size_t(N))
                       : R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const u32 chunk = blockIdx.x * 8 + warp;
-    const ulonglong2* xs2 =
-        reinterpret_cast<const ulonglong2*>(src + size_t(row) * N + size_t(chunk) * Gm::M + (lane << Gm::LOGE));
-    u64* x = data + size_t(row) * N + size_t(chunk) * Gm::M;
-    u64 v[E];
+    const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
+    u64 v[E], nx[E];
+    auto load = [&](u64 (&dst)[E], u32 pp) {
+        const ulonglong2* xs2 =
+            reinterpret_cast<const ulonglong2*>(src + size_t(pp * rpp + r) * N + off + (lane << Gm::LOGE));
 #pragma unroll
-    for (int j = 0; j < E / 2; ++j) {
-        const ulonglong2 t = xs2[j];
-        v[2 * j] = t.x;
-        v[2 * j + 1] = t.y;
-    }
+        for (int j = 0; j < E / 2; ++j) {
+            const ulonglong2 t = xs2[j];
+            dst[2 * j] = t.x;
+            dst[2 * j + 1] = t.y;
+        }
+    };
+    load(v, p);
     stage_chunk_twiddles<E, false>(sw, sws, w, w + N, logN1, blockIdx.x);
     __syncthreads();
-    if (fp) {  // canonical u64 in, doubles (|v| <= 1.5q, raw bits) out to phase B
-        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
-        double vd[E];
+    for (; p < pend; ++p) {
+        if (p + 1 < pend) load(nx, p + 1);
+        if (fp) {  // canonical u64 in, doubles (|v| <= 1.5q, raw bits) out to phase B
+            const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+            double vd[E];
 #pragma unroll
-        for (int j = 0; j < E; ++j) vd[j] = u2d(v[j]);
-        winv_all_fp<E, true>(vd, sm + warp * Gm::CS, lane, sw, qd, qi, warp);
+            for (int j = 0; j < E; ++j) vd[j] = u2d(v[j]);
+            winv_all_fp<E, true>(vd, sm + warp * Gm::CS, lane, sw, qd, qi, warp);
 #pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = static_cast<u64>(__double_as_longlong(vd[j]));
-    } else if (q < kSmallQ) {
-        winv_all<E, true, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
-        const u64 one = R.one_shoup[mi];
+            for (int j = 0; j < E; ++j) v[j] = static_cast<u64>(__double_as_longlong(vd[j]));
+        } else if (q < kSmallQ) {
+            winv_all<E, true, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+            const u64 one = R.one_shoup[mi];
 #pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = shoup_lazy(v[j], 1, one, q);  // < 512q -> [0, 2q)
-    } else {
-        winv_all<E, true, false>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+            for (int j = 0; j < E; ++j) v[j] = shoup_lazy(v[j], 1, one, q);  // < 512q -> [0, 2q)
+        } else {
+            winv_all<E, true, false>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+        }
+        u64* x = data + size_t(p * rpp + r) * N + off;
+#pragma unroll
+        for (int j = 0; j < E; ++j) x[lane + 32 * j] = v[j];
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = nx[j];
     }
-#pragma unroll
-    for (int j = 0; j < E; ++j) x[lane + 32 * j] = v[j];
 }
 
 // Phase B inverse: 8 columns x M1 rows, then the N^-1 scaling.
 template <int E>
 __global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
-kw_inv_cols(DevRing R, u64* data, u32 row_base, u32 rpp, int level) {
+kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level) {
     using Gm = WGeo<E>;
+    const u32 r = blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
+    u32 p = blockIdx.z * ppb;
+    if (p >= pend) return;
     extern __shared__ u64 dyn[];
-    u64* sm = dyn;
-    u64* sw = dyn + 8 * Gm::CS;
+    u64* tiles = dyn;
+    u64* sw = dyn + 16 * Gm::CS;
     u64* sws = sw + Gm::TW_COL;
-    const u32 N = R.N, N2 = N >> Gm::LOGM;
-    const u32 row = row_base + blockIdx.y;
-    const u32 mi = mod_index(row % rpp, level, R.q_count);
+    const u32 N = R.N;
+    const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
     const bool fp = q < kFpMaxQ;
     const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N + 2 * size_t(N))
                       : R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
     const u64 ninv = R.ninv[2 * mi], ninv_s = R.ninv[2 * mi + 1];
-    u64* x = data + size_t(row) * N + blockIdx.x * 8;
-    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
-        sm[(e & 7) * Gm::CS + wpad(e >> 3)] = x[size_t(e >> 3) * N2 + (e & 7)];
+    const u32 c0 = blockIdx.x * 8;
+    issue_col_tile<E>(tiles, data, p * rpp + r, c0, N);
     stage_col_twiddles<E, false>(sw, sws, w, w + N);
-    __syncthreads();
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    u64* col = sm + warp * Gm::CS;
-    if (fp) {  // phase-A doubles in, canonical u64 out (N^-1 applied in FP64)
-        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1], nd = R.qd[4 * mi + 2], ndq = R.qd[4 * mi + 3];
-        const double* cold = reinterpret_cast<const double*>(col);
-        double v[E];
+    u32 cur = 0;
+    for (; p < pend; ++p) {
+        if (p + 1 < pend) {
+            issue_col_tile<E>(tiles + (cur ^ 1) * 8 * Gm::CS, data, (p + 1) * rpp + r, c0, N);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        u64* tile = tiles + cur * 8 * Gm::CS;
+        u64* col = tile + warp * Gm::CS;
+        if (fp) {  // phase-A doubles in, canonical u64 out (N^-1 applied in FP64)
+            const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1], nd = R.qd[4 * mi + 2], ndq = R.qd[4 * mi + 3];
+            const double* cold = reinterpret_cast<const double*>(col);
+            double v[E];
 #pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = cold[wpad((lane << Gm::LOGE) | j)];
-        winv_all_fp<E, false>(v, col, lane, sw, qd, qi, 0);
-        __syncwarp();
+            for (int j = 0; j < E; ++j) v[j] = cold[wpad((lane << Gm::LOGE) | j)];
+            winv_all_fp<E, false>(v, col, lane, sw, qd, qi, 0);
+            __syncwarp();
 #pragma unroll
-        for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canonical(fp_mulmod(v[j], nd, ndq, qd), qd);
-    } else {
-        u64 v[E];
+            for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canonical(fp_mulmod(v[j], nd, ndq, qd), qd);
+        } else {
+            u64 v[E];
 #pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = col[wpad((lane << Gm::LOGE) | j)];
-        if (q < kSmallQ) winv_all<E, false, true>(v, col, lane, sw, sws, q, 0);
-        else winv_all<E, false, false>(v, col, lane, sw, sws, q, 0);
-        __syncwarp();
+            for (int j = 0; j < E; ++j) v[j] = col[wpad((lane << Gm::LOGE) | j)];
+            if (q < kSmallQ) winv_all<E, false, true>(v, col, lane, sw, sws, q, 0);
+            else winv_all<E, false, false>(v, col, lane, sw, sws, q, 0);
+            __syncwarp();
 #pragma unroll
-        for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = shoup(v[j], ninv, ninv_s, q);
+            for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = shoup(v[j], ninv, ninv_s, q);
+        }
+        __syncthreads();
+        store_col_tile<E>(tile, data, p * rpp + r, c0, N);
+        __syncthreads();  // the tile is the next prefetch target
+        cur ^= 1;
     }
-    __syncthreads();
-    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
-        x[size_t(e >> 3) * N2 + (e & 7)] = sm[(e & 7) * Gm::CS + wpad(e >> 3)];
 }
 
 // (E1, E2) for N = M1 * M2 handled by the warp kernels.
@@ -567,20 +658,34 @@ void set_smem_attrs() {
     (void)done;
 }
 
-template <int E1, int E2>
-void launch_fwd_w(const DevRing& R, u64* data, const u64* src, u32 base, u32 rows, u32 rpp, int level, cudaStream_t s,
-                  u32 skip_gs) {
-    set_smem_attrs<E1, E2>();
-    const u32 M1 = 32 * E1, M2 = 32 * E2;
-    kw_fwd_cols<E1><<<dim3(M2 / 8, rows), 256, col_smem<E1>(), s>>>(R, data, src, base, rpp, level, skip_gs);
-    kw_fwd_chunks<E2><<<dim3(M1 / 8, rows), 256, chunk_smem<E2>(), s>>>(R, data, base, rpp, level, WGeo<E1>::LOGM,
-                                                                          skip_gs);
+// Polys per block: keep at least ~4 blocks per SM in the grid, otherwise let
+// each block walk as many polys as possible (twiddle reuse, prefetch).
+inline u32 polys_per_block(u32 blocks_per_row, u32 rpp, u32 npolys, int sms) {
+    const u64 one = u64(blocks_per_row) * rpp * npolys, target = u64(sms) * 4;
+    const u64 ppb = one / target;
+    return u32(ppb < 1 ? 1 : ppb > npolys ? npolys : ppb);
 }
 
 template <int E1, int E2>
-void launch_inv_w(const DevRing& R, u64* data, const u64* src, u32 base, u32 rows, u32 rpp, int level, cudaStream_t s) {
+void launch_fwd_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp, u32 npolys, int level,
+                  cudaStream_t s, u32 skip_gs) {
     set_smem_attrs<E1, E2>();
     const u32 M1 = 32 * E1, M2 = 32 * E2;
-    kw_inv_chunks<E2><<<dim3(M1 / 8, rows), 256, chunk_smem<E2>(), s>>>(R, data, src, base, rpp, level, WGeo<E1>::LOGM);
-    kw_inv_cols<E1><<<dim3(M2 / 8, rows), 256, col_smem<E1>(), s>>>(R, data, base, rpp, level);
+    const u32 p1 = polys_per_block(M2 / 8, rpp, npolys, sms), p2 = polys_per_block(M1 / 8, rpp, npolys, sms);
+    kw_fwd_cols<E1><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, src, rpp, npolys,
+                                                                                         p1, level, skip_gs);
+    kw_fwd_chunks<E2><<<dim3(M1 / 8, rpp, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
+        R, data, rpp, npolys, p2, level, WGeo<E1>::LOGM, skip_gs);
+}
+
+template <int E1, int E2>
+void launch_inv_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp, u32 npolys, int level,
+                  cudaStream_t s) {
+    set_smem_attrs<E1, E2>();
+    const u32 M1 = 32 * E1, M2 = 32 * E2;
+    const u32 p1 = polys_per_block(M2 / 8, rpp, npolys, sms), p2 = polys_per_block(M1 / 8, rpp, npolys, sms);
+    kw_inv_chunks<E2><<<dim3(M1 / 8, rpp, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
+        R, data, src, rpp, npolys, p2, level, WGeo<E1>::LOGM);
+    kw_inv_cols<E1><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys, p1,
+                                                                                         level);
 }
