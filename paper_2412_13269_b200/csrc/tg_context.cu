@@ -376,7 +376,8 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
         u128 qmax = 0, allmax = 0;
         for (u32 r = 0; r < nq; ++r) qmax = std::max<u128>(qmax, mod[r]);
         for (u32 r = 0; r < nmod; ++r) allmax = std::max<u128>(allmax, mod[r]);
-        g->g.lazy_moddown = (u128(2 * K + 1) * qmax) < (u128(1) << 64);
+        // x + (neg terms) + 2Kq - (pos terms) < (4K + 1) q (k_mod_down_v)
+        g->g.lazy_moddown = (u128(4 * K + 2) * qmax) < (u128(1) << 64);
         g->g.lazy_modup = (u128(2 * gs) * allmax) < (u128(1) << 64);
     }
     size_t words = src.size() + conv.size() + md.size();

@@ -11,6 +11,7 @@
 // (ModDown) and keeps the <=16 source residues in registers, so each source
 // word is read once and each output word written once.
 #include "tg_internal.cuh"
+#include "tg_fp64.cuh"
 
 namespace tg {
 namespace {
@@ -189,6 +190,266 @@ k_mod_down(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict_
     }
 }
 
+// ---- register-blocked variants (lazy sums) --------------------------------
+// Same arithmetic as k_modup / k_mod_down, restructured so that the per-row
+// constants are staged once per block in shared memory (one uniform LDS.128
+// per (row, source) pair, shared by the CPT consecutive coefficients a thread
+// owns), the source residues stay in registers sized by a compile-time bound
+// (GMAX / KMAX), and every global access is a 16-byte vector.
+
+template <int GMAX, int CPT>
+__global__ void __launch_bounds__(kMUThreads)
+k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict__ d, int level,
+          const u64* __restrict__ d_eval, u32 rows_per_group) {
+    const u32 N = R.N, lvl = u32(level), K = R.K;
+    const u32 j = blockIdx.y, gs = G.group_size, first = j * gs;
+    const u32 active = min(gs, lvl + 1 - first);
+    const u32 rows_out = lvl + 1 + K, nrest = rows_out - active;
+    const u64* src_tb = G.src + ((size_t(j) * gs + (active - 1)) * gs) * 2;
+    const u64* conv_tb = G.conv + ((size_t(j) * gs + (active - 1)) * gs) * R.nmod * 2;
+    // FP64 rows: every source q_i and the target q_t below 2^50.5 (the
+    // q-chain): y_i * w mod q_t by fp_mulmod with |term| <= 0.68 q_t (|y_i|
+    // < 2^50.5 makes the quotient estimate error <= 0.18), summed exactly in
+    // doubles (reduced every 8 terms: |sum| <= 5.5 q_t < 2^53). Other rows
+    // (60-bit special primes) take the 64-bit Shoup path.
+    bool src_fp = true;
+    for (u32 i = 0; i < active; ++i) src_fp &= R.q[first + i] < kFpMaxQ;
+    extern __shared__ ulonglong2 smw[];                                  // [nrest][active] (w, w') | (w, w/q) doubles
+    u64* sq = reinterpret_cast<u64*>(smw + size_t(nrest) * active);      // [nrest] q, [nrest] one_shoup | 1/q
+    for (u32 e = threadIdx.x; e < nrest * active; e += kMUThreads) {
+        const u32 v = e / active, i = e - v * active;
+        const u32 r = v < first ? v : v + active;
+        const u32 t = mod_index(r, level, R.q_count);
+        const u64* cw = conv_tb + (size_t(i) * R.nmod + t) * 2;
+        if (src_fp && R.q[t] < kFpMaxQ) {
+            const double wd = u2d(cw[0]);
+            smw[e] = make_ulonglong2(static_cast<u64>(__double_as_longlong(wd)),
+                                     static_cast<u64>(__double_as_longlong(__ddiv_rn(wd, u2d(R.q[t])))));
+        } else {
+            smw[e] = make_ulonglong2(cw[0], cw[1]);
+        }
+    }
+    for (u32 v = threadIdx.x; v < nrest; v += kMUThreads) {
+        const u32 t = mod_index(v < first ? v : v + active, level, R.q_count);
+        sq[v] = R.q[t];
+        sq[nrest + v] = src_fp && R.q[t] < kFpMaxQ
+                            ? static_cast<u64>(__double_as_longlong(__ddiv_rn(1.0, u2d(R.q[t]))))
+                            : R.one_shoup[t];
+    }
+    __syncthreads();
+    const u32 c0 = (blockIdx.x * kMUThreads + threadIdx.x) * CPT;
+    if (c0 >= N) return;
+    u64* out = digits + size_t(j) * rows_out * N + c0;
+    u64 y[GMAX][CPT];
+    // blockIdx.z = group of output rows (more threads in flight); the
+    // sources are re-read per group, the own-group copy is group 0's
+    const u32 v_begin = blockIdx.z * rows_per_group, v_end = min(nrest, v_begin + rows_per_group);
+    const bool copy = blockIdx.z == 0;
+#pragma unroll
+    for (int i = 0; i < GMAX; ++i) {
+        if (u32(i) < active) {
+            const u32 s = first + i;
+            const u64 q = R.q[s], w = src_tb[2 * i], ws = src_tb[2 * i + 1];
+            u64 x[CPT];
+            if constexpr (CPT == 2) {
+                const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(d + size_t(s) * N + c0);
+                x[0] = t.x;
+                x[1] = t.y;
+                // own-group row: exact copy (eval form when the caller has it;
+                // the digit NTT then skips the row)
+                if (copy)
+                    *reinterpret_cast<ulonglong2*>(out + size_t(s) * N) =
+                        d_eval ? *reinterpret_cast<const ulonglong2*>(d_eval + size_t(s) * N + c0) : t;
+            } else {
+                x[0] = d[size_t(s) * N + c0];
+                if (copy) out[size_t(s) * N] = d_eval ? d_eval[size_t(s) * N + c0] : x[0];
+            }
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) y[i][cc] = shoup(x[cc], w, ws, q);
+        }
+    }
+    for (u32 v = v_begin; v < v_end; ++v) {
+        const u64 q = sq[v];
+        const ulonglong2* wr = smw + size_t(v) * active;
+        const u32 r = v < first ? v : v + active;
+        if (src_fp && q < kFpMaxQ) {
+            const double qd = u2d(q), qi = __longlong_as_double(static_cast<long long>(sq[nrest + v]));
+            double acc[CPT];
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) acc[cc] = 0.0;
+#pragma unroll
+            for (int i = 0; i < GMAX; ++i) {
+                if (u32(i) < active) {
+                    const ulonglong2 w = wr[i];
+                    const double wd = __longlong_as_double(static_cast<long long>(w.x));
+                    const double wq = __longlong_as_double(static_cast<long long>(w.y));
+#pragma unroll
+                    for (int cc = 0; cc < CPT; ++cc) {
+                        acc[cc] = __dadd_rn(acc[cc], fp_mulmod(u2d(y[i][cc]), wd, wq, qd));
+                        if ((i & 7) == 7 && u32(i + 1) < active) acc[cc] = fp_reduce(acc[cc], qd, qi);
+                    }
+                }
+            }
+            u64 o[CPT];
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) o[cc] = fp_canonical(fp_reduce(acc[cc], qd, qi), qd);
+            if constexpr (CPT == 2) *reinterpret_cast<ulonglong2*>(out + size_t(r) * N) = make_ulonglong2(o[0], o[1]);
+            else out[size_t(r) * N] = o[0];
+            continue;
+        }
+        u64 acc[CPT];
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) acc[cc] = 0;
+#pragma unroll
+        for (int i = 0; i < GMAX; ++i) {
+            if (u32(i) < active) {
+                const ulonglong2 w = wr[i];
+#pragma unroll
+                for (int cc = 0; cc < CPT; ++cc) acc[cc] += shoup_lazy(y[i][cc], w.x, w.y, q);
+            }
+        }
+        const u64 one = sq[nrest + v];
+        if constexpr (CPT == 2) {
+            *reinterpret_cast<ulonglong2*>(out + size_t(r) * N) =
+                make_ulonglong2(shoup(acc[0], 1, one, q), shoup(acc[1], 1, one, q));
+        } else {
+            out[size_t(r) * N] = shoup(acc[0], 1, one, q);
+        }
+    }
+}
+
+template <int KMAX, int CPT>
+__global__ void __launch_bounds__(256)
+k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict__ in, int level, u32 npolys,
+             const u64* __restrict__ addend, u32 rows_per_group) {
+    const u32 N = R.N, K = R.K, nq = R.q_count, lvl = u32(level);
+    const u32 rin = lvl + 1 + K, rout = lvl + 1;
+    const u64* c_s = G.md;                        // [K][2]
+    const u64* w_sr = G.md + 2 * K;               // [K][nq][4]: +w, +w', -w, -w'
+    const u64* pinv = w_sr + size_t(K) * nq * 4;  // [nq][2]
+    extern __shared__ ulonglong2 smd[];           // [rout][K] (+w, +w'), then [rout] (pinv, pinv'), [rout] q
+    ulonglong2* sp = smd + size_t(rout) * K;
+    u64* sq = reinterpret_cast<u64*>(sp + rout);
+    for (u32 e = threadIdx.x; e < rout * K; e += blockDim.x) {
+        const u32 r = e / K, s = e - r * K;
+        const u64* w = w_sr + (size_t(s) * nq + r) * 4;
+        smd[e] = make_ulonglong2(w[0], w[1]);
+    }
+    for (u32 r = threadIdx.x; r < rout; r += blockDim.x) {
+        sp[r] = make_ulonglong2(pinv[2 * r], pinv[2 * r + 1]);
+        sq[r] = R.q[r];
+    }
+    __syncthreads();
+    const u32 per_poly = N / CPT;
+    const u64 total = u64(npolys) * per_poly;
+    for (u64 idx = blockIdx.x * u64(blockDim.x) + threadIdx.x; idx < total; idx += u64(gridDim.x) * blockDim.x) {
+        const u32 p = u32(idx / per_poly);
+        const u32 c0 = u32(idx - u64(p) * per_poly) * CPT;
+        const u64* src = in + size_t(p) * rin * N + c0;
+        u64* dst = out + size_t(p) * rout * N + c0;
+        const u64* add = addend ? addend + size_t(p) * rout * N + c0 : nullptr;
+        u64 mag[KMAX][CPT];
+        bool neg[KMAX][CPT];
+#pragma unroll
+        for (int s = 0; s < KMAX; ++s) {
+            if (u32(s) < K) {
+                const u64 ps = R.q[nq + s], cw = c_s[2 * s], cws = c_s[2 * s + 1];
+                u64 x[CPT];
+                if constexpr (CPT == 2) {
+                    const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(src + size_t(lvl + 1 + s) * N);
+                    x[0] = t.x;
+                    x[1] = t.y;
+                } else {
+                    x[0] = src[size_t(lvl + 1 + s) * N];
+                }
+#pragma unroll
+                for (int cc = 0; cc < CPT; ++cc) {
+                    const u64 v = shoup(x[cc], cw, cws, ps);
+                    neg[s][cc] = v > ps / 2;  // to_centered (common.hpp:84-86)
+                    mag[s][cc] = neg[s][cc] ? ps - v : v;
+                }
+            }
+        }
+        const u32 r_end = min(rout, (blockIdx.y + 1) * rows_per_group);  // blockIdx.y = group of output rows
+        for (u32 r = blockIdx.y * rows_per_group; r < r_end; ++r) {
+            const u64 q = sq[r];
+            const ulonglong2* wr = smd + size_t(r) * K;
+            u64 ap[CPT], an[CPT];
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) ap[cc] = an[cc] = 0;
+#pragma unroll
+            for (int s = 0; s < KMAX; ++s) {
+                if (u32(s) < K) {
+                    const ulonglong2 w = wr[s];
+#pragma unroll
+                    for (int cc = 0; cc < CPT; ++cc) {
+                        const u64 t = shoup_lazy(mag[s][cc], w.x, w.y, q);
+                        ap[cc] += neg[s][cc] ? 0 : t;
+                        an[cc] += neg[s][cc] ? t : 0;
+                    }
+                }
+            }
+            const ulonglong2 pv = sp[r];
+            const u64 bias = 2 * u64(K) * q;
+            u64 o[CPT], x[CPT], a[CPT];
+            if constexpr (CPT == 2) {
+                const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(src + size_t(r) * N);
+                x[0] = t.x;
+                x[1] = t.y;
+                if (add) {
+                    const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(add + size_t(r) * N);
+                    a[0] = u.x;
+                    a[1] = u.y;
+                }
+            } else {
+                x[0] = src[size_t(r) * N];
+                if (add) a[0] = add[size_t(r) * N];
+            }
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) {
+                // (x - conv) * P^-1 with conv = ap - an (mod q)
+                o[cc] = shoup(x[cc] + an[cc] + bias - ap[cc], pv.x, pv.y, q);
+                if (add) o[cc] = add_mod(o[cc], a[cc], q);
+            }
+            if constexpr (CPT == 2) *reinterpret_cast<ulonglong2*>(dst + size_t(r) * N) = make_ulonglong2(o[0], o[1]);
+            else dst[size_t(r) * N] = o[0];
+        }
+    }
+}
+
+// Output-row groups so that about 1024 threads per SM are in flight.
+inline u32 row_groups(u64 threads, u32 rows, int sms) {
+    const u64 want = u64(sms) * 1024;
+    u64 g = (want + threads - 1) / threads;
+    return u32(g < 1 ? 1 : g > rows ? rows : g);
+}
+
+template <int GMAX, int CPT>
+void launch_modup_v(const DevRing& R, const GadgetDev& G, int sms, u64* digits, const u64* d, int level, u32 nd,
+                    const u64* d_eval, cudaStream_t s) {
+    // worst-case table over the digits (the last digit may be partial)
+    const u32 gs = G.group_size, rows_out = u32(level) + 1 + R.K;
+    const size_t smem = size_t(rows_out) * gs * 16 + size_t(rows_out) * 16;
+    const u32 bx = (R.N / CPT + kMUThreads - 1) / kMUThreads;
+    const u32 groups = row_groups(u64(bx) * nd * kMUThreads, rows_out, sms);
+    const u32 rpg = (rows_out + groups - 1) / groups;
+    const dim3 grid(bx, nd, (rows_out + rpg - 1) / rpg);
+    k_modup_v<GMAX, CPT><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg);
+}
+
+template <int KMAX, int CPT>
+void launch_mod_down_v(const DevRing& R, const GadgetDev& G, int sms, u64* out, const u64* in, int level,
+                       u32 npolys, const u64* addend, cudaStream_t s) {
+    const u32 rout = u32(level) + 1;
+    const size_t smem = size_t(rout) * R.K * 16 + size_t(rout) * 24;
+    const u64 work = u64(npolys) * R.N / CPT;
+    const u32 blocks = u32(std::min<u64>((work + 255) / 256, u64(sms) * 8));
+    const u32 groups = row_groups(u64(blocks) * 256, rout, sms);
+    const u32 rpg = (rout + groups - 1) / groups;
+    k_mod_down_v<KMAX, CPT><<<dim3(blocks, (rout + rpg - 1) / rpg), 256, smem, s>>>(R, G, out, in, level, npolys,
+                                                                                  addend, rpg);
+}
+
 }  // namespace
 
 int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, const u64* d_eval = nullptr) {
@@ -198,7 +459,11 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
     dim3 grid((R.N + kMUThreads - 1) / kMUThreads, nd);
     {
         ProfScope prof(ctx, TG_OP_MODUP, 8.0 * R.N * (double(level + 1) + double(nd) * (level + 1 + R.K)), s);
-        k_modup<<<grid, kMUThreads, 0, s>>>(R, g->g, digits, d, level, d_eval);
+        const GadgetDev& G = g->g;
+        if (G.lazy_modup && G.group_size <= 4) launch_modup_v<4, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s);
+        else if (G.lazy_modup && G.group_size <= 8) launch_modup_v<8, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s);
+        else if (G.lazy_modup && G.group_size <= 16) launch_modup_v<16, 1>(R, G, ctx->sms, digits, d, level, nd, d_eval, s);
+        else k_modup<<<grid, kMUThreads, 0, s>>>(R, G, digits, d, level, d_eval);
     }
     TG_LAUNCH_CHECK();
     return ntt_forward_oop(ctx, digits, digits, level, int(R.K), nd, s, d_eval ? g->g.group_size : 0);
@@ -208,7 +473,12 @@ int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaS
              const u64* addend = nullptr) {
     const DevRing& R = g->ctx->ring;
     ProfScope prof(g->ctx, TG_OP_MOD_DOWN, 8.0 * R.N * npolys * (2.0 * (level + 1) + R.K + (addend ? level + 1 : 0)), s);
-    k_mod_down<<<grid_for(size_t(npolys) * R.N), kThreads, 0, s>>>(R, g->g, out, in, level, npolys, addend);
+    const GadgetDev& G = g->g;
+    const int sms = g->ctx->sms;
+    if (G.lazy_moddown && R.K <= 4) launch_mod_down_v<4, 2>(R, G, sms, out, in, level, npolys, addend, s);
+    else if (G.lazy_moddown && R.K <= 8) launch_mod_down_v<8, 2>(R, G, sms, out, in, level, npolys, addend, s);
+    else if (G.lazy_moddown && R.K <= 16) launch_mod_down_v<16, 1>(R, G, sms, out, in, level, npolys, addend, s);
+    else k_mod_down<<<grid_for(size_t(npolys) * R.N), kThreads, 0, s>>>(R, G, out, in, level, npolys, addend);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
