@@ -596,7 +596,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=4, help="concurrent ciphertext pipelines per GPU")
+    ap.add_argument("--streams", type=int, default=8, help="concurrent record-block pipelines per GPU")
     ap.add_argument("--poly-eval", choices=["bsgs", "ladder"], default="bsgs",
                     help="Chebyshev evaluator of the sign stages (BASELINE configs specify BSGS)")
     ap.add_argument("--config", type=int, choices=[3, 4, 5], default=4,
