@@ -203,6 +203,7 @@ class Statement:
     def __init__(self, G, W, spec, rank=0, world=1, rotations=True, device=True):
         from paper_2412_13269_b200 import distributed as D
         self.G, self.W, self.spec = G, W, spec
+        self.batched, self.max_blocks = True, 8
         self.d = W.statement_data(spec)
         if not device:  # inputs only (the CPU reference arm)
             return
@@ -226,7 +227,10 @@ class Statement:
         if not self.blocks:
             return None
         q, bl = self._bind(client, self.blocks)
-        return self.W.statement_partial(self.S, q, bl, self.W.threshold_fn(self.S, self.chain, mode), streams)
+        thr = self.W.threshold_fn(self.S, self.chain, mode)
+        if self.batched:  # blocks as ciphertext batches (shared launches and key reads)
+            return self.W.statement_partial_batched(self.S, q, bl, thr, streams=streams, max_blocks=self.max_blocks)
+        return self.W.statement_partial(self.S, q, bl, thr, streams)
 
     def plain_count(self):
         return self.W.statement_plain_count(self.d)
@@ -303,6 +307,8 @@ def run_b200(args):
     t0 = time.time()
     from paper_2412_13269_b200 import distributed as D
     wl = WORKLOADS[args.config](G, W, spec, rank, world, rotations=(rank == 0))
+    if isinstance(wl, Statement):
+        wl.batched, wl.max_blocks = not args.no_batch, args.max_blocks
     S, chain = wl.S, wl.chain
     D.check_exact(world, S.primes)
     S.ring.synchronize()
@@ -458,6 +464,7 @@ def run_b200(args):
                    "q_bits": spec.q_bits, "special_primes": f"{spec.K}x{spec.sp_bits}b",
                    "dnum": -(-spec.nq // spec.group), "chain_degrees": list(spec.degrees), "alpha": spec.alpha,
                    "epsilon": spec.epsilon, "poly_eval": args.poly_eval, "streams": args.streams,
+                   "batched": bool(getattr(wl, "batched", False)), "max_blocks": getattr(wl, "max_blocks", None),
                    "record_blocks": spec.n_cts, "slots": spec.slots, "secret_hw": spec.h,
                    "amortized_us_per_record": round(ms_step * 1e3 / records, 4),
                    "l2": "1 GiB buffer written between timed steps; working set (keys, blocks) > 126 MB L2",
@@ -599,6 +606,9 @@ def main():
     ap.add_argument("--streams", type=int, default=8, help="concurrent record-block pipelines per GPU")
     ap.add_argument("--poly-eval", choices=["bsgs", "ladder"], default="bsgs",
                     help="Chebyshev evaluator of the sign stages (BASELINE configs specify BSGS)")
+    ap.add_argument("--no-batch", action="store_true",
+                    help="statement workloads: one ciphertext per pipeline instead of ciphertext batches")
+    ap.add_argument("--max-blocks", type=int, default=8, help="record blocks per ciphertext batch")
     ap.add_argument("--config", type=int, choices=[3, 4, 5], default=4,
                     help="BASELINE.json workload: 4 = full TETRIS statement (default), 3 = threshold count, "
                          "5 = scale-out stress")

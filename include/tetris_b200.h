@@ -176,6 +176,12 @@ int tg_rescale(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, ui
 int tg_lincomb(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* terms,
                const uint64_t* part_strides, const uint64_t* coeffs, const uint64_t* add_per_row,
                int add_all, int level, uint32_t nparts, int rescale, void* stream);
+/* tg_lincomb over a batch of ciphertexts stored part-major (parts
+ * [0, add_polys) are the batch's part-0 polys): the constant goes to each
+ * of the first add_polys parts. */
+int tg_lincomb_batch(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* terms,
+                     const uint64_t* part_strides, const uint64_t* coeffs, const uint64_t* add_per_row,
+                     int add_all, int level, uint32_t nparts, uint32_t add_polys, int rescale, void* stream);
 
 /* ---- CKKS products ------------------------------------------------------ */
 /* Evaluator::mul tensor step (ckks.hpp:229-237), eval form inputs:
@@ -238,6 +244,14 @@ int tg_switch_key_apply(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint
 int tg_keyswitch_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
                      const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
                      const uint64_t* add0, const uint64_t* add1, void* stream);
+/* tg_keyswitch_add for `npolys` sources under ONE key (a batch of
+ * ciphertexts relinearised together, e.g. the record blocks of a query):
+ * d, d_eval, out0, out1, add0, add1 each hold npolys polys back to back.
+ * Same per-source result as npolys tg_keyswitch_add calls; the key is read
+ * once per batch and every launch covers the whole batch. */
+int tg_keyswitch_add_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
+                           const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
+                           const uint64_t* add0, const uint64_t* add1, uint32_t npolys, void* stream);
 
 #ifdef __cplusplus
 }

@@ -82,11 +82,17 @@ struct Ciphertext {
     Domain domain = Domain::coeffs;
     u64 sk_id = 0;
     double noise_bound = 0.0;
+    // Extension (not in the reference): `batch` ciphertexts of one shape and
+    // scale evaluated together, stored part-major: part k of ciphertext i is
+    // parts[k * batch + i]. Every op treats a batch exactly as `batch`
+    // independent ciphertexts (same residues); launches and key reads are
+    // shared. See stack_ciphertexts / unstack_ciphertext.
+    u32 batch = 1;
 
     const RingParams& ring() const { return parts.at(0).ring(); }
     int level() const { return parts.at(0).level(); }
     Form form() const { return parts.at(0).form(); }
-    int degree() const { return int(parts.size()) - 1; }
+    int degree() const { return int(parts.size() / batch) - 1; }
     void to_coeff();
     void to_eval();
     void drop_to_level(int new_level);
@@ -94,6 +100,13 @@ struct Ciphertext {
     void sub_inplace(const Ciphertext& o);
     void negate_inplace();
 };
+
+// Batches: stack (copies into one part-major block; equal degree, level,
+// form, domain, key and scale within 1e-4), unstack and slice (copies of
+// ciphertexts [first, first + count) into their own block).
+Ciphertext stack_ciphertexts(const std::vector<Ciphertext>& cts);
+std::vector<Ciphertext> unstack_ciphertext(const Ciphertext& ct);
+Ciphertext slice_ciphertext(const Ciphertext& ct, u32 first, u32 count);
 
 // Switching key (rlwe.hpp:325-333). b[i]/a[i] are views into one HBM block.
 struct SwitchingKey {

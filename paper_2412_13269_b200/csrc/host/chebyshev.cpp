@@ -31,24 +31,43 @@ struct LinTerm {
     std::vector<u64> coef;  // one integer per q row 0..level
 };
 
+// The kernel addresses part p of term t at ptr[t] + p * stride[t]: parts of
+// a term must be uniformly strided (a single ciphertext always is; a batch
+// is when its parts share one block, else it is gathered first).
+bool uniform_parts(const std::vector<Poly>& parts) {
+    if (parts.size() <= 2) return true;
+    const u64 s = u64(parts[1].data() - parts[0].data());
+    for (std::size_t p = 2; p < parts.size(); ++p)
+        if (u64(parts[p].data() - parts[0].data()) != s * p) return false;
+    return true;
+}
+
 std::vector<Poly> fused_lincomb(const RingParams& R, const std::vector<LinTerm>& terms,
                                 const std::vector<u64>& add_per_row, int level, bool rescale) {
     const u32 nt = u32(terms.size());
+    const u32 B = terms[0].ct->batch;
     std::vector<const u64*> ptrs(nt);
     std::vector<u64> strides(nt);
     std::vector<u64> coeffs(std::size_t(nt) * (level + 1));
+    std::vector<Poly> keep;
     for (u32 t = 0; t < nt; ++t) {
         const Ciphertext& c = *terms[t].ct;
-        if (c.parts.size() != 2 || c.form() != Form::coeff || c.level() < level || c.parts[0].nspecial() != 0)
+        if (c.batch != B || c.parts.size() != 2 * B || c.form() != Form::coeff || c.level() < level ||
+            c.parts[0].nspecial() != 0)
             throw TetrisError("ckks", "fused combination expects degree-1 coefficient-form terms");
-        ptrs[t] = c.parts[0].data();
-        strides[t] = u64(c.parts[1].data()) / 8 - u64(c.parts[0].data()) / 8;  // words (mod 2^64)
+        if (uniform_parts(c.parts)) {
+            ptrs[t] = c.parts[0].data();
+            strides[t] = u64(c.parts[1].data()) / 8 - u64(c.parts[0].data()) / 8;  // words (mod 2^64)
+        } else {
+            ptrs[t] = detail::group_data(c.parts, 0, c.parts.size(), keep);
+            strides[t] = c.parts[0].words();
+        }
         for (int r = 0; r <= level; ++r) coeffs[std::size_t(t) * (level + 1) + r] = terms[t].coef[r];
     }
-    std::vector<Poly> out = fresh_parts(R, 2, rescale ? level - 1 : level, Form::coeff);
-    check_tg(tg_lincomb(R.dev(), const_cast<u64*>(out[0].data()), nt, ptrs.data(), strides.data(), coeffs.data(),
-                        add_per_row.empty() ? nullptr : add_per_row.data(), 0, level, 2, rescale ? 1 : 0,
-                        R.stream()));
+    std::vector<Poly> out = fresh_parts(R, int(2 * B), rescale ? level - 1 : level, Form::coeff);
+    check_tg(tg_lincomb_batch(R.dev(), const_cast<u64*>(out[0].data()), nt, ptrs.data(), strides.data(),
+                              coeffs.data(), add_per_row.empty() ? nullptr : add_per_row.data(), 0, level, 2 * B, B,
+                              rescale ? 1 : 0, R.stream()));
     return out;
 }
 
@@ -100,6 +119,7 @@ struct Ladder {
             res.parts = fused_lincomb(R, {LinTerm{&prod, residues_of(R, 2, lvl)}, LinTerm{&tc0, negv}}, {}, lvl, true);
             res.noise_bound = (two_noise + tc0.noise_bound) / double(ql) + 1.0;
         }
+        res.batch = prod.batch;
         res.scale = prod.scale / double(ql);
         res.domain = prod.domain;
         res.sk_id = prod.sk_id;
@@ -160,6 +180,7 @@ Ciphertext combine(Ladder& L, const Ciphertext& x, const std::vector<std::size_t
             for (std::size_t j = i; j < std::min(terms.size(), i + step); ++j) chunk.push_back(terms[j]);
             const bool last = i + step >= terms.size();
             Ciphertext next;
+            next.batch = x.batch;
             next.parts = fused_lincomb(R, chunk, last ? add : std::vector<u64>{}, lvl, last);
             next.scale = acc_scale;
             partial = std::move(next);
@@ -167,6 +188,7 @@ Ciphertext combine(Ladder& L, const Ciphertext& x, const std::vector<std::size_t
         out.parts = partial.parts;
     }
     const u64 ql = R.modulus(u32(lvl));
+    out.batch = x.batch;
     out.scale = acc_scale / double(ql);
     out.noise_bound = acc_noise / double(ql) + 1.0;
     out.domain = x.domain;

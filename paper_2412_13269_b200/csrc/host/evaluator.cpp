@@ -279,6 +279,7 @@ Ciphertext Evaluator::sub(const Ciphertext& a, const Ciphertext& b) const {
 Ciphertext Evaluator::mul(const Ciphertext& a, const Ciphertext& b) const {
     if (a.domain != b.domain) throw TetrisError("ckks", "domain tag mismatch in mul");
     if (a.degree() != 1 || b.degree() != 1) throw TetrisError("ckks", "mul expects degree-1 operands");
+    if (a.batch != b.batch) throw TetrisError("ckks", "batch size mismatch in mul");
     Ciphertext x = a, y = b;
     align_levels(x, y);
     if (x.level() == 0) throw TetrisError("ckks", "exhausted ciphertext: no level left to rescale");
@@ -286,11 +287,17 @@ Ciphertext Evaluator::mul(const Ciphertext& a, const Ciphertext& b) const {
     y.to_eval();
     const RingParams& R = ring();
     const int lvl = x.level();
-    std::vector<Poly> p = fresh_parts(R, 3, lvl, Form::eval);
-    check_tg(tg_tensor(R.dev(), const_cast<u64*>(p[0].data()), const_cast<u64*>(p[1].data()),
-                       const_cast<u64*>(p[2].data()), x.parts[0].data(), x.parts[1].data(), y.parts[0].data(),
-                       y.parts[1].data(), lvl, 1, R.stream()));
+    const u32 B = x.batch;
+    std::vector<Poly> keep;
+    const u64* x0 = detail::group_data(x.parts, 0, B, keep);
+    const u64* x1 = detail::group_data(x.parts, B, B, keep);
+    const u64* y0 = detail::group_data(y.parts, 0, B, keep);
+    const u64* y1 = detail::group_data(y.parts, B, B, keep);
+    std::vector<Poly> p = fresh_parts(R, int(3 * B), lvl, Form::eval);
+    check_tg(tg_tensor(R.dev(), const_cast<u64*>(p[0].data()), const_cast<u64*>(p[B].data()),
+                       const_cast<u64*>(p[2 * B].data()), x0, x1, y0, y1, lvl, B, R.stream()));
     Ciphertext out;
+    out.batch = B;
     out.parts = std::move(p);
     out.scale = x.scale * y.scale;
     out.domain = x.domain;
@@ -361,11 +368,28 @@ Ciphertext Evaluator::add_scalar(const Ciphertext& ct, double c) const {
     const RingParams& R = ring();
     std::vector<u64> add(R.moduli().size(), 0);
     for (int r = 0; r < p0.rows(); ++r) add[p0.modulus_index(r)] = scaled_residue(c * ct.scale, p0.row_modulus(r));
-    // keep all parts in one block (batched launches downstream)
-    const std::size_t np = ct.parts.size();
+    // keep all parts in one block (batched launches downstream); a batch
+    // adds the constant to each ciphertext's part 0 (parts [0, batch))
+    const std::size_t np = ct.parts.size(), B = ct.batch;
     std::vector<Poly> dst = fresh_parts(R, int(np), p0.level(), p0.form(), p0.nspecial());
-    check_tg(tg_poly_add_scalar(R.dev(), const_cast<u64*>(dst[0].data()), p0.data(), add.data(), tg_form(p0.form()),
-                                p0.level(), p0.nspecial(), 1, R.stream()));
+    std::vector<Poly> keep;
+    for (std::size_t i = 1; i < B; ++i)
+        if (ct.parts[i].level() != p0.level() || ct.parts[i].form() != p0.form())
+            throw TetrisError("ckks", "batch parts of different shapes");
+    check_tg(tg_poly_add_scalar(R.dev(), const_cast<u64*>(dst[0].data()), detail::group_data(ct.parts, 0, B, keep),
+                                add.data(), tg_form(p0.form()), p0.level(), p0.nspecial(), u32(B), R.stream()));
+    if (B > 1) {
+        if (contiguous(ct.parts, B, np - B)) {
+            check_tg(tg_memcpy_d2d(R.dev(), const_cast<u64*>(dst[B].data()), ct.parts[B].data(),
+                                   dst[B].words() * 8 * (np - B), R.stream()));
+        } else {
+            for (std::size_t i = B; i < np; ++i)
+                check_tg(tg_memcpy_d2d(R.dev(), const_cast<u64*>(dst[i].data()), ct.parts[i].data(),
+                                       dst[i].words() * 8, R.stream()));
+        }
+        out.parts = std::move(dst);
+        return out;
+    }
     for (std::size_t i = 1; i < np; ++i) {
         if (ct.parts[i].level() != p0.level() || ct.parts[i].form() != p0.form()) {  // irregular: keep as is
             out.parts[0] = dst[0];

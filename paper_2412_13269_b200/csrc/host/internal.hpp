@@ -40,6 +40,23 @@ inline bool exclusively_owned(const std::vector<Poly>& parts) {
 
 inline int tg_form(Form f) { return f == Form::eval ? TG_FORM_EVAL : TG_FORM_COEFF; }
 
+// Device pointer to parts[first..first+n) back to back: the parts' own
+// storage when they already are, else a gathered copy kept alive in `keep`.
+inline const u64* group_data(const std::vector<Poly>& parts, std::size_t first, std::size_t n,
+                             std::vector<Poly>& keep) {
+    if (n == 1 || contiguous(parts, first, n)) return parts[first].data();
+    const Poly& p0 = parts[first];
+    const RingParams& ring = p0.ring();
+    std::vector<Poly> g = fresh_parts(ring, int(n), p0.level(), p0.form(), p0.nspecial());
+    for (std::size_t i = 0; i < n; ++i) {
+        parts[first + i].check_shape(p0);
+        check_tg(tg_memcpy_d2d(ring.dev(), const_cast<u64*>(g[i].data()), parts[first + i].data(), g[i].words() * 8,
+                               ring.stream()));
+    }
+    keep.insert(keep.end(), g.begin(), g.end());
+    return g[0].data();
+}
+
 // Applies a per-part kernel `fn(dst, src, npolys)` to all parts, writing one
 // fresh contiguous block of shape (out_level, out_form): a single batched
 // launch when the sources are contiguous, one launch per part otherwise.

@@ -129,6 +129,8 @@ static std::size_t uniform_stride(const std::vector<Poly>& parts) {
     std::size_t S = p0.words();
     if (parts.size() > 1) S = parts[1].offset() - p0.offset();
     if (S < p0.words() || S % n != 0) return 0;
+    // a level-dropped view: the stride is a poly of some level of this ring
+    if (S / n > std::size_t(p0.ring().q_count()) + std::size_t(p0.nspecial())) return 0;
     for (std::size_t i = 0; i < parts.size(); ++i) {
         const Poly& p = parts[i];
         if (p.storage() != p0.storage() || p.level() != p0.level() || p.nspecial() != p0.nspecial() ||
@@ -195,7 +197,7 @@ void Ciphertext::drop_to_level(int new_level) {
 }
 
 static void addsub_ct(Ciphertext& x, const Ciphertext& o, int op) {
-    if (x.parts.size() != o.parts.size()) throw TetrisError("rlwe", "ciphertext degree mismatch");
+    if (x.parts.size() != o.parts.size() || x.batch != o.batch) throw TetrisError("rlwe", "ciphertext degree mismatch");
     if (x.domain != o.domain) throw TetrisError("rlwe", "domain tag mismatch");
     const std::size_t np = x.parts.size();
     for (std::size_t i = 0; i < np; ++i) x.parts[i].check_shape(o.parts[i]);
@@ -314,6 +316,7 @@ Ciphertext KeyContext::encrypt_pk(const PublicKey& pk, const Poly& m, double sca
 
 Poly KeyContext::decrypt(const SecretKey& sk, const Ciphertext& ct) const {
     if (ct.sk_id != 0 && ct.sk_id != sk.id()) throw TetrisError("rlwe", "ciphertext bound to a different secret");
+    if (ct.batch != 1) throw TetrisError("rlwe", "decrypt expects a single ciphertext (unstack the batch)");
     const int lvl = ct.level();
     Poly s = sk.shaped(lvl, 0);
     Poly acc = ct.parts[0].form() == Form::eval ? ct.parts[0] : ntt_transform(ct.parts[0], Form::eval);
@@ -426,21 +429,35 @@ SwitchingKey KeyContext::relin_key_gen(const SecretKey& sk, Rng& rng) const {
 Ciphertext KeyContext::relinearize(const Ciphertext& ct, const SwitchingKey& rlk) const {
     if (ct.degree() != 2) throw TetrisError("rlwe", "relinearize expects a degree-2 ciphertext");
     if (rlk.to_id != ct.sk_id) throw TetrisError("rlwe", "relinearization key mismatch");
+    const u32 B = ct.batch;
     // keep the eval form of c2 (the tensor output): the digits' own-group rows
     // are its rows, so ModUp copies them instead of re-transforming
-    Poly c2_eval;
-    if (ct.parts[2].form() == Form::eval && ct.parts[2].nspecial() == 0) c2_eval = ct.parts[2];
+    const u64* c2_eval = nullptr;
+    std::vector<Poly> keep;
+    if (ct.parts[2 * B].form() == Form::eval && ct.parts[2 * B].nspecial() == 0 && contiguous(ct.parts, 2 * B, B)) {
+        keep.push_back(ct.parts[2 * B]);  // holds the block
+        c2_eval = ct.parts[2 * B].data();
+    }
     Ciphertext src = ct;
-    src.to_coeff();  // one batched iNTT when the three parts share a block
+    src.to_coeff();  // one batched iNTT when the parts share a block
     const int lvl = ct.level();
-    const Poly& c2 = src.parts[2];
+    const Poly& c2 = src.parts[2 * B];
     if (c2.form() != Form::coeff || c2.nspecial() != 0)
         throw TetrisError("rlwe", "decompose expects coeff form without special rows");
-    std::vector<Poly> dst = fresh_parts(*ring_, 2, lvl, Form::coeff);
-    check_tg(tg_keyswitch_add(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[1].data()),
-                              c2.data(), c2_eval.empty() ? nullptr : c2_eval.data(), key_base(rlk), rlk.digits(),
-                              lvl, src.parts[0].data(), src.parts[1].data(), ring_->stream()));
+    const u64* d = detail::group_data(src.parts, 2 * B, B, keep);
+    const u64* add0 = detail::group_data(src.parts, 0, B, keep);
+    const u64* add1 = detail::group_data(src.parts, B, B, keep);
+    std::vector<Poly> dst = fresh_parts(*ring_, int(2 * B), lvl, Form::coeff);
+    u64* out0 = const_cast<u64*>(dst[0].data());
+    u64* out1 = const_cast<u64*>(dst[B].data());
+    if (B == 1)
+        check_tg(tg_keyswitch_add(plan_->dev(), out0, out1, d, c2_eval, key_base(rlk), rlk.digits(), lvl, add0, add1,
+                                  ring_->stream()));
+    else
+        check_tg(tg_keyswitch_add_batch(plan_->dev(), out0, out1, d, c2_eval, key_base(rlk), rlk.digits(), lvl, add0,
+                                        add1, B, ring_->stream()));
     Ciphertext out;
+    out.batch = B;
     out.parts = std::move(dst);
     out.scale = ct.scale;
     out.domain = ct.domain;
@@ -468,6 +485,7 @@ SwitchingKey KeyContext::galois_key_gen(const SecretKey& sk, u64 exponent, Rng& 
 // apply_galois (rlwe.hpp:637-654)
 Ciphertext KeyContext::apply_galois(const Ciphertext& ct, u64 exponent, const SwitchingKey& swk) const {
     if (ct.degree() != 1) throw TetrisError("rlwe", "apply_galois expects degree-1 input");
+    if (ct.batch != 1) throw TetrisError("rlwe", "apply_galois on a batch is not supported (unstack it)");
     Ciphertext src = ct;
     src.to_coeff();
     const int lvl = ct.level();
@@ -516,6 +534,71 @@ SecretKey KeyContext::square_secret(const SecretKey& sk) const {
             else sq[k - n] -= v;
         }
     return SecretKey(*ring_, std::move(sq), splitmix64(sk.id() ^ 0x5157ULL));
+}
+
+// ---------------------------------------------------------------------------
+// Ciphertext batches (extension): part-major stacking of equal-shape cts
+// ---------------------------------------------------------------------------
+Ciphertext stack_ciphertexts(const std::vector<Ciphertext>& cts) {
+    if (cts.empty()) throw TetrisError("ckks", "stack of no ciphertexts");
+    const Ciphertext& c0 = cts[0];
+    const u32 B = u32(cts.size());
+    const std::size_t deg1 = c0.parts.size();
+    double noise = 0;
+    for (const auto& c : cts) {
+        if (c.batch != 1 || c.parts.size() != deg1) throw TetrisError("ckks", "stack expects single ciphertexts of one degree");
+        if (c.domain != c0.domain || c.sk_id != c0.sk_id) throw TetrisError("ckks", "stack: domain or key mismatch");
+        if (std::abs(c.scale / c0.scale - 1.0) > 1e-4) throw TetrisError("ckks", "scaling factors diverged beyond tolerance");
+        for (const auto& p : c.parts) p.check_shape(c0.parts[0]);
+        noise = std::max(noise, c.noise_bound);
+    }
+    const Poly& p0 = c0.parts[0];
+    const RingParams& ring = p0.ring();
+    std::vector<Poly> out = fresh_parts(ring, int(deg1 * B), p0.level(), p0.form(), p0.nspecial());
+    for (std::size_t k = 0; k < deg1; ++k)
+        for (u32 i = 0; i < B; ++i)
+            check_tg(tg_memcpy_d2d(ring.dev(), const_cast<u64*>(out[k * B + i].data()), cts[i].parts[k].data(),
+                                   out[k * B + i].words() * 8, ring.stream()));
+    Ciphertext r;
+    r.parts = std::move(out);
+    r.batch = B;
+    r.scale = c0.scale;
+    r.domain = c0.domain;
+    r.sk_id = c0.sk_id;
+    r.noise_bound = noise;
+    return r;
+}
+
+// Slices are copied into their own part-major block, so every downstream op
+// sees the standard batch layout (one launch per op, no strided views).
+Ciphertext slice_ciphertext(const Ciphertext& ct, u32 first, u32 count) {
+    const u32 B = ct.batch;
+    if (count == 0 || first + count > B) throw TetrisError("ckks", "batch slice out of range");
+    const std::size_t deg1 = ct.parts.size() / B;
+    const Poly& p0 = ct.parts[0];
+    const RingParams& ring = p0.ring();
+    std::vector<Poly> out = fresh_parts(ring, int(deg1 * count), p0.level(), p0.form(), p0.nspecial());
+    for (std::size_t k = 0; k < deg1; ++k) {
+        const std::size_t src = k * B + first;
+        if (contiguous(ct.parts, src, count)) {
+            check_tg(tg_memcpy_d2d(ring.dev(), const_cast<u64*>(out[k * count].data()), ct.parts[src].data(),
+                                   out[0].words() * 8 * count, ring.stream()));
+        } else {
+            for (u32 i = 0; i < count; ++i)
+                check_tg(tg_memcpy_d2d(ring.dev(), const_cast<u64*>(out[k * count + i].data()),
+                                       ct.parts[src + i].data(), out[0].words() * 8, ring.stream()));
+        }
+    }
+    Ciphertext r = ct;
+    r.parts = std::move(out);
+    r.batch = count;
+    return r;
+}
+
+std::vector<Ciphertext> unstack_ciphertext(const Ciphertext& ct) {
+    std::vector<Ciphertext> out;
+    for (u32 i = 0; i < ct.batch; ++i) out.push_back(slice_ciphertext(ct, i, 1));
+    return out;
 }
 
 }  // namespace tetris_b200

@@ -165,6 +165,7 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("level", &Ciphertext::level)
         .def("form", &Ciphertext::form)
         .def("degree", &Ciphertext::degree)
+        .def_readonly("batch", &Ciphertext::batch)
         .def("copy", [](const Ciphertext& c) { return Ciphertext(c); })
         .def("to_coeff", &Ciphertext::to_coeff)
         .def("to_eval", &Ciphertext::to_eval)
@@ -242,6 +243,11 @@ PYBIND11_MODULE(_tetris_b200, m) {
             std::memcpy(out.mutable_data(), h.data(), h.size() * 8);
             return out;
         });
+
+    // ciphertext batches (extension): part-major stacks evaluated together
+    m.def("stack_ciphertexts", &stack_ciphertexts, py::call_guard<py::gil_scoped_release>());
+    m.def("unstack_ciphertext", &unstack_ciphertext);
+    m.def("slice_ciphertext", &slice_ciphertext, py::arg("ct"), py::arg("first"), py::arg("count"));
 
     py::class_<Evaluator>(m, "Evaluator")
         .def(py::init<const KeyContext&>(), py::keep_alive<1, 2>())

@@ -128,6 +128,50 @@ k_key_inner(DevRing R, u64* __restrict__ acc0, u64* __restrict__ acc1, const u64
     }
 }
 
+// Batched key inner product: npolys sources share one key. A thread owns one
+// word (row, coefficient) of the key rows, keeps its nd (b, a) key words in
+// registers and loops over the sources, so every key word is read once per
+// batch ("switching key read once per batch").
+// acc layout: [2][npolys][rows][N] (all b-accumulators, then all a).
+template <int NDMAX>
+__global__ void __launch_bounds__(kThreads)
+k_key_inner_b(DevRing R, u64* __restrict__ acc, const u64* __restrict__ digits, u32 nd, u32 npolys,
+              const u64* __restrict__ key, int level) {
+    const u32 N = R.N, K = R.K;
+    const u32 rows = u32(level) + 1 + K;
+    const u64 words = u64(rows) * N;
+    const size_t key_rows = size_t(R.nmod);
+    for (u64 i = blockIdx.x * u64(kThreads) + threadIdx.x; i < words; i += u64(gridDim.x) * kThreads) {
+        const u32 r = u32(i >> R.logN);
+        const u32 c = u32(i & (N - 1));
+        const u32 m = mod_index(r, level, R.q_count);
+        const u64 q = R.q[m], rl = R.ratio[2 * m], rh = R.ratio[2 * m + 1];
+        u64 kb[NDMAX], ka[NDMAX];
+#pragma unroll
+        for (int k = 0; k < NDMAX; ++k) {
+            if (u32(k) < nd) {
+                const u64* base = key + (size_t(k) * 2) * key_rows * N + size_t(m) * N + c;
+                kb[k] = base[0];
+                ka[k] = base[key_rows * N];
+            }
+        }
+        for (u32 b = 0; b < npolys; ++b) {
+            const u64* dig = digits + size_t(b) * nd * words + i;
+            U128 s0{0, 0}, s1{0, 0};
+#pragma unroll
+            for (int k = 0; k < NDMAX; ++k) {  // nd <= NDMAX <= 15: products < 2^124, no mid reduction
+                if (u32(k) < nd) {
+                    const u64 dv = dig[size_t(k) * words];
+                    mac128(s0, dv, kb[k]);
+                    mac128(s1, dv, ka[k]);
+                }
+            }
+            acc[size_t(b) * words + i] = barrett128(s0.lo, s0.hi, q, rl, rh);
+            acc[(size_t(npolys) + b) * words + i] = barrett128(s1.lo, s1.hi, q, rl, rh);
+        }
+    }
+}
+
 // ModDown of npolys polys (each level+1+K rows, coeff) -> level+1 rows,
 // optionally added to `addend` (out = addend + ModDown(in); the relinearise
 // / Galois epilogue, rlwe.hpp:612-613, :647). Centered y_s = |y_s| * sign
@@ -452,21 +496,33 @@ void launch_mod_down_v(const DevRing& R, const GadgetDev& G, int sms, u64* out, 
 
 }  // namespace
 
-int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, const u64* d_eval = nullptr) {
+// ModUp of npolys coeff-form sources (level+1 rows each, back to back) into
+// digits [npolys][nd][level+1+K][N], then one batched forward NTT of all
+// digits (own-group rows skipped when the eval form d_eval is supplied).
+int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, const u64* d_eval = nullptr,
+          u32 npolys = 1) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const u32 nd = tg_gadget_digit_count(g, level);
+    const size_t in_words = size_t(level + 1) * R.N, dig_words = size_t(nd) * (level + 1 + R.K) * R.N;
     dim3 grid((R.N + kMUThreads - 1) / kMUThreads, nd);
     {
-        ProfScope prof(ctx, TG_OP_MODUP, 8.0 * R.N * (double(level + 1) + double(nd) * (level + 1 + R.K)), s);
+        ProfScope prof(ctx, TG_OP_MODUP,
+                       8.0 * R.N * npolys * (double(level + 1) + double(nd) * (level + 1 + R.K)), s);
         const GadgetDev& G = g->g;
-        if (G.lazy_modup && G.group_size <= 4) launch_modup_v<4, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s);
-        else if (G.lazy_modup && G.group_size <= 8) launch_modup_v<8, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s);
-        else if (G.lazy_modup && G.group_size <= 16) launch_modup_v<16, 1>(R, G, ctx->sms, digits, d, level, nd, d_eval, s);
-        else k_modup<<<grid, kMUThreads, 0, s>>>(R, G, digits, d, level, d_eval);
+        for (u32 b = 0; b < npolys; ++b) {
+            u64* dg = digits + b * dig_words;
+            const u64* src = d + b * in_words;
+            const u64* ev = d_eval ? d_eval + b * in_words : nullptr;
+            if (G.lazy_modup && G.group_size <= 4) launch_modup_v<4, 2>(R, G, ctx->sms, dg, src, level, nd, ev, s);
+            else if (G.lazy_modup && G.group_size <= 8) launch_modup_v<8, 2>(R, G, ctx->sms, dg, src, level, nd, ev, s);
+            else if (G.lazy_modup && G.group_size <= 16) launch_modup_v<16, 1>(R, G, ctx->sms, dg, src, level, nd, ev, s);
+            else k_modup<<<grid, kMUThreads, 0, s>>>(R, G, dg, src, level, ev);
+        }
     }
     TG_LAUNCH_CHECK();
-    return ntt_forward_oop(ctx, digits, digits, level, int(R.K), nd, s, d_eval ? g->g.group_size : 0);
+    const u32 skip = d_eval ? (g->g.group_size | (npolys > 1 ? nd << 16 : 0u)) : 0u;
+    return ntt_forward_oop(ctx, digits, digits, level, int(R.K), nd * npolys, s, skip);
 }
 
 int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaStream_t s,
@@ -501,6 +557,29 @@ int ks_inner(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd, cons
         return mod_down(g, out0, acc, level, 2, s, add0);
     if (int rc = mod_down(g, out0, acc, level, 1, s, add0)) return rc;
     return mod_down(g, out1, acc + words, level, 1, s, add1);
+}
+
+// Batched key inner product + iNTT + ModDown(+add) for npolys sources.
+// acc: [2][npolys][level+1+K][N] scratch; out0/out1/add0/add1: npolys polys
+// of level+1 rows back to back.
+int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd, u32 npolys, const u64* key,
+                   int level, u64* acc, cudaStream_t s, const u64* add0, const u64* add1) {
+    tg_context* ctx = g->ctx;
+    const DevRing& R = ctx->ring;
+    const size_t words = size_t(level + 1 + R.K) * R.N;
+    {
+        // digits once, key once per batch, two accumulators written
+        ProfScope prof(ctx, TG_OP_KEY_INNER, 8.0 * words * (npolys * (nd + 2.0) + 2.0 * nd), s);
+        const u32 blocks = grid_for(words);
+        if (nd <= 4) k_key_inner_b<4><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level);
+        else if (nd <= 8) k_key_inner_b<8><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level);
+        else if (nd <= 15) k_key_inner_b<15><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level);
+        else return fail(TG_E_ARG, "[rlwe] batched key switch supports at most 15 digits");
+    }
+    TG_LAUNCH_CHECK();
+    if (int rc = ntt_inverse_rows(ctx, acc, level, int(R.K), 2 * npolys, s)) return rc;
+    if (int rc = mod_down(g, out0, acc, level, npolys, s, add0)) return rc;
+    return mod_down(g, out1, acc + size_t(npolys) * words, level, npolys, s, add1);
 }
 
 }  // namespace tg
@@ -563,6 +642,28 @@ extern "C" int tg_keyswitch_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, co
     u64* digits = static_cast<u64*>(scratch);
     int rc = modup(g, digits, d, level, s, d_eval);
     if (rc == TG_OK) rc = ks_inner(g, out0, out1, digits, nd, key, level, digits + size_t(nd) * words, s, add0, add1);
+    cudaFreeAsync(scratch, s);
+    return rc;
+}
+
+extern "C" int tg_keyswitch_add_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
+                                      const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
+                                      const uint64_t* add0, const uint64_t* add1, uint32_t npolys, void* stream) {
+    if (int rc = check_ks(g, level)) return rc;
+    if (npolys == 0) return TG_OK;
+    tg_context* ctx = g->ctx;
+    const u32 nd = tg_gadget_digit_count(g, level);
+    if (nd > key_digits) return fail(TG_E_ARG, "[rlwe] switching key has too few digits");
+    DeviceGuard guard(ctx->device);
+    cudaStream_t s = as_stream(stream);
+    const size_t words = size_t(level + 1 + ctx->ring.K) * ctx->ring.N;
+    void* scratch = nullptr;
+    TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
+    u64* digits = static_cast<u64*>(scratch);
+    int rc = modup(g, digits, d, level, s, d_eval, npolys);
+    if (rc == TG_OK)
+        rc = ks_inner_batch(g, out0, out1, digits, nd, npolys, key, level, digits + size_t(npolys) * nd * words, s,
+                            add0, add1);
     cudaFreeAsync(scratch, s);
     return rc;
 }

@@ -22,7 +22,7 @@ inline u32 grid_for(size_t work) {
 }
 
 struct LinComb {
-    u32 nterms, nparts, rescale, add_all;
+    u32 nterms, nparts, rescale, add_all, add_polys;
     int level;
     const u64* ptr[TG_LINCOMB_MAX_TERMS];
     u64 pstride[TG_LINCOMB_MAX_TERMS];
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(DevRing R, LinComb L, u64*
     const u64 total = u64(L.nparts) * N;
     for (u64 i = blockIdx.x * u64(kThreads) + threadIdx.x; i < total; i += u64(gridDim.x) * kThreads) {
         const u32 p = u32(i >> R.logN), c = u32(i & (N - 1));
-        const bool add_here = p == 0 && (L.add_all || c == 0);
+        const bool add_here = p < L.add_polys && (L.add_all || c == 0);
         u64* dst = out + size_t(p) * rout * N;
         if (!L.rescale) {
             for (u32 r = 0; r <= lvl; ++r) dst[size_t(r) * N + c] = lc_row(R, L, p, r, c, add_here);
@@ -76,6 +76,14 @@ using namespace tg;
 extern "C" int tg_lincomb(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* terms,
                           const uint64_t* part_strides, const uint64_t* coeffs, const uint64_t* add_per_row,
                           int add_all, int level, uint32_t nparts, int rescale, void* stream) {
+    return tg_lincomb_batch(ctx, out, nterms, terms, part_strides, coeffs, add_per_row, add_all, level, nparts, 1,
+                            rescale, stream);
+}
+
+extern "C" int tg_lincomb_batch(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* terms,
+                                const uint64_t* part_strides, const uint64_t* coeffs, const uint64_t* add_per_row,
+                                int add_all, int level, uint32_t nparts, uint32_t add_polys, int rescale,
+                                void* stream) {
     if (!ctx) return fail(TG_E_ARG, "[ring] null context");
     const DevRing& R = ctx->ring;
     if (level < 0 || u32(level) >= R.q_count) return fail(TG_E_ARG, "[ring] poly level out of range");
@@ -89,6 +97,7 @@ extern "C" int tg_lincomb(tg_context* ctx, uint64_t* out, uint32_t nterms, const
     L.nparts = nparts;
     L.rescale = rescale ? 1 : 0;
     L.add_all = add_all ? 1 : 0;
+    L.add_polys = add_polys;
     L.level = level;
     for (u32 t = 0; t < nterms; ++t) {
         L.ptr[t] = terms[t];

@@ -25,10 +25,13 @@ constexpr u32 kLogTile = 11;
 
 // Row-skip rule of ModUp digit transforms: poly p = digit p, whose own-group
 // rows (r <= level, r / group_size == p) were copied already in eval form.
-__device__ __forceinline__ bool ntt_row_skipped(u32 row, u32 rpp, int level, u32 skip_gs) {
-    if (!skip_gs) return false;
+// skip = group_size | (digits per source poly << 16): poly p is digit
+// p % digits of source p / digits (digits = 0: one source, digit p).
+__device__ __forceinline__ bool ntt_row_skipped(u32 row, u32 rpp, int level, u32 skip) {
+    if (!skip) return false;
+    const u32 gs = skip & 0xFFFFu, nd = skip >> 16;
     const u32 r = row % rpp, p = row / rpp;
-    return r <= u32(level) && r / skip_gs == p;
+    return r <= u32(level) && r / gs == (nd ? p % nd : p);
 }  // 2048 words = 16 KiB of shared memory per block
 
 struct Plan {

@@ -169,8 +169,11 @@ __device__ __forceinline__ void wxchg(T (&v)[E], u64* colw, u32 lane, u32 lo_fro
 // 3 stages: from |v| <= q each stage adds |t| <= 1.5q, so |v| <= 5.5q < 2^53,
 // then every value is reduced to |v| <= q/2 + 1. Inverse butterflies reduce
 // a+b every stage (|a|,|b| <= 1.5q => |a-b| <= 3q, |a+b| reduced).
-template <int E, bool CHUNK, int LAY, int HI, int LO>
-__device__ __forceinline__ void wfwd_fp(double (&v)[E], u32 lane, const u64* sw, double q, double qi, u32 c) {
+// NP independent transforms of the same modulus and position (NP polys) run
+// interleaved: each staged twiddle feeds NP butterflies and the FP64
+// dependency chains of one transform hide behind the other's.
+template <int NP, int E, bool CHUNK, int LAY, int HI, int LO>
+__device__ __forceinline__ void wfwd_fp(double (&v)[NP][E], u32 lane, const u64* sw, double q, double qi, u32 c) {
     constexpr int LOGE = WGeo<E>::LOGE, LOGM = WGeo<E>::LOGM;
 #pragma unroll
     for (int p = HI; p >= LO; --p) {
@@ -181,18 +184,23 @@ __device__ __forceinline__ void wfwd_fp(double (&v)[E], u32 lane, const u64* sw,
             const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
             const u32 t = tw_slot<E, true, CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
             const double2 tw = reinterpret_cast<const double2*>(sw)[t];
-            const double x = fp_mulmod(v[j | (1 << b)], tw.x, tw.y, q);
-            const double a = v[j];
-            v[j] = __dadd_rn(a, x);
-            v[j | (1 << b)] = __dsub_rn(a, x);
+#pragma unroll
+            for (int n = 0; n < NP; ++n) {
+                const double x = fp_mulmod(v[n][j | (1 << b)], tw.x, tw.y, q);
+                const double a = v[n][j];
+                v[n][j] = __dadd_rn(a, x);
+                v[n][j | (1 << b)] = __dsub_rn(a, x);
+            }
         }
     }
 #pragma unroll
-    for (int j = 0; j < E; ++j) v[j] = fp_reduce(v[j], q, qi);
+    for (int n = 0; n < NP; ++n)
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[n][j] = fp_reduce(v[n][j], q, qi);
 }
 
-template <int E, bool CHUNK, int LAY, int LO, int HI>
-__device__ __forceinline__ void winv_fp(double (&v)[E], u32 lane, const u64* sw, double q, double qi, u32 c) {
+template <int NP, int E, bool CHUNK, int LAY, int LO, int HI>
+__device__ __forceinline__ void winv_fp(double (&v)[NP][E], u32 lane, const u64* sw, double q, double qi, u32 c) {
     constexpr int LOGE = WGeo<E>::LOGE, LOGM = WGeo<E>::LOGM;
 #pragma unroll
     for (int p = LO; p <= HI; ++p) {
@@ -203,50 +211,73 @@ __device__ __forceinline__ void winv_fp(double (&v)[E], u32 lane, const u64* sw,
             const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
             const u32 t = tw_slot<E, false, CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
             const double2 tw = reinterpret_cast<const double2*>(sw)[t];
-            const double a = v[j], bb = v[j | (1 << b)];
-            v[j] = fp_reduce(__dadd_rn(a, bb), q, qi);
-            v[j | (1 << b)] = fp_mulmod(__dsub_rn(a, bb), tw.x, tw.y, q);
+#pragma unroll
+            for (int n = 0; n < NP; ++n) {
+                const double a = v[n][j], bb = v[n][j | (1 << b)];
+                v[n][j] = fp_reduce(__dadd_rn(a, bb), q, qi);
+                v[n][j | (1 << b)] = fp_mulmod(__dsub_rn(a, bb), tw.x, tw.y, q);
+            }
         }
     }
 }
 
-template <int E, bool CHUNK>
-__device__ __forceinline__ void wfwd_all_fp(double (&v)[E], u64* col, u32 lane, const u64* sw, double q, double qi,
-                                            u32 c) {
-    if constexpr (E == 8) {
-        wfwd_fp<8, CHUNK, 5, 7, 5>(v, lane, sw, q, qi, c);
-        wxchg<8>(v, col, lane, 5, 2);
-        wfwd_fp<8, CHUNK, 2, 4, 2>(v, lane, sw, q, qi, c);
-        wxchg<8>(v, col, lane, 2, 0);
-        wfwd_fp<8, CHUNK, 0, 1, 0>(v, lane, sw, q, qi, c);
-    } else {
-        wfwd_fp<4, CHUNK, 5, 6, 5>(v, lane, sw, q, qi, c);
-        wxchg<4>(v, col, lane, 5, 3);
-        wfwd_fp<4, CHUNK, 3, 4, 3>(v, lane, sw, q, qi, c);
-        wxchg<4>(v, col, lane, 3, 1);
-        wfwd_fp<4, CHUNK, 1, 2, 1>(v, lane, sw, q, qi, c);
-        wxchg<4>(v, col, lane, 1, 0);
-        wfwd_fp<4, CHUNK, 0, 0, 0>(v, lane, sw, q, qi, c);
+// NP warp-private exchange columns, `cs` words apart.
+template <int NP, int E>
+__device__ __forceinline__ void wxchg_fp(double (&v)[NP][E], u64* colw, u32 cs, u32 lane, u32 lo_from, u32 lo_to) {
+    constexpr int LOGE = WGeo<E>::LOGE;
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < NP; ++n) {
+        double* col = reinterpret_cast<double*>(colw + n * cs);
+#pragma unroll
+        for (int j = 0; j < E; ++j) col[wpad(wins<LOGE>(lane, u32(j), lo_from))] = v[n][j];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < NP; ++n) {
+        const double* col = reinterpret_cast<const double*>(colw + n * cs);
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[n][j] = col[wpad(wins<LOGE>(lane, u32(j), lo_to))];
     }
 }
 
-template <int E, bool CHUNK>
-__device__ __forceinline__ void winv_all_fp(double (&v)[E], u64* col, u32 lane, const u64* sw, double q, double qi,
-                                            u32 c) {
+template <int NP, int E, bool CHUNK>
+__device__ __forceinline__ void wfwd_all_fp(double (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double q,
+                                            double qi, u32 c) {
     if constexpr (E == 8) {
-        winv_fp<8, CHUNK, 0, 0, 2>(v, lane, sw, q, qi, c);
-        wxchg<8>(v, col, lane, 0, 3);
-        winv_fp<8, CHUNK, 3, 3, 5>(v, lane, sw, q, qi, c);
-        wxchg<8>(v, col, lane, 3, 5);
-        winv_fp<8, CHUNK, 5, 6, 7>(v, lane, sw, q, qi, c);
+        wfwd_fp<NP, 8, CHUNK, 5, 7, 5>(v, lane, sw, q, qi, c);
+        wxchg_fp<NP, 8>(v, col, cs, lane, 5, 2);
+        wfwd_fp<NP, 8, CHUNK, 2, 4, 2>(v, lane, sw, q, qi, c);
+        wxchg_fp<NP, 8>(v, col, cs, lane, 2, 0);
+        wfwd_fp<NP, 8, CHUNK, 0, 1, 0>(v, lane, sw, q, qi, c);
     } else {
-        winv_fp<4, CHUNK, 0, 0, 1>(v, lane, sw, q, qi, c);
-        wxchg<4>(v, col, lane, 0, 2);
-        winv_fp<4, CHUNK, 2, 2, 3>(v, lane, sw, q, qi, c);
-        wxchg<4>(v, col, lane, 2, 4);
-        winv_fp<4, CHUNK, 4, 4, 5>(v, lane, sw, q, qi, c);
-        wxchg<4>(v, col, lane, 4, 5);
-        winv_fp<4, CHUNK, 5, 6, 6>(v, lane, sw, q, qi, c);
+        wfwd_fp<NP, 4, CHUNK, 5, 6, 5>(v, lane, sw, q, qi, c);
+        wxchg_fp<NP, 4>(v, col, cs, lane, 5, 3);
+        wfwd_fp<NP, 4, CHUNK, 3, 4, 3>(v, lane, sw, q, qi, c);
+        wxchg_fp<NP, 4>(v, col, cs, lane, 3, 1);
+        wfwd_fp<NP, 4, CHUNK, 1, 2, 1>(v, lane, sw, q, qi, c);
+        wxchg_fp<NP, 4>(v, col, cs, lane, 1, 0);
+        wfwd_fp<NP, 4, CHUNK, 0, 0, 0>(v, lane, sw, q, qi, c);
+    }
+}
+
+template <int NP, int E, bool CHUNK>
+__device__ __forceinline__ void winv_all_fp(double (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double q,
+                                            double qi, u32 c) {
+    if constexpr (E == 8) {
+        winv_fp<NP, 8, CHUNK, 0, 0, 2>(v, lane, sw, q, qi, c);
+        wxchg_fp<NP, 8>(v, col, cs, lane, 0, 3);
+        winv_fp<NP, 8, CHUNK, 3, 3, 5>(v, lane, sw, q, qi, c);
+        wxchg_fp<NP, 8>(v, col, cs, lane, 3, 5);
+        winv_fp<NP, 8, CHUNK, 5, 6, 7>(v, lane, sw, q, qi, c);
+    } else {
+        winv_fp<NP, 4, CHUNK, 0, 0, 1>(v, lane, sw, q, qi, c);
+        wxchg_fp<NP, 4>(v, col, cs, lane, 0, 2);
+        winv_fp<NP, 4, CHUNK, 2, 2, 3>(v, lane, sw, q, qi, c);
+        wxchg_fp<NP, 4>(v, col, cs, lane, 2, 4);
+        winv_fp<NP, 4, CHUNK, 4, 4, 5>(v, lane, sw, q, qi, c);
+        wxchg_fp<NP, 4>(v, col, cs, lane, 4, 5);
+        winv_fp<NP, 4, CHUNK, 5, 6, 6>(v, lane, sw, q, qi, c);
     }
 }
 
@@ -362,8 +393,8 @@ constexpr size_t col_smem() {  // two tiles + twiddles
     return size_t(8) * (16 * WGeo<E>::CS + 2 * WGeo<E>::TW_COL);
 }
 template <int E>
-constexpr size_t chunk_smem() {
-    return size_t(8) * (8 * WGeo<E>::CS + 2 * WGeo<E>::TW_CHUNK);
+constexpr size_t chunk_smem() {  // exchange columns of two transforms per warp + twiddles
+    return size_t(8) * (16 * WGeo<E>::CS + 2 * WGeo<E>::TW_CHUNK);
 }
 
 // Column tile of row `row` (8 columns x M1, element (m, c) at c*CS + wpad(m)).
@@ -420,14 +451,14 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
         u64* col = tile + warp * Gm::CS;
         if (fp) {  // canonical u64 in, doubles (|v| <= q/2 + 1, raw bits) out to phase 2
             const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
-            double v[E];
+            double v[1][E];
 #pragma unroll
-            for (int j = 0; j < E; ++j) v[j] = u2d(col[wpad(lane + 32 * j)]);
-            wfwd_all_fp<E, false>(v, col, lane, sw, qd, qi, 0);
+            for (int j = 0; j < E; ++j) v[0][j] = u2d(col[wpad(lane + 32 * j)]);
+            wfwd_all_fp<1, E, false>(v, col, 0, lane, sw, qd, qi, 0);
             __syncwarp();
             double* cold = reinterpret_cast<double*>(col);
 #pragma unroll
-            for (int j = 0; j < E; ++j) cold[wpad((lane << Gm::LOGE) | j)] = v[j];
+            for (int j = 0; j < E; ++j) cold[wpad((lane << Gm::LOGE) | j)] = v[0][j];
         } else {
             u64 v[E];
 #pragma unroll
@@ -446,7 +477,69 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
     }
 }
 
+// Chunk-phase loads/stores of one warp's chunk (lane-strided in, lane-
+// contiguous 16-byte vectors out, or the reverse for the inverse).
+template <int E>
+__device__ __forceinline__ void ld_strided(u64 (&v)[E], const u64* x, u32 lane) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = x[lane + 32 * j];
+}
+template <int E>
+__device__ __forceinline__ void st_strided(u64* x, const u64 (&v)[E], u32 lane) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) x[lane + 32 * j] = v[j];
+}
+template <int E>
+__device__ __forceinline__ void ld_vec(u64 (&v)[E], const u64* x, u32 lane) {
+    const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x + (lane << WGeo<E>::LOGE));
+#pragma unroll
+    for (int j = 0; j < E / 2; ++j) {
+        const ulonglong2 t = x2[j];
+        v[2 * j] = t.x;
+        v[2 * j + 1] = t.y;
+    }
+}
+template <int E>
+__device__ __forceinline__ void st_vec(u64* x, const u64 (&v)[E], u32 lane) {
+    ulonglong2* x2 = reinterpret_cast<ulonglong2*>(x + (lane << WGeo<E>::LOGE));
+#pragma unroll
+    for (int j = 0; j < E / 2; ++j) x2[j] = make_ulonglong2(v[2 * j], v[2 * j + 1]);
+}
+
+// FP64 chunk phase of NP polys: forward (phase-1 doubles in, canonical out)
+template <int NP, int E>
+__device__ __forceinline__ void chunk_fwd_fp(u64 (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double qd,
+                                             double qi, u32 warp) {
+    double vd[NP][E];
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+#pragma unroll
+        for (int j = 0; j < E; ++j) vd[n][j] = __longlong_as_double(static_cast<long long>(v[n][j]));
+    wfwd_all_fp<NP, E, true>(vd, col, cs, lane, sw, qd, qi, warp);
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[n][j] = fp_canonical(vd[n][j], qd);
+}
+// inverse (canonical in, doubles |v| <= 1.5q as raw bits out to phase B)
+template <int NP, int E>
+__device__ __forceinline__ void chunk_inv_fp(u64 (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double qd,
+                                             double qi, u32 warp) {
+    double vd[NP][E];
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+#pragma unroll
+        for (int j = 0; j < E; ++j) vd[n][j] = u2d(v[n][j]);
+    winv_all_fp<NP, E, true>(vd, col, cs, lane, sw, qd, qi, warp);
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[n][j] = static_cast<u64>(__double_as_longlong(vd[n][j]));
+}
+
 // Phase 2 forward: one warp per contiguous chunk of M2, final canonical reduce.
+// FP64 rows take the block's polys two at a time (interleaved transforms);
+// integer rows one at a time with the next poly prefetched.
 template <int E>
 __global__ void __launch_bounds__(256, NTT_CHUNK_MIN_BLOCKS)
 kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 logN1, u32 skip_gs) {
@@ -456,7 +549,7 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
     if (p >= pend) return;
     extern __shared__ u64 dyn[];
     u64* sm = dyn;
-    u64* sw = dyn + 8 * Gm::CS;
+    u64* sw = dyn + 16 * Gm::CS;
     u64* sws = sw + Gm::TW_CHUNK;
     const u32 N = R.N;
     const u32 mi = mod_index(r, level, R.q_count);
@@ -465,36 +558,49 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
     const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N) : R.tw + size_t(mi) * 4 * N;
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
-    u64 v[E], nx[E];
-    {
-        const u64* x = data + size_t(p * rpp + r) * N + off;
-#pragma unroll
-        for (int j = 0; j < E; ++j) v[j] = x[lane + 32 * j];
+    u64* col = sm + warp * Gm::CS;
+    constexpr u32 CS2 = 8 * Gm::CS;  // second transform's column
+    auto row = [&](u32 pp) { return data + size_t(pp * rpp + r) * N + off; };
+    if (fp) {
+        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+        u32 p2 = next_poly(p + 1, pend, r, rpp, level, skip_gs);
+        u64 v[2][E];
+        ld_strided<E>(v[0], row(p), lane);
+        if (p2 < pend) ld_strided<E>(v[1], row(p2), lane);
+        stage_chunk_twiddles<E, true>(sw, sws, w, w + N, logN1, blockIdx.x);
+        __syncthreads();
+        while (true) {
+            if (p2 < pend) {
+                chunk_fwd_fp<2, E>(v, col, CS2, lane, sw, qd, qi, warp);
+                st_vec<E>(row(p), v[0], lane);
+                st_vec<E>(row(p2), v[1], lane);
+                p = next_poly(p2 + 1, pend, r, rpp, level, skip_gs);
+            } else {
+                chunk_fwd_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), col, CS2, lane, sw, qd, qi, warp);
+                st_vec<E>(row(p), v[0], lane);
+                p = p2;
+            }
+            if (p >= pend) break;
+            p2 = next_poly(p + 1, pend, r, rpp, level, skip_gs);
+            ld_strided<E>(v[0], row(p), lane);
+            if (p2 < pend) ld_strided<E>(v[1], row(p2), lane);
+        }
+        return;
     }
+    u64 v[E], nx[E];
+    ld_strided<E>(v, row(p), lane);
     stage_chunk_twiddles<E, true>(sw, sws, w, w + N, logN1, blockIdx.x);
     __syncthreads();
     while (p < pend) {
         const u32 pn = next_poly(p + 1, pend, r, rpp, level, skip_gs);
-        if (pn < pend) {  // next poly's chunk in flight during this one's stages
-            const u64* x = data + size_t(pn * rpp + r) * N + off;
-#pragma unroll
-            for (int j = 0; j < E; ++j) nx[j] = x[lane + 32 * j];
-        }
-        if (fp) {  // phase-1 doubles in, canonical u64 out
-            const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
-            double vd[E];
-#pragma unroll
-            for (int j = 0; j < E; ++j) vd[j] = __longlong_as_double(static_cast<long long>(v[j]));
-            wfwd_all_fp<E, true>(vd, sm + warp * Gm::CS, lane, sw, qd, qi, warp);
-#pragma unroll
-            for (int j = 0; j < E; ++j) v[j] = fp_canonical(vd[j], qd);
-        } else if (q < kSmallQ) {
-            wfwd_all<E, true, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+        if (pn < pend) ld_strided<E>(nx, row(pn), lane);  // in flight during this poly's stages
+        if (q < kSmallQ) {
+            wfwd_all<E, true, true>(v, col, lane, sw, sws, q, warp);
             const u64 one = R.one_shoup[mi];
 #pragma unroll
             for (int j = 0; j < E; ++j) v[j] = shoup(v[j], 1, one, q);  // < 33q -> canonical
         } else {
-            wfwd_all<E, true, false>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+            wfwd_all<E, true, false>(v, col, lane, sw, sws, q, warp);
             const u64 q2 = 2 * q;
 #pragma unroll
             for (int j = 0; j < E; ++j) {
@@ -504,10 +610,7 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
                 v[j] = t;
             }
         }
-        ulonglong2* x2 =
-            reinterpret_cast<ulonglong2*>(data + size_t(p * rpp + r) * N + off + (lane << Gm::LOGE));
-#pragma unroll
-        for (int j = 0; j < E / 2; ++j) x2[j] = make_ulonglong2(v[2 * j], v[2 * j + 1]);
+        st_vec<E>(row(p), v, lane);
 #pragma unroll
         for (int j = 0; j < E; ++j) v[j] = nx[j];
         p = pn;
@@ -524,7 +627,7 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
     if (p >= pend) return;
     extern __shared__ u64 dyn[];
     u64* sm = dyn;
-    u64* sw = dyn + 8 * Gm::CS;
+    u64* sw = dyn + 16 * Gm::CS;
     u64* sws = sw + Gm::TW_CHUNK;
     const u32 N = R.N;
     const u32 mi = mod_index(r, level, R.q_count);
@@ -534,41 +637,49 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
                       : R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
-    u64 v[E], nx[E];
-    auto load = [&](u64 (&dst)[E], u32 pp) {
-        const ulonglong2* xs2 =
-            reinterpret_cast<const ulonglong2*>(src + size_t(pp * rpp + r) * N + off + (lane << Gm::LOGE));
-#pragma unroll
-        for (int j = 0; j < E / 2; ++j) {
-            const ulonglong2 t = xs2[j];
-            dst[2 * j] = t.x;
-            dst[2 * j + 1] = t.y;
+    u64* col = sm + warp * Gm::CS;
+    constexpr u32 CS2 = 8 * Gm::CS;
+    auto in = [&](u32 pp) { return src + size_t(pp * rpp + r) * N + off; };
+    auto out = [&](u32 pp) { return data + size_t(pp * rpp + r) * N + off; };
+    if (fp) {
+        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+        u64 v[2][E];
+        ld_vec<E>(v[0], in(p), lane);
+        if (p + 1 < pend) ld_vec<E>(v[1], in(p + 1), lane);
+        stage_chunk_twiddles<E, false>(sw, sws, w, w + N, logN1, blockIdx.x);
+        __syncthreads();
+        while (true) {
+            if (p + 1 < pend) {
+                chunk_inv_fp<2, E>(v, col, CS2, lane, sw, qd, qi, warp);
+                st_strided<E>(out(p), v[0], lane);
+                st_strided<E>(out(p + 1), v[1], lane);
+                p += 2;
+            } else {
+                chunk_inv_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), col, CS2, lane, sw, qd, qi, warp);
+                st_strided<E>(out(p), v[0], lane);
+                p += 1;
+            }
+            if (p >= pend) break;
+            ld_vec<E>(v[0], in(p), lane);
+            if (p + 1 < pend) ld_vec<E>(v[1], in(p + 1), lane);
         }
-    };
-    load(v, p);
+        return;
+    }
+    u64 v[E], nx[E];
+    ld_vec<E>(v, in(p), lane);
     stage_chunk_twiddles<E, false>(sw, sws, w, w + N, logN1, blockIdx.x);
     __syncthreads();
     for (; p < pend; ++p) {
-        if (p + 1 < pend) load(nx, p + 1);
-        if (fp) {  // canonical u64 in, doubles (|v| <= 1.5q, raw bits) out to phase B
-            const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
-            double vd[E];
-#pragma unroll
-            for (int j = 0; j < E; ++j) vd[j] = u2d(v[j]);
-            winv_all_fp<E, true>(vd, sm + warp * Gm::CS, lane, sw, qd, qi, warp);
-#pragma unroll
-            for (int j = 0; j < E; ++j) v[j] = static_cast<u64>(__double_as_longlong(vd[j]));
-        } else if (q < kSmallQ) {
-            winv_all<E, true, true>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+        if (p + 1 < pend) ld_vec<E>(nx, in(p + 1), lane);
+        if (q < kSmallQ) {
+            winv_all<E, true, true>(v, col, lane, sw, sws, q, warp);
             const u64 one = R.one_shoup[mi];
 #pragma unroll
             for (int j = 0; j < E; ++j) v[j] = shoup_lazy(v[j], 1, one, q);  // < 512q -> [0, 2q)
         } else {
-            winv_all<E, true, false>(v, sm + warp * Gm::CS, lane, sw, sws, q, warp);
+            winv_all<E, true, false>(v, col, lane, sw, sws, q, warp);
         }
-        u64* x = data + size_t(p * rpp + r) * N + off;
-#pragma unroll
-        for (int j = 0; j < E; ++j) x[lane + 32 * j] = v[j];
+        st_strided<E>(out(p), v, lane);
 #pragma unroll
         for (int j = 0; j < E; ++j) v[j] = nx[j];
     }
@@ -611,13 +722,13 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level) {
         if (fp) {  // phase-A doubles in, canonical u64 out (N^-1 applied in FP64)
             const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1], nd = R.qd[4 * mi + 2], ndq = R.qd[4 * mi + 3];
             const double* cold = reinterpret_cast<const double*>(col);
-            double v[E];
+            double v[1][E];
 #pragma unroll
-            for (int j = 0; j < E; ++j) v[j] = cold[wpad((lane << Gm::LOGE) | j)];
-            winv_all_fp<E, false>(v, col, lane, sw, qd, qi, 0);
+            for (int j = 0; j < E; ++j) v[0][j] = cold[wpad((lane << Gm::LOGE) | j)];
+            winv_all_fp<1, E, false>(v, col, 0, lane, sw, qd, qi, 0);
             __syncwarp();
 #pragma unroll
-            for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canonical(fp_mulmod(v[j], nd, ndq, qd), qd);
+            for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canonical(fp_mulmod(v[0][j], nd, ndq, qd), qd);
         } else {
             u64 v[E];
 #pragma unroll

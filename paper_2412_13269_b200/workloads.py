@@ -204,6 +204,8 @@ def run_concurrent(T, ring, fn, items, streams):
     errs = []
     k = min(streams, len(items))
     scoped = hasattr(T, "stream_scope")  # the CPU reference: plain threads (protocol.hpp:297-311)
+    if scoped:
+        ring.synchronize()  # inputs made on the caller's stream are complete before other streams read them
 
     def worker(w):
         try:
@@ -376,4 +378,37 @@ def statement_partial(S, q, blocks, threshold, streams=1):
     acc = None
     for o in outs:
         acc = o if acc is None else S.ev.add(acc, o)
+    return acc
+
+
+def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8):
+    """B200 module: the same per-block statement with the blocks evaluated as
+    ciphertext batches (stack_ciphertexts): per chunk of <= max_blocks blocks,
+    one batched threshold over the sugar and pressure columns (same level and
+    norm) and one over the risk scores, then the AND products batched. Each
+    block's output is bit-identical to statement_block's (a batch is exactly
+    `batch` independent ciphertexts; tests/test_gpu_statement.py); launches
+    and switching-key reads are shared by the batch."""
+    T, ev, keys = S.T, S.ev, S.keys
+    risks = run_concurrent(T, S.ring, lambda blk: linear_score(S, q.ct_w, blk.pt_attr, blk.attr_scale), blocks,
+                           streams)
+    chunks = [list(range(i, min(len(blocks), i + max_blocks))) for i in range(0, len(blocks), max_blocks)]
+    jobs = []
+    for ch in chunks:
+        nb = len(ch)
+        xa = T.stack_ciphertexts([blocks[i].ct_sugar for i in ch] + [blocks[i].ct_bp for i in ch])
+        ta = T.stack_ciphertexts([q.ct_t[0]] * nb + [q.ct_t[1]] * nb)
+        xb = T.stack_ciphertexts([risks[i] for i in ch])
+        tb = T.stack_ciphertexts([q.ct_t[2]] * nb)
+        jobs += [(xa, ta, 1.0), (xb, tb, RISK_NORM)]
+    outs = run_concurrent(T, S.ring, lambda j: threshold(*j), jobs, streams)
+    acc = None
+    for c, ch in enumerate(chunks):
+        nb = len(ch)
+        ba, bb = outs[2 * c], outs[2 * c + 1]
+        a = ev.rescale(ev.mul_relin(T.slice_ciphertext(ba, 0, nb), T.slice_ciphertext(ba, nb, nb), keys))
+        a = ev.rescale(ev.mul_relin(a, bb, keys))
+        for i, ct in zip(ch, T.unstack_ciphertext(a)):
+            o = ev.rescale(ev.mul_plain(ct, blocks[i].pt_flag, blocks[i].flag_scale))
+            acc = o if acc is None else ev.add(acc, o)
     return acc

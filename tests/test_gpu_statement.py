@@ -89,6 +89,46 @@ def test_config4_statement_bsgs_bit_exact(G, R, stmt4):
     assert abs(per_slot.sum() - W.statement_plain_count(d)) < 3
 
 
+def test_config4_statement_batched_bit_exact(G, R, stmt4):
+    """Blocks evaluated as ciphertext batches (one batched threshold per
+    column group, batched AND products) == the reference per block."""
+    spec, chain_g, g, r, chain_r, d, qg, qr, bg, br = stmt4
+    for mode, thr_r in ((G.PolyEval.ladder, W.threshold_fn(r, chain_r)),
+                        (G.PolyEval.bsgs,
+                         lambda x, t, norm: bsgs_ref.threshold_plain_norm_bsgs(R, r.ev, x, t, norm, chain_r, r.keys))):
+        acc_g = W.statement_partial_batched(g, qg, bg, W.threshold_fn(g, chain_g, mode), streams=2, max_blocks=3)
+        acc_r = W.statement_partial(r, qr, br, thr_r)
+        assert acc_g.batch == 1
+        assert_ct_equal(acc_g, acc_r, f"batched statement ({mode})")
+
+
+def test_batch_ops_match_single(G, gpu_available):
+    """stack / slice / unstack round trip and batch-aware ops (tensor,
+    relinearize, add_scalar, fused combinations) against single ciphertexts."""
+    spec = dataclasses.replace(W.CONFIGS[4], N=256, nq=6, K=2, group=2, records=512, n_cts=4)
+    g = W.make_context(G, spec)
+    vals = [np.linspace(-0.5, 0.5, spec.slots) * (i + 1) / 4 for i in range(3)]
+    cts = W.encrypt_many(g, vals, g.ring.max_level(), [1, 2, 3])
+    fat = G.stack_ciphertexts(cts)
+    assert fat.batch == 3 and fat.degree() == 1
+    for a, b in zip(G.unstack_ciphertext(fat), cts):
+        assert_ct_equal(a, b, "unstack")
+    prod = g.ev.rescale(g.ev.mul_relin(fat, fat, g.keys))
+    sq = [g.ev.rescale(g.ev.mul_relin(c, c, g.keys)) for c in cts]
+    for a, b in zip(G.unstack_ciphertext(prod), sq):
+        assert_ct_equal(a, b, "batched mul_relin + rescale")
+    sc = g.ev.add_scalar(prod, 0.25)
+    for a, b in zip(G.unstack_ciphertext(sc), sq):
+        assert_ct_equal(a, g.ev.add_scalar(b, 0.25), "batched add_scalar")
+    mid = G.slice_ciphertext(prod, 1, 2)
+    for a, b in zip(G.unstack_ciphertext(g.ev.add(mid, mid)), sq[1:]):
+        assert_ct_equal(a, g.ev.add(b, b), "slice + add")
+    coeffs = [0.1, 0.5, 0.0, -0.25]
+    ch = G.eval_chebyshev(g.ev, fat, coeffs, g.keys)
+    for a, b in zip(G.unstack_ciphertext(ch), cts):
+        assert_ct_equal(a, G.eval_chebyshev(g.ev, b, coeffs, g.keys), "batched eval_chebyshev")
+
+
 def test_config5_statement_deg63_bsgs_bit_exact(G, R, gpu_available):
     """Config 5's chain (three degree-63 stages, alpha 13), L = 28, dnum = 3
     (group 10 under 9 special primes) at N = 1024."""

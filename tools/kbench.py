@@ -9,6 +9,7 @@ ModDown, rescale at config-3 shapes.
 from __future__ import annotations
 
 import argparse
+import os
 import json
 import sys
 from pathlib import Path
@@ -28,6 +29,7 @@ def main():
     ap.add_argument("--levels", default="20,10")
     ap.add_argument("--batch", type=int, default=1, help="polys per NTT launch")
     ap.add_argument("--ops", default="ntt,intt,relin,rescale")
+    ap.add_argument("--bsizes", default="1,2,4,8,16,32", help="poly counts of the batch op")
     a = ap.parse_args()
     spec = W.CONFIGS[3]
     S = W.make_context(G, spec)
@@ -40,11 +42,16 @@ def main():
             fn()
         ring.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        prof = os.environ.get("TG_PROFILE_REGION") == "1"  # ncu --profile-from-start off
+        if prof:
+            torch.cuda.cudart().cudaProfilerStart()
         e0.record(ext)
         for _ in range(a.reps):
             fn()
         e1.record(ext)
         ring.synchronize()
+        if prof:
+            torch.cuda.cudart().cudaProfilerStop()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.reps
         res[name] = {"us": round(ms * 1e3, 2)}
@@ -56,7 +63,7 @@ def main():
     if "batch" in a.ops:  # NTT launch cost vs rows: P polys x 21 rows in one launch
         import numpy as np
         lvl = ring.max_level()
-        for P in (1, 2, 4, 8, 16, 32):
+        for P in (int(x) for x in a.bsizes.split(",")):
             arr = np.random.default_rng(P).integers(0, 1 << 40, size=(P, lvl + 1, spec.N), dtype=np.uint64)
             ct = G.ciphertext_from_numpy(ring, arr, lvl, G.Form.coeff, 1.0, G.Domain.slots, 0)
 
