@@ -156,6 +156,7 @@ class ThresholdCount:
     def __init__(self, G, W, spec, rank=0, world=1, rotations=True, device=True):
         from paper_2412_13269_b200 import distributed as D
         self.G, self.W, self.spec = G, W, spec
+        self.batched, self.max_blocks = True, 8
         self.scores, self.thr, _, _ = W.linear_scores(spec)
         if not device:  # inputs only (the CPU reference arm)
             return
@@ -170,8 +171,15 @@ class ThresholdCount:
         cts, ct_t = client[:-1], client[-1]
         if not cts:
             return None
-        outs = self.G.eval_private_threshold_plain_norm_many(self.S.ev, cts, ct_t, self.spec.norm, self.chain,
-                                                             self.S.keys, streams, mode)
+        if self.batched and len(cts) > 1:  # all score blocks as one ciphertext batch
+            G, ev = self.G, self.S.ev
+            fat = G.eval_private_threshold_plain_norm(ev, G.stack_ciphertexts(cts),
+                                                     G.stack_ciphertexts([ct_t] * len(cts)), self.spec.norm,
+                                                     self.chain, self.S.keys, mode)
+            outs = G.unstack_ciphertext(fat)
+        else:
+            outs = self.G.eval_private_threshold_plain_norm_many(self.S.ev, cts, ct_t, self.spec.norm, self.chain,
+                                                                 self.S.keys, streams, mode)
         acc = outs[0]
         for o in outs[1:]:
             acc = self.S.ev.add(acc, o)
@@ -275,8 +283,10 @@ class Statement:
     def gpu_ladder(self, blocks):
         q, bl = self._bind(self.client, self.blocks)
         sel = [bl[self.mine.index(b)] for b in blocks]
-        return self.W.statement_partial(self.S, q, sel, self.W.threshold_fn(self.S, self.chain,
-                                                                              self.G.PolyEval.ladder), len(sel))
+        thr = self.W.threshold_fn(self.S, self.chain, self.G.PolyEval.ladder)
+        if self.batched:  # the product path, in ladder mode
+            return self.W.statement_partial_batched(self.S, q, sel, thr, streams=2, max_blocks=self.max_blocks)
+        return self.W.statement_partial(self.S, q, sel, thr, len(sel))
 
 
 WORKLOADS = {3: ThresholdCount, 4: Statement, 5: Statement}
@@ -307,8 +317,7 @@ def run_b200(args):
     t0 = time.time()
     from paper_2412_13269_b200 import distributed as D
     wl = WORKLOADS[args.config](G, W, spec, rank, world, rotations=(rank == 0))
-    if isinstance(wl, Statement):
-        wl.batched, wl.max_blocks = not args.no_batch, args.max_blocks
+    wl.batched, wl.max_blocks = not args.no_batch, args.max_blocks
     S, chain = wl.S, wl.chain
     D.check_exact(world, S.primes)
     S.ring.synchronize()
@@ -603,7 +612,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=8, help="concurrent record-block pipelines per GPU")
+    ap.add_argument("--streams", type=int, default=4, help="concurrent pipelines (host thread + CUDA stream each) per GPU")
     ap.add_argument("--poly-eval", choices=["bsgs", "ladder"], default="bsgs",
                     help="Chebyshev evaluator of the sign stages (BASELINE configs specify BSGS)")
     ap.add_argument("--no-batch", action="store_true",
