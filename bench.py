@@ -53,28 +53,46 @@ def log(*a):
 # clocks sampling (B200_PROFILING.md: sample during the timed region)
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + clock-event reasons sampled in-process through NVML every
+    0.1 s during the timed region (spawning nvidia-smi repeatedly stalls the
+    driver and shows up as step-time spikes)."""
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, pci_bus_id: str | None = None):
         self.device = device
-        self.rows: list[list[str]] = []
+        self.pci = pci_bus_id
+        self.samples: list[tuple[int, int, int]] = []
         self._stop = threading.Event()
         self._thr = None
+        self.error = None
 
     def _run(self):
-        while not self._stop.is_set():
+        try:
+            import pynvml
+            pynvml.nvmlInit()
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                for line in out.stdout.strip().splitlines():
-                    self.rows.append([x.strip() for x in line.split(",")])
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(self.pci) if self.pci else None
             except Exception:
-                pass
-            self._stop.wait(0.2)
+                h = None
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                try:
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((sm, smax, rs))
+                self._stop.wait(0.1)
+            pynvml.nvmlShutdown()
+        except Exception as e:  # reported in the JSON line
+            self.error = str(e)[:120]
 
     def __enter__(self):
+        if os.environ.get("TG_NO_CLOCKS") == "1":  # diagnostics: no sampler
+            return self
         self._thr = threading.Thread(target=self._run, daemon=True)
         self._thr.start()
         return self
@@ -85,18 +103,13 @@ class ClockSampler:
             self._thr.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for i, n in enumerate(names):
-                if len(r) > 5 + i and r[5 + i].lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.error or "NVML unavailable"],
+                    "samples": 0}
+        reasons = sorted({n for _, _, rs in self.samples for n, bit in self.REASONS if rs & bit})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "NVML"}
 
 
 def measured_peaks():
@@ -323,6 +336,8 @@ def run_b200(args):
     S.ring.synchronize()
     log(f"[rank {rank}] setup {time.time() - t0:.1f}s: {spec.name} N={spec.N} L={spec.nq - 1} K={spec.K} "
         f"blocks={wl.mine}")
+    # stream-ordered pool grown once up front: no memory mapping inside timed steps
+    G.pool_reserve(S.ring, int(args.pool_gb * (1 << 30)))
     mode = G.PolyEval.bsgs if args.poly_eval == "bsgs" else G.PolyEval.ladder
     ext = torch.cuda.ExternalStream(S.ring.stream_handle(), device=torch.device("cuda", local))
     flush = torch.empty(64 << 22, dtype=torch.int32, device="cuda")  # 1 GiB > 126 MB L2
@@ -372,7 +387,12 @@ def run_b200(args):
     barrier()
     # timed region (device-resident inputs)
     prof_region = os.environ.get("TG_PROFILE_REGION") == "1"  # ncu --profile-from-start off
-    with ClockSampler(local) as clocks:
+    try:  # NVML handle by PCI address (CUDA and NVML indices can differ)
+        pr = torch.cuda.get_device_properties(local)
+        pci = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+    except Exception:
+        pci = None
+    with ClockSampler(local, pci) as clocks:
         barrier()
         if prof_region:
             torch.cuda.cudart().cudaProfilerStart()
@@ -381,6 +401,7 @@ def run_b200(args):
             torch.cuda.cudart().cudaProfilerStop()
         barrier()
     ms_step = sum(ms_list) / len(ms_list)
+    log(f"[rank {rank}] step ms: " + " ".join(f"{m:.1f}" for m in ms_list))
     if world > 1:
         tt = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -399,32 +420,40 @@ def run_b200(args):
 
     # end to end through the public API: the query's client ciphertexts come
     # from pinned host memory every step, the count goes back to the host
-    host_in = []
+    # all client ciphertexts in one pinned buffer -> one H2D DMA per step
+    metas, off = [], 0
     for c in wl.client:
-        arr = G.pinned_empty([len(c.parts), c.level() + 1, spec.N])
-        G.ciphertext_to_numpy(c, arr)
-        host_in.append((arr, c.level(), c.scale, c.sk_id))
+        metas.append((off, len(c.parts), c.level(), c.scale, c.sk_id))
+        off += len(c.parts) * (c.level() + 1) * spec.N
+    host_buf = G.pinned_empty([off])
+    for c, m in zip(wl.client, metas):
+        n = m[1] * (m[2] + 1) * spec.N
+        G.ciphertext_to_numpy(c, host_buf[m[0]:m[0] + n])
     out_lvl = res.level() if rank == 0 else 0
     host_out = G.pinned_empty([2, out_lvl + 1, spec.N])
 
+    uploader = G.HostUpload(S.ring, host_buf, metas, G.Form.coeff, G.Domain.slots)
+
     def e2e_step():
-        ups = [G.ciphertext_from_numpy(S.ring, a, lv, G.Form.coeff, sc, G.Domain.slots, sid)
-               for (a, lv, sc, sid) in host_in]
+        ups = uploader.upload()  # every step: pinned host -> HBM, one DMA
         r = query(ups)
         if rank == 0:
             G.ciphertext_to_numpy(r, host_out)
         return r
 
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(max(2, args.warmup)):
         e2e_step()
     barrier()
     e2e_ms_list, _ = timed(e2e_step, args.steps)
     e2e_ms = sum(e2e_ms_list) / len(e2e_ms_list)
+    log(f"[rank {rank}] e2e step ms: " + " ".join(f"{m:.1f}" for m in e2e_ms_list))
+    res_b, used_hi = G.pool_stats(S.ring)
+    log(f"[rank {rank}] pool reserved {res_b / 2**30:.1f} GiB, used high-water {used_hi / 2**30:.1f} GiB")
     if world > 1:
         tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    h2d = sum(a.nbytes for a, _, _, _ in host_in)
+    h2d = int(host_buf.nbytes)
     d2h = host_out.nbytes if rank == 0 else 0
 
     # decrypt + check the count (rank 0)
@@ -618,6 +647,7 @@ def main():
     ap.add_argument("--no-batch", action="store_true",
                     help="statement workloads: one ciphertext per pipeline instead of ciphertext batches")
     ap.add_argument("--max-blocks", type=int, default=8, help="record blocks per ciphertext batch")
+    ap.add_argument("--pool-gb", type=float, default=48.0, help="device memory pool reserved up front (GiB)")
     ap.add_argument("--config", type=int, choices=[3, 4, 5], default=4,
                     help="BASELINE.json workload: 4 = full TETRIS statement (default), 3 = threshold count, "
                          "5 = scale-out stress")

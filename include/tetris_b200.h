@@ -80,6 +80,13 @@ int tg_stream_destroy(tg_context* ctx, void* stream);
 /* Device index the context lives on. */
 int tg_context_device(const tg_context* ctx);
 
+/* Device memory pool of a context (stream-ordered allocations of every op).
+ * tg_pool_reserve grows the pool to hold at least `bytes` (allocate + free),
+ * so later allocations never map new memory inside a timed region;
+ * tg_pool_stats reports reserved bytes and the used high-water mark. */
+int tg_pool_reserve(tg_context* ctx, uint64_t bytes);
+int tg_pool_stats(tg_context* ctx, uint64_t* reserved, uint64_t* used_high);
+
 /* Page-locked host memory (end-to-end H2D/D2H staging). */
 int tg_host_alloc_pinned(void** ptr, size_t bytes);
 int tg_host_free_pinned(void* ptr);

@@ -214,6 +214,8 @@ public:
     std::shared_ptr<DeviceBuffer> find_eval(std::size_t off, int level, int nspecial, int nparts, void* stream) const;
     void put_eval(std::size_t off, int level, int nspecial, int nparts, void* stream,
                   std::shared_ptr<DeviceBuffer> buf) const;
+    // contents are about to be overwritten (reused upload buffers)
+    void clear_eval_cache() const;
 
 private:
     std::shared_ptr<DeviceState> dev_;

@@ -308,6 +308,11 @@ void DeviceBuffer::put_eval(std::size_t off, int level, int nspecial, int nparts
     cache_.push_back(EvalCache{off, level, nspecial, nparts, stream, std::move(buf)});
 }
 
+void DeviceBuffer::clear_eval_cache() const {
+    std::lock_guard<std::mutex> g(cache_mu_);
+    cache_.clear();
+}
+
 // Freed on the destroying thread's current stream: ordered after that
 // thread's uses; buffers crossing threads are handed over only after the
 // producing stream was synchronized (see eval_private_threshold_many).

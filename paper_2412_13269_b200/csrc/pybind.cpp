@@ -339,6 +339,15 @@ PYBIND11_MODULE(_tetris_b200, m) {
             if (n[i]) d[tg_profile_op_name(i)] = py::make_tuple(ms[i], n[i], bytes[i]);
         return d;
     });
+    m.def("pool_reserve", [](const RingParams& r, uint64_t bytes) {
+        py::gil_scoped_release nogil;
+        check_tg(tg_pool_reserve(r.dev(), bytes));
+    });
+    m.def("pool_stats", [](const RingParams& r) {
+        uint64_t res = 0, hi = 0;
+        check_tg(tg_pool_stats(r.dev(), &res, &hi));
+        return py::make_tuple(res, hi);
+    });
     m.def("pinned_empty", [](std::vector<py::ssize_t> shape) {
         py::ssize_t count = 1;
         for (auto s : shape) count *= s;
@@ -371,6 +380,80 @@ PYBIND11_MODULE(_tetris_b200, m) {
             return ct;
         },
         py::keep_alive<0, 1>());
+    // Many ciphertexts from ONE host buffer: one H2D copy into one HBM block
+    // (one DMA, one synchronize). metas: (word offset, parts, level, scale,
+    // sk_id) per ciphertext, parts of (level+1) x N words back to back.
+    m.def(
+        "ciphertexts_from_host",
+        [](const RingParams& ring, py::array_t<uint64_t, py::array::c_style> a,
+           const std::vector<std::tuple<std::size_t, int, int, double, u64>>& metas, Form form, Domain domain) {
+            const std::size_t total = std::size_t(a.size());
+            for (const auto& m : metas) {
+                const std::size_t need = std::get<0>(m) + std::size_t(std::get<1>(m)) * (std::get<2>(m) + 1) * ring.degree();
+                if (need > total) throw TetrisError("ckks", "ciphertexts_from_host: buffer too small");
+            }
+            auto blk = std::make_shared<DeviceBuffer>(ring, total);
+            {
+                py::gil_scoped_release nogil;
+                check_tg(tg_memcpy_h2d(ring.dev(), blk->data(), a.data(), total * 8, ring.stream()));
+                ring.synchronize();
+            }
+            std::vector<Ciphertext> out;
+            for (const auto& [off, np, level, scale, sk] : metas) {
+                const std::size_t w = std::size_t(level + 1) * ring.degree();
+                Ciphertext ct;
+                for (int i = 0; i < np; ++i) ct.parts.push_back(Poly::view(ring, blk, off + w * i, level, form, 0));
+                ct.scale = scale;
+                ct.domain = domain;
+                ct.sk_id = sk;
+                out.push_back(std::move(ct));
+            }
+            return out;
+        });
+    // Reused upload target for end-to-end runs: the same HBM block receives
+    // the host buffer on every upload() (one DMA + synchronize); memoised
+    // transforms of the previous contents are dropped first.
+    struct HostUpload {
+        const RingParams* ring;
+        py::array_t<uint64_t, py::array::c_style> host;
+        std::vector<std::tuple<std::size_t, int, int, double, u64>> metas;
+        Form form;
+        Domain domain;
+        std::shared_ptr<DeviceBuffer> blk;
+    };
+    py::class_<HostUpload>(m, "HostUpload")
+        .def(py::init([](const RingParams& ring, py::array_t<uint64_t, py::array::c_style> a,
+                         std::vector<std::tuple<std::size_t, int, int, double, u64>> metas, Form form, Domain domain) {
+                 for (const auto& mt : metas) {
+                     const std::size_t need =
+                         std::get<0>(mt) + std::size_t(std::get<1>(mt)) * (std::get<2>(mt) + 1) * ring.degree();
+                     if (need > std::size_t(a.size())) throw TetrisError("ckks", "HostUpload: buffer too small");
+                 }
+                 auto blk = std::make_shared<DeviceBuffer>(ring, std::size_t(a.size()));
+                 return HostUpload{&ring, a, std::move(metas), form, domain, blk};
+             }),
+             py::keep_alive<1, 2>())
+        .def("upload", [](HostUpload& u) {
+            const RingParams& ring = *u.ring;
+            {
+                py::gil_scoped_release nogil;
+                u.blk->clear_eval_cache();
+                check_tg(tg_memcpy_h2d(ring.dev(), u.blk->data(), u.host.data(), std::size_t(u.host.size()) * 8,
+                                       ring.stream()));
+                ring.synchronize();
+            }
+            std::vector<Ciphertext> out;
+            for (const auto& [off, np, level, scale, sk] : u.metas) {
+                const std::size_t w = std::size_t(level + 1) * ring.degree();
+                Ciphertext ct;
+                for (int i = 0; i < np; ++i) ct.parts.push_back(Poly::view(ring, u.blk, off + w * i, level, u.form, 0));
+                ct.scale = scale;
+                ct.domain = u.domain;
+                ct.sk_id = sk;
+                out.push_back(std::move(ct));
+            }
+            return out;
+        });
     m.def("ciphertext_to_numpy", [](const Ciphertext& ct, py::array_t<uint64_t, py::array::c_style> out) {
         const RingParams& ring = ct.ring();
         const std::size_t w = ct.parts[0].words();

@@ -159,10 +159,28 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
         R.twd = static_cast<const double*>(ctx->dev_fp);
         R.qd = R.twd + nt;
     }
-    // stream-ordered pool: keep freed blocks cached (no release back to the OS)
-    cudaDeviceGetDefaultMemPool(&ctx->pool, device);
-    uint64_t threshold = UINT64_MAX;
-    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    // stream-ordered pool of this context: freed blocks stay cached (no
+    // release back to the driver), and a block freed on one stream is reused
+    // by another only once the free is known complete (opportunistic reuse):
+    // the allocator never inserts waits between streams, so concurrent
+    // pipelines (one stream each) are not serialised by memory reuse.
+    {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaError_t e = cudaMemPoolCreate(&ctx->pool, &props);
+        if (e != cudaSuccess) {
+            cudaFree(ctx->dev_block);
+            if (ctx->dev_fp) cudaFree(ctx->dev_fp);
+            delete ctx;
+            return cuda_fail(e, "cudaMemPoolCreate");
+        }
+        uint64_t threshold = UINT64_MAX;
+        int no = 0;
+        cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+        cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolReuseAllowInternalDependencies, &no);
+    }
     *out = ctx;
     return TG_OK;
 }
@@ -178,6 +196,7 @@ extern "C" void tg_context_destroy(tg_context* ctx) {
     for (auto e : ctx->prof_free) cudaEventDestroy(e);
     cudaFree(ctx->dev_block);
     if (ctx->dev_fp) cudaFree(ctx->dev_fp);
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     delete ctx;
 }
 
@@ -413,4 +432,26 @@ extern "C" void tg_gadget_destroy(tg_gadget* g) {
 extern "C" uint32_t tg_gadget_digit_count(const tg_gadget* g, int level) {
     // group_count(level) = (level + group_size) / group_size (rlwe.hpp:50-52)
     return g ? (u32(level) + g->g.group_size) / g->g.group_size : 0;
+}
+
+extern "C" int tg_pool_reserve(tg_context* ctx, uint64_t bytes) {
+    if (!ctx) return fail(TG_E_ARG, "[gpu] null context");
+    if (bytes == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    void* p = nullptr;
+    TG_CUDA(cudaMallocFromPoolAsync(&p, bytes, ctx->pool, nullptr));
+    TG_CUDA(cudaFreeAsync(p, nullptr));
+    TG_CUDA(cudaStreamSynchronize(nullptr));
+    return TG_OK;
+}
+
+extern "C" int tg_pool_stats(tg_context* ctx, uint64_t* reserved, uint64_t* used_high) {
+    if (!ctx) return fail(TG_E_ARG, "[gpu] null context");
+    DeviceGuard guard(ctx->device);
+    unsigned long long r = 0, u = 0;
+    TG_CUDA(cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &r));
+    TG_CUDA(cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemHigh, &u));
+    if (reserved) *reserved = r;
+    if (used_high) *used_high = u;
+    return TG_OK;
 }

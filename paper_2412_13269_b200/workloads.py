@@ -384,8 +384,8 @@ def statement_partial(S, q, blocks, threshold, streams=1):
 def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8):
     """B200 module: the same per-block statement with the blocks evaluated as
     ciphertext batches (stack_ciphertexts): per chunk of <= max_blocks blocks,
-    one batched threshold over the sugar and pressure columns (same level and
-    norm) and one over the risk scores, then the AND products batched. Each
+    one batched threshold per column (sugar, pressure, risk score; the three
+    run concurrently), then the AND products batched. Each
     block's output is bit-identical to statement_block's (a batch is exactly
     `batch` independent ciphertexts; tests/test_gpu_statement.py); launches
     and switching-key reads are shared by the batch."""
@@ -394,20 +394,17 @@ def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8):
                            streams)
     chunks = [list(range(i, min(len(blocks), i + max_blocks))) for i in range(0, len(blocks), max_blocks)]
     jobs = []
-    for ch in chunks:
+    for ch in chunks:  # three equal batches per chunk, run concurrently
         nb = len(ch)
-        xa = T.stack_ciphertexts([blocks[i].ct_sugar for i in ch] + [blocks[i].ct_bp for i in ch])
-        ta = T.stack_ciphertexts([q.ct_t[0]] * nb + [q.ct_t[1]] * nb)
-        xb = T.stack_ciphertexts([risks[i] for i in ch])
-        tb = T.stack_ciphertexts([q.ct_t[2]] * nb)
-        jobs += [(xa, ta, 1.0), (xb, tb, RISK_NORM)]
+        for col, k, norm in ((lambda b: blocks[b].ct_sugar, 0, 1.0), (lambda b: blocks[b].ct_bp, 1, 1.0),
+                             (lambda b: risks[b], 2, RISK_NORM)):
+            jobs.append((T.stack_ciphertexts([col(i) for i in ch]), T.stack_ciphertexts([q.ct_t[k]] * nb), norm))
     outs = run_concurrent(T, S.ring, lambda j: threshold(*j), jobs, streams)
     acc = None
     for c, ch in enumerate(chunks):
-        nb = len(ch)
-        ba, bb = outs[2 * c], outs[2 * c + 1]
-        a = ev.rescale(ev.mul_relin(T.slice_ciphertext(ba, 0, nb), T.slice_ciphertext(ba, nb, nb), keys))
-        a = ev.rescale(ev.mul_relin(a, bb, keys))
+        b1, b2, b3 = outs[3 * c], outs[3 * c + 1], outs[3 * c + 2]
+        a = ev.rescale(ev.mul_relin(b1, b2, keys))
+        a = ev.rescale(ev.mul_relin(a, b3, keys))
         for i, ct in zip(ch, T.unstack_ciphertext(a)):
             o = ev.rescale(ev.mul_plain(ct, blocks[i].pt_flag, blocks[i].flag_scale))
             acc = o if acc is None else ev.add(acc, o)
