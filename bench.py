@@ -477,8 +477,18 @@ def run_b200(args):
     achieved = (dbytes / dn) / (per_launch_ms / 1e3) / 1e9
     total_prof_ms = sum(v[0] for v in prof.values())
     launches = sum(v[1] * (2 if k.startswith("ntt") else 1) for k, v in prof.items()) // args.steps * args.steps
+    # DRAM traffic per launch of the dominant class from the committed ncu
+    # capture of this workload (profiles/traffic_<workload>.json), else null
+    traffic = None
+    tf = ROOT / "profiles" / f"traffic_{spec.name}.json"
+    if tf.exists():
+        tcls = json.loads(tf.read_text()).get("classes", {}).get(dname)
+        if tcls:
+            traffic = {"bytes_per_launch": tcls["dram_bytes_per_launch"],
+                       "vs_algorithmic": round(tcls["dram_bytes_per_launch"] / (dbytes / dn), 3),
+                       "source": str(tf.relative_to(ROOT))}
     roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                 "bytes_per_launch": dbytes / dn, "ms_per_launch": per_launch_ms,
                 "share_of_step": round(dms / total_prof_ms, 3),
                 "per_kernel": {k: {"ms": round(v[0] / args.steps, 4), "launches": v[1] // args.steps,
