@@ -200,6 +200,12 @@ int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const u
  * (modulus index m) times plain row m; plain holds >= level+1 rows. */
 int tg_mul_plain(tg_context* ctx, uint64_t* out, const uint64_t* ct_part, const uint64_t* plain,
                  int level, uint32_t nparts, void* stream);
+/* LinearTransformPlan::apply giant-bucket sum (ckks.hpp:455-476), eval form:
+ * out = sum_t ct_t (x) plain_t over nparts parts of level+1 rows; each ct_t
+ * holds nparts parts back to back, each plain_t >= level+1 rows. */
+#define TG_PLAIN_SUM_MAX_TERMS 256
+int tg_mul_plain_sum(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* cts,
+                     const uint64_t* const* plains, int level, uint32_t nparts, void* stream);
 
 /* ---- slot encoder ------------------------------------------------------- */
 /* Encoder::encode_slots (ckks.hpp:59-86) for `batch` slot vectors of n slots:
@@ -256,6 +262,13 @@ int tg_keyswitch_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_
  * d, d_eval, out0, out1, add0, add1 each hold npolys polys back to back.
  * Same per-source result as npolys tg_keyswitch_add calls; the key is read
  * once per batch and every launch covers the whole batch. */
+/* ks_inner on given eval-form digits with the epilogue add (out_i = add_i +
+ * ModDown(iNTT(sum_k digit_k * key_k))): the hoisted rotation of
+ * Evaluator::apply_galois_many (ckks.hpp:338-367), whose digits are the
+ * automorphism of ONE decomposition. add0/add1 may be NULL. */
+int tg_ks_inner_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* digits, uint32_t ndigits,
+                    const uint64_t* key, uint32_t key_digits, int level, const uint64_t* add0,
+                    const uint64_t* add1, void* stream);
 int tg_keyswitch_add_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
                            const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
                            const uint64_t* add0, const uint64_t* add1, uint32_t npolys, void* stream);

@@ -10,6 +10,7 @@
 #include <complex>
 #include <functional>
 #include <map>
+#include <set>
 
 #include "tetris_b200/keys.hpp"
 
@@ -77,9 +78,41 @@ public:
     Ciphertext rescale(const Ciphertext& ct) const;
     Ciphertext rotate(const Ciphertext& ct, u32 k, const EvalKeys& keys) const;
     Ciphertext conjugate(const Ciphertext& ct, const EvalKeys& keys) const;
+    // Hoisted automorphism batch (ckks.hpp:338-367).
+    std::vector<Ciphertext> apply_galois_many(const Ciphertext& ct, const std::vector<u64>& exps,
+                                              const EvalKeys& keys) const;
 
 private:
     const KeyContext* ctx_;
+};
+
+// BSGS linear transform plan (ckks.hpp:373-507): the nonzero diagonals of an
+// n x n slot matrix, encoded once (device encoder) and pre-rotated for the
+// giant steps; apply() = hoisted baby rotations, one plaintext-product sum
+// kernel per giant bucket, giant rotations, rescale. Bit-exact with the
+// reference plan.
+class LinearTransformPlan {
+public:
+    LinearTransformPlan(const Encoder& enc, const std::map<u32, std::vector<cplx>>& diagonals, double plain_scale,
+                        int encode_level);
+    static std::map<u32, std::vector<cplx>> diagonals_of(const std::vector<std::vector<cplx>>& m);
+    const std::vector<u64>& required_rotations() const { return rotations_; }
+    double plain_scale() const { return plain_scale_; }
+    u32 baby_count() const { return n1_; }
+    Ciphertext apply(const Evaluator& ev, const Ciphertext& ct, const EvalKeys& keys) const;
+
+private:
+    struct Term {
+        u32 g, b;
+        Poly plain;  // eval form at encode_level
+    };
+    u32 n_;
+    u32 n1_;
+    double plain_scale_;
+    int encode_level_;
+    std::vector<Term> terms_;
+    std::set<u64> baby_, giant_;
+    std::vector<u64> rotations_;
 };
 
 // Chebyshev ladder evaluation (ckks.hpp:515-579), bit-exact with the reference.

@@ -147,6 +147,11 @@ public:
     Ciphertext relinearize(const Ciphertext& ct, const SwitchingKey& rlk) const;
     SwitchingKey galois_key_gen(const SecretKey& sk, u64 exponent, Rng& rng) const;
     Ciphertext apply_galois(const Ciphertext& ct, u64 exponent, const SwitchingKey& swk) const;
+    // Hoisted automorphisms (Evaluator::apply_galois_many, ckks.hpp:338-367):
+    // c1 decomposed once, the eval-form digits permuted per exponent; keys[i]
+    // is the Galois key of exps[i] (ignored for exponent 1).
+    std::vector<Ciphertext> apply_galois_hoisted(const Ciphertext& ct, const std::vector<u64>& exps,
+                                                 const std::vector<const SwitchingKey*>& keys) const;
     double ks_noise_estimate() const;
     SecretKey square_secret(const SecretKey& sk) const;
 

@@ -239,7 +239,16 @@ PYBIND11_MODULE(tetris_ref, m) {
         .def("rescale", &Evaluator::rescale, py::call_guard<py::gil_scoped_release>())
         .def("rotate", &Evaluator::rotate, py::call_guard<py::gil_scoped_release>())
         .def("conjugate", &Evaluator::conjugate, py::call_guard<py::gil_scoped_release>())
+        .def("apply_galois_many", &Evaluator::apply_galois_many, py::call_guard<py::gil_scoped_release>())
         .def_static("scaled_residue", &Evaluator::scaled_residue);
+
+    py::class_<LinearTransformPlan>(m, "LinearTransformPlan")
+        .def(py::init<const Encoder&, const std::map<u32, std::vector<cplx>>&, double, int>(), py::keep_alive<1, 2>())
+        .def_static("diagonals_of", &LinearTransformPlan::diagonals_of)
+        .def("required_rotations", &LinearTransformPlan::required_rotations)
+        .def("plain_scale", &LinearTransformPlan::plain_scale)
+        .def("baby_count", &LinearTransformPlan::baby_count)
+        .def("apply", &LinearTransformPlan::apply, py::call_guard<py::gil_scoped_release>());
 
     m.def("eval_chebyshev", &eval_chebyshev, py::call_guard<py::gil_scoped_release>());
     m.def("inner_sum", &inner_sum, py::call_guard<py::gil_scoped_release>());

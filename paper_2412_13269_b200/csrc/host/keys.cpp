@@ -514,6 +514,48 @@ Ciphertext KeyContext::apply_galois(const Ciphertext& ct, u64 exponent, const Sw
     return out;
 }
 
+std::vector<Ciphertext> KeyContext::apply_galois_hoisted(const Ciphertext& ct, const std::vector<u64>& exps,
+                                                         const std::vector<const SwitchingKey*>& keys) const {
+    if (ct.degree() != 1) throw TetrisError("ckks", "hoisting expects degree-1 input");
+    if (ct.batch != 1) throw TetrisError("ckks", "hoisting on a batch is not supported (unstack it)");
+    Ciphertext src = ct;
+    src.to_coeff();
+    const int lvl = src.level(), k = int(ring_->special_count());
+    const u64 two_n = 2 * u64(ring_->degree());
+    std::vector<Poly> digits = plan_->decompose(src.parts[1]);  // eval form, one block
+    const u32 nd = u32(digits.size());
+    std::vector<Ciphertext> out;
+    out.reserve(exps.size());
+    for (std::size_t e = 0; e < exps.size(); ++e) {
+        const u64 g = exps[e];
+        if (g == 1) {
+            out.push_back(src);
+            continue;
+        }
+        if ((g % two_n) % 2 == 0) throw TetrisError("ring", "automorphism exponent must be odd");
+        const SwitchingKey& swk = *keys.at(e);
+        std::vector<Poly> rd = fresh_parts(*ring_, int(nd), lvl, Form::eval, k);
+        check_tg(tg_automorphism(ring_->dev(), const_cast<u64*>(rd[0].data()), digits[0].data(), g % two_n,
+                                 TG_FORM_EVAL, lvl, k, nd, ring_->stream()));
+        std::vector<Poly> c0g = fresh_parts(*ring_, 1, lvl, Form::coeff);
+        check_tg(tg_automorphism(ring_->dev(), const_cast<u64*>(c0g[0].data()), src.parts[0].data(), g % two_n,
+                                 TG_FORM_COEFF, lvl, 0, 1, ring_->stream()));
+        std::vector<Poly> dst = fresh_parts(*ring_, 2, lvl, Form::coeff);
+        // (phi(c0) + d0, d1): the add fused into ModDown
+        check_tg(tg_ks_inner_add(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[1].data()),
+                                 rd[0].data(), nd, key_base(swk), swk.digits(), lvl, c0g[0].data(), nullptr,
+                                 ring_->stream()));
+        Ciphertext r;
+        r.parts = std::move(dst);
+        r.scale = ct.scale;
+        r.domain = ct.domain;
+        r.sk_id = ct.sk_id;
+        r.noise_bound = ct.noise_bound + ks_noise_estimate();
+        out.push_back(std::move(r));
+    }
+    return out;
+}
+
 double KeyContext::ks_noise_estimate() const {
     return 6.0 * noise_.gaussian_sigma * std::sqrt(double(ring_->degree())) *
            double(plan_->digit_count(ring_->max_level()));

@@ -262,7 +262,16 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("rescale", &Evaluator::rescale, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("rotate", &Evaluator::rotate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("conjugate", &Evaluator::conjugate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("apply_galois_many", &Evaluator::apply_galois_many, py::call_guard<py::gil_scoped_release>())
         .def_static("scaled_residue", &Evaluator::scaled_residue);
+
+    py::class_<LinearTransformPlan>(m, "LinearTransformPlan")
+        .def(py::init<const Encoder&, const std::map<u32, std::vector<cplx>>&, double, int>(), py::keep_alive<1, 2>())
+        .def_static("diagonals_of", &LinearTransformPlan::diagonals_of)
+        .def("required_rotations", &LinearTransformPlan::required_rotations)
+        .def("plain_scale", &LinearTransformPlan::plain_scale)
+        .def("baby_count", &LinearTransformPlan::baby_count)
+        .def("apply", &LinearTransformPlan::apply, py::keep_alive<0, 2>(), py::call_guard<py::gil_scoped_release>());
 
     m.def("eval_chebyshev", &eval_chebyshev, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>());
     m.def("eval_chebyshev_bsgs", &eval_chebyshev_bsgs, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>());

@@ -667,3 +667,20 @@ extern "C" int tg_keyswitch_add_batch(tg_gadget* g, uint64_t* out0, uint64_t* ou
     cudaFreeAsync(scratch, s);
     return rc;
 }
+
+extern "C" int tg_ks_inner_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* digits,
+                               uint32_t ndigits, const uint64_t* key, uint32_t key_digits, int level,
+                               const uint64_t* add0, const uint64_t* add1, void* stream) {
+    if (int rc = check_ks(g, level)) return rc;
+    if (ndigits == 0) return fail(TG_E_ARG, "[rlwe] empty decomposition");
+    if (ndigits > key_digits) return fail(TG_E_ARG, "[rlwe] switching key has too few digits");
+    tg_context* ctx = g->ctx;
+    DeviceGuard guard(ctx->device);
+    cudaStream_t s = as_stream(stream);
+    const size_t words = size_t(level + 1 + ctx->ring.K) * ctx->ring.N;
+    void* acc = nullptr;
+    TG_CUDA(cudaMallocFromPoolAsync(&acc, 2 * words * 8, ctx->pool, s));
+    int rc = ks_inner(g, out0, out1, digits, ndigits, key, level, static_cast<u64*>(acc), s, add0, add1);
+    cudaFreeAsync(acc, s);
+    return rc;
+}

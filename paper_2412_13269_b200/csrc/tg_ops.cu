@@ -133,6 +133,37 @@ __global__ void k_tensor(DevRing R, Shape S, u64* p0, u64* p1, u64* p2, const u6
     }
 }
 
+// LinearTransformPlan::apply giant bucket (ckks.hpp:455-476):
+// out[p][r][i] = sum_t ct_t[p][r][i] * plain_t[r][i] mod q_r, 128-bit lazy
+// accumulation (reduced every 15 terms: products < 2^124), one Barrett per
+// output. ct_t parts are back to back (level+1 rows each); plain_t has at
+// least level+1 rows.
+struct PlainSum {
+    u32 nterms;
+    const u64* ct[TG_PLAIN_SUM_MAX_TERMS];
+    const u64* plain[TG_PLAIN_SUM_MAX_TERMS];
+};
+
+__global__ void k_mul_plain_sum(DevRing R, u64* __restrict__ out, const PlainSum P, int level, u32 nparts) {
+    const u32 N = R.N, rows = u32(level) + 1;
+    const u64 per = u64(rows) * N, total = per * nparts;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
+        const u64 w = i % per;
+        const u32 m = u32(w >> R.logN);
+        const u64 q = R.q[m], rl = R.ratio[2 * m], rh = R.ratio[2 * m + 1];
+        U128 acc{0, 0};
+        u32 pending = 0;
+        for (u32 t = 0; t < P.nterms; ++t) {
+            mac128(acc, P.ct[t][i], P.plain[t][w]);
+            if (++pending == 15 && t + 1 < P.nterms) {
+                acc = U128{barrett128(acc.lo, acc.hi, q, rl, rh), 0};
+                pending = 0;
+            }
+        }
+        out[i] = barrett128(acc.lo, acc.hi, q, rl, rh);
+    }
+}
+
 // Evaluator::mul_plain (ckks.hpp:257-265): part row r x plain row m (= r here)
 __global__ void k_mul_plain(DevRing R, u64* out, const u64* ct, const u64* plain, int level, u32 nparts) {
     const u32 N = R.N, rows = u32(level) + 1;
@@ -317,6 +348,25 @@ extern "C" int tg_poly_reduce(tg_context* ctx, uint64_t* data, int level, int ns
     Shape S = shape_of(ctx, level, nspecial, npolys);
     PROF(TG_OP_REDUCE, 16 * S.words);
     k_reduce<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, data);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_mul_plain_sum(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* cts,
+                                const uint64_t* const* plains, int level, uint32_t nparts, void* stream) {
+    if (int rc = check_shape(ctx, level, 0)) return rc;
+    if (nterms == 0 || nterms > TG_PLAIN_SUM_MAX_TERMS) return fail(TG_E_ARG, "[ckks] plain sum: 1..256 terms");
+    if (nparts == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    PlainSum P{};
+    P.nterms = nterms;
+    for (u32 t = 0; t < nterms; ++t) {
+        P.ct[t] = cts[t];
+        P.plain[t] = plains[t];
+    }
+    const size_t words = size_t(level + 1) * ctx->ring.N * nparts;
+    PROF(TG_OP_MUL_PLAIN, 8.0 * words * (nterms + 1) + 8.0 * words / nparts * nterms);
+    k_mul_plain_sum<<<grid_for(words), kThreads, 0, as_stream(stream)>>>(ctx->ring, out, P, level, nparts);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
