@@ -162,6 +162,14 @@ int tg_poly_add_scalar(tg_context* ctx, uint64_t* out, const uint64_t* a,
  * signed scatter, eval form a slot gather. out must not alias in. */
 int tg_automorphism(tg_context* ctx, uint64_t* out, const uint64_t* in, uint64_t exponent,
                     int form, int level, int nspecial, uint32_t npolys, void* stream);
+/* Poly::mul_monomial (ring.hpp:343-361): out = X^e * in, coeff form.
+ * out must not alias in. */
+int tg_mul_monomial(tg_context* ctx, uint64_t* out, const uint64_t* in, uint64_t e, int level,
+                    int nspecial, uint32_t npolys, void* stream);
+/* raise_level (ring.hpp:523-545): level-0 coeff polys (one row each) lifted
+ * to (new_level, nspecial) rows as centered integers mod q0. */
+int tg_raise_level(tg_context* ctx, uint64_t* out, const uint64_t* in, int new_level, int nspecial,
+                   uint32_t npolys, void* stream);
 /* rescale_round (ring.hpp:493-518): coeff form, level -> level-1 rows.
  * out (level rows) must not alias in (level+1 rows). */
 int tg_rescale(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, uint32_t npolys,

@@ -294,6 +294,11 @@ Poly ntt_transform(const Poly& p, Form target);
 Poly poly_mul(const Poly& a, const Poly& b);
 Poly automorphism_apply(const Poly& p, u64 exponent);
 Poly rescale_round(const Poly& p);
+// Poly::mul_monomial (ring.hpp:343-361): X^e * p, coefficient form.
+Poly mul_monomial(const Poly& p, u32 e);
+// raise_level (ring.hpp:523-545): a level-0 coefficient poly lifted to
+// (new_level, nspecial) as the centered integer mod q0.
+Poly raise_level(const Poly& p, int new_level, int nspecial = 0);
 
 // Samplers: drawn on the host from the same streams as the reference
 // (ring.hpp:442-487), then uploaded.

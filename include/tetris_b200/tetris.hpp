@@ -6,3 +6,4 @@
 #include "tetris_b200/core.hpp"
 #include "tetris_b200/evaluator.hpp"
 #include "tetris_b200/keys.hpp"
+#include "tetris_b200/bootstrap.hpp"

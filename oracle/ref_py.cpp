@@ -20,6 +20,7 @@
 #include <atomic>
 
 #include "tetris/threshold.hpp"
+#include "tetris/bootstrap.hpp"
 
 namespace py = pybind11;
 using namespace tetris;
@@ -119,6 +120,7 @@ PYBIND11_MODULE(tetris_ref, m) {
         .def("copy", [](const Poly& p) { return Poly(p); })
         .def("ntt_forward", &Poly::ntt_forward)
         .def("ntt_inverse", &Poly::ntt_inverse)
+        .def("mul_monomial", &Poly::mul_monomial)
         .def("add_inplace", &Poly::add_inplace)
         .def("sub_inplace", &Poly::sub_inplace)
         .def("negate_inplace", &Poly::negate_inplace)
@@ -129,6 +131,7 @@ PYBIND11_MODULE(tetris_ref, m) {
         .def("drop_to_level", &Poly::drop_to_level);
 
     m.def("ntt_transform", &ntt_transform);
+    m.def("raise_level", &raise_level, py::arg("p"), py::arg("new_level"), py::arg("nspecial") = 0);
     m.def("automorphism_apply", &automorphism_apply);
     m.def("rescale_round", &rescale_round);
     m.def("sample_uniform", &sample_uniform, py::keep_alive<0, 1>());
@@ -284,6 +287,39 @@ PYBIND11_MODULE(tetris_ref, m) {
     m.def("eval_private_threshold", &eval_private_threshold, py::call_guard<py::gil_scoped_release>());
     m.def("eval_private_threshold_plain_norm", &eval_private_threshold_plain_norm, py::call_guard<py::gil_scoped_release>());
 
+
+    // ---- Half-BTS (bootstrap.hpp) ----
+    py::class_<EvalModConfig>(m, "EvalModConfig")
+        .def(py::init([](u32 d, u32 a, u32 k, u32 s, double w) { return EvalModConfig{d, a, k, s, w}; }),
+             py::arg("cheb_degree") = 30, py::arg("double_angles") = 3, py::arg("lattice_bound") = 16,
+             py::arg("arcsine_degree") = 7, py::arg("arcsine_window") = 0.65)
+        .def_readwrite("cheb_degree", &EvalModConfig::cheb_degree)
+        .def_readwrite("double_angles", &EvalModConfig::double_angles)
+        .def_readwrite("lattice_bound", &EvalModConfig::lattice_bound)
+        .def_readwrite("arcsine_degree", &EvalModConfig::arcsine_degree)
+        .def_readwrite("arcsine_window", &EvalModConfig::arcsine_window);
+    py::class_<BootstrapParams>(m, "BootstrapParams")
+        .def(py::init<>())
+        .def_readwrite("slots", &BootstrapParams::slots)
+        .def_readwrite("sparse_log_gap", &BootstrapParams::sparse_log_gap)
+        .def_readwrite("secret_hw", &BootstrapParams::secret_hw)
+        .def_readwrite("ephemeral_hw", &BootstrapParams::ephemeral_hw)
+        .def_readwrite("evalmod", &BootstrapParams::evalmod)
+        .def_readwrite("delta_input", &BootstrapParams::delta_input)
+        .def_readwrite("delta_evalmod", &BootstrapParams::delta_evalmod)
+        .def("depth", &BootstrapParams::depth);
+    py::class_<BootstrapEvaluator>(m, "BootstrapEvaluator")
+        .def(py::init<const KeyContext&, BootstrapParams>(), py::keep_alive<1, 2>(),
+             py::call_guard<py::gil_scoped_release>())
+        .def("required_galois_exponents", &BootstrapEvaluator::required_galois_exponents)
+        .def("trace_exponents", &BootstrapEvaluator::trace_exponents)
+        .def("output_level", &BootstrapEvaluator::output_level)
+        .def("mod_raise", &BootstrapEvaluator::mod_raise, py::call_guard<py::gil_scoped_release>())
+        .def("trace_map", &BootstrapEvaluator::trace_map, py::call_guard<py::gil_scoped_release>())
+        .def("coeffs_to_slots", &BootstrapEvaluator::coeffs_to_slots, py::call_guard<py::gil_scoped_release>())
+        .def("eval_mod", &BootstrapEvaluator::eval_mod, py::call_guard<py::gil_scoped_release>())
+        .def("slots_to_coeffs", &BootstrapEvaluator::slots_to_coeffs, py::call_guard<py::gil_scoped_release>())
+        .def("half_bts", &BootstrapEvaluator::half_bts, py::call_guard<py::gil_scoped_release>());
     // Multi-threaded driver for the CPU baseline: evaluates the threshold on
     // each ciphertext with a std::thread pool (the reference's own granularity,
     // protocol.hpp:297-311), sums the outputs in index order and runs

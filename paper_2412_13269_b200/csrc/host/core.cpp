@@ -493,6 +493,25 @@ Poly automorphism_apply(const Poly& p, u64 exponent) {
     return Poly::view(ring, std::move(st), 0, p.level(), p.form(), p.nspecial());
 }
 
+Poly mul_monomial(const Poly& p, u32 e) {
+    if (p.form() != Form::coeff) throw TetrisError("ring", "mul_monomial expects coeff form");
+    const RingParams& ring = p.ring();
+    auto st = std::make_shared<DeviceBuffer>(ring, p.words());
+    check_tg(tg_mul_monomial(ring.dev(), st->data(), p.data(), e % (2 * ring.degree()), p.level(), p.nspecial(), 1,
+                             ring.stream()));
+    return Poly::view(ring, std::move(st), 0, p.level(), Form::coeff, p.nspecial());
+}
+
+Poly raise_level(const Poly& p, int new_level, int nspecial) {
+    if (p.level() != 0 || p.nspecial() != 0) throw TetrisError("ring", "raise_level expects a level-0 poly");
+    if (p.form() != Form::coeff) throw TetrisError("ring", "raise_level expects coeff form");
+    const RingParams& ring = p.ring();
+    if (new_level < 0 || new_level > ring.max_level()) throw TetrisError("ring", "poly level out of range");
+    auto st = std::make_shared<DeviceBuffer>(ring, std::size_t(new_level + 1 + nspecial) * ring.degree());
+    check_tg(tg_raise_level(ring.dev(), st->data(), p.data(), new_level, nspecial, 1, ring.stream()));
+    return Poly::view(ring, std::move(st), 0, new_level, Form::coeff, nspecial);
+}
+
 Poly rescale_round(const Poly& p) {
     if (p.level() < 1) throw TetrisError("ring", "cannot rescale at level 0");
     if (p.nspecial() != 0) throw TetrisError("ring", "rescale with special rows");

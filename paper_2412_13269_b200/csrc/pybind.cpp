@@ -116,11 +116,14 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("mul_acc_pointwise", &Poly::mul_acc_pointwise)
         .def("mul_scalar_inplace", &Poly::mul_scalar_inplace)
         .def("mul_small_scalar_inplace", &Poly::mul_small_scalar_inplace)
-        .def("drop_to_level", &Poly::drop_to_level);
+        .def("drop_to_level", &Poly::drop_to_level)
+        .def("mul_monomial", [](const Poly& p, u32 e) { return mul_monomial(p, e); }, py::keep_alive<0, 1>());
 
     m.def("ntt_transform", &ntt_transform, py::keep_alive<0, 1>());
     m.def("automorphism_apply", &automorphism_apply, py::keep_alive<0, 1>());
     m.def("rescale_round", &rescale_round, py::keep_alive<0, 1>());
+    m.def("raise_level", &raise_level, py::arg("p"), py::arg("new_level"), py::arg("nspecial") = 0,
+          py::keep_alive<0, 1>());
     m.def("sample_uniform", &sample_uniform, py::keep_alive<0, 1>());
     m.def("sample_gaussian", &sample_gaussian, py::keep_alive<0, 1>());
     m.def("sample_ternary_hw", &sample_ternary_hw, py::keep_alive<0, 1>());
@@ -334,6 +337,39 @@ PYBIND11_MODULE(_tetris_b200, m) {
         "stream_scope", [](const RingParams& ring, std::size_t i) { return PyStreamScope{&ring, i, nullptr}; },
         py::keep_alive<0, 1>());
 
+
+    // ---- Half-BTS (bootstrap.hpp) ----
+    py::class_<EvalModConfig>(m, "EvalModConfig")
+        .def(py::init([](u32 d, u32 a, u32 k, u32 s, double w) { return EvalModConfig{d, a, k, s, w}; }),
+             py::arg("cheb_degree") = 30, py::arg("double_angles") = 3, py::arg("lattice_bound") = 16,
+             py::arg("arcsine_degree") = 7, py::arg("arcsine_window") = 0.65)
+        .def_readwrite("cheb_degree", &EvalModConfig::cheb_degree)
+        .def_readwrite("double_angles", &EvalModConfig::double_angles)
+        .def_readwrite("lattice_bound", &EvalModConfig::lattice_bound)
+        .def_readwrite("arcsine_degree", &EvalModConfig::arcsine_degree)
+        .def_readwrite("arcsine_window", &EvalModConfig::arcsine_window);
+    py::class_<BootstrapParams>(m, "BootstrapParams")
+        .def(py::init<>())
+        .def_readwrite("slots", &BootstrapParams::slots)
+        .def_readwrite("sparse_log_gap", &BootstrapParams::sparse_log_gap)
+        .def_readwrite("secret_hw", &BootstrapParams::secret_hw)
+        .def_readwrite("ephemeral_hw", &BootstrapParams::ephemeral_hw)
+        .def_readwrite("evalmod", &BootstrapParams::evalmod)
+        .def_readwrite("delta_input", &BootstrapParams::delta_input)
+        .def_readwrite("delta_evalmod", &BootstrapParams::delta_evalmod)
+        .def("depth", &BootstrapParams::depth);
+    py::class_<BootstrapEvaluator>(m, "BootstrapEvaluator")
+        .def(py::init<const KeyContext&, BootstrapParams>(), py::keep_alive<1, 2>(),
+             py::call_guard<py::gil_scoped_release>())
+        .def("required_galois_exponents", &BootstrapEvaluator::required_galois_exponents)
+        .def("trace_exponents", &BootstrapEvaluator::trace_exponents)
+        .def("output_level", &BootstrapEvaluator::output_level)
+        .def("mod_raise", &BootstrapEvaluator::mod_raise, py::call_guard<py::gil_scoped_release>())
+        .def("trace_map", &BootstrapEvaluator::trace_map, py::call_guard<py::gil_scoped_release>())
+        .def("coeffs_to_slots", &BootstrapEvaluator::coeffs_to_slots, py::call_guard<py::gil_scoped_release>())
+        .def("eval_mod", &BootstrapEvaluator::eval_mod, py::call_guard<py::gil_scoped_release>())
+        .def("slots_to_coeffs", &BootstrapEvaluator::slots_to_coeffs, py::call_guard<py::gil_scoped_release>())
+        .def("half_bts", &BootstrapEvaluator::half_bts, py::call_guard<py::gil_scoped_release>());
     // ---- kernel timing, end-to-end transfer helpers --------------------------
     m.def("profile_enable", [](const RingParams& r, bool on) { check_tg(tg_profile_enable(r.dev(), on ? 1 : 0)); });
     m.def("profile_read", [](const RingParams& r) {

@@ -84,6 +84,37 @@ __global__ void k_auto_coeff(DevRing R, Shape S, u64* out, const u64* in, u64 g)
     }
 }
 
+// Poly::mul_monomial (ring.hpp:343-361): X^e * a, coefficient i -> i + e
+// (mod 2N) with the negacyclic sign.
+__global__ void k_mul_monomial(DevRing R, Shape S, u64* out, const u64* in, u64 e) {
+    const u64 two_n = 2 * u64(R.N);
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u64 row_off = i & ~u64(R.N - 1);
+        const u64 j = ((i & (R.N - 1)) + e) % two_n;
+        const u64 v = in[i];
+        if (j < R.N) out[row_off + j] = v;
+        else out[row_off + j - R.N] = neg_mod(v, R.q[row_mod(R, S, i)]);
+    }
+}
+
+// raise_level (ring.hpp:523-545): level-0 residues a (mod q0) lifted to every
+// row of the new shape as the centered integer (a > q0/2 -> a - q0).
+__global__ void k_raise_level(DevRing R, Shape S, u64* out, const u64* in) {
+    const u64 q0 = R.q[0], half = q0 >> 1;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u64 poly = i / (u64(S.rpp) * R.N);
+        const u64 a = in[poly * R.N + (i & (R.N - 1))];
+        const u32 m = row_mod(R, S, i);
+        if (m == 0) {
+            out[i] = a;
+            continue;
+        }
+        const u64 q = R.q[m], rl = R.ratio[2 * m], rh = R.ratio[2 * m + 1];
+        const u64 v = reduce64(a, q, rl, rh);
+        out[i] = a > half ? sub_mod(v, reduce64(q0, q, rl, rh), q) : v;
+    }
+}
+
 // automorphism_apply, evaluation form (ring.hpp:428-434): slot gather
 __global__ void k_auto_eval(DevRing R, Shape S, u64* out, const u64* in, u64 g) {
     const u64 two_n = 2 * u64(R.N);
@@ -367,6 +398,31 @@ extern "C" int tg_mul_plain_sum(tg_context* ctx, uint64_t* out, uint32_t nterms,
     const size_t words = size_t(level + 1) * ctx->ring.N * nparts;
     PROF(TG_OP_MUL_PLAIN, 8.0 * words * (nterms + 1) + 8.0 * words / nparts * nterms);
     k_mul_plain_sum<<<grid_for(words), kThreads, 0, as_stream(stream)>>>(ctx->ring, out, P, level, nparts);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_mul_monomial(tg_context* ctx, uint64_t* out, const uint64_t* in, uint64_t e, int level,
+                               int nspecial, uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, nspecial, npolys);
+    PROF(TG_OP_AUTOMORPHISM, 16.0 * S.words);
+    k_mul_monomial<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, in,
+                                                                         e % (2 * u64(ctx->ring.N)));
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_raise_level(tg_context* ctx, uint64_t* out, const uint64_t* in, int new_level, int nspecial,
+                              uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, new_level, nspecial)) return rc;
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, new_level, nspecial, npolys);
+    PROF(TG_OP_SCALAR, 8.0 * S.words + 8.0 * ctx->ring.N * npolys);
+    k_raise_level<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, in);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
