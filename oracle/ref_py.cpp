@@ -21,6 +21,7 @@
 
 #include "tetris/threshold.hpp"
 #include "tetris/bootstrap.hpp"
+#include "tetris/serialize.hpp"
 
 namespace py = pybind11;
 using namespace tetris;
@@ -320,6 +321,25 @@ PYBIND11_MODULE(tetris_ref, m) {
         .def("eval_mod", &BootstrapEvaluator::eval_mod, py::call_guard<py::gil_scoped_release>())
         .def("slots_to_coeffs", &BootstrapEvaluator::slots_to_coeffs, py::call_guard<py::gil_scoped_release>())
         .def("half_bts", &BootstrapEvaluator::half_bts, py::call_guard<py::gil_scoped_release>());
+
+    // ---- wire formats (serialize.hpp) ----
+    auto to_bytes = [](const std::vector<uint8_t>& v) { return py::bytes(reinterpret_cast<const char*>(v.data()), v.size()); };
+    auto from_bytes = [](const py::bytes& b) {
+        std::string s = b;
+        return std::vector<uint8_t>(s.begin(), s.end());
+    };
+    m.def("serialize_ciphertext", [to_bytes](const Ciphertext& c) { return to_bytes(serialize_ciphertext(c)); });
+    m.def("deserialize_ciphertext", [from_bytes](const py::bytes& b, const RingParams& r) {
+        return deserialize_ciphertext(from_bytes(b), r); });
+    m.def("ciphertext_size", &ciphertext_size, py::arg("ring"), py::arg("level"), py::arg("parts") = 2);
+    m.def("serialize_switching_key", [to_bytes](const SwitchingKey& k) { return to_bytes(serialize_switching_key(k)); });
+    m.def("deserialize_switching_key", [from_bytes](const py::bytes& b, const RingParams& r) {
+        return deserialize_switching_key(from_bytes(b), r); });
+    m.def("serialize_chain", [to_bytes](const MinimaxChain& c) { return to_bytes(serialize_chain(c)); });
+    m.def("deserialize_chain", [from_bytes](const py::bytes& b) { return deserialize_chain(from_bytes(b)); });
+    m.def("serialize_secret_key", [to_bytes](const SecretKey& k) { return to_bytes(serialize_secret_key(k)); });
+    m.def("deserialize_secret_key", [from_bytes](const py::bytes& b, const RingParams& r) {
+        return deserialize_secret_key(from_bytes(b), r); });
     // Multi-threaded driver for the CPU baseline: evaluates the threshold on
     // each ciphertext with a std::thread pool (the reference's own granularity,
     // protocol.hpp:297-311), sums the outputs in index order and runs

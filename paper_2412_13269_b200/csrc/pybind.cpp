@@ -9,6 +9,7 @@
 #include <chrono>
 
 #include "tetris_b200/tetris.hpp"
+#include "tetris_b200/serialize.hpp"
 
 namespace py = pybind11;
 using namespace tetris_b200;
@@ -370,6 +371,25 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("eval_mod", &BootstrapEvaluator::eval_mod, py::call_guard<py::gil_scoped_release>())
         .def("slots_to_coeffs", &BootstrapEvaluator::slots_to_coeffs, py::call_guard<py::gil_scoped_release>())
         .def("half_bts", &BootstrapEvaluator::half_bts, py::call_guard<py::gil_scoped_release>());
+
+    // ---- wire formats (serialize.hpp) ----
+    auto to_bytes = [](const std::vector<uint8_t>& v) { return py::bytes(reinterpret_cast<const char*>(v.data()), v.size()); };
+    auto from_bytes = [](const py::bytes& b) {
+        std::string s = b;
+        return std::vector<uint8_t>(s.begin(), s.end());
+    };
+    m.def("serialize_ciphertext", [to_bytes](const Ciphertext& c) { return to_bytes(serialize_ciphertext(c)); });
+    m.def("deserialize_ciphertext", [from_bytes](const py::bytes& b, const RingParams& r) {
+        return deserialize_ciphertext(from_bytes(b), r); }, py::keep_alive<0, 2>());
+    m.def("ciphertext_size", &ciphertext_size, py::arg("ring"), py::arg("level"), py::arg("parts") = 2);
+    m.def("serialize_switching_key", [to_bytes](const SwitchingKey& k) { return to_bytes(serialize_switching_key(k)); });
+    m.def("deserialize_switching_key", [from_bytes](const py::bytes& b, const RingParams& r) {
+        return deserialize_switching_key(from_bytes(b), r); }, py::keep_alive<0, 2>());
+    m.def("serialize_chain", [to_bytes](const MinimaxChain& c) { return to_bytes(serialize_chain(c)); });
+    m.def("deserialize_chain", [from_bytes](const py::bytes& b) { return deserialize_chain(from_bytes(b)); });
+    m.def("serialize_secret_key", [to_bytes](const SecretKey& k) { return to_bytes(serialize_secret_key(k)); });
+    m.def("deserialize_secret_key", [from_bytes](const py::bytes& b, const RingParams& r) {
+        return deserialize_secret_key(from_bytes(b), r); }, py::keep_alive<0, 2>());
     // ---- kernel timing, end-to-end transfer helpers --------------------------
     m.def("profile_enable", [](const RingParams& r, bool on) { check_tg(tg_profile_enable(r.dev(), on ? 1 : 0)); });
     m.def("profile_read", [](const RingParams& r) {
