@@ -162,6 +162,21 @@ int tg_poly_add_scalar(tg_context* ctx, uint64_t* out, const uint64_t* a,
  * signed scatter, eval form a slot gather. out must not alias in. */
 int tg_automorphism(tg_context* ctx, uint64_t* out, const uint64_t* in, uint64_t exponent,
                     int form, int level, int nspecial, uint32_t npolys, void* stream);
+/* Large-domain PFE eval_scores (pfe.hpp:73-114): out holds nrows
+ * ciphertexts (2 parts x level+1 rows), row r = sum_c X^{exps[r*ncols+c]} tv_c.
+ * tvs: ncols device pointers to test-vector ciphertexts (parts back to back);
+ * exps: device array [nrows][ncols] of exponents in [0, 2N). */
+#define TG_PFE_MAX_COLS 64
+int tg_pfe_eval(tg_context* ctx, uint64_t* out, const uint64_t* const* tvs, uint32_t ncols,
+                const uint32_t* exps, uint32_t nrows, int level, void* stream);
+/* merge_embed / ring_split data movement (rlwe.hpp:702-790), ring-agnostic:
+ * out[row][k*stride + i] = in_dev[i][row][k] (NULL or i >= count -> 0) over
+ * rows_total rows of n_small; in_dev is a DEVICE array of count pointers.
+ * tg_deinterleave is the inverse gather of one residue class (parity). */
+int tg_interleave(uint64_t* out, const uint64_t* const* in_dev, uint32_t count, uint32_t stride,
+                  uint32_t n_small, uint64_t rows_total, void* stream);
+int tg_deinterleave(uint64_t* out, const uint64_t* in, uint32_t parity, uint32_t stride, uint32_t n_small,
+                    uint64_t rows_total, void* stream);
 /* Poly::mul_monomial (ring.hpp:343-361): out = X^e * in, coeff form.
  * out must not alias in. */
 int tg_mul_monomial(tg_context* ctx, uint64_t* out, const uint64_t* in, uint64_t e, int level,

@@ -132,6 +132,8 @@ PYBIND11_MODULE(tetris_ref, m) {
         .def("drop_to_level", &Poly::drop_to_level);
 
     m.def("ntt_transform", &ntt_transform);
+    m.def("poly_from_i64", &poly_from_i64, py::arg("ring"), py::arg("coeffs"), py::arg("level"),
+          py::arg("nspecial") = 0);
     m.def("raise_level", &raise_level, py::arg("p"), py::arg("new_level"), py::arg("nspecial") = 0);
     m.def("automorphism_apply", &automorphism_apply);
     m.def("rescale_round", &rescale_round);
@@ -340,6 +342,61 @@ PYBIND11_MODULE(tetris_ref, m) {
     m.def("serialize_secret_key", [to_bytes](const SecretKey& k) { return to_bytes(serialize_secret_key(k)); });
     m.def("deserialize_secret_key", [from_bytes](const py::bytes& b, const RingParams& r) {
         return deserialize_secret_key(from_bytes(b), r); });
+
+    // ---- PFE, repacking, ring merge/split (pfe.hpp, repack.hpp, rlwe.hpp:684-802) ----
+    auto ct_ptrs = [](const py::list& l) {
+        std::vector<const Ciphertext*> v;
+        for (auto h : l) v.push_back(h.is_none() ? nullptr : &h.cast<const Ciphertext&>());
+        return v;
+    };
+    py::class_<FunctionSpec>(m, "FunctionSpec")
+        .def(py::init<>())
+        .def_readwrite("lo", &FunctionSpec::lo)
+        .def_readwrite("hi", &FunctionSpec::hi)
+        .def_readwrite("table", &FunctionSpec::table)
+        .def_readwrite("out_min", &FunctionSpec::out_min)
+        .def_readwrite("out_max", &FunctionSpec::out_max)
+        .def("max_value", &FunctionSpec::max_value)
+        .def("validate", &FunctionSpec::validate);
+    py::class_<TestVector>(m, "TestVector")
+        .def(py::init<>())
+        .def_readwrite("ct", &TestVector::ct)
+        .def_readwrite("lo", &TestVector::lo)
+        .def_readwrite("hi", &TestVector::hi)
+        .def_readwrite("max_value", &TestVector::max_value);
+    m.def("encode_input", &encode_input);
+    m.def("build_test_vector", &build_test_vector);
+    m.def("lookup", &lookup);
+    m.def("eval_scores", [](const std::vector<std::vector<double>>& rows, const std::vector<TestVector>& tvs,
+                            bool trace) {
+        std::vector<std::string> t;
+        auto out = eval_scores(rows, tvs, trace ? &t : nullptr);
+        return py::make_tuple(out, t);
+    }, py::arg("rows"), py::arg("tvs"), py::arg("trace") = false);
+    py::class_<RepackKeySet>(m, "RepackKeySet")
+        .def(py::init<>())
+        .def_readwrite("exponents", &RepackKeySet::exponents)
+        .def_readwrite("keys", &RepackKeySet::keys)
+        .def_readwrite("sk_id", &RepackKeySet::sk_id);
+    m.def("repack_exponents", &repack_exponents);
+    m.def("gen_repack_keys", &gen_repack_keys);
+    m.def("repack", [ct_ptrs](const KeyContext& ctx, const py::list& cts, const RepackKeySet& keys) {
+        RepackStats st;
+        auto v = ct_ptrs(cts);
+        Ciphertext out;
+        {
+            py::gil_scoped_release nogil;
+            out = repack(ctx, v, keys, &st);
+        }
+        return py::make_tuple(out, st.automorphisms);
+    });
+    m.def("embed_secret", &embed_secret);
+    m.def("merge_embed", [ct_ptrs](const py::list& cts, const RingParams& big) { return merge_embed(ct_ptrs(cts), big); });
+    m.def("ring_merge", &ring_merge);
+    m.def("ring_merge_many", [ct_ptrs](const KeyContext& ctx, const py::list& cts, const SwitchingKey& swk) {
+        return ring_merge_many(ctx, ct_ptrs(cts), swk);
+    });
+    m.def("ring_split", &ring_split);
     // Multi-threaded driver for the CPU baseline: evaluates the threshold on
     // each ciphertext with a std::thread pool (the reference's own granularity,
     // protocol.hpp:297-311), sums the outputs in index order and runs

@@ -10,11 +10,40 @@
 
 #include "tetris_b200/tetris.hpp"
 #include "tetris_b200/serialize.hpp"
+#include "tetris_b200/pfe.hpp"
 
 namespace py = pybind11;
 using namespace tetris_b200;
 
 namespace {
+
+// Polys borrow their RingParams by raw pointer (the reference's ownership,
+// ring.hpp:369). Results returned inside lists / tuples cannot carry a
+// keep_alive, so each element is tied to the ring's Python object here.
+py::object tie_to_ring(py::object result, const RingParams& ring) {
+    py::handle ring_obj = py::cast(&ring, py::return_value_policy::reference);
+    auto tie = [&](py::handle h) {
+        if (py::isinstance<Ciphertext>(h) || py::isinstance<Poly>(h) || py::isinstance<SecretKey>(h) ||
+            py::isinstance<PublicKey>(h))
+            py::detail::keep_alive_impl(h, ring_obj);
+    };
+    if (py::isinstance<py::tuple>(result) || py::isinstance<py::list>(result)) {
+        for (py::handle h : result) {
+            if (py::isinstance<py::list>(h))
+                for (py::handle g : h) tie(g);
+            else
+                tie(h);
+        }
+    } else {
+        tie(result);
+    }
+    return result;
+}
+
+template <class T>
+py::object tied(T&& value, const RingParams& ring) {
+    return tie_to_ring(py::cast(std::forward<T>(value)), ring);
+}
 
 py::array_t<uint64_t> poly_to_numpy(const Poly& p) {
     const u32 n = p.ring().degree();
@@ -123,6 +152,8 @@ PYBIND11_MODULE(_tetris_b200, m) {
     m.def("ntt_transform", &ntt_transform, py::keep_alive<0, 1>());
     m.def("automorphism_apply", &automorphism_apply, py::keep_alive<0, 1>());
     m.def("rescale_round", &rescale_round, py::keep_alive<0, 1>());
+    m.def("poly_from_i64", &poly_from_i64, py::arg("ring"), py::arg("coeffs"), py::arg("level"),
+          py::arg("nspecial") = 0, py::keep_alive<0, 1>());
     m.def("raise_level", &raise_level, py::arg("p"), py::arg("new_level"), py::arg("nspecial") = 0,
           py::keep_alive<0, 1>());
     m.def("sample_uniform", &sample_uniform, py::keep_alive<0, 1>());
@@ -198,7 +229,7 @@ PYBIND11_MODULE(_tetris_b200, m) {
 
     py::class_<KeyContext>(m, "KeyContext")
         .def(py::init<const RingParams&, NoiseParams, GadgetVector>(), py::keep_alive<1, 2>())
-        .def("keygen", &KeyContext::keygen)
+        .def("keygen", [](const KeyContext& c, Rng& rng) { return tied(c.keygen(rng), c.ring()); })
         .def("relin_key_gen", &KeyContext::relin_key_gen, py::keep_alive<0, 1>())
         .def("galois_key_gen", &KeyContext::galois_key_gen, py::keep_alive<0, 1>())
         .def("switch_key_gen", &KeyContext::switch_key_gen, py::keep_alive<0, 1>())
@@ -231,8 +262,12 @@ PYBIND11_MODULE(_tetris_b200, m) {
                  if (a.ndim() != 2) throw TetrisError("ckks", "encode_slots_many expects a [batch][slots] array");
                  std::vector<std::vector<cplx>> vs(a.shape(0));
                  for (py::ssize_t b = 0; b < a.shape(0); ++b) vs[b].assign(a.data(b, 0), a.data(b, 0) + a.shape(1));
-                 py::gil_scoped_release nogil;
-                 return e.encode_slots_many(vs, scale, level);
+                 std::vector<Poly> out;
+                 {
+                     py::gil_scoped_release nogil;
+                     out = e.encode_slots_many(vs, scale, level);
+                 }
+                 return tied(std::move(out), e.ring());
              })
         .def("decode_slots", &Encoder::decode_slots, py::call_guard<py::gil_scoped_release>())
         .def("encode_coeffs", &Encoder::encode_coeffs)
@@ -250,7 +285,7 @@ PYBIND11_MODULE(_tetris_b200, m) {
 
     // ciphertext batches (extension): part-major stacks evaluated together
     m.def("stack_ciphertexts", &stack_ciphertexts, py::call_guard<py::gil_scoped_release>());
-    m.def("unstack_ciphertext", &unstack_ciphertext);
+    m.def("unstack_ciphertext", [](const Ciphertext& ct) { return tied(unstack_ciphertext(ct), ct.ring()); });
     m.def("slice_ciphertext", &slice_ciphertext, py::arg("ct"), py::arg("first"), py::arg("count"));
 
     py::class_<Evaluator>(m, "Evaluator")
@@ -266,7 +301,15 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("rescale", &Evaluator::rescale, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("rotate", &Evaluator::rotate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("conjugate", &Evaluator::conjugate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
-        .def("apply_galois_many", &Evaluator::apply_galois_many, py::call_guard<py::gil_scoped_release>())
+        .def("apply_galois_many",
+             [](const Evaluator& ev, const Ciphertext& ct, const std::vector<u64>& exps, const EvalKeys& keys) {
+                 std::vector<Ciphertext> out;
+                 {
+                     py::gil_scoped_release nogil;
+                     out = ev.apply_galois_many(ct, exps, keys);
+                 }
+                 return tied(std::move(out), ev.ring());
+             })
         .def_static("scaled_residue", &Evaluator::scaled_residue);
 
     py::class_<LinearTransformPlan>(m, "LinearTransformPlan")
@@ -367,10 +410,25 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("output_level", &BootstrapEvaluator::output_level)
         .def("mod_raise", &BootstrapEvaluator::mod_raise, py::call_guard<py::gil_scoped_release>())
         .def("trace_map", &BootstrapEvaluator::trace_map, py::call_guard<py::gil_scoped_release>())
-        .def("coeffs_to_slots", &BootstrapEvaluator::coeffs_to_slots, py::call_guard<py::gil_scoped_release>())
+        .def("coeffs_to_slots",
+             [](const BootstrapEvaluator& b, const Evaluator& ev, const Ciphertext& ct, const EvalKeys& keys) {
+                 std::pair<Ciphertext, Ciphertext> out;
+                 {
+                     py::gil_scoped_release nogil;
+                     out = b.coeffs_to_slots(ev, ct, keys);
+                 }
+                 return tied(std::move(out), ev.ring());
+             })
         .def("eval_mod", &BootstrapEvaluator::eval_mod, py::call_guard<py::gil_scoped_release>())
         .def("slots_to_coeffs", &BootstrapEvaluator::slots_to_coeffs, py::call_guard<py::gil_scoped_release>())
-        .def("half_bts", &BootstrapEvaluator::half_bts, py::call_guard<py::gil_scoped_release>());
+        .def("half_bts", [](const BootstrapEvaluator& b, const Evaluator& ev, const Ciphertext& ct, const EvalKeys& keys) {
+            std::pair<Ciphertext, Ciphertext> out;
+            {
+                py::gil_scoped_release nogil;
+                out = b.half_bts(ev, ct, keys);
+            }
+            return tied(std::move(out), ev.ring());
+        });
 
     // ---- wire formats (serialize.hpp) ----
     auto to_bytes = [](const std::vector<uint8_t>& v) { return py::bytes(reinterpret_cast<const char*>(v.data()), v.size()); };
@@ -390,6 +448,66 @@ PYBIND11_MODULE(_tetris_b200, m) {
     m.def("serialize_secret_key", [to_bytes](const SecretKey& k) { return to_bytes(serialize_secret_key(k)); });
     m.def("deserialize_secret_key", [from_bytes](const py::bytes& b, const RingParams& r) {
         return deserialize_secret_key(from_bytes(b), r); }, py::keep_alive<0, 2>());
+
+    // ---- PFE, repacking, ring merge/split (pfe.hpp, repack.hpp, rlwe.hpp:684-802) ----
+    auto ct_ptrs = [](const py::list& l) {
+        std::vector<const Ciphertext*> v;
+        for (auto h : l) v.push_back(h.is_none() ? nullptr : &h.cast<const Ciphertext&>());
+        return v;
+    };
+    py::class_<FunctionSpec>(m, "FunctionSpec")
+        .def(py::init<>())
+        .def_readwrite("lo", &FunctionSpec::lo)
+        .def_readwrite("hi", &FunctionSpec::hi)
+        .def_readwrite("table", &FunctionSpec::table)
+        .def_readwrite("out_min", &FunctionSpec::out_min)
+        .def_readwrite("out_max", &FunctionSpec::out_max)
+        .def("max_value", &FunctionSpec::max_value)
+        .def("validate", &FunctionSpec::validate);
+    py::class_<TestVector>(m, "TestVector")
+        .def(py::init<>())
+        .def_readwrite("ct", &TestVector::ct)
+        .def_readwrite("lo", &TestVector::lo)
+        .def_readwrite("hi", &TestVector::hi)
+        .def_readwrite("max_value", &TestVector::max_value);
+    m.def("encode_input", &encode_input);
+    m.def("build_test_vector", &build_test_vector, py::keep_alive<0, 1>());
+    m.def("lookup", [](const TestVector& tv, u32 e) { return tied(lookup(tv, e), tv.ct.ring()); });
+    m.def("eval_scores", [](const std::vector<std::vector<double>>& rows, const std::vector<TestVector>& tvs,
+                            bool trace) {
+        std::vector<std::string> t;
+        auto out = eval_scores(rows, tvs, trace ? &t : nullptr);
+        py::object res = tvs.empty() ? py::object(py::list()) : tied(std::move(out), tvs[0].ct.ring());
+        return py::make_tuple(res, t);
+    }, py::arg("rows"), py::arg("tvs"), py::arg("trace") = false);
+    py::class_<RepackKeySet>(m, "RepackKeySet")
+        .def(py::init<>())
+        .def_readwrite("exponents", &RepackKeySet::exponents)
+        .def_readwrite("keys", &RepackKeySet::keys)
+        .def_readwrite("sk_id", &RepackKeySet::sk_id);
+    m.def("repack_exponents", &repack_exponents);
+    m.def("gen_repack_keys", &gen_repack_keys, py::keep_alive<0, 1>());
+    m.def("repack", [ct_ptrs](const KeyContext& ctx, const py::list& cts, const RepackKeySet& keys) {
+        RepackStats st;
+        auto v = ct_ptrs(cts);
+        Ciphertext out;
+        {
+            py::gil_scoped_release nogil;
+            out = repack(ctx, v, keys, &st);
+        }
+        return py::make_tuple(tied(std::move(out), ctx.ring()), st.automorphisms);
+    });
+    m.def("embed_secret", &embed_secret, py::keep_alive<0, 2>());
+    m.def("merge_embed", [ct_ptrs](const py::list& cts, const RingParams& big) { return merge_embed(ct_ptrs(cts), big); },
+          py::keep_alive<0, 2>());
+    m.def("ring_merge", &ring_merge, py::keep_alive<0, 1>());
+    m.def("ring_merge_many", [ct_ptrs](const KeyContext& ctx, const py::list& cts, const SwitchingKey& swk) {
+        return ring_merge_many(ctx, ct_ptrs(cts), swk);
+    }, py::keep_alive<0, 1>());
+    m.def("ring_split", [](const KeyContext& big_ctx, const RingParams& small, const Ciphertext& ct,
+                           const SwitchingKey& swk, u64 small_sk_id) {
+        return tied(ring_split(big_ctx, small, ct, swk, small_sk_id), small);
+    });
     // ---- kernel timing, end-to-end transfer helpers --------------------------
     m.def("profile_enable", [](const RingParams& r, bool on) { check_tg(tg_profile_enable(r.dev(), on ? 1 : 0)); });
     m.def("profile_read", [](const RingParams& r) {

@@ -115,6 +115,58 @@ __global__ void k_raise_level(DevRing R, Shape S, u64* out, const u64* in) {
     }
 }
 
+// Large-domain PFE (pfe.hpp:73-114): row r of the output is
+// sum_c X^{e[r][c]} * tv_c, a sum of negacyclic rotations of the test
+// vectors (parts back to back, level+1 rows each). Gather form: coefficient j
+// of X^e a is a[(j - e) mod 2N] if that index is < N, else -a[(j + N - e) mod 2N].
+struct PfeTables {
+    u32 ncols;
+    const u64* tv[TG_PFE_MAX_COLS];
+};
+
+__global__ void k_pfe_eval(DevRing R, u64* __restrict__ out, const PfeTables T, const u32* __restrict__ exps,
+                           u32 nrows, u32 rows) {
+    const u64 N = R.N, two_n = 2 * N, per_ct = 2 * u64(rows) * N;
+    const u64 total = per_ct * nrows;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
+        const u64 r = i / per_ct, w = i - r * per_ct;  // w: offset inside the ciphertext
+        const u64 j = w & (N - 1), row_off = w - j;
+        const u32 m = u32((w / N) % rows);
+        const u64 q = R.q[m];
+        u64 acc = 0;
+        for (u32 c = 0; c < T.ncols; ++c) {
+            const u64 e = exps[r * T.ncols + c];
+            const u64 src = (j + two_n - e) % two_n;
+            const u64 v = src < N ? T.tv[c][row_off + src] : neg_mod(T.tv[c][row_off + src - N], q);
+            acc = add_mod(acc, v, q);
+        }
+        out[i] = acc;
+    }
+}
+
+// merge_embed (rlwe.hpp:702-735): small-ring polys interleaved into one big
+// ring poly, out[row][k * stride + i] = in_i[row][k]; absent inputs are zero.
+// ring_split's extract (rlwe.hpp:780-790) is the inverse gather.
+__global__ void k_interleave(u64* __restrict__ out, const u64* const* __restrict__ in, u32 count, u32 stride,
+                             u32 n_small, u64 rows_total) {
+    const u64 N = u64(n_small) * stride, total = rows_total * N;
+    for (u64 x = blockIdx.x * u64(blockDim.x) + threadIdx.x; x < total; x += u64(gridDim.x) * blockDim.x) {
+        const u64 row = x / N, c = x - row * N;
+        const u32 i = u32(c % stride);
+        const u64 k = c / stride;
+        out[x] = (i < count && in[i]) ? in[i][row * n_small + k] : 0;
+    }
+}
+
+__global__ void k_deinterleave(u64* __restrict__ out, const u64* __restrict__ in, u32 parity, u32 stride,
+                               u32 n_small, u64 rows_total) {
+    const u64 total = rows_total * n_small;
+    for (u64 x = blockIdx.x * u64(blockDim.x) + threadIdx.x; x < total; x += u64(gridDim.x) * blockDim.x) {
+        const u64 row = x / n_small, k = x - row * n_small;
+        out[x] = in[row * u64(n_small) * stride + k * stride + parity];
+    }
+}
+
 // automorphism_apply, evaluation form (ring.hpp:428-434): slot gather
 __global__ void k_auto_eval(DevRing R, Shape S, u64* out, const u64* in, u64 g) {
     const u64 two_n = 2 * u64(R.N);
@@ -423,6 +475,43 @@ extern "C" int tg_raise_level(tg_context* ctx, uint64_t* out, const uint64_t* in
     Shape S = shape_of(ctx, new_level, nspecial, npolys);
     PROF(TG_OP_SCALAR, 8.0 * S.words + 8.0 * ctx->ring.N * npolys);
     k_raise_level<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, in);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_pfe_eval(tg_context* ctx, uint64_t* out, const uint64_t* const* tvs, uint32_t ncols,
+                           const uint32_t* exps, uint32_t nrows, int level, void* stream) {
+    if (int rc = check_shape(ctx, level, 0)) return rc;
+    if (ncols == 0 || ncols > TG_PFE_MAX_COLS) return fail(TG_E_ARG, "[pfe] 1..64 scoring functions");
+    if (nrows == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    PfeTables T{};
+    T.ncols = ncols;
+    for (u32 c = 0; c < ncols; ++c) T.tv[c] = tvs[c];
+    const u32 rows = u32(level) + 1;
+    const size_t words = size_t(nrows) * 2 * rows * ctx->ring.N;
+    PROF(TG_OP_AUTOMORPHISM, 8.0 * words + 16.0 * ncols * rows * ctx->ring.N);
+    k_pfe_eval<<<grid_for(words), kThreads, 0, as_stream(stream)>>>(ctx->ring, out, T, exps, nrows, rows);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_interleave(uint64_t* out, const uint64_t* const* in_dev, uint32_t count, uint32_t stride,
+                             uint32_t n_small, uint64_t rows_total, void* stream) {
+    if (!out || !in_dev || stride == 0 || count > stride) return fail(TG_E_ARG, "[rlwe] interleave arguments");
+    const size_t words = size_t(rows_total) * n_small * stride;
+    if (words == 0) return TG_OK;
+    k_interleave<<<grid_for(words), kThreads, 0, as_stream(stream)>>>(out, in_dev, count, stride, n_small, rows_total);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_deinterleave(uint64_t* out, const uint64_t* in, uint32_t parity, uint32_t stride, uint32_t n_small,
+                               uint64_t rows_total, void* stream) {
+    if (!out || !in || parity >= stride) return fail(TG_E_ARG, "[rlwe] deinterleave arguments");
+    const size_t words = size_t(rows_total) * n_small;
+    if (words == 0) return TG_OK;
+    k_deinterleave<<<grid_for(words), kThreads, 0, as_stream(stream)>>>(out, in, parity, stride, n_small, rows_total);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
