@@ -247,7 +247,8 @@ int tg_encode_slots(tg_context* ctx, uint64_t* out, const double* v, uint32_t ba
 
 /* ---- key switching ------------------------------------------------------ */
 /* GadgetPlan (rlwe.hpp:28-206) for this ring: RNS digit groups of group_size
- * primes (base2_bits must be 0: base-2 refinement is not on the device path)
+ * primes (base2_bits > 0: single-prime groups split into balanced signed
+ * base-2^b sub-digits, rlwe.hpp:103-135)
  * and the ModDown constants of mod_down_p (rlwe.hpp:555-579). */
 int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group_size, uint32_t base2_bits);
 void tg_gadget_destroy(tg_gadget* g);

@@ -315,8 +315,9 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
     if (!out || !ctx) return fail(TG_E_ARG, "[rlwe] null argument");
     *out = nullptr;
     if (group_size == 0) return fail(TG_E_ARG, "[rlwe] gadget group size must be positive");
-    if (base2_bits != 0)
-        return fail(TG_E_ARG, "[rlwe] base-2 gadget refinement is not supported on the device path");
+    if (base2_bits != 0 && group_size != 1)
+        return fail(TG_E_ARG, "[rlwe] base2 refinement requires single-prime groups");
+    if (base2_bits > 62) return fail(TG_E_ARG, "[rlwe] base2 digit width out of range");
     if (group_size > u32(kMaxGroup)) return fail(TG_E_ARG, "[rlwe] gadget group size exceeds 16");
     DeviceGuard guard(ctx->device);
     const DevRing& R = ctx->ring;
@@ -327,6 +328,14 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
     g->ctx = ctx;
     g->g.group_size = gs;
     g->g.ngroups = ng;
+    g->g.base2_bits = base2_bits;
+    if (base2_bits) {  // GadgetVector::sub_digits (rlwe.hpp:20-25)
+        for (u32 j = 0; j < nq; ++j) {
+            u32 bits = 0;
+            while ((mod[j] >> bits) != 0) ++bits;
+            g->nsub.push_back((bits + base2_bits - 1) / base2_bits);
+        }
+    }
     std::vector<u64> src(size_t(ng) * gs * gs * 2, 0);
     std::vector<u64> conv(size_t(ng) * gs * gs * nmod * 2, 0);
     for (u32 j = 0; j < ng; ++j) {
@@ -430,8 +439,13 @@ extern "C" void tg_gadget_destroy(tg_gadget* g) {
 }
 
 extern "C" uint32_t tg_gadget_digit_count(const tg_gadget* g, int level) {
-    // group_count(level) = (level + group_size) / group_size (rlwe.hpp:50-52)
-    return g ? (u32(level) + g->g.group_size) / g->g.group_size : 0;
+    if (!g || level < 0) return 0;
+    // group_count(level) = (level + group_size) / group_size (rlwe.hpp:50-61)
+    const u32 groups = (u32(level) + g->g.group_size) / g->g.group_size;
+    if (!g->g.base2_bits) return groups;
+    u32 n = 0;
+    for (u32 j = 0; j < groups && j < g->nsub.size(); ++j) n += g->nsub[j];
+    return n;
 }
 
 extern "C" int tg_pool_reserve(tg_context* ctx, uint64_t bytes) {

@@ -165,6 +165,7 @@ struct GadgetDev {
     u64* conv;  // [ngroups][group_size][group_size][nmod][2]
     u64* md;    // ModDown: [K][2] (P/p_s)^-1 mod p_s; [K][q_count][4] +-(P/p_s) mod q_r; [q_count][2] P^-1 mod q_r
     bool lazy_modup, lazy_moddown;  // lazy sums provably fit a word (checked on the host)
+    u32 base2_bits;                 // 0: RNS digits; else balanced base-2^b sub-digits (group_size 1)
 };
 
 }  // namespace tg
@@ -235,6 +236,7 @@ struct tg_gadget {
     tg_context* ctx = nullptr;
     tg::GadgetDev g{};
     std::vector<tg::u32> group_first, group_count;
+    std::vector<tg::u32> nsub;  // base-2 sub-digits per prime (rlwe.hpp:20-25)
     void* dev_block = nullptr;
 };
 

@@ -95,6 +95,41 @@ k_modup(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict_
     }
 }
 
+// GadgetPlan::decompose with base-2^b refinement (rlwe.hpp:103-135): group j
+// is the single prime q_j; its centered residue splits into nsub balanced
+// signed sub-digits (carry chain, the last sub-digit unbalanced), each written
+// as from_centered(digit, q_r) to every row of its digit poly.
+__global__ void k_decompose_base2(DevRing R, u64* __restrict__ digits, const u64* __restrict__ d, int level,
+                                  u32 src, u32 nsub, u32 b) {
+    const u32 N = R.N, rows = u32(level) + 1 + R.K;
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const u64 q = R.q[src], x = d[size_t(src) * N + t];
+    const long long c = x > q / 2 ? (long long)x - (long long)q : (long long)x;  // to_centered
+    const u64 mag = c < 0 ? u64(-c) : u64(c);
+    const long long sign = c < 0 ? -1 : 1;
+    const u64 half_base = u64(1) << (b - 1), mask = (u64(1) << b) - 1;
+    u64 carry = 0;
+    for (u32 s = 0; s < nsub; ++s) {
+        const u64 u = ((mag >> (s * b)) & mask) + carry;
+        long long dv;
+        if (s + 1 < nsub && u >= half_base) {
+            dv = (long long)u - (long long)(u64(1) << b);
+            carry = 1;
+        } else {
+            dv = (long long)u;
+            carry = 0;
+        }
+        dv *= sign;
+        u64* out = digits + size_t(s) * rows * N + t;
+        for (u32 r = 0; r < rows; ++r) {
+            const u64 qr = R.q[mod_index(r, level, R.q_count)];
+            // |dv| <= 2^b < q_r: from_centered is one conditional add
+            out[size_t(r) * N] = dv < 0 ? qr - u64(-dv) : u64(dv);
+        }
+    }
+}
+
 // acc{0,1}[r][c] = sum_i digit_i[r][c] * key[i][{b,a}][m(r)][c], 128-bit lazy
 // accumulation with a reduction every 15 terms (products < 2^124).
 __global__ void __launch_bounds__(kThreads)
@@ -510,6 +545,19 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
         ProfScope prof(ctx, TG_OP_MODUP,
                        8.0 * R.N * npolys * (double(level + 1) + double(nd) * (level + 1 + R.K)), s);
         const GadgetDev& G = g->g;
+        if (G.base2_bits) {  // sub-digits per prime, no own-group rows to reuse
+            const size_t per_digit = size_t(level + 1 + R.K) * R.N;
+            for (u32 b = 0; b < npolys; ++b) {
+                size_t off = 0;
+                for (u32 j = 0; j <= u32(level); ++j) {
+                    k_decompose_base2<<<(R.N + 127) / 128, 128, 0, s>>>(R, digits + b * dig_words + off * per_digit,
+                                                                       d + b * in_words, level, j, g->nsub[j],
+                                                                       G.base2_bits);
+                    off += g->nsub[j];
+                }
+            }
+            d_eval = nullptr;
+        } else
         for (u32 b = 0; b < npolys; ++b) {
             u64* dg = digits + b * dig_words;
             const u64* src = d + b * in_words;

@@ -101,3 +101,29 @@ def test_ring_merge_and_split_bit_exact(G, R, gpu_available):
         res[T] = (merged, even, odd, back)
     for name, a, b in zip(("merge_many", "split even", "split odd", "merge back"), res[G], res[R]):
         assert_ct_equal(a, b, name)
+
+
+def test_base2_gadget_keyswitch_bit_exact(G, R, gpu_available):
+    """Base-2^b gadget refinement (rlwe.hpp:103-135; the small-ring profile's
+    small_base2 = 30): single-prime groups split into balanced sub-digits."""
+    N = 64
+    primes = list(R.find_ntt_primes(55, 1, 2 * N)) + list(R.find_ntt_primes(54, 2, 2 * N, R.find_ntt_primes(55, 1, 2 * N)))
+    sp = list(R.find_ntt_primes(60, 1, 2 * N, primes))
+    outs = {}
+    for T in (G, R):
+        ring = T.RingParams(N, primes + sp, 1)
+        ctx = T.KeyContext(ring, T.NoiseParams(3.2, 32), T.GadgetVector(1, 30))
+        rng = T.Rng(17)
+        sk, _ = ctx.keygen(rng)
+        keys = T.gen_repack_keys(ctx, sk, rng.split(3))
+        relin = ctx.relin_key_gen(sk, rng.split(4))
+        cts = []
+        for i in range(6):
+            m = T.poly_from_i64(ring, [i * 100 + 7] + [0] * (N - 1), ring.max_level())
+            cts.append(ctx.encrypt(sk, m, 2.0 ** 20, rng.split(100 + i), T.Domain.coeffs))
+        ev = T.Evaluator(ctx)
+        ek = T.EvalKeys()
+        ek.relin = relin
+        outs[T] = (T.repack(ctx, cts, keys)[0], ev.mul_relin(cts[1], cts[2], ek), ctx, ring)
+    for name, a, b in zip(("repack", "mul_relin"), outs[G][:2], outs[R][:2]):
+        assert_ct_equal(a, b, f"base2 {name}")
