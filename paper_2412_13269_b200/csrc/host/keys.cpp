@@ -485,27 +485,33 @@ SwitchingKey KeyContext::galois_key_gen(const SecretKey& sk, u64 exponent, Rng& 
 // apply_galois (rlwe.hpp:637-654)
 Ciphertext KeyContext::apply_galois(const Ciphertext& ct, u64 exponent, const SwitchingKey& swk) const {
     if (ct.degree() != 1) throw TetrisError("rlwe", "apply_galois expects degree-1 input");
-    if (ct.batch != 1) throw TetrisError("rlwe", "apply_galois on a batch is not supported (unstack it)");
+    const u32 B = ct.batch;  // a batch: every ciphertext rotated under the same key
     Ciphertext src = ct;
     src.to_coeff();
     const int lvl = ct.level();
     const u64 g = exponent % (2 * u64(ring_->degree()));
     if (g % 2 == 0) throw TetrisError("ring", "automorphism exponent must be odd");
-    std::vector<Poly> rot = fresh_parts(*ring_, 2, lvl, Form::coeff);
-    if (contiguous(src.parts, 0, 2)) {
+    std::vector<Poly> rot = fresh_parts(*ring_, int(2 * B), lvl, Form::coeff);
+    if (contiguous(src.parts, 0, 2 * B)) {
         check_tg(tg_automorphism(ring_->dev(), const_cast<u64*>(rot[0].data()), src.parts[0].data(), g, TG_FORM_COEFF,
-                                 lvl, 0, 2, ring_->stream()));
+                                 lvl, 0, 2 * B, ring_->stream()));
     } else {
-        for (int i = 0; i < 2; ++i)
+        for (u32 i = 0; i < 2 * B; ++i)
             check_tg(tg_automorphism(ring_->dev(), const_cast<u64*>(rot[i].data()), src.parts[i].data(), g,
                                      TG_FORM_COEFF, lvl, 0, 1, ring_->stream()));
     }
     // (phi(c0) + d0, d1): the add fused into ModDown
     Ciphertext out;
-    std::vector<Poly> dst = fresh_parts(*ring_, 2, lvl, Form::coeff);
-    check_tg(tg_keyswitch_add(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[1].data()),
-                              rot[1].data(), nullptr, key_base(swk), swk.digits(), lvl, rot[0].data(), nullptr,
-                              ring_->stream()));
+    std::vector<Poly> dst = fresh_parts(*ring_, int(2 * B), lvl, Form::coeff);
+    if (B == 1)
+        check_tg(tg_keyswitch_add(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[1].data()),
+                                  rot[1].data(), nullptr, key_base(swk), swk.digits(), lvl, rot[0].data(), nullptr,
+                                  ring_->stream()));
+    else
+        check_tg(tg_keyswitch_add_batch(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[B].data()),
+                                        rot[B].data(), nullptr, key_base(swk), swk.digits(), lvl, rot[0].data(),
+                                        nullptr, B, ring_->stream()));
+    out.batch = B;
     out.parts = std::move(dst);
     out.scale = ct.scale;
     out.domain = ct.domain;

@@ -147,8 +147,10 @@ RepackKeySet gen_repack_keys(const KeyContext& ctx, const SecretKey& sk, Rng& rn
     return set;
 }
 
-Ciphertext repack(const KeyContext& ctx, const std::vector<const Ciphertext*>& cts, const RepackKeySet& keys,
-                  RepackStats* stats) {
+// The reference butterfly one pair at a time (inputs with differing key ids
+// or domains keep the reference's exact per-pair behaviour).
+static Ciphertext repack_serial(const KeyContext& ctx, const std::vector<const Ciphertext*>& cts,
+                                const RepackKeySet& keys, RepackStats* stats) {
     const RingParams& ring = ctx.ring();
     const u32 n = ring.degree();
     if (cts.size() > n) throw TetrisError("repack", "more inputs than ring coefficients");
@@ -214,6 +216,96 @@ Ciphertext repack(const KeyContext& ctx, const std::vector<const Ciphertext*>& c
         }
     }
     return std::move(c[0]);
+}
+
+// The butterfly with every round as ONE ciphertext batch: slots [0, t) and
+// [t, 2t) of the state are combined by batched monomial shifts, adds, subs
+// and a batched automorphism + key switch (one key per round). Absent inputs
+// are exact zero ciphertexts, which every step maps to zero, so the live
+// slots carry the reference's residues; liveness and noise bounds are tracked
+// on the host exactly as the reference's per-pair loop does.
+Ciphertext repack(const KeyContext& ctx, const std::vector<const Ciphertext*>& cts, const RepackKeySet& keys,
+                  RepackStats* stats) {
+    const RingParams& ring = ctx.ring();
+    const u32 n = ring.degree();
+    if (cts.size() > n) throw TetrisError("repack", "more inputs than ring coefficients");
+    const Ciphertext* first = nullptr;
+    for (auto* c : cts)
+        if (c) {
+            first = c;
+            break;
+        }
+    if (!first) throw TetrisError("repack", "all-zero repack batch");
+    const int lvl = first->level();
+    const double scale = first->scale;
+    bool uniform = true;
+    for (auto* c : cts) {
+        if (!c) continue;
+        if (c->level() != lvl) throw TetrisError("repack", "repack inputs at mixed levels");
+        if (c->scale != scale) throw TetrisError("repack", "repack inputs at mixed scales");
+        uniform &= c->degree() == 1 && c->batch == 1 && c->sk_id == first->sk_id && c->domain == first->domain;
+    }
+    if (!uniform || ring.log_degree() == 0) return repack_serial(ctx, cts, keys, stats);
+    std::vector<u64> n_inv(ring.moduli().size());
+    for (std::size_t i = 0; i < n_inv.size(); ++i) n_inv[i] = inv_mod(n, ring.moduli()[i]);
+
+    // state: n slots, part-major, zeros where absent
+    const std::size_t w = std::size_t(lvl + 1) * n;
+    std::vector<Poly> parts = fresh_parts(ring, int(2 * n), lvl, Form::coeff);
+    check_tg(tg_memset0(ring.dev(), const_cast<u64*>(parts[0].data()), 2 * n * w * 8, ring.stream()));
+    std::vector<bool> live(n, false);
+    std::vector<double> noise(n, 0.0);
+    for (std::size_t i = 0; i < cts.size(); ++i) {
+        if (!cts[i]) continue;
+        Ciphertext c = *cts[i];
+        c.to_coeff();
+        for (int part = 0; part < 2; ++part)
+            check_tg(tg_memcpy_d2d(ring.dev(), const_cast<u64*>(parts[part * n + i].data()), c.parts[part].data(),
+                                   w * 8, ring.stream()));
+        live[i] = true;
+        noise[i] = c.noise_bound;
+    }
+    Ciphertext state;
+    state.parts = std::move(parts);
+    state.batch = n;
+    state.scale = scale;
+    state.domain = first->domain;
+    state.sk_id = first->sk_id;
+    {  // x n^-1: the per-round doublings cancel (one launch for all slots)
+        std::vector<Poly> scaled = fresh_parts(ring, int(2 * n), lvl, Form::coeff);
+        check_tg(tg_poly_mul_scalar(ring.dev(), const_cast<u64*>(scaled[0].data()), state.parts[0].data(),
+                                    n_inv.data(), lvl, 0, 2 * n, ring.stream()));
+        state.parts = std::move(scaled);
+    }
+    const double ks_noise = ctx.ks_noise_estimate();
+    for (u32 round = 0; round < ring.log_degree(); ++round) {
+        const u32 t = n >> (round + 1);
+        const u64 g = keys.exponents[round];
+        const SwitchingKey& swk = keys.key(g);
+        for (u32 j = 0; j < t; ++j) {  // the reference's bookkeeping
+            const bool lj = live[j], lh = live[j + t];
+            if (!lj && !lh) continue;
+            const double dn = (lj ? noise[j] : 0.0) + (lh ? noise[j + t] : 0.0);
+            noise[j] = dn + (dn + ks_noise);  // sum + rotated(diff)
+            live[j] = true;
+            if (stats) ++stats->automorphisms;
+        }
+        Ciphertext a = slice_ciphertext(state, 0, t);
+        Ciphertext h = slice_ciphertext(state, t, t);
+        std::vector<Poly> sh = fresh_parts(ring, int(2 * t), lvl, Form::coeff);
+        check_tg(tg_mul_monomial(ring.dev(), const_cast<u64*>(sh[0].data()), h.parts[0].data(), t, lvl, 0, 2 * t,
+                                 ring.stream()));
+        h.parts = std::move(sh);
+        Ciphertext sum = a, diff = a;
+        sum.add_inplace(h);
+        diff.sub_inplace(h);
+        Ciphertext rotated = ctx.apply_galois(diff, g, swk);
+        sum.add_inplace(rotated);
+        state = std::move(sum);
+    }
+    state.batch = 1;  // one slot left
+    state.noise_bound = noise[0];
+    return state;
 }
 
 // ---------------------------------------------------------------------------

@@ -100,10 +100,12 @@ k_modup(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict_
 // signed sub-digits (carry chain, the last sub-digit unbalanced), each written
 // as from_centered(digit, q_r) to every row of its digit poly.
 __global__ void k_decompose_base2(DevRing R, u64* __restrict__ digits, const u64* __restrict__ d, int level,
-                                  u32 src, u32 nsub, u32 b) {
+                                  u32 src, u32 nsub, u32 b, u64 dig_words, u64 in_words) {
     const u32 N = R.N, rows = u32(level) + 1 + R.K;
     const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= N) return;
+    digits += blockIdx.y * dig_words;  // source poly blockIdx.y of the batch
+    d += blockIdx.y * in_words;
     const u64 q = R.q[src], x = d[size_t(src) * N + t];
     const long long c = x > q / 2 ? (long long)x - (long long)q : (long long)x;  // to_centered
     const u64 mag = c < 0 ? u64(-c) : u64(c);
@@ -171,12 +173,17 @@ k_key_inner(DevRing R, u64* __restrict__ acc0, u64* __restrict__ acc1, const u64
 template <int NDMAX>
 __global__ void __launch_bounds__(kThreads)
 k_key_inner_b(DevRing R, u64* __restrict__ acc, const u64* __restrict__ digits, u32 nd, u32 npolys,
-              const u64* __restrict__ key, int level) {
+              const u64* __restrict__ key, int level, u32 polys_per_thread) {
     const u32 N = R.N, K = R.K;
     const u32 rows = u32(level) + 1 + K;
     const u64 words = u64(rows) * N;
     const size_t key_rows = size_t(R.nmod);
-    for (u64 i = blockIdx.x * u64(kThreads) + threadIdx.x; i < words; i += u64(gridDim.x) * kThreads) {
+    // work item = (word, chunk of polys_per_thread sources): small rings with
+    // large batches still fill the GPU
+    const u32 chunks = (npolys + polys_per_thread - 1) / polys_per_thread;
+    for (u64 it = blockIdx.x * u64(kThreads) + threadIdx.x; it < words * chunks; it += u64(gridDim.x) * kThreads) {
+        const u64 i = it % words;
+        const u32 b0 = u32(it / words) * polys_per_thread, b1 = min(npolys, b0 + polys_per_thread);
         const u32 r = u32(i >> R.logN);
         const u32 c = u32(i & (N - 1));
         const u32 m = mod_index(r, level, R.q_count);
@@ -190,7 +197,7 @@ k_key_inner_b(DevRing R, u64* __restrict__ acc, const u64* __restrict__ digits, 
                 ka[k] = base[key_rows * N];
             }
         }
-        for (u32 b = 0; b < npolys; ++b) {
+        for (u32 b = b0; b < b1; ++b) {
             const u64* dig = digits + size_t(b) * nd * words + i;
             U128 s0{0, 0}, s1{0, 0};
 #pragma unroll
@@ -547,14 +554,11 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
         const GadgetDev& G = g->g;
         if (G.base2_bits) {  // sub-digits per prime, no own-group rows to reuse
             const size_t per_digit = size_t(level + 1 + R.K) * R.N;
-            for (u32 b = 0; b < npolys; ++b) {
-                size_t off = 0;
-                for (u32 j = 0; j <= u32(level); ++j) {
-                    k_decompose_base2<<<(R.N + 127) / 128, 128, 0, s>>>(R, digits + b * dig_words + off * per_digit,
-                                                                       d + b * in_words, level, j, g->nsub[j],
-                                                                       G.base2_bits);
-                    off += g->nsub[j];
-                }
+            size_t off = 0;
+            for (u32 j = 0; j <= u32(level); ++j) {  // one launch per prime for the whole batch
+                k_decompose_base2<<<dim3((R.N + 127) / 128, npolys), 128, 0, s>>>(
+                    R, digits + off * per_digit, d, level, j, g->nsub[j], G.base2_bits, dig_words, in_words);
+                off += g->nsub[j];
             }
             d_eval = nullptr;
         } else
@@ -618,10 +622,15 @@ int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd
     {
         // digits once, key once per batch, two accumulators written
         ProfScope prof(ctx, TG_OP_KEY_INNER, 8.0 * words * (npolys * (nd + 2.0) + 2.0 * nd), s);
-        const u32 blocks = grid_for(words);
-        if (nd <= 4) k_key_inner_b<4><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level);
-        else if (nd <= 8) k_key_inner_b<8><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level);
-        else if (nd <= 15) k_key_inner_b<15><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level);
+        // sources per thread: all of them when the words alone fill the GPU
+        // (each key word read once per batch), fewer for small rings
+        const u64 want = u64(ctx->sms) * 2048;
+        u32 ppt = npolys;
+        while (ppt > 1 && words * ((npolys + ppt - 1) / ppt) < want) ppt = (ppt + 1) / 2;
+        const u32 blocks = grid_for(words * ((npolys + ppt - 1) / ppt));
+        if (nd <= 4) k_key_inner_b<4><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
+        else if (nd <= 8) k_key_inner_b<8><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
+        else if (nd <= 15) k_key_inner_b<15><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
         else return fail(TG_E_ARG, "[rlwe] batched key switch supports at most 15 digits");
     }
     TG_LAUNCH_CHECK();
