@@ -286,9 +286,16 @@ k_mod_down(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict_
 template <int GMAX, int CPT>
 __global__ void __launch_bounds__(kMUThreads)
 k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict__ d, int level,
-          const u64* __restrict__ d_eval, u32 rows_per_group) {
+          const u64* __restrict__ d_eval, u32 rows_per_group, u32 nd) {
     const u32 N = R.N, lvl = u32(level), K = R.K;
-    const u32 j = blockIdx.y, gs = G.group_size, first = j * gs;
+    // blockIdx.y = source poly * nd + digit: the whole batch in one launch
+    const u32 j = blockIdx.y % nd, bsrc = blockIdx.y / nd, gs = G.group_size, first = j * gs;
+    {
+        const size_t in_words = size_t(lvl + 1) * N;
+        d += bsrc * in_words;
+        if (d_eval) d_eval += bsrc * in_words;
+        digits += size_t(bsrc) * nd * (lvl + 1 + K) * N;
+    }
     const u32 active = min(gs, lvl + 1 - first);
     const u32 rows_out = lvl + 1 + K, nrest = rows_out - active;
     const u64* src_tb = G.src + ((size_t(j) * gs + (active - 1)) * gs) * 2;
@@ -512,15 +519,15 @@ inline u32 row_groups(u64 threads, u32 rows, int sms) {
 
 template <int GMAX, int CPT>
 void launch_modup_v(const DevRing& R, const GadgetDev& G, int sms, u64* digits, const u64* d, int level, u32 nd,
-                    const u64* d_eval, cudaStream_t s) {
+                    const u64* d_eval, cudaStream_t s, u32 npolys = 1) {
     // worst-case table over the digits (the last digit may be partial)
     const u32 gs = G.group_size, rows_out = u32(level) + 1 + R.K;
     const size_t smem = size_t(rows_out) * gs * 16 + size_t(rows_out) * 16;
     const u32 bx = (R.N / CPT + kMUThreads - 1) / kMUThreads;
-    const u32 groups = row_groups(u64(bx) * nd * kMUThreads, rows_out, sms);
+    const u32 groups = row_groups(u64(bx) * nd * npolys * kMUThreads, rows_out, sms);
     const u32 rpg = (rows_out + groups - 1) / groups;
-    const dim3 grid(bx, nd, (rows_out + rpg - 1) / rpg);
-    k_modup_v<GMAX, CPT><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg);
+    const dim3 grid(bx, nd * npolys, (rows_out + rpg - 1) / rpg);
+    k_modup_v<GMAX, CPT><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg, nd);
 }
 
 template <int KMAX, int CPT>
@@ -562,15 +569,16 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
             }
             d_eval = nullptr;
         } else
-        for (u32 b = 0; b < npolys; ++b) {
-            u64* dg = digits + b * dig_words;
-            const u64* src = d + b * in_words;
-            const u64* ev = d_eval ? d_eval + b * in_words : nullptr;
-            if (G.lazy_modup && G.group_size <= 4) launch_modup_v<4, 2>(R, G, ctx->sms, dg, src, level, nd, ev, s);
-            else if (G.lazy_modup && G.group_size <= 8) launch_modup_v<8, 2>(R, G, ctx->sms, dg, src, level, nd, ev, s);
-            else if (G.lazy_modup && G.group_size <= 16) launch_modup_v<16, 1>(R, G, ctx->sms, dg, src, level, nd, ev, s);
-            else k_modup<<<grid, kMUThreads, 0, s>>>(R, G, dg, src, level, ev);
-        }
+        if (G.lazy_modup && G.group_size <= 4)
+            launch_modup_v<4, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
+        else if (G.lazy_modup && G.group_size <= 8)
+            launch_modup_v<8, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
+        else if (G.lazy_modup && G.group_size <= 16)
+            launch_modup_v<16, 1>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
+        else
+            for (u32 b = 0; b < npolys; ++b)
+                k_modup<<<grid, kMUThreads, 0, s>>>(R, G, digits + b * dig_words, d + b * in_words, level,
+                                                    d_eval ? d_eval + b * in_words : nullptr);
     }
     TG_LAUNCH_CHECK();
     const u32 skip = d_eval ? (g->g.group_size | (npolys > 1 ? nd << 16 : 0u)) : 0u;
