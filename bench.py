@@ -327,6 +327,9 @@ def run_b200(args):
     G.set_default_device(local)
 
     spec = W.CONFIGS[args.config]
+    if args.K or args.group:  # gadget / special-prime experiments
+        import dataclasses
+        spec = dataclasses.replace(spec, K=args.K or spec.K, group=args.group or spec.group)
     t0 = time.time()
     from paper_2412_13269_b200 import distributed as D
     wl = WORKLOADS[args.config](G, W, spec, rank, world, rotations=(rank == 0))
@@ -658,6 +661,8 @@ def main():
                     help="statement workloads: one ciphertext per pipeline instead of ciphertext batches")
     ap.add_argument("--max-blocks", type=int, default=8, help="record blocks per ciphertext batch")
     ap.add_argument("--pool-gb", type=float, default=48.0, help="device memory pool reserved up front (GiB)")
+    ap.add_argument("--K", type=int, default=0, help="override the special-prime count (experiments)")
+    ap.add_argument("--group", type=int, default=0, help="override the gadget group size (experiments)")
     ap.add_argument("--config", type=int, choices=[3, 4, 5], default=4,
                     help="BASELINE.json workload: 4 = full TETRIS statement (default), 3 = threshold count, "
                          "5 = scale-out stress")

@@ -116,6 +116,23 @@ __device__ __forceinline__ u32 tw_slot(u32 u, u32 c, u32 i) {
     else return (1u << u) + pi;
 }
 
+// Cheap twiddle addressing. In layout LAY, lane l / register j of stage p
+// reads group i = k0 >> (p+1) = (H << nj) | (j >> (p+1-LAY)) with
+// H = l >> LAY the lane-high bits; its transposed slot is
+// base_u + H + ((j >> (p+1-LAY)) << HB), HB = LOGM-LAY-LOGE. So one lane base
+// per stage plus a compile-time offset per register: no per-butterfly index
+// arithmetic (tw_slot computes the same slot generically).
+template <int E, bool CHUNK, int LAY>
+__device__ __forceinline__ u32 tw_lane_base(u32 u, u32 c, u32 lane) {
+    constexpr int HB = WGeo<E>::LOGM - LAY - WGeo<E>::LOGE;
+    const u32 H = HB > 0 ? (lane >> LAY) : 0u;
+    return (CHUNK ? 8 * ((1u << u) - 1) + (c << u) : (1u << u)) + H;
+}
+template <int E, int LAY>
+__host__ __device__ constexpr u32 tw_reg_off(int j, int p) {
+    return u32(j >> (p + 1 - LAY)) << (WGeo<E>::LOGM - LAY - WGeo<E>::LOGE);
+}
+
 // Forward (CT) stages on bits HI..LO (descending) of layout LAY; stage s = LOGM-1-p.
 template <int E, bool CHUNK, bool SQ, int LAY, int HI, int LO>
 __device__ __forceinline__ void wfwd(u64 (&v)[E], u32 lane, const u64* sw, const u64* sws, u64 q, u32 c) {
@@ -123,12 +140,11 @@ __device__ __forceinline__ void wfwd(u64 (&v)[E], u32 lane, const u64* sw, const
 #pragma unroll
     for (int p = HI; p >= LO; --p) {
         const int b = p - LAY;
+        const ulonglong2* tb = reinterpret_cast<const ulonglong2*>(sw) + tw_lane_base<E, CHUNK, LAY>(u32(LOGM - 1 - p), c, lane);
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             if (j & (1 << b)) continue;
-            const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
-            const u32 t = tw_slot<E, true, CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
-            const ulonglong2 tw = reinterpret_cast<const ulonglong2*>(sw)[t];
+            const ulonglong2 tw = tb[tw_reg_off<E, LAY>(j, p)];
             ct_bfly<SQ>(v[j], v[j | (1 << b)], tw.x, tw.y, q);
         }
     }
@@ -141,12 +157,11 @@ __device__ __forceinline__ void winv(u64 (&v)[E], u32 lane, const u64* sw, const
 #pragma unroll
     for (int p = LO; p <= HI; ++p) {
         const int b = p - LAY;
+        const ulonglong2* tb = reinterpret_cast<const ulonglong2*>(sw) + tw_lane_base<E, CHUNK, LAY>(u32(LOGM - 1 - p), c, lane);
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             if (j & (1 << b)) continue;
-            const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
-            const u32 t = tw_slot<E, false, CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
-            const ulonglong2 tw = reinterpret_cast<const ulonglong2*>(sw)[t];
+            const ulonglong2 tw = tb[tw_reg_off<E, LAY>(j, p)];
             gs_bfly<SQ>(v[j], v[j | (1 << b)], tw.x, tw.y, q, (2 * q) << p);
         }
     }
@@ -178,12 +193,11 @@ __device__ __forceinline__ void wfwd_fp(double (&v)[NP][E], u32 lane, const u64*
 #pragma unroll
     for (int p = HI; p >= LO; --p) {
         const int b = p - LAY;
+        const double2* tb = reinterpret_cast<const double2*>(sw) + tw_lane_base<E, CHUNK, LAY>(u32(LOGM - 1 - p), c, lane);
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             if (j & (1 << b)) continue;
-            const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
-            const u32 t = tw_slot<E, true, CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
-            const double2 tw = reinterpret_cast<const double2*>(sw)[t];
+            const double2 tw = tb[tw_reg_off<E, LAY>(j, p)];
 #pragma unroll
             for (int n = 0; n < NP; ++n) {
                 const double x = fp_mulmod(v[n][j | (1 << b)], tw.x, tw.y, q);
@@ -205,12 +219,11 @@ __device__ __forceinline__ void winv_fp(double (&v)[NP][E], u32 lane, const u64*
 #pragma unroll
     for (int p = LO; p <= HI; ++p) {
         const int b = p - LAY;
+        const double2* tb = reinterpret_cast<const double2*>(sw) + tw_lane_base<E, CHUNK, LAY>(u32(LOGM - 1 - p), c, lane);
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             if (j & (1 << b)) continue;
-            const u32 k0 = wins<LOGE>(lane, u32(j), u32(LAY));
-            const u32 t = tw_slot<E, false, CHUNK>(u32(LOGM - 1 - p), c, k0 >> (p + 1));
-            const double2 tw = reinterpret_cast<const double2*>(sw)[t];
+            const double2 tw = tb[tw_reg_off<E, LAY>(j, p)];
 #pragma unroll
             for (int n = 0; n < NP; ++n) {
                 const double a = v[n][j], bb = v[n][j | (1 << b)];
@@ -437,6 +450,50 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
     issue_col_tile<E>(tiles, src, p * rpp + r, c0, N);
     stage_col_twiddles<E, true>(sw, sws, w, w + N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (fp) {  // polys in pairs on the block's two tiles: each staged twiddle feeds two interleaved transforms
+        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+        bool first = true;
+        while (p < pend) {
+            const u32 p2 = next_poly(p + 1, pend, r, rpp, level, skip_gs);
+            const bool pair = p2 < pend;
+            if (!first) issue_col_tile<E>(tiles, src, p * rpp + r, c0, N);
+            if (pair) issue_col_tile<E>(tiles + 8 * Gm::CS, src, p2 * rpp + r, c0, N);
+            first = false;
+            cp_async_wait<0>();
+            __syncthreads();
+            u64* col = tiles + warp * Gm::CS;
+            if (pair) {  // canonical u64 in, doubles (|v| <= q/2 + 1, raw bits) out to phase 2
+                double v[2][E];
+#pragma unroll
+                for (int n = 0; n < 2; ++n)
+#pragma unroll
+                    for (int j = 0; j < E; ++j) v[n][j] = u2d(col[n * 8 * Gm::CS + wpad(lane + 32 * j)]);
+                wfwd_all_fp<2, E, false>(v, col, 8 * Gm::CS, lane, sw, qd, qi, 0);
+                __syncwarp();
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                    double* cold = reinterpret_cast<double*>(col + n * 8 * Gm::CS);
+#pragma unroll
+                    for (int j = 0; j < E; ++j) cold[wpad((lane << Gm::LOGE) | j)] = v[n][j];
+                }
+            } else {
+                double v[1][E];
+#pragma unroll
+                for (int j = 0; j < E; ++j) v[0][j] = u2d(col[wpad(lane + 32 * j)]);
+                wfwd_all_fp<1, E, false>(v, col, 0, lane, sw, qd, qi, 0);
+                __syncwarp();
+                double* cold = reinterpret_cast<double*>(col);
+#pragma unroll
+                for (int j = 0; j < E; ++j) cold[wpad((lane << Gm::LOGE) | j)] = v[0][j];
+            }
+            __syncthreads();
+            store_col_tile<E>(tiles, data, p * rpp + r, c0, N);
+            if (pair) store_col_tile<E>(tiles + 8 * Gm::CS, data, p2 * rpp + r, c0, N);
+            __syncthreads();
+            p = pair ? next_poly(p2 + 1, pend, r, rpp, level, skip_gs) : p2;
+        }
+        return;
+    }
     u32 cur = 0;
     while (p < pend) {
         const u32 pn = next_poly(p + 1, pend, r, rpp, level, skip_gs);
@@ -708,6 +765,48 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level) {
     issue_col_tile<E>(tiles, data, p * rpp + r, c0, N);
     stage_col_twiddles<E, false>(sw, sws, w, w + N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (fp) {  // polys in pairs on the block's two tiles (see kw_fwd_cols)
+        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1], nd = R.qd[4 * mi + 2], ndq = R.qd[4 * mi + 3];
+        for (bool first = true; p < pend; first = false) {
+            const bool pair = p + 1 < pend;
+            if (!first) issue_col_tile<E>(tiles, data, p * rpp + r, c0, N);
+            if (pair) issue_col_tile<E>(tiles + 8 * Gm::CS, data, (p + 1) * rpp + r, c0, N);
+            cp_async_wait<0>();
+            __syncthreads();
+            u64* col = tiles + warp * Gm::CS;
+            if (pair) {
+                double v[2][E];
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                    const double* cold = reinterpret_cast<const double*>(col + n * 8 * Gm::CS);
+#pragma unroll
+                    for (int j = 0; j < E; ++j) v[n][j] = cold[wpad((lane << Gm::LOGE) | j)];
+                }
+                winv_all_fp<2, E, false>(v, col, 8 * Gm::CS, lane, sw, qd, qi, 0);
+                __syncwarp();
+#pragma unroll
+                for (int n = 0; n < 2; ++n)
+#pragma unroll
+                    for (int j = 0; j < E; ++j)
+                        col[n * 8 * Gm::CS + wpad(lane + 32 * j)] = fp_canonical(fp_mulmod(v[n][j], nd, ndq, qd), qd);
+            } else {
+                const double* cold = reinterpret_cast<const double*>(col);
+                double v[1][E];
+#pragma unroll
+                for (int j = 0; j < E; ++j) v[0][j] = cold[wpad((lane << Gm::LOGE) | j)];
+                winv_all_fp<1, E, false>(v, col, 0, lane, sw, qd, qi, 0);
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canonical(fp_mulmod(v[0][j], nd, ndq, qd), qd);
+            }
+            __syncthreads();
+            store_col_tile<E>(tiles, data, p * rpp + r, c0, N);
+            if (pair) store_col_tile<E>(tiles + 8 * Gm::CS, data, (p + 1) * rpp + r, c0, N);
+            __syncthreads();
+            p += pair ? 2 : 1;
+        }
+        return;
+    }
     u32 cur = 0;
     for (; p < pend; ++p) {
         if (p + 1 < pend) {
