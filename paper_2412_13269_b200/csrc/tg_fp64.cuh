@@ -1,4 +1,4 @@
-// Exact modular arithmetic on FP64 for moduli q < 2^50.5 (every q-chain
+// Exact modular arithmetic on FP64 for moduli q < 2^50 (every q-chain
 // prime of the configs). B200 has full-rate FP64 (64 DFMA/clk/SM, a pipe
 // separate from the integer IMAD/ALU pipes that bound the 64-bit Shoup path),
 // and residues < 2^52 are exact doubles. All values are integers held in
@@ -11,8 +11,8 @@
 namespace tg {
 
 constexpr double kTwo52 = 4503599627370496.0;        // 2^52
-constexpr double kRoundMagic = 6755399441055744.0;   // 1.5 * 2^52
-constexpr u64 kFpMaxQ = 1591222034138579ull;          // floor(2^50.5): FP path bound
+constexpr double kRoundMagic = 6755399441055744.0;   // M = 1.5 * 2^52
+constexpr u64 kFpMaxQ = u64(1) << 50;                  // FP path for q < 2^50 (bounds below)
 
 // u64 x < 2^52 -> exact double (bit trick: 2^52 + x has x as its mantissa).
 __device__ __forceinline__ double u2d(u64 x) {
@@ -23,15 +23,22 @@ __device__ __forceinline__ u64 d2u(double v) {
     return static_cast<u64>(__double_as_longlong(__dadd_rn(v, kTwo52))) & 0x000FFFFFFFFFFFFFull;
 }
 
-// r == b*w (mod q), |r| <= 1.5q, for integer doubles |b| < 2^53, 0 <= w < q,
-// wq = fl(w/q), q < 2^50.5.
-//   h = fl(b w), l = b w - h exactly (FMA error-free product; |b w| < 2^104).
-//   k = rint(b * wq) via fma(b, wq, 1.5*2^52) - 1.5*2^52 (one rounding of the
-//       exact product to an integer; |b wq| < 2^51 so the sum lies in
-//       [2^52, 2^53) where ulp = 1). |b wq - b w/q| <= |b| 2^-53 <= 1, so
-//       |b w/q - k| <= 1.5 and |b w - k q| <= 1.5 q.
-//   fma(-k, q, h) = h - k q exactly: |h - k q| <= 1.5q + |l| <= 1.5q + 2^51 < 2^53.
-//   (h - k q) + l = b w - k q exactly (|.| <= 1.5q < 2^53).
+// r == b*w (mod q) exactly, for integer doubles b with |b| < 2^53 and
+// b*wq >= -2^51, 0 <= w < q < 2^50, wq = fl(w/q) (|wq - w/q| <= 2^-54).
+//   h = fl(b w) (an integer: |b w| < 2^103), l = b w - h exactly (FMA
+//       error-free product), |l| <= 2^50.
+//   t = fl(b wq + M): one rounding of the exact product-sum. b wq >= -2^51
+//       puts t in [2^52, 2^54), where doubles are integers (ulp 1 or 2), so
+//       k = t - M is an integer (Sterbenz: exact) with
+//       |b wq - k| <= 1/2 (t < 2^53) or <= 1 (t >= 2^53).
+//   |b w/q - k| <= |b| 2^-54 + {1/2 | 1}, so |b w - k q| <= q (1 + 1/2) < 2^52
+//       and fma(-k, q, h) = h - k q is an exact integer (|.| < 2^53),
+//       as is r = (h - k q) + l = b w - k q.
+// Bound: |r| <= q (1/2 + |b| 2^-54) when b wq < 2^51, else q (1 + |b| 2^-54).
+// NTT use (q < 2^50): forward stage blocks start from [0, q) (column phase)
+// or |v| <= q/2 + 1 (chunk phase); three stages keep every multiplier input
+// in [-1.2q, 2.2q] resp. |b| <= 1.6q, i.e. b wq > -2^51, and |v| < 3.4q
+// before the block's fp_reduce. Inverse inputs stay within |b| <= 1.2q.
 __device__ __forceinline__ double fp_mulmod(double b, double w, double wq, double q) {
     const double h = __dmul_rn(b, w);
     const double l = __fma_rn(b, w, -h);

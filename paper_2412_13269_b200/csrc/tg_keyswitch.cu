@@ -300,11 +300,11 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
     const u32 rows_out = lvl + 1 + K, nrest = rows_out - active;
     const u64* src_tb = G.src + ((size_t(j) * gs + (active - 1)) * gs) * 2;
     const u64* conv_tb = G.conv + ((size_t(j) * gs + (active - 1)) * gs) * R.nmod * 2;
-    // FP64 rows: every source q_i and the target q_t below 2^50.5 (the
-    // q-chain): y_i * w mod q_t by fp_mulmod with |term| <= 0.68 q_t (|y_i|
-    // < 2^50.5 makes the quotient estimate error <= 0.18), summed exactly in
-    // doubles (reduced every 8 terms: |sum| <= 5.5 q_t < 2^53). Other rows
-    // (60-bit special primes) take the 64-bit Shoup path.
+    // FP64 rows: every source q_i and the target q_t below 2^50 (the
+    // q-chain): y_i * w mod q_t by fp_mulmod; 0 <= y_i < 2^50 gives
+    // |term| <= q_t (1/2 + 2^-4) (tg_fp64.cuh), summed exactly in doubles
+    // (reduced every 8 terms: |sum| <= 4.5 q_t < 2^53). Other rows (60-bit
+    // special primes) take the 64-bit Shoup path.
     bool src_fp = true;
     for (u32 i = 0; i < active; ++i) src_fp &= R.q[first + i] < kFpMaxQ;
     extern __shared__ ulonglong2 smw[];                                  // [nrest][active] (w, w') | (w, w/q) doubles

@@ -179,11 +179,13 @@ __device__ __forceinline__ void wxchg(T (&v)[E], u64* colw, u32 lane, u32 lo_fro
     for (int j = 0; j < E; ++j) v[j] = col[wpad(wins<LOGE>(lane, u32(j), lo_to))];
 }
 
-// ---- FP64 path (q < 2^50.5; tg_fp64.cuh) ---------------------------------
+// ---- FP64 path (q < 2^50; tg_fp64.cuh) ------------------------------------
 // Staged twiddle pairs are (w, fl(w/q)) doubles. Forward blocks hold at most
-// 3 stages: from |v| <= q each stage adds |t| <= 1.5q, so |v| <= 5.5q < 2^53,
-// then every value is reduced to |v| <= q/2 + 1. Inverse butterflies reduce
-// a+b every stage (|a|,|b| <= 1.5q => |a-b| <= 3q, |a+b| reduced).
+// 3 stages; with the bounds of tg_fp64.cuh every multiplier input stays in
+// [-1.2q, 2.2q] (column phase, inputs [0, q)) or |b| <= 1.6q (chunk phase,
+// inputs |v| <= q/2 + 1) and |v| < 3.4q < 2^53 before the block-final
+// fp_reduce to |v| <= q/2 + 1. Inverse butterflies reduce a+b every stage
+// (|a|,|b| <= 0.6q after the first stage, so |a-b| <= 1.2q).
 // NP independent transforms of the same modulus and position (NP polys) run
 // interleaved: each staged twiddle feeds NP butterflies and the FP64
 // dependency chains of one transform hide behind the other's.
