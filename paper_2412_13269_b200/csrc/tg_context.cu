@@ -127,7 +127,7 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
         return cuda_fail(e, "cudaMemcpy(tables)");
     }
     // FP64 NTT tables: w, fl(w/q), winv, fl(winv/q) per modulus (exact w as a
-    // double when q < 2^50, the only moduli that take the FP64 path) and
+    // double when q < 1.2 * 2^50, the only moduli that take the FP64 path) and
     // q, fl(1/q), n_inv, fl(n_inv/q).
     {
         const size_t nt = size_t(4) * nmod * degree, nq4 = size_t(4) * nmod;

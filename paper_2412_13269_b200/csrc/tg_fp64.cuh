@@ -1,4 +1,4 @@
-// Exact modular arithmetic on FP64 for moduli q < 2^50 (every q-chain
+// Exact modular arithmetic on FP64 for moduli q < 1.2 * 2^50 (every q-chain
 // prime of the configs). B200 has full-rate FP64 (64 DFMA/clk/SM, a pipe
 // separate from the integer IMAD/ALU pipes that bound the 64-bit Shoup path),
 // and residues < 2^52 are exact doubles. All values are integers held in
@@ -12,7 +12,7 @@ namespace tg {
 
 constexpr double kTwo52 = 4503599627370496.0;        // 2^52
 constexpr double kRoundMagic = 6755399441055744.0;   // M = 1.5 * 2^52
-constexpr u64 kFpMaxQ = u64(1) << 50;                  // FP path for q < 2^50 (bounds below)
+constexpr u64 kFpMaxQ = 1351079888211148ull;          // 1.2 * 2^50: FP path bound (see below)
 
 // u64 x < 2^52 -> exact double (bit trick: 2^52 + x has x as its mantissa).
 __device__ __forceinline__ double u2d(u64 x) {
@@ -24,7 +24,7 @@ __device__ __forceinline__ u64 d2u(double v) {
 }
 
 // r == b*w (mod q) exactly, for integer doubles b with |b| < 2^53 and
-// b*wq >= -2^51, 0 <= w < q < 2^50, wq = fl(w/q) (|wq - w/q| <= 2^-54).
+// b*wq >= -2^51, 0 <= w < q < 1.2 * 2^50, wq = fl(w/q) (|wq - w/q| <= 2^-54).
 //   h = fl(b w) (an integer: |b w| < 2^103), l = b w - h exactly (FMA
 //       error-free product), |l| <= 2^50.
 //   t = fl(b wq + M): one rounding of the exact product-sum. b wq >= -2^51
@@ -35,10 +35,12 @@ __device__ __forceinline__ u64 d2u(double v) {
 //       and fma(-k, q, h) = h - k q is an exact integer (|.| < 2^53),
 //       as is r = (h - k q) + l = b w - k q.
 // Bound: |r| <= q (1/2 + |b| 2^-54) when b wq < 2^51, else q (1 + |b| 2^-54).
-// NTT use (q < 2^50): forward stage blocks start from [0, q) (column phase)
-// or |v| <= q/2 + 1 (chunk phase); three stages keep every multiplier input
-// in [-1.2q, 2.2q] resp. |b| <= 1.6q, i.e. b wq > -2^51, and |v| < 3.4q
-// before the block's fp_reduce. Inverse inputs stay within |b| <= 1.2q.
+// NTT use (q < 1.2 * 2^50, so q 2^-54 <= 0.075): forward stage blocks start
+// from [0, q) (column phase) or |v| <= q/2 + 1 (chunk phase); three stages
+// keep every multiplier input in [-1.19q, 2.19q] resp. |b| <= 1.62q, i.e.
+// b wq > -1.95 * 2^50 > -2^51, and |v| <= 3.35q < 2^52 before the block's
+// fp_reduce. Inverse inputs stay within |b| <= 1.2q. The config primes are
+// the 50-bit NTT primes nearest 2^50 (both sides), all below the bound.
 __device__ __forceinline__ double fp_mulmod(double b, double w, double wq, double q) {
     const double h = __dmul_rn(b, w);
     const double l = __fma_rn(b, w, -h);

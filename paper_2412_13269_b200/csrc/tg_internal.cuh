@@ -40,7 +40,7 @@ struct DevRing {
     const u32* slot_of_exp;  // [2N]
     const u64* rs;           // [q_count][q_count][4]: ql mod q_r, ql^-1, shoup, half(ql)
     const u64* one_shoup;    // [nmod]: floor(2^64 / q) (Shoup companion of 1: word -> [0,2q))
-    // FP64 NTT path (q < 2^50): [nmod][4][N] doubles w | w/q | winv | winv/q,
+    // FP64 NTT path (q < 1.2 * 2^50): [nmod][4][N] doubles w | w/q | winv | winv/q,
     // and [nmod][4] doubles q | 1/q | n_inv | n_inv/q (see tg_fp64.cuh)
     const double* twd;
     const double* qd;

@@ -300,10 +300,10 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
     const u32 rows_out = lvl + 1 + K, nrest = rows_out - active;
     const u64* src_tb = G.src + ((size_t(j) * gs + (active - 1)) * gs) * 2;
     const u64* conv_tb = G.conv + ((size_t(j) * gs + (active - 1)) * gs) * R.nmod * 2;
-    // FP64 rows: every source q_i and the target q_t below 2^50 (the
-    // q-chain): y_i * w mod q_t by fp_mulmod; 0 <= y_i < 2^50 gives
-    // |term| <= q_t (1/2 + 2^-4) (tg_fp64.cuh), summed exactly in doubles
-    // (reduced every 8 terms: |sum| <= 4.5 q_t < 2^53). Other rows (60-bit
+    // FP64 rows: every source q_i and the target q_t below 1.2 * 2^50
+    // (the q-chain): y_i * w mod q_t by fp_mulmod; 0 <= y_i < 1.2 * 2^50
+    // gives |term| <= 0.575 q_t (tg_fp64.cuh), summed exactly in doubles
+    // (reduced every 8 terms: |sum| <= 4.6 q_t < 2^53). Other rows (60-bit
     // special primes) take the 64-bit Shoup path.
     bool src_fp = true;
     for (u32 i = 0; i < active; ++i) src_fp &= R.q[first + i] < kFpMaxQ;

@@ -179,7 +179,7 @@ __device__ __forceinline__ void wxchg(T (&v)[E], u64* colw, u32 lane, u32 lo_fro
     for (int j = 0; j < E; ++j) v[j] = col[wpad(wins<LOGE>(lane, u32(j), lo_to))];
 }
 
-// ---- FP64 path (q < 2^50; tg_fp64.cuh) ------------------------------------
+// ---- FP64 path (q < 1.2 * 2^50; tg_fp64.cuh) ------------------------------
 // Staged twiddle pairs are (w, fl(w/q)) doubles. Forward blocks hold at most
 // 3 stages; with the bounds of tg_fp64.cuh every multiplier input stays in
 // [-1.2q, 2.2q] (column phase, inputs [0, q)) or |b| <= 1.6q (chunk phase,

@@ -244,3 +244,65 @@ def test_config1_shape_ops(G, R, gpu_available, N, nq, K, gs, bits, spbits):
     assert_ct_equal(g.ev.mul_relin(a_g, b_g, g.keys), r.ev.mul_relin(a_r, b_r, r.keys), "tensor+relin")
     assert_ct_equal(g.ev.rescale(a_g), r.ev.rescale(a_r), "rescale")
     assert_ct_equal(g.ev.rotate(a_g, 1, g.keys), r.ev.rotate(a_r, 1, r.keys), "rotate 1")
+
+
+def _is_prime(n):
+    if n < 2:
+        return False
+    for p in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        if n % p == 0:
+            return n == p
+    d, s = n - 1, 0
+    while d % 2 == 0:
+        d, s = d // 2, s + 1
+    for a in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):  # deterministic below 3.3e24
+        x = pow(a, d, n)
+        if x in (1, n - 1):
+            continue
+        for _ in range(s - 1):
+            x = x * x % n
+            if x == n - 1:
+                break
+        else:
+            return False
+    return True
+
+
+@pytest.mark.parametrize("N", [1 << 14, 1 << 15, 1 << 16])
+def test_ntt_fp64_extreme_inputs(G, R, gpu_available, N):
+    """The FP64 path at its bounds (q < 1.2 * 2^50): the 50-bit NTT primes
+    nearest 2^50 (one each side) and the largest NTT primes below the bound,
+    with inputs that maximise butterfly growth (all q-1, alternating 0/q-1,
+    impulses, a ramp), forward and inverse, vs the reference NTT."""
+    bound = 1351079888211148
+    near = list(R.find_ntt_primes(50, 2, 2 * N))
+    top, c = [], bound - bound % (2 * N) + 1
+    while len(top) < 2:  # the largest NTT primes below the FP64 bound
+        if c < bound and _is_prime(c):
+            top.append(c)
+        c -= 2 * N
+    primes = near + top
+    rg, rr = G.RingParams(N, primes, 0), R.RingParams(N, primes, 0)
+    pats = []
+    for name in ("max", "alt", "impulse", "ramp"):
+        a = np.zeros((len(primes), N), dtype=np.uint64)
+        for r, q in enumerate(primes):
+            if name == "max":
+                a[r] = q - 1
+            elif name == "alt":
+                a[r, ::2] = q - 1
+            elif name == "impulse":
+                a[r, 0] = q - 1
+                a[r, N // 2] = q - 1
+            else:
+                a[r] = (np.arange(N, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15 % q)) % np.uint64(q)
+        pats.append((name, a))
+    for name, a in pats:
+        lv = len(primes) - 1
+        pg = G.Poly.from_numpy(rg, a, lv, G.Form.coeff)
+        pr = R.Poly.from_numpy(rr, a, lv, R.Form.coeff)
+        fg, fr = G.ntt_transform(pg, G.Form.eval), R.ntt_transform(pr, R.Form.eval)
+        assert_poly_equal(fg, fr, f"fwd {name}")
+        eg = G.Poly.from_numpy(rg, a, lv, G.Form.eval)
+        er = R.Poly.from_numpy(rr, a, lv, R.Form.eval)
+        assert_poly_equal(G.ntt_transform(eg, G.Form.coeff), R.ntt_transform(er, R.Form.coeff), f"inv {name}")
