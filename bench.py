@@ -161,10 +161,21 @@ def reduce_partial_to_root(G, torch, dist, ct, ext_stream, N):
 # Workloads: per-query client ciphertexts (uploaded by the e2e leg), resident
 # server data, and the per-rank partial result before the NCCL reduce.
 # ---------------------------------------------------------------------------
+def decrypted_count(G, S, spec, res, plain):
+    enc = G.Encoder(S.ring, spec.slots)
+    dec = np.array(enc.decode_slots(S.ctx.decrypt(S.sk, res), res.scale))
+    return {"decrypted_count": round(float(dec[0].real), 3), "plaintext_comparator_count": plain,
+            "count_level": res.level()}
+
+
 class ThresholdCount:
     """Config 3: private threshold of every encrypted score block against an
     encrypted threshold (plain norm), summed."""
     metric = "encrypted records/sec per TETRIS threshold-count query (amortized us/record in config)"
+    slot_sum = True
+
+    def check(self, res):
+        return decrypted_count(self.G, self.S, self.spec, res, self.plain_count())
 
     def __init__(self, G, W, spec, rank=0, world=1, rotations=True, device=True):
         from paper_2412_13269_b200 import distributed as D
@@ -220,6 +231,10 @@ class Statement:
     """Configs 4/5: the full TETRIS statement per record block (linear risk
     score, three private thresholds, AND, plaintext flag), summed."""
     metric = "encrypted records/sec per TETRIS query (full statement; amortized us/record in config)"
+    slot_sum = True
+
+    def check(self, res):
+        return decrypted_count(self.G, self.S, self.spec, res, self.plain_count())
 
     def __init__(self, G, W, spec, rank=0, world=1, rotations=True, device=True):
         from paper_2412_13269_b200 import distributed as D
@@ -302,7 +317,63 @@ class Statement:
         return self.W.statement_partial(self.S, q, sel, thr, len(sel))
 
 
-WORKLOADS = {3: ThresholdCount, 4: Statement, 5: Statement}
+class LinearScore:
+    """Config 2: encrypted linear score per record block, sum_j mul_plain(
+    Enc(w_j), pt(attr_j)) + rescale (8 pt x ct MACs); plaintext attributes
+    resident on the server, the 8 weight ciphertexts are the query."""
+    metric = "encrypted records/sec per linear-score query (8 pt x ct MACs + rescale per block)"
+    slot_sum = False
+
+    def __init__(self, G, W, spec, rank=0, world=1, rotations=True, device=True):
+        from paper_2412_13269_b200 import distributed as D
+        self.G, self.W, self.spec = G, W, spec
+        self.batched, self.max_blocks = True, 8
+        self.attrs, self.w = W.linear_score_data(spec)
+        if not device:
+            return
+        self.S = W.make_context(G, spec, relin=False)
+        self.chain = None
+        self.mine = D.shard(spec.n_cts, world, rank)
+        inp = W.config2_inputs(self.S, self.attrs, self.w)
+        self.blocks = [inp.blocks[b] for b in self.mine]
+        self.plain_scale = inp.plain_scale
+        self.client = list(inp.ct_w)
+
+    def partial(self, client, streams, mode):
+        return self.W.run_concurrent(self.G, self.S.ring,
+                                     lambda pts: self.W.linear_score(self.S, client, pts, self.plain_scale),
+                                     self.blocks, streams)
+
+    def check(self, res):
+        n = self.spec.slots
+        err = 0.0
+        enc = self.G.Encoder(self.S.ring, n)
+        for b, ct in zip(self.mine, res):
+            got = np.array(enc.decode_slots(self.S.ctx.decrypt(self.S.sk, ct), ct.scale)).real
+            want = self.attrs[b * n:(b + 1) * n] @ self.w / self.W.ATTR_NORM
+            err = max(err, float(np.max(np.abs(got - want))))
+        return {"max_abs_err_vs_plaintext": err, "tolerance": 2.0 ** -20, "within_tolerance": err < 2.0 ** -20}
+
+    def ref_inputs(self, R, SR, chain_r, host_encode, blocks):
+        from types import SimpleNamespace as NS
+        W, n, L = self.W, self.spec.slots, SR.ring.max_level()
+        ct_w = [host_encode([wj] * n, 400 + j) for j, wj in enumerate(self.w)]
+        out = []
+        for b in blocks:
+            pts, sc = W.encode_plaintexts(SR, [self.attrs[b * n:(b + 1) * n, j] / W.ATTR_NORM for j in range(8)], L)
+            out.append(NS(pts=pts, scale=sc))
+        return ct_w, out
+
+    def ref_step(self, R, SR, chain_r, inp, threads):
+        ct_w, blocks = inp
+        return [self.W.linear_score(SR, ct_w, b.pts, b.scale) for b in blocks]
+
+    def gpu_ladder(self, blocks):
+        return [self.W.linear_score(self.S, self.client, self.blocks[self.mine.index(b)], self.plain_scale)
+                for b in blocks]
+
+
+WORKLOADS = {2: LinearScore, 3: ThresholdCount, 4: Statement, 5: Statement}
 
 
 # ---------------------------------------------------------------------------
@@ -351,6 +422,8 @@ def run_b200(args):
         # record blocks run concurrently (one host thread + CUDA stream each);
         # outputs are summed in block order
         acc = wl.partial(client, streams, mode)
+        if not wl.slot_sum:  # per-block results stay on their rank (no exchange)
+            return acc
         if world > 1:
             if "level" not in out_meta:  # ranks without blocks learn the output level once
                 lv = torch.tensor([acc.level() if acc is not None else -1], device="cuda", dtype=torch.int64)
@@ -432,16 +505,18 @@ def run_b200(args):
     for c, m in zip(wl.client, metas):
         n = m[1] * (m[2] + 1) * spec.N
         G.ciphertext_to_numpy(c, host_buf[m[0]:m[0] + n])
-    out_lvl = res.level() if rank == 0 else 0
-    host_out = G.pinned_empty([2, out_lvl + 1, spec.N])
+    res_list = res if isinstance(res, list) else [res]
+    host_out = [G.pinned_empty([len(c.parts), c.level() + 1, spec.N]) for c in res_list] \
+        if (rank == 0 or not wl.slot_sum) else []
 
     uploader = G.HostUpload(S.ring, host_buf, metas, G.Form.coeff, G.Domain.slots)
 
     def e2e_step():
         ups = uploader.upload()  # every step: pinned host -> HBM, one DMA
         r = query(ups)
-        if rank == 0:
-            G.ciphertext_to_numpy(r, host_out)
+        if host_out:  # the result back on the host every step
+            for c, h in zip(r if isinstance(r, list) else [r], host_out):
+                G.ciphertext_to_numpy(c, h)
         return r
 
     for _ in range(max(2, args.warmup)):
@@ -457,15 +532,12 @@ def run_b200(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
     h2d = int(host_buf.nbytes)
-    d2h = host_out.nbytes if rank == 0 else 0
+    d2h = int(sum(h.nbytes for h in host_out))
 
     # decrypt + check the count (rank 0)
     check = {}
     if rank == 0:
-        enc = G.Encoder(S.ring, spec.slots)
-        dec = np.array(enc.decode_slots(S.ctx.decrypt(S.sk, res), res.scale))
-        check = {"decrypted_count": round(float(dec[0].real), 3), "plaintext_comparator_count": wl.plain_count(),
-                 "count_level": res.level()}
+        check = wl.check(res)
 
     if rank != 0:
         if dist is not None:
@@ -550,12 +622,16 @@ def _ref_setup(G, W, spec, wl, blocks, rotations=False):
     R = _ref_module()
     if R is None:
         raise RuntimeError("oracle/_ref not built")
-    SR = W.make_context(R, spec, rotations=W.inner_sum_rotations(spec.slots) if rotations else [])
+    SR = W.make_context(R, spec, rotations=W.inner_sum_rotations(spec.slots) if rotations else [],
+                        relin=bool(spec.degrees))
     sys.path.insert(0, str(ROOT / "tests"))
     from common import copy_chain
     # the B200 arm's chain when present (bit-identical, saves the host Remez
     # time of degree-63 chains), else the reference's own build_chain
-    chain_r = copy_chain(R, wl.chain) if hasattr(wl, "chain") else W.config3_chain(R, spec)
+    if not spec.degrees:  # no threshold in this workload
+        chain_r = None
+    else:
+        chain_r = copy_chain(R, wl.chain) if getattr(wl, "chain", None) is not None else W.config3_chain(R, spec)
     ringG = G.RingParams(spec.N, SR.primes + SR.sp, spec.K)
     encG = G.Encoder(ringG, spec.slots)
 
@@ -573,28 +649,38 @@ def _ref_setup(G, W, spec, wl, blocks, rotations=False):
     return R, SR, chain_r, wl.ref_inputs(R, SR, chain_r, host_encode, blocks)
 
 
+def ref_threads(wl, nblocks):
+    """Host threads the reference uses: one per threshold job (protocol.hpp:297-311);
+    the linear score is one thread (no threads in the reference's scoring)."""
+    per = 3 if isinstance(wl, Statement) else (1 if isinstance(wl, ThresholdCount) else 0)
+    return max(1, min(nblocks * per, os.cpu_count() or 1)) if per else 1
+
+
 def cpu_baseline(G, W, spec, wl):
     """Bounded sample (~10-30 s of CPU work): the reference on one record
     block (config 3: all blocks, one thread each), compared residue for
     residue with the GPU ladder run of the same block(s)."""
-    blocks = list(range(spec.n_cts)) if isinstance(wl, ThresholdCount) else [0]
+    blocks = [0] if isinstance(wl, Statement) else list(range(spec.n_cts))
     R, SR, chain_r, inp = _ref_setup(G, W, spec, wl, blocks)
-    threads = min(len(blocks) * (3 if isinstance(wl, Statement) else 1), os.cpu_count() or 1)
+    threads = ref_threads(wl, len(blocks))
     t0 = time.perf_counter()
     res = wl.ref_step(R, SR, chain_r, inp, threads)
     secs = time.perf_counter() - t0
     lad = wl.gpu_ladder(blocks)
-    same = all(np.array_equal(a.to_numpy(), b.to_numpy()) for a, b in zip(res.parts, lad.parts)) \
-        and res.scale == lad.scale and res.level() == lad.level()
+    res_l, lad_l = (res, lad) if isinstance(res, list) else ([res], [lad])
+    same = all(all(np.array_equal(a.to_numpy(), b.to_numpy()) for a, b in zip(x.parts, y.parts))
+               and x.scale == y.scale and x.level() == y.level() for x, y in zip(res_l, lad_l))
     recs = len(blocks) * spec.slots
+    what = {ThresholdCount: "threshold", Statement: "statement ops", LinearScore: "linear score"}[type(wl)]
     return {"value": round(recs / secs, 2), "unit": "records/s", "cores": threads, "kind": "reference",
             "sample": f"{len(blocks)} record block(s) x {spec.slots} records through the reference's own "
-                      f"{'threshold' if isinstance(wl, ThresholdCount) else 'statement ops'} on {threads} threads "
-                      f"(unmodified headers, g++ -O2), {secs:.1f} s; slot-sum not in the sample",
+                      f"{what} on {threads} thread(s) (unmodified headers, g++ -O2), {secs:.2f} s"
+                      + ("; slot-sum not in the sample" if wl.slot_sum else ""),
             "seconds": round(secs, 2), "bit_exact_vs_gpu_ladder": bool(same),
-            "note": "reference = its own T_k-ladder polynomial evaluator; the GPU ladder run of the same blocks is "
-                    "compared residue for residue (BSGS parity vs its oracle: tests/test_gpu_bsgs.py, "
-                    "tests/test_gpu_statement.py)"}
+            "note": ("reference = its own T_k-ladder polynomial evaluator; the GPU ladder run of the same blocks is "
+                     "compared residue for residue (BSGS parity vs its oracle: tests/test_gpu_bsgs.py, "
+                     "tests/test_gpu_statement.py)") if spec.degrees else
+                    "the GPU outputs of the same blocks are compared residue for residue"}
 
 
 def run_reference(args):
@@ -612,13 +698,15 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     per_block = 3 if WORKLOADS[args.config] is Statement else 1
     nblk = max(1, min(spec.n_cts, cores // per_block))
+    if WORKLOADS[args.config] is LinearScore:
+        nblk = spec.n_cts  # the whole (small) query
     blocks = list(range(nblk))
     t0 = time.time()
 
     wl = WORKLOADS[args.config](G, W, spec, device=False)
     R, SR, chain, inp = _ref_setup(G, W, spec, wl, blocks)
-    log(f"[reference] setup {time.time() - t0:.1f}s, sample {nblk} blocks on {nblk * per_block} threads")
-    threads = nblk * per_block
+    threads = ref_threads(wl, nblk)
+    log(f"[reference] setup {time.time() - t0:.1f}s, sample {nblk} blocks on {threads} threads")
 
     def step():
         t = time.perf_counter()
@@ -663,7 +751,7 @@ def main():
     ap.add_argument("--pool-gb", type=float, default=48.0, help="device memory pool reserved up front (GiB)")
     ap.add_argument("--K", type=int, default=0, help="override the special-prime count (experiments)")
     ap.add_argument("--group", type=int, default=0, help="override the gadget group size (experiments)")
-    ap.add_argument("--config", type=int, choices=[3, 4, 5], default=4,
+    ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=4,
                     help="BASELINE.json workload: 4 = full TETRIS statement (default), 3 = threshold count, "
                          "5 = scale-out stress")
     args = ap.parse_args()

@@ -78,6 +78,11 @@ public:
     Ciphertext rescale(const Ciphertext& ct) const;
     Ciphertext rotate(const Ciphertext& ct, u32 k, const EvalKeys& keys) const;
     Ciphertext conjugate(const Ciphertext& ct, const EvalKeys& keys) const;
+    // Extension: sum_j mul_plain(cts[j], plains[j], plain_scale) in one
+    // device pass (128-bit lazy accumulation); identical to the reference's
+    // mul_plain / add sequence in j order (config 2's pt x ct MAC).
+    Ciphertext mul_plain_sum(const std::vector<Ciphertext>& cts, const std::vector<Poly>& plains_eval,
+                             double plain_scale) const;
     // Hoisted automorphism batch (ckks.hpp:338-367).
     std::vector<Ciphertext> apply_galois_many(const Ciphertext& ct, const std::vector<u64>& exps,
                                               const EvalKeys& keys) const;

@@ -21,6 +21,42 @@ std::vector<Ciphertext> Evaluator::apply_galois_many(const Ciphertext& ct, const
     return ctx_->apply_galois_hoisted(ct, exps, ks);
 }
 
+Ciphertext Evaluator::mul_plain_sum(const std::vector<Ciphertext>& cts, const std::vector<Poly>& plains_eval,
+                                    double plain_scale) const {
+    if (cts.empty() || cts.size() != plains_eval.size()) throw TetrisError("ckks", "mul_plain_sum: size mismatch");
+    if (cts.size() > TG_PLAIN_SUM_MAX_TERMS) throw TetrisError("ckks", "mul_plain_sum: too many terms");
+    const RingParams& R = ring();
+    std::vector<Ciphertext> ev(cts);
+    const int lvl = ev[0].level();
+    for (const auto& c : ev)
+        if (c.level() != lvl) throw TetrisError("ckks", "mul_plain_sum expects ciphertexts at one level");
+    double noise = 0;
+    std::vector<Poly> keep;
+    std::vector<const u64*> cp, pp;
+    for (std::size_t j = 0; j < ev.size(); ++j) {
+        Ciphertext& c = ev[j];
+        if (c.degree() != 1 || c.batch != 1) throw TetrisError("ckks", "mul_plain_sum expects single degree-1 ciphertexts");
+        if (c.domain != ev[0].domain) throw TetrisError("rlwe", "domain tag mismatch");
+        check_scales_match(c.scale, ev[0].scale);  // add's precondition on the products (same plain_scale)
+        c.to_eval();
+        if (plains_eval[j].level() < lvl || plains_eval[j].nspecial() != 0)
+            throw TetrisError("ckks", "plaintext has fewer rows than the ciphertext");
+        cp.push_back(detail::group_data(c.parts, 0, 2, keep));
+        pp.push_back(plains_eval[j].data());
+        noise += c.noise_bound * plain_scale;
+    }
+    std::vector<Poly> out = fresh_parts(R, 2, lvl, Form::eval);
+    check_tg(tg_mul_plain_sum(R.dev(), const_cast<u64*>(out[0].data()), u32(ev.size()), cp.data(), pp.data(), lvl, 2,
+                              R.stream()));
+    Ciphertext r;
+    r.parts = std::move(out);
+    r.scale = ev[0].scale * plain_scale;
+    r.domain = ev[0].domain;
+    r.sk_id = ev[0].sk_id;
+    r.noise_bound = noise;
+    return r;
+}
+
 LinearTransformPlan::LinearTransformPlan(const Encoder& enc, const std::map<u32, std::vector<cplx>>& diagonals,
                                          double plain_scale, int encode_level)
     : n_(enc.slots()), plain_scale_(plain_scale), encode_level_(encode_level) {

@@ -301,6 +301,8 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("rescale", &Evaluator::rescale, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("rotate", &Evaluator::rotate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("conjugate", &Evaluator::conjugate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("mul_plain_sum", &Evaluator::mul_plain_sum, py::keep_alive<0, 1>(),
+             py::call_guard<py::gil_scoped_release>())
         .def("apply_galois_many",
              [](const Evaluator& ev, const Ciphertext& ct, const std::vector<u64>& exps, const EvalKeys& keys) {
                  std::vector<Ciphertext> out;
