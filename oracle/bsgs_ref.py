@@ -17,7 +17,12 @@ Algorithm (depth = ceil(log2 d) + 1, the same level budget as the ladder):
   p = q * T_n + r by Chebyshev division at the largest giant n <= deg p:
       q = [c_n, 2 c_{n+1}, ..., 2 c_m],  r_i = c_i  (i < n),  r_{n-i} -= c_{n+i};
   blocks of degree < b are the reference's combination step
-      rescale( sum_k mul_scalar(T_k, c_k, q_lvl) + add_scalar(c_0) ).
+      rescale( sum_k mul_scalar(T_k, c_k, s) + add_scalar(c_0) ),
+  with s = q_lvl * target / scale(T_first) so that every block lands on the
+  scale its consumer needs: the output at scale(x) (as the ladder's), and each
+  quotient Q at target * q_lp / scale(T_n) so Q * T_n rescales onto target.
+  Without this the giant-step products drift from Delta by scale(T_n)/q per
+  level and deep chains (config 5, degree 63) fail the 1e-4 scale check.
 """
 from __future__ import annotations
 
@@ -64,20 +69,38 @@ def eval_chebyshev_bsgs(T, ev, x, coeffs, keys):
         cache[k] = res
         return res
 
-    def base(cs):  # degree < b: the reference combination step (ckks.hpp:556-578)
+    def base_terms(cs):
         ks = [k for k in range(1, len(cs)) if cs[k] != 0.0]
         if not ks:
-            ks_use = [1]
-            cvals = {1: 0.0}
-        else:
-            ks_use = ks
-            cvals = {k: cs[k] for k in ks}
+            return [1], {1: 0.0}
+        return ks, {k: cs[k] for k in ks}
+
+    def level_of(cs):  # output level of rec(cs); levels do not depend on scales
+        cs = _trim(cs)
+        if all(v == 0.0 for v in cs):
+            return None
+        m = len(cs) - 1
+        if m < b:
+            ks_use, _ = base_terms(cs)
+            return min([x.level()] + [get(k).level() for k in ks_use]) - 1
+        n, q, r = split(cs)
+        lq, lr = level_of(q), level_of(r)
+        if lq is None:
+            return lr
+        lp = min(lq, get(n).level()) - 1
+        return lp if lr is None else min(lp, lr)
+
+    def base(cs, target):  # degree < b: the reference combination step (ckks.hpp:556-578)
+        ks_use, cvals = base_terms(cs)
         for k in ks_use:
             get(k)
         lvl = x.level()
         for k in ks_use:
             lvl = min(lvl, get(k).level())
-        comb = float(ev.ring().modulus(lvl))
+        # combination scale q_lvl * target / scale(T_first): the rescaled block
+        # lands exactly on `target`, so giant-step products and remainders add
+        # at matching scales however far the prime chain is from Delta
+        comb = float(ev.ring().modulus(lvl)) * (target / get(ks_use[0]).scale)
         acc = None
         for k in ks_use:
             term = get(k).copy()
@@ -93,13 +116,8 @@ def eval_chebyshev_bsgs(T, ev, x, coeffs, keys):
             acc = ev.add_scalar(acc, cs[0])
         return ev.rescale(acc)
 
-    def rec(cs):
-        cs = _trim(cs)
-        if all(v == 0.0 for v in cs):
-            return None
+    def split(cs):  # Chebyshev division at the largest giant n <= deg
         m = len(cs) - 1
-        if m < b:
-            return base(cs)
         n = b
         while 2 * n <= m:
             n *= 2
@@ -107,14 +125,29 @@ def eval_chebyshev_bsgs(T, ev, x, coeffs, keys):
         r = [cs[i] for i in range(n)]
         for i in range(1, m - n + 1):
             r[n - i] = r[n - i] - cs[n + i]
-        Q = rec(q)
-        Rr = rec(r)
+        return n, q, r
+
+    def rec(cs, target):  # the block evaluated at output scale `target`
+        cs = _trim(cs)
+        if all(v == 0.0 for v in cs):
+            return None
+        m = len(cs) - 1
+        if m < b:
+            return base(cs, target)
+        n, q, r = split(cs)
+        lq = level_of(q)
+        Q = None
+        if lq is not None:  # Q * T_n rescaled by q_lp must land on target
+            tn = get(n)
+            lp = min(lq, tn.level())
+            Q = rec(q, target * float(ev.ring().modulus(lp)) / tn.scale)
+        Rr = rec(r, target)
         if Q is None:
             return Rr
         P = ev.rescale(ev.mul_relin(Q, get(n), keys))
         return P if Rr is None else ev.add(P, Rr)
 
-    out = rec(c)
+    out = rec(c, x.scale)
     if out is None:  # identically zero: a fresh encoding of 0 (as d == 0 does)
         return ev.add_scalar(ev.mul_scalar(x, 0.0, 1.0), 0.0)
     return out

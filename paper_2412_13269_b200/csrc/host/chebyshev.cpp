@@ -130,12 +130,15 @@ struct Ladder {
 // The reference combination step (ckks.hpp:556-578) over ladder terms
 // ks (coefficients cs[k]), at the common level min(x.level, T_k.level):
 // rescale( sum_k mul_scalar(T_k, c_k, q_lvl) + add_scalar(c_0) ).
+// target > 0 (BSGS blocks): the combination scale becomes
+// q_lvl * target / scale(T_first), so the rescaled block lands on `target`.
 Ciphertext combine(Ladder& L, const Ciphertext& x, const std::vector<std::size_t>& ks, const std::vector<double>& cs,
-                   double c0) {
+                   double c0, double target = 0.0) {
     const RingParams& R = L.R;
     int lvl = x.level();
     for (std::size_t k : ks) lvl = std::min(lvl, L.get(k).level());
-    const double comb_scale = double(R.modulus(u32(lvl)));
+    double comb_scale = double(R.modulus(u32(lvl)));
+    if (target > 0.0) comb_scale = comb_scale * (target / L.get(ks[0]).scale);
     std::vector<LinTerm> terms;
     std::vector<Ciphertext> conv;  // coefficient-form copies of eval-form terms (T_1 may be eval)
     conv.reserve(ks.size());
@@ -239,41 +242,84 @@ Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const s
     const std::size_t b = std::size_t(1) << lb;
     Ladder L(ev, x, keys);
 
-    auto base = [&](const std::vector<double>& cs) {
+    auto base_terms = [&](const std::vector<double>& cs) {
         std::vector<std::size_t> ks;
         for (std::size_t k = 1; k < cs.size(); ++k)
             if (cs[k] != 0.0) ks.push_back(k);
-        if (ks.empty()) {  // constant block: carried by 0 * T_1
-            std::vector<double> z = {cs[0], 0.0};
-            for (std::size_t k : {std::size_t(1)}) L.get(k);
-            return combine(L, x, {1}, z, cs[0]);
-        }
-        for (std::size_t k : ks) L.get(k);
-        return combine(L, x, ks, cs, cs[0]);
+        return ks;
     };
-
-    std::function<std::optional<Ciphertext>(std::vector<double>)> rec =
-        [&](std::vector<double> cs) -> std::optional<Ciphertext> {
-        cs = trimmed(cs);
-        bool all_zero = true;
-        for (double v : cs) all_zero &= v == 0.0;
-        if (all_zero) return std::nullopt;
+    // Chebyshev division at the largest giant n <= deg: cs = q * T_n + r
+    auto split = [&](const std::vector<double>& cs, std::vector<double>& q, std::vector<double>& r) {
         const std::size_t m = cs.size() - 1;
-        if (m < b) return base(cs);
         std::size_t n = b;
         while (2 * n <= m) n *= 2;
-        std::vector<double> q(m - n + 1), r(cs.begin(), cs.begin() + n);
+        q.assign(m - n + 1, 0.0);
+        r.assign(cs.begin(), cs.begin() + n);
         q[0] = cs[n];
         for (std::size_t i = 1; i <= m - n; ++i) q[i] = 2.0 * cs[n + i];
         for (std::size_t i = 1; i <= m - n; ++i) r[n - i] = r[n - i] - cs[n + i];
-        std::optional<Ciphertext> Q = rec(q);
-        std::optional<Ciphertext> Rr = rec(r);
+        return n;
+    };
+    auto all_zero = [](const std::vector<double>& cs) {
+        for (double v : cs)
+            if (v != 0.0) return false;
+        return true;
+    };
+    // output level of rec(cs) (levels do not depend on scales); -1: zero block
+    std::function<int(std::vector<double>)> level_of = [&](std::vector<double> cs) -> int {
+        cs = trimmed(cs);
+        if (all_zero(cs)) return -1;
+        if (cs.size() - 1 < b) {
+            std::vector<std::size_t> ks = base_terms(cs);
+            if (ks.empty()) ks = {1};
+            int lvl = x.level();
+            for (std::size_t k : ks) lvl = std::min(lvl, L.get(k).level());
+            return lvl - 1;
+        }
+        std::vector<double> q, r;
+        const std::size_t n = split(cs, q, r);
+        const int lq = level_of(q), lr = level_of(r);
+        if (lq < 0) return lr;
+        const int lp = std::min(lq, L.get(n).level()) - 1;
+        return lr < 0 ? lp : std::min(lp, lr);
+    };
+
+    auto base = [&](const std::vector<double>& cs, double target) {
+        std::vector<std::size_t> ks = base_terms(cs);
+        if (ks.empty()) {  // constant block: carried by 0 * T_1
+            std::vector<double> z = {cs[0], 0.0};
+            L.get(1);
+            return combine(L, x, {1}, z, cs[0], target);
+        }
+        for (std::size_t k : ks) L.get(k);
+        return combine(L, x, ks, cs, cs[0], target);
+    };
+
+    // the block evaluated at output scale `target`: blocks land exactly on the
+    // scale their consumer needs (the output on scale(x), like the ladder's;
+    // each quotient on target * q_lp / scale(T_n) so Q * T_n rescales onto
+    // target), so deep chains keep matching scales (oracle/bsgs_ref.py)
+    std::function<std::optional<Ciphertext>(std::vector<double>, double)> rec =
+        [&](std::vector<double> cs, double target) -> std::optional<Ciphertext> {
+        cs = trimmed(cs);
+        if (all_zero(cs)) return std::nullopt;
+        if (cs.size() - 1 < b) return base(cs, target);
+        std::vector<double> q, r;
+        const std::size_t n = split(cs, q, r);
+        const int lq = level_of(q);
+        std::optional<Ciphertext> Q;
+        if (lq >= 0) {
+            const Ciphertext& tn = L.get(n);
+            const int lp = std::min(lq, tn.level());
+            Q = rec(q, target * double(L.R.modulus(u32(lp))) / tn.scale);
+        }
+        std::optional<Ciphertext> Rr = rec(r, target);
         if (!Q) return Rr;
         Ciphertext P = ev.rescale(ev.mul_relin(*Q, L.get(n), keys));
         if (!Rr) return P;
         return ev.add(P, *Rr);
     };
-    std::optional<Ciphertext> out = rec(c);
+    std::optional<Ciphertext> out = rec(c, x.scale);
     if (!out) return ev.add_scalar(ev.mul_scalar(x, 0.0, 1.0), 0.0);
     return *out;
 }
