@@ -8,6 +8,8 @@
 #include <cstring>
 #include <mutex>
 
+#include <cstdlib>
+
 #include "tg_internal.cuh"
 
 namespace tg {
@@ -62,6 +64,7 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
 
     auto* ctx = new tg_context();
     ctx->device = device;
+    if (const char* e = std::getenv("TG_NTT_INT_EVERY")) ctx->ring.int_every = u32(std::strtoul(e, nullptr, 10));
     if (cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || ctx->sms <= 0)
         ctx->sms = 148;
     DevRing& R = ctx->ring;

@@ -382,6 +382,15 @@ __device__ __forceinline__ void stage_col_twiddles(u64* sw, u64* sws, const u64*
     }
 }
 
+// Which rows take the FP64 path: every q < kFpMaxQ row, except that one row
+// in R.int_every (0: none) keeps the 64-bit integer path so the FP64 and the
+// integer pipes work side by side. Both phases of a transform make the same
+// choice (the inter-phase format differs).
+__device__ __forceinline__ bool ntt_use_fp(const DevRing& R, u64 q, u32 r) {
+    if (q >= kFpMaxQ) return false;
+    return R.int_every == 0 || r % R.int_every != R.int_every - 1;
+}
+
 // ---- poly loop ------------------------------------------------------------
 // Grid: x = column / chunk block, y = row r of a poly (modulus), z = group of
 // `ppb` polys. A block transforms row r of each of its polys in turn: the
@@ -446,7 +455,7 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
     const u32 N = R.N;
     const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
-    const bool fp = q < kFpMaxQ;  // FP64 path; the phase-2 kernel makes the same choice
+    const bool fp = ntt_use_fp(R, q, r);  // FP64 path; the other phase makes the same choice
     const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N) : R.tw + size_t(mi) * 4 * N;
     const u32 c0 = blockIdx.x * 8;
     issue_col_tile<E>(tiles, src, p * rpp + r, c0, N);
@@ -613,7 +622,7 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
     const u32 N = R.N;
     const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
-    const bool fp = q < kFpMaxQ;
+    const bool fp = ntt_use_fp(R, q, r);
     const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N) : R.tw + size_t(mi) * 4 * N;
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
@@ -691,7 +700,7 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
     const u32 N = R.N;
     const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
-    const bool fp = q < kFpMaxQ;
+    const bool fp = ntt_use_fp(R, q, r);
     const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N + 2 * size_t(N))
                       : R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -759,7 +768,7 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level) {
     const u32 N = R.N;
     const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
-    const bool fp = q < kFpMaxQ;
+    const bool fp = ntt_use_fp(R, q, r);
     const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N + 2 * size_t(N))
                       : R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
     const u64 ninv = R.ninv[2 * mi], ninv_s = R.ninv[2 * mi + 1];
