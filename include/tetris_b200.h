@@ -142,6 +142,11 @@ int tg_ntt_inverse_oop(tg_context* ctx, uint64_t* out, const uint64_t* in, int l
  * out may alias a or b. For neg, b is ignored. op: 0 add, 1 sub, 2 neg. */
 int tg_poly_addsub(tg_context* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int op,
                    int level, int nspecial, uint32_t npolys, void* stream);
+/* tg_poly_addsub (op 0/1) over level-dropped views: operand poly p starts at
+ * p * stride words (stride >= (level+1+nspecial) * N); out is packed. */
+int tg_poly_addsub_strided(tg_context* ctx, uint64_t* out, const uint64_t* a, uint64_t a_stride,
+                           const uint64_t* b, uint64_t b_stride, int op, int level, int nspecial,
+                           uint32_t npolys, void* stream);
 /* Poly::mul_pointwise_inplace (ring.hpp:278-288): out = a*b mod q (eval form). */
 int tg_poly_mul(tg_context* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int level,
                 int nspecial, uint32_t npolys, void* stream);

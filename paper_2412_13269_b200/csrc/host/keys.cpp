@@ -214,6 +214,15 @@ static void addsub_ct(Ciphertext& x, const Ciphertext& o, int op) {
     const Poly& p0 = x.parts[0];
     const RingParams& ring = p0.ring();
     const int lvl = p0.level(), ns = p0.nspecial();
+    // level-dropped views of one block each (aligned operands): one strided launch
+    const std::size_t sx = uniform_stride(x.parts), so = uniform_stride(o.parts);
+    if (sx && so && op != 2) {
+        std::vector<Poly> dst = fresh_parts(ring, int(np), lvl, p0.form(), ns);
+        check_tg(tg_poly_addsub_strided(ring.dev(), const_cast<u64*>(dst[0].data()), p0.data(), sx,
+                                        o.parts[0].data(), so, op, lvl, ns, u32(np), ring.stream()));
+        x.parts = std::move(dst);
+        return;
+    }
     x.parts = detail::map_parts2(x.parts, o.parts, [&](u64* d, const u64* a, const u64* b, u32 n) {
         check_tg(tg_poly_addsub(ring.dev(), d, a, b, op, lvl, ns, n, ring.stream()));
     });

@@ -37,6 +37,18 @@ __global__ void k_addsub(DevRing R, Shape S, u64* out, const u64* a, const u64* 
     }
 }
 
+// add/sub of level-dropped views: operand poly p starts at p * stride (words),
+// the output is packed.
+__global__ void k_addsub_strided(DevRing R, Shape S, u64* out, const u64* a, u64 sa, const u64* b, u64 sb, int op) {
+    const u64 per = u64(S.rpp) * R.N;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u64 p = i / per, w = i - p * per;
+        const u64 q = R.q[row_mod(R, S, i)];
+        const u64 x = a[p * sa + w], y = b[p * sb + w];
+        out[i] = op == 0 ? add_mod(x, y, q) : sub_mod(x, y, q);
+    }
+}
+
 // Poly::mul_pointwise_inplace (ring.hpp:278-288) and mul_acc_pointwise (:290-304)
 __global__ void k_mul(DevRing R, Shape S, u64* out, const u64* a, const u64* b, int acc) {
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
@@ -512,6 +524,21 @@ extern "C" int tg_deinterleave(uint64_t* out, const uint64_t* in, uint32_t parit
     const size_t words = size_t(rows_total) * n_small;
     if (words == 0) return TG_OK;
     k_deinterleave<<<grid_for(words), kThreads, 0, as_stream(stream)>>>(out, in, parity, stride, n_small, rows_total);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_poly_addsub_strided(tg_context* ctx, uint64_t* out, const uint64_t* a, uint64_t a_stride,
+                                      const uint64_t* b, uint64_t b_stride, int op, int level, int nspecial,
+                                      uint32_t npolys, void* stream) {
+    if (int rc = check_shape(ctx, level, nspecial)) return rc;
+    if (op != 0 && op != 1) return fail(TG_E_ARG, "[ring] strided addsub: op must be add or sub");
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, nspecial, npolys);
+    PROF(TG_OP_ADDSUB, 24 * S.words);
+    k_addsub_strided<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, a, a_stride, b,
+                                                                           b_stride, op);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
