@@ -9,7 +9,10 @@
 // evaluated here in one pass: each input word read once, each output word
 // written once, no intermediate polys. Results are bit-identical to the
 // sequential reference ops (canonical residues of the same integers).
+#include <cstring>
+
 #include "tg_internal.cuh"
+#include "tg_fp64.cuh"
 
 namespace tg {
 namespace {
@@ -31,9 +34,23 @@ struct LinComb {
     u64 add[TG_LINCOMB_MAX_ROWS];
 };
 
-// sum_t c_t * term_t[p][r][c] (+ const) mod q_r, canonical
+// sum_t c_t * term_t[p][r][c] (+ const) mod q_r, canonical. Rows with
+// q < kFpMaxQ (the host stored (c, c/q) as doubles in (c, cs)) use exact
+// FP64 products (tg_fp64.cuh): canonical x < q gives |term| <= 0.575q, eight
+// terms plus the constant stay below 2^53 between reductions.
 __device__ __forceinline__ u64 lc_row(const DevRing& R, const LinComb& L, u32 p, u32 r, u32 c, bool add_here) {
     const u64 q = R.q[r], one = R.one_shoup[r];
+    if (q < kFpMaxQ) {
+        const double qd = R.qd[4 * r], qi = R.qd[4 * r + 1];
+        double acc = add_here ? u2d(L.add[r]) : 0.0;
+        for (u32 t = 0; t < L.nterms; ++t) {
+            const u64 x = L.ptr[t][p * L.pstride[t] + size_t(r) * R.N + c];
+            acc = __dadd_rn(acc, fp_mulmod(u2d(x), __longlong_as_double(static_cast<long long>(L.c[t][r])),
+                                           __longlong_as_double(static_cast<long long>(L.cs[t][r])), qd));
+            if ((t & 7) == 7) acc = fp_reduce(acc, qd, qi);
+        }
+        return fp_canonical(fp_reduce(acc, qd, qi), qd);
+    }
     u64 acc = add_here ? L.add[r] : 0;
     for (u32 t = 0; t < L.nterms; ++t) {
         const u64 x = L.ptr[t][p * L.pstride[t] + size_t(r) * R.N + c];
@@ -105,8 +122,14 @@ extern "C" int tg_lincomb_batch(tg_context* ctx, uint64_t* out, uint32_t nterms,
         for (int r = 0; r <= level; ++r) {
             const u64 q = ctx->h_q[r];
             const u64 v = coeffs[size_t(t) * (level + 1) + r] % q;
-            L.c[t][r] = v;
-            L.cs[t][r] = h_shoup(v, q);
+            if (q < kFpMaxQ) {  // FP64 row: (v, fl(v/q)) as double bits (exact: v < 2^53)
+                const double vd = double(v), vq = vd / double(q);
+                std::memcpy(&L.c[t][r], &vd, 8);
+                std::memcpy(&L.cs[t][r], &vq, 8);
+            } else {
+                L.c[t][r] = v;
+                L.cs[t][r] = h_shoup(v, q);
+            }
         }
     }
     for (int r = 0; r <= level; ++r) L.add[r] = add_per_row ? add_per_row[r] % ctx->h_q[r] : 0;
