@@ -31,6 +31,8 @@ PYMOD = PKG / f"_tetris_b200{EXT}"
 
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(INCLUDE),
                      "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+# tuning experiments only (e.g. TG_NVCC_EXTRA="-DNTT_MIN_BLOCKS=3")
+NVCC_FLAGS += os.environ.get("TG_NVCC_EXTRA", "").split()
 # Host code is compiled like the reference (g++ -O2, no -march): the
 # encoder's FP64 DFT must round exactly as the reference build does.
 CXX_FLAGS = ["-O2", "-fPIC", "-std=c++20", "-pthread", "-I", str(INCLUDE), "-I", str(CUDA_HOME / "include")]
