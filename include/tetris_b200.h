@@ -194,6 +194,11 @@ int tg_raise_level(tg_context* ctx, uint64_t* out, const uint64_t* in, int new_l
  * out (level rows) must not alias in (level+1 rows). */
 int tg_rescale(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, uint32_t npolys,
                void* stream);
+/* rescale_round on eval-form rows (level+1 rows in, level rows out):
+ * == NTT(tg_rescale(iNTT(in))) residue for residue, with one inverse row and
+ * `level` forward rows per poly instead of level+1 and level. */
+int tg_rescale_eval(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, uint32_t npolys,
+                    void* stream);
 
 /* ---- fused residue expressions ------------------------------------------ */
 #define TG_LINCOMB_MAX_TERMS 32
@@ -298,6 +303,14 @@ int tg_keyswitch_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_
 int tg_ks_inner_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* digits, uint32_t ndigits,
                     const uint64_t* key, uint32_t key_digits, int level, const uint64_t* add0,
                     const uint64_t* add1, void* stream);
+/* tg_keyswitch_add_batch with EVAL-form output and eval-form addends: the
+ * accumulators never leave the evaluation domain except their K special rows
+ * (ModDown's conversion is computed in coefficient form and transformed
+ * forward). d is the coefficient form of the sources (d_eval optional).
+ * out_i == NTT(tg_keyswitch_add_batch output with coefficient-form addends). */
+int tg_keyswitch_add_eval(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
+                          const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
+                          const uint64_t* add0, const uint64_t* add1, uint32_t npolys, void* stream);
 int tg_keyswitch_add_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
                            const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
                            const uint64_t* add0, const uint64_t* add1, uint32_t npolys, void* stream);

@@ -71,6 +71,10 @@ public:
     Ciphertext sub(const Ciphertext& a, const Ciphertext& b) const;
     Ciphertext mul(const Ciphertext& a, const Ciphertext& b) const;
     Ciphertext mul_relin(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys) const;
+    // Eval-form pipeline (B200 extensions): outputs stay in evaluation form;
+    // to_coeff() of each equals mul_relin / rescale residue for residue.
+    Ciphertext mul_relin_eval(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys) const;
+    Ciphertext rescale_eval(const Ciphertext& ct) const;
     Ciphertext mul_plain(const Ciphertext& ct, const Poly& plain_eval, double plain_scale) const;
     Ciphertext mul_scalar(const Ciphertext& ct, double c, double scalar_scale) const;
     static u64 scaled_residue(double value, u64 q);
@@ -128,6 +132,11 @@ Ciphertext eval_chebyshev(const Evaluator& ev, const Ciphertext& x, const std::v
 // same algorithm composed of the reference's Evaluator primitives.
 Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
                                const EvalKeys& keys);
+// Chebyshev evaluation keeps intermediate products in evaluation form (default
+// on; TG_EVAL_PIPELINE=0 or set_eval_pipeline(false) selects the coefficient-
+// form pipeline). Results are identical either way.
+void set_eval_pipeline(bool on);
+bool eval_pipeline_enabled();
 // Which Chebyshev evaluator the threshold stages use.
 enum class PolyEval { ladder, bsgs };
 std::vector<double> power_to_chebyshev(const std::vector<double>& pow_coeffs);

@@ -145,6 +145,11 @@ public:
 
     SwitchingKey relin_key_gen(const SecretKey& sk, Rng& rng) const;
     Ciphertext relinearize(const Ciphertext& ct, const SwitchingKey& rlk) const;
+    // relinearize with EVAL-form output (B200 extension): the tensor's
+    // eval-form c0/c1 are the ModDown addends as they are; only c2 and the
+    // accumulators' special rows are inverse transformed. to_coeff() of the
+    // result equals relinearize(ct, rlk) residue for residue.
+    Ciphertext relinearize_eval(const Ciphertext& ct, const SwitchingKey& rlk) const;
     SwitchingKey galois_key_gen(const SecretKey& sk, u64 exponent, Rng& rng) const;
     Ciphertext apply_galois(const Ciphertext& ct, u64 exponent, const SwitchingKey& swk) const;
     // Hoisted automorphisms (Evaluator::apply_galois_many, ckks.hpp:338-367):

@@ -11,8 +11,15 @@
 // (tg_lincomb) after the relinearised product; scales and noise bounds follow
 // the reference's add_inplace / mul_scalar / sub_inplace / add_scalar /
 // rescale sequence exactly.
+// Eval-form pipeline (default; TG_EVAL_PIPELINE=0 selects the coefficient-
+// form one): products, combinations and rescales stay in evaluation form
+// (relinearize_eval / tg_rescale_eval), saving about two transformed rows
+// per row of each product; the result is converted to coefficient form once
+// at the end, residue for residue the same ciphertext.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <optional>
@@ -42,19 +49,32 @@ bool uniform_parts(const std::vector<Poly>& parts) {
     return true;
 }
 
+std::atomic<int> g_eval_pipeline{-1};
+
+bool eval_pipeline() {
+    int v = g_eval_pipeline.load();
+    if (v < 0) {
+        const char* e = std::getenv("TG_EVAL_PIPELINE");
+        v = (e && e[0] == '0') ? 0 : 1;
+        g_eval_pipeline.store(v);
+    }
+    return v != 0;
+}
+
 std::vector<Poly> fused_lincomb(const RingParams& R, const std::vector<LinTerm>& terms,
                                 const std::vector<u64>& add_per_row, int level, bool rescale) {
     const u32 nt = u32(terms.size());
     const u32 B = terms[0].ct->batch;
+    const Form f = terms[0].ct->form();
     std::vector<const u64*> ptrs(nt);
     std::vector<u64> strides(nt);
     std::vector<u64> coeffs(std::size_t(nt) * (level + 1));
     std::vector<Poly> keep;
     for (u32 t = 0; t < nt; ++t) {
         const Ciphertext& c = *terms[t].ct;
-        if (c.batch != B || c.parts.size() != 2 * B || c.form() != Form::coeff || c.level() < level ||
+        if (c.batch != B || c.parts.size() != 2 * B || c.form() != f || c.level() < level ||
             c.parts[0].nspecial() != 0)
-            throw TetrisError("ckks", "fused combination expects degree-1 coefficient-form terms");
+            throw TetrisError("ckks", "fused combination expects degree-1 terms of one form");
         if (uniform_parts(c.parts)) {
             ptrs[t] = c.parts[0].data();
             strides[t] = u64(c.parts[1].data()) / 8 - u64(c.parts[0].data()) / 8;  // words (mod 2^64)
@@ -64,11 +84,17 @@ std::vector<Poly> fused_lincomb(const RingParams& R, const std::vector<LinTerm>&
         }
         for (int r = 0; r <= level; ++r) coeffs[std::size_t(t) * (level + 1) + r] = terms[t].coef[r];
     }
-    std::vector<Poly> out = fresh_parts(R, int(2 * B), rescale ? level - 1 : level, Form::coeff);
+    // eval form: a constant is added at every evaluation point; rescale runs
+    // after the combination (tg_rescale_eval)
+    const bool ev = f == Form::eval, fused_rs = rescale && !ev;
+    std::vector<Poly> out = fresh_parts(R, int(2 * B), fused_rs ? level - 1 : level, f);
     check_tg(tg_lincomb_batch(R.dev(), const_cast<u64*>(out[0].data()), nt, ptrs.data(), strides.data(),
-                              coeffs.data(), add_per_row.empty() ? nullptr : add_per_row.data(), 0, level, 2 * B, B,
-                              rescale ? 1 : 0, R.stream()));
-    return out;
+                              coeffs.data(), add_per_row.empty() ? nullptr : add_per_row.data(), ev ? 1 : 0, level,
+                              2 * B, B, fused_rs ? 1 : 0, R.stream()));
+    if (!rescale || !ev) return out;
+    std::vector<Poly> rs = fresh_parts(R, int(2 * B), level - 1, Form::eval);
+    check_tg(tg_rescale_eval(R.dev(), const_cast<u64*>(rs[0].data()), out[0].data(), level, 2 * B, R.stream()));
+    return rs;
 }
 
 std::vector<u64> residues_of(const RingParams& R, i64 v, int level) {
@@ -83,8 +109,19 @@ struct Ladder {
     const EvalKeys& keys;
     const RingParams& R;
     std::map<std::size_t, Ciphertext> T;
+    const bool eval = eval_pipeline();
     Ladder(const Evaluator& e, const Ciphertext& x, const EvalKeys& k) : ev(e), keys(k), R(e.ring()) {
-        T.emplace(1, x);
+        Ciphertext x1 = x;
+        if (eval) x1.to_eval();
+        T.emplace(1, std::move(x1));
+    }
+    void to_form(Ciphertext& c) const { eval ? c.to_eval() : c.to_coeff(); }
+    // the finished result in the reference's (coefficient) form
+    Ciphertext finish(Ciphertext c) const {
+        if (c.form() == Form::coeff) return c;
+        const Ciphertext src = c;  // shared: transformed out of place, then cached
+        detail::to_coeff_keep_eval(c);
+        return c;
     }
 
     const Ciphertext& get(std::size_t k) {
@@ -93,8 +130,8 @@ struct Ladder {
         const std::size_t a = k / 2, b = k - a;
         const Ciphertext& ta = get(a);
         const Ciphertext& tb = get(b);
-        Ciphertext prod = ev.mul_relin(ta, tb, keys);
-        prod.to_coeff();
+        Ciphertext prod = eval ? ev.mul_relin_eval(ta, tb, keys) : ev.mul_relin(ta, tb, keys);
+        to_form(prod);
         const int lvl = prod.level();
         if (lvl == 0) throw TetrisError("ckks", "cannot rescale at level 0");
         const double two_noise = prod.noise_bound + prod.noise_bound;  // add_inplace(prod)
@@ -107,7 +144,7 @@ struct Ladder {
             res.noise_bound = two_noise / double(ql) + 1.0;
         } else {  // rescale(2 prod - mul_scalar(T_{b-a}, 1, ratio))
             Ciphertext tc0 = get(b - a);
-            tc0.to_coeff();
+            to_form(tc0);
             const double ratio = prod.scale / tc0.scale;
             if (std::abs(1.0) * ratio >= 9.0e18)
                 throw TetrisError("ckks", "scalar multiplier exceeds the integer range");
@@ -140,15 +177,16 @@ Ciphertext combine(Ladder& L, const Ciphertext& x, const std::vector<std::size_t
     double comb_scale = double(R.modulus(u32(lvl)));
     if (target > 0.0) comb_scale = comb_scale * (target / L.get(ks[0]).scale);
     std::vector<LinTerm> terms;
-    std::vector<Ciphertext> conv;  // coefficient-form copies of eval-form terms (T_1 may be eval)
+    std::vector<Ciphertext> conv;  // copies of terms in the ladder's form
     conv.reserve(ks.size());
+    const Form f = L.eval ? Form::eval : Form::coeff;
     double acc_scale = 0, acc_noise = 0;
     bool first = true;
     for (std::size_t k : ks) {
         const Ciphertext* tk = &L.get(k);
-        if (tk->form() != Form::coeff) {
+        if (tk->form() != f) {
             conv.push_back(*tk);
-            conv.back().to_coeff();
+            L.to_form(conv.back());
             tk = &conv.back();
         }
         const double c = cs[k];
@@ -207,6 +245,9 @@ std::vector<double> trimmed(const std::vector<double>& c) {
 
 }  // namespace
 
+void set_eval_pipeline(bool on) { g_eval_pipeline.store(on ? 1 : 0); }
+bool eval_pipeline_enabled() { return eval_pipeline(); }
+
 Ciphertext eval_chebyshev(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
                           const EvalKeys& keys) {
     std::size_t d = cheb_coeffs.size() - 1;
@@ -225,7 +266,7 @@ Ciphertext eval_chebyshev(const Evaluator& ev, const Ciphertext& x, const std::v
             L.get(k);
             ks.push_back(k);
         }
-    return combine(L, x, ks, cheb_coeffs, cheb_coeffs[0]);
+    return L.finish(combine(L, x, ks, cheb_coeffs, cheb_coeffs[0]));
 }
 
 Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
@@ -315,13 +356,25 @@ Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const s
         }
         std::optional<Ciphertext> Rr = rec(r, target);
         if (!Q) return Rr;
-        Ciphertext P = ev.rescale(ev.mul_relin(*Q, L.get(n), keys));
+        if (!L.eval) {
+            Ciphertext P = ev.rescale(ev.mul_relin(*Q, L.get(n), keys));
+            if (!Rr) return P;
+            return ev.add(P, *Rr);
+        }
+        Ciphertext P = ev.rescale_eval(ev.mul_relin_eval(*Q, L.get(n), keys));
         if (!Rr) return P;
-        return ev.add(P, *Rr);
+        // Evaluator::add in eval form: level alignment drops rows in place
+        Ciphertext y = *Rr;
+        Evaluator::check_scales_match(P.scale, y.scale);
+        const int lvl = std::min(P.level(), y.level());
+        P.drop_to_level(lvl);
+        y.drop_to_level(lvl);
+        P.add_inplace(y);
+        return P;
     };
     std::optional<Ciphertext> out = rec(c, x.scale);
     if (!out) return ev.add_scalar(ev.mul_scalar(x, 0.0, 1.0), 0.0);
-    return *out;
+    return L.finish(*out);
 }
 
 }  // namespace tetris_b200

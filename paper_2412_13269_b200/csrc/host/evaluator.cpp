@@ -310,6 +310,10 @@ Ciphertext Evaluator::mul_relin(const Ciphertext& a, const Ciphertext& b, const 
     return ctx_->relinearize(mul(a, b), keys.relin);
 }
 
+Ciphertext Evaluator::mul_relin_eval(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys) const {
+    return ctx_->relinearize_eval(mul(a, b), keys.relin);
+}
+
 Ciphertext Evaluator::mul_plain(const Ciphertext& ct, const Poly& plain_eval, double plain_scale) const {
     Ciphertext out = ct;
     out.to_eval();
@@ -413,6 +417,23 @@ Ciphertext Evaluator::rescale(const Ciphertext& ct) const {
         if (p.nspecial() != 0) throw TetrisError("ring", "rescale with special rows");
     out.parts = detail::map_parts(out.parts, lvl - 1, Form::coeff, [&](u64* d, const u64* s, u32 n) {
         check_tg(tg_rescale(R.dev(), d, s, lvl, n, R.stream()));
+    });
+    out.scale = ct.scale / double(ql);
+    out.noise_bound = ct.noise_bound / double(ql) + 1.0;
+    return out;
+}
+
+Ciphertext Evaluator::rescale_eval(const Ciphertext& ct) const {
+    if (ct.level() == 0) throw TetrisError("ckks", "cannot rescale at level 0");
+    Ciphertext out = ct;
+    out.to_eval();
+    const u64 ql = ring().modulus(u32(ct.level()));
+    const RingParams& R = ring();
+    const int lvl = out.level();
+    for (const auto& p : out.parts)
+        if (p.nspecial() != 0) throw TetrisError("ring", "rescale with special rows");
+    out.parts = detail::map_parts(out.parts, lvl - 1, Form::eval, [&](u64* d, const u64* s, u32 n) {
+        check_tg(tg_rescale_eval(R.dev(), d, s, lvl, n, R.stream()));
     });
     out.scale = ct.scale / double(ql);
     out.noise_bound = ct.noise_bound / double(ql) + 1.0;

@@ -61,6 +61,10 @@ inline const u64* group_data(const std::vector<Poly>& parts, std::size_t first, 
 // fresh contiguous block of shape (out_level, out_form): a single batched
 // launch when the sources are contiguous, one launch per part otherwise.
 // Keeping outputs contiguous keeps every downstream op batched.
+// to_coeff() that leaves the eval-form source in the result's transform
+// cache, so a later to_eval() of the result (the next product) is free.
+void to_coeff_keep_eval(Ciphertext& ct);
+
 template <class F>
 std::vector<Poly> map_parts(const std::vector<Poly>& src, int out_level, Form out_form, F fn) {
     const Poly& p0 = src[0];

@@ -147,7 +147,7 @@ static std::size_t uniform_stride(const std::vector<Poly>& parts) {
 // poly's transform). A shared block's forward transform is memoised on the
 // block, so ladder operands used several times (squares included) are
 // transformed once.
-static void transform_parts(Ciphertext& ct, Form target) {
+static void transform_parts(Ciphertext& ct, Form target, bool keep_eval = false) {
     const Form from = target == Form::eval ? Form::coeff : Form::eval;
     bool any = false;
     for (auto& p : ct.parts) any |= p.form() == from;
@@ -178,6 +178,8 @@ static void transform_parts(Ciphertext& ct, Form target) {
                 check_tg(tg_ntt_inverse_oop(ring.dev(), dst, p0.data(), full_level, ns, u32(np), ring.stream()));
             if (!own && target == Form::eval)
                 p0.storage()->put_eval(p0.offset(), full_level, ns, int(np), ring.stream(), out_blk);
+            if (keep_eval && !own && target == Form::coeff && out_off == 0 && p0.offset() == 0)
+                out_blk->put_eval(0, full_level, ns, int(np), ring.stream(), p0.storage());
         }
         std::vector<Poly> v;
         v.reserve(np);
@@ -190,6 +192,7 @@ static void transform_parts(Ciphertext& ct, Form target) {
 }
 
 void Ciphertext::to_coeff() { transform_parts(*this, Form::coeff); }
+void detail::to_coeff_keep_eval(Ciphertext& ct) { transform_parts(ct, Form::coeff, true); }
 void Ciphertext::to_eval() { transform_parts(*this, Form::eval); }
 
 void Ciphertext::drop_to_level(int new_level) {
@@ -465,6 +468,36 @@ Ciphertext KeyContext::relinearize(const Ciphertext& ct, const SwitchingKey& rlk
     else
         check_tg(tg_keyswitch_add_batch(plan_->dev(), out0, out1, d, c2_eval, key_base(rlk), rlk.digits(), lvl, add0,
                                         add1, B, ring_->stream()));
+    Ciphertext out;
+    out.batch = B;
+    out.parts = std::move(dst);
+    out.scale = ct.scale;
+    out.domain = ct.domain;
+    out.sk_id = ct.sk_id;
+    out.noise_bound = ct.noise_bound + ks_noise_estimate();
+    return out;
+}
+
+Ciphertext KeyContext::relinearize_eval(const Ciphertext& ct, const SwitchingKey& rlk) const {
+    if (ct.degree() != 2) throw TetrisError("rlwe", "relinearize expects a degree-2 ciphertext");
+    if (rlk.to_id != ct.sk_id) throw TetrisError("rlwe", "relinearization key mismatch");
+    const u32 B = ct.batch;
+    Ciphertext src = ct;
+    src.to_eval();
+    const int lvl = ct.level();
+    for (const auto& p : src.parts)
+        if (p.nspecial() != 0) throw TetrisError("rlwe", "decompose expects a ciphertext without special rows");
+    std::vector<Poly> keep;
+    const u64* add0 = detail::group_data(src.parts, 0, B, keep);
+    const u64* add1 = detail::group_data(src.parts, B, B, keep);
+    const u64* c2_eval = detail::group_data(src.parts, 2 * B, B, keep);
+    // c2 alone back to coefficient form (ModUp's source)
+    std::vector<Poly> c2 = fresh_parts(*ring_, int(B), lvl, Form::coeff);
+    check_tg(tg_ntt_inverse_oop(ring_->dev(), const_cast<u64*>(c2[0].data()), c2_eval, lvl, 0, B, ring_->stream()));
+    std::vector<Poly> dst = fresh_parts(*ring_, int(2 * B), lvl, Form::eval);
+    check_tg(tg_keyswitch_add_eval(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[B].data()),
+                                   c2[0].data(), c2_eval, key_base(rlk), rlk.digits(), lvl, add0, add1, B,
+                                   ring_->stream()));
     Ciphertext out;
     out.batch = B;
     out.parts = std::move(dst);

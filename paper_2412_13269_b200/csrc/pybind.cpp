@@ -246,6 +246,7 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("switch_key_apply", &KeyContext::switch_key_apply)
         .def("mod_down_p", &KeyContext::mod_down_p, py::keep_alive<0, 1>())
         .def("relinearize", &KeyContext::relinearize, py::keep_alive<0, 1>())
+        .def("relinearize_eval", &KeyContext::relinearize_eval, py::keep_alive<0, 1>())
         .def("apply_galois", &KeyContext::apply_galois, py::keep_alive<0, 1>())
         .def("square_secret", &KeyContext::square_secret, py::keep_alive<0, 1>());
 
@@ -299,6 +300,10 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("mul_scalar", &Evaluator::mul_scalar, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("add_scalar", &Evaluator::add_scalar, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("rescale", &Evaluator::rescale, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("rescale_eval", &Evaluator::rescale_eval, py::keep_alive<0, 1>(),
+             py::call_guard<py::gil_scoped_release>())
+        .def("mul_relin_eval", &Evaluator::mul_relin_eval, py::keep_alive<0, 1>(),
+             py::call_guard<py::gil_scoped_release>())
         .def("rotate", &Evaluator::rotate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("conjugate", &Evaluator::conjugate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("mul_plain_sum", &Evaluator::mul_plain_sum, py::keep_alive<0, 1>(),
@@ -323,6 +328,8 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("apply", &LinearTransformPlan::apply, py::keep_alive<0, 2>(), py::call_guard<py::gil_scoped_release>());
 
     m.def("eval_chebyshev", &eval_chebyshev, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>());
+    m.def("set_eval_pipeline", &set_eval_pipeline);
+    m.def("eval_pipeline_enabled", &eval_pipeline_enabled);
     m.def("eval_chebyshev_bsgs", &eval_chebyshev_bsgs, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>());
     py::enum_<PolyEval>(m, "PolyEval").value("ladder", PolyEval::ladder).value("bsgs", PolyEval::bsgs);
     m.def("inner_sum", &inner_sum, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>());

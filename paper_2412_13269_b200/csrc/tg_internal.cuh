@@ -245,9 +245,11 @@ namespace tg {
 // Launch helpers implemented in tg_ntt.cu (used by the keyswitch pipeline).
 int ntt_forward_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s);
 int ntt_inverse_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s);
+// Row ranges: rows [row0, row0 + nrows) of every poly (nrows 0: to the end).
 int ntt_forward_oop(tg_context* ctx, u64* dst, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s,
-                    u32 skip_gs = 0);
-int ntt_inverse_oop(tg_context* ctx, u64* dst, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s);
+                    u32 skip_gs = 0, u32 row0 = 0, u32 nrows = 0);
+int ntt_inverse_oop(tg_context* ctx, u64* dst, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s,
+                    u32 row0 = 0, u32 nrows = 0);
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {

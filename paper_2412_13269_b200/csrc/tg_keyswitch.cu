@@ -411,7 +411,9 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
     }
 }
 
-template <int KMAX, int CPT>
+// CONV: the Q rows of `in` are not read (taken as 0): out = -conv * P^-1, the
+// eval-form ModDown's coefficient part (tg_keyswitch_add_eval).
+template <int KMAX, int CPT, bool CONV = false>
 __global__ void __launch_bounds__(256)
 k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict__ in, int level, u32 npolys,
              const u64* __restrict__ addend, u32 rows_per_group) {
@@ -485,7 +487,10 @@ k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restric
             const ulonglong2 pv = sp[r];
             const u64 bias = 2 * u64(K) * q;
             u64 o[CPT], x[CPT], a[CPT];
-            if constexpr (CPT == 2) {
+            if constexpr (CONV) {
+#pragma unroll
+                for (int cc = 0; cc < CPT; ++cc) x[cc] = 0;
+            } else if constexpr (CPT == 2) {
                 const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(src + size_t(r) * N);
                 x[0] = t.x;
                 x[1] = t.y;
@@ -530,7 +535,7 @@ void launch_modup_v(const DevRing& R, const GadgetDev& G, int sms, u64* digits, 
     k_modup_v<GMAX, CPT><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg, nd);
 }
 
-template <int KMAX, int CPT>
+template <int KMAX, int CPT, bool CONV = false>
 void launch_mod_down_v(const DevRing& R, const GadgetDev& G, int sms, u64* out, const u64* in, int level,
                        u32 npolys, const u64* addend, cudaStream_t s) {
     const u32 rout = u32(level) + 1;
@@ -539,8 +544,27 @@ void launch_mod_down_v(const DevRing& R, const GadgetDev& G, int sms, u64* out, 
     const u32 blocks = u32(std::min<u64>((work + 255) / 256, u64(sms) * 8));
     const u32 groups = row_groups(u64(blocks) * 256, rout, sms);
     const u32 rpg = (rout + groups - 1) / groups;
-    k_mod_down_v<KMAX, CPT><<<dim3(blocks, (rout + rpg - 1) / rpg), 256, smem, s>>>(R, G, out, in, level, npolys,
-                                                                                  addend, rpg);
+    k_mod_down_v<KMAX, CPT, CONV><<<dim3(blocks, (rout + rpg - 1) / rpg), 256, smem, s>>>(R, G, out, in, level,
+                                                                                        npolys, addend, rpg);
+}
+
+// Eval-form ModDown epilogue: out_r = acc_r * P^-1 + negconv_r (+ add_r), all
+// eval form; acc holds level+1+K rows per poly (Q rows read), negconv and add
+// level+1 rows per poly. negconv = NTT(-conv * P^-1) from k_mod_down_v<CONV>.
+__global__ void k_mod_down_finish(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict__ acc,
+                                  const u64* __restrict__ negconv, const u64* __restrict__ add, int level,
+                                  u32 npolys) {
+    const u32 N = R.N, K = R.K, nq = R.q_count, rout = u32(level) + 1, rin = rout + K;
+    const u64* pinv = G.md + 2 * K + size_t(K) * nq * 4;  // [nq][2]
+    const u64 per = u64(rout) * N, total = per * npolys;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
+        const u64 p = i / per, w = i - p * per;
+        const u32 r = u32(w >> R.logN);
+        const u64 q = R.q[r];
+        u64 o = add_mod(shoup(acc[p * rin * N + w], pinv[2 * r], pinv[2 * r + 1], q), negconv[i], q);
+        if (add) o = add_mod(o, add[i], q);
+        out[i] = o;
+    }
 }
 
 }  // namespace
@@ -747,5 +771,69 @@ extern "C" int tg_ks_inner_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, con
     TG_CUDA(cudaMallocFromPoolAsync(&acc, 2 * words * 8, ctx->pool, s));
     int rc = ks_inner(g, out0, out1, digits, ndigits, key, level, static_cast<u64*>(acc), s, add0, add1);
     cudaFreeAsync(acc, s);
+    return rc;
+}
+
+// Key switch with the epilogue add, eval-form output (tg_keyswitch_add_eval).
+// Same residues as tg_keyswitch_add_batch followed by a forward NTT of its
+// output: acc stays in eval form; only its K special rows are inverse
+// transformed (out of place), ModDown's conversion -conv * P^-1 is computed in
+// coefficient form and forward transformed (level+1 rows), and the epilogue
+// out = acc * P^-1 + NTT(-conv * P^-1) + add runs on eval-form rows.
+extern "C" int tg_keyswitch_add_eval(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
+                                     const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
+                                     const uint64_t* add0, const uint64_t* add1, uint32_t npolys, void* stream) {
+    if (int rc = check_ks(g, level)) return rc;
+    if (npolys == 0) return TG_OK;
+    tg_context* ctx = g->ctx;
+    const DevRing& R = ctx->ring;
+    const u32 nd = tg_gadget_digit_count(g, level);
+    if (nd > key_digits) return fail(TG_E_ARG, "[rlwe] switching key has too few digits");
+    if (!g->g.lazy_moddown || R.K > 16) return fail(TG_E_ARG, "[rlwe] eval-form ModDown needs the lazy ModDown path");
+    DeviceGuard guard(ctx->device);
+    cudaStream_t s = as_stream(stream);
+    const size_t words = size_t(level + 1 + R.K) * R.N, qwords = size_t(level + 1) * R.N;
+    // digits | acc (2 * npolys polys) | specials scratch (same shape as acc) | negconv (2 * npolys x level+1 rows)
+    void* scratch = nullptr;
+    TG_CUDA(cudaMallocFromPoolAsync(&scratch, (size_t(npolys) * (nd + 4) * words + 2 * npolys * qwords) * 8,
+                                    ctx->pool, s));
+    u64* digits = static_cast<u64*>(scratch);
+    u64* acc = digits + size_t(npolys) * nd * words;
+    u64* spec = acc + 2 * size_t(npolys) * words;
+    u64* negc = spec + 2 * size_t(npolys) * words;
+    int rc = modup(g, digits, d, level, s, d_eval, npolys);
+    if (rc == TG_OK) {
+        ProfScope prof(ctx, TG_OP_KEY_INNER, 8.0 * words * (npolys * (nd + 2.0) + 2.0 * nd), s);
+        const u64 want = u64(ctx->sms) * 2048;
+        u32 ppt = npolys;
+        while (ppt > 1 && words * ((npolys + ppt - 1) / ppt) < want) ppt = (ppt + 1) / 2;
+        const u32 blocks = grid_for(words * ((npolys + ppt - 1) / ppt));
+        if (nd <= 4) k_key_inner_b<4><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
+        else if (nd <= 8) k_key_inner_b<8><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
+        else if (nd <= 15) k_key_inner_b<15><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
+        else rc = fail(TG_E_ARG, "[rlwe] batched key switch supports at most 15 digits");
+        if (rc == TG_OK) rc = cudaGetLastError() == cudaSuccess ? TG_OK : cuda_fail(cudaGetLastError(), "key inner");
+    }
+    // the K special rows of both accumulators back to coefficient form
+    if (rc == TG_OK)
+        rc = ntt_inverse_oop(ctx, spec, acc, level, int(R.K), 2 * npolys, s, u32(level) + 1, R.K);
+    if (rc == TG_OK) {
+        ProfScope prof(ctx, TG_OP_MOD_DOWN, 8.0 * R.N * 2 * npolys * (R.K + (level + 1.0)), s);
+        const GadgetDev& G = g->g;
+        if (R.K <= 4) launch_mod_down_v<4, 2, true>(R, G, ctx->sms, negc, spec, level, 2 * npolys, nullptr, s);
+        else if (R.K <= 8) launch_mod_down_v<8, 2, true>(R, G, ctx->sms, negc, spec, level, 2 * npolys, nullptr, s);
+        else launch_mod_down_v<16, 1, true>(R, G, ctx->sms, negc, spec, level, 2 * npolys, nullptr, s);
+        rc = cudaGetLastError() == cudaSuccess ? TG_OK : cuda_fail(cudaGetLastError(), "mod_down conv");
+    }
+    if (rc == TG_OK) rc = ntt_forward_oop(ctx, negc, negc, level, 0, 2 * npolys, s);
+    if (rc == TG_OK) {
+        ProfScope prof(ctx, TG_OP_MOD_DOWN, 8.0 * qwords * npolys * 2 * 4, s);
+        const size_t n_out = size_t(npolys) * qwords;
+        k_mod_down_finish<<<grid_for(n_out), kThreads, 0, s>>>(R, g->g, out0, acc, negc, add0, level, npolys);
+        k_mod_down_finish<<<grid_for(n_out), kThreads, 0, s>>>(R, g->g, out1, acc + size_t(npolys) * words,
+                                                                negc + size_t(npolys) * qwords, add1, level, npolys);
+        rc = cudaGetLastError() == cudaSuccess ? TG_OK : cuda_fail(cudaGetLastError(), "mod_down finish");
+    }
+    cudaFreeAsync(scratch, s);
     return rc;
 }

@@ -206,18 +206,29 @@ int ntt_inverse_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 np
 }
 
 int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s,
-                    u32 skip_gs) {
+                    u32 skip_gs, u32 row0, u32 nrows) {
     const DevRing& R = ctx->ring;
     const Plan p = make_plan(R.logN);
     const u32 rpp = u32(level + 1 + nspecial);
+    if (nrows == 0) nrows = rpp - row0;
     const u32 total = rpp * npolys;
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
-    ProfScope prof(ctx, TG_OP_NTT_FWD, 16.0 * total * R.N, s);
+    ProfScope prof(ctx, TG_OP_NTT_FWD, 16.0 * nrows * npolys * R.N, s);
     int e1 = 0, e2 = 0;
     if (warp_plan(R.logN, e1, e2) && npolys <= 65535) {
-        if (e1 == 8) launch_fwd_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs);
-        else if (e2 == 8) launch_fwd_w<4, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs);
-        else launch_fwd_w<4, 4>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs);
+        if (e1 == 8) launch_fwd_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows);
+        else if (e2 == 8) launch_fwd_w<4, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows);
+        else launch_fwd_w<4, 4>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows);
+        TG_LAUNCH_CHECK();
+        return TG_OK;
+    }
+    if (row0 != 0 || nrows != rpp) {  // generic path: one launch pair per poly's row range
+        for (u32 q = 0; q < npolys; ++q) {
+            const u32 base = q * rpp + row0;
+            dim3 g1((R.N >> p.logN1) >> p.logC, nrows), g2((1u << p.logN1) >> p.logCpb, nrows);
+            k_fwd_cols<<<g1, kThreads, sm1, s>>>(R, data, src, base, rpp, level, p.logN1, p.logC, skip_gs);
+            k_fwd_chunks<<<g2, kThreads, sm2, s>>>(R, data, base, rpp, level, p.logN1, p.logCpb, skip_gs);
+        }
         TG_LAUNCH_CHECK();
         return TG_OK;
     }
@@ -231,18 +242,30 @@ int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     return TG_OK;
 }
 
-int ntt_inverse_oop(tg_context* ctx, u64* data, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s) {
+int ntt_inverse_oop(tg_context* ctx, u64* data, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s,
+                    u32 row0, u32 nrows) {
     const DevRing& R = ctx->ring;
     const Plan p = make_plan(R.logN);
     const u32 rpp = u32(level + 1 + nspecial);
+    if (nrows == 0) nrows = rpp - row0;
     const u32 total = rpp * npolys;
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
-    ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * total * R.N, s);
+    ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * nrows * npolys * R.N, s);
     int e1 = 0, e2 = 0;
     if (warp_plan(R.logN, e1, e2) && npolys <= 65535) {
-        if (e1 == 8) launch_inv_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s);
-        else if (e2 == 8) launch_inv_w<4, 8>(R, ctx->sms, data, src, rpp, npolys, level, s);
-        else launch_inv_w<4, 4>(R, ctx->sms, data, src, rpp, npolys, level, s);
+        if (e1 == 8) launch_inv_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, row0, nrows);
+        else if (e2 == 8) launch_inv_w<4, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, row0, nrows);
+        else launch_inv_w<4, 4>(R, ctx->sms, data, src, rpp, npolys, level, s, row0, nrows);
+        TG_LAUNCH_CHECK();
+        return TG_OK;
+    }
+    if (row0 != 0 || nrows != rpp) {
+        for (u32 q = 0; q < npolys; ++q) {
+            const u32 base = q * rpp + row0;
+            dim3 g1((R.N >> p.logN1) >> p.logC, nrows), g2((1u << p.logN1) >> p.logCpb, nrows);
+            k_inv_chunks<<<g2, kThreads, sm2, s>>>(R, data, src, base, rpp, level, p.logN1, p.logCpb);
+            k_inv_cols<<<g1, kThreads, sm1, s>>>(R, data, base, rpp, level, p.logN1, p.logC);
+        }
         TG_LAUNCH_CHECK();
         return TG_OK;
     }

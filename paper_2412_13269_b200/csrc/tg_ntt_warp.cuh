@@ -443,9 +443,11 @@ __device__ __forceinline__ void store_col_tile(const u64* tile, u64* dst, u32 ro
 // Phase 1 forward: 8 columns x M1 rows, stages 0 .. log M1 - 1.
 template <int E>
 __global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
-kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, int level, u32 skip_gs) {
+kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, int level, u32 skip_gs,
+            u32 row0) {
     using Gm = WGeo<E>;
-    const u32 r = blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
+    // row r of every poly (rows [row0, row0 + gridDim.y) are transformed)
+    const u32 r = row0 + blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
     u32 p = next_poly(blockIdx.z * ppb, pend, r, rpp, level, skip_gs);
     if (p >= pend) return;
     extern __shared__ u64 dyn[];
@@ -610,9 +612,11 @@ __device__ __forceinline__ void chunk_inv_fp(u64 (&v)[NP][E], u64* col, u32 cs, 
 // integer rows one at a time with the next poly prefetched.
 template <int E>
 __global__ void __launch_bounds__(256, NTT_CHUNK_MIN_BLOCKS)
-kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 logN1, u32 skip_gs) {
+kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 logN1, u32 skip_gs,
+              u32 row0) {
     using Gm = WGeo<E>;
-    const u32 r = blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
+    // row r of every poly (rows [row0, row0 + gridDim.y) are transformed)
+    const u32 r = row0 + blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
     u32 p = next_poly(blockIdx.z * ppb, pend, r, rpp, level, skip_gs);
     if (p >= pend) return;
     extern __shared__ u64 dyn[];
@@ -688,9 +692,11 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
 // Phase A inverse: one warp per contiguous chunk (stages t = 1 .. M2/2).
 template <int E>
 __global__ void __launch_bounds__(256, NTT_CHUNK_MIN_BLOCKS)
-kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, int level, u32 logN1) {
+kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, int level, u32 logN1,
+              u32 row0) {
     using Gm = WGeo<E>;
-    const u32 r = blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
+    // row r of every poly (rows [row0, row0 + gridDim.y) are transformed)
+    const u32 r = row0 + blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
     u32 p = blockIdx.z * ppb;
     if (p >= pend) return;
     extern __shared__ u64 dyn[];
@@ -756,9 +762,10 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
 // Phase B inverse: 8 columns x M1 rows, then the N^-1 scaling.
 template <int E>
 __global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
-kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level) {
+kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 row0) {
     using Gm = WGeo<E>;
-    const u32 r = blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
+    // row r of every poly (rows [row0, row0 + gridDim.y) are transformed)
+    const u32 r = row0 + blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
     u32 p = blockIdx.z * ppb;
     if (p >= pend) return;
     extern __shared__ u64 dyn[];
@@ -889,24 +896,24 @@ inline u32 polys_per_block(u32 blocks_per_row, u32 rpp, u32 npolys, int sms) {
 
 template <int E1, int E2>
 void launch_fwd_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp, u32 npolys, int level,
-                  cudaStream_t s, u32 skip_gs) {
+                  cudaStream_t s, u32 skip_gs, u32 row0, u32 nrows) {
     set_smem_attrs<E1, E2>();
     const u32 M1 = 32 * E1, M2 = 32 * E2;
-    const u32 p1 = polys_per_block(M2 / 8, rpp, npolys, sms), p2 = polys_per_block(M1 / 8, rpp, npolys, sms);
-    kw_fwd_cols<E1><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, src, rpp, npolys,
-                                                                                         p1, level, skip_gs);
-    kw_fwd_chunks<E2><<<dim3(M1 / 8, rpp, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
-        R, data, rpp, npolys, p2, level, WGeo<E1>::LOGM, skip_gs);
+    const u32 p1 = polys_per_block(M2 / 8, nrows, npolys, sms), p2 = polys_per_block(M1 / 8, nrows, npolys, sms);
+    kw_fwd_cols<E1><<<dim3(M2 / 8, nrows, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(
+        R, data, src, rpp, npolys, p1, level, skip_gs, row0);
+    kw_fwd_chunks<E2><<<dim3(M1 / 8, nrows, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
+        R, data, rpp, npolys, p2, level, WGeo<E1>::LOGM, skip_gs, row0);
 }
 
 template <int E1, int E2>
 void launch_inv_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp, u32 npolys, int level,
-                  cudaStream_t s) {
+                  cudaStream_t s, u32 row0, u32 nrows) {
     set_smem_attrs<E1, E2>();
     const u32 M1 = 32 * E1, M2 = 32 * E2;
-    const u32 p1 = polys_per_block(M2 / 8, rpp, npolys, sms), p2 = polys_per_block(M1 / 8, rpp, npolys, sms);
-    kw_inv_chunks<E2><<<dim3(M1 / 8, rpp, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
-        R, data, src, rpp, npolys, p2, level, WGeo<E1>::LOGM);
-    kw_inv_cols<E1><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys, p1,
-                                                                                         level);
+    const u32 p1 = polys_per_block(M2 / 8, nrows, npolys, sms), p2 = polys_per_block(M1 / 8, nrows, npolys, sms);
+    kw_inv_chunks<E2><<<dim3(M1 / 8, nrows, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
+        R, data, src, rpp, npolys, p2, level, WGeo<E1>::LOGM, row0);
+    kw_inv_cols<E1><<<dim3(M2 / 8, nrows, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys,
+                                                                                           p1, level, row0);
 }

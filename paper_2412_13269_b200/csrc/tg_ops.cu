@@ -211,6 +211,41 @@ __global__ void k_rescale(DevRing R, u64* out, const u64* in, int level, u32 npo
     }
 }
 
+// Eval-form rescale_round, step 1: from the inverse-transformed last row,
+// t_r = centered(last) mod q_r into rows 0..level-1 of the scratch t (same
+// layout as the input, level+1 rows per poly).
+__global__ void k_rescale_eval_prep(DevRing R, u64* __restrict__ t, int level, u32 npolys) {
+    const u32 N = R.N, lvl = u32(level);
+    const u64 total = u64(npolys) * N;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
+        const u64 p = i >> R.logN, c = i & (N - 1);
+        u64* base = t + p * (lvl + 1) * N;
+        const u64 last = base[size_t(lvl) * N + c];
+        for (u32 r = 0; r < lvl; ++r) {
+            const u64 q = R.q[r];
+            const u64* e = R.rs + (size_t(lvl) * R.q_count + r) * 4;
+            u64 v = last < q ? last : reduce64(last, q, R.ratio[2 * r], R.ratio[2 * r + 1]);
+            if (last > e[3]) v = sub_mod(v, e[0], q);
+            base[size_t(r) * N + c] = v;
+        }
+    }
+}
+
+// step 3: out_r = (x_r - NTT(t)_r) * q_l^-1 on eval-form rows
+__global__ void k_rescale_eval_finish(DevRing R, u64* __restrict__ out, const u64* __restrict__ in,
+                                      const u64* __restrict__ t, int level, u32 npolys) {
+    const u32 N = R.N, lvl = u32(level);
+    const u64 per = u64(lvl) * N, total = per * npolys;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
+        const u64 p = i / per, w = i - p * per;
+        const u32 r = u32(w >> R.logN);
+        const u64 q = R.q[r];
+        const u64* e = R.rs + (size_t(lvl) * R.q_count + r) * 4;
+        const size_t src = p * (lvl + 1) * N + w;
+        out[i] = shoup(sub_mod(in[src], t[src], q), e[1], e[2], q);
+    }
+}
+
 // Evaluator::mul tensor (ckks.hpp:229-237)
 __global__ void k_tensor(DevRing R, Shape S, u64* p0, u64* p1, u64* p2, const u64* x0, const u64* x1,
                          const u64* y0, const u64* y1) {
@@ -408,6 +443,40 @@ extern "C" int tg_rescale(tg_context* ctx, uint64_t* out, const uint64_t* in, in
                                                                                           npolys);
     TG_LAUNCH_CHECK();
     return TG_OK;
+}
+
+// rescale_round on EVAL-form input and output: only the dropped row is
+// inverse transformed; its centered residues are forward transformed per
+// remaining modulus (NTT(t mod q_r) is what rescale subtracts in eval form).
+// NTT(tg_rescale(iNTT(in))) == tg_rescale_eval(in), residue for residue.
+extern "C" int tg_rescale_eval(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, uint32_t npolys,
+                               void* stream) {
+    if (int rc = check_shape(ctx, level, 0)) return rc;
+    TG_REQUIRE(level >= 1, "[ring] cannot rescale at level 0");
+    TG_REQUIRE(out != in, "[ring] rescale output must not alias its input");
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    const DevRing& R = ctx->ring;
+    cudaStream_t s = as_stream(stream);
+    void* scratch = nullptr;
+    const size_t words = size_t(npolys) * (level + 1) * R.N;
+    TG_CUDA(cudaMallocFromPoolAsync(&scratch, words * 8, ctx->pool, s));
+    u64* t = static_cast<u64*>(scratch);
+    int rc = ntt_inverse_oop(ctx, t, in, level, 0, npolys, s, u32(level), 1);
+    if (rc == TG_OK) {
+        PROF(TG_OP_RESCALE, 8.0 * npolys * R.N * (level + 1));
+        k_rescale_eval_prep<<<grid_for(size_t(npolys) * R.N), kThreads, 0, s>>>(R, t, level, npolys);
+        rc = cudaGetLastError() == cudaSuccess ? TG_OK : cuda_fail(cudaGetLastError(), "rescale prep");
+    }
+    if (rc == TG_OK) rc = ntt_forward_oop(ctx, t, t, level, 0, npolys, s, 0, 0, u32(level));
+    if (rc == TG_OK) {
+        PROF(TG_OP_RESCALE, 8.0 * npolys * R.N * 3.0 * level);
+        k_rescale_eval_finish<<<grid_for(size_t(npolys) * level * R.N), kThreads, 0, s>>>(R, out, in, t, level,
+                                                                                           npolys);
+        rc = cudaGetLastError() == cudaSuccess ? TG_OK : cuda_fail(cudaGetLastError(), "rescale finish");
+    }
+    cudaFreeAsync(scratch, s);
+    return rc;
 }
 
 extern "C" int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const uint64_t* x0,
