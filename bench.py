@@ -249,23 +249,32 @@ class Statement:
         self.mine = D.shard(spec.n_cts, world, rank)
         q = W.statement_query_inputs(self.S, self.d)
         self.blocks = [W.statement_block_inputs(self.S, self.d, b) for b in self.mine]
-        self.client = q.ct_w + q.ct_t + [c for blk in self.blocks for c in (blk.ct_sugar, blk.ct_bp)]
+        # client ciphertexts in the order the query consumes them: weights,
+        # thresholds, then the record columns (staged uploads, e2e)
+        nb = len(self.blocks)
+        self.client = q.ct_w + q.ct_t + [b.ct_sugar for b in self.blocks] + [b.ct_bp for b in self.blocks]
+        self.upload_groups = {"w": (0, 8), "t": (8, 11), "sugar": (11, 11 + nb), "bp": (11 + nb, 11 + 2 * nb)}
 
     def _bind(self, client, blocks):
         from types import SimpleNamespace as NS
+        nb = len(blocks)
         q = NS(ct_w=client[:8], ct_t=client[8:11])
-        bl = [NS(ct_sugar=client[11 + 2 * i], ct_bp=client[12 + 2 * i], pt_attr=b.pt_attr,
+        bl = [NS(ct_sugar=client[11 + i], ct_bp=client[11 + nb + i], pt_attr=b.pt_attr,
                  attr_scale=b.attr_scale, pt_flag=b.pt_flag, flag_scale=b.flag_scale)
               for i, b in enumerate(blocks)]
         return q, bl
 
-    def partial(self, client, streams, mode):
+    def partial(self, client, streams, mode, ready=None):
         if not self.blocks:
             return None
         q, bl = self._bind(client, self.blocks)
         thr = self.W.threshold_fn(self.S, self.chain, mode)
         if self.batched:  # blocks as ciphertext batches (shared launches and key reads)
-            return self.W.statement_partial_batched(self.S, q, bl, thr, streams=streams, max_blocks=self.max_blocks)
+            return self.W.statement_partial_batched(self.S, q, bl, thr, streams=streams, max_blocks=self.max_blocks,
+                                                    ready=ready)
+        if ready:
+            for name in self.upload_groups:
+                ready(name)
         return self.W.statement_partial(self.S, q, bl, thr, streams)
 
     def plain_count(self):
@@ -417,11 +426,11 @@ def run_b200(args):
     flush = torch.empty(64 << 22, dtype=torch.int32, device="cuda")  # 1 GiB > 126 MB L2
     out_meta = {}
 
-    def query(client, streams=None):
+    def query(client, streams=None, ready=None):
         streams = streams or args.streams
         # record blocks run concurrently (one host thread + CUDA stream each);
         # outputs are summed in block order
-        acc = wl.partial(client, streams, mode)
+        acc = wl.partial(client, streams, mode, ready=ready) if ready else wl.partial(client, streams, mode)
         if not wl.slot_sum:  # per-block results stay on their rank (no exchange)
             return acc
         if world > 1:
@@ -511,9 +520,15 @@ def run_b200(args):
 
     uploader = G.HostUpload(S.ring, host_buf, metas, G.Form.coeff, G.Domain.slots)
 
+    groups = getattr(wl, "upload_groups", None) if not args.no_staged_upload else None
+
     def e2e_step():
-        ups = uploader.upload()  # every step: pinned host -> HBM, one DMA
-        r = query(ups)
+        if groups:  # every step: pinned host -> HBM, one DMA per input group on a copy
+            # stream; each job waits (on the device) for its own group only
+            ups = uploader.upload_async([hi - lo for lo, hi in groups.values()])
+            r = query(ups, ready=lambda name: uploader.wait(list(range(*groups[name]))))
+        else:  # every step: pinned host -> HBM, one DMA
+            r = query(uploader.upload())
         if host_out:  # the result back on the host every step
             for c, h in zip(r if isinstance(r, list) else [r], host_out):
                 G.ciphertext_to_numpy(c, h)
@@ -745,6 +760,8 @@ def main():
     ap.add_argument("--streams", type=int, default=4, help="concurrent pipelines (host thread + CUDA stream each) per GPU")
     ap.add_argument("--poly-eval", choices=["bsgs", "ladder"], default="bsgs",
                     help="Chebyshev evaluator of the sign stages (BASELINE configs specify BSGS)")
+    ap.add_argument("--no-staged-upload", action="store_true",
+                    help="e2e: one synchronous upload per step instead of per-group DMAs overlapping compute")
     ap.add_argument("--no-batch", action="store_true",
                     help="statement workloads: one ciphertext per pipeline instead of ciphertext batches")
     ap.add_argument("--max-blocks", type=int, default=8, help="record blocks per ciphertext batch")

@@ -77,6 +77,12 @@ int tg_stream_sync(tg_context* ctx, void* stream);
 /* A non-blocking stream on the context's device (*stream = cudaStream_t). */
 int tg_stream_create(tg_context* ctx, void** stream);
 int tg_stream_destroy(tg_context* ctx, void* stream);
+/* Events for cross-stream ordering without host synchronisation (staged
+ * host->device uploads overlapping compute). */
+int tg_event_create(tg_context* ctx, void** event);
+int tg_event_destroy(tg_context* ctx, void* event);
+int tg_event_record(tg_context* ctx, void* event, void* stream);
+int tg_stream_wait_event(tg_context* ctx, void* stream, void* event);
 /* Device index the context lives on. */
 int tg_context_device(const tg_context* ctx);
 

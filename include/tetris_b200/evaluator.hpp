@@ -132,9 +132,9 @@ Ciphertext eval_chebyshev(const Evaluator& ev, const Ciphertext& x, const std::v
 // same algorithm composed of the reference's Evaluator primitives.
 Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
                                const EvalKeys& keys);
-// Chebyshev evaluation keeps intermediate products in evaluation form (default
-// on; TG_EVAL_PIPELINE=0 or set_eval_pipeline(false) selects the coefficient-
-// form pipeline). Results are identical either way.
+// Chebyshev evaluation with intermediate products kept in evaluation form
+// (opt-in: TG_EVAL_PIPELINE=1 or set_eval_pipeline(true); slower for the
+// BSGS shapes measured, see chebyshev.cpp). Results are identical either way.
 void set_eval_pipeline(bool on);
 bool eval_pipeline_enabled();
 // Which Chebyshev evaluator the threshold stages use.

@@ -11,11 +11,14 @@
 // (tg_lincomb) after the relinearised product; scales and noise bounds follow
 // the reference's add_inplace / mul_scalar / sub_inplace / add_scalar /
 // rescale sequence exactly.
-// Eval-form pipeline (default; TG_EVAL_PIPELINE=0 selects the coefficient-
-// form one): products, combinations and rescales stay in evaluation form
-// (relinearize_eval / tg_rescale_eval), saving about two transformed rows
-// per row of each product; the result is converted to coefficient form once
-// at the end, residue for residue the same ciphertext.
+// Eval-form pipeline (opt-in: TG_EVAL_PIPELINE=1 or set_eval_pipeline):
+// products, combinations and rescales stay in evaluation form
+// (relinearize_eval / tg_rescale_eval); the result is converted to
+// coefficient form once at the end, residue for residue the same ciphertext.
+// It saves two transformed rows per row of a product whose result is
+// multiplied again, but every rescale then needs `level` forward rows, so
+// for the BSGS shapes here it is slower (config 4: 121 vs 105 ms per step,
+// DESIGN.md) and the coefficient-form pipeline is the default.
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -55,7 +58,7 @@ bool eval_pipeline() {
     int v = g_eval_pipeline.load();
     if (v < 0) {
         const char* e = std::getenv("TG_EVAL_PIPELINE");
-        v = (e && e[0] == '0') ? 0 : 1;
+        v = (e && e[0] == '1') ? 1 : 0;
         g_eval_pipeline.store(v);
     }
     return v != 0;

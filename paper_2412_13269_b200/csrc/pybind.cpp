@@ -605,6 +605,12 @@ PYBIND11_MODULE(_tetris_b200, m) {
     // Reused upload target for end-to-end runs: the same HBM block receives
     // the host buffer on every upload() (one DMA + synchronize); memoised
     // transforms of the previous contents are dropped first.
+    // Pinned host -> HBM upload of a query's client ciphertexts into one
+    // reused device block. upload(): one DMA, synchronised. upload_async(
+    // groups): one DMA per group of consecutive ciphertexts on a copy stream,
+    // each followed by an event; wait(i) makes the calling thread's current
+    // stream wait (on the device) for the group holding ciphertext i, so
+    // compute on early groups overlaps the copy of later ones.
     struct HostUpload {
         const RingParams* ring;
         py::array_t<uint64_t, py::array::c_style> host;
@@ -612,8 +618,34 @@ PYBIND11_MODULE(_tetris_b200, m) {
         Form form;
         Domain domain;
         std::shared_ptr<DeviceBuffer> blk;
+        void* copy_stream = nullptr;
+        std::vector<void*> events;    // one per group, plus [0] = "upload issued"
+        std::vector<int> group_of;    // ciphertext -> group
+        ~HostUpload() {
+            if (!ring) return;
+            tg_context* c = ring->dev();
+            for (void* e : events) tg_event_destroy(c, e);
+            if (copy_stream) tg_stream_destroy(c, copy_stream);
+        }
+        std::vector<Ciphertext> views() const {
+            std::vector<Ciphertext> out;
+            for (const auto& [off, np, level, scale, sk] : metas) {
+                const std::size_t w = std::size_t(level + 1) * ring->degree();
+                Ciphertext ct;
+                for (int i = 0; i < np; ++i) ct.parts.push_back(Poly::view(*ring, blk, off + w * i, level, form, 0));
+                ct.scale = scale;
+                ct.domain = domain;
+                ct.sk_id = sk;
+                out.push_back(std::move(ct));
+            }
+            return out;
+        }
+        std::size_t end_of(std::size_t i) const {
+            const auto& m = metas[i];
+            return std::get<0>(m) + std::size_t(std::get<1>(m)) * (std::get<2>(m) + 1) * ring->degree();
+        }
     };
-    py::class_<HostUpload>(m, "HostUpload")
+    py::class_<HostUpload, std::unique_ptr<HostUpload>>(m, "HostUpload")
         .def(py::init([](const RingParams& ring, py::array_t<uint64_t, py::array::c_style> a,
                          std::vector<std::tuple<std::size_t, int, int, double, u64>> metas, Form form, Domain domain) {
                  for (const auto& mt : metas) {
@@ -622,7 +654,14 @@ PYBIND11_MODULE(_tetris_b200, m) {
                      if (need > std::size_t(a.size())) throw TetrisError("ckks", "HostUpload: buffer too small");
                  }
                  auto blk = std::make_shared<DeviceBuffer>(ring, std::size_t(a.size()));
-                 return HostUpload{&ring, a, std::move(metas), form, domain, blk};
+                 auto u = std::make_unique<HostUpload>();
+                 u->ring = &ring;
+                 u->host = a;
+                 u->metas = std::move(metas);
+                 u->form = form;
+                 u->domain = domain;
+                 u->blk = blk;
+                 return u;
              }),
              py::keep_alive<1, 2>())
         .def("upload", [](HostUpload& u) {
@@ -634,17 +673,56 @@ PYBIND11_MODULE(_tetris_b200, m) {
                                        ring.stream()));
                 ring.synchronize();
             }
-            std::vector<Ciphertext> out;
-            for (const auto& [off, np, level, scale, sk] : u.metas) {
-                const std::size_t w = std::size_t(level + 1) * ring.degree();
-                Ciphertext ct;
-                for (int i = 0; i < np; ++i) ct.parts.push_back(Poly::view(ring, u.blk, off + w * i, level, u.form, 0));
-                ct.scale = scale;
-                ct.domain = u.domain;
-                ct.sk_id = sk;
-                out.push_back(std::move(ct));
+            return u.views();
+        })
+        .def("upload_async", [](HostUpload& u, const std::vector<int>& groups) {
+            const RingParams& ring = *u.ring;
+            std::size_t total = 0;
+            for (int g : groups) {
+                if (g <= 0) throw TetrisError("ckks", "HostUpload: empty group");
+                total += std::size_t(g);
             }
-            return out;
+            if (total != u.metas.size()) throw TetrisError("ckks", "HostUpload: groups must cover every ciphertext");
+            for (std::size_t i = 1; i < u.metas.size(); ++i)
+                if (std::get<0>(u.metas[i]) < u.end_of(i - 1))
+                    throw TetrisError("ckks", "HostUpload: staged upload needs ciphertexts in buffer order");
+            tg_context* c = ring.dev();
+            py::gil_scoped_release nogil;
+            if (!u.copy_stream) check_tg(tg_stream_create(c, &u.copy_stream));
+            while (u.events.size() < groups.size() + 1) {
+                void* e = nullptr;
+                check_tg(tg_event_create(c, &e));
+                u.events.push_back(e);
+            }
+            u.blk->clear_eval_cache();
+            // the copies start after everything issued so far on the caller's
+            // stream (the previous step's readers of this block included)
+            check_tg(tg_event_record(c, u.events[0], ring.stream()));
+            check_tg(tg_stream_wait_event(c, u.copy_stream, u.events[0]));
+            u.group_of.assign(u.metas.size(), 0);
+            std::size_t first = 0;
+            for (std::size_t g = 0; g < groups.size(); ++g) {
+                const std::size_t last = first + std::size_t(groups[g]) - 1;
+                const std::size_t lo = std::get<0>(u.metas[first]), hi = u.end_of(last);
+                check_tg(tg_memcpy_h2d(c, u.blk->data() + lo, u.host.data() + lo, (hi - lo) * 8, u.copy_stream));
+                check_tg(tg_event_record(c, u.events[g + 1], u.copy_stream));
+                for (std::size_t i = first; i <= last; ++i) u.group_of[i] = int(g) + 1;
+                first = last + 1;
+            }
+            return u.views();
+        })
+        .def("wait", [](HostUpload& u, const std::vector<int>& idx) {
+            const RingParams& ring = *u.ring;
+            int g = 0;
+            for (int i : idx) {
+                if (i < 0 || std::size_t(i) >= u.group_of.size())
+                    throw TetrisError("ckks", "HostUpload.wait: no staged upload holds this ciphertext");
+                g = std::max(g, u.group_of[std::size_t(i)]);
+            }
+            if (g > 0) check_tg(tg_stream_wait_event(ring.dev(), ring.stream(), u.events[std::size_t(g)]));
+        }, "the current stream waits for the staged groups holding these ciphertexts (groups complete in order)")
+        .def("synchronize", [](HostUpload& u) {
+            if (u.copy_stream) check_tg(tg_stream_sync(u.ring->dev(), u.copy_stream));
         });
     m.def("ciphertext_to_numpy", [](const Ciphertext& ct, py::array_t<uint64_t, py::array::c_style> out) {
         const RingParams& ring = ct.ring();

@@ -308,6 +308,32 @@ extern "C" int tg_stream_destroy(tg_context* ctx, void* stream) {
     TG_CUDA(cudaStreamDestroy(as_stream(stream)));
     return TG_OK;
 }
+extern "C" int tg_event_create(tg_context* ctx, void** event) {
+    if (!ctx || !event) return fail(TG_E_ARG, "[gpu] tg_event_create: null argument");
+    DeviceGuard guard(ctx->device);
+    cudaEvent_t e = nullptr;
+    TG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    *event = e;
+    return TG_OK;
+}
+extern "C" int tg_event_destroy(tg_context* ctx, void* event) {
+    if (!ctx || !event) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    TG_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(event)));
+    return TG_OK;
+}
+extern "C" int tg_event_record(tg_context* ctx, void* event, void* stream) {
+    if (!ctx || !event) return fail(TG_E_ARG, "[gpu] tg_event_record: null argument");
+    DeviceGuard guard(ctx->device);
+    TG_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event), as_stream(stream)));
+    return TG_OK;
+}
+extern "C" int tg_stream_wait_event(tg_context* ctx, void* stream, void* event) {
+    if (!ctx || !event) return fail(TG_E_ARG, "[gpu] tg_stream_wait_event: null argument");
+    DeviceGuard guard(ctx->device);
+    TG_CUDA(cudaStreamWaitEvent(as_stream(stream), static_cast<cudaEvent_t>(event), 0));
+    return TG_OK;
+}
 extern "C" int tg_context_device(const tg_context* ctx) { return ctx ? ctx->device : -1; }
 
 // ---------------------------------------------------------------------------

@@ -383,28 +383,43 @@ def statement_partial(S, q, blocks, threshold, streams=1):
     return acc
 
 
-def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8):
+def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8, ready=None):
     """B200 module: the same per-block statement with the blocks evaluated as
     ciphertext batches (stack_ciphertexts): per chunk of <= max_blocks blocks,
     one batched threshold per column (sugar, pressure, risk score; the three
     run concurrently), then the AND products batched. Each
     block's output is bit-identical to statement_block's (a batch is exactly
     `batch` independent ciphertexts; tests/test_gpu_statement.py); launches
-    and switching-key reads are shared by the batch."""
+    and switching-key reads are shared by the batch.
+    ready (optional, staged uploads): ready(name) makes the current stream
+    wait until the client ciphertexts `name` ("w", "t", "sugar", "bp") are
+    resident, so each job starts as soon as its own inputs have arrived."""
     T, ev, keys = S.T, S.ev, S.keys
-    risks = run_concurrent(T, S.ring, lambda blk: linear_score(S, q.ct_w, blk.pt_attr, blk.attr_scale), blocks,
-                           streams)
+    wait = ready or (lambda name: None)
+
+    def score(blk):
+        wait("w")
+        return linear_score(S, q.ct_w, blk.pt_attr, blk.attr_scale)
+
+    risks = run_concurrent(T, S.ring, score, blocks, streams)
     chunks = [list(range(i, min(len(blocks), i + max_blocks))) for i in range(0, len(blocks), max_blocks)]
-    jobs = []
-    for ch in chunks:  # three equal batches per chunk, run concurrently
-        nb = len(ch)
-        for col, k, norm in ((lambda b: blocks[b].ct_sugar, 0, 1.0), (lambda b: blocks[b].ct_bp, 1, 1.0),
-                             (lambda b: risks[b], 2, RISK_NORM)):
-            jobs.append((T.stack_ciphertexts([col(i) for i in ch]), T.stack_ciphertexts([q.ct_t[k]] * nb), norm))
-    outs = run_concurrent(T, S.ring, lambda j: threshold(*j), jobs, streams)
+    # three equal batches per chunk, run concurrently; the risk batch first
+    # (its inputs are resident before the record columns)
+    cols = (("risk", 2, RISK_NORM), ("sugar", 0, 1.0), ("bp", 1, 1.0))
+    jobs = [(ch, col, k, norm) for ch in chunks for col, k, norm in cols]
+
+    def job(j):
+        ch, col, k, norm = j
+        wait("t")
+        if col != "risk":
+            wait(col)
+        xs = [risks[b] if col == "risk" else getattr(blocks[b], "ct_" + col) for b in ch]
+        return threshold(T.stack_ciphertexts(xs), T.stack_ciphertexts([q.ct_t[k]] * len(ch)), norm)
+
+    outs = run_concurrent(T, S.ring, job, jobs, streams)
     acc = None
     for c, ch in enumerate(chunks):
-        b1, b2, b3 = outs[3 * c], outs[3 * c + 1], outs[3 * c + 2]
+        b3, b1, b2 = outs[3 * c], outs[3 * c + 1], outs[3 * c + 2]
         a = ev.rescale(ev.mul_relin(b1, b2, keys))
         a = ev.rescale(ev.mul_relin(a, b3, keys))
         for i, ct in zip(ch, T.unstack_ciphertext(a)):
