@@ -48,6 +48,27 @@ __device__ __forceinline__ double fp_mulmod(double b, double w, double wq, doubl
     return __dadd_rn(__fma_rn(-k, q, h), l);
 }
 
+// r == a*b (mod q) exactly for canonical a, b in [0, q), q < 1.2 * 2^50,
+// qi = fl(1/q); no per-operand quotient table (both operands are data):
+//   h = fl(a b) (an integer), l = a b - h exactly (FMA), |l| <= 2^48.
+//   h qi = (a b / q)(1 + e), |e| <= 2^-52 + 2^-106, so |h qi - a b/q| <=
+//       1.2 * 2^50 * 2^-51.99 < 0.31; h qi in [0, 2^51) puts t = fl(h qi + M)
+//       in [1.5 * 2^52, 2^53) (ulp 1): k = t - M is exact, |k - a b/q| < 0.81.
+//   h - k q = (a b - k q) - l, |.| < 0.81 q + 2^48 < 2^51: fma(-k, q, h) is
+//       exact, and r = (h - k q) + l = a b - k q with |r| < 0.81 q.
+__device__ __forceinline__ double fp_mulmod_qi(double a, double b, double q, double qi) {
+    const double h = __dmul_rn(a, b);
+    const double l = __fma_rn(a, b, -h);
+    const double k = __dsub_rn(__fma_rn(h, qi, kRoundMagic), kRoundMagic);
+    return __dadd_rn(__fma_rn(-k, q, h), l);
+}
+
+// |v| < q -> canonical u64 in [0, q)
+__device__ __forceinline__ u64 fp_canonical1(double v, double q) {
+    if (v < 0) v = __dadd_rn(v, q);
+    return d2u(v);
+}
+
 // v - rint(v/q) q for integer |v| < 2^53: |result| <= q/2 + 1 (qi = fl(1/q)
 // gives |v qi - v/q| <= 2^-52 |v/q| < 1/2), exact by the same FMA argument.
 __device__ __forceinline__ double fp_reduce(double v, double q, double qi) {

@@ -178,38 +178,86 @@ k_key_inner_b(DevRing R, u64* __restrict__ acc, const u64* __restrict__ digits, 
     const u32 rows = u32(level) + 1 + K;
     const u64 words = u64(rows) * N;
     const size_t key_rows = size_t(R.nmod);
-    // work item = (word, chunk of polys_per_thread sources): small rings with
-    // large batches still fill the GPU
+    // work item = (word pair, chunk of polys_per_thread sources): small rings
+    // with large batches still fill the GPU. Two words per thread (16-byte
+    // loads) and the next source's digits prefetched while the current one
+    // is reduced keep enough loads in flight to cover HBM latency.
+    const u64 pairs = words / 2;
     const u32 chunks = (npolys + polys_per_thread - 1) / polys_per_thread;
-    for (u64 it = blockIdx.x * u64(kThreads) + threadIdx.x; it < words * chunks; it += u64(gridDim.x) * kThreads) {
-        const u64 i = it % words;
-        const u32 b0 = u32(it / words) * polys_per_thread, b1 = min(npolys, b0 + polys_per_thread);
+    for (u64 it = blockIdx.x * u64(kThreads) + threadIdx.x; it < pairs * chunks; it += u64(gridDim.x) * kThreads) {
+        const u64 i = (it % pairs) * 2;
+        const u32 b0 = u32(it / pairs) * polys_per_thread, b1 = min(npolys, b0 + polys_per_thread);
         const u32 r = u32(i >> R.logN);
         const u32 c = u32(i & (N - 1));
         const u32 m = mod_index(r, level, R.q_count);
         const u64 q = R.q[m], rl = R.ratio[2 * m], rh = R.ratio[2 * m + 1];
-        u64 kb[NDMAX], ka[NDMAX];
+        ulonglong2 kb[NDMAX], ka[NDMAX], dv[NDMAX];
 #pragma unroll
         for (int k = 0; k < NDMAX; ++k) {
             if (u32(k) < nd) {
                 const u64* base = key + (size_t(k) * 2) * key_rows * N + size_t(m) * N + c;
-                kb[k] = base[0];
-                ka[k] = base[key_rows * N];
+                kb[k] = *reinterpret_cast<const ulonglong2*>(base);
+                ka[k] = *reinterpret_cast<const ulonglong2*>(base + key_rows * N);
+                dv[k] = *reinterpret_cast<const ulonglong2*>(digits + (size_t(b0) * nd + k) * words + i);
             }
         }
+        const bool fp = q < kFpMaxQ;  // q-chain rows: exact FP64 products (tg_fp64.cuh)
+        const double qd = fp ? R.qd[4 * m] : 0.0, qi = fp ? R.qd[4 * m + 1] : 0.0;
         for (u32 b = b0; b < b1; ++b) {
-            const u64* dig = digits + size_t(b) * nd * words + i;
-            U128 s0{0, 0}, s1{0, 0};
+            ulonglong2 dn[NDMAX];
+            if (b + 1 < b1) {
+#pragma unroll
+                for (int k = 0; k < NDMAX; ++k)
+                    if (u32(k) < nd)
+                        dn[k] = *reinterpret_cast<const ulonglong2*>(digits + (size_t(b + 1) * nd + k) * words + i);
+            }
+            if (fp) {
+                // |product| < 0.81q; reduced every 4 digits: |sum| < q/2 + 1 + 3.3q < 2^53
+                double s0 = 0, s1 = 0, t0 = 0, t1 = 0;
+#pragma unroll
+                for (int k = 0; k < NDMAX; ++k) {
+                    if (u32(k) < nd) {
+                        const double dx = u2d(dv[k].x), dy = u2d(dv[k].y);
+                        s0 = __dadd_rn(s0, fp_mulmod_qi(dx, u2d(kb[k].x), qd, qi));
+                        s1 = __dadd_rn(s1, fp_mulmod_qi(dx, u2d(ka[k].x), qd, qi));
+                        t0 = __dadd_rn(t0, fp_mulmod_qi(dy, u2d(kb[k].y), qd, qi));
+                        t1 = __dadd_rn(t1, fp_mulmod_qi(dy, u2d(ka[k].y), qd, qi));
+                        if ((k & 3) == 3) {
+                            s0 = fp_reduce(s0, qd, qi);
+                            s1 = fp_reduce(s1, qd, qi);
+                            t0 = fp_reduce(t0, qd, qi);
+                            t1 = fp_reduce(t1, qd, qi);
+                        }
+                    }
+                }
+                *reinterpret_cast<ulonglong2*>(acc + size_t(b) * words + i) = make_ulonglong2(
+                    fp_canonical(fp_reduce(s0, qd, qi), qd), fp_canonical(fp_reduce(t0, qd, qi), qd));
+                *reinterpret_cast<ulonglong2*>(acc + (size_t(npolys) + b) * words + i) = make_ulonglong2(
+                    fp_canonical(fp_reduce(s1, qd, qi), qd), fp_canonical(fp_reduce(t1, qd, qi), qd));
+                if (b + 1 < b1) {
+#pragma unroll
+                    for (int k = 0; k < NDMAX; ++k) dv[k] = dn[k];
+                }
+                continue;
+            }
+            U128 s0{0, 0}, s1{0, 0}, t0{0, 0}, t1{0, 0};
 #pragma unroll
             for (int k = 0; k < NDMAX; ++k) {  // nd <= NDMAX <= 15: products < 2^124, no mid reduction
                 if (u32(k) < nd) {
-                    const u64 dv = dig[size_t(k) * words];
-                    mac128(s0, dv, kb[k]);
-                    mac128(s1, dv, ka[k]);
+                    mac128(s0, dv[k].x, kb[k].x);
+                    mac128(s1, dv[k].x, ka[k].x);
+                    mac128(t0, dv[k].y, kb[k].y);
+                    mac128(t1, dv[k].y, ka[k].y);
                 }
             }
-            acc[size_t(b) * words + i] = barrett128(s0.lo, s0.hi, q, rl, rh);
-            acc[(size_t(npolys) + b) * words + i] = barrett128(s1.lo, s1.hi, q, rl, rh);
+            *reinterpret_cast<ulonglong2*>(acc + size_t(b) * words + i) =
+                make_ulonglong2(barrett128(s0.lo, s0.hi, q, rl, rh), barrett128(t0.lo, t0.hi, q, rl, rh));
+            *reinterpret_cast<ulonglong2*>(acc + (size_t(npolys) + b) * words + i) =
+                make_ulonglong2(barrett128(s1.lo, s1.hi, q, rl, rh), barrett128(t1.lo, t1.hi, q, rl, rh));
+            if (b + 1 < b1) {
+#pragma unroll
+                for (int k = 0; k < NDMAX; ++k) dv[k] = dn[k];
+            }
         }
     }
 }
@@ -658,8 +706,8 @@ int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd
         // (each key word read once per batch), fewer for small rings
         const u64 want = u64(ctx->sms) * 2048;
         u32 ppt = npolys;
-        while (ppt > 1 && words * ((npolys + ppt - 1) / ppt) < want) ppt = (ppt + 1) / 2;
-        const u32 blocks = grid_for(words * ((npolys + ppt - 1) / ppt));
+        while (ppt > 1 && words / 2 * ((npolys + ppt - 1) / ppt) < want) ppt = (ppt + 1) / 2;
+        const u32 blocks = grid_for(words / 2 * ((npolys + ppt - 1) / ppt));
         if (nd <= 4) k_key_inner_b<4><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
         else if (nd <= 8) k_key_inner_b<8><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
         else if (nd <= 15) k_key_inner_b<15><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
@@ -806,8 +854,8 @@ extern "C" int tg_keyswitch_add_eval(tg_gadget* g, uint64_t* out0, uint64_t* out
         ProfScope prof(ctx, TG_OP_KEY_INNER, 8.0 * words * (npolys * (nd + 2.0) + 2.0 * nd), s);
         const u64 want = u64(ctx->sms) * 2048;
         u32 ppt = npolys;
-        while (ppt > 1 && words * ((npolys + ppt - 1) / ppt) < want) ppt = (ppt + 1) / 2;
-        const u32 blocks = grid_for(words * ((npolys + ppt - 1) / ppt));
+        while (ppt > 1 && words / 2 * ((npolys + ppt - 1) / ppt) < want) ppt = (ppt + 1) / 2;
+        const u32 blocks = grid_for(words / 2 * ((npolys + ppt - 1) / ppt));
         if (nd <= 4) k_key_inner_b<4><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
         else if (nd <= 8) k_key_inner_b<8><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
         else if (nd <= 15) k_key_inner_b<15><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);

@@ -1,6 +1,7 @@
 // Element-wise ring and CKKS residue kernels (HBM-bound, coalesced, one
 // grid-stride pass per op). Each kernel cites the reference loop it replaces.
 #include "tg_internal.cuh"
+#include "tg_fp64.cuh"
 
 namespace tg {
 namespace {
@@ -54,7 +55,13 @@ __global__ void k_mul(DevRing R, Shape S, u64* out, const u64* a, const u64* b, 
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
         const u32 m = row_mod(R, S, i);
         const u64 q = R.q[m];
-        u64 r = mul_mod(a[i], b[i], q, R.ratio[2 * m], R.ratio[2 * m + 1]);
+        u64 r;
+        if (q < kFpMaxQ) {  // exact FP64 product (tg_fp64.cuh)
+            const double qd = R.qd[4 * m];
+            r = fp_canonical1(fp_mulmod_qi(u2d(a[i]), u2d(b[i]), qd, R.qd[4 * m + 1]), qd);
+        } else {
+            r = mul_mod(a[i], b[i], q, R.ratio[2 * m], R.ratio[2 * m + 1]);
+        }
         if (acc) r = add_mod(out[i], r, q);
         out[i] = r;
     }
@@ -253,6 +260,14 @@ __global__ void k_tensor(DevRing R, Shape S, u64* p0, u64* p1, u64* p2, const u6
         const u32 m = row_mod(R, S, i);
         const u64 q = R.q[m], rl = R.ratio[2 * m], rh = R.ratio[2 * m + 1];
         const u64 a0 = x0[i], a1 = x1[i], b0 = y0[i], b1 = y1[i];
+        if (q < kFpMaxQ) {  // exact FP64 products (tg_fp64.cuh): |r| < 0.81q each
+            const double qd = R.qd[4 * m], qi = R.qd[4 * m + 1];
+            const double da0 = u2d(a0), da1 = u2d(a1), db0 = u2d(b0), db1 = u2d(b1);
+            p0[i] = fp_canonical1(fp_mulmod_qi(da0, db0, qd, qi), qd);
+            p1[i] = fp_canonical(__dadd_rn(fp_mulmod_qi(da0, db1, qd, qi), fp_mulmod_qi(da1, db0, qd, qi)), qd);
+            p2[i] = fp_canonical1(fp_mulmod_qi(da1, db1, qd, qi), qd);
+            continue;
+        }
         p0[i] = mul_mod(a0, b0, q, rl, rh);
         // x0*y1 + x1*y0 as one 128-bit sum (< 2^125), one reduction
         U128 acc{0, 0};
@@ -281,6 +296,16 @@ __global__ void k_mul_plain_sum(DevRing R, u64* __restrict__ out, const PlainSum
         const u64 w = i % per;
         const u32 m = u32(w >> R.logN);
         const u64 q = R.q[m], rl = R.ratio[2 * m], rh = R.ratio[2 * m + 1];
+        if (q < kFpMaxQ) {  // exact FP64 products, reduced every 4 terms (|sum| < q/2 + 1 + 4 * 0.81q < 2^53)
+            const double qd = R.qd[4 * m], qi = R.qd[4 * m + 1];
+            double s = 0.0;
+            for (u32 t = 0; t < P.nterms; ++t) {
+                s = __dadd_rn(s, fp_mulmod_qi(u2d(P.ct[t][i]), u2d(P.plain[t][w]), qd, qi));
+                if ((t & 3) == 3) s = fp_reduce(s, qd, qi);
+            }
+            out[i] = fp_canonical(fp_reduce(s, qd, qi), qd);
+            continue;
+        }
         U128 acc{0, 0};
         u32 pending = 0;
         for (u32 t = 0; t < P.nterms; ++t) {
@@ -301,7 +326,13 @@ __global__ void k_mul_plain(DevRing R, u64* out, const u64* ct, const u64* plain
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
         const u64 w = i % per;
         const u32 m = u32(w >> R.logN);
-        out[i] = mul_mod(ct[i], plain[w], R.q[m], R.ratio[2 * m], R.ratio[2 * m + 1]);
+        const u64 q = R.q[m];
+        if (q < kFpMaxQ) {
+            const double qd = R.qd[4 * m];
+            out[i] = fp_canonical1(fp_mulmod_qi(u2d(ct[i]), u2d(plain[w]), qd, R.qd[4 * m + 1]), qd);
+        } else {
+            out[i] = mul_mod(ct[i], plain[w], q, R.ratio[2 * m], R.ratio[2 * m + 1]);
+        }
     }
 }
 
