@@ -317,6 +317,15 @@ int tg_ks_inner_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t
 int tg_keyswitch_add_eval(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
                           const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
                           const uint64_t* add0, const uint64_t* add1, uint32_t npolys, void* stream);
+/* relinearize (rlwe.hpp:601-620) of npolys part-major degree-2 ciphertexts
+ * straight from the tensor product: c2 (coefficient form; c2_eval optional)
+ * is key-switched, and c0/c1 in EVAL form are folded into the accumulators'
+ * Q rows as P * c before ModDown, which returns c + ModDown(acc) in
+ * coefficient form. out0/out1 == tg_keyswitch_add_batch with the coefficient
+ * forms of c0/c1 as addends, residue for residue. */
+int tg_relinearize_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* c2,
+                         const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits, int level,
+                         const uint64_t* c0_eval, const uint64_t* c1_eval, uint32_t npolys, void* stream);
 int tg_keyswitch_add_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
                            const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
                            const uint64_t* add0, const uint64_t* add1, uint32_t npolys, void* stream);

@@ -442,6 +442,32 @@ Ciphertext KeyContext::relinearize(const Ciphertext& ct, const SwitchingKey& rlk
     if (ct.degree() != 2) throw TetrisError("rlwe", "relinearize expects a degree-2 ciphertext");
     if (rlk.to_id != ct.sk_id) throw TetrisError("rlwe", "relinearization key mismatch");
     const u32 B = ct.batch;
+    const int lvl0 = ct.level();
+    bool all_eval = true;
+    for (const auto& p : ct.parts) all_eval &= p.form() == Form::eval && p.nspecial() == 0;
+    if (all_eval) {
+        // the tensor product's output: only c2 goes back to coefficient form
+        // (ModUp's source); c0/c1 stay in eval form and are folded into the
+        // key-switch accumulators (tg_relinearize_batch)
+        std::vector<Poly> keep;
+        const u64* a0 = detail::group_data(ct.parts, 0, B, keep);
+        const u64* a1 = detail::group_data(ct.parts, B, B, keep);
+        const u64* c2e = detail::group_data(ct.parts, 2 * B, B, keep);
+        std::vector<Poly> c2 = fresh_parts(*ring_, int(B), lvl0, Form::coeff);
+        check_tg(tg_ntt_inverse_oop(ring_->dev(), const_cast<u64*>(c2[0].data()), c2e, lvl0, 0, B, ring_->stream()));
+        std::vector<Poly> dst = fresh_parts(*ring_, int(2 * B), lvl0, Form::coeff);
+        check_tg(tg_relinearize_batch(plan_->dev(), const_cast<u64*>(dst[0].data()), const_cast<u64*>(dst[B].data()),
+                                      c2[0].data(), c2e, key_base(rlk), rlk.digits(), lvl0, a0, a1, B,
+                                      ring_->stream()));
+        Ciphertext out;
+        out.batch = B;
+        out.parts = std::move(dst);
+        out.scale = ct.scale;
+        out.domain = ct.domain;
+        out.sk_id = ct.sk_id;
+        out.noise_bound = ct.noise_bound + ks_noise_estimate();
+        return out;
+    }
     // keep the eval form of c2 (the tensor output): the digits' own-group rows
     // are its rows, so ModUp copies them instead of re-transforming
     const u64* c2_eval = nullptr;

@@ -397,7 +397,10 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
     // [K][nq][4] (P/p_s) mod q_r, Shoup, its negation q_r - w, Shoup (so a
     // centered y_s < 0 multiplies |y_s| by -w: no per-term reduction);
     // [nq][2] P^-1 mod q_r + Shoup.
-    std::vector<u64> md(size_t(K) * 2 + size_t(K) * nq * 4 + size_t(nq) * 2, 0);
+    // [nq][4] P mod q_r, Shoup, and as FP64 (P mod q_r, fl((P mod q_r) / q_r))
+    // bit patterns: eval-form addends folded into the key-switch accumulators
+    // as P * c (tg_relinearize_batch).
+    std::vector<u64> md(size_t(K) * 2 + size_t(K) * nq * 4 + size_t(nq) * 2 + size_t(nq) * 4, 0);
     for (u32 s = 0; s < K; ++s) {
         u64 ps = mod[nq + s];
         u64 rest = 1;
@@ -427,6 +430,14 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
         u64* e = &md[2 * K + size_t(K) * nq * 4 + size_t(r) * 2];
         e[0] = pinv;
         e[1] = h_shoup(pinv, q);
+        u64 pm = 1;
+        for (u32 t = 0; t < K; ++t) pm = h_mul_mod(pm, mod[nq + t] % q, q);
+        u64* f = &md[2 * K + size_t(K) * nq * 4 + size_t(nq) * 2 + size_t(r) * 4];
+        const double pd = double(pm), pq = double(pm) / double(q);
+        f[0] = pm;
+        f[1] = h_shoup(pm, q);
+        std::memcpy(&f[2], &pd, 8);
+        std::memcpy(&f[3], &pq, 8);
     }
     // lazy-sum safety: 2*K*q_max + q_max < 2^64 for ModDown, 2*group*q < 2^64 for ModUp
     {

@@ -164,7 +164,8 @@ struct GadgetDev {
     u32 group_size, ngroups;
     u64* src;   // [ngroups][group_size(active-1)][group_size(i)][2]
     u64* conv;  // [ngroups][group_size][group_size][nmod][2]
-    u64* md;    // ModDown: [K][2] (P/p_s)^-1 mod p_s; [K][q_count][4] +-(P/p_s) mod q_r; [q_count][2] P^-1 mod q_r
+    u64* md;    // ModDown: [K][2] (P/p_s)^-1 mod p_s; [K][q_count][4] +-(P/p_s) mod q_r; [q_count][2] P^-1 mod q_r;
+                // [q_count][4] P mod q_r (u64, Shoup, FP64 value, FP64 quotient)
     bool lazy_modup, lazy_moddown;  // lazy sums provably fit a word (checked on the host)
     u32 base2_bits;                 // 0: RNS digits; else balanced base-2^b sub-digits (group_size 1)
 };

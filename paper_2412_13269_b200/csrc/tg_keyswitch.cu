@@ -173,7 +173,8 @@ k_key_inner(DevRing R, u64* __restrict__ acc0, u64* __restrict__ acc1, const u64
 template <int NDMAX>
 __global__ void __launch_bounds__(kThreads)
 k_key_inner_b(DevRing R, u64* __restrict__ acc, const u64* __restrict__ digits, u32 nd, u32 npolys,
-              const u64* __restrict__ key, int level, u32 polys_per_thread) {
+              const u64* __restrict__ key, int level, u32 polys_per_thread, const u64* __restrict__ add0 = nullptr,
+              const u64* __restrict__ add1 = nullptr, const u64* __restrict__ pmod = nullptr) {
     const u32 N = R.N, K = R.K;
     const u32 rows = u32(level) + 1 + K;
     const u64 words = u64(rows) * N;
@@ -203,6 +204,18 @@ k_key_inner_b(DevRing R, u64* __restrict__ acc, const u64* __restrict__ digits, 
         }
         const bool fp = q < kFpMaxQ;  // q-chain rows: exact FP64 products (tg_fp64.cuh)
         const double qd = fp ? R.qd[4 * m] : 0.0, qi = fp ? R.qd[4 * m + 1] : 0.0;
+        // eval-form addends (c0, c1 of a relinearisation) enter the Q rows as
+        // P * c: ModDown((acc + P c)) = ModDown(acc) + c (mod q_r)
+        const bool addq = add0 && r <= u32(level);
+        const u64 qwords = u64(level + 1) * N;
+        u64 pm = 0, pms = 0;
+        double pmd = 0, pmq = 0;
+        if (addq) {
+            pm = pmod[4 * r];
+            pms = pmod[4 * r + 1];
+            pmd = __longlong_as_double(static_cast<long long>(pmod[4 * r + 2]));
+            pmq = __longlong_as_double(static_cast<long long>(pmod[4 * r + 3]));
+        }
         for (u32 b = b0; b < b1; ++b) {
             ulonglong2 dn[NDMAX];
             if (b + 1 < b1) {
@@ -230,6 +243,14 @@ k_key_inner_b(DevRing R, u64* __restrict__ acc, const u64* __restrict__ digits, 
                         }
                     }
                 }
+                if (addq) {  // |P c| < 0.58q on top of |sum| < 3.3q
+                    const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(add0 + size_t(b) * qwords + i);
+                    const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(add1 + size_t(b) * qwords + i);
+                    s0 = __dadd_rn(s0, fp_mulmod(u2d(a0.x), pmd, pmq, qd));
+                    t0 = __dadd_rn(t0, fp_mulmod(u2d(a0.y), pmd, pmq, qd));
+                    s1 = __dadd_rn(s1, fp_mulmod(u2d(a1.x), pmd, pmq, qd));
+                    t1 = __dadd_rn(t1, fp_mulmod(u2d(a1.y), pmd, pmq, qd));
+                }
                 *reinterpret_cast<ulonglong2*>(acc + size_t(b) * words + i) = make_ulonglong2(
                     fp_canonical(fp_reduce(s0, qd, qi), qd), fp_canonical(fp_reduce(t0, qd, qi), qd));
                 *reinterpret_cast<ulonglong2*>(acc + (size_t(npolys) + b) * words + i) = make_ulonglong2(
@@ -250,6 +271,15 @@ k_key_inner_b(DevRing R, u64* __restrict__ acc, const u64* __restrict__ digits, 
                     mac128(t1, dv[k].y, ka[k].y);
                 }
             }
+            if (addq) {  // products < 2^124 each, at most 16 terms: no overflow
+                const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(add0 + size_t(b) * qwords + i);
+                const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(add1 + size_t(b) * qwords + i);
+                mac128(s0, a0.x, pm);
+                mac128(t0, a0.y, pm);
+                mac128(s1, a1.x, pm);
+                mac128(t1, a1.y, pm);
+            }
+            (void)pms;
             *reinterpret_cast<ulonglong2*>(acc + size_t(b) * words + i) =
                 make_ulonglong2(barrett128(s0.lo, s0.hi, q, rl, rh), barrett128(t0.lo, t0.hi, q, rl, rh));
             *reinterpret_cast<ulonglong2*>(acc + (size_t(npolys) + b) * words + i) =
@@ -514,7 +544,35 @@ k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restric
             }
         }
         const u32 r_end = min(rout, (blockIdx.y + 1) * rows_per_group);  // blockIdx.y = group of output rows
+        // row r's input (and addend) words are loaded one row ahead
+        u64 xn[CPT], anx[CPT];
+        auto load_row = [&](u32 r) {
+            if constexpr (CONV) {
+#pragma unroll
+                for (int cc = 0; cc < CPT; ++cc) xn[cc] = anx[cc] = 0;
+            } else if constexpr (CPT == 2) {
+                const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(src + size_t(r) * N);
+                xn[0] = t.x;
+                xn[1] = t.y;
+                if (add) {
+                    const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(add + size_t(r) * N);
+                    anx[0] = u.x;
+                    anx[1] = u.y;
+                }
+            } else {
+                xn[0] = src[size_t(r) * N];
+                if (add) anx[0] = add[size_t(r) * N];
+            }
+        };
+        if (blockIdx.y * rows_per_group < r_end) load_row(blockIdx.y * rows_per_group);
         for (u32 r = blockIdx.y * rows_per_group; r < r_end; ++r) {
+            u64 x[CPT], a[CPT];
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) {
+                x[cc] = xn[cc];
+                a[cc] = anx[cc];
+            }
+            if (r + 1 < r_end) load_row(r + 1);
             const u64 q = sq[r];
             const ulonglong2* wr = smd + size_t(r) * K;
             u64 ap[CPT], an[CPT];
@@ -534,23 +592,7 @@ k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restric
             }
             const ulonglong2 pv = sp[r];
             const u64 bias = 2 * u64(K) * q;
-            u64 o[CPT], x[CPT], a[CPT];
-            if constexpr (CONV) {
-#pragma unroll
-                for (int cc = 0; cc < CPT; ++cc) x[cc] = 0;
-            } else if constexpr (CPT == 2) {
-                const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(src + size_t(r) * N);
-                x[0] = t.x;
-                x[1] = t.y;
-                if (add) {
-                    const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(add + size_t(r) * N);
-                    a[0] = u.x;
-                    a[1] = u.y;
-                }
-            } else {
-                x[0] = src[size_t(r) * N];
-                if (add) a[0] = add[size_t(r) * N];
-            }
+            u64 o[CPT];
 #pragma unroll
             for (int cc = 0; cc < CPT; ++cc) {
                 // (x - conv) * P^-1 with conv = ap - an (mod q)
@@ -695,7 +737,7 @@ int ks_inner(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd, cons
 // acc: [2][npolys][level+1+K][N] scratch; out0/out1/add0/add1: npolys polys
 // of level+1 rows back to back.
 int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd, u32 npolys, const u64* key,
-                   int level, u64* acc, cudaStream_t s, const u64* add0, const u64* add1) {
+                   int level, u64* acc, cudaStream_t s, const u64* add0, const u64* add1, bool eval_add = false) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const size_t words = size_t(level + 1 + R.K) * R.N;
@@ -708,15 +750,21 @@ int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd
         u32 ppt = npolys;
         while (ppt > 1 && words / 2 * ((npolys + ppt - 1) / ppt) < want) ppt = (ppt + 1) / 2;
         const u32 blocks = grid_for(words / 2 * ((npolys + ppt - 1) / ppt));
-        if (nd <= 4) k_key_inner_b<4><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
-        else if (nd <= 8) k_key_inner_b<8><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
-        else if (nd <= 15) k_key_inner_b<15><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt);
+        const u64* ea0 = eval_add ? add0 : nullptr;
+        const u64* ea1 = eval_add ? add1 : nullptr;
+        const u64* pmod = g->g.md + 2 * R.K + size_t(R.K) * R.q_count * 4 + size_t(R.q_count) * 2;
+        if (nd <= 4)
+            k_key_inner_b<4><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt, ea0, ea1, pmod);
+        else if (nd <= 8)
+            k_key_inner_b<8><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt, ea0, ea1, pmod);
+        else if (nd <= 15)
+            k_key_inner_b<15><<<blocks, kThreads, 0, s>>>(R, acc, digits, nd, npolys, key, level, ppt, ea0, ea1, pmod);
         else return fail(TG_E_ARG, "[rlwe] batched key switch supports at most 15 digits");
     }
     TG_LAUNCH_CHECK();
     if (int rc = ntt_inverse_rows(ctx, acc, level, int(R.K), 2 * npolys, s)) return rc;
-    if (int rc = mod_down(g, out0, acc, level, npolys, s, add0)) return rc;
-    return mod_down(g, out1, acc + size_t(npolys) * words, level, npolys, s, add1);
+    if (int rc = mod_down(g, out0, acc, level, npolys, s, eval_add ? nullptr : add0)) return rc;
+    return mod_down(g, out1, acc + size_t(npolys) * words, level, npolys, s, eval_add ? nullptr : add1);
 }
 
 }  // namespace tg
@@ -801,6 +849,36 @@ extern "C" int tg_keyswitch_add_batch(tg_gadget* g, uint64_t* out0, uint64_t* ou
     if (rc == TG_OK)
         rc = ks_inner_batch(g, out0, out1, digits, nd, npolys, key, level, digits + size_t(npolys) * nd * words, s,
                             add0, add1);
+    cudaFreeAsync(scratch, s);
+    return rc;
+}
+
+// relinearize of a batch (rlwe.hpp:601-620) from the tensor product's eval-
+// form parts: c2 in coefficient form (ModUp source; its eval form, optional,
+// supplies the digits' own-group rows), c0/c1 in eval form are folded into
+// the accumulators' Q rows as P * c before the inverse transform, so
+// ModDown(acc + P c) = c + ModDown(acc) needs no coefficient form of c0/c1.
+extern "C" int tg_relinearize_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* c2,
+                                    const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits, int level,
+                                    const uint64_t* c0_eval, const uint64_t* c1_eval, uint32_t npolys,
+                                    void* stream) {
+    if (int rc = check_ks(g, level)) return rc;
+    if (npolys == 0) return TG_OK;
+    if (!c0_eval || !c1_eval) return fail(TG_E_ARG, "[rlwe] relinearize needs both eval-form parts");
+    tg_context* ctx = g->ctx;
+    const u32 nd = tg_gadget_digit_count(g, level);
+    if (nd > key_digits) return fail(TG_E_ARG, "[rlwe] switching key has too few digits");
+    if (nd > 15) return fail(TG_E_ARG, "[rlwe] batched key switch supports at most 15 digits");
+    DeviceGuard guard(ctx->device);
+    cudaStream_t s = as_stream(stream);
+    const size_t words = size_t(level + 1 + ctx->ring.K) * ctx->ring.N;
+    void* scratch = nullptr;
+    TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
+    u64* digits = static_cast<u64*>(scratch);
+    int rc = modup(g, digits, c2, level, s, c2_eval, npolys);
+    if (rc == TG_OK)
+        rc = ks_inner_batch(g, out0, out1, digits, nd, npolys, key, level, digits + size_t(npolys) * nd * words, s,
+                            c0_eval, c1_eval, true);
     cudaFreeAsync(scratch, s);
     return rc;
 }

@@ -60,6 +60,37 @@ __device__ __forceinline__ u64 lc_row(const DevRing& R, const LinComb& L, u32 p,
     return shoup(acc, 1, one, q);
 }
 
+// Two rows at once (r, r2 with r2 == r allowed): their term loads are
+// independent and issued together, so each thread keeps twice the loads in
+// flight (the kernel is latency-bound on HBM at one row per pass).
+__device__ __forceinline__ void lc_row2(const DevRing& R, const LinComb& L, u32 p, u32 r, u32 r2, u32 c,
+                                        bool add_here, u64& v, u64& v2) {
+    const u64 q = R.q[r], q2 = R.q[r2];
+    if (q < kFpMaxQ && q2 < kFpMaxQ) {
+        const double qd = R.qd[4 * r], qi = R.qd[4 * r + 1], qd2 = R.qd[4 * r2], qi2 = R.qd[4 * r2 + 1];
+        double acc = add_here ? u2d(L.add[r]) : 0.0, acc2 = add_here ? u2d(L.add[r2]) : 0.0;
+        const size_t o = size_t(r) * R.N + c, o2 = size_t(r2) * R.N + c;
+#pragma unroll 4
+        for (u32 t = 0; t < L.nterms; ++t) {
+            const u64* base = L.ptr[t] + p * L.pstride[t];
+            const u64 x = base[o], x2 = base[o2];
+            acc = __dadd_rn(acc, fp_mulmod(u2d(x), __longlong_as_double(static_cast<long long>(L.c[t][r])),
+                                           __longlong_as_double(static_cast<long long>(L.cs[t][r])), qd));
+            acc2 = __dadd_rn(acc2, fp_mulmod(u2d(x2), __longlong_as_double(static_cast<long long>(L.c[t][r2])),
+                                             __longlong_as_double(static_cast<long long>(L.cs[t][r2])), qd2));
+            if ((t & 7) == 7) {
+                acc = fp_reduce(acc, qd, qi);
+                acc2 = fp_reduce(acc2, qd2, qi2);
+            }
+        }
+        v = fp_canonical(fp_reduce(acc, qd, qi), qd);
+        v2 = fp_canonical(fp_reduce(acc2, qd2, qi2), qd2);
+        return;
+    }
+    v = lc_row(R, L, p, r, c, add_here);
+    v2 = lc_row(R, L, p, r2, c, add_here);
+}
+
 __global__ void __launch_bounds__(kThreads) k_lincomb(DevRing R, LinComb L, u64* __restrict__ out) {
     const u32 N = R.N, lvl = u32(L.level);
     const u32 rout = L.rescale ? lvl : lvl + 1;
@@ -69,18 +100,31 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(DevRing R, LinComb L, u64*
         const bool add_here = p < L.add_polys && (L.add_all || c == 0);
         u64* dst = out + size_t(p) * rout * N;
         if (!L.rescale) {
-            for (u32 r = 0; r <= lvl; ++r) dst[size_t(r) * N + c] = lc_row(R, L, p, r, c, add_here);
+            for (u32 r = 0; r <= lvl; r += 2) {
+                const u32 r2 = min(r + 1, lvl);
+                u64 v, v2;
+                lc_row2(R, L, p, r, r2, c, add_here, v, v2);
+                dst[size_t(r) * N + c] = v;
+                if (r2 != r) dst[size_t(r2) * N + c] = v2;
+            }
             continue;
         }
         // rescale_round (ring.hpp:493-518) of the combined poly
         const u64 last = lc_row(R, L, p, lvl, c, add_here);
-        for (u32 r = 0; r < lvl; ++r) {
-            const u64 q = R.q[r];
-            const u64* e = R.rs + (size_t(lvl) * R.q_count + r) * 4;
-            u64 t = last < q ? last : reduce64(last, q, R.ratio[2 * r], R.ratio[2 * r + 1]);
-            if (last > e[3]) t = sub_mod(t, e[0], q);
-            const u64 v = lc_row(R, L, p, r, c, add_here);
-            dst[size_t(r) * N + c] = shoup(sub_mod(v, t, q), e[1], e[2], q);
+        for (u32 r = 0; r < lvl; r += 2) {
+            const u32 r2 = min(r + 1, lvl - 1);
+            u64 v[2];
+            lc_row2(R, L, p, r, r2, c, add_here, v[0], v[1]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const u32 rr = h ? r2 : r;
+                if (h && r2 == r) break;
+                const u64 q = R.q[rr];
+                const u64* e = R.rs + (size_t(lvl) * R.q_count + rr) * 4;
+                u64 t = last < q ? last : reduce64(last, q, R.ratio[2 * rr], R.ratio[2 * rr + 1]);
+                if (last > e[3]) t = sub_mod(t, e[0], q);
+                dst[size_t(rr) * N + c] = shoup(sub_mod(v[h], t, q), e[1], e[2], q);
+            }
         }
     }
 }
