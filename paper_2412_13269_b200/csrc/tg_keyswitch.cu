@@ -763,8 +763,14 @@ int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd
     }
     TG_LAUNCH_CHECK();
     if (int rc = ntt_inverse_rows(ctx, acc, level, int(R.K), 2 * npolys, s)) return rc;
-    if (int rc = mod_down(g, out0, acc, level, npolys, s, eval_add ? nullptr : add0)) return rc;
-    return mod_down(g, out1, acc + size_t(npolys) * words, level, npolys, s, eval_add ? nullptr : add1);
+    const u64* m0 = eval_add ? nullptr : add0;
+    const u64* m1 = eval_add ? nullptr : add1;
+    const size_t qwords = size_t(level + 1) * R.N;
+    // both halves in one launch when outputs (and addends) are back to back
+    if (out1 == out0 + size_t(npolys) * qwords && (m0 ? m1 == m0 + size_t(npolys) * qwords : !m1))
+        return mod_down(g, out0, acc, level, 2 * npolys, s, m0);
+    if (int rc = mod_down(g, out0, acc, level, npolys, s, m0)) return rc;
+    return mod_down(g, out1, acc + size_t(npolys) * words, level, npolys, s, m1);
 }
 
 }  // namespace tg
