@@ -134,7 +134,15 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
     // q, fl(1/q), n_inv, fl(n_inv/q).
     {
         const size_t nt = size_t(4) * nmod * degree, nq4 = size_t(4) * nmod;
-        std::vector<double> fp(nt + nq4);
+        const u32 qc = nmod - special_count;
+        std::vector<double> fp(nt + nq4 + size_t(qc) * qc * 2);
+        // rescale in FP64: (ql mod q_r)^-1 and fl(that / q_r) per (level, row)
+        for (u32 l = 1; l < qc; ++l)
+            for (u32 r = 0; r < l; ++r) {
+                const u64 inv = h_inv_mod(moduli[l] % moduli[r], moduli[r]);
+                fp[nt + nq4 + (size_t(l) * qc + r) * 2] = double(inv);
+                fp[nt + nq4 + (size_t(l) * qc + r) * 2 + 1] = double(inv) / double(moduli[r]);
+            }
         for (u32 i = 0; i < nmod; ++i) {
             const double qd = double(moduli[i]);
             const u64* t = tables + size_t(4) * i * degree;
@@ -161,6 +169,7 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
         }
         R.twd = static_cast<const double*>(ctx->dev_fp);
         R.qd = R.twd + nt;
+        R.rsd = R.qd + nq4;
     }
     // stream-ordered pool of this context: freed blocks stay cached (no
     // release back to the driver), and a block freed on one stream is reused

@@ -44,6 +44,7 @@ struct DevRing {
     // and [nmod][4] doubles q | 1/q | n_inv | n_inv/q (see tg_fp64.cuh)
     const double* twd;
     const double* qd;
+    const double* rsd;  // [q_count][q_count][2]: (ql mod q_r)^-1, fl(. / q_r) (FP64 rescale)
     u32 int_every;  // NTT: one FP64-eligible row in int_every takes the integer path (0: none)
 };
 

@@ -25,7 +25,7 @@ inline u32 grid_for(size_t work) {
 }
 
 struct LinComb {
-    u32 nterms, nparts, rescale, add_all, add_polys;
+    u32 nterms, nparts, rescale, add_all, add_polys, all_fp;
     int level;
     const u64* ptr[TG_LINCOMB_MAX_TERMS];
     u64 pstride[TG_LINCOMB_MAX_TERMS];
@@ -58,6 +58,22 @@ __device__ __forceinline__ u64 lc_row(const DevRing& R, const LinComb& L, u32 p,
         if ((t & 7) == 7) acc = shoup_lazy(acc, 1, one, q);  // keep the lazy sum < 16q < 2^64
     }
     return shoup(acc, 1, one, q);
+}
+
+// FP64 row sum reduced to |v| <= q/2 + 1 (not canonicalised): the rescale
+// below consumes it directly.
+__device__ __forceinline__ double lc_row_fp(const DevRing& R, const LinComb& L, u32 p, u32 r, u32 c, bool add_here) {
+    const double qd = R.qd[4 * r], qi = R.qd[4 * r + 1];
+    double acc = add_here ? u2d(L.add[r]) : 0.0;
+    const size_t o = size_t(r) * R.N + c;
+#pragma unroll 4
+    for (u32 t = 0; t < L.nterms; ++t) {
+        const u64 x = L.ptr[t][p * L.pstride[t] + o];
+        acc = __dadd_rn(acc, fp_mulmod(u2d(x), __longlong_as_double(static_cast<long long>(L.c[t][r])),
+                                       __longlong_as_double(static_cast<long long>(L.cs[t][r])), qd));
+        if ((t & 7) == 7) acc = fp_reduce(acc, qd, qi);
+    }
+    return fp_reduce(acc, qd, qi);
 }
 
 // Two rows at once (r, r2 with r2 == r allowed): their term loads are
@@ -110,6 +126,31 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(DevRing R, LinComb L, u64*
             continue;
         }
         // rescale_round (ring.hpp:493-518) of the combined poly
+        if (L.all_fp) {
+            // all rows FP64: the last row's centred residue x (|x| <= (ql-1)/2)
+            // is t mod q_r as a signed integer (|x| < q_r), and
+            // out_r = (v_r - x) * ql^-1 with |v_r - x| < 1.1 q_r: one exact
+            // FP64 product per row (tg_fp64.cuh), no integer reductions
+            const double ql = R.qd[4 * lvl], hl = double(R.q[lvl] >> 1);
+            double x = lc_row_fp(R, L, p, lvl, c, add_here);
+            if (x > hl) x = __dsub_rn(x, ql);
+            if (x < -hl) x = __dadd_rn(x, ql);
+            const double* rsd = R.rsd + size_t(lvl) * R.q_count * 2;
+            for (u32 r = 0; r < lvl; r += 2) {
+                const u32 r2 = min(r + 1, lvl - 1);
+                const double v = lc_row_fp(R, L, p, r, c, add_here);
+                const double v2 = r2 != r ? lc_row_fp(R, L, p, r2, c, add_here) : 0.0;
+                const double qd = R.qd[4 * r];
+                dst[size_t(r) * N + c] =
+                    fp_canonical1(fp_mulmod(__dsub_rn(v, x), rsd[2 * r], rsd[2 * r + 1], qd), qd);
+                if (r2 != r) {
+                    const double qd2 = R.qd[4 * r2];
+                    dst[size_t(r2) * N + c] =
+                        fp_canonical1(fp_mulmod(__dsub_rn(v2, x), rsd[2 * r2], rsd[2 * r2 + 1], qd2), qd2);
+                }
+            }
+            continue;
+        }
         const u64 last = lc_row(R, L, p, lvl, c, add_here);
         for (u32 r = 0; r < lvl; r += 2) {
             const u32 r2 = min(r + 1, lvl - 1);
@@ -125,6 +166,56 @@ __global__ void __launch_bounds__(kThreads) k_lincomb(DevRing R, LinComb L, u64*
                 if (last > e[3]) t = sub_mod(t, e[0], q);
                 dst[size_t(rr) * N + c] = shoup(sub_mod(v[h], t, q), e[1], e[2], q);
             }
+        }
+    }
+}
+
+// All rows FP64 and at most NT terms (the ladder steps and most combination
+// steps): per-term base pointers hoisted out of the row loop and the term
+// loop unrolled at compile time, so a row costs NT loads and NT exact FP64
+// products instead of re-deriving every address from the parameter block.
+template <int NT>
+__global__ void __launch_bounds__(kThreads) k_lincomb_fp(DevRing R, LinComb L, u64* __restrict__ out) {
+    const u32 N = R.N, lvl = u32(L.level);
+    const u32 rout = L.rescale ? lvl : lvl + 1;
+    const u64 total = u64(L.nparts) * N;
+    for (u64 i = blockIdx.x * u64(kThreads) + threadIdx.x; i < total; i += u64(gridDim.x) * kThreads) {
+        const u32 p = u32(i >> R.logN), c = u32(i & (N - 1));
+        const bool add_here = p < L.add_polys && (L.add_all || c == 0);
+        const u64* base[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) base[t] = u32(t) < L.nterms ? L.ptr[t] + p * L.pstride[t] + c : nullptr;
+        auto row = [&](u32 r) {
+            const double qd = R.qd[4 * r], qi = R.qd[4 * r + 1];
+            u64 x[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+                if (u32(t) < L.nterms) x[t] = base[t][size_t(r) * N];
+            double acc = add_here ? u2d(L.add[r]) : 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                if (u32(t) < L.nterms)
+                    acc = __dadd_rn(acc, fp_mulmod(u2d(x[t]), __longlong_as_double(static_cast<long long>(L.c[t][r])),
+                                                   __longlong_as_double(static_cast<long long>(L.cs[t][r])), qd));
+                if ((t & 7) == 7) acc = fp_reduce(acc, qd, qi);
+            }
+            return fp_reduce(acc, qd, qi);  // |.| <= q/2 + 1
+        };
+        u64* dst = out + size_t(p) * rout * N + c;
+        if (!L.rescale) {
+            for (u32 r = 0; r <= lvl; ++r) dst[size_t(r) * N] = fp_canonical(row(r), R.qd[4 * r]);
+            continue;
+        }
+        // rescale_round (ring.hpp:493-518): centred last row, then
+        // (v_r - x) * ql^-1 per row (see k_lincomb)
+        const double ql = R.qd[4 * lvl], hl = double(R.q[lvl] >> 1);
+        double x = row(lvl);
+        if (x > hl) x = __dsub_rn(x, ql);
+        if (x < -hl) x = __dadd_rn(x, ql);
+        const double* rsd = R.rsd + size_t(lvl) * R.q_count * 2;
+        for (u32 r = 0; r < lvl; ++r) {
+            const double qd = R.qd[4 * r];
+            dst[size_t(r) * N] = fp_canonical1(fp_mulmod(__dsub_rn(row(r), x), rsd[2 * r], rsd[2 * r + 1], qd), qd);
         }
     }
 }
@@ -177,10 +268,18 @@ extern "C" int tg_lincomb_batch(tg_context* ctx, uint64_t* out, uint32_t nterms,
         }
     }
     for (int r = 0; r <= level; ++r) L.add[r] = add_per_row ? add_per_row[r] % ctx->h_q[r] : 0;
+    L.all_fp = 1;
+    for (int r = 0; r <= level; ++r) L.all_fp &= ctx->h_q[r] < kFpMaxQ ? 1u : 0u;
     const double rows = double(level + 1);
     ProfScope prof(ctx, TG_OP_LINCOMB, 8.0 * nparts * R.N * (rows * nterms + (rescale ? rows - 1 : rows)),
                    as_stream(stream));
-    k_lincomb<<<grid_for(size_t(nparts) * R.N), kThreads, 0, as_stream(stream)>>>(R, L, out);
+    const u32 grid = grid_for(size_t(nparts) * R.N);
+    cudaStream_t st = as_stream(stream);
+    if (L.all_fp && nterms <= 1) k_lincomb_fp<1><<<grid, kThreads, 0, st>>>(R, L, out);
+    else if (L.all_fp && nterms <= 2) k_lincomb_fp<2><<<grid, kThreads, 0, st>>>(R, L, out);
+    else if (L.all_fp && nterms <= 4) k_lincomb_fp<4><<<grid, kThreads, 0, st>>>(R, L, out);
+    else if (L.all_fp && nterms <= 8) k_lincomb_fp<8><<<grid, kThreads, 0, st>>>(R, L, out);
+    else k_lincomb<<<grid, kThreads, 0, st>>>(R, L, out);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

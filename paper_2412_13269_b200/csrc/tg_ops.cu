@@ -207,14 +207,23 @@ __global__ void k_rescale(DevRing R, u64* out, const u64* in, int level, u32 npo
         const u64* src = in + p * (lvl + 1) * N;
         u64* dst = out + p * lvl * N;
         const u64 last = src[size_t(lvl) * N + c];
+        const u64 hl = ql >> 1;
+        // centred last residue as a signed FP64 integer (FP64 rows below)
+        const double x = last > hl ? __dsub_rn(u2d(last), u2d(ql)) : u2d(last);
         for (u32 r = 0; r < lvl; ++r) {
             const u64 q = R.q[r];
+            if (q < kFpMaxQ && ql < kFpMaxQ) {  // (v - x) * ql^-1, |v - x| < 1.1q: one exact FP64 product
+                const double qd = R.qd[4 * r];
+                const double* rsd = R.rsd + (size_t(lvl) * R.q_count + r) * 2;
+                dst[size_t(r) * N + c] =
+                    fp_canonical1(fp_mulmod(__dsub_rn(u2d(src[size_t(r) * N + c]), x), rsd[0], rsd[1], qd), qd);
+                continue;
+            }
             const u64* e = R.rs + (size_t(lvl) * R.q_count + r) * 4;
             u64 t = last < q ? last : reduce64(last, q, R.ratio[2 * r], R.ratio[2 * r + 1]);
             if (last > e[3]) t = sub_mod(t, e[0], q);  // centered remainder
             dst[size_t(r) * N + c] = shoup(sub_mod(src[size_t(r) * N + c], t, q), e[1], e[2], q);
         }
-        (void)ql;
     }
 }
 

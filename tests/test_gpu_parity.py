@@ -306,3 +306,41 @@ def test_ntt_fp64_extreme_inputs(G, R, gpu_available, N):
         eg = G.Poly.from_numpy(rg, a, lv, G.Form.eval)
         er = R.Poly.from_numpy(rr, a, lv, R.Form.eval)
         assert_poly_equal(G.ntt_transform(eg, G.Form.coeff), R.ntt_transform(er, R.Form.coeff), f"inv {name}")
+
+
+@pytest.mark.parametrize("N", [1024])
+def test_fp64_elementwise_extreme_inputs(G, R, gpu_available, N):
+    """FP64 products and the FP64 rescale at their bounds: primes nearest 2^50
+    and the largest NTT primes below 1.2 * 2^50 (in both orders, so the
+    dropped modulus is larger and smaller than the kept ones), residues 0,
+    1, q-1, floor(q/2) and floor(q/2)+1 (the centring boundary of
+    rescale_round), vs the reference."""
+    bound = 1351079888211148
+    near = list(R.find_ntt_primes(50, 2, 2 * N))
+    top, c = [], bound - bound % (2 * N) + 1
+    while len(top) < 2:
+        if c < bound and _is_prime(c):
+            top.append(c)
+        c -= 2 * N
+    for primes in (near + top, top + near, [top[0], near[0], top[1], near[1]]):
+        rg, rr = G.RingParams(N, primes, 0), R.RingParams(N, primes, 0)
+        lv = len(primes) - 1
+        specials = lambda q: np.array([0, 1, q - 1, q // 2, q // 2 + 1, q - 2, 2, q // 2 - 1], dtype=np.uint64)
+        a = np.zeros((len(primes), N), dtype=np.uint64)
+        b = np.zeros((len(primes), N), dtype=np.uint64)
+        g = np.random.Generator(np.random.PCG64(N + len(primes)))
+        for r, q in enumerate(primes):
+            sp = specials(q)
+            a[r] = np.resize(sp, N)
+            b[r] = np.resize(np.roll(sp, r + 1), N)
+            a[r, 512:] = g.integers(0, q, N - 512, dtype=np.uint64)
+        # last row sweeps the centring boundary against every other row's pattern
+        ql = primes[-1]
+        a[-1, :8 * 8] = np.repeat(specials(ql), 8)
+        pg, pr = G.Poly.from_numpy(rg, a, lv, G.Form.eval), R.Poly.from_numpy(rr, a, lv, R.Form.eval)
+        qg, qr = G.Poly.from_numpy(rg, b, lv, G.Form.eval), R.Poly.from_numpy(rr, b, lv, R.Form.eval)
+        pg.mul_pointwise_inplace(qg)
+        pr.mul_pointwise_inplace(qr)
+        assert_poly_equal(pg, pr, "mul_pointwise extremes")
+        pg, pr = G.Poly.from_numpy(rg, a, lv, G.Form.coeff), R.Poly.from_numpy(rr, a, lv, R.Form.coeff)
+        assert_poly_equal(G.rescale_round(pg), R.rescale_round(pr), "rescale_round extremes")
