@@ -22,7 +22,7 @@ try:
 except ImportError as e:  # pragma: no cover - exercised only on a broken build
     raise ImportError(
         "paper_2412_13269_b200: native extension not built "
-        "(run `python -m paper_2412_13269_b200.build`): " + str(e)) from e
+        "(run `python __graft_entry__.py build`): " + str(e)) from e
 
 
 def load_c_abi() -> ctypes.CDLL:
