@@ -11,6 +11,7 @@
 #include <cstdlib>
 
 #include "tg_internal.cuh"
+#include "tg_fp64.cuh"
 
 namespace tg {
 
@@ -457,7 +458,38 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
         g->g.lazy_moddown = (u128(4 * K + 2) * qmax) < (u128(1) << 64);
         g->g.lazy_modup = (u128(2 * gs) * allmax) < (u128(1) << 64);
     }
-    size_t words = src.size() + conv.size() + md.size();
+    // FP64 ModDown tables (k_mod_down_fp), used when every modulus is below
+    // the FP64 bound: [K][4] (p_s, fl(c_s/p_s), c_s, floor(p_s/2));
+    // [nq][K][2] (w, fl(w/q_r)), w = -(P/p_s) P^-1 mod q_r;
+    // [nq][4] (P^-1 mod q_r, fl(./q_r), q_r, fl(1/q_r)).
+    std::vector<double> mdf(size_t(K) * 4 + size_t(nq) * K * 2 + size_t(nq) * 4, 0.0);
+    g->g.fp_moddown = K > 0;
+    for (u32 t = 0; t < nmod; ++t) g->g.fp_moddown &= mod[t] < kFpMaxQ;
+    if (const char* e = getenv("TG_INT_MODDOWN"); e && *e == '1') g->g.fp_moddown = false;  // A/B experiments
+    if (g->g.fp_moddown) {
+        for (u32 s = 0; s < K; ++s) {
+            const u64 ps = mod[nq + s], c = md[2 * s];
+            mdf[4 * s] = double(ps);
+            mdf[4 * s + 1] = double(c) / double(ps);
+            mdf[4 * s + 2] = double(c);
+            mdf[4 * s + 3] = double(ps / 2);
+        }
+        for (u32 r = 0; r < nq; ++r) {
+            const u64 q = mod[r], pinv = md[2 * K + size_t(K) * nq * 4 + size_t(r) * 2];
+            for (u32 s = 0; s < K; ++s) {
+                const u64 ws = md[2 * K + (size_t(s) * nq + r) * 4];
+                const u64 w = h_mul_mod(ws ? q - ws : 0, pinv, q);
+                mdf[4 * K + (size_t(r) * K + s) * 2] = double(w);
+                mdf[4 * K + (size_t(r) * K + s) * 2 + 1] = double(w) / double(q);
+            }
+            double* e = &mdf[4 * K + size_t(nq) * K * 2 + size_t(r) * 4];
+            e[0] = double(pinv);
+            e[1] = double(pinv) / double(q);
+            e[2] = double(q);
+            e[3] = 1.0 / double(q);
+        }
+    }
+    size_t words = src.size() + conv.size() + md.size() + mdf.size();
     cudaError_t e = cudaMalloc(&g->dev_block, words * 8);
     if (e != cudaSuccess) {
         delete g;
@@ -467,9 +499,11 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
     g->g.src = p;
     g->g.conv = p + src.size();
     g->g.md = p + src.size() + conv.size();
+    g->g.mdf = reinterpret_cast<double*>(g->g.md + md.size());
     e = cudaMemcpy(g->g.src, src.data(), src.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g->g.conv, conv.data(), conv.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !md.empty()) e = cudaMemcpy(g->g.md, md.data(), md.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !mdf.empty()) e = cudaMemcpy(g->g.mdf, mdf.data(), mdf.size() * 8, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         cudaFree(g->dev_block);
         delete g;

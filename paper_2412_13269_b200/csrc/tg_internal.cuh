@@ -167,7 +167,9 @@ struct GadgetDev {
     u64* conv;  // [ngroups][group_size][group_size][nmod][2]
     u64* md;    // ModDown: [K][2] (P/p_s)^-1 mod p_s; [K][q_count][4] +-(P/p_s) mod q_r; [q_count][2] P^-1 mod q_r;
                 // [q_count][4] P mod q_r (u64, Shoup, FP64 value, FP64 quotient)
+    double* mdf;  // FP64 ModDown (all moduli < kFpMaxQ): see k_mod_down_fp
     bool lazy_modup, lazy_moddown;  // lazy sums provably fit a word (checked on the host)
+    bool fp_moddown;                // every modulus below the FP64 bound: ModDown on the FP64 pipe
     u32 base2_bits;                 // 0: RNS digits; else balanced base-2^b sub-digits (group_size 1)
 };
 

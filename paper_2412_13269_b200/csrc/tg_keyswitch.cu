@@ -605,6 +605,99 @@ k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restric
     }
 }
 
+// FP64 ModDown (every special and q-chain prime below kFpMaxQ, tg_fp64.cuh):
+// y_s = centered([x_s (P/p_s)^-1]_{p_s}) exactly as doubles, then
+// out_r = x_r P^-1 + sum_s y_s (-(P/p_s) P^-1 mod q_r)  (mod q_r), which is
+// (x_r - conv_r) P^-1 with the same canonical residue as mod_down_p
+// (rlwe.hpp:579-589). Bounds: every product has |b| <= max(q, p/2) and
+// b wq >= -0.6 * 2^50, so |term| <= 0.58 q; sums are reduced every 8 terms
+// (|sum| <= 8 * 0.58 q + q/2 < 2^53).
+// Host tables (G.mdf): [K][4] (p_s, fl(c_s/p_s), c_s, floor(p_s/2)) with
+// c_s = (P/p_s)^-1 mod p_s; [nq][K][2] (w, fl(w/q_r)) with
+// w = -(P/p_s) P^-1 mod q_r; [nq][4] (P^-1 mod q_r, fl(./q_r), q_r, fl(1/q_r)).
+template <int KMAX>
+__global__ void __launch_bounds__(256)
+k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict__ in, int level, u32 npolys,
+              const u64* __restrict__ addend, u32 rows_per_group) {
+    const u32 N = R.N, K = R.K, nq = R.q_count, lvl = u32(level);
+    const u32 rin = lvl + 1 + K, rout = lvl + 1;
+    const double* ys_t = G.mdf;                         // [K][4]
+    const double* w_rs = G.mdf + 4 * K;                 // [nq][K][2]
+    const double* p_r = w_rs + size_t(nq) * K * 2;      // [nq][4]
+    extern __shared__ double2 smf[];                    // [rout][K] (w, wq), then [rout][2] (pinv, pinvq | q, qi)
+    double2* sp = smf + size_t(rout) * K;
+    for (u32 e = threadIdx.x; e < rout * K; e += blockDim.x) smf[e] = make_double2(w_rs[2 * e], w_rs[2 * e + 1]);
+    for (u32 e = threadIdx.x; e < 2 * rout; e += blockDim.x) sp[e] = make_double2(p_r[2 * e], p_r[2 * e + 1]);
+    __syncthreads();
+    const u32 per_poly = N / 2;
+    const u64 total = u64(npolys) * per_poly;
+    for (u64 idx = blockIdx.x * u64(blockDim.x) + threadIdx.x; idx < total; idx += u64(gridDim.x) * blockDim.x) {
+        const u32 p = u32(idx / per_poly);
+        const u32 c0 = u32(idx - u64(p) * per_poly) * 2;
+        const u64* src = in + size_t(p) * rin * N + c0;
+        u64* dst = out + size_t(p) * rout * N + c0;
+        const u64* add = addend ? addend + size_t(p) * rout * N + c0 : nullptr;
+        double y[KMAX][2];
+#pragma unroll
+        for (int s = 0; s < KMAX; ++s) {
+            if (u32(s) < K) {
+                const double ps = ys_t[4 * s], cq = ys_t[4 * s + 1], cw = ys_t[4 * s + 2], half = ys_t[4 * s + 3];
+                const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(src + size_t(lvl + 1 + s) * N);
+                const u64 xs[2] = {t.x, t.y};
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    double v = fp_mulmod(u2d(xs[cc]), cw, cq, ps);  // |v| <= 0.58 p
+                    if (v < 0) v = __dadd_rn(v, ps);                 // canonical [0, p)
+                    if (v > half) v = __dsub_rn(v, ps);              // to_centered (common.hpp:84-86)
+                    y[s][cc] = v;
+                }
+            }
+        }
+        const u32 r_end = min(rout, (blockIdx.y + 1) * rows_per_group);
+        u64 xn[2] = {0, 0}, anx[2] = {0, 0};
+        auto load_row = [&](u32 r) {
+            const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(src + size_t(r) * N);
+            xn[0] = t.x;
+            xn[1] = t.y;
+            if (add) {
+                const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(add + size_t(r) * N);
+                anx[0] = u.x;
+                anx[1] = u.y;
+            }
+        };
+        if (blockIdx.y * rows_per_group < r_end) load_row(blockIdx.y * rows_per_group);
+        for (u32 r = blockIdx.y * rows_per_group; r < r_end; ++r) {
+            const u64 x[2] = {xn[0], xn[1]}, a[2] = {anx[0], anx[1]};
+            if (r + 1 < r_end) load_row(r + 1);
+            const double2 pv = sp[2 * r], qv = sp[2 * r + 1];
+            const double q = qv.x, qi = qv.y;
+            const double2* wr = smf + size_t(r) * K;
+            double acc[2];
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) acc[cc] = fp_mulmod(u2d(x[cc]), pv.x, pv.y, q);
+#pragma unroll
+            for (int s = 0; s < KMAX; ++s) {
+                if (u32(s) < K) {
+                    const double2 w = wr[s];
+#pragma unroll
+                    for (int cc = 0; cc < 2; ++cc) {
+                        acc[cc] = __dadd_rn(acc[cc], fp_mulmod(y[s][cc], w.x, w.y, q));
+                        if ((s & 7) == 6 && u32(s + 1) < K) acc[cc] = fp_reduce(acc[cc], q, qi);
+                    }
+                }
+            }
+            u64 o[2];
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                double v = fp_reduce(acc[cc], q, qi);  // |v| <= q/2 + 1
+                if (add) v = __dadd_rn(v, u2d(a[cc]));
+                o[cc] = fp_canonical(v, q);
+            }
+            *reinterpret_cast<ulonglong2*>(dst + size_t(r) * N) = make_ulonglong2(o[0], o[1]);
+        }
+    }
+}
+
 // Output-row groups so that about 1024 threads per SM are in flight.
 inline u32 row_groups(u64 threads, u32 rows, int sms) {
     const u64 want = u64(sms) * 1024;
@@ -699,13 +792,28 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
     return ntt_forward_oop(ctx, digits, digits, level, int(R.K), nd * npolys, s, skip);
 }
 
+template <int KMAX>
+void launch_mod_down_fp(const DevRing& R, const GadgetDev& G, int sms, u64* out, const u64* in, int level,
+                        u32 npolys, const u64* addend, cudaStream_t s) {
+    const u32 rout = u32(level) + 1;
+    const size_t smem = size_t(rout) * R.K * 16 + size_t(rout) * 32;
+    const u64 work = u64(npolys) * R.N / 2;
+    const u32 blocks = u32(std::min<u64>((work + 255) / 256, u64(sms) * 8));
+    const u32 groups = row_groups(u64(blocks) * 256, rout, sms);
+    const u32 rpg = (rout + groups - 1) / groups;
+    k_mod_down_fp<KMAX><<<dim3(blocks, (rout + rpg - 1) / rpg), 256, smem, s>>>(R, G, out, in, level, npolys, addend,
+                                                                               rpg);
+}
+
 int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaStream_t s,
              const u64* addend = nullptr) {
     const DevRing& R = g->ctx->ring;
     ProfScope prof(g->ctx, TG_OP_MOD_DOWN, 8.0 * R.N * npolys * (2.0 * (level + 1) + R.K + (addend ? level + 1 : 0)), s);
     const GadgetDev& G = g->g;
     const int sms = g->ctx->sms;
-    if (G.lazy_moddown && R.K <= 4) launch_mod_down_v<4, 2>(R, G, sms, out, in, level, npolys, addend, s);
+    if (G.fp_moddown && R.K <= 8) launch_mod_down_fp<8>(R, G, sms, out, in, level, npolys, addend, s);
+    else if (G.fp_moddown && R.K <= 16) launch_mod_down_fp<16>(R, G, sms, out, in, level, npolys, addend, s);
+    else if (G.lazy_moddown && R.K <= 4) launch_mod_down_v<4, 2>(R, G, sms, out, in, level, npolys, addend, s);
     else if (G.lazy_moddown && R.K <= 8) launch_mod_down_v<8, 2>(R, G, sms, out, in, level, npolys, addend, s);
     else if (G.lazy_moddown && R.K <= 16) launch_mod_down_v<16, 1>(R, G, sms, out, in, level, npolys, addend, s);
     else k_mod_down<<<grid_for(size_t(npolys) * R.N), kThreads, 0, s>>>(R, G, out, in, level, npolys, addend);

@@ -54,7 +54,7 @@ CONFIGS = {
     2: Spec("config2-linear-score", N=1 << 15, nq=4, q_bits=40, q0_bits=60, K=1, sp_bits=60, group=4, h=192,
             delta_log2=40, n_cts=4, records=1 << 16, seed=0xC0F2),
     # configs[2]: private threshold count, 2^17 records, (15,15,27)
-    3: Spec("config3-threshold-count", N=1 << 16, nq=21, q_bits=50, K=6, sp_bits=60, group=7, h=192,
+    3: Spec("config3-threshold-count", N=1 << 16, nq=21, q_bits=50, K=7, sp_bits=50, group=7, h=192,
             delta_log2=50, degrees=(15, 15, 27), alpha=8, epsilon=0.0, norm=1.0, n_cts=4, records=1 << 17,
             seed=0xC0F3),
     # configs[3]: full TETRIS statement, 2^18 records: three private thresholds
@@ -63,13 +63,13 @@ CONFIGS = {
     # thresholds take 17 from L (risk score: from L-1 after its rescale), two
     # AND products + the flag product take 3 more -> count at level L-20 = 1
     # (two limbs for decoding, ckks.hpp:121-134) with L = 21.
-    4: Spec("config4-tetris-statement", N=1 << 16, nq=22, q_bits=50, K=6, sp_bits=60, group=7, h=192,
+    4: Spec("config4-tetris-statement", N=1 << 16, nq=22, q_bits=50, K=7, sp_bits=50, group=7, h=192,
             delta_log2=50, degrees=(15, 15, 27), alpha=8, epsilon=0.0, norm=1.0, n_cts=8, records=1 << 18,
             seed=0xC0F4),
     # configs[4]: scale-out stress, 2^20 records (32 record blocks), three
     # degree-63 stages (levels_required 22), L = 28, dnum = 3 (group 10:
     # 10 x 50-bit digits under P = 9 x 60-bit specials). Count at level 3.
-    5: Spec("config5-stress", N=1 << 16, nq=29, q_bits=50, K=9, sp_bits=60, group=10, h=192,
+    5: Spec("config5-stress", N=1 << 16, nq=29, q_bits=50, K=10, sp_bits=50, group=10, h=192,
             delta_log2=50, degrees=(63, 63, 63), alpha=13, epsilon=0.0, norm=1.0, n_cts=32, records=1 << 20,
             seed=0xC0F5),
 }

@@ -29,9 +29,10 @@ def main():
     ap.add_argument("--levels", default="20,10")
     ap.add_argument("--batch", type=int, default=1, help="polys per NTT launch")
     ap.add_argument("--ops", default="ntt,intt,relin,rescale")
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--bsizes", default="1,2,4,8,16,32", help="poly counts of the batch op")
     a = ap.parse_args()
-    spec = W.CONFIGS[3]
+    spec = W.CONFIGS[a.config]
     S = W.make_context(G, spec)
     ring = S.ring
     ext = torch.cuda.ExternalStream(ring.stream_handle())
@@ -89,6 +90,26 @@ def main():
             timeit(f"mul_relin_l{lvl}", lambda: S.ev.mul_relin(x, x, S.keys))
         if "rescale" in a.ops:
             timeit(f"rescale_l{lvl}", lambda: S.ev.rescale(x), 8 * spec.N * 2 * (2 * lvl + 1))
+        if "relinb" in a.ops:  # batched (8 record blocks, part-major stack) mul_relin + rescale, per class
+            xs = []
+            for b in range(8):
+                c = G.Ciphertext()
+                c.parts = [G.sample_uniform(ring, lvl, 0, rng.split(100 + 2 * b + i)) for i in range(2)]
+                c.scale, c.domain, c.sk_id = spec.delta, G.Domain.slots, S.sk.id()
+                xs.append(c)
+            xb = G.stack_ciphertexts(xs)
+            timeit(f"mul_relin_rescale_batch8_l{lvl}", lambda: S.ev.rescale(S.ev.mul_relin(xb, xb, S.keys)))
+            G.profile_enable(ring, True)
+            for _ in range(5):
+                S.ev.rescale(S.ev.mul_relin(xb, xb, S.keys))
+            ring.synchronize()
+            pr = G.profile_read(ring)
+            G.profile_enable(ring, False)
+            tot = sum(v[0] for v in pr.values()) / 5
+            for k, v in sorted(pr.items(), key=lambda kv: -kv[1][0]):
+                if v[1]:
+                    print(f"  batch8 l{lvl} {k}: {v[0] / 5 * 1e3:.1f} us ({v[0] / 5 / tot * 100:.0f}%), launches {v[1] // 5}, "
+                          f"{v[2] / v[1] / (v[0] / v[1] / 1e3) / 1e9:.0f} GB/s", flush=True)
         if "prof" in a.ops:
             G.profile_enable(ring, True)
             for _ in range(5):
