@@ -254,6 +254,15 @@ int ntt_forward_oop(tg_context* ctx, u64* dst, const u64* src, int level, int ns
                     u32 skip_gs = 0, u32 row0 = 0, u32 nrows = 0);
 int ntt_inverse_oop(tg_context* ctx, u64* dst, const u64* src, int level, int nspecial, u32 npolys, cudaStream_t s,
                     u32 row0 = 0, u32 nrows = 0);
+// Fused key-switch core (tg_ks_fused.cuh): usable when every modulus takes
+// the FP64 path and N has a warp plan (2^14..2^16). The digits hold the
+// forward column phase's output (ntt_forward_cols); acc receives both
+// accumulators after the inverse chunk phase (finish with ntt_inverse_cols).
+bool ks_fused_ok(const tg_context* ctx);
+int ntt_forward_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s, u32 skip_gs);
+int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s);
+int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key, int level,
+                    u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s);
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {

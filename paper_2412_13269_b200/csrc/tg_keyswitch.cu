@@ -756,7 +756,7 @@ __global__ void k_mod_down_finish(DevRing R, GadgetDev G, u64* __restrict__ out,
 // digits [npolys][nd][level+1+K][N], then one batched forward NTT of all
 // digits (own-group rows skipped when the eval form d_eval is supplied).
 int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, const u64* d_eval = nullptr,
-          u32 npolys = 1) {
+          u32 npolys = 1, bool cols_only = false) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const u32 nd = tg_gadget_digit_count(g, level);
@@ -789,6 +789,7 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
     }
     TG_LAUNCH_CHECK();
     const u32 skip = d_eval ? (g->g.group_size | (npolys > 1 ? nd << 16 : 0u)) : 0u;
+    if (cols_only) return ntt_forward_cols(ctx, digits, level, int(R.K), nd * npolys, s, skip);
     return ntt_forward_oop(ctx, digits, digits, level, int(R.K), nd * npolys, s, skip);
 }
 
@@ -881,6 +882,35 @@ int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd
     return mod_down(g, out1, acc + size_t(npolys) * words, level, npolys, s, m1);
 }
 
+// Batched key switch through the fused core (ks_fused_ok): ModUp base
+// conversion + forward column phase of the digits, kw_ks_chunks (digits'
+// forward chunk phase, key inner product, accumulators' inverse chunk
+// phase), inverse column phase, ModDown(+add). scratch: npolys*(nd+2) polys
+// of level+1+K rows (digits, then both accumulators).
+int ks_fused_batch(tg_gadget* g, u64* out0, u64* out1, const u64* d, const u64* d_eval, u32 nd, u32 npolys,
+                   const u64* key, int level, u64* scratch, cudaStream_t s, const u64* add0, const u64* add1,
+                   bool eval_add) {
+    tg_context* ctx = g->ctx;
+    const DevRing& R = ctx->ring;
+    const size_t words = size_t(level + 1 + R.K) * R.N;
+    u64* digits = scratch;
+    u64* acc = scratch + size_t(npolys) * nd * words;
+    if (int rc = modup(g, digits, d, level, s, d_eval, npolys, true)) return rc;
+    const u64* pmod = g->g.md + 2 * R.K + size_t(R.K) * R.q_count * 4 + size_t(R.q_count) * 2;
+    const u32 own = (d_eval && !g->g.base2_bits) ? g->g.group_size : 0u;
+    if (int rc = ks_fused_chunks(ctx, acc, digits, nd, npolys, key, level, own, eval_add ? add0 : nullptr,
+                                 eval_add ? add1 : nullptr, pmod, s))
+        return rc;
+    if (int rc = ntt_inverse_cols(ctx, acc, level, int(R.K), 2 * npolys, s)) return rc;
+    const u64* m0 = eval_add ? nullptr : add0;
+    const u64* m1 = eval_add ? nullptr : add1;
+    const size_t qwords = size_t(level + 1) * R.N;
+    if (out1 == out0 + size_t(npolys) * qwords && (m0 ? m1 == m0 + size_t(npolys) * qwords : !m1))
+        return mod_down(g, out0, acc, level, 2 * npolys, s, m0);
+    if (int rc = mod_down(g, out0, acc, level, npolys, s, m0)) return rc;
+    return mod_down(g, out1, acc + size_t(npolys) * words, level, npolys, s, m1);
+}
+
 }  // namespace tg
 
 using namespace tg;
@@ -939,8 +969,14 @@ extern "C" int tg_keyswitch_add(tg_gadget* g, uint64_t* out0, uint64_t* out1, co
     void* scratch = nullptr;
     TG_CUDA(cudaMallocFromPoolAsync(&scratch, (nd + 2) * words * 8, ctx->pool, s));
     u64* digits = static_cast<u64*>(scratch);
-    int rc = modup(g, digits, d, level, s, d_eval);
-    if (rc == TG_OK) rc = ks_inner(g, out0, out1, digits, nd, key, level, digits + size_t(nd) * words, s, add0, add1);
+    int rc;
+    if (ks_fused_ok(ctx)) {
+        rc = ks_fused_batch(g, out0, out1, d, d_eval, nd, 1, key, level, digits, s, add0, add1, false);
+    } else {
+        rc = modup(g, digits, d, level, s, d_eval);
+        if (rc == TG_OK)
+            rc = ks_inner(g, out0, out1, digits, nd, key, level, digits + size_t(nd) * words, s, add0, add1);
+    }
     cudaFreeAsync(scratch, s);
     return rc;
 }
@@ -959,10 +995,15 @@ extern "C" int tg_keyswitch_add_batch(tg_gadget* g, uint64_t* out0, uint64_t* ou
     void* scratch = nullptr;
     TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
     u64* digits = static_cast<u64*>(scratch);
-    int rc = modup(g, digits, d, level, s, d_eval, npolys);
-    if (rc == TG_OK)
-        rc = ks_inner_batch(g, out0, out1, digits, nd, npolys, key, level, digits + size_t(npolys) * nd * words, s,
-                            add0, add1);
+    int rc;
+    if (ks_fused_ok(ctx)) {
+        rc = ks_fused_batch(g, out0, out1, d, d_eval, nd, npolys, key, level, digits, s, add0, add1, false);
+    } else {
+        rc = modup(g, digits, d, level, s, d_eval, npolys);
+        if (rc == TG_OK)
+            rc = ks_inner_batch(g, out0, out1, digits, nd, npolys, key, level, digits + size_t(npolys) * nd * words,
+                                s, add0, add1);
+    }
     cudaFreeAsync(scratch, s);
     return rc;
 }
@@ -989,10 +1030,15 @@ extern "C" int tg_relinearize_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1
     void* scratch = nullptr;
     TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
     u64* digits = static_cast<u64*>(scratch);
-    int rc = modup(g, digits, c2, level, s, c2_eval, npolys);
-    if (rc == TG_OK)
-        rc = ks_inner_batch(g, out0, out1, digits, nd, npolys, key, level, digits + size_t(npolys) * nd * words, s,
-                            c0_eval, c1_eval, true);
+    int rc;
+    if (ks_fused_ok(ctx)) {
+        rc = ks_fused_batch(g, out0, out1, c2, c2_eval, nd, npolys, key, level, digits, s, c0_eval, c1_eval, true);
+    } else {
+        rc = modup(g, digits, c2, level, s, c2_eval, npolys);
+        if (rc == TG_OK)
+            rc = ks_inner_batch(g, out0, out1, digits, nd, npolys, key, level, digits + size_t(npolys) * nd * words,
+                                s, c0_eval, c1_eval, true);
+    }
     cudaFreeAsync(scratch, s);
     return rc;
 }

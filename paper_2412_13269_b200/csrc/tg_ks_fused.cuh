@@ -1,0 +1,152 @@
+// Fused key-switch core (included by tg_ntt.cu after tg_ntt_warp.cuh, inside
+// the anonymous namespace). Used when every modulus of the ring takes the
+// FP64 path (tg_fp64.cuh).
+//
+// KeyContext::ks_inner (rlwe.hpp:501-540) after ModUp is: forward NTT of every
+// digit (rlwe.hpp:137), acc_{0,1} = sum_i digit_i * key_{b,a}[i] (eval form,
+// rlwe.hpp:514-536), inverse NTT of both accumulators (rlwe.hpp:537-538).
+// Both transforms are four-step (tg_ntt_warp.cuh): the forward's second phase
+// and the inverse's first phase work on the same contiguous M-word chunks of
+// one row, and the inner product is pointwise. So one kernel per (row r,
+// chunk block) takes the digits straight from the forward column phase,
+// finishes their transform, multiplies by the key chunk, accumulates, and
+// runs the accumulators' first inverse phase: neither the eval-form digits
+// nor the eval-form accumulators go through HBM, and the separate inner-
+// product pass disappears. The inverse column phase (N^-1) follows as usual.
+//
+// Digits' own-group rows copied in eval form by ModUp (d_eval given; the
+// NTT's skip rule) are read as they are. Relinearisation's eval-form c0/c1
+// enter the Q rows as P * c (see tg_relinearize_batch). Every product is an
+// exact FP64 modular product; canonical residues are identical to the
+// unfused path's.
+//
+// Bounds (tg_fp64.cuh): transformed digits |v| <= q/2 + 1, own rows [0, q);
+// fp_mulmod_qi with |a| <= q/2 + 1, b in [0, q): |term| < 0.81q; sums reduced
+// every 4 digits: |sum| < q/2 + 1 + 4 * 0.81q (+ 0.58q for P * c) < 2^53.
+
+template <int E>
+constexpr size_t ks_chunk_smem() {  // two exchange columns per warp + forward and inverse chunk twiddles
+    return size_t(8) * (16 * WGeo<E>::CS + 4 * WGeo<E>::TW_CHUNK);
+}
+
+template <int E>
+__global__ void __launch_bounds__(256, 2)
+kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb, const u64* key, int level,
+             u32 logN1, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod) {
+    using Gm = WGeo<E>;
+    extern __shared__ u64 dyn[];
+    u64* swf = dyn + 16 * Gm::CS;
+    u64* swi = swf + 2 * Gm::TW_CHUNK;
+    const u32 N = R.N, rows = u32(level) + 1 + R.K;
+    const u32 r = blockIdx.y;
+    const u32 b0 = blockIdx.z * ppb, b1 = min(npolys, b0 + ppb);
+    if (b0 >= b1) return;
+    const u32 m = mod_index(r, level, R.q_count);
+    const double qd = R.qd[4 * m], qi = R.qd[4 * m + 1];
+    const u64* tw = reinterpret_cast<const u64*>(R.twd + size_t(m) * 4 * N);
+    stage_chunk_twiddles<E, true>(swf, nullptr, tw, tw + N, logN1, blockIdx.x);
+    stage_chunk_twiddles<E, false>(swi, nullptr, tw + 2 * size_t(N), tw + 3 * size_t(N), logN1, blockIdx.x);
+    __syncthreads();
+    const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
+    u64* col = dyn + warp * Gm::CS;
+    constexpr u32 CS2 = 8 * Gm::CS;
+    const size_t words = size_t(rows) * N, key_rows = R.nmod;
+    const bool addq = add0 && r <= u32(level);
+    double pmd = 0, pmq = 0;
+    if (addq) {
+        pmd = __longlong_as_double(static_cast<long long>(pmod[4 * r + 2]));
+        pmq = __longlong_as_double(static_cast<long long>(pmod[4 * r + 3]));
+    }
+    // digit d's own-group row (already eval form, canonical)
+    const u32 own = (own_gs && r <= u32(level)) ? r / own_gs : 0xFFFFFFFFu;
+    const u32 vo = lane << Gm::LOGE;  // layout 0: this lane's E contiguous eval slots
+    auto mac = [&](double (&a0)[E], double (&a1)[E], const double (&v)[E], u32 d) {
+        const ulonglong2* kb = reinterpret_cast<const ulonglong2*>(key + (size_t(d) * 2 * key_rows + m) * N + off + vo);
+        const ulonglong2* ka = reinterpret_cast<const ulonglong2*>(key + ((size_t(d) * 2 + 1) * key_rows + m) * N + off + vo);
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) {
+            const ulonglong2 tb = kb[j], ta = ka[j];
+            a0[2 * j] = __dadd_rn(a0[2 * j], fp_mulmod_qi(v[2 * j], u2d(tb.x), qd, qi));
+            a0[2 * j + 1] = __dadd_rn(a0[2 * j + 1], fp_mulmod_qi(v[2 * j + 1], u2d(tb.y), qd, qi));
+            a1[2 * j] = __dadd_rn(a1[2 * j], fp_mulmod_qi(v[2 * j], u2d(ta.x), qd, qi));
+            a1[2 * j + 1] = __dadd_rn(a1[2 * j + 1], fp_mulmod_qi(v[2 * j + 1], u2d(ta.y), qd, qi));
+        }
+    };
+    for (u32 b = b0; b < b1; ++b) {
+        double a[2][E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) a[0][j] = a[1][j] = 0.0;
+        const u64* dig = digits + size_t(b) * nd * words + size_t(r) * N + off;
+        for (u32 d = 0; d < nd; d += 2) {
+            const bool pair = d + 1 < nd;
+            double v[2][E];
+            if (pair && own != d && own != d + 1) {  // two digits transformed together
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                    u64 t[E];
+                    ld_strided<E>(t, dig + size_t(d + n) * words, lane);
+#pragma unroll
+                    for (int j = 0; j < E; ++j) v[n][j] = __longlong_as_double(static_cast<long long>(t[j]));
+                }
+                wfwd_all_fp<2, E, true>(v, col, CS2, lane, swf, qd, qi, warp);
+                mac(a[0], a[1], v[0], d);
+                mac(a[0], a[1], v[1], d + 1);
+            } else {
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                    if (n == 1 && !pair) break;
+                    const u32 dd = d + n;
+                    double (&vn)[1][E] = reinterpret_cast<double(&)[1][E]>(v[n]);
+                    u64 t[E];
+                    if (dd == own) {
+                        ld_vec<E>(t, dig + size_t(dd) * words, lane);
+#pragma unroll
+                        for (int j = 0; j < E; ++j) vn[0][j] = u2d(t[j]);
+                    } else {
+                        ld_strided<E>(t, dig + size_t(dd) * words, lane);
+#pragma unroll
+                        for (int j = 0; j < E; ++j) vn[0][j] = __longlong_as_double(static_cast<long long>(t[j]));
+                        wfwd_all_fp<1, E, true>(vn, col, CS2, lane, swf, qd, qi, warp);
+                    }
+                    mac(a[0], a[1], vn[0], dd);
+                }
+            }
+            if ((d & 3) == 2 && d + 2 < nd) {
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    a[0][j] = fp_reduce(a[0][j], qd, qi);
+                    a[1][j] = fp_reduce(a[1][j], qd, qi);
+                }
+            }
+        }
+        if (addq) {  // + P * c on the Q rows
+            const size_t qw = size_t(level + 1) * N;
+            const ulonglong2* c0 = reinterpret_cast<const ulonglong2*>(add0 + size_t(b) * qw + size_t(r) * N + off + vo);
+            const ulonglong2* c1 = reinterpret_cast<const ulonglong2*>(add1 + size_t(b) * qw + size_t(r) * N + off + vo);
+#pragma unroll
+            for (int j = 0; j < E / 2; ++j) {
+                const ulonglong2 x0 = c0[j], x1 = c1[j];
+                a[0][2 * j] = __dadd_rn(a[0][2 * j], fp_mulmod(u2d(x0.x), pmd, pmq, qd));
+                a[0][2 * j + 1] = __dadd_rn(a[0][2 * j + 1], fp_mulmod(u2d(x0.y), pmd, pmq, qd));
+                a[1][2 * j] = __dadd_rn(a[1][2 * j], fp_mulmod(u2d(x1.x), pmd, pmq, qd));
+                a[1][2 * j + 1] = __dadd_rn(a[1][2 * j + 1], fp_mulmod(u2d(x1.y), pmd, pmq, qd));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            a[0][j] = fp_reduce(a[0][j], qd, qi);
+            a[1][j] = fp_reduce(a[1][j], qd, qi);
+        }
+        // inverse chunk phase of both accumulators (layout 0 in, layout 5 out),
+        // doubles (|v| <= 1.5q, raw bits) to the inverse column phase
+        winv_all_fp<2, E, true>(a, col, CS2, lane, swi, qd, qi, warp);
+        u64* o0 = acc + (size_t(b) * rows + r) * N + off;
+        u64* o1 = acc + (size_t(npolys + b) * rows + r) * N + off;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            o0[lane + 32 * j] = static_cast<u64>(__double_as_longlong(a[0][j]));
+            o1[lane + 32 * j] = static_cast<u64>(__double_as_longlong(a[1][j]));
+        }
+    }
+}

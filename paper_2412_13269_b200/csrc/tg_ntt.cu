@@ -194,8 +194,97 @@ k_inv_cols(DevRing R, u64* __restrict__ data, u32 row_base, u32 rows_per_poly, i
 }
 
 #include "tg_ntt_warp.cuh"
+#include "tg_ks_fused.cuh"
+
+template <int E1, int E2>
+void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key,
+                     int level, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s) {
+    static const bool attr = [] {
+        cudaFuncSetAttribute(kw_ks_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ks_chunk_smem<E2>()));
+        return true;
+    }();
+    (void)attr;
+    const u32 M1 = 32 * E1, rows = u32(level) + 1 + R.K;
+    // batch split so that the grid covers about two waves (2 blocks per SM)
+    const u64 base = u64(M1 / 8) * rows;
+    u32 z = u32(std::min<u64>(npolys, (u64(sms) * 4 + base - 1) / base));
+    if (z < 1) z = 1;
+    const u32 ppb = (npolys + z - 1) / z;
+    kw_ks_chunks<E2><<<dim3(M1 / 8, rows, (npolys + ppb - 1) / ppb), 256, ks_chunk_smem<E2>(), s>>>(
+        R, acc, digits, nd, npolys, ppb, key, level, WGeo<E1>::LOGM, own_gs, add0, add1, pmod);
+}
+
+template <int E1, int E2>
+void launch_fwd_cols_only(const DevRing& R, int sms, u64* data, u32 rpp, u32 npolys, int level, cudaStream_t s,
+                          u32 skip_gs) {
+    set_smem_attrs<E1, E2>();
+    const u32 M2 = 32 * E2;
+    const u32 p1 = polys_per_block(M2 / 8, rpp, npolys, sms);
+    kw_fwd_cols<E1><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(
+        R, data, data, rpp, npolys, p1, level, skip_gs, 0);
+}
+
+template <int E1, int E2>
+void launch_inv_cols_only(const DevRing& R, int sms, u64* data, u32 rpp, u32 npolys, int level, cudaStream_t s) {
+    set_smem_attrs<E1, E2>();
+    const u32 M2 = 32 * E2;
+    const u32 p1 = polys_per_block(M2 / 8, rpp, npolys, sms);
+    kw_inv_cols<E1><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys,
+                                                                                          p1, level, 0);
+}
 
 }  // namespace
+
+bool ks_fused_ok(const tg_context* ctx) {
+    static const bool off = [] {
+        const char* e = getenv("TG_KS_FUSED");
+        return e && *e == '0';
+    }();
+    int e1 = 0, e2 = 0;
+    if (off || !warp_plan(ctx->ring.logN, e1, e2)) return false;
+    for (u64 q : ctx->h_q)
+        if (q >= kFpMaxQ) return false;
+    return true;
+}
+
+int ntt_forward_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s, u32 skip_gs) {
+    const DevRing& R = ctx->ring;
+    const u32 rpp = u32(level + 1 + nspecial);
+    ProfScope prof(ctx, TG_OP_NTT_FWD, 8.0 * rpp * npolys * R.N, s);  // half a transform's bytes
+    if (R.logN == 16) launch_fwd_cols_only<8, 8>(R, ctx->sms, data, rpp, npolys, level, s, skip_gs);
+    else if (R.logN == 15) launch_fwd_cols_only<4, 8>(R, ctx->sms, data, rpp, npolys, level, s, skip_gs);
+    else launch_fwd_cols_only<4, 4>(R, ctx->sms, data, rpp, npolys, level, s, skip_gs);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s) {
+    const DevRing& R = ctx->ring;
+    const u32 rpp = u32(level + 1 + nspecial);
+    ProfScope prof(ctx, TG_OP_NTT_INV, 8.0 * rpp * npolys * R.N, s);
+    if (R.logN == 16) launch_inv_cols_only<8, 8>(R, ctx->sms, data, rpp, npolys, level, s);
+    else if (R.logN == 15) launch_inv_cols_only<4, 8>(R, ctx->sms, data, rpp, npolys, level, s);
+    else launch_inv_cols_only<4, 4>(R, ctx->sms, data, rpp, npolys, level, s);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key, int level,
+                    u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s) {
+    const DevRing& R = ctx->ring;
+    const double rows = double(level + 1 + R.K);
+    // algorithmic: digits (phase-1 form) read, key once per batch, P*c addends, accumulators written
+    ProfScope prof(ctx, TG_OP_KEY_INNER,
+                   8.0 * R.N * (rows * (npolys * (nd + 2.0) + 2.0 * nd) + (add0 ? 2.0 * npolys * (level + 1) : 0.0)),
+                   s);
+    if (R.logN == 16)
+        launch_ks_fused<8, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s);
+    else if (R.logN == 15)
+        launch_ks_fused<4, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s);
+    else launch_ks_fused<4, 4>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
 
 int ntt_forward_rows(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s) {
     return ntt_forward_oop(ctx, data, data, level, nspecial, npolys, s);

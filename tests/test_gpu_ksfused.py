@@ -1,0 +1,59 @@
+"""Fused key-switch core (tg_ks_fused.cuh) vs the compiled reference.
+
+Rings whose moduli all take the FP64 path (50-bit q-chain AND 50-bit special
+primes, the configs 3-5 parameters) with N in the warp-NTT range 2^14..2^16
+run key switching through kw_ks_chunks: digits' forward chunk phase, key
+inner product (KeyContext::ks_inner, rlwe.hpp:501-540) and the accumulators'
+inverse chunk phase in one pass. Relinearisation (rlwe.hpp:601-620), Galois
+key switching (rlwe.hpp:637-654) and batched relinearisation must stay bit-
+exact with the reference at full and partial digit counts.
+"""
+from __future__ import annotations
+
+import pytest
+
+from common import assert_ct_equal, make_setup
+
+pytestmark = pytest.mark.gpu
+
+
+def _cts(S, n, level, seed):
+    T = S.T
+    rng = T.Rng(seed)
+    out = []
+    for i in range(n):
+        c = T.Ciphertext()
+        c.parts = [T.sample_uniform(S.ring, level, 0, rng.split(10 * i + j)) for j in range(2)]
+        c.scale = 2.0 ** 50
+        c.domain = T.Domain.slots
+        c.sk_id = S.sk.id()
+        out.append(c)
+    return out
+
+
+@pytest.mark.parametrize("N,nq,K,gs", [(1 << 14, 9, 4, 3), (1 << 15, 8, 3, 3), (1 << 16, 7, 3, 3)])
+def test_fused_keyswitch_bit_exact(G, R, gpu_available, N, nq, K, gs):
+    kw = dict(N=N, nq=nq, K=K, group_size=gs, seed=11, q_bits=50, sp_bits=50, h=192, rotations=(1, 5))
+    g, r = make_setup(G, **kw), make_setup(R, **kw)
+    top = g.ring.max_level()
+    for level in (top, 4, 2):  # full, partial (own row in the last digit) and small digit counts
+        (a_g, b_g), (a_r, b_r) = _cts(g, 2, level, 100 + level), _cts(r, 2, level, 100 + level)
+        assert_ct_equal(g.ev.mul_relin(a_g, b_g, g.keys), r.ev.mul_relin(a_r, b_r, r.keys),
+                        f"mul_relin N={N} level={level}")
+        assert_ct_equal(g.ev.mul_relin(a_g, a_g, g.keys), r.ev.mul_relin(a_r, a_r, r.keys),
+                        f"square N={N} level={level}")
+        for k in (1, 5):
+            assert_ct_equal(g.ev.rotate(a_g, k, g.keys), r.ev.rotate(a_r, k, r.keys),
+                            f"rotate {k} N={N} level={level}")
+
+
+@pytest.mark.parametrize("batch", [3, 8])
+def test_fused_keyswitch_batched(G, R, gpu_available, batch):
+    kw = dict(N=1 << 14, nq=8, K=3, group_size=3, seed=13, q_bits=50, sp_bits=50, h=192)
+    g, r = make_setup(G, **kw), make_setup(R, **kw)
+    level = g.ring.max_level()
+    xs_g, ys_g = _cts(g, batch, level, 7), _cts(g, batch, level, 8)
+    xs_r, ys_r = _cts(r, batch, level, 7), _cts(r, batch, level, 8)
+    prod = g.ev.rescale(g.ev.mul_relin(G.stack_ciphertexts(xs_g), G.stack_ciphertexts(ys_g), g.keys))
+    for i, got in enumerate(G.unstack_ciphertext(prod)):
+        assert_ct_equal(got, r.ev.rescale(r.ev.mul_relin(xs_r[i], ys_r[i], r.keys)), f"batched relin block {i}")
