@@ -567,7 +567,7 @@ def run_b200(args):
     per_launch_ms = dms / dn
     achieved = (dbytes / dn) / (per_launch_ms / 1e3) / 1e9
     total_prof_ms = sum(v[0] for v in prof.values())
-    launches = sum(v[1] * (2 if k.startswith("ntt") else 1) for k, v in prof.items()) // args.steps * args.steps
+    launches = sum(v[1] for v in prof.values()) // args.steps * args.steps  # kernel launches (tg_profile_read)
     # DRAM traffic per launch of the dominant class from the committed ncu
     # capture of this workload (profiles/traffic_<workload>.json), else null
     traffic = None

@@ -119,6 +119,7 @@ enum {
     TG_OP_REDUCE,
     TG_OP_LINCOMB,
     TG_OP_ENCODE,
+    TG_OP_KS_FUSED, /* fused key-switch core: digits' NTT chunk phase + key inner product + iNTT chunk phase */
     TG_OP_COUNT
 };
 int tg_profile_enable(tg_context* ctx, int on);

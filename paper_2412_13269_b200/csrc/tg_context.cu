@@ -288,7 +288,7 @@ extern "C" int tg_profile_read(tg_context* ctx, double* ms, uint64_t* launches, 
         float t = 0;
         TG_CUDA(cudaEventElapsedTime(&t, r.start, r.stop));
         if (ms) ms[r.op] += t;
-        if (launches) launches[r.op] += 1;
+        if (launches) launches[r.op] += u64(r.kernels);
         if (bytes) bytes[r.op] += r.bytes;
         ctx->prof_free.push_back(r.start);
         ctx->prof_free.push_back(r.stop);
@@ -300,7 +300,7 @@ extern "C" int tg_profile_read(tg_context* ctx, double* ms, uint64_t* launches, 
 extern "C" const char* tg_profile_op_name(int op) {
     static const char* names[TG_OP_COUNT] = {"ntt_fwd", "ntt_inv",  "addsub", "mul_pointwise", "mul_scalar",
                                              "automorphism", "rescale", "tensor", "mul_plain", "modup_baseconv",
-                                             "key_inner", "mod_down", "reduce", "lincomb", "encode"};
+                                             "key_inner", "mod_down", "reduce", "lincomb", "encode", "ks_fused"};
     return op >= 0 && op < TG_OP_COUNT ? names[op] : "?";
 }
 

@@ -76,6 +76,17 @@ __device__ __forceinline__ double fp_reduce(double v, double q, double qi) {
     return __fma_rn(-k, q, v);
 }
 
+// integer v in (-q, q) -> canonical u64 in [0, q), one FP64 add: v + 1.5 * 2^52
+// lies in [2^52, 2^53) (|v| < 2^51), where doubles are the integers, so its
+// mantissa field is exactly 2^51 + v; the sign fix-up runs on the integer ALU
+// (fp_canonical spends three compares and three adds on the FP64 pipe).
+__device__ __forceinline__ u64 fp_canon_small(double v, u64 q) {
+    const long long m = static_cast<long long>(
+        static_cast<u64>(__double_as_longlong(__dadd_rn(v, kRoundMagic))) & 0x000FFFFFFFFFFFFFull);
+    const long long x = m - (1ll << 51);
+    return static_cast<u64>(x < 0 ? x + static_cast<long long>(q) : x);
+}
+
 // |v| < 2q integer -> canonical u64 in [0, q)
 __device__ __forceinline__ u64 fp_canonical(double v, double q) {
     if (v < 0) v = __dadd_rn(v, q);

@@ -178,6 +178,7 @@ struct GadgetDev {
 namespace tg {
 struct ProfRecord {
     int op;
+    int kernels;  // kernel launches in the scope
     double bytes;
     cudaEvent_t start, stop;
 };
@@ -205,9 +206,10 @@ struct ProfScope {
     tg_context* ctx;
     ProfRecord rec{};
     bool on;
-    ProfScope(tg_context* c, int op, double bytes, cudaStream_t s) : ctx(c), on(c && c->prof_on) {
+    ProfScope(tg_context* c, int op, double bytes, cudaStream_t s, int kernels = 1) : ctx(c), on(c && c->prof_on) {
         if (!on) return;
         rec.op = op;
+        rec.kernels = kernels;
         rec.bytes = bytes;
         {
             std::lock_guard<std::mutex> g(ctx->prof_mu);

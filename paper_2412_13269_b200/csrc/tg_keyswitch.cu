@@ -252,9 +252,9 @@ k_key_inner_b(DevRing R, u64* __restrict__ acc, const u64* __restrict__ digits, 
                     t1 = __dadd_rn(t1, fp_mulmod(u2d(a1.y), pmd, pmq, qd));
                 }
                 *reinterpret_cast<ulonglong2*>(acc + size_t(b) * words + i) = make_ulonglong2(
-                    fp_canonical(fp_reduce(s0, qd, qi), qd), fp_canonical(fp_reduce(t0, qd, qi), qd));
+                    fp_canon_small(fp_reduce(s0, qd, qi), q), fp_canon_small(fp_reduce(t0, qd, qi), q));
                 *reinterpret_cast<ulonglong2*>(acc + (size_t(npolys) + b) * words + i) = make_ulonglong2(
-                    fp_canonical(fp_reduce(s1, qd, qi), qd), fp_canonical(fp_reduce(t1, qd, qi), qd));
+                    fp_canon_small(fp_reduce(s1, qd, qi), q), fp_canon_small(fp_reduce(t1, qd, qi), q));
                 if (b + 1 < b1) {
 #pragma unroll
                     for (int k = 0; k < NDMAX; ++k) dv[k] = dn[k];
@@ -463,7 +463,7 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
             }
             u64 o[CPT];
 #pragma unroll
-            for (int cc = 0; cc < CPT; ++cc) o[cc] = fp_canonical(fp_reduce(acc[cc], qd, qi), qd);
+            for (int cc = 0; cc < CPT; ++cc) o[cc] = fp_canon_small(fp_reduce(acc[cc], qd, qi), q);
             if constexpr (CPT == 2) *reinterpret_cast<ulonglong2*>(out + size_t(r) * N) = make_ulonglong2(o[0], o[1]);
             else out[size_t(r) * N] = o[0];
             continue;
@@ -624,10 +624,12 @@ k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restri
     const double* ys_t = G.mdf;                         // [K][4]
     const double* w_rs = G.mdf + 4 * K;                 // [nq][K][2]
     const double* p_r = w_rs + size_t(nq) * K * 2;      // [nq][4]
-    extern __shared__ double2 smf[];                    // [rout][K] (w, wq), then [rout][2] (pinv, pinvq | q, qi)
+    extern __shared__ double2 smf[];  // [rout][K] (w, wq), then [rout][2] (pinv, pinvq | q, qi), then [rout] q (u64)
     double2* sp = smf + size_t(rout) * K;
+    u64* sq64 = reinterpret_cast<u64*>(sp + 2 * rout);
     for (u32 e = threadIdx.x; e < rout * K; e += blockDim.x) smf[e] = make_double2(w_rs[2 * e], w_rs[2 * e + 1]);
     for (u32 e = threadIdx.x; e < 2 * rout; e += blockDim.x) sp[e] = make_double2(p_r[2 * e], p_r[2 * e + 1]);
+    for (u32 e = threadIdx.x; e < rout; e += blockDim.x) sq64[e] = R.q[e];
     __syncthreads();
     const u32 per_poly = N / 2;
     const u64 total = u64(npolys) * per_poly;
@@ -686,12 +688,12 @@ k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restri
                     }
                 }
             }
+            const u64 qu = sq64[r];
             u64 o[2];
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc) {
-                double v = fp_reduce(acc[cc], q, qi);  // |v| <= q/2 + 1
-                if (add) v = __dadd_rn(v, u2d(a[cc]));
-                o[cc] = fp_canonical(v, q);
+                o[cc] = fp_canon_small(fp_reduce(acc[cc], q, qi), qu);  // |.| <= q/2 + 1
+                if (add) o[cc] = add_mod(o[cc], a[cc], qu);
             }
             *reinterpret_cast<ulonglong2*>(dst + size_t(r) * N) = make_ulonglong2(o[0], o[1]);
         }
@@ -797,7 +799,7 @@ template <int KMAX>
 void launch_mod_down_fp(const DevRing& R, const GadgetDev& G, int sms, u64* out, const u64* in, int level,
                         u32 npolys, const u64* addend, cudaStream_t s) {
     const u32 rout = u32(level) + 1;
-    const size_t smem = size_t(rout) * R.K * 16 + size_t(rout) * 32;
+    const size_t smem = size_t(rout) * R.K * 16 + size_t(rout) * 40;
     const u64 work = u64(npolys) * R.N / 2;
     const u32 blocks = u32(std::min<u64>((work + 255) / 256, u64(sms) * 8));
     const u32 groups = row_groups(u64(blocks) * 256, rout, sms);

@@ -274,7 +274,7 @@ int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 np
     const DevRing& R = ctx->ring;
     const double rows = double(level + 1 + R.K);
     // algorithmic: digits (phase-1 form) read, key once per batch, P*c addends, accumulators written
-    ProfScope prof(ctx, TG_OP_KEY_INNER,
+    ProfScope prof(ctx, TG_OP_KS_FUSED,
                    8.0 * R.N * (rows * (npolys * (nd + 2.0) + 2.0 * nd) + (add0 ? 2.0 * npolys * (level + 1) : 0.0)),
                    s);
     if (R.logN == 16)
@@ -302,7 +302,7 @@ int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     if (nrows == 0) nrows = rpp - row0;
     const u32 total = rpp * npolys;
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
-    ProfScope prof(ctx, TG_OP_NTT_FWD, 16.0 * nrows * npolys * R.N, s);
+    ProfScope prof(ctx, TG_OP_NTT_FWD, 16.0 * nrows * npolys * R.N, s, 2);
     int e1 = 0, e2 = 0;
     if (warp_plan(R.logN, e1, e2) && npolys <= 65535) {
         if (e1 == 8) launch_fwd_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows);
@@ -339,7 +339,7 @@ int ntt_inverse_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     if (nrows == 0) nrows = rpp - row0;
     const u32 total = rpp * npolys;
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
-    ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * nrows * npolys * R.N, s);
+    ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * nrows * npolys * R.N, s, 2);
     int e1 = 0, e2 = 0;
     if (warp_plan(R.logN, e1, e2) && npolys <= 65535) {
         if (e1 == 8) launch_inv_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, row0, nrows);

@@ -579,7 +579,7 @@ __device__ __forceinline__ void st_vec(u64* x, const u64 (&v)[E], u32 lane) {
 // FP64 chunk phase of NP polys: forward (phase-1 doubles in, canonical out)
 template <int NP, int E>
 __device__ __forceinline__ void chunk_fwd_fp(u64 (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double qd,
-                                             double qi, u32 warp) {
+                                             double qi, u32 warp, u64 q) {
     double vd[NP][E];
 #pragma unroll
     for (int n = 0; n < NP; ++n)
@@ -589,7 +589,7 @@ __device__ __forceinline__ void chunk_fwd_fp(u64 (&v)[NP][E], u64* col, u32 cs, 
 #pragma unroll
     for (int n = 0; n < NP; ++n)
 #pragma unroll
-        for (int j = 0; j < E; ++j) v[n][j] = fp_canonical(vd[n][j], qd);
+        for (int j = 0; j < E; ++j) v[n][j] = fp_canon_small(vd[n][j], q);  // |vd| <= q/2 + 1 (fp_reduce)
 }
 // inverse (canonical in, doubles |v| <= 1.5q as raw bits out to phase B)
 template <int NP, int E>
@@ -643,12 +643,12 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
         __syncthreads();
         while (true) {
             if (p2 < pend) {
-                chunk_fwd_fp<2, E>(v, col, CS2, lane, sw, qd, qi, warp);
+                chunk_fwd_fp<2, E>(v, col, CS2, lane, sw, qd, qi, warp, q);
                 st_vec<E>(row(p), v[0], lane);
                 st_vec<E>(row(p2), v[1], lane);
                 p = next_poly(p2 + 1, pend, r, rpp, level, skip_gs);
             } else {
-                chunk_fwd_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), col, CS2, lane, sw, qd, qi, warp);
+                chunk_fwd_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), col, CS2, lane, sw, qd, qi, warp, q);
                 st_vec<E>(row(p), v[0], lane);
                 p = p2;
             }
@@ -806,7 +806,7 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 r
                 for (int n = 0; n < 2; ++n)
 #pragma unroll
                     for (int j = 0; j < E; ++j)
-                        col[n * 8 * Gm::CS + wpad(lane + 32 * j)] = fp_canonical(fp_mulmod(v[n][j], nd, ndq, qd), qd);
+                        col[n * 8 * Gm::CS + wpad(lane + 32 * j)] = fp_canon_small(fp_mulmod(v[n][j], nd, ndq, qd), q);
             } else {
                 const double* cold = reinterpret_cast<const double*>(col);
                 double v[1][E];
@@ -815,7 +815,7 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 r
                 winv_all_fp<1, E, false>(v, col, 0, lane, sw, qd, qi, 0);
                 __syncwarp();
 #pragma unroll
-                for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canonical(fp_mulmod(v[0][j], nd, ndq, qd), qd);
+                for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canon_small(fp_mulmod(v[0][j], nd, ndq, qd), q);
             }
             __syncthreads();
             store_col_tile<E>(tiles, data, p * rpp + r, c0, N);
@@ -845,7 +845,7 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 r
             winv_all_fp<1, E, false>(v, col, 0, lane, sw, qd, qi, 0);
             __syncwarp();
 #pragma unroll
-            for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canonical(fp_mulmod(v[0][j], nd, ndq, qd), qd);
+            for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canon_small(fp_mulmod(v[0][j], nd, ndq, qd), q);
         } else {
             u64 v[E];
 #pragma unroll

@@ -45,9 +45,10 @@ def main():
     for cls, pat in (("ntt_fwd", "kw_fwd_"), ("ntt_inv", "kw_inv_")):
         ks = [a for k, a in agg.items() if k.startswith(pat)]
         if ks:
-            n = max(a[0] for a in ks)  # one column + one chunk launch per transform
+            n = sum(a[0] for a in ks)  # per kernel launch (column and chunk phases), as tg_profile_read counts
             classes[cls] = {"dram_bytes_per_launch": sum(a[2] for a in ks) / n, "launches": n}
     for cls, pat in (("mod_down", "k_mod_down"), ("key_inner", "k_key_inner_b"), ("modup_baseconv", "k_modup"),
+                     ("ks_fused", "kw_ks_chunks"),
                      ("lincomb", "k_lincomb"), ("tensor", "k_tensor")):
         ks = [a for k, a in agg.items() if k.startswith(pat)]
         if ks:
