@@ -13,6 +13,8 @@
 // intermediate of a batched launch stays in the 126 MB L2). Butterflies are
 // Harvey-lazy: values live in [0,4q) (forward) / [0,2q) (inverse) and are
 // made canonical only at the end of the last phase.
+#include <utility>
+
 #include "tg_internal.cuh"
 #include "tg_fp64.cuh"
 
@@ -220,7 +222,7 @@ void launch_fwd_cols_only(const DevRing& R, int sms, u64* data, u32 rpp, u32 npo
     set_smem_attrs<E1, E2>();
     const u32 M2 = 32 * E2;
     const u32 p1 = polys_per_block(M2 / 8, rpp, npolys, sms);
-    kw_fwd_cols<E1><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(
+    kw_fwd_cols<E1, E2><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(
         R, data, data, rpp, npolys, p1, level, skip_gs, 0);
 }
 
@@ -229,7 +231,7 @@ void launch_inv_cols_only(const DevRing& R, int sms, u64* data, u32 rpp, u32 npo
     set_smem_attrs<E1, E2>();
     const u32 M2 = 32 * E2;
     const u32 p1 = polys_per_block(M2 / 8, rpp, npolys, sms);
-    kw_inv_cols<E1><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys,
+    kw_inv_cols<E1, E2><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys,
                                                                                           p1, level, 0);
 }
 

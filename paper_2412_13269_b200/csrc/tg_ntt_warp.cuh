@@ -421,27 +421,39 @@ constexpr size_t chunk_smem() {  // exchange columns of two transforms per warp 
     return size_t(8) * (16 * WGeo<E>::CS + 2 * WGeo<E>::TW_CHUNK);
 }
 
-// Column tile of row `row` (8 columns x M1, element (m, c) at c*CS + wpad(m)).
-template <int E>
-__device__ __forceinline__ void issue_col_tile(u64* tile, const u64* src, u32 row, u32 c0, u32 N) {
+// Column tile (8 columns x M1 rows, element (m, c) at c*CS + wpad(m)) of the
+// row starting at rb (= row base + first column). N2 = M2 is the row stride
+// of the M1 x N2 view: with it a compile-time constant every per-element
+// address is the thread's base plus an immediate offset (thread t copies
+// elements m = t/8 + 32i, c = t%8; wpad(m + 32i) = wpad(m) + 36i).
+template <int OS, int OG>
+__device__ __forceinline__ void cp_async8_imm(u32 sa, const u64* g) {
+    asm volatile("cp.async.ca.shared.global [%0+%2], [%1+%3], 8;\n" ::"r"(sa), "l"(g), "n"(OS), "n"(OG) : "memory");
+}
+template <int N2, int... I>
+__device__ __forceinline__ void issue_col_elems(u32 sa, const u64* g, std::integer_sequence<int, I...>) {
+    (cp_async8_imm<I * 36 * 8, I * 32 * N2 * 8>(sa, g), ...);
+}
+template <int E, int N2>
+__device__ __forceinline__ void issue_col_tile(u64* tile, const u64* rb) {
     using Gm = WGeo<E>;
-    const u32 N2 = N >> Gm::LOGM;
-    const u64* xs = src + size_t(row) * N + c0;
-    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
-        cp_async8(&tile[(e & 7) * Gm::CS + wpad(e >> 3)], xs + size_t(e >> 3) * N2 + (e & 7));
+    const u32 t = threadIdx.x, c = t & 7, m0 = t >> 3;
+    const u32 sa = static_cast<u32>(__cvta_generic_to_shared(tile + c * Gm::CS + wpad(m0)));
+    issue_col_elems<N2>(sa, rb + size_t(m0) * N2 + c, std::make_integer_sequence<int, Gm::M / 32>{});
     cp_async_commit();
 }
-template <int E>
-__device__ __forceinline__ void store_col_tile(const u64* tile, u64* dst, u32 row, u32 c0, u32 N) {
+template <int E, int N2>
+__device__ __forceinline__ void store_col_tile(const u64* tile, u64* rb) {
     using Gm = WGeo<E>;
-    const u32 N2 = N >> Gm::LOGM;
-    u64* xd = dst + size_t(row) * N + c0;
-    for (u32 e = threadIdx.x; e < 8u * Gm::M; e += 256)
-        xd[size_t(e >> 3) * N2 + (e & 7)] = tile[(e & 7) * Gm::CS + wpad(e >> 3)];
+    const u32 t = threadIdx.x, c = t & 7, m0 = t >> 3;
+    const u64* sm = tile + c * Gm::CS + wpad(m0);
+    u64* g = rb + size_t(m0) * N2 + c;
+#pragma unroll
+    for (int i = 0; i < Gm::M / 32; ++i) g[size_t(i) * 32 * N2] = sm[36 * i];
 }
 
 // Phase 1 forward: 8 columns x M1 rows, stages 0 .. log M1 - 1.
-template <int E>
+template <int E, int E2>
 __global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
 kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, int level, u32 skip_gs,
             u32 row0) {
@@ -454,13 +466,13 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
     u64* tiles = dyn;
     u64* sw = dyn + 16 * Gm::CS;
     u64* sws = sw + Gm::TW_COL;
-    const u32 N = R.N;
+    constexpr u32 N = 32 * E * 32 * E2;  // == R.N (warp_plan)
     const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
     const bool fp = ntt_use_fp(R, q, r);  // FP64 path; the other phase makes the same choice
     const u64* w = fp ? reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N) : R.tw + size_t(mi) * 4 * N;
     const u32 c0 = blockIdx.x * 8;
-    issue_col_tile<E>(tiles, src, p * rpp + r, c0, N);
+    issue_col_tile<E, 32 * E2>(tiles, src + size_t(p * rpp + r) * N + c0);
     stage_col_twiddles<E, true>(sw, sws, w, w + N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (fp) {  // polys in pairs on the block's two tiles: each staged twiddle feeds two interleaved transforms
@@ -469,8 +481,8 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
         while (p < pend) {
             const u32 p2 = next_poly(p + 1, pend, r, rpp, level, skip_gs);
             const bool pair = p2 < pend;
-            if (!first) issue_col_tile<E>(tiles, src, p * rpp + r, c0, N);
-            if (pair) issue_col_tile<E>(tiles + 8 * Gm::CS, src, p2 * rpp + r, c0, N);
+            if (!first) issue_col_tile<E, 32 * E2>(tiles, src + size_t(p * rpp + r) * N + c0);
+            if (pair) issue_col_tile<E, 32 * E2>(tiles + 8 * Gm::CS, src + size_t(p2 * rpp + r) * N + c0);
             first = false;
             cp_async_wait<0>();
             __syncthreads();
@@ -500,8 +512,8 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
                 for (int j = 0; j < E; ++j) cold[wpad((lane << Gm::LOGE) | j)] = v[0][j];
             }
             __syncthreads();
-            store_col_tile<E>(tiles, data, p * rpp + r, c0, N);
-            if (pair) store_col_tile<E>(tiles + 8 * Gm::CS, data, p2 * rpp + r, c0, N);
+            store_col_tile<E, 32 * E2>(tiles, data + size_t(p * rpp + r) * N + c0);
+            if (pair) store_col_tile<E, 32 * E2>(tiles + 8 * Gm::CS, data + size_t(p2 * rpp + r) * N + c0);
             __syncthreads();
             p = pair ? next_poly(p2 + 1, pend, r, rpp, level, skip_gs) : p2;
         }
@@ -511,7 +523,7 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
     while (p < pend) {
         const u32 pn = next_poly(p + 1, pend, r, rpp, level, skip_gs);
         if (pn < pend) {
-            issue_col_tile<E>(tiles + (cur ^ 1) * 8 * Gm::CS, src, pn * rpp + r, c0, N);
+            issue_col_tile<E, 32 * E2>(tiles + (cur ^ 1) * 8 * Gm::CS, src + size_t(pn * rpp + r) * N + c0);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
@@ -540,7 +552,7 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
             for (int j = 0; j < E; ++j) col[wpad((lane << Gm::LOGE) | j)] = v[j];
         }
         __syncthreads();
-        store_col_tile<E>(tile, data, p * rpp + r, c0, N);
+        store_col_tile<E, 32 * E2>(tile, data + size_t(p * rpp + r) * N + c0);
         __syncthreads();  // the tile is the next prefetch target
         p = pn;
         cur ^= 1;
@@ -760,7 +772,7 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
 }
 
 // Phase B inverse: 8 columns x M1 rows, then the N^-1 scaling.
-template <int E>
+template <int E, int E2>
 __global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
 kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 row0) {
     using Gm = WGeo<E>;
@@ -772,7 +784,7 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 r
     u64* tiles = dyn;
     u64* sw = dyn + 16 * Gm::CS;
     u64* sws = sw + Gm::TW_COL;
-    const u32 N = R.N;
+    constexpr u32 N = 32 * E * 32 * E2;  // == R.N (warp_plan)
     const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
     const bool fp = ntt_use_fp(R, q, r);
@@ -780,15 +792,15 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 r
                       : R.tw + size_t(mi) * 4 * N + 2 * size_t(N);
     const u64 ninv = R.ninv[2 * mi], ninv_s = R.ninv[2 * mi + 1];
     const u32 c0 = blockIdx.x * 8;
-    issue_col_tile<E>(tiles, data, p * rpp + r, c0, N);
+    issue_col_tile<E, 32 * E2>(tiles, data + size_t(p * rpp + r) * N + c0);
     stage_col_twiddles<E, false>(sw, sws, w, w + N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (fp) {  // polys in pairs on the block's two tiles (see kw_fwd_cols)
         const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1], nd = R.qd[4 * mi + 2], ndq = R.qd[4 * mi + 3];
         for (bool first = true; p < pend; first = false) {
             const bool pair = p + 1 < pend;
-            if (!first) issue_col_tile<E>(tiles, data, p * rpp + r, c0, N);
-            if (pair) issue_col_tile<E>(tiles + 8 * Gm::CS, data, (p + 1) * rpp + r, c0, N);
+            if (!first) issue_col_tile<E, 32 * E2>(tiles, data + size_t(p * rpp + r) * N + c0);
+            if (pair) issue_col_tile<E, 32 * E2>(tiles + 8 * Gm::CS, data + size_t((p + 1) * rpp + r) * N + c0);
             cp_async_wait<0>();
             __syncthreads();
             u64* col = tiles + warp * Gm::CS;
@@ -818,8 +830,8 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 r
                 for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = fp_canon_small(fp_mulmod(v[0][j], nd, ndq, qd), q);
             }
             __syncthreads();
-            store_col_tile<E>(tiles, data, p * rpp + r, c0, N);
-            if (pair) store_col_tile<E>(tiles + 8 * Gm::CS, data, (p + 1) * rpp + r, c0, N);
+            store_col_tile<E, 32 * E2>(tiles, data + size_t(p * rpp + r) * N + c0);
+            if (pair) store_col_tile<E, 32 * E2>(tiles + 8 * Gm::CS, data + size_t((p + 1) * rpp + r) * N + c0);
             __syncthreads();
             p += pair ? 2 : 1;
         }
@@ -828,7 +840,7 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 r
     u32 cur = 0;
     for (; p < pend; ++p) {
         if (p + 1 < pend) {
-            issue_col_tile<E>(tiles + (cur ^ 1) * 8 * Gm::CS, data, (p + 1) * rpp + r, c0, N);
+            issue_col_tile<E, 32 * E2>(tiles + (cur ^ 1) * 8 * Gm::CS, data + size_t((p + 1) * rpp + r) * N + c0);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
@@ -857,7 +869,7 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 r
             for (int j = 0; j < E; ++j) col[wpad(lane + 32 * j)] = shoup(v[j], ninv, ninv_s, q);
         }
         __syncthreads();
-        store_col_tile<E>(tile, data, p * rpp + r, c0, N);
+        store_col_tile<E, 32 * E2>(tile, data + size_t(p * rpp + r) * N + c0);
         __syncthreads();  // the tile is the next prefetch target
         cur ^= 1;
     }
@@ -877,8 +889,8 @@ template <int E1, int E2>
 void set_smem_attrs() {
     // thread-safe one-time init (one process drives one device)
     static const bool done = [] {
-        cudaFuncSetAttribute(kw_fwd_cols<E1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
-        cudaFuncSetAttribute(kw_inv_cols<E1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
+        cudaFuncSetAttribute(kw_fwd_cols<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
+        cudaFuncSetAttribute(kw_inv_cols<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
         cudaFuncSetAttribute(kw_fwd_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
         cudaFuncSetAttribute(kw_inv_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
         return true;
@@ -900,7 +912,7 @@ void launch_fwd_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp,
     set_smem_attrs<E1, E2>();
     const u32 M1 = 32 * E1, M2 = 32 * E2;
     const u32 p1 = polys_per_block(M2 / 8, nrows, npolys, sms), p2 = polys_per_block(M1 / 8, nrows, npolys, sms);
-    kw_fwd_cols<E1><<<dim3(M2 / 8, nrows, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(
+    kw_fwd_cols<E1, E2><<<dim3(M2 / 8, nrows, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(
         R, data, src, rpp, npolys, p1, level, skip_gs, row0);
     kw_fwd_chunks<E2><<<dim3(M1 / 8, nrows, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
         R, data, rpp, npolys, p2, level, WGeo<E1>::LOGM, skip_gs, row0);
@@ -914,6 +926,6 @@ void launch_inv_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp,
     const u32 p1 = polys_per_block(M2 / 8, nrows, npolys, sms), p2 = polys_per_block(M1 / 8, nrows, npolys, sms);
     kw_inv_chunks<E2><<<dim3(M1 / 8, nrows, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
         R, data, src, rpp, npolys, p2, level, WGeo<E1>::LOGM, row0);
-    kw_inv_cols<E1><<<dim3(M2 / 8, nrows, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys,
+    kw_inv_cols<E1, E2><<<dim3(M2 / 8, nrows, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys,
                                                                                            p1, level, row0);
 }

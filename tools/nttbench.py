@@ -21,7 +21,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-DEFAULT_CASES = "fwd:16:20:0,fwd:32:20:6,inv:16:20:6,inv:16:20:0,fwd:4:20:6,inv:2:10:6"
+DEFAULT_CASES = "fwd:16:20:0,fwd:32:20:7,inv:16:20:7,inv:16:20:0,fwd:4:20:7,inv:2:10:7"
 
 
 def main():
