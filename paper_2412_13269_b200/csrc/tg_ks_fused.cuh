@@ -24,6 +24,10 @@
 // fp_mulmod_qi with |a| <= q/2 + 1, b in [0, q): |term| < 0.81q; sums reduced
 // every 4 digits: |sum| < q/2 + 1 + 4 * 0.81q (+ 0.58q for P * c) < 2^53.
 
+#ifndef KS_KEY_PREFETCH
+#define KS_KEY_PREFETCH 0
+#endif
+
 template <int E>
 constexpr size_t ks_chunk_smem() {  // two exchange columns per warp + forward and inverse chunk twiddles
     return size_t(8) * (16 * WGeo<E>::CS + 4 * WGeo<E>::TW_CHUNK);
@@ -64,6 +68,29 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
     auto kptr = [&](u32 d, u32 part) {
         return reinterpret_cast<const ulonglong2*>(key + ((size_t(d) * 2 + part) * key_rows + m) * N + off + vo);
     };
+#if KS_KEY_PREFETCH
+    // key chunk of one digit (E words of each half), loaded ahead of its transform
+    auto kload = [&](ulonglong2 (&kb)[E / 2], ulonglong2 (&ka)[E / 2], u32 d) {
+        const ulonglong2* pb = kptr(d, 0);
+        const ulonglong2* pa = kptr(d, 1);
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) {
+            kb[j] = __ldg(pb + j);
+            ka[j] = __ldg(pa + j);
+        }
+    };
+    auto mack = [&](double (&a0)[E], double (&a1)[E], const double (&v)[E], const ulonglong2 (&kb)[E / 2],
+                    const ulonglong2 (&ka)[E / 2]) {
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) {
+            const ulonglong2 tb = kb[j], ta = ka[j];
+            a0[2 * j] = __dadd_rn(a0[2 * j], fp_mulmod_qi(v[2 * j], u2d(tb.x), qd, qi));
+            a0[2 * j + 1] = __dadd_rn(a0[2 * j + 1], fp_mulmod_qi(v[2 * j + 1], u2d(tb.y), qd, qi));
+            a1[2 * j] = __dadd_rn(a1[2 * j], fp_mulmod_qi(v[2 * j], u2d(ta.x), qd, qi));
+            a1[2 * j + 1] = __dadd_rn(a1[2 * j + 1], fp_mulmod_qi(v[2 * j + 1], u2d(ta.y), qd, qi));
+        }
+    };
+#endif
     auto mac = [&](double (&a0)[E], double (&a1)[E], const double (&v)[E], u32 d) {
         const ulonglong2* kb = kptr(d, 0);
         const ulonglong2* ka = kptr(d, 1);
@@ -92,8 +119,15 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
 #pragma unroll
                     for (int j = 0; j < E; ++j) v[n][j] = __longlong_as_double(static_cast<long long>(t[j]));
                 }
+#if KS_KEY_PREFETCH
+                ulonglong2 kb[E / 2], ka[E / 2];
+                kload(kb, ka, d);  // in flight during the transform
+                wfwd_all_fp<2, E, true>(v, col, CS2, lane, swf, qd, qi, warp);
+                mack(a[0], a[1], v[0], kb, ka);
+#else
                 wfwd_all_fp<2, E, true>(v, col, CS2, lane, swf, qd, qi, warp);
                 mac(a[0], a[1], v[0], d);
+#endif
                 mac(a[0], a[1], v[1], d + 1);
             } else {
 #pragma unroll

@@ -25,6 +25,12 @@ constexpr u64 kSmallQ = u64(1) << 55;  // lazy-bound threshold of the SQ path
 #ifndef NTT_MIN_BLOCKS
 #define NTT_MIN_BLOCKS 3
 #endif
+#ifndef NTT_COLS_PAIR
+#define NTT_COLS_PAIR 1  // FP64 column phase: polys in interleaved pairs (1) or one at a time, next prefetched (0)
+#endif
+#ifndef NTT_CHUNK_STAGE
+#define NTT_CHUNK_STAGE 0
+#endif
 #ifndef NTT_CHUNK_MIN_BLOCKS
 #define NTT_CHUNK_MIN_BLOCKS 2  // registers for two interleaved transforms (measured best)
 #endif
@@ -417,8 +423,24 @@ constexpr size_t col_smem() {  // two tiles + twiddles
     return size_t(8) * (16 * WGeo<E>::CS + 2 * WGeo<E>::TW_COL);
 }
 template <int E>
-constexpr size_t chunk_smem() {  // exchange columns of two transforms per warp + twiddles
-    return size_t(8) * (16 * WGeo<E>::CS + 2 * WGeo<E>::TW_CHUNK);
+constexpr size_t chunk_smem() {  // exchange columns of two transforms per warp + twiddles (+ staging)
+    return size_t(8) * (16 * WGeo<E>::CS + 2 * WGeo<E>::TW_CHUNK + (NTT_CHUNK_STAGE ? 16 * (WGeo<E>::M + WGeo<E>::M / 4) : 0));
+}
+// Chunk staging (NTT_CHUNK_STAGE): per warp two polys' chunks, prefetched by
+// 16-byte cp.async while the current pair is transformed (forward: dense,
+// read lane-strided; inverse: 2 pad words per 8, read as 16-byte vectors).
+__device__ __forceinline__ u32 ipad(u32 k) { return k + 2 * (k >> 3); }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const u32 a = static_cast<u32>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(gmem) : "memory");
+}
+template <int E, bool PAD>
+__device__ __forceinline__ void stage_chunk(u64* s, const u64* g, u32 lane) {
+#pragma unroll
+    for (int i = 0; i < WGeo<E>::M / 64; ++i) {
+        const u32 k = 2 * (lane + 32 * i);
+        cp_async16(s + (PAD ? ipad(k) : k), g + k);
+    }
 }
 
 // Column tile (8 columns x M1 rows, element (m, c) at c*CS + wpad(m)) of the
@@ -475,7 +497,7 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
     issue_col_tile<E, 32 * E2>(tiles, src + size_t(p * rpp + r) * N + c0);
     stage_col_twiddles<E, true>(sw, sws, w, w + N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (fp) {  // polys in pairs on the block's two tiles: each staged twiddle feeds two interleaved transforms
+    if (fp && NTT_COLS_PAIR) {  // polys in pairs on the block's two tiles: each staged twiddle feeds two interleaved transforms
         const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
         bool first = true;
         while (p < pend) {
@@ -631,7 +653,7 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
     const u32 r = row0 + blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
     u32 p = next_poly(blockIdx.z * ppb, pend, r, rpp, level, skip_gs);
     if (p >= pend) return;
-    extern __shared__ u64 dyn[];
+    extern __shared__ __align__(16) u64 dyn[];
     u64* sm = dyn;
     u64* sw = dyn + 16 * Gm::CS;
     u64* sws = sw + Gm::TW_CHUNK;
@@ -645,6 +667,49 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
     u64* col = sm + warp * Gm::CS;
     constexpr u32 CS2 = 8 * Gm::CS;  // second transform's column
     auto row = [&](u32 pp) { return data + size_t(pp * rpp + r) * N + off; };
+    if (fp && NTT_CHUNK_STAGE) {
+        constexpr u32 SW = Gm::M + Gm::M / 4;
+        u64* stg = dyn + 16 * Gm::CS + 2 * Gm::TW_CHUNK + warp * 2 * SW;
+        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+        u32 p2 = next_poly(p + 1, pend, r, rpp, level, skip_gs);
+        stage_chunk<E, false>(stg, row(p), lane);
+        if (p2 < pend) stage_chunk<E, false>(stg + SW, row(p2), lane);
+        cp_async_commit();
+        stage_chunk_twiddles<E, true>(sw, sws, w, w + N, logN1, blockIdx.x);
+        __syncthreads();
+        while (true) {
+            const bool pair = p2 < pend;
+            cp_async_wait<0>();
+            __syncwarp();
+            u64 v[2][E];
+#pragma unroll
+            for (int j = 0; j < E; ++j) v[0][j] = stg[lane + 32 * j];
+            if (pair) {
+#pragma unroll
+                for (int j = 0; j < E; ++j) v[1][j] = stg[SW + lane + 32 * j];
+            }
+            __syncwarp();
+            const u32 pn = pair ? next_poly(p2 + 1, pend, r, rpp, level, skip_gs) : pend;
+            const u32 pn2 = pn < pend ? next_poly(pn + 1, pend, r, rpp, level, skip_gs) : pend;
+            if (pn < pend) {  // the next pair is in flight during this pair's stages
+                stage_chunk<E, false>(stg, row(pn), lane);
+                if (pn2 < pend) stage_chunk<E, false>(stg + SW, row(pn2), lane);
+            }
+            cp_async_commit();
+            if (pair) {
+                chunk_fwd_fp<2, E>(v, col, CS2, lane, sw, qd, qi, warp, q);
+                st_vec<E>(row(p), v[0], lane);
+                st_vec<E>(row(p2), v[1], lane);
+            } else {
+                chunk_fwd_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), col, CS2, lane, sw, qd, qi, warp, q);
+                st_vec<E>(row(p), v[0], lane);
+            }
+            if (pn >= pend) break;
+            p = pn;
+            p2 = pn2;
+        }
+        return;
+    }
     if (fp) {
         const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
         u32 p2 = next_poly(p + 1, pend, r, rpp, level, skip_gs);
@@ -711,7 +776,7 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
     const u32 r = row0 + blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
     u32 p = blockIdx.z * ppb;
     if (p >= pend) return;
-    extern __shared__ u64 dyn[];
+    extern __shared__ __align__(16) u64 dyn[];
     u64* sm = dyn;
     u64* sw = dyn + 16 * Gm::CS;
     u64* sws = sw + Gm::TW_CHUNK;
@@ -727,6 +792,52 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
     constexpr u32 CS2 = 8 * Gm::CS;
     auto in = [&](u32 pp) { return src + size_t(pp * rpp + r) * N + off; };
     auto out = [&](u32 pp) { return data + size_t(pp * rpp + r) * N + off; };
+    if (fp && NTT_CHUNK_STAGE) {
+        constexpr u32 SW = Gm::M + Gm::M / 4;
+        u64* stg = dyn + 16 * Gm::CS + 2 * Gm::TW_CHUNK + warp * 2 * SW;
+        const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+        stage_chunk<E, true>(stg, in(p), lane);
+        if (p + 1 < pend) stage_chunk<E, true>(stg + SW, in(p + 1), lane);
+        cp_async_commit();
+        stage_chunk_twiddles<E, false>(sw, sws, w, w + N, logN1, blockIdx.x);
+        __syncthreads();
+        const u32 base = ipad(lane << Gm::LOGE);
+        while (true) {
+            const bool pair = p + 1 < pend;
+            cp_async_wait<0>();
+            __syncwarp();
+            u64 v[2][E];
+#pragma unroll
+            for (int n = 0; n < 2; ++n) {
+                if (n == 1 && !pair) break;
+                const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(stg + n * SW + base);
+#pragma unroll
+                for (int j = 0; j < E / 2; ++j) {
+                    const ulonglong2 t = s2[j];
+                    v[n][2 * j] = t.x;
+                    v[n][2 * j + 1] = t.y;
+                }
+            }
+            __syncwarp();
+            const u32 pn = p + (pair ? 2 : 1);
+            if (pn < pend) {
+                stage_chunk<E, true>(stg, in(pn), lane);
+                if (pn + 1 < pend) stage_chunk<E, true>(stg + SW, in(pn + 1), lane);
+            }
+            cp_async_commit();
+            if (pair) {
+                chunk_inv_fp<2, E>(v, col, CS2, lane, sw, qd, qi, warp);
+                st_strided<E>(out(p), v[0], lane);
+                st_strided<E>(out(p + 1), v[1], lane);
+            } else {
+                chunk_inv_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), col, CS2, lane, sw, qd, qi, warp);
+                st_strided<E>(out(p), v[0], lane);
+            }
+            if (pn >= pend) break;
+            p = pn;
+        }
+        return;
+    }
     if (fp) {
         const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
         u64 v[2][E];
@@ -795,7 +906,7 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 r
     issue_col_tile<E, 32 * E2>(tiles, data + size_t(p * rpp + r) * N + c0);
     stage_col_twiddles<E, false>(sw, sws, w, w + N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (fp) {  // polys in pairs on the block's two tiles (see kw_fwd_cols)
+    if (fp && NTT_COLS_PAIR) {  // polys in pairs on the block's two tiles (see kw_fwd_cols)
         const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1], nd = R.qd[4 * mi + 2], ndq = R.qd[4 * mi + 3];
         for (bool first = true; p < pend; first = false) {
             const bool pair = p + 1 < pend;

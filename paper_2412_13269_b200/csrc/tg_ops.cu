@@ -227,6 +227,43 @@ __global__ void k_rescale(DevRing R, u64* out, const u64* in, int level, u32 npo
     }
 }
 
+// rescale_round when every row and q_l take the FP64 path: two coefficients
+// per thread (16-byte accesses) and four rows' words loaded before any is
+// used, so each thread keeps several loads in flight (k_rescale waits on one
+// load per row).
+__global__ void __launch_bounds__(256) k_rescale_fp(DevRing R, u64* out, const u64* in, int level, u32 npolys) {
+    const u32 N = R.N, lvl = u32(level), half = N / 2;
+    const u64 total = u64(npolys) * half;
+    const u64 ql = R.q[lvl], hl = ql >> 1;
+    const double qld = u2d(ql);
+    const double* rsd = R.rsd + size_t(lvl) * R.q_count * 2;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
+        const u64 p = i / half, c = (i - p * half) * 2;
+        const u64* src = in + p * (lvl + 1) * N + c;
+        u64* dst = out + p * lvl * N + c;
+        const ulonglong2 lv = *reinterpret_cast<const ulonglong2*>(src + size_t(lvl) * N);
+        // centred last residues as signed FP64 integers
+        const double x0 = lv.x > hl ? __dsub_rn(u2d(lv.x), qld) : u2d(lv.x);
+        const double x1 = lv.y > hl ? __dsub_rn(u2d(lv.y), qld) : u2d(lv.y);
+        auto one = [&](u32 r, ulonglong2 v) {  // (v - x) * ql^-1, |v - x| < 1.1q: one exact FP64 product each
+            const double qd = R.qd[4 * r], w = rsd[2 * r], wq = rsd[2 * r + 1];
+            const u64 q = R.q[r];
+            *reinterpret_cast<ulonglong2*>(dst + size_t(r) * N) =
+                make_ulonglong2(fp_canon_small(fp_mulmod(__dsub_rn(u2d(v.x), x0), w, wq, qd), q),
+                                fp_canon_small(fp_mulmod(__dsub_rn(u2d(v.y), x1), w, wq, qd), q));
+        };
+        u32 r = 0;
+        for (; r + 4 <= lvl; r += 4) {
+            ulonglong2 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const ulonglong2*>(src + size_t(r + k) * N);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) one(r + k, v[k]);
+        }
+        for (; r < lvl; ++r) one(r, *reinterpret_cast<const ulonglong2*>(src + size_t(r) * N));
+    }
+}
+
 // Eval-form rescale_round, step 1: from the inverse-transformed last row,
 // t_r = centered(last) mod q_r into rows 0..level-1 of the scratch t (same
 // layout as the input, level+1 rows per poly).
@@ -479,6 +516,14 @@ extern "C" int tg_rescale(tg_context* ctx, uint64_t* out, const uint64_t* in, in
     if (npolys == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     PROF(TG_OP_RESCALE, 8.0 * npolys * ctx->ring.N * (2 * level + 1));
+    bool all_fp = true;
+    for (int r = 0; r <= level; ++r) all_fp &= ctx->h_q[r] < kFpMaxQ;
+    if (all_fp) {
+        k_rescale_fp<<<grid_for(size_t(npolys) * ctx->ring.N / 2), 256, 0, as_stream(stream)>>>(ctx->ring, out, in,
+                                                                                                level, npolys);
+        TG_LAUNCH_CHECK();
+        return TG_OK;
+    }
     k_rescale<<<grid_for(size_t(npolys) * ctx->ring.N), kThreads, 0, as_stream(stream)>>>(ctx->ring, out, in, level,
                                                                                           npolys);
     TG_LAUNCH_CHECK();
