@@ -220,6 +220,87 @@ __global__ void __launch_bounds__(kThreads) k_lincomb_fp(DevRing R, LinComb L, u
     }
 }
 
+// k_lincomb_fp with two coefficients per thread (16-byte loads and stores)
+// and the next row's words loaded while the current row is combined: four
+// times the loads in flight per thread (the one-coefficient kernel waits on
+// NT loads per row; the fused ladder steps have NT = 1..2).
+template <int NT>
+__global__ void __launch_bounds__(kThreads) k_lincomb_fp2(DevRing R, LinComb L, u64* __restrict__ out) {
+    const u32 N = R.N, lvl = u32(L.level), half = N / 2;
+    const u32 rout = L.rescale ? lvl : lvl + 1;
+    const u64 total = u64(L.nparts) * half;
+    for (u64 i = blockIdx.x * u64(kThreads) + threadIdx.x; i < total; i += u64(gridDim.x) * kThreads) {
+        const u32 p = u32(i / half), c = u32(i - u64(p) * half) * 2;
+        const bool addp = p < L.add_polys;
+        const bool add0 = addp && (L.add_all || c == 0), add1 = addp && L.add_all;
+        const u64* base[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) base[t] = u32(t) < L.nterms ? L.ptr[t] + p * L.pstride[t] + c : nullptr;
+        auto load = [&](u32 r, ulonglong2 (&x)[NT]) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+                if (u32(t) < L.nterms) x[t] = *reinterpret_cast<const ulonglong2*>(base[t] + size_t(r) * N);
+        };
+        // sum_t c_t x_t (+ const) for both coefficients, reduced to |.| <= q/2 + 1
+        auto comb = [&](u32 r, const ulonglong2 (&x)[NT], double& o0, double& o1) {
+            const double qd = R.qd[4 * r], qi = R.qd[4 * r + 1];
+            const double ad = u2d(L.add[r]);
+            double a0 = add0 ? ad : 0.0, a1 = add1 ? ad : 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                if (u32(t) < L.nterms) {
+                    const double w = __longlong_as_double(static_cast<long long>(L.c[t][r]));
+                    const double wq = __longlong_as_double(static_cast<long long>(L.cs[t][r]));
+                    a0 = __dadd_rn(a0, fp_mulmod(u2d(x[t].x), w, wq, qd));
+                    a1 = __dadd_rn(a1, fp_mulmod(u2d(x[t].y), w, wq, qd));
+                }
+                if ((t & 7) == 7) {
+                    a0 = fp_reduce(a0, qd, qi);
+                    a1 = fp_reduce(a1, qd, qi);
+                }
+            }
+            o0 = fp_reduce(a0, qd, qi);
+            o1 = fp_reduce(a1, qd, qi);
+        };
+        u64* dst = out + size_t(p) * rout * N + c;
+        ulonglong2 xa[NT], xb[NT];
+        if (!L.rescale) {
+            load(0, xa);
+            for (u32 r = 0; r <= lvl; ++r) {
+                if (r < lvl) load(r + 1, (r & 1) ? xa : xb);
+                double o0, o1;
+                comb(r, (r & 1) ? xb : xa, o0, o1);
+                const u64 q = R.q[r];
+                *reinterpret_cast<ulonglong2*>(dst + size_t(r) * N) =
+                    make_ulonglong2(fp_canon_small(o0, q), fp_canon_small(o1, q));
+            }
+            continue;
+        }
+        // rescale_round (ring.hpp:493-518): centred last row, then
+        // (v_r - x) * ql^-1 per row (see k_lincomb)
+        const double ql = R.qd[4 * lvl], hl = double(R.q[lvl] >> 1);
+        double x0, x1;
+        load(lvl, xa);
+        load(0, xb);
+        comb(lvl, xa, x0, x1);
+        if (x0 > hl) x0 = __dsub_rn(x0, ql);
+        if (x0 < -hl) x0 = __dadd_rn(x0, ql);
+        if (x1 > hl) x1 = __dsub_rn(x1, ql);
+        if (x1 < -hl) x1 = __dadd_rn(x1, ql);
+        const double* rsd = R.rsd + size_t(lvl) * R.q_count * 2;
+        for (u32 r = 0; r < lvl; ++r) {  // row r's words are in xb (r even) / xa (r odd)
+            if (r + 1 < lvl) load(r + 1, (r & 1) ? xb : xa);
+            double v0, v1;
+            comb(r, (r & 1) ? xa : xb, v0, v1);
+            const double qd = R.qd[4 * r], w = rsd[2 * r], wq = rsd[2 * r + 1];
+            const u64 q = R.q[r];
+            *reinterpret_cast<ulonglong2*>(dst + size_t(r) * N) =
+                make_ulonglong2(fp_canon_small(fp_mulmod(__dsub_rn(v0, x0), w, wq, qd), q),
+                                fp_canon_small(fp_mulmod(__dsub_rn(v1, x1), w, wq, qd), q));
+        }
+    }
+}
+
 }  // namespace
 }  // namespace tg
 
@@ -275,9 +356,10 @@ extern "C" int tg_lincomb_batch(tg_context* ctx, uint64_t* out, uint32_t nterms,
                    as_stream(stream));
     const u32 grid = grid_for(size_t(nparts) * R.N);
     cudaStream_t st = as_stream(stream);
-    if (L.all_fp && nterms <= 1) k_lincomb_fp<1><<<grid, kThreads, 0, st>>>(R, L, out);
-    else if (L.all_fp && nterms <= 2) k_lincomb_fp<2><<<grid, kThreads, 0, st>>>(R, L, out);
-    else if (L.all_fp && nterms <= 4) k_lincomb_fp<4><<<grid, kThreads, 0, st>>>(R, L, out);
+    const u32 grid2 = grid_for(size_t(nparts) * R.N / 2);
+    if (L.all_fp && nterms <= 1) k_lincomb_fp2<1><<<grid2, kThreads, 0, st>>>(R, L, out);
+    else if (L.all_fp && nterms <= 2) k_lincomb_fp2<2><<<grid2, kThreads, 0, st>>>(R, L, out);
+    else if (L.all_fp && nterms <= 4) k_lincomb_fp2<4><<<grid2, kThreads, 0, st>>>(R, L, out);
     else if (L.all_fp && nterms <= 8) k_lincomb_fp<8><<<grid, kThreads, 0, st>>>(R, L, out);
     else k_lincomb<<<grid, kThreads, 0, st>>>(R, L, out);
     TG_LAUNCH_CHECK();
