@@ -30,7 +30,13 @@ inline u32 grid_for(size_t work) {
 // and only the other rows are computed, 4 at a time for ILP. Terms are
 // accumulated lazily (Shoup outputs in [0,2q), sum < 2*active*q < 2^64,
 // checked on the host) and reduced once per output.
-constexpr u32 kMUThreads = 128;
+#ifndef MODUP_THREADS
+#define MODUP_THREADS 128
+#endif
+#ifndef MODUP_CPT8
+#define MODUP_CPT8 2  // coefficients per thread of the group-size <= 8 ModUp (measured)
+#endif
+constexpr u32 kMUThreads = MODUP_THREADS;
 
 __global__ void __launch_bounds__(kMUThreads)
 k_modup(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict__ d, int level,
@@ -787,7 +793,7 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
         if (G.lazy_modup && G.group_size <= 4)
             launch_modup_v<4, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
         else if (G.lazy_modup && G.group_size <= 8)
-            launch_modup_v<8, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
+            launch_modup_v<8, MODUP_CPT8>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
         else if (G.lazy_modup && G.group_size <= 16)
             launch_modup_v<16, 1>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
         else
