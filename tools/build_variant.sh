@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build a copy of the extension with extra nvcc flags into variants/<name>/
-# (A/B kernel experiments: PYTHONPATH=variants/<name> python tools/nttbench.py).
+# (A/B kernel experiments: TG_ROOT=variants/<name> python tools/nttbench.py).
 #   tools/build_variant.sh <name> "<nvcc flags>"
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)

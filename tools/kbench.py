@@ -15,7 +15,8 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-sys.path.insert(0, str(ROOT))
+# TG_ROOT: load the package from a variant build (tools/build_variant.sh)
+sys.path.insert(0, os.environ.get("TG_ROOT", str(ROOT)))
 
 
 def main():

@@ -13,13 +13,15 @@ a forward->inverse round-trip check.
 from __future__ import annotations
 
 import argparse
+import os
 import ctypes
 import json
 import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-sys.path.insert(0, str(ROOT))
+# TG_ROOT: load the package from a variant build (tools/build_variant.sh)
+sys.path.insert(0, os.environ.get("TG_ROOT", str(ROOT)))
 
 DEFAULT_CASES = "fwd:16:20:0,fwd:32:20:7,inv:16:20:7,inv:16:20:0,fwd:4:20:7,inv:2:10:7"
 
@@ -50,6 +52,7 @@ def main():
     ee = np.ascontiguousarray(ring.eval_exp_table(), dtype=np.uint32)
     se = np.ascontiguousarray(ring.slot_of_exp_table(), dtype=np.uint32)
     L = load_c_abi()
+    print("library:", L._name, flush=True)
     P64, P32, VP = ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_void_p
     ctx = VP()
     moda = np.array(mods, dtype=np.uint64)
