@@ -445,12 +445,16 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
             for (int cc = 0; cc < CPT; ++cc) y[i][cc] = shoup(x[cc], w, ws, q);
         }
     }
-    // sources as exact doubles once (FP64 targets), not per target row
-    double yd[GMAX][CPT];
+    // sources as exact doubles once (FP64 targets), not per target row; the
+    // 16-source variant converts per use (registers: measured slower hoisted)
+    constexpr bool kHoist = GMAX <= 8;
+    double yd[kHoist ? GMAX : 1][CPT];
+    if constexpr (kHoist) {
 #pragma unroll
-    for (int i = 0; i < GMAX; ++i)
+        for (int i = 0; i < GMAX; ++i)
 #pragma unroll
-        for (int cc = 0; cc < CPT; ++cc) yd[i][cc] = (src_fp && u32(i) < active) ? u2d(y[i][cc]) : 0.0;
+            for (int cc = 0; cc < CPT; ++cc) yd[i][cc] = (src_fp && u32(i) < active) ? u2d(y[i][cc]) : 0.0;
+    }
     for (u32 v = v_begin; v < v_end; ++v) {
         const u64 q = sq[v];
         const ulonglong2* wr = smw + size_t(v) * active;
@@ -468,7 +472,8 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
                     const double wq = __longlong_as_double(static_cast<long long>(w.y));
 #pragma unroll
                     for (int cc = 0; cc < CPT; ++cc) {
-                        acc[cc] = __dadd_rn(acc[cc], fp_mulmod(yd[i][cc], wd, wq, qd));
+                        const double yv = kHoist ? yd[kHoist ? i : 0][cc] : u2d(y[i][cc]);
+                        acc[cc] = __dadd_rn(acc[cc], fp_mulmod(yv, wd, wq, qd));
                         if ((i & 7) == 7 && u32(i + 1) < active) acc[cc] = fp_reduce(acc[cc], qd, qi);
                     }
                 }
