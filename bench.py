@@ -40,7 +40,7 @@ from pathlib import Path
 import numpy as np
 
 ROOT = Path(__file__).resolve().parent
-sys.path.insert(0, str(ROOT))
+sys.path.insert(0, os.environ.get("TG_ROOT", str(ROOT)))  # TG_ROOT: a variant build (tools/build_variant.sh)
 
 RECORDS_PER_CT = None  # set from the spec
 

@@ -360,7 +360,7 @@ extern "C" int tg_lincomb_batch(tg_context* ctx, uint64_t* out, uint32_t nterms,
     if (L.all_fp && nterms <= 1) k_lincomb_fp2<1><<<grid2, kThreads, 0, st>>>(R, L, out);
     else if (L.all_fp && nterms <= 2) k_lincomb_fp2<2><<<grid2, kThreads, 0, st>>>(R, L, out);
     else if (L.all_fp && nterms <= 4) k_lincomb_fp2<4><<<grid2, kThreads, 0, st>>>(R, L, out);
-    else if (L.all_fp && nterms <= 8) k_lincomb_fp<8><<<grid, kThreads, 0, st>>>(R, L, out);
+    else if (L.all_fp && nterms <= 8) k_lincomb_fp2<8><<<grid2, kThreads, 0, st>>>(R, L, out);
     else k_lincomb<<<grid, kThreads, 0, st>>>(R, L, out);
     TG_LAUNCH_CHECK();
     return TG_OK;
