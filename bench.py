@@ -138,6 +138,24 @@ class _CAI:
                                          "strides": None}
 
 
+FP64_PEAK_OPS = 18.3e12  # DP ops/s, tools/diag/fp64_peak.cu on this pool's B200 (61-63 ops/clk/SM at 1965 MHz)
+
+
+def fp64_roofline(prof, N):
+    """FP64-pipe roofline of the NTT classes: algorithmic ops (8 per
+    butterfly) per second vs the measured FP64 peak."""
+    import math
+    ms = sum(v[0] for k, v in prof.items() if k.startswith("ntt"))
+    byts = sum(v[2] for k, v in prof.items() if k.startswith("ntt"))
+    if ms <= 0:
+        return None
+    ops = byts * math.log2(N) / 4.0
+    ach = ops / (ms / 1e3)
+    return {"kernel": "ntt (fwd+inv)", "achieved": round(ach / 1e12, 3), "peak": FP64_PEAK_OPS / 1e12,
+            "unit": "TFLOP/s (FP64 DP ops, 8 per butterfly)", "frac": round(ach / FP64_PEAK_OPS, 4),
+            "peak_kind": "measured (tools/diag/fp64_peak.cu: DADD/DMUL/DFMA throughput probe)"}
+
+
 def reduce_partial_to_root(G, torch, dist, ct, ext_stream, N):
     """Integer NCCL sum of every rank's partial ciphertext into rank 0's
     buffer (exact: ranks * q < 2^64 for the <=60-bit q-chain), then the mod-q
@@ -582,6 +600,10 @@ def run_b200(args):
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                 "bytes_per_launch": dbytes / dn, "ms_per_launch": per_launch_ms,
                 "share_of_step": round(dms / total_prof_ms, 3),
+                # the NTT's actual bound is the FP64 pipe: algorithmic
+                # FP64 ops = 8 per butterfly (exact modmul 6 + add/sub 2), N/2 log N
+                # butterflies per row = bytes * log N / 4, against the measured pipe peak
+                "fp64": fp64_roofline(prof, spec.N) if dname.startswith("ntt") else None,
                 "per_kernel": {k: {"ms": round(v[0] / args.steps, 4), "launches": v[1] // args.steps,
                                    "GBps": round((v[2] / v[1]) / ((v[0] / v[1]) / 1e3) / 1e9, 1)}
                                for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}}
