@@ -216,23 +216,16 @@ void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32
         R, acc, digits, nd, npolys, ppb, key, level, WGeo<E1>::LOGM, own_gs, add0, add1, pmod);
 }
 
-template <int E1, int E2>
-void launch_fwd_cols_only(const DevRing& R, int sms, u64* data, u32 rpp, u32 npolys, int level, cudaStream_t s,
-                          u32 skip_gs) {
-    set_smem_attrs<E1, E2>();
-    const u32 M2 = 32 * E2;
-    const u32 p1 = polys_per_block(M2 / 8, rpp, npolys, sms);
-    kw_fwd_cols<E1, E2><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(
-        R, data, data, rpp, npolys, p1, level, skip_gs, 0);
-}
-
-template <int E1, int E2>
-void launch_inv_cols_only(const DevRing& R, int sms, u64* data, u32 rpp, u32 npolys, int level, cudaStream_t s) {
-    set_smem_attrs<E1, E2>();
-    const u32 M2 = 32 * E2;
-    const u32 p1 = polys_per_block(M2 / 8, rpp, npolys, sms);
-    kw_inv_cols<E1, E2><<<dim3(M2 / 8, rpp, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys,
-                                                                                          p1, level, 0);
+// every modulus on the FP64 path and no integer-row knob: column-pair kernels
+bool ntt_pair_ok(const tg_context* ctx) {
+    static const bool off = [] {
+        const char* e = getenv("TG_NTT_PAIR");
+        return e && *e == '0';
+    }();
+    if (off || ctx->ring.int_every != 0) return false;
+    for (u64 q : ctx->h_q)
+        if (q >= kFpMaxQ) return false;
+    return true;
 }
 
 }  // namespace
@@ -253,9 +246,10 @@ int ntt_forward_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 np
     const DevRing& R = ctx->ring;
     const u32 rpp = u32(level + 1 + nspecial);
     ProfScope prof(ctx, TG_OP_NTT_FWD, 8.0 * rpp * npolys * R.N, s);  // half a transform's bytes
-    if (R.logN == 16) launch_fwd_cols_only<8, 8>(R, ctx->sms, data, rpp, npolys, level, s, skip_gs);
-    else if (R.logN == 15) launch_fwd_cols_only<4, 8>(R, ctx->sms, data, rpp, npolys, level, s, skip_gs);
-    else launch_fwd_cols_only<4, 4>(R, ctx->sms, data, rpp, npolys, level, s, skip_gs);
+    const bool pair = ntt_pair_ok(ctx);
+    if (R.logN == 16) launch_fwd_cols_any<8, 8>(R, ctx->sms, data, data, rpp, npolys, level, s, skip_gs, 0, rpp, pair);
+    else if (R.logN == 15) launch_fwd_cols_any<4, 8>(R, ctx->sms, data, data, rpp, npolys, level, s, skip_gs, 0, rpp, pair);
+    else launch_fwd_cols_any<4, 4>(R, ctx->sms, data, data, rpp, npolys, level, s, skip_gs, 0, rpp, pair);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -264,9 +258,10 @@ int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 np
     const DevRing& R = ctx->ring;
     const u32 rpp = u32(level + 1 + nspecial);
     ProfScope prof(ctx, TG_OP_NTT_INV, 8.0 * rpp * npolys * R.N, s);
-    if (R.logN == 16) launch_inv_cols_only<8, 8>(R, ctx->sms, data, rpp, npolys, level, s);
-    else if (R.logN == 15) launch_inv_cols_only<4, 8>(R, ctx->sms, data, rpp, npolys, level, s);
-    else launch_inv_cols_only<4, 4>(R, ctx->sms, data, rpp, npolys, level, s);
+    const bool pair = ntt_pair_ok(ctx);
+    if (R.logN == 16) launch_inv_cols_any<8, 8>(R, ctx->sms, data, rpp, npolys, level, s, 0, rpp, pair);
+    else if (R.logN == 15) launch_inv_cols_any<4, 8>(R, ctx->sms, data, rpp, npolys, level, s, 0, rpp, pair);
+    else launch_inv_cols_any<4, 4>(R, ctx->sms, data, rpp, npolys, level, s, 0, rpp, pair);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -306,10 +301,11 @@ int ntt_forward_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
     ProfScope prof(ctx, TG_OP_NTT_FWD, 16.0 * nrows * npolys * R.N, s, 2);
     int e1 = 0, e2 = 0;
+    const bool pair = ntt_pair_ok(ctx);
     if (warp_plan(R.logN, e1, e2) && npolys <= 65535) {
-        if (e1 == 8) launch_fwd_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows);
-        else if (e2 == 8) launch_fwd_w<4, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows);
-        else launch_fwd_w<4, 4>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows);
+        if (e1 == 8) launch_fwd_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows, pair);
+        else if (e2 == 8) launch_fwd_w<4, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows, pair);
+        else launch_fwd_w<4, 4>(R, ctx->sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows, pair);
         TG_LAUNCH_CHECK();
         return TG_OK;
     }
@@ -343,10 +339,11 @@ int ntt_inverse_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
     const size_t sm1 = size_t(8) << (p.logN1 + p.logC), sm2 = size_t(8) << (p.logN2 + p.logCpb);
     ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * nrows * npolys * R.N, s, 2);
     int e1 = 0, e2 = 0;
+    const bool pair = ntt_pair_ok(ctx);
     if (warp_plan(R.logN, e1, e2) && npolys <= 65535) {
-        if (e1 == 8) launch_inv_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, row0, nrows);
-        else if (e2 == 8) launch_inv_w<4, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, row0, nrows);
-        else launch_inv_w<4, 4>(R, ctx->sms, data, src, rpp, npolys, level, s, row0, nrows);
+        if (e1 == 8) launch_inv_w<8, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, row0, nrows, pair);
+        else if (e2 == 8) launch_inv_w<4, 8>(R, ctx->sms, data, src, rpp, npolys, level, s, row0, nrows, pair);
+        else launch_inv_w<4, 4>(R, ctx->sms, data, src, rpp, npolys, level, s, row0, nrows, pair);
         TG_LAUNCH_CHECK();
         return TG_OK;
     }

@@ -986,6 +986,8 @@ kw_inv_cols(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 r
     }
 }
 
+#include "tg_ntt_cols2.cuh"
+
 // (E1, E2) for N = M1 * M2 handled by the warp kernels.
 inline bool warp_plan(u32 logN, int& e1, int& e2) {
     switch (logN) {
@@ -1004,6 +1006,8 @@ void set_smem_attrs() {
         cudaFuncSetAttribute(kw_inv_cols<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(col_smem<E1>()));
         cudaFuncSetAttribute(kw_fwd_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
         cudaFuncSetAttribute(kw_inv_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
+        cudaFuncSetAttribute(kw_fwd_cols2<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pair_smem<E1>()));
+        cudaFuncSetAttribute(kw_inv_cols2<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pair_smem<E1>()));
         return true;
     }();
     (void)done;
@@ -1017,26 +1021,56 @@ inline u32 polys_per_block(u32 blocks_per_row, u32 rpp, u32 npolys, int sms) {
     return u32(ppb < 1 ? 1 : ppb > npolys ? npolys : ppb);
 }
 
+// Column phases: the column-pair kernels when every row is FP64 (pair).
 template <int E1, int E2>
-void launch_fwd_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp, u32 npolys, int level,
-                  cudaStream_t s, u32 skip_gs, u32 row0, u32 nrows) {
+void launch_fwd_cols_any(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp, u32 npolys, int level,
+                         cudaStream_t s, u32 skip_gs, u32 row0, u32 nrows, bool pair) {
     set_smem_attrs<E1, E2>();
-    const u32 M1 = 32 * E1, M2 = 32 * E2;
-    const u32 p1 = polys_per_block(M2 / 8, nrows, npolys, sms), p2 = polys_per_block(M1 / 8, nrows, npolys, sms);
+    const u32 M2 = 32 * E2;
+    if (pair && E1 == 8) {  // column pairs (tg_ntt_cols2.cuh), N = 2^16
+        const u32 p1 = polys_per_block(M2 / 16, nrows, npolys, sms);
+        kw_fwd_cols2<E1, E2><<<dim3(M2 / 16, nrows, (npolys + p1 - 1) / p1), 256, pair_smem<E1>(), s>>>(
+            R, data, src, rpp, npolys, p1, level, skip_gs, row0);
+        return;
+    }
+    const u32 p1 = polys_per_block(M2 / 8, nrows, npolys, sms);
     kw_fwd_cols<E1, E2><<<dim3(M2 / 8, nrows, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(
         R, data, src, rpp, npolys, p1, level, skip_gs, row0);
+}
+template <int E1, int E2>
+void launch_inv_cols_any(const DevRing& R, int sms, u64* data, u32 rpp, u32 npolys, int level, cudaStream_t s,
+                         u32 row0, u32 nrows, bool pair) {
+    set_smem_attrs<E1, E2>();
+    const u32 M2 = 32 * E2;
+    if (pair && E1 == 8) {
+        const u32 p1 = polys_per_block(M2 / 16, nrows, npolys, sms);
+        kw_inv_cols2<E1, E2><<<dim3(M2 / 16, nrows, (npolys + p1 - 1) / p1), 256, pair_smem<E1>(), s>>>(
+            R, data, rpp, npolys, p1, level, row0);
+        return;
+    }
+    const u32 p1 = polys_per_block(M2 / 8, nrows, npolys, sms);
+    kw_inv_cols<E1, E2><<<dim3(M2 / 8, nrows, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys,
+                                                                                           p1, level, row0);
+}
+
+template <int E1, int E2>
+void launch_fwd_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp, u32 npolys, int level,
+                  cudaStream_t s, u32 skip_gs, u32 row0, u32 nrows, bool pair = false) {
+    set_smem_attrs<E1, E2>();
+    const u32 M1 = 32 * E1;
+    const u32 p2 = polys_per_block(M1 / 8, nrows, npolys, sms);
+    launch_fwd_cols_any<E1, E2>(R, sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows, pair);
     kw_fwd_chunks<E2><<<dim3(M1 / 8, nrows, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
         R, data, rpp, npolys, p2, level, WGeo<E1>::LOGM, skip_gs, row0);
 }
 
 template <int E1, int E2>
 void launch_inv_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp, u32 npolys, int level,
-                  cudaStream_t s, u32 row0, u32 nrows) {
+                  cudaStream_t s, u32 row0, u32 nrows, bool pair = false) {
     set_smem_attrs<E1, E2>();
-    const u32 M1 = 32 * E1, M2 = 32 * E2;
-    const u32 p1 = polys_per_block(M2 / 8, nrows, npolys, sms), p2 = polys_per_block(M1 / 8, nrows, npolys, sms);
+    const u32 M1 = 32 * E1;
+    const u32 p2 = polys_per_block(M1 / 8, nrows, npolys, sms);
     kw_inv_chunks<E2><<<dim3(M1 / 8, nrows, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
         R, data, src, rpp, npolys, p2, level, WGeo<E1>::LOGM, row0);
-    kw_inv_cols<E1, E2><<<dim3(M2 / 8, nrows, (npolys + p1 - 1) / p1), 256, col_smem<E1>(), s>>>(R, data, rpp, npolys,
-                                                                                           p1, level, row0);
+    launch_inv_cols_any<E1, E2>(R, sms, data, rpp, npolys, level, s, row0, nrows, pair);
 }
