@@ -128,9 +128,12 @@ __device__ __forceinline__ void store_pair_tile(const double2* tile, u64* rb) {
     }
 }
 
+#ifndef NTT_PAIR_PREFETCH
+#define NTT_PAIR_PREFETCH 1  // two tiles: the next poly's tile loads during the current transform
+#endif
 template <int E>
-constexpr size_t pair_smem() {  // 8 column-pair tiles + column twiddles
-    return size_t(16) * 8 * PGeo<E>::M + size_t(8) * 2 * WGeo<E>::TW_COL;
+constexpr size_t pair_smem() {  // column-pair tile(s) + column twiddles
+    return size_t(16) * 8 * PGeo<E>::M * (NTT_PAIR_PREFETCH ? 2 : 1) + size_t(8) * 2 * WGeo<E>::TW_COL;
 }
 
 // Phase 1 forward (all rows FP64): 16 columns x M1 rows per poly, stages
@@ -145,19 +148,32 @@ kw_fwd_cols2(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb,
     u32 p = next_poly(blockIdx.z * ppb, pend, r, rpp, level, skip_gs);
     if (p >= pend) return;
     extern __shared__ __align__(16) u64 dyn[];
-    double2* tile = reinterpret_cast<double2*>(dyn);
-    u64* sw = dyn + 16 * Pg::M;  // after the M x 8 units of the tile
+    constexpr u32 NT = NTT_PAIR_PREFETCH ? 2 : 1;
+    u64* sw = dyn + 16 * Pg::M * NT;  // after the M x 8 units of each tile
     const u32 mi = mod_index(r, level, R.q_count);
     const u64* w = reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N);
     const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
     const u32 c0 = blockIdx.x * 16;
-    issue_pair_tile<E, N2>(tile, src + size_t(p * rpp + r) * N + c0);
+    issue_pair_tile<E, N2>(reinterpret_cast<double2*>(dyn), src + size_t(p * rpp + r) * N + c0);
     stage_col_twiddles<E, true>(sw, nullptr, w, w + N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double2* pr = tile;
-    for (bool first = true; p < pend; first = false) {
-        if (!first) issue_pair_tile<E, N2>(tile, src + size_t(p * rpp + r) * N + c0);
-        cp_async_wait<0>();
+    for (u32 cur = 0, first = 1; p < pend; first = 0) {
+        const u32 pn = next_poly(p + 1, pend, r, rpp, level, skip_gs);
+        double2* tile = reinterpret_cast<double2*>(dyn) + cur * 8 * Pg::M;
+        if constexpr (NT == 2) {
+            if (pn < pend) {  // next poly's tile in flight during this transform
+                issue_pair_tile<E, N2>(reinterpret_cast<double2*>(dyn) + (cur ^ 1) * 8 * Pg::M,
+                                       src + size_t(pn * rpp + r) * N + c0);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+        } else {
+            if (!first) issue_pair_tile<E, N2>(tile, src + size_t(p * rpp + r) * N + c0);
+            cp_async_wait<0>();
+        }
+        (void)first;
+        double2* pr = tile;
         __syncthreads();
         double v[2][E];
 #pragma unroll
@@ -172,8 +188,9 @@ kw_fwd_cols2(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb,
         for (int j = 0; j < E; ++j) pr[pu((lane << WGeo<E>::LOGE) | j, warp)] = make_double2(v[0][j], v[1][j]);
         __syncthreads();
         store_pair_tile<E, N2>(tile, data + size_t(p * rpp + r) * N + c0);
-        __syncthreads();
-        p = next_poly(p + 1, pend, r, rpp, level, skip_gs);
+        __syncthreads();  // the tile is the next prefetch target
+        p = pn;
+        cur ^= (NT - 1);
     }
 }
 
@@ -187,20 +204,32 @@ kw_inv_cols2(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 
     u32 p = blockIdx.z * ppb;
     if (p >= pend) return;
     extern __shared__ __align__(16) u64 dyn[];
-    double2* tile = reinterpret_cast<double2*>(dyn);
-    u64* sw = dyn + 16 * Pg::M;  // after the M x 8 units of the tile
+    constexpr u32 NT = NTT_PAIR_PREFETCH ? 2 : 1;
+    u64* sw = dyn + 16 * Pg::M * NT;
     const u32 mi = mod_index(r, level, R.q_count);
     const u64 q = R.q[mi];
     const u64* w = reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N + 2 * size_t(N));
     const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1], nd = R.qd[4 * mi + 2], ndq = R.qd[4 * mi + 3];
     const u32 c0 = blockIdx.x * 16;
-    issue_pair_tile<E, N2>(tile, data + size_t(p * rpp + r) * N + c0);
+    issue_pair_tile<E, N2>(reinterpret_cast<double2*>(dyn), data + size_t(p * rpp + r) * N + c0);
     stage_col_twiddles<E, false>(sw, nullptr, w, w + N);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double2* pr = tile;
-    for (bool first = true; p < pend; first = false, ++p) {
-        if (!first) issue_pair_tile<E, N2>(tile, data + size_t(p * rpp + r) * N + c0);
-        cp_async_wait<0>();
+    for (u32 cur = 0, first = 1; p < pend; first = 0, ++p, cur ^= (NT - 1)) {
+        double2* tile = reinterpret_cast<double2*>(dyn) + cur * 8 * Pg::M;
+        if constexpr (NT == 2) {
+            if (p + 1 < pend) {
+                issue_pair_tile<E, N2>(reinterpret_cast<double2*>(dyn) + (cur ^ 1) * 8 * Pg::M,
+                                       data + size_t((p + 1) * rpp + r) * N + c0);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+        } else {
+            if (!first) issue_pair_tile<E, N2>(tile, data + size_t(p * rpp + r) * N + c0);
+            cp_async_wait<0>();
+        }
+        (void)first;
+        double2* pr = tile;
         __syncthreads();
         double v[2][E];
 #pragma unroll
@@ -220,6 +249,6 @@ kw_inv_cols2(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 
         }
         __syncthreads();
         store_pair_tile<E, N2>(tile, data + size_t(p * rpp + r) * N + c0);
-        __syncthreads();
+        __syncthreads();  // the tile is the next prefetch target
     }
 }
