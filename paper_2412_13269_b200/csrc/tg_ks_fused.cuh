@@ -53,7 +53,7 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
     __syncthreads();
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
-    u64* col = dyn + warp * Gm::CS;
+    u64* col = dyn + warp * 2 * Gm::CS;  // the warp's contiguous pair-exchange region
     constexpr u32 CS2 = 8 * Gm::CS;
     const size_t words = size_t(rows) * N, key_rows = R.nmod;
     const bool addq = add0 && r <= u32(level);
@@ -122,10 +122,10 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
 #if KS_KEY_PREFETCH
                 ulonglong2 kb[E / 2], ka[E / 2];
                 kload(kb, ka, d);  // in flight during the transform
-                wfwd_all_fp<2, E, true>(v, col, CS2, lane, swf, qd, qi, warp);
+                wfwd_all_fp<2, E, true, true>(v, col, CS2, lane, swf, qd, qi, warp);
                 mack(a[0], a[1], v[0], kb, ka);
 #else
-                wfwd_all_fp<2, E, true>(v, col, CS2, lane, swf, qd, qi, warp);
+                wfwd_all_fp<2, E, true, true>(v, col, CS2, lane, swf, qd, qi, warp);
                 mac(a[0], a[1], v[0], d);
 #endif
                 mac(a[0], a[1], v[1], d + 1);
@@ -177,7 +177,7 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
         }
         // inverse chunk phase of both accumulators (layout 0 in, layout 5 out),
         // doubles (|v| <= 1.5q, raw bits) to the inverse column phase
-        winv_all_fp<2, E, true>(a, col, CS2, lane, swi, qd, qi, warp);
+        winv_all_fp<2, E, true, true>(a, col, CS2, lane, swi, qd, qi, warp);
         u64* o0 = acc + (size_t(b) * rows + r) * N + off;
         u64* o1 = acc + (size_t(npolys + b) * rows + r) * N + off;
 #pragma unroll

@@ -262,42 +262,66 @@ __device__ __forceinline__ void wxchg_fp(double (&v)[NP][E], u64* colw, u32 cs, 
     }
 }
 
-template <int NP, int E, bool CHUNK>
+// NP = 2 exchange with both transforms' values of element k moved as one
+// 16-byte word, in the warp's contiguous 2*CS-word region: half the shared-
+// memory instructions of two separate columns, conflict-free (wpad).
+template <int E>
+__device__ __forceinline__ void wxchg_fp_pair(double (&v)[2][E], u64* colw, u32 lane, u32 lo_from, u32 lo_to) {
+    constexpr int LOGE = WGeo<E>::LOGE;
+    double2* pr = reinterpret_cast<double2*>(colw);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < E; ++j) pr[wpad(wins<LOGE>(lane, u32(j), lo_from))] = make_double2(v[0][j], v[1][j]);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const double2 t = pr[wpad(wins<LOGE>(lane, u32(j), lo_to))];
+        v[0][j] = t.x;
+        v[1][j] = t.y;
+    }
+}
+template <int NP, int E, bool PX>
+__device__ __forceinline__ void wxchg_any(double (&v)[NP][E], u64* col, u32 cs, u32 lane, u32 lo_from, u32 lo_to) {
+    if constexpr (PX && NP == 2) wxchg_fp_pair<E>(v, col, lane, lo_from, lo_to);
+    else wxchg_fp<NP, E>(v, col, cs, lane, lo_from, lo_to);
+}
+
+template <int NP, int E, bool CHUNK, bool PX = false>
 __device__ __forceinline__ void wfwd_all_fp(double (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double q,
                                             double qi, u32 c) {
     if constexpr (E == 8) {
         wfwd_fp<NP, 8, CHUNK, 5, 7, 5>(v, lane, sw, q, qi, c);
-        wxchg_fp<NP, 8>(v, col, cs, lane, 5, 2);
+        wxchg_any<NP, 8, PX>(v, col, cs, lane, 5, 2);
         wfwd_fp<NP, 8, CHUNK, 2, 4, 2>(v, lane, sw, q, qi, c);
-        wxchg_fp<NP, 8>(v, col, cs, lane, 2, 0);
+        wxchg_any<NP, 8, PX>(v, col, cs, lane, 2, 0);
         wfwd_fp<NP, 8, CHUNK, 0, 1, 0>(v, lane, sw, q, qi, c);
     } else {
         wfwd_fp<NP, 4, CHUNK, 5, 6, 5>(v, lane, sw, q, qi, c);
-        wxchg_fp<NP, 4>(v, col, cs, lane, 5, 3);
+        wxchg_any<NP, 4, PX>(v, col, cs, lane, 5, 3);
         wfwd_fp<NP, 4, CHUNK, 3, 4, 3>(v, lane, sw, q, qi, c);
-        wxchg_fp<NP, 4>(v, col, cs, lane, 3, 1);
+        wxchg_any<NP, 4, PX>(v, col, cs, lane, 3, 1);
         wfwd_fp<NP, 4, CHUNK, 1, 2, 1>(v, lane, sw, q, qi, c);
-        wxchg_fp<NP, 4>(v, col, cs, lane, 1, 0);
+        wxchg_any<NP, 4, PX>(v, col, cs, lane, 1, 0);
         wfwd_fp<NP, 4, CHUNK, 0, 0, 0>(v, lane, sw, q, qi, c);
     }
 }
 
-template <int NP, int E, bool CHUNK>
+template <int NP, int E, bool CHUNK, bool PX = false>
 __device__ __forceinline__ void winv_all_fp(double (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double q,
                                             double qi, u32 c) {
     if constexpr (E == 8) {
         winv_fp<NP, 8, CHUNK, 0, 0, 2>(v, lane, sw, q, qi, c);
-        wxchg_fp<NP, 8>(v, col, cs, lane, 0, 3);
+        wxchg_any<NP, 8, PX>(v, col, cs, lane, 0, 3);
         winv_fp<NP, 8, CHUNK, 3, 3, 5>(v, lane, sw, q, qi, c);
-        wxchg_fp<NP, 8>(v, col, cs, lane, 3, 5);
+        wxchg_any<NP, 8, PX>(v, col, cs, lane, 3, 5);
         winv_fp<NP, 8, CHUNK, 5, 6, 7>(v, lane, sw, q, qi, c);
     } else {
         winv_fp<NP, 4, CHUNK, 0, 0, 1>(v, lane, sw, q, qi, c);
-        wxchg_fp<NP, 4>(v, col, cs, lane, 0, 2);
+        wxchg_any<NP, 4, PX>(v, col, cs, lane, 0, 2);
         winv_fp<NP, 4, CHUNK, 2, 2, 3>(v, lane, sw, q, qi, c);
-        wxchg_fp<NP, 4>(v, col, cs, lane, 2, 4);
+        wxchg_any<NP, 4, PX>(v, col, cs, lane, 2, 4);
         winv_fp<NP, 4, CHUNK, 4, 4, 5>(v, lane, sw, q, qi, c);
-        wxchg_fp<NP, 4>(v, col, cs, lane, 4, 5);
+        wxchg_any<NP, 4, PX>(v, col, cs, lane, 4, 5);
         winv_fp<NP, 4, CHUNK, 5, 6, 6>(v, lane, sw, q, qi, c);
     }
 }
@@ -611,7 +635,7 @@ __device__ __forceinline__ void st_vec(u64* x, const u64 (&v)[E], u32 lane) {
 }
 
 // FP64 chunk phase of NP polys: forward (phase-1 doubles in, canonical out)
-template <int NP, int E>
+template <int NP, int E, bool PX = false>
 __device__ __forceinline__ void chunk_fwd_fp(u64 (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double qd,
                                              double qi, u32 warp, u64 q) {
     double vd[NP][E];
@@ -619,14 +643,14 @@ __device__ __forceinline__ void chunk_fwd_fp(u64 (&v)[NP][E], u64* col, u32 cs, 
     for (int n = 0; n < NP; ++n)
 #pragma unroll
         for (int j = 0; j < E; ++j) vd[n][j] = __longlong_as_double(static_cast<long long>(v[n][j]));
-    wfwd_all_fp<NP, E, true>(vd, col, cs, lane, sw, qd, qi, warp);
+    wfwd_all_fp<NP, E, true, PX>(vd, col, cs, lane, sw, qd, qi, warp);
 #pragma unroll
     for (int n = 0; n < NP; ++n)
 #pragma unroll
         for (int j = 0; j < E; ++j) v[n][j] = fp_canon_small(vd[n][j], q);  // |vd| <= q/2 + 1 (fp_reduce)
 }
 // inverse (canonical in, doubles |v| <= 1.5q as raw bits out to phase B)
-template <int NP, int E>
+template <int NP, int E, bool PX = false>
 __device__ __forceinline__ void chunk_inv_fp(u64 (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double qd,
                                              double qi, u32 warp) {
     double vd[NP][E];
@@ -634,7 +658,7 @@ __device__ __forceinline__ void chunk_inv_fp(u64 (&v)[NP][E], u64* col, u32 cs, 
     for (int n = 0; n < NP; ++n)
 #pragma unroll
         for (int j = 0; j < E; ++j) vd[n][j] = u2d(v[n][j]);
-    winv_all_fp<NP, E, true>(vd, col, cs, lane, sw, qd, qi, warp);
+    winv_all_fp<NP, E, true, PX>(vd, col, cs, lane, sw, qd, qi, warp);
 #pragma unroll
     for (int n = 0; n < NP; ++n)
 #pragma unroll
@@ -665,6 +689,7 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
     u64* col = sm + warp * Gm::CS;
+    u64* colp = sm + warp * 2 * Gm::CS;  // FP64 paths: the warp's contiguous pair region
     constexpr u32 CS2 = 8 * Gm::CS;  // second transform's column
     auto row = [&](u32 pp) { return data + size_t(pp * rpp + r) * N + off; };
     if (fp && NTT_CHUNK_STAGE) {
@@ -697,11 +722,11 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
             }
             cp_async_commit();
             if (pair) {
-                chunk_fwd_fp<2, E>(v, col, CS2, lane, sw, qd, qi, warp, q);
+                chunk_fwd_fp<2, E, true>(v, colp, CS2, lane, sw, qd, qi, warp, q);
                 st_vec<E>(row(p), v[0], lane);
                 st_vec<E>(row(p2), v[1], lane);
             } else {
-                chunk_fwd_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), col, CS2, lane, sw, qd, qi, warp, q);
+                chunk_fwd_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), colp, CS2, lane, sw, qd, qi, warp, q);
                 st_vec<E>(row(p), v[0], lane);
             }
             if (pn >= pend) break;
@@ -720,12 +745,12 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
         __syncthreads();
         while (true) {
             if (p2 < pend) {
-                chunk_fwd_fp<2, E>(v, col, CS2, lane, sw, qd, qi, warp, q);
+                chunk_fwd_fp<2, E, true>(v, colp, CS2, lane, sw, qd, qi, warp, q);
                 st_vec<E>(row(p), v[0], lane);
                 st_vec<E>(row(p2), v[1], lane);
                 p = next_poly(p2 + 1, pend, r, rpp, level, skip_gs);
             } else {
-                chunk_fwd_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), col, CS2, lane, sw, qd, qi, warp, q);
+                chunk_fwd_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), colp, CS2, lane, sw, qd, qi, warp, q);
                 st_vec<E>(row(p), v[0], lane);
                 p = p2;
             }
@@ -789,6 +814,7 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
     u64* col = sm + warp * Gm::CS;
+    u64* colp = sm + warp * 2 * Gm::CS;  // FP64 paths: the warp's contiguous pair region
     constexpr u32 CS2 = 8 * Gm::CS;
     auto in = [&](u32 pp) { return src + size_t(pp * rpp + r) * N + off; };
     auto out = [&](u32 pp) { return data + size_t(pp * rpp + r) * N + off; };
@@ -826,11 +852,11 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
             }
             cp_async_commit();
             if (pair) {
-                chunk_inv_fp<2, E>(v, col, CS2, lane, sw, qd, qi, warp);
+                chunk_inv_fp<2, E, true>(v, colp, CS2, lane, sw, qd, qi, warp);
                 st_strided<E>(out(p), v[0], lane);
                 st_strided<E>(out(p + 1), v[1], lane);
             } else {
-                chunk_inv_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), col, CS2, lane, sw, qd, qi, warp);
+                chunk_inv_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), colp, CS2, lane, sw, qd, qi, warp);
                 st_strided<E>(out(p), v[0], lane);
             }
             if (pn >= pend) break;
@@ -847,12 +873,12 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
         __syncthreads();
         while (true) {
             if (p + 1 < pend) {
-                chunk_inv_fp<2, E>(v, col, CS2, lane, sw, qd, qi, warp);
+                chunk_inv_fp<2, E, true>(v, colp, CS2, lane, sw, qd, qi, warp);
                 st_strided<E>(out(p), v[0], lane);
                 st_strided<E>(out(p + 1), v[1], lane);
                 p += 2;
             } else {
-                chunk_inv_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), col, CS2, lane, sw, qd, qi, warp);
+                chunk_inv_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), colp, CS2, lane, sw, qd, qi, warp);
                 st_strided<E>(out(p), v[0], lane);
                 p += 1;
             }
