@@ -267,17 +267,21 @@ class Statement:
         self.mine = D.shard(spec.n_cts, world, rank)
         q = W.statement_query_inputs(self.S, self.d)
         self.blocks = [W.statement_block_inputs(self.S, self.d, b) for b in self.mine]
-        # client ciphertexts in the order the query consumes them: weights,
-        # thresholds, then the record columns (staged uploads, e2e)
+        # client ciphertexts in the order the query consumes them (staged
+        # uploads, e2e): each threshold job needs its column and ONE threshold,
+        # so the first job (risk: weights + t2) starts after 198 MB, not after
+        # all three thresholds as well
         nb = len(self.blocks)
-        self.client = q.ct_w + q.ct_t + [b.ct_sugar for b in self.blocks] + [b.ct_bp for b in self.blocks]
-        self.upload_groups = {"w": (0, 8), "t": (8, 11), "sugar": (11, 11 + nb), "bp": (11 + nb, 11 + 2 * nb)}
+        self.client = (q.ct_w + [q.ct_t[2], q.ct_t[0]] + [b.ct_sugar for b in self.blocks] + [q.ct_t[1]] +
+                       [b.ct_bp for b in self.blocks])
+        self.upload_groups = {"w": (0, 8), "t2": (8, 9), "t0": (9, 10), "sugar": (10, 10 + nb),
+                              "t1": (10 + nb, 11 + nb), "bp": (11 + nb, 11 + 2 * nb)}
 
     def _bind(self, client, blocks):
         from types import SimpleNamespace as NS
         nb = len(blocks)
-        q = NS(ct_w=client[:8], ct_t=client[8:11])
-        bl = [NS(ct_sugar=client[11 + i], ct_bp=client[11 + nb + i], pt_attr=b.pt_attr,
+        q = NS(ct_w=client[:8], ct_t=[client[9], client[10 + nb], client[8]])
+        bl = [NS(ct_sugar=client[10 + i], ct_bp=client[11 + nb + i], pt_attr=b.pt_attr,
                  attr_scale=b.attr_scale, pt_flag=b.pt_flag, flag_scale=b.flag_scale)
               for i, b in enumerate(blocks)]
         return q, bl

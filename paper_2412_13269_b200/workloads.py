@@ -392,7 +392,7 @@ def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8, 
     `batch` independent ciphertexts; tests/test_gpu_statement.py); launches
     and switching-key reads are shared by the batch.
     ready (optional, staged uploads): ready(name) makes the current stream
-    wait until the client ciphertexts `name` ("w", "t", "sugar", "bp") are
+    wait until the client ciphertexts `name` ("w", "t0".."t2", "sugar", "bp") are
     resident, so each job starts as soon as its own inputs have arrived."""
     T, ev, keys = S.T, S.ev, S.keys
     wait = ready or (lambda name: None)
@@ -410,7 +410,7 @@ def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8, 
 
     def job(j):
         ch, col, k, norm = j
-        wait("t")
+        wait(f"t{k}")  # this column's threshold only
         if col != "risk":
             wait(col)
         xs = [risks[b] if col == "risk" else getattr(blocks[b], "ct_" + col) for b in ch]
