@@ -33,6 +33,40 @@ inline u32 grid_for(size_t work) {
 #ifndef MODUP_THREADS
 #define MODUP_THREADS 128
 #endif
+// ModUp target rows of an all-FP64 digit with A active sources known at
+// compile time: no per-term predicates or branches in the row loop (ncu: the
+// generic loop spent ~60 integer/branch instructions per row around ~90 FP64
+// ones). Same terms, same bounds, same order as the generic FP64 path.
+template <int A, int CPT, int GMAX>
+__device__ __forceinline__ void modup_rows_fp(const double (&yd)[GMAX][CPT], const ulonglong2* smw, const u64* sq,
+                                              u32 nrest, u32 v_begin, u32 v_end, u32 first, u64* out, u32 N) {
+    for (u32 v = v_begin; v < v_end; ++v) {
+        const u64 q = sq[v];
+        const double qd = u2d(q), qi = __longlong_as_double(static_cast<long long>(sq[nrest + v]));
+        const ulonglong2* wr = smw + size_t(v) * A;
+        const u32 r = v < first ? v : v + A;
+        double acc[CPT];
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) acc[cc] = 0.0;
+#pragma unroll
+        for (int i = 0; i < A; ++i) {
+            const ulonglong2 w = wr[i];
+            const double wd = __longlong_as_double(static_cast<long long>(w.x));
+            const double wq = __longlong_as_double(static_cast<long long>(w.y));
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) {
+                acc[cc] = __dadd_rn(acc[cc], fp_mulmod(yd[i][cc], wd, wq, qd));
+                if ((i & 7) == 7 && i + 1 < A) acc[cc] = fp_reduce(acc[cc], qd, qi);
+            }
+        }
+        u64 o[CPT];
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) o[cc] = fp_canon_small(fp_reduce(acc[cc], qd, qi), q);
+        if constexpr (CPT == 2) *reinterpret_cast<ulonglong2*>(out + size_t(r) * N) = make_ulonglong2(o[0], o[1]);
+        else out[size_t(r) * N] = o[0];
+    }
+}
+
 #ifndef MODUP_CPT16
 #define MODUP_CPT16 2  // measured: 110 -> 108 ms (config 5)
 #endif
@@ -409,14 +443,16 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
             smw[e] = make_ulonglong2(cw[0], cw[1]);
         }
     }
+    int tgt_fp = 1;  // every target row of this digit on the FP64 path
     for (u32 v = threadIdx.x; v < nrest; v += kMUThreads) {
         const u32 t = mod_index(v < first ? v : v + active, level, R.q_count);
         sq[v] = R.q[t];
         sq[nrest + v] = src_fp && R.q[t] < kFpMaxQ
                             ? static_cast<u64>(__double_as_longlong(__ddiv_rn(1.0, u2d(R.q[t]))))
                             : R.one_shoup[t];
+        tgt_fp &= (src_fp && R.q[t] < kFpMaxQ) ? 1 : 0;
     }
-    __syncthreads();
+    const bool all_fp = __syncthreads_and(tgt_fp) != 0;
     const u32 c0 = (blockIdx.x * kMUThreads + threadIdx.x) * CPT;
     if (c0 >= N) return;
     u64* out = digits + size_t(j) * rows_out * N + c0;
@@ -457,6 +493,22 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
         for (int i = 0; i < GMAX; ++i)
 #pragma unroll
             for (int cc = 0; cc < CPT; ++cc) yd[i][cc] = (src_fp && u32(i) < active) ? u2d(y[i][cc]) : 0.0;
+    }
+    if constexpr (kHoist) {
+        if (all_fp) {  // block-uniform: the source count as a compile-time constant
+            u64* o = out;
+            const u32 vb = v_begin, ve = v_end;
+            switch (active) {
+#define TG_MU_CASE(A) \
+    case A:           \
+        if constexpr (A <= GMAX) modup_rows_fp<A, CPT, GMAX>(yd, smw, sq, nrest, vb, ve, first, o, N); \
+        return;
+                TG_MU_CASE(1) TG_MU_CASE(2) TG_MU_CASE(3) TG_MU_CASE(4)
+                TG_MU_CASE(5) TG_MU_CASE(6) TG_MU_CASE(7) TG_MU_CASE(8)
+#undef TG_MU_CASE
+                default: break;
+            }
+        }
     }
     for (u32 v = v_begin; v < v_end; ++v) {
         const u64 q = sq[v];
