@@ -82,3 +82,21 @@ def test_chebyshev_pipelines_identical(G, R, setups, deg):
     # the result's eval form is cached: the next product does not re-transform it
     nxt = g.ev.mul_relin(out[True][0], out[True][0], g.keys)
     assert nxt.level() == out[True][0].level()
+
+
+@pytest.mark.parametrize("batch", [1, 2])
+def test_eval_pipeline_warp_ntt_n65536(G, gpu_available, batch):
+    """The same identities at N = 2^16 with 50-bit q-chain AND special primes:
+    the warp NTT kernels with row ranges (rescale_eval's single inverse row
+    and per-modulus forward rows) on the column-pair path, and the fused
+    key-switch core in the coefficient-form reference products."""
+    g = make_setup(G, N=1 << 16, nq=6, K=3, group_size=3, seed=73, q_bits=50, sp_bits=50, h=192)
+    vals = np.linspace(-0.9, 0.8, 64)
+    xs = [enc_slots(g, vals * (i + 1) / 4, 2.0 ** 45, G.Rng(30 + i)) for i in range(batch)]
+    ys = [enc_slots(g, vals[::-1], 2.0 ** 45, G.Rng(40 + i)) for i in range(batch)]
+    x = G.stack_ciphertexts(xs) if batch > 1 else xs[0]
+    y = G.stack_ciphertexts(ys) if batch > 1 else ys[0]
+    want_c = _coeff(g.ev.mul_relin(x, y, g.keys))
+    assert_ct_equal(_coeff(g.ev.mul_relin_eval(x, y, g.keys)), want_c, f"relinearize_eval N=2^16 B={batch}")
+    rs = g.ev.rescale_eval(g.ev.mul_relin_eval(x, y, g.keys))
+    assert_ct_equal(_coeff(rs), g.ev.rescale(want_c), f"rescale_eval N=2^16 B={batch}")
