@@ -13,6 +13,7 @@
 // intermediate of a batched launch stays in the 126 MB L2). Butterflies are
 // Harvey-lazy: values live in [0,4q) (forward) / [0,2q) (inverse) and are
 // made canonical only at the end of the last phase.
+#include <cstdlib>
 #include <utility>
 
 #include "tg_internal.cuh"
@@ -210,6 +211,11 @@ void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32
     // batch split so that the grid covers about two waves (2 blocks per SM)
     const u64 base = u64(M1 / 8) * rows;
     u32 z = u32(std::min<u64>(npolys, (u64(sms) * 4 + base - 1) / base));
+    static const int zf = [] {  // experiments: TG_KS_Z forces the batch split
+        const char* e = getenv("TG_KS_Z");
+        return e ? atoi(e) : 0;
+    }();
+    if (zf > 0) z = std::min<u32>(npolys, u32(zf));
     if (z < 1) z = 1;
     const u32 ppb = (npolys + z - 1) / z;
     kw_ks_chunks<E2><<<dim3(M1 / 8, rows, (npolys + ppb - 1) / ppb), 256, ks_chunk_smem<E2>(), s>>>(
