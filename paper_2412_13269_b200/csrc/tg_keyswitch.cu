@@ -10,6 +10,8 @@
 // One thread owns one coefficient of one digit (ModUp) / one output poly
 // (ModDown) and keeps the <=16 source residues in registers, so each source
 // word is read once and each output word written once.
+#include <type_traits>
+
 #include "tg_internal.cuh"
 #include "tg_fp64.cuh"
 
@@ -37,8 +39,8 @@ inline u32 grid_for(size_t work) {
 // compile time: no per-term predicates or branches in the row loop (ncu: the
 // generic loop spent ~60 integer/branch instructions per row around ~90 FP64
 // ones). Same terms, same bounds, same order as the generic FP64 path.
-template <int A, int CPT, int GMAX>
-__device__ __forceinline__ void modup_rows_fp(const double (&yd)[GMAX][CPT], const ulonglong2* smw, const u64* sq,
+template <int A, int CPT, int GMAX, class Y>
+__device__ __forceinline__ void modup_rows_fp(const Y (&yd)[GMAX][CPT], const ulonglong2* smw, const u64* sq,
                                               u32 nrest, u32 v_begin, u32 v_end, u32 first, u64* out, u32 N) {
     for (u32 v = v_begin; v < v_end; ++v) {
         const u64 q = sq[v];
@@ -55,7 +57,10 @@ __device__ __forceinline__ void modup_rows_fp(const double (&yd)[GMAX][CPT], con
             const double wq = __longlong_as_double(static_cast<long long>(w.y));
 #pragma unroll
             for (int cc = 0; cc < CPT; ++cc) {
-                acc[cc] = __dadd_rn(acc[cc], fp_mulmod(yd[i][cc], wd, wq, qd));
+                double yv;  // hoisted doubles, or u64 sources converted per use (16-source groups)
+                if constexpr (sizeof(Y) == 8 && std::is_same<Y, double>::value) yv = yd[i][cc];
+                else yv = u2d(yd[i][cc]);
+                acc[cc] = __dadd_rn(acc[cc], fp_mulmod(yv, wd, wq, qd));
                 if ((i & 7) == 7 && i + 1 < A) acc[cc] = fp_reduce(acc[cc], qd, qi);
             }
         }
@@ -494,20 +499,23 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
 #pragma unroll
             for (int cc = 0; cc < CPT; ++cc) yd[i][cc] = (src_fp && u32(i) < active) ? u2d(y[i][cc]) : 0.0;
     }
-    if constexpr (kHoist) {
-        if (all_fp) {  // block-uniform: the source count as a compile-time constant
-            u64* o = out;
-            const u32 vb = v_begin, ve = v_end;
-            switch (active) {
-#define TG_MU_CASE(A) \
-    case A:           \
-        if constexpr (A <= GMAX) modup_rows_fp<A, CPT, GMAX>(yd, smw, sq, nrest, vb, ve, first, o, N); \
+    if (all_fp) {  // block-uniform: the source count as a compile-time constant
+        u64* o = out;
+        const u32 vb = v_begin, ve = v_end;
+        switch (active) {
+#define TG_MU_CASE(A)                                                                                 \
+    case A:                                                                                           \
+        if constexpr (A <= GMAX) {                                                                    \
+            if constexpr (kHoist) modup_rows_fp<A, CPT, GMAX>(yd, smw, sq, nrest, vb, ve, first, o, N); \
+            else modup_rows_fp<A, CPT, GMAX>(y, smw, sq, nrest, vb, ve, first, o, N);                 \
+        }                                                                                             \
         return;
-                TG_MU_CASE(1) TG_MU_CASE(2) TG_MU_CASE(3) TG_MU_CASE(4)
-                TG_MU_CASE(5) TG_MU_CASE(6) TG_MU_CASE(7) TG_MU_CASE(8)
+            TG_MU_CASE(1) TG_MU_CASE(2) TG_MU_CASE(3) TG_MU_CASE(4)
+            TG_MU_CASE(5) TG_MU_CASE(6) TG_MU_CASE(7) TG_MU_CASE(8)
+            TG_MU_CASE(9) TG_MU_CASE(10) TG_MU_CASE(11) TG_MU_CASE(12)
+            TG_MU_CASE(13) TG_MU_CASE(14) TG_MU_CASE(15) TG_MU_CASE(16)
 #undef TG_MU_CASE
-                default: break;
-            }
+            default: break;
         }
     }
     for (u32 v = v_begin; v < v_end; ++v) {
