@@ -695,11 +695,14 @@ k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restric
 // Host tables (G.mdf): [K][4] (p_s, fl(c_s/p_s), c_s, floor(p_s/2)) with
 // c_s = (P/p_s)^-1 mod p_s; [nq][K][2] (w, fl(w/q_r)) with
 // w = -(P/p_s) P^-1 mod q_r; [nq][4] (P^-1 mod q_r, fl(./q_r), q_r, fl(1/q_r)).
+// KMAX = K exactly (dispatch in mod_down): every per-special loop is
+// compile-time, no predicated terms.
 template <int KMAX>
 __global__ void __launch_bounds__(256)
 k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict__ in, int level, u32 npolys,
               const u64* __restrict__ addend, u32 rows_per_group) {
-    const u32 N = R.N, K = R.K, nq = R.q_count, lvl = u32(level);
+    constexpr u32 K = KMAX;
+    const u32 N = R.N, nq = R.q_count, lvl = u32(level);
     const u32 rin = lvl + 1 + K, rout = lvl + 1;
     const double* ys_t = G.mdf;                         // [K][4]
     const double* w_rs = G.mdf + 4 * K;                 // [nq][K][2]
@@ -894,9 +897,21 @@ int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaS
     ProfScope prof(g->ctx, TG_OP_MOD_DOWN, 8.0 * R.N * npolys * (2.0 * (level + 1) + R.K + (addend ? level + 1 : 0)), s);
     const GadgetDev& G = g->g;
     const int sms = g->ctx->sms;
-    if (G.fp_moddown && R.K <= 8) launch_mod_down_fp<8>(R, G, sms, out, in, level, npolys, addend, s);
-    else if (G.fp_moddown && R.K <= 16) launch_mod_down_fp<16>(R, G, sms, out, in, level, npolys, addend, s);
-    else if (G.lazy_moddown && R.K <= 4) launch_mod_down_v<4, 2>(R, G, sms, out, in, level, npolys, addend, s);
+    bool done = false;
+    if (G.fp_moddown) {
+        done = true;
+        switch (R.K) {
+#define TG_MD_CASE(k) \
+    case k: launch_mod_down_fp<k>(R, G, sms, out, in, level, npolys, addend, s); break;
+            TG_MD_CASE(1) TG_MD_CASE(2) TG_MD_CASE(3) TG_MD_CASE(4) TG_MD_CASE(5) TG_MD_CASE(6) TG_MD_CASE(7)
+            TG_MD_CASE(8) TG_MD_CASE(9) TG_MD_CASE(10) TG_MD_CASE(11) TG_MD_CASE(12) TG_MD_CASE(13)
+            TG_MD_CASE(14) TG_MD_CASE(15) TG_MD_CASE(16)
+#undef TG_MD_CASE
+            default: done = false;
+        }
+    }
+    if (done) {
+    } else if (G.lazy_moddown && R.K <= 4) launch_mod_down_v<4, 2>(R, G, sms, out, in, level, npolys, addend, s);
     else if (G.lazy_moddown && R.K <= 8) launch_mod_down_v<8, 2>(R, G, sms, out, in, level, npolys, addend, s);
     else if (G.lazy_moddown && R.K <= 16) launch_mod_down_v<16, 1>(R, G, sms, out, in, level, npolys, addend, s);
     else k_mod_down<<<grid_for(size_t(npolys) * R.N), kThreads, 0, s>>>(R, G, out, in, level, npolys, addend);
