@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(kThreads) k_lincomb_fp(DevRing R, LinComb L, u
 // and the next row's words loaded while the current row is combined: four
 // times the loads in flight per thread (the one-coefficient kernel waits on
 // NT loads per row; the fused ladder steps have NT = 1..2).
+// NT = the exact term count (dispatch in tg_lincomb_batch): every term loop
+// is compile-time, no predicated terms.
 template <int NT>
 __global__ void __launch_bounds__(kThreads) k_lincomb_fp2(DevRing R, LinComb L, u64* __restrict__ out) {
     const u32 N = R.N, lvl = u32(L.level), half = N / 2;
@@ -235,11 +237,11 @@ __global__ void __launch_bounds__(kThreads) k_lincomb_fp2(DevRing R, LinComb L, 
         const bool add0 = addp && (L.add_all || c == 0), add1 = addp && L.add_all;
         const u64* base[NT];
 #pragma unroll
-        for (int t = 0; t < NT; ++t) base[t] = u32(t) < L.nterms ? L.ptr[t] + p * L.pstride[t] + c : nullptr;
+        for (int t = 0; t < NT; ++t) base[t] = u32(t) < u32(NT) ? L.ptr[t] + p * L.pstride[t] + c : nullptr;
         auto load = [&](u32 r, ulonglong2 (&x)[NT]) {
 #pragma unroll
             for (int t = 0; t < NT; ++t)
-                if (u32(t) < L.nterms) x[t] = *reinterpret_cast<const ulonglong2*>(base[t] + size_t(r) * N);
+                if (u32(t) < u32(NT)) x[t] = *reinterpret_cast<const ulonglong2*>(base[t] + size_t(r) * N);
         };
         // sum_t c_t x_t (+ const) for both coefficients, reduced to |.| <= q/2 + 1
         auto comb = [&](u32 r, const ulonglong2 (&x)[NT], double& o0, double& o1) {
@@ -248,7 +250,7 @@ __global__ void __launch_bounds__(kThreads) k_lincomb_fp2(DevRing R, LinComb L, 
             double a0 = add0 ? ad : 0.0, a1 = add1 ? ad : 0.0;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                if (u32(t) < L.nterms) {
+                if (u32(t) < u32(NT)) {
                     const double w = __longlong_as_double(static_cast<long long>(L.c[t][r]));
                     const double wq = __longlong_as_double(static_cast<long long>(L.cs[t][r]));
                     a0 = __dadd_rn(a0, fp_mulmod(u2d(x[t].x), w, wq, qd));
@@ -357,10 +359,15 @@ extern "C" int tg_lincomb_batch(tg_context* ctx, uint64_t* out, uint32_t nterms,
     const u32 grid = grid_for(size_t(nparts) * R.N);
     cudaStream_t st = as_stream(stream);
     const u32 grid2 = grid_for(size_t(nparts) * R.N / 2);
-    if (L.all_fp && nterms <= 1) k_lincomb_fp2<1><<<grid2, kThreads, 0, st>>>(R, L, out);
-    else if (L.all_fp && nterms <= 2) k_lincomb_fp2<2><<<grid2, kThreads, 0, st>>>(R, L, out);
-    else if (L.all_fp && nterms <= 4) k_lincomb_fp2<4><<<grid2, kThreads, 0, st>>>(R, L, out);
-    else if (L.all_fp && nterms <= 8) k_lincomb_fp2<8><<<grid2, kThreads, 0, st>>>(R, L, out);
+    if (L.all_fp && nterms <= 8) {
+        switch (nterms) {
+#define TG_LC_CASE(n) \
+    case n: k_lincomb_fp2<n><<<grid2, kThreads, 0, st>>>(R, L, out); break;
+            TG_LC_CASE(1) TG_LC_CASE(2) TG_LC_CASE(3) TG_LC_CASE(4) TG_LC_CASE(5) TG_LC_CASE(6) TG_LC_CASE(7)
+            TG_LC_CASE(8)
+#undef TG_LC_CASE
+        }
+    }
     else k_lincomb<<<grid, kThreads, 0, st>>>(R, L, out);
     TG_LAUNCH_CHECK();
     return TG_OK;
