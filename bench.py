@@ -601,7 +601,10 @@ def run_b200(args):
                        "vs_algorithmic": round(tcls["dram_bytes_per_launch"] / (dbytes / dn), 3),
                        "source": str(tf.relative_to(ROOT))}
     roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "frac": round(achieved / peak, 4),
+                # DRAM bytes per launch of the dominant class (ncu capture), details alongside
+                "traffic": round(traffic["bytes_per_launch"]) if traffic else None, "traffic_detail": traffic,
+                "peak_kind": peak_kind,
                 "bytes_per_launch": dbytes / dn, "ms_per_launch": per_launch_ms,
                 "share_of_step": round(dms / total_prof_ms, 3),
                 # the NTT's actual bound is the FP64 pipe: algorithmic
