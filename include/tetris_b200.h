@@ -201,6 +201,14 @@ int tg_raise_level(tg_context* ctx, uint64_t* out, const uint64_t* in, int new_l
  * out (level rows) must not alias in (level+1 rows). */
 int tg_rescale(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, uint32_t npolys,
                void* stream);
+/* Evaluator::add(rescale(in), addend) in one pass (ckks.hpp:315-324 then
+ * :195-210), for rings whose rows 0..level are all below the FP64 bound:
+ * out (out_level+1 rows per poly, packed) = rescale_round(in)[0..out_level]
+ * + addend, coeff form; addend poly p starts at p * addend_stride words and
+ * has at least out_level+1 rows; out_level <= level-1. TG_E_ARG (no work)
+ * when a row is not FP64-eligible: the caller then runs the two ops. */
+int tg_rescale_add(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, uint32_t npolys,
+                   const uint64_t* addend, uint64_t addend_stride, int out_level, void* stream);
 /* rescale_round on eval-form rows (level+1 rows in, level rows out):
  * == NTT(tg_rescale(iNTT(in))) residue for residue, with one inverse row and
  * `level` forward rows per poly instead of level+1 and level. */

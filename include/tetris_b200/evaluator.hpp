@@ -80,6 +80,10 @@ public:
     static u64 scaled_residue(double value, u64 q);
     Ciphertext add_scalar(const Ciphertext& ct, double c) const;
     Ciphertext rescale(const Ciphertext& ct) const;
+    // Extension: add(rescale(prod), y) with identical results (ckks.hpp:315-324
+    // then :195-210), one pass when every row is FP64-eligible and both are
+    // coefficient-form degree-1 batches of the same shape.
+    Ciphertext rescale_add(const Ciphertext& prod, const Ciphertext& y) const;
     Ciphertext rotate(const Ciphertext& ct, u32 k, const EvalKeys& keys) const;
     Ciphertext conjugate(const Ciphertext& ct, const EvalKeys& keys) const;
     // Extension: sum_j mul_plain(cts[j], plains[j], plain_scale) in one

@@ -423,6 +423,39 @@ Ciphertext Evaluator::rescale(const Ciphertext& ct) const {
     return out;
 }
 
+Ciphertext Evaluator::rescale_add(const Ciphertext& prod, const Ciphertext& y) const {
+    auto two_ops = [&] { return add(rescale(prod), y); };
+    if (prod.level() == 0 || prod.form() != Form::coeff || y.form() != Form::coeff) return two_ops();
+    if (prod.degree() != 1 || y.degree() != 1 || prod.batch != y.batch || prod.domain != y.domain) return two_ops();
+    const RingParams& R = ring();
+    const std::size_t np = prod.parts.size();
+    if (y.parts.size() != np || !contiguous(prod.parts, 0, np)) return two_ops();
+    for (std::size_t i = 0; i < np; ++i)
+        if (prod.parts[i].nspecial() != 0 || y.parts[i].nspecial() != 0) return two_ops();
+    for (int r = 0; r <= prod.level(); ++r)
+        if (R.modulus(u32(r)) >= 1351079888211148ull) return two_ops();  // kFpMaxQ (tg_fp64.cuh)
+    const std::size_t ys = contiguous(y.parts, 0, np) ? y.parts[0].words() : detail::uniform_stride(y.parts);
+    if (ys == 0) return two_ops();
+    const u64 ql = R.modulus(u32(prod.level()));
+    // rescale's metadata (ckks.hpp:321-323), then add's (level alignment,
+    // scale check on the rescaled operand first, noise sum)
+    const double pscale = prod.scale / double(ql);
+    const double pnoise = prod.noise_bound / double(ql) + 1.0;
+    const int lvl = std::min(prod.level() - 1, y.level());
+    check_scales_match(pscale, y.scale);
+    std::vector<Poly> dst = fresh_parts(R, int(np), lvl, Form::coeff);
+    check_tg(tg_rescale_add(R.dev(), const_cast<u64*>(dst[0].data()), prod.parts[0].data(), prod.level(), u32(np),
+                            y.parts[0].data(), ys, lvl, R.stream()));
+    Ciphertext out;
+    out.batch = prod.batch;
+    out.parts = std::move(dst);
+    out.scale = pscale;
+    out.domain = prod.domain;
+    out.sk_id = prod.sk_id;
+    out.noise_bound = pnoise + y.noise_bound;
+    return out;
+}
+
 Ciphertext Evaluator::rescale_eval(const Ciphertext& ct) const {
     if (ct.level() == 0) throw TetrisError("ckks", "cannot rescale at level 0");
     Ciphertext out = ct;

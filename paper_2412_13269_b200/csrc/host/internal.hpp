@@ -20,6 +20,10 @@ inline std::vector<Poly> fresh_parts(const RingParams& ring, int n, int level, F
     return out;
 }
 
+// Parts that share one block at a uniform stride (keys.cpp): the stride in
+// words, 0 if the parts are not laid out that way.
+std::size_t uniform_stride(const std::vector<Poly>& parts);
+
 // True if parts[first..first+n) have one shape and sit back to back in one block.
 inline bool contiguous(const std::vector<Poly>& parts, std::size_t first, std::size_t n) {
     if (n == 0 || first + n > parts.size()) return false;

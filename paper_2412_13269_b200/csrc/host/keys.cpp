@@ -123,7 +123,7 @@ Poly SecretKey::shaped(int level, int nspecial) const {
 // Parts that share one block at a uniform stride S (a contiguous block, or
 // one whose level was dropped: each part is then a row prefix of an S-word
 // poly). Returns S in words, 0 if the parts are not laid out that way.
-static std::size_t uniform_stride(const std::vector<Poly>& parts) {
+std::size_t detail::uniform_stride(const std::vector<Poly>& parts) {
     const Poly& p0 = parts[0];
     const std::size_t n = p0.ring().degree();
     std::size_t S = p0.words();
@@ -153,7 +153,7 @@ static void transform_parts(Ciphertext& ct, Form target, bool keep_eval = false)
     for (auto& p : ct.parts) any |= p.form() == from;
     if (!any) return;
     const std::size_t np = ct.parts.size();
-    const std::size_t S = uniform_stride(ct.parts);
+    const std::size_t S = detail::uniform_stride(ct.parts);
     if (S) {
         const Poly& p0 = ct.parts[0];
         const RingParams& ring = p0.ring();
@@ -218,7 +218,7 @@ static void addsub_ct(Ciphertext& x, const Ciphertext& o, int op) {
     const RingParams& ring = p0.ring();
     const int lvl = p0.level(), ns = p0.nspecial();
     // level-dropped views of one block each (aligned operands): one strided launch
-    const std::size_t sx = uniform_stride(x.parts), so = uniform_stride(o.parts);
+    const std::size_t sx = detail::uniform_stride(x.parts), so = detail::uniform_stride(o.parts);
     if (sx && so && op != 2) {
         std::vector<Poly> dst = fresh_parts(ring, int(np), lvl, p0.form(), ns);
         check_tg(tg_poly_addsub_strided(ring.dev(), const_cast<u64*>(dst[0].data()), p0.data(), sx,

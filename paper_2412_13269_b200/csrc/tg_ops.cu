@@ -231,8 +231,13 @@ __global__ void k_rescale(DevRing R, u64* out, const u64* in, int level, u32 npo
 // per thread (16-byte accesses) and four rows' words loaded before any is
 // used, so each thread keeps several loads in flight (k_rescale waits on one
 // load per row).
-__global__ void __launch_bounds__(256) k_rescale_fp(DevRing R, u64* out, const u64* in, int level, u32 npolys) {
+__global__ void __launch_bounds__(256) k_rescale_fp(DevRing R, u64* out, const u64* in, int level, u32 npolys,
+                                                    const u64* __restrict__ add = nullptr, u64 astride = 0,
+                                                    u32 orows = 0) {
+    // add: Evaluator::add of the rescaled rows 0..orows-1 with `add` (poly p at
+    // p * astride words), out packed at orows rows per poly
     const u32 N = R.N, lvl = u32(level), half = N / 2;
+    const u32 nout = add ? orows : lvl;
     const u64 total = u64(npolys) * half;
     const u64 ql = R.q[lvl], hl = ql >> 1;
     const double qld = u2d(ql);
@@ -240,7 +245,8 @@ __global__ void __launch_bounds__(256) k_rescale_fp(DevRing R, u64* out, const u
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
         const u64 p = i / half, c = (i - p * half) * 2;
         const u64* src = in + p * (lvl + 1) * N + c;
-        u64* dst = out + p * lvl * N + c;
+        u64* dst = out + p * nout * N + c;
+        const u64* ad = add ? add + p * astride + c : nullptr;
         const ulonglong2 lv = *reinterpret_cast<const ulonglong2*>(src + size_t(lvl) * N);
         // centred last residues as signed FP64 integers
         const double x0 = lv.x > hl ? __dsub_rn(u2d(lv.x), qld) : u2d(lv.x);
@@ -248,19 +254,24 @@ __global__ void __launch_bounds__(256) k_rescale_fp(DevRing R, u64* out, const u
         auto one = [&](u32 r, ulonglong2 v) {  // (v - x) * ql^-1, |v - x| < 1.1q: one exact FP64 product each
             const double qd = R.qd[4 * r], w = rsd[2 * r], wq = rsd[2 * r + 1];
             const u64 q = R.q[r];
-            *reinterpret_cast<ulonglong2*>(dst + size_t(r) * N) =
-                make_ulonglong2(fp_canon_small(fp_mulmod(__dsub_rn(u2d(v.x), x0), w, wq, qd), q),
-                                fp_canon_small(fp_mulmod(__dsub_rn(u2d(v.y), x1), w, wq, qd), q));
+            u64 o0 = fp_canon_small(fp_mulmod(__dsub_rn(u2d(v.x), x0), w, wq, qd), q);
+            u64 o1 = fp_canon_small(fp_mulmod(__dsub_rn(u2d(v.y), x1), w, wq, qd), q);
+            if (ad) {
+                const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(ad + size_t(r) * N);
+                o0 = add_mod(o0, a.x, q);
+                o1 = add_mod(o1, a.y, q);
+            }
+            *reinterpret_cast<ulonglong2*>(dst + size_t(r) * N) = make_ulonglong2(o0, o1);
         };
         u32 r = 0;
-        for (; r + 4 <= lvl; r += 4) {
+        for (; r + 4 <= nout; r += 4) {
             ulonglong2 v[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const ulonglong2*>(src + size_t(r + k) * N);
 #pragma unroll
             for (int k = 0; k < 4; ++k) one(r + k, v[k]);
         }
-        for (; r < lvl; ++r) one(r, *reinterpret_cast<const ulonglong2*>(src + size_t(r) * N));
+        for (; r < nout; ++r) one(r, *reinterpret_cast<const ulonglong2*>(src + size_t(r) * N));
     }
 }
 
@@ -504,6 +515,24 @@ extern "C" int tg_automorphism(tg_context* ctx, uint64_t* out, const uint64_t* i
         k_auto_coeff<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, in, g);
     else
         k_auto_eval<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, out, in, g);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_rescale_add(tg_context* ctx, uint64_t* out, const uint64_t* in, int level, uint32_t npolys,
+                              const uint64_t* addend, uint64_t addend_stride, int out_level, void* stream) {
+    if (int rc = check_shape(ctx, level, 0)) return rc;
+    TG_REQUIRE(level >= 1, "[ring] cannot rescale at level 0");
+    TG_REQUIRE(out_level >= 0 && out_level <= level - 1, "[ring] rescale_add output level out of range");
+    TG_REQUIRE(addend && addend_stride >= u64(out_level + 1) * ctx->ring.N, "[ring] rescale_add addend shape");
+    TG_REQUIRE(out != in, "[ring] rescale output must not alias its input");
+    for (int r = 0; r <= level; ++r)
+        if (ctx->h_q[r] >= kFpMaxQ) return fail(TG_E_ARG, "[ring] rescale_add needs FP64-eligible rows");
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    PROF(TG_OP_RESCALE, 8.0 * npolys * ctx->ring.N * (level + 1 + 2.0 * (out_level + 1)));
+    k_rescale_fp<<<grid_for(size_t(npolys) * ctx->ring.N / 2), 256, 0, as_stream(stream)>>>(
+        ctx->ring, out, in, level, npolys, addend, addend_stride, u32(out_level + 1));
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
