@@ -300,6 +300,8 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("mul_scalar", &Evaluator::mul_scalar, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("add_scalar", &Evaluator::add_scalar, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("rescale", &Evaluator::rescale, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("rescale_add", &Evaluator::rescale_add, py::keep_alive<0, 1>(),
+             py::call_guard<py::gil_scoped_release>())
         .def("rescale_eval", &Evaluator::rescale_eval, py::keep_alive<0, 1>(),
              py::call_guard<py::gil_scoped_release>())
         .def("mul_relin_eval", &Evaluator::mul_relin_eval, py::keep_alive<0, 1>(),

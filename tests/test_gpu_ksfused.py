@@ -57,3 +57,37 @@ def test_fused_keyswitch_batched(G, R, gpu_available, batch):
     prod = g.ev.rescale(g.ev.mul_relin(G.stack_ciphertexts(xs_g), G.stack_ciphertexts(ys_g), g.keys))
     for i, got in enumerate(G.unstack_ciphertext(prod)):
         assert_ct_equal(got, r.ev.rescale(r.ev.mul_relin(xs_r[i], ys_r[i], r.keys)), f"batched relin block {i}")
+
+
+@pytest.mark.parametrize("N", [1 << 12, 1 << 16])
+def test_rescale_add_matches_add_of_rescale(G, R, gpu_available, N):
+    """Evaluator::rescale_add (one pass) == add(rescale(prod), y) of the
+    reference, for y at a lower / equal / higher level, a level-dropped view,
+    an eval-form y (two-op fallback) and a batch."""
+    kw = dict(N=N, nq=7, K=3, group_size=3, seed=17, q_bits=50, sp_bits=50, h=192)
+    g, r = make_setup(G, **kw), make_setup(R, **kw)
+    top = g.ring.max_level()
+    (a_g, b_g), (a_r, b_r) = _cts(g, 2, top, 5), _cts(r, 2, top, 5)
+    prod_g, prod_r = g.ev.mul_relin(a_g, b_g, g.keys), r.ev.mul_relin(a_r, b_r, r.keys)
+    for ylvl in (top - 3, top - 1, top):
+        (y_g,), (y_r,) = _cts(g, 1, ylvl, 9 + ylvl), _cts(r, 1, ylvl, 9 + ylvl)
+        want = r.ev.add(r.ev.rescale(prod_r), y_r)
+        assert_ct_equal(g.ev.rescale_add(prod_g, y_g), want, f"rescale_add y level {ylvl}")
+    (y_g,), (y_r,) = _cts(g, 1, top, 21), _cts(r, 1, top, 21)
+    yv = y_g.copy()
+    yv.drop_to_level(top - 2)  # a level-dropped view (strided parts)
+    yr = y_r.copy()
+    yr.drop_to_level(top - 2)
+    assert_ct_equal(g.ev.rescale_add(prod_g, yv), r.ev.add(r.ev.rescale(prod_r), yr), "rescale_add view")
+    ye = y_g.copy()
+    ye.to_eval()  # fallback path
+    yre = y_r.copy()
+    yre.to_eval()
+    assert_ct_equal(g.ev.rescale_add(prod_g, ye), r.ev.add(r.ev.rescale(prod_r), yre), "rescale_add eval y")
+    xs_g, ys_g = _cts(g, 3, top, 31), _cts(g, 3, top - 1, 32)
+    xs_r, ys_r = _cts(r, 3, top, 31), _cts(r, 3, top - 1, 32)
+    pb = g.ev.mul_relin(G.stack_ciphertexts(xs_g), G.stack_ciphertexts(xs_g), g.keys)
+    got = G.unstack_ciphertext(g.ev.rescale_add(pb, G.stack_ciphertexts(ys_g)))
+    for i in range(3):
+        want = r.ev.add(r.ev.rescale(r.ev.mul_relin(xs_r[i], xs_r[i], r.keys)), ys_r[i])
+        assert_ct_equal(got[i], want, f"rescale_add batch block {i}")
