@@ -186,22 +186,30 @@ def decrypted_count(G, S, spec, res, plain):
             "count_level": res.level()}
 
 
+def _timed_encode(SR, arr, scale, level, threads):
+    """The reference's own Encoder::encode_slots over every row of `arr`
+    (oracle/_ref binding: the unmodified code on a std::thread pool)."""
+    enc = SR.T.Encoder(SR.ring, SR.spec.slots)
+    return list(enc.encode_slots_many(np.asarray(arr, dtype=np.complex128), scale, level, threads))
+
+
 class ThresholdCount:
     """Config 3: private threshold of every encrypted score block against an
     encrypted threshold (plain norm), summed."""
     metric = "encrypted records/sec per TETRIS threshold-count query (amortized us/record in config)"
     slot_sum = True
+    columns = 1  # threshold jobs per record block
 
     def check(self, res):
         return decrypted_count(self.G, self.S, self.spec, res, self.plain_count())
 
     def __init__(self, G, W, spec, rank=0, world=1, rotations=True, device=True):
-        from paper_2412_13269_b200 import distributed as D
         self.G, self.W, self.spec = G, W, spec
         self.batched, self.max_blocks = True, 8
         self.scores, self.thr, _, _ = W.linear_scores(spec)
-        if not device:  # inputs only (the CPU reference arm)
+        if not device:  # inputs only (the CPU reference arm: no product import)
             return
+        from paper_2412_13269_b200 import distributed as D
         rot = W.inner_sum_rotations(spec.slots) if rotations else []
         self.S = W.make_context(G, spec, rotations=rot)
         self.chain = W.config3_chain(G, spec)
@@ -209,7 +217,7 @@ class ThresholdCount:
         cts, ct_t, _, _ = W.config3_inputs(self.S, ct_indices=self.mine, scores=self.scores, t=self.thr)
         self.client = cts + [ct_t]
 
-    def partial(self, client, streams, mode):
+    def partial(self, client, streams, mode, keep=None):
         cts, ct_t = client[:-1], client[-1]
         if not cts:
             return None
@@ -222,6 +230,8 @@ class ThresholdCount:
         else:
             outs = self.G.eval_private_threshold_plain_norm_many(self.S.ev, cts, ct_t, self.spec.norm, self.chain,
                                                                  self.S.keys, streams, mode)
+        if keep is not None:
+            keep.extend(outs)
         acc = outs[0]
         for o in outs[1:]:
             acc = self.S.ev.add(acc, o)
@@ -230,19 +240,51 @@ class ThresholdCount:
     def plain_count(self):
         return int((self.scores >= self.thr).sum())
 
-    def ref_inputs(self, R, SR, chain_r, host_encode, blocks):
-        n = self.spec.slots
-        cts = [host_encode(self.scores[b * n:(b + 1) * n], 100 + b) for b in blocks]
-        return cts, host_encode([self.thr] * n, 99)
+    def ref_inputs(self, SR, blocks, threads):
+        """Client ciphertexts of `blocks` for the reference arm, encoded by the
+        reference's own Encoder (threaded) and encrypted with the same Rng
+        labels as the B200 arm's (bit-identical inputs)."""
+        W, n, L = self.W, self.spec.slots, SR.ring.max_level()
+        vecs = [self.scores[b * n:(b + 1) * n] for b in blocks] + [[self.thr] * n]
+        t0 = time.perf_counter()
+        ms = _timed_encode(SR, vecs, self.spec.delta, L, threads)
+        enc_s = time.perf_counter() - t0
+        labels = [100 + b for b in blocks] + [99]
+        cts = [SR.ctx.encrypt(SR.sk, m, self.spec.delta, SR.T.Rng(self.spec.seed).split(lab), SR.T.Domain.slots)
+               for m, lab in zip(ms, labels)]
+        return (cts[:-1], cts[-1]), {"client_vectors": len(vecs), "client_encode_s": round(enc_s, 2),
+                                     "server_vectors": 0, "server_encode_s": 0.0}
 
     def ref_step(self, R, SR, chain_r, inp, threads):
+        """The reference's own threshold on every block (thread pool,
+        protocol.hpp:297-311), sum in block order, one inner_sum. Returns
+        (count ciphertext, {phase: seconds})."""
         cts, ct_t = inp
-        return R.threshold_count_pool(SR.ev, cts, ct_t, self.spec.norm, chain_r, SR.keys, self.spec.slots,
-                                      threads, False)[0]
+        t0 = time.perf_counter()
+        acc = R.threshold_count_pool(SR.ev, cts, ct_t, self.spec.norm, chain_r, SR.keys, self.spec.slots,
+                                     threads, False)[0]
+        t1 = time.perf_counter()
+        cnt = R.inner_sum(SR.ev, acc, self.spec.slots, SR.keys)
+        return cnt, {"blocks_s": t1 - t0, "slot_sum_s": time.perf_counter() - t1}
 
-    def gpu_ladder(self, blocks):
-        cts = [self.client[self.mine.index(b)] for b in blocks]
-        return self.partial(cts + [self.client[-1]], len(cts), self.G.PolyEval.ladder)
+    def oracle_check(self, R, W, threads):
+        """Full query through the BSGS oracle (all blocks + inner_sum) vs the
+        product's full query output, residue for residue and by count."""
+        import fullsize as F
+        SR, chain_r = F.oracle_context(R, W, self.spec, self.S, self.chain)
+        cnt_r, outs_r, secs = F.oracle_threshold_count(R, W, SR, chain_r, self.scores, self.thr,
+                                                       list(range(self.spec.n_cts)), threads)
+        keep = []
+        acc = self.partial(self.client, 4, self.G.PolyEval.bsgs, keep=keep)
+        cnt_g = self.G.inner_sum(self.S.ev, acc, self.spec.slots, self.S.keys)
+        same_blocks = all(F.ct_equal(a, b) for a, b in zip(keep, outs_r))
+        return secs, len(outs_r), {
+            "oracle_blocks": list(range(self.spec.n_cts)),
+            "bit_exact_vs_oracle_bsgs": bool(same_blocks and F.ct_equal(cnt_g, cnt_r)),
+            "oracle_decrypted_count": round(F.decrypted_count(SR, cnt_r), 3),
+            "gpu_decrypted_count": round(F.decrypted_count(self.S, cnt_g), 3),
+            "what": "the whole query (all score blocks, sum, inner_sum) through the product path as timed vs the "
+                    "BSGS oracle (oracle/bsgs_ref.py over oracle/_ref)"}
 
 
 class Statement:
@@ -250,17 +292,18 @@ class Statement:
     score, three private thresholds, AND, plaintext flag), summed."""
     metric = "encrypted records/sec per TETRIS query (full statement; amortized us/record in config)"
     slot_sum = True
+    columns = 3
 
     def check(self, res):
         return decrypted_count(self.G, self.S, self.spec, res, self.plain_count())
 
     def __init__(self, G, W, spec, rank=0, world=1, rotations=True, device=True):
-        from paper_2412_13269_b200 import distributed as D
         self.G, self.W, self.spec = G, W, spec
         self.batched, self.max_blocks = True, 8
         self.d = W.statement_data(spec)
-        if not device:  # inputs only (the CPU reference arm)
+        if not device:  # inputs only (the CPU reference arm: no product import)
             return
+        from paper_2412_13269_b200 import distributed as D
         rot = W.inner_sum_rotations(spec.slots) if rotations else []
         self.S = W.make_context(G, spec, rotations=rot)
         self.chain = W.config3_chain(G, spec)
@@ -286,14 +329,14 @@ class Statement:
               for i, b in enumerate(blocks)]
         return q, bl
 
-    def partial(self, client, streams, mode, ready=None):
+    def partial(self, client, streams, mode, ready=None, keep=None):
         if not self.blocks:
             return None
         q, bl = self._bind(client, self.blocks)
         thr = self.W.threshold_fn(self.S, self.chain, mode)
-        if self.batched:  # blocks as ciphertext batches (shared launches and key reads)
+        if self.batched:  # (column, block) jobs as ciphertext batches (shared launches and key reads)
             return self.W.statement_partial_batched(self.S, q, bl, thr, streams=streams, max_blocks=self.max_blocks,
-                                                    ready=ready)
+                                                    ready=ready, keep=keep)
         if ready:
             for name in self.upload_groups:
                 ready(name)
@@ -302,22 +345,47 @@ class Statement:
     def plain_count(self):
         return self.W.statement_plain_count(self.d)
 
-    def ref_inputs(self, R, SR, chain_r, host_encode, blocks):
+    def server_plaintexts(self, S, blocks):
+        """Server-side plaintexts of `blocks` (8 risk attributes + the flag
+        per block): the slot vectors encoded at scale q_L and NTT'd."""
+        n = self.spec.slots
+        return [self.d.attrs[b * n:(b + 1) * n, j] for b in blocks for j in range(8)] + \
+               [self.d.flag[b * n:(b + 1) * n] for b in blocks]
+
+    def ref_inputs(self, SR, blocks, threads):
+        """The query's and `blocks`' inputs for the reference arm: every slot
+        vector encoded by the reference's own Encoder (threaded), client
+        vectors encrypted with the B200 arm's Rng labels (bit-identical)."""
         from types import SimpleNamespace as NS
-        W, d, n, L = self.W, self.d, self.spec.slots, SR.ring.max_level()
-        ct_w = [host_encode([wj] * n, 400 + j) for j, wj in enumerate(d.w)]
-        ct_t = [host_encode([tk] * n, 90 + k) for k, tk in enumerate(d.t)]
-        out = []
+        W, d, n, L, spec = self.W, self.d, self.spec.slots, SR.ring.max_level(), self.spec
+        client = [[wj] * n for wj in d.w] + [[tk] * n for tk in d.t]
+        labels = [400 + j for j in range(8)] + [90, 91, 92]
         for b in blocks:
-            sl = slice(b * n, (b + 1) * n)
-            pts, sc = W.encode_plaintexts(SR, [d.attrs[sl, j] for j in range(8)] + [d.flag[sl]], L)
-            out.append(NS(ct_sugar=host_encode(d.sugar[sl], 200 + b), ct_bp=host_encode(d.bp[sl], 300 + b),
-                          pt_attr=pts[:8], attr_scale=sc, pt_flag=pts[8], flag_scale=sc))
-        return NS(ct_w=ct_w, ct_t=ct_t), out
+            client += [d.sugar[b * n:(b + 1) * n], d.bp[b * n:(b + 1) * n]]
+            labels += [200 + b, 300 + b]
+        t0 = time.perf_counter()
+        ms = _timed_encode(SR, client, spec.delta, L, threads)
+        t1 = time.perf_counter()
+        server = self.server_plaintexts(SR, blocks)
+        scale = float(SR.ring.modulus(L))
+        pts = _timed_encode(SR, server, scale, L, threads)
+        for p in pts:  # eval form for mul_plain (workloads.encode_plaintexts)
+            p.ntt_forward()
+        t2 = time.perf_counter()
+        cts = [SR.ctx.encrypt(SR.sk, m, spec.delta, SR.T.Rng(spec.seed).split(lab), SR.T.Domain.slots)
+               for m, lab in zip(ms, labels)]
+        q = NS(ct_w=cts[:8], ct_t=cts[8:11])
+        nb = len(blocks)
+        out = [NS(ct_sugar=cts[11 + 2 * i], ct_bp=cts[12 + 2 * i], pt_attr=pts[8 * i:8 * i + 8], attr_scale=scale,
+                  pt_flag=pts[8 * nb + i], flag_scale=scale) for i in range(nb)]
+        return (q, out), {"client_vectors": len(client), "client_encode_s": round(t1 - t0, 2),
+                          "server_vectors": len(server), "server_encode_s": round(t2 - t1, 2)}
 
     def ref_step(self, R, SR, chain_r, inp, threads):
-        """The reference's own code path, threads over blocks x thresholds;
-        per block the same ops as workloads.statement_block."""
+        """The reference's own code path: threads over blocks x thresholds
+        (protocol.hpp:297-311), per block the ops of workloads.statement_block,
+        sum in block order, one inner_sum (protocol.hpp:319-323). Returns
+        (count ciphertext, {phase: seconds})."""
         from concurrent.futures import ThreadPoolExecutor
         W, ev, keys = self.W, SR.ev, SR.keys
         q, blocks = inp
@@ -325,27 +393,53 @@ class Statement:
         def thr(x, t, norm):
             return R.eval_private_threshold_plain_norm(ev, x, t, norm, chain_r, keys)
 
+        t0 = time.perf_counter()
         with ThreadPoolExecutor(max(1, threads)) as ex:
             risks = list(ex.map(lambda b: W.linear_score(SR, q.ct_w, b.pt_attr, b.attr_scale), blocks))
             futs = [(ex.submit(thr, b.ct_sugar, q.ct_t[0], 1.0), ex.submit(thr, b.ct_bp, q.ct_t[1], 1.0),
                      ex.submit(thr, r, q.ct_t[2], W.RISK_NORM)) for b, r in zip(blocks, risks)]
-            outs = []
-            for b, (f1, f2, f3) in zip(blocks, futs):
+
+            def finish(i):
+                b, (f1, f2, f3) = blocks[i], futs[i]
                 a = ev.rescale(ev.mul_relin(f1.result(), f2.result(), keys))
                 a = ev.rescale(ev.mul_relin(a, f3.result(), keys))
-                outs.append(ev.rescale(ev.mul_plain(a, b.pt_flag, b.flag_scale)))
+                return ev.rescale(ev.mul_plain(a, b.pt_flag, b.flag_scale))
+
+            outs = list(ex.map(finish, range(len(blocks))))
         acc = outs[0]
         for o in outs[1:]:
             acc = ev.add(acc, o)
-        return acc
+        t1 = time.perf_counter()
+        cnt = R.inner_sum(ev, acc, self.spec.slots, keys)
+        return cnt, {"blocks_s": t1 - t0, "slot_sum_s": time.perf_counter() - t1}
 
-    def gpu_ladder(self, blocks):
-        q, bl = self._bind(self.client, self.blocks)
-        sel = [bl[self.mine.index(b)] for b in blocks]
-        thr = self.W.threshold_fn(self.S, self.chain, self.G.PolyEval.ladder)
-        if self.batched:  # the product path, in ladder mode
-            return self.W.statement_partial_batched(self.S, q, sel, thr, streams=2, max_blocks=self.max_blocks)
-        return self.W.statement_partial(self.S, q, sel, thr, len(sel))
+    def oracle_check(self, R, W, threads):
+        """Blocks 0 and n-1 of the product path as timed (BSGS, record blocks
+        as ciphertext batches) vs the BSGS oracle, residue for residue, and
+        the decrypted count of their sum + inner_sum in both."""
+        import fullsize as F
+        # blocks 0 and n-1, plus the block with the most matching records (by
+        # the plaintext comparator) so that the sampled count is not trivially 0
+        n = self.spec.slots
+        d = self.d
+        hit = (d.sugar >= d.t[0]) & (d.bp >= d.t[1]) & (d.attrs @ d.w >= d.t[2]) & (d.flag > 0)
+        busiest = int(np.argmax(hit[:self.spec.n_cts * n].reshape(self.spec.n_cts, n).sum(axis=1)))
+        ids = sorted({0, self.spec.n_cts - 1, busiest})
+        SR, chain_r = F.oracle_context(R, W, self.spec, self.S, self.chain)
+        outs_r, secs = F.oracle_statement_blocks(R, W, SR, chain_r, self.d, ids, threads)
+        keep = []
+        self.partial(self.client, 4, self.G.PolyEval.bsgs, keep=keep)
+        got = [keep[self.mine.index(b)] for b in ids]
+        same = all(F.ct_equal(a, b) for a, b in zip(got, outs_r))
+        cnt_g, cnt_r = F.sum_and_count(self.S, got), F.sum_and_count(SR, outs_r)
+        return secs, len(ids), {
+            "oracle_blocks": ids,
+            "bit_exact_vs_oracle_bsgs": bool(same and F.ct_equal(cnt_g, cnt_r)),
+            "oracle_decrypted_count": round(F.decrypted_count(SR, cnt_r), 3),
+            "gpu_decrypted_count": round(F.decrypted_count(self.S, cnt_g), 3),
+            "what": f"blocks {ids} of the product path as timed (BSGS, {self.max_blocks}-block ciphertext batches) "
+                    f"vs the BSGS oracle (oracle/bsgs_ref.py over oracle/_ref), residue for residue, and the "
+                    f"decrypted count of their sum + inner_sum"}
 
 
 class LinearScore:
@@ -354,14 +448,15 @@ class LinearScore:
     resident on the server, the 8 weight ciphertexts are the query."""
     metric = "encrypted records/sec per linear-score query (8 pt x ct MACs + rescale per block)"
     slot_sum = False
+    columns = 1
 
     def __init__(self, G, W, spec, rank=0, world=1, rotations=True, device=True):
-        from paper_2412_13269_b200 import distributed as D
         self.G, self.W, self.spec = G, W, spec
         self.batched, self.max_blocks = True, 8
         self.attrs, self.w = W.linear_score_data(spec)
         if not device:
             return
+        from paper_2412_13269_b200 import distributed as D
         self.S = W.make_context(G, spec, relin=False)
         self.chain = None
         self.mine = D.shard(spec.n_cts, world, rank)
@@ -370,7 +465,7 @@ class LinearScore:
         self.plain_scale = inp.plain_scale
         self.client = list(inp.ct_w)
 
-    def partial(self, client, streams, mode):
+    def partial(self, client, streams, mode, keep=None):
         # one stream: each block is a single plaintext-product-sum launch plus
         # a rescale, too small for host threads to pay off, and the weights'
         # eval form is then computed once per step instead of once per stream
@@ -386,23 +481,50 @@ class LinearScore:
             err = max(err, float(np.max(np.abs(got - want))))
         return {"max_abs_err_vs_plaintext": err, "tolerance": 2.0 ** -20, "within_tolerance": err < 2.0 ** -20}
 
-    def ref_inputs(self, R, SR, chain_r, host_encode, blocks):
+    def server_plaintexts(self, S, blocks):
+        n = self.spec.slots
+        return [self.attrs[b * n:(b + 1) * n, j] / self.W.ATTR_NORM for b in blocks for j in range(8)]
+
+    def ref_inputs(self, SR, blocks, threads):
         from types import SimpleNamespace as NS
-        W, n, L = self.W, self.spec.slots, SR.ring.max_level()
-        ct_w = [host_encode([wj] * n, 400 + j) for j, wj in enumerate(self.w)]
-        out = []
-        for b in blocks:
-            pts, sc = W.encode_plaintexts(SR, [self.attrs[b * n:(b + 1) * n, j] / W.ATTR_NORM for j in range(8)], L)
-            out.append(NS(pts=pts, scale=sc))
-        return ct_w, out
+        n, L, spec = self.spec.slots, SR.ring.max_level(), self.spec
+        client = [[wj] * n for wj in self.w]
+        t0 = time.perf_counter()
+        ms = _timed_encode(SR, client, spec.delta, L, threads)
+        t1 = time.perf_counter()
+        server = self.server_plaintexts(SR, blocks)
+        scale = float(SR.ring.modulus(L))
+        pts = _timed_encode(SR, server, scale, L, threads)
+        for p in pts:
+            p.ntt_forward()
+        t2 = time.perf_counter()
+        ct_w = [SR.ctx.encrypt(SR.sk, m, spec.delta, SR.T.Rng(spec.seed).split(400 + j), SR.T.Domain.slots)
+                for j, m in enumerate(ms)]
+        out = [NS(pts=pts[8 * i:8 * i + 8], scale=scale) for i in range(len(blocks))]
+        return (ct_w, out), {"client_vectors": len(client), "client_encode_s": round(t1 - t0, 2),
+                             "server_vectors": len(server), "server_encode_s": round(t2 - t1, 2)}
 
     def ref_step(self, R, SR, chain_r, inp, threads):
+        from concurrent.futures import ThreadPoolExecutor
         ct_w, blocks = inp
-        return [self.W.linear_score(SR, ct_w, b.pts, b.scale) for b in blocks]
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max(1, threads)) as ex:  # one block per thread (protocol.hpp:297-311)
+            out = list(ex.map(lambda b: self.W.linear_score(SR, ct_w, b.pts, b.scale), blocks))
+        return out, {"blocks_s": time.perf_counter() - t0, "slot_sum_s": 0.0}
 
-    def gpu_ladder(self, blocks):
-        return [self.W.linear_score(self.S, self.client, self.blocks[self.mine.index(b)], self.plain_scale)
-                for b in blocks]
+    def oracle_check(self, R, W, threads):
+        """Every block's score through the reference's own mul_plain/add/
+        rescale vs the product's, residue for residue."""
+        import fullsize as F
+        SR, _ = F.oracle_context(R, W, self.spec, self.S, None, rotations=False)
+        inp = W.config2_inputs(SR, self.attrs, self.w)
+        t0 = time.perf_counter()
+        ref = [W.linear_score(SR, inp.ct_w, inp.blocks[b], inp.plain_scale) for b in self.mine]
+        secs = time.perf_counter() - t0
+        got = self.partial(self.client, 1, None)
+        return secs, len(ref), {"oracle_blocks": list(self.mine),
+                                "bit_exact_vs_reference": all(F.ct_equal(a, b) for a, b in zip(got, ref)),
+                                "what": "every block's score vs the reference's mul_plain/add/rescale"}
 
 
 WORKLOADS = {2: LinearScore, 3: ThresholdCount, 4: Statement, 5: Statement}
@@ -489,9 +611,16 @@ def run_b200(args):
         torch.cuda.synchronize()
         return [a.elapsed_time(b) for a, b in times], out
 
+    def fresh_query(streams=None):
+        # every step pays the whole query: memoised eval forms of the client
+        # ciphertexts (weights' forward NTTs) from the previous step dropped
+        for c in wl.client:
+            c.clear_eval_cache()
+        return query(wl.client, streams)
+
     # warm-up
     for _ in range(args.warmup):
-        res = query(wl.client)
+        res = fresh_query()
     barrier()
     # timed region (device-resident inputs)
     prof_region = os.environ.get("TG_PROFILE_REGION") == "1"  # ncu --profile-from-start off
@@ -504,7 +633,7 @@ def run_b200(args):
         barrier()
         if prof_region:
             torch.cuda.cudart().cudaProfilerStart()
-        ms_list, res = timed(lambda: query(wl.client), args.steps)
+        ms_list, res = timed(fresh_query, args.steps)
         if prof_region:
             torch.cuda.cudart().cudaProfilerStop()
         barrier()
@@ -522,7 +651,7 @@ def run_b200(args):
     barrier()
     # one stream here, so every kernel's event-bracketed duration is its own
     # (concurrent streams would time-share the SMs inside the brackets)
-    _, _ = timed(lambda: query(wl.client, streams=1), args.steps)
+    _, _ = timed(lambda: fresh_query(streams=1), args.steps)
     prof = G.profile_read(S.ring)
     G.profile_enable(S.ring, False)
 
@@ -615,6 +744,26 @@ def run_b200(args):
                                    "GBps": round((v[2] / v[1]) / ((v[0] / v[1]) / 1e3) / 1e9, 1)}
                                for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}}
 
+    # server-side plaintext encoding (reported as its own line,
+    # outside the query): this shard's slot vectors -> plaintexts on the device
+    server_enc = None
+    if hasattr(wl, "server_plaintexts"):
+        vecs = wl.server_plaintexts(S, wl.mine)
+        with torch.cuda.stream(ext):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            W.encode_plaintexts(S, vecs, S.ring.max_level())  # warm
+            S.ring.synchronize()
+            a.record(ext)
+            W.encode_plaintexts(S, vecs, S.ring.max_level())
+            b.record(ext)
+        S.ring.synchronize()
+        ms = a.elapsed_time(b)
+        server_enc = {"vectors": len(vecs), "ms": round(ms, 3),
+                      "records_per_s": round(len(wl.mine) * spec.slots / (ms / 1e3), 1),
+                      "what": "Encoder::encode_slots at scale q_L + forward NTT of the shard's server plaintexts "
+                              "(tg_encode_slots, one launch), device-timed; not inside the query (the reference's "
+                              "p-dependent accounting, cli.hpp:240-244)"}
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -628,25 +777,49 @@ def run_b200(args):
         "value": round(value, 1), "unit": "records/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u64 (mod-q RNS residues)", "data": "synthetic",
-        "config": {"workload": spec.name, "records": records, "N": spec.N, "levels": spec.nq - 1,
-                   "q_bits": spec.q_bits, "special_primes": f"{spec.K}x{spec.sp_bits}b",
-                   "dnum": -(-spec.nq // spec.group), "chain_degrees": list(spec.degrees), "alpha": spec.alpha,
-                   "epsilon": spec.epsilon, "poly_eval": args.poly_eval, "streams": args.streams,
-                   "batched": bool(getattr(wl, "batched", False)), "max_blocks": getattr(wl, "max_blocks", None),
-                   "record_blocks": spec.n_cts, "slots": spec.slots, "secret_hw": spec.h,
-                   "amortized_us_per_record": round(ms_step * 1e3 / records, 4),
-                   "l2": "1 GiB buffer written between timed steps; working set (keys, blocks) > 126 MB L2",
-                   "parallelism": f"block-shard x{world}", **check},
+        "config": workload_config(spec),
+        "amortized_us_per_record": round(ms_step * 1e3 / records, 4),
+        "impl_detail": {"poly_eval": args.poly_eval, "streams": args.streams,
+                        "batched": bool(getattr(wl, "batched", False)),
+                        "max_blocks": getattr(wl, "max_blocks", None), "parallelism": f"block-shard x{world}",
+                        "l2": "1 GiB buffer written between timed steps; working set (keys, blocks) > 126 MB L2",
+                        "inputs": "client ciphertexts device-resident; their memoised eval forms dropped every step"},
+        "check": check,
         "e2e": {"value": round(records / (e2e_ms / 1e3), 1), "unit": "records/s", "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches // args.steps),
         "roofline": roofline,
+        "server_encode": server_enc,
         "cpu_baseline": cpu,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def workload_config(spec):
+    """The workload (BASELINE.json config) both arms run: identical dicts, so
+    the driver's same-config check compares like with like. Implementation
+    choices (evaluator, batching, threads) go in impl_detail."""
+    cfg = {"workload": spec.name, "records": spec.records, "N": spec.N, "levels": spec.nq - 1,
+           "q_bits": spec.q_bits, "special_primes": f"{spec.K}x{spec.sp_bits}b", "dnum": -(-spec.nq // spec.group),
+           "record_blocks": spec.n_cts, "slots": spec.slots, "secret_hw": spec.h, "seed": spec.seed}
+    if spec.degrees:
+        cfg.update({"chain_degrees": list(spec.degrees), "alpha": spec.alpha, "epsilon": spec.epsilon})
+    return cfg
+
+
+def host_cpu():
+    model = "unknown"
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count() or 1, "model": model}
 
 
 # ---------------------------------------------------------------------------
@@ -658,125 +831,134 @@ def _ref_module():
     return load_ref()
 
 
-def _ref_setup(G, W, spec, wl, blocks, rotations=False):
-    """Reference context + the workload's inputs for `blocks`, bit-identical to
-    the B200 arm's (same keys/randomness streams; slot vectors encoded with the
-    product's multi-threaded HOST encoder, which reproduces the reference
-    Encoder's residues exactly - tests/test_host_cpu.py - instead of its
-    single-threaded O(n^2) DFT)."""
-    R = _ref_module()
-    if R is None:
-        raise RuntimeError("oracle/_ref not built")
-    SR = W.make_context(R, spec, rotations=W.inner_sum_rotations(spec.slots) if rotations else [],
-                        relin=bool(spec.degrees))
-    sys.path.insert(0, str(ROOT / "tests"))
-    from common import copy_chain
-    # the B200 arm's chain when present (bit-identical, saves the host Remez
-    # time of degree-63 chains), else the reference's own build_chain
-    if not spec.degrees:  # no threshold in this workload
-        chain_r = None
-    else:
-        chain_r = copy_chain(R, wl.chain) if getattr(wl, "chain", None) is not None else W.config3_chain(R, spec)
-    ringG = G.RingParams(spec.N, SR.primes + SR.sp, spec.K)
-    encG = G.Encoder(ringG, spec.slots)
-
-    def encode_host(SR_, arr, scale, level):
-        return [R.Poly.from_numpy(SR_.ring, encG.encode_slots_host([complex(x) for x in v], scale, level), level,
-                                  R.Form.coeff, 0) for v in arr]
-
-    SR.encode = encode_host
-    lvl = SR.ring.max_level()
-
-    def host_encode(values, label):
-        m = encode_host(SR, [values], spec.delta, lvl)[0]
-        return SR.ctx.encrypt(SR.sk, m, spec.delta, R.Rng(spec.seed).split(label), R.Domain.slots)
-
-    return R, SR, chain_r, wl.ref_inputs(R, SR, chain_r, host_encode, blocks)
-
-
-def ref_threads(wl, nblocks):
-    """Host threads the reference uses: one per threshold job (protocol.hpp:297-311);
-    the linear score is one thread (no threads in the reference's scoring)."""
-    per = 3 if isinstance(wl, Statement) else (1 if isinstance(wl, ThresholdCount) else 0)
-    return max(1, min(nblocks * per, os.cpu_count() or 1)) if per else 1
+def load_workloads():
+    """paper_2412_13269_b200/workloads.py by path (numpy only): the reference
+    arm must not import the package, whose __init__ loads the B200 library."""
+    import importlib.util
+    if "paper_2412_13269_b200.workloads" in sys.modules:
+        return sys.modules["paper_2412_13269_b200.workloads"]
+    name = "tg_workloads_standalone"
+    if name not in sys.modules:
+        sp = importlib.util.spec_from_file_location(name, ROOT / "paper_2412_13269_b200" / "workloads.py")
+        mod = importlib.util.module_from_spec(sp)
+        sys.modules[name] = mod
+        sp.loader.exec_module(mod)
+    return sys.modules[name]
 
 
 def cpu_baseline(G, W, spec, wl):
-    """Bounded sample (~10-30 s of CPU work): the reference on one record
-    block (config 3: all blocks, one thread each), compared residue for
-    residue with the GPU ladder run of the same block(s)."""
-    blocks = [0] if isinstance(wl, Statement) else list(range(spec.n_cts))
-    R, SR, chain_r, inp = _ref_setup(G, W, spec, wl, blocks)
-    threads = ref_threads(wl, len(blocks))
-    t0 = time.perf_counter()
-    res = wl.ref_step(R, SR, chain_r, inp, threads)
-    secs = time.perf_counter() - t0
-    lad = wl.gpu_ladder(blocks)
-    res_l, lad_l = (res, lad) if isinstance(res, list) else ([res], [lad])
-    same = all(all(np.array_equal(a.to_numpy(), b.to_numpy()) for a, b in zip(x.parts, y.parts))
-               and x.scale == y.scale and x.level() == y.level() for x, y in zip(res_l, lad_l))
-    recs = len(blocks) * spec.slots
-    what = {ThresholdCount: "threshold", Statement: "statement ops", LinearScore: "linear score"}[type(wl)]
-    return {"value": round(recs / secs, 2), "unit": "records/s", "cores": threads, "kind": "reference",
-            "sample": f"{len(blocks)} record block(s) x {spec.slots} records through the reference's own "
-                      f"{what} on {threads} thread(s) (unmodified headers, g++ -O2), {secs:.2f} s"
-                      + ("; slot-sum not in the sample" if wl.slot_sum else ""),
-            "seconds": round(secs, 2), "bit_exact_vs_gpu_ladder": bool(same),
-            "note": ("reference = its own T_k-ladder polynomial evaluator; the GPU ladder run of the same blocks is "
-                     "compared residue for residue (BSGS parity vs its oracle: tests/test_gpu_bsgs.py, "
-                     "tests/test_gpu_statement.py)") if spec.degrees else
-                    "the GPU outputs of the same blocks are compared residue for residue"}
+    """Bounded sample (~10-60 s of CPU work) of the same workload through the
+    oracle on the host cores, compared residue for residue with the product
+    path exactly as timed (wl.oracle_check): configs 4/5 blocks 0 and n-1
+    through the BSGS oracle (oracle/bsgs_ref.py over oracle/_ref), plus the
+    decrypted count of their sum + inner_sum in both; config 3 the whole
+    query; config 2 every block through the reference's own ops."""
+    R = _ref_module()
+    if R is None:
+        raise RuntimeError("oracle/_ref not built")
+    nblk = min(spec.n_cts, 3) if isinstance(wl, Statement) else spec.n_cts
+    threads = max(1, min(nblk * wl.columns, os.cpu_count() or 1))
+    secs, nb, chk = wl.oracle_check(R, W, threads)
+    recs = nb * spec.slots
+    kind = "port" if spec.degrees else "reference"
+    return {"value": round(recs / secs, 2), "unit": "records/s", "cores": threads, "kind": kind,
+            "sample": f"{nb} record block(s) x {spec.slots} records through "
+                      + ("the BSGS oracle (oracle/bsgs_ref.py: the product's BSGS order restated over the compiled "
+                         "reference's Evaluator primitives, oracle/_ref, g++ -O2)" if spec.degrees else
+                         "the reference's own ops (oracle/_ref, g++ -O2)")
+                      + f" on {threads} thread(s), {secs:.2f} s"
+                      + ("; config 3 includes the inner_sum" if isinstance(wl, ThresholdCount) else ""),
+            "seconds": round(secs, 2), **chk, "host": host_cpu()}
+
+
+def ref_threads(wl, nblocks):
+    """Host threads the reference uses: one per threshold job (protocol.hpp:297-311)."""
+    return max(1, min(nblocks * wl.columns, os.cpu_count() or 1))
 
 
 def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    headers, g++ -O2) on this host's cores, on the same workload config as the
+    B200 arm. Nothing from paper_2412_13269_b200 is imported or loaded here:
+    inputs are encoded by the reference's Encoder (threaded over vectors) and
+    encrypted with the same seeds as the B200 arm's."""
     world, rank, _ = dist_env()
     if rank != 0:
         return  # rank 0 alone runs the CPU reference
-    from paper_2412_13269_b200 import tetris as G
-    from paper_2412_13269_b200 import workloads as W
-
+    W = load_workloads()
     spec = W.CONFIGS[args.config]
-    if _ref_module() is None:
+    R = _ref_module()
+    if R is None:
         print(json.dumps({"impl": "reference",
                           "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
         return
     cores = os.cpu_count() or 1
-    per_block = 3 if WORKLOADS[args.config] is Statement else 1
-    nblk = max(1, min(spec.n_cts, cores // per_block))
-    if WORKLOADS[args.config] is LinearScore:
-        nblk = spec.n_cts  # the whole (small) query
+    cls = WORKLOADS[args.config]
+    nblk = spec.n_cts if cls is LinearScore else max(1, min(spec.n_cts, cores // cls.columns))
     blocks = list(range(nblk))
     t0 = time.time()
-
-    wl = WORKLOADS[args.config](G, W, spec, device=False)
-    R, SR, chain, inp = _ref_setup(G, W, spec, wl, blocks)
+    wl = cls(None, W, spec, device=False)
+    SR = W.make_context(R, spec, rotations=W.inner_sum_rotations(spec.slots) if wl.slot_sum else [],
+                        relin=bool(spec.degrees))
+    chain = W.config3_chain(R, spec) if spec.degrees else None
     threads = ref_threads(wl, nblk)
-    log(f"[reference] setup {time.time() - t0:.1f}s, sample {nblk} blocks on {threads} threads")
+    inp, enc = wl.ref_inputs(SR, blocks, cores)
+    log(f"[reference] setup {time.time() - t0:.1f}s, sample {nblk} blocks on {threads} threads, encode {enc}")
+
+    # one record block on ONE thread, once (the reference's single-threaded figure)
+    one = None
+    if not args.no_1thread and nblk >= 1:
+        sub = (inp[0][:1], inp[1]) if cls is ThresholdCount else (inp[0], inp[1][:1])
+        _, ph = wl.ref_step(R, SR, chain, sub, 1)
+        s1 = ph["blocks_s"] + ph["slot_sum_s"]
+        one = {"value": round(spec.slots / s1, 2), "unit": "records/s", "cores": 1, "seconds": round(s1, 2),
+               "sample": "record block 0 through the same code path on one thread" +
+                         (", incl. the slot-sum of its output" if wl.slot_sum else "")}
+
+    phases = []
 
     def step():
         t = time.perf_counter()
-        wl.ref_step(R, SR, chain, inp, threads)
+        _, ph = wl.ref_step(R, SR, chain, inp, threads)
+        phases.append(ph)
         return time.perf_counter() - t
 
     for _ in range(args.warmup):
         step()
+    phases.clear()
     secs = [step() for _ in range(args.steps)]
     s = sum(secs) / len(secs)
     recs = nblk * spec.slots
     value = recs / s
-    sample = (f"each step = {nblk} of {spec.n_cts} record blocks ({recs} records) through the reference's own "
-              f"code path on {threads} threads (unmodified headers, g++ -O2); per-record work is identical across "
-              f"blocks; the once-per-query slot-sum is not in the sample")
+    blk_s = sum(p["blocks_s"] for p in phases) / len(phases)
+    ss_s = sum(p["slot_sum_s"] for p in phases) / len(phases)
+    sample = (f"each step = {nblk} of {spec.n_cts} record blocks ({recs} records) through the reference's own code "
+              f"path on {threads} threads (unmodified headers, g++ -O2; the reference's T_k-ladder polynomial "
+              f"evaluator)" + (", then the sum and ONE inner_sum of the sample's output inside the step "
+                               f"({ss_s:.2f} s of {s:.2f} s)" if wl.slot_sum else "")
+              + "; per-record work is identical across blocks")
+    # server plaintext encoding by the reference's own encoder, as its own line
+    senc = None
+    if enc.get("server_vectors"):
+        senc = {"vectors": enc["server_vectors"], "seconds": enc["server_encode_s"], "threads": cores,
+                "records_per_s": round(nblk * spec.slots / enc["server_encode_s"], 2),
+                "what": "Encoder::encode_slots (O(n^2) DFT, ckks.hpp:59-86) at scale q_L + NTT of the sample's "
+                        "server plaintexts, vectors spread over a std::thread pool; not inside the query"}
     print(json.dumps({
-        "impl": "reference", "metric": WORKLOADS[args.config].metric,
+        "impl": "reference", "metric": cls.metric,
         "value": round(value, 2), "unit": "records/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(s * 1e3, 1), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u64 (mod-q RNS residues)", "data": "synthetic",
-        "config": {"workload": spec.name, "records": spec.records, "N": spec.N, "levels": spec.nq - 1,
-                   "sample_records": recs, "amortized_us_per_record": round(s * 1e6 / recs, 2)},
+        "config": workload_config(spec),
+        "amortized_us_per_record": round(s * 1e6 / recs, 2),
+        "impl_detail": {"poly_eval": "ladder (reference eval_chebyshev)", "threads": threads,
+                        "sample_records": recs, "blocks_s": round(blk_s, 3), "slot_sum_s": round(ss_s, 3)},
         "cpu_baseline": {"value": round(value, 2), "unit": "records/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "host": host_cpu()},
+        "cpu_1thread": one,
+        "server_encode": senc,
         "e2e": {"value": round(value, 2), "unit": "records/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_loaded": any(m.startswith("paper_2412_13269_b200") for m in sys.modules),
     }), flush=True)
 
 
@@ -798,6 +980,7 @@ def main():
     ap.add_argument("--pool-gb", type=float, default=48.0, help="device memory pool reserved up front (GiB)")
     ap.add_argument("--K", type=int, default=0, help="override the special-prime count (experiments)")
     ap.add_argument("--group", type=int, default=0, help="override the gadget group size (experiments)")
+    ap.add_argument("--no-1thread", action="store_true", help="reference arm: skip the one-thread row")
     ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=4,
                     help="BASELINE.json workload: 4 = full TETRIS statement (default), 3 = threshold count, "
                          "5 = scale-out stress")

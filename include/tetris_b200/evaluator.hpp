@@ -37,6 +37,9 @@ public:
     // host residues of encode_slots (no device needed)
     std::vector<u64> encode_slots_host(const std::vector<cplx>& v, double scale, int level) const;
     std::vector<cplx> decode_slots_host(const u64* rows01, int level, double scale) const;
+    // the encoder's tables: psi[t] = exp(i pi t / 2n) (4n entries), rot5[j] = 5^j mod 4n
+    const std::vector<cplx>& psi() const { return psi_; }
+    const std::vector<u32>& rot5() const { return rot5_; }
 
 private:
     const RingParams* ring_;

@@ -230,7 +230,44 @@ PYBIND11_MODULE(tetris_ref, m) {
         .def("encode_slots", &Encoder::encode_slots)
         .def("decode_slots", &Encoder::decode_slots)
         .def("encode_coeffs", &Encoder::encode_coeffs)
-        .def("decode_coeffs", &Encoder::decode_coeffs);
+        .def("decode_coeffs", &Encoder::decode_coeffs)
+        // The reference's own Encoder::encode_slots (ckks.hpp:70-86, O(n^2)
+        // DFT) on every row of `arr` ([batch][slots] complex128), rows spread
+        // over a std::thread pool: the unmodified code, only run concurrently
+        // (the encoder is const and shares nothing mutable).
+        .def("encode_slots_many",
+             [](const Encoder& enc, py::array_t<std::complex<double>, py::array::c_style | py::array::forcecast> arr,
+                double scale, int level, int threads) {
+                 if (arr.ndim() != 2 || arr.shape(1) != py::ssize_t(enc.slots()))
+                     throw TetrisError("oracle", "encode_slots_many: shape mismatch");
+                 const size_t B = size_t(arr.shape(0)), n = enc.slots();
+                 std::vector<std::vector<cplx>> in(B);
+                 for (size_t b = 0; b < B; ++b) in[b].assign(arr.data() + b * n, arr.data() + (b + 1) * n);
+                 std::vector<Poly> out(B);
+                 {
+                     py::gil_scoped_release nogil;
+                     std::atomic<size_t> next{0};
+                     std::exception_ptr err;
+                     std::mutex mu;
+                     auto worker = [&]() {
+                         for (size_t b; (b = next.fetch_add(1)) < B;) {
+                             try {
+                                 out[b] = enc.encode_slots(in[b], scale, level);
+                             } catch (...) {
+                                 std::lock_guard<std::mutex> g(mu);
+                                 err = std::current_exception();
+                             }
+                         }
+                     };
+                     std::vector<std::thread> pool;
+                     const int nt = std::max(1, std::min<int>(threads, int(B)));
+                     for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
+                     for (auto& th : pool) th.join();
+                     if (err) std::rethrow_exception(err);
+                 }
+                 return out;
+             },
+             py::arg("arr"), py::arg("scale"), py::arg("level"), py::arg("threads") = 1);
 
     py::class_<Evaluator>(m, "Evaluator")
         .def(py::init<const KeyContext&>(), py::keep_alive<1, 2>())

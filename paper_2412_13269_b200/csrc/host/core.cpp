@@ -349,6 +349,8 @@ u64* Poly::mutable_data() {
         check_tg(tg_memcpy_d2d(ring_->dev(), fresh->data(), st_->data() + off_, words() * 8, ring_->stream()));
         st_ = std::move(fresh);
         off_ = 0;
+    } else {
+        st_->clear_eval_cache();  // written in place: a memoised transform of the old contents is stale
     }
     return st_->data() + off_;
 }

@@ -165,9 +165,10 @@ static void transform_parts(Ciphertext& ct, Form target, bool keep_eval = false)
         if (!own && target == Form::eval)
             out_blk = p0.storage()->find_eval(p0.offset(), full_level, ns, int(np), ring.stream());
         if (!out_blk) {
-            if (own) {
+            if (own) {  // transformed in place: drop memoised transforms of the old contents
                 out_blk = p0.storage();
                 out_off = p0.offset();
+                out_blk->clear_eval_cache();
             } else {
                 out_blk = detail::new_block(ring, S * np);
             }
@@ -207,8 +208,10 @@ static void addsub_ct(Ciphertext& x, const Ciphertext& o, int op) {
     if (contiguous(x.parts, 0, np) && contiguous(o.parts, 0, np)) {
         const Poly& p0 = x.parts[0];
         const RingParams& ring = p0.ring();
+        const bool in_place = exclusively_owned(x.parts);
+        if (in_place) p0.storage()->clear_eval_cache();  // the old contents' memoised eval form goes stale
         std::vector<Poly> dst =
-            exclusively_owned(x.parts) ? x.parts : fresh_parts(ring, int(np), p0.level(), p0.form(), p0.nspecial());
+            in_place ? x.parts : fresh_parts(ring, int(np), p0.level(), p0.form(), p0.nspecial());
         check_tg(tg_poly_addsub(ring.dev(), const_cast<u64*>(dst[0].data()), p0.data(), o.parts[0].data(), op,
                                 p0.level(), p0.nspecial(), u32(np), ring.stream()));
         x.parts = std::move(dst);

@@ -147,77 +147,6 @@ RepackKeySet gen_repack_keys(const KeyContext& ctx, const SecretKey& sk, Rng& rn
     return set;
 }
 
-// The reference butterfly one pair at a time (inputs with differing key ids
-// or domains keep the reference's exact per-pair behaviour).
-static Ciphertext repack_serial(const KeyContext& ctx, const std::vector<const Ciphertext*>& cts,
-                                const RepackKeySet& keys, RepackStats* stats) {
-    const RingParams& ring = ctx.ring();
-    const u32 n = ring.degree();
-    if (cts.size() > n) throw TetrisError("repack", "more inputs than ring coefficients");
-    const Ciphertext* first = nullptr;
-    for (auto* c : cts)
-        if (c) {
-            first = c;
-            break;
-        }
-    if (!first) throw TetrisError("repack", "all-zero repack batch");
-    const int lvl = first->level();
-    const double scale = first->scale;
-    for (auto* c : cts) {
-        if (!c) continue;
-        if (c->level() != lvl) throw TetrisError("repack", "repack inputs at mixed levels");
-        if (c->scale != scale) throw TetrisError("repack", "repack inputs at mixed scales");
-    }
-    std::vector<u64> n_inv(ring.moduli().size());
-    for (std::size_t i = 0; i < n_inv.size(); ++i) n_inv[i] = inv_mod(n, ring.moduli()[i]);
-
-    std::vector<Ciphertext> c(n);
-    std::vector<bool> live(n, false);
-    for (std::size_t i = 0; i < cts.size(); ++i) {
-        if (!cts[i]) continue;
-        c[i] = *cts[i];
-        c[i].to_coeff();
-        for (auto& p : c[i].parts) p.mul_scalar_inplace(n_inv);  // the per-round doublings cancel
-        live[i] = true;
-    }
-    auto shift = [](const Ciphertext& ct, u32 e) {
-        Ciphertext out = ct;
-        for (auto& p : out.parts) p = mul_monomial(p, e);
-        return out;
-    };
-    for (u32 round = 0; round < ring.log_degree(); ++round) {
-        const u32 t = n >> (round + 1);
-        const u64 g = keys.exponents[round];
-        const SwitchingKey& swk = keys.key(g);
-        for (u32 j = 0; j < t; ++j) {
-            const bool lj = live[j], lh = live[j + t];
-            if (!lj && !lh) continue;
-            Ciphertext shifted;
-            if (lh) shifted = shift(c[j + t], t);
-            Ciphertext sum, diff;
-            if (lj && lh) {
-                sum = c[j];
-                sum.add_inplace(shifted);
-                diff = c[j];
-                diff.sub_inplace(shifted);
-            } else if (lj) {
-                sum = c[j];
-                diff = c[j];
-            } else {
-                sum = shifted;
-                diff = shifted;
-                diff.negate_inplace();
-            }
-            Ciphertext rotated = ctx.apply_galois(diff, g, swk);
-            if (stats) ++stats->automorphisms;
-            sum.add_inplace(rotated);
-            c[j] = std::move(sum);
-            live[j] = true;
-        }
-    }
-    return std::move(c[0]);
-}
-
 // The butterfly with every round as ONE ciphertext batch: slots [0, t) and
 // [t, 2t) of the state are combined by batched monomial shifts, adds, subs
 // and a batched automorphism + key switch (one key per round). Absent inputs
@@ -238,14 +167,20 @@ Ciphertext repack(const KeyContext& ctx, const std::vector<const Ciphertext*>& c
     if (!first) throw TetrisError("repack", "all-zero repack batch");
     const int lvl = first->level();
     const double scale = first->scale;
-    bool uniform = true;
     for (auto* c : cts) {
         if (!c) continue;
         if (c->level() != lvl) throw TetrisError("repack", "repack inputs at mixed levels");
         if (c->scale != scale) throw TetrisError("repack", "repack inputs at mixed scales");
-        uniform &= c->degree() == 1 && c->batch == 1 && c->sk_id == first->sk_id && c->domain == first->domain;
+        if (c->degree() != 1 || c->batch != 1)
+            throw TetrisError("repack", "repack inputs must be single degree-1 ciphertexts");
+        // the butterfly adds every live input into slot 0, where the reference
+        // throws on the first domain mismatch (rlwe.hpp:302-309); inputs under
+        // different secret keys have no meaningful repacking (the reference
+        // key-switches them with one key set regardless) and are refused
+        if (c->domain != first->domain) throw TetrisError("rlwe", "domain tag mismatch");
+        if (c->sk_id != first->sk_id) throw TetrisError("repack", "repack inputs under different secret keys");
     }
-    if (!uniform || ring.log_degree() == 0) return repack_serial(ctx, cts, keys, stats);
+    if (ring.log_degree() == 0) throw TetrisError("repack", "ring degree 1 has no repacking butterfly");
     std::vector<u64> n_inv(ring.moduli().size());
     for (std::size_t i = 0; i < n_inv.size(); ++i) n_inv[i] = inv_mod(n, ring.moduli()[i]);
 

@@ -206,7 +206,10 @@ PYBIND11_MODULE(_tetris_b200, m) {
         .def("to_eval", &Ciphertext::to_eval)
         .def("drop_to_level", &Ciphertext::drop_to_level)
         .def("add_inplace", &Ciphertext::add_inplace)
-        .def("sub_inplace", &Ciphertext::sub_inplace);
+        .def("sub_inplace", &Ciphertext::sub_inplace)
+        .def("clear_eval_cache", [](const Ciphertext& c) {
+            for (const auto& p : c.parts) p.storage()->clear_eval_cache();
+        }, "drop memoised eval-form transforms of the parts' blocks (benchmarks: every step pays them)");
 
     py::class_<SwitchingKey>(m, "SwitchingKey")
         .def_readonly("b", &SwitchingKey::b)

@@ -302,6 +302,9 @@ def config2_query(S, inp, streams=1):
 # ---------------------------------------------------------------------------
 
 RISK_NORM = 0.5  # |risk - t| <= 1.05 for risk in [-1,1], |t| <= 0.05
+COLUMNS = ("risk", "sugar", "bp")   # threshold job columns, in upload order
+COLUMN_T = {"risk": 2, "sugar": 0, "bp": 1}  # index into the query's thresholds
+COLUMN_NORM = {"risk": RISK_NORM, "sugar": 1.0, "bp": 1.0}
 
 
 def statement_data(spec: Spec, seed_offset: int = 0):
@@ -383,17 +386,37 @@ def statement_partial(S, q, blocks, threshold, streams=1):
     return acc
 
 
-def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8, ready=None):
-    """B200 module: the same per-block statement with the blocks evaluated as
-    ciphertext batches (stack_ciphertexts): per chunk of <= max_blocks blocks,
-    one batched threshold per column (sugar, pressure, risk score; the three
-    run concurrently), then the AND products batched. Each
-    block's output is bit-identical to statement_block's (a batch is exactly
-    `batch` independent ciphertexts; tests/test_gpu_statement.py); launches
-    and switching-key reads are shared by the batch.
+def statement_jobs(nblocks: int, max_batch: int):
+    """The (column, block) threshold jobs of `nblocks` record blocks cut into
+    ciphertext batches of <= max_batch near-equal parts: the risk column
+    (its inputs are resident first in a staged upload; level L-1 after the
+    score's rescale, norm RISK_NORM) on its own, the sugar and pressure
+    columns (level L, norm 1) together, so a batch may mix those two and a
+    shard of one record block still runs them as one batch of two."""
+    out = []
+    for group in (("risk",), ("sugar", "bp")):
+        jobs = [(col, i) for col in group for i in range(nblocks)]
+        if not jobs:
+            continue
+        nb = -(-len(jobs) // max(1, max_batch))
+        size = -(-len(jobs) // nb)
+        out += [jobs[i:i + size] for i in range(0, len(jobs), size)]
+    return out
+
+
+def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8, ready=None, keep=None):
+    """B200 module: the per-block statement with the blocks evaluated as
+    ciphertext batches (stack_ciphertexts): the (column, block) threshold jobs
+    in batches of <= max_blocks (statement_jobs; the batches run on
+    concurrent streams), then the AND products per chunk of <= max_blocks
+    blocks, batched. Each block's output is bit-identical to
+    statement_block's (a batch is exactly `batch` independent ciphertexts;
+    tests/test_gpu_statement.py); launches and switching-key reads are shared
+    by the batch.
     ready (optional, staged uploads): ready(name) makes the current stream
     wait until the client ciphertexts `name` ("w", "t0".."t2", "sugar", "bp") are
-    resident, so each job starts as soon as its own inputs have arrived."""
+    resident, so each job starts as soon as its own inputs have arrived.
+    keep (optional list): receives every block's output before the sum."""
     T, ev, keys = S.T, S.ev, S.keys
     wait = ready or (lambda name: None)
 
@@ -402,27 +425,52 @@ def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8, 
         return linear_score(S, q.ct_w, blk.pt_attr, blk.attr_scale)
 
     risks = run_concurrent(T, S.ring, score, blocks, streams)
-    chunks = [list(range(i, min(len(blocks), i + max_blocks))) for i in range(0, len(blocks), max_blocks)]
-    # three equal batches per chunk, run concurrently; the risk batch first
-    # (its inputs are resident before the record columns)
-    cols = (("risk", 2, RISK_NORM), ("sugar", 0, 1.0), ("bp", 1, 1.0))
-    jobs = [(ch, col, k, norm) for ch in chunks for col, k, norm in cols]
+    batches = statement_jobs(len(blocks), max_blocks)
 
-    def job(j):
-        ch, col, k, norm = j
-        wait(f"t{k}")  # this column's threshold only
-        if col != "risk":
-            wait(col)
-        xs = [risks[b] if col == "risk" else getattr(blocks[b], "ct_" + col) for b in ch]
-        return threshold(T.stack_ciphertexts(xs), T.stack_ciphertexts([q.ct_t[k]] * len(ch)), norm)
+    def job(batch):
+        xs, ts = [], []
+        for col, i in batch:
+            k = COLUMN_T[col]
+            wait(f"t{k}")  # this job's threshold only
+            if col != "risk":
+                wait(col)
+            xs.append(risks[i] if col == "risk" else getattr(blocks[i], "ct_" + col))
+            ts.append(q.ct_t[k])
+        return threshold(T.stack_ciphertexts(xs), T.stack_ciphertexts(ts), COLUMN_NORM[batch[0][0]])
 
-    outs = run_concurrent(T, S.ring, job, jobs, streams)
+    outs = run_concurrent(T, S.ring, job, batches, streams)
+    where = {}  # (column, block) -> (batch, position)
+    for bi, batch in enumerate(batches):
+        for pos, jb in enumerate(batch):
+            where[jb] = (bi, pos)
+    pieces = {}
+
+    def indicator(col, i):
+        bi, pos = where[(col, i)]
+        if outs[bi].batch == 1:
+            return outs[bi]
+        if bi not in pieces:
+            pieces[bi] = T.unstack_ciphertext(outs[bi])
+        return pieces[bi][pos]
+
+    def column_batch(col, chunk):
+        """The indicators of `col` for the blocks of `chunk` as one batch: a
+        job batch as it is when it holds exactly those, else restacked."""
+        bi, _ = where[(col, chunk[0])]
+        if batches[bi] == [(col, i) for i in chunk]:
+            return outs[bi]
+        xs = [indicator(col, i) for i in chunk]
+        return xs[0] if len(xs) == 1 else T.stack_ciphertexts(xs)
+
     acc = None
-    for c, ch in enumerate(chunks):
-        b3, b1, b2 = outs[3 * c], outs[3 * c + 1], outs[3 * c + 2]
+    for c0 in range(0, len(blocks), max_blocks):
+        chunk = list(range(c0, min(len(blocks), c0 + max_blocks)))
+        b1, b2, b3 = column_batch("sugar", chunk), column_batch("bp", chunk), column_batch("risk", chunk)
         a = ev.rescale(ev.mul_relin(b1, b2, keys))
         a = ev.rescale(ev.mul_relin(a, b3, keys))
-        for i, ct in zip(ch, T.unstack_ciphertext(a)):
+        for i, ct in zip(chunk, T.unstack_ciphertext(a) if a.batch > 1 else [a]):
             o = ev.rescale(ev.mul_plain(ct, blocks[i].pt_flag, blocks[i].flag_scale))
+            if keep is not None:
+                keep.append(o)
             acc = o if acc is None else ev.add(acc, o)
     return acc

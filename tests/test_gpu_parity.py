@@ -153,6 +153,28 @@ def test_evaluator_ops(G, R, pair64):
         assert_ct_equal(fn(g, xg, yg), fn(r, xr, yr), name)
 
 
+def test_inplace_write_after_memoised_transform(G, R, pair64):
+    """mul(a, b) memoises a's eval form on its block; a later in-place
+    add/sub/negate must not reuse it (stale eval-form cache)."""
+    g, r = pair64
+    xg, xr, _ = _pair_cts(g, r, 32, seed=21)
+    yg, yr, _ = _pair_cts(g, r, 32, seed=22)
+    zg, zr, _ = _pair_cts(g, r, 32, seed=23)
+    outs = []
+    for S, x, y, z in ((g, xg, yg, zg), (r, xr, yr, zr)):
+        a = x.copy()
+        hold = a.copy()              # a shared block: mul memoises its eval form
+        m1 = S.ev.mul(a, y)
+        del hold                     # a's block is exclusively owned again
+        a.add_inplace(z)             # in place on the block whose eval form was memoised
+        m2 = S.ev.mul(a, y)
+        a.sub_inplace(y)
+        m3 = S.ev.mul_relin(a, z, S.keys)
+        outs.append((m1, m2, m3))
+    for name, cg_, cr_ in zip(("mul", "mul after add_inplace", "mul_relin after sub_inplace"), outs[0], outs[1]):
+        assert_ct_equal(cg_, cr_, name)
+
+
 def test_mul_plain(G, R, pair64):
     g, r = pair64
     xg, xr, _ = _pair_cts(g, r, 32, seed=8)
