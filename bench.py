@@ -962,6 +962,305 @@ def run_reference(args):
     }), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# Config 1 (BASELINE.json configs[0]): the CKKS ring-op microbench
+# ---------------------------------------------------------------------------
+CONFIG1_METRIC = ("ciphertexts/sec through the config-1 ring-op sequence (forward NTT, inverse NTT, tensor + "
+                  "relinearisation with ct_(i+1 mod 64), rescale, rotation by 1; every op on all 64 ciphertexts)")
+
+
+def config1_inputs(T, W, spec, n_cts):
+    """64 ciphertexts of uniform residues (sample_uniform per part from
+    Rng(seed).split(5).split(2i + j)), keys from the workload's keygen."""
+    S = W.make_context(T, spec, rotations=(1,))
+    rng = T.Rng(spec.seed).split(5)
+    L = S.ring.max_level()
+    cts = []
+    for i in range(n_cts):
+        c = T.Ciphertext()
+        c.parts = [T.sample_uniform(S.ring, L, 0, rng.split(2 * i + j)) for j in range(2)]
+        c.scale, c.domain, c.sk_id = spec.delta, T.Domain.slots, S.sk.id()
+        cts.append(c)
+    return S, cts
+
+
+def config1_ops(ev, keys, x, y, x_eval):
+    """One step: every op of the config on the whole batch. Inputs are fresh
+    exclusively owned blocks (mul by 1 costs one HBM pass, counted as
+    scalar_copy) so the transforms are real, not memoised."""
+    f = ev.mul_scalar(x, 1.0, 1.0)
+    f.to_eval()                                   # forward NTT, 64 x 2 x 8 rows
+    g = ev.mul_scalar(x_eval, 1.0, 1.0)
+    g.to_coeff()                                  # inverse NTT
+    pr = ev.rescale(ev.mul_relin(x, y, keys))     # tensor + relinearisation, rescale
+    rot = ev.rotate(x, 1, keys)                   # rotation by 1 (5^1)
+    return f, g, pr, rot
+
+
+def run_config1(args):
+    import torch
+
+    from paper_2412_13269_b200 import tetris as G
+    from paper_2412_13269_b200 import workloads as W
+
+    world, rank, local = dist_env()
+    if world > 1:  # every rank runs its own 64 ciphertexts (weak scaling, no exchange)
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None
+        torch.cuda.set_device(local)
+    if G.device_count() < 1:
+        raise SystemExit("bench.py: no CUDA device visible (the B200 arm has no CPU fallback)")
+    G.set_default_device(local)
+    spec = W.CONFIGS[1]
+    n = spec.n_cts
+    S, cts = config1_inputs(G, W, spec, n)
+    ev, keys, ring = S.ev, S.keys, S.ring
+    x = G.stack_ciphertexts(cts)
+    y = G.stack_ciphertexts(cts[1:] + cts[:1])
+    x_eval = x.copy()
+    x_eval.to_eval()
+    ext = torch.cuda.ExternalStream(ring.stream_handle(), device=torch.device("cuda", local))
+    flush = torch.empty(64 << 22, dtype=torch.int32, device="cuda")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ring.synchronize()
+
+    def timed(fn, steps):
+        ev_pairs = []
+        out = None
+        for _ in range(steps):
+            with torch.cuda.stream(ext):
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(ext)
+            out = fn()
+            b.record(ext)
+            ev_pairs.append((a, b))
+        ring.synchronize()
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in ev_pairs], out
+
+    step = lambda: config1_ops(ev, keys, x, y, x_eval)  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    try:
+        pr_ = torch.cuda.get_device_properties(local)
+        pci = f"{pr_.pci_domain_id:08x}:{pr_.pci_bus_id:02x}:{pr_.pci_device_id:02x}.0"
+    except Exception:
+        pci = None
+    with ClockSampler(local, pci) as clocks:
+        barrier()
+        ms_list, outs = timed(step, args.steps)
+        barrier()
+    ms = sum(ms_list) / len(ms_list)
+    log(f"[rank {rank}] config-1 step ms: " + " ".join(f"{m:.3f}" for m in ms_list))
+    if dist is not None:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    # per-op device times (one op per timed bracket) and kernel classes
+    per_op = {}
+    for name, fn in (("scalar_copy", lambda: ev.mul_scalar(x, 1.0, 1.0)),
+                     ("ntt_fwd", lambda: config1_ops(ev, keys, x, y, x_eval)[0]),
+                     ("tensor_relin_rescale", lambda: ev.rescale(ev.mul_relin(x, y, keys))),
+                     ("rotate_1", lambda: ev.rotate(x, 1, keys))):
+        if name == "ntt_fwd":
+            def fn():  # noqa: F811
+                f = ev.mul_scalar(x, 1.0, 1.0)
+                f.to_eval()
+                return f
+        t, _ = timed(fn, max(3, args.steps))
+        per_op[name] = round(sum(t) / len(t), 4)
+    G.profile_enable(ring, True)
+    barrier()
+    timed(step, args.steps)
+    prof = G.profile_read(ring)
+    G.profile_enable(ring, False)
+
+    # end to end: the 64 ciphertexts from pinned host memory every step, the
+    # relinearised-rescaled products and the rotations back to the host
+    limbs = spec.nq
+    host_in = G.pinned_empty([n * 2 * limbs * spec.N])
+    metas = []
+    for i, c in enumerate(cts):
+        off = i * 2 * limbs * spec.N
+        metas.append((off, 2, c.level(), c.scale, c.sk_id))
+        G.ciphertext_to_numpy(c, host_in[off:off + 2 * limbs * spec.N])
+    up = G.HostUpload(ring, host_in, metas, G.Form.coeff, G.Domain.slots)
+    host_pr = G.pinned_empty([2 * n, limbs - 1, spec.N])
+    host_rot = G.pinned_empty([2 * n, limbs, spec.N])
+
+    def e2e_step():
+        c = up.upload()
+        xx = G.stack_ciphertexts(c)
+        yy = G.stack_ciphertexts(c[1:] + c[:1])
+        xe = xx.copy()
+        xe.to_eval()
+        o = config1_ops(ev, keys, xx, yy, xe)
+        G.ciphertext_to_numpy(o[2], host_pr)
+        G.ciphertext_to_numpy(o[3], host_rot)
+        return o
+
+    for _ in range(max(2, args.warmup)):
+        e2e_step()
+    barrier()
+    e2e_list, _ = timed(e2e_step, args.steps)
+    e2e_ms = sum(e2e_list) / len(e2e_list)
+    if dist is not None:
+        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+        if rank != 0:
+            dist.destroy_process_group()
+            return
+
+    peak, peak_kind = measured_peaks()
+    dname, (dms, dn, dbytes) = max(prof.items(), key=lambda kv: kv[1][0])
+    per_launch = dms / dn
+    achieved = (dbytes / dn) / (per_launch / 1e3) / 1e9
+    total = sum(v[0] for v in prof.values())
+    mib = 1 << 20
+    limb = spec.N * 8
+    # SURVEY 8(d) config-1 totals (algorithmic bytes; limb-poly = N*8 B)
+    alg = {"ntt_fwd": 2 * n * 2 * limbs * limb, "ntt_inv": 2 * n * 2 * limbs * limb,
+           "tensor_relin_rescale": (6 * limbs + (4 * limbs - 2)) * n * limb
+           + 2 * (-(-limbs // spec.group)) * (limbs + spec.K) * limb,
+           "rotate_1": (4 * limbs) * n * limb + 2 * (-(-limbs // spec.group)) * (limbs + spec.K) * limb}
+    net_fwd = per_op["ntt_fwd"] - per_op["scalar_copy"]
+    ops = {"ntt_fwd": {"ms": round(net_fwd, 4), "GBps": round(alg["ntt_fwd"] / (net_fwd / 1e3) / 1e9, 1),
+                       "note": "net of the exclusive copy"},
+           "tensor_relin_rescale": {"ms": per_op["tensor_relin_rescale"],
+                                    "GBps": round(alg["tensor_relin_rescale"] / (per_op["tensor_relin_rescale"] / 1e3)
+                                                  / 1e9, 1)},
+           "rotate_1": {"ms": per_op["rotate_1"],
+                        "GBps": round(alg["rotate_1"] / (per_op["rotate_1"] / 1e3) / 1e9, 1)}}
+    for k in ops:
+        ops[k]["frac_of_hbm"] = round(ops[k]["GBps"] / peak, 4)
+        ops[k]["alg_MiB"] = round(alg[k] / mib, 1)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = config1_cpu_baseline(G, W, spec, outs)
+        except Exception as e:
+            cpu = {"value": None, "error": str(e)[:300]}
+    line = {
+        "metric": CONFIG1_METRIC, "value": round(world * n / (ms / 1e3), 1), "unit": "ciphertexts/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 (mod-q RNS residues)",
+        "data": "synthetic", "config": workload_config(spec),
+        "impl_detail": {"batch": n, "parallelism": f"replicas x{world} (no exchange)",
+                        "l2": "1 GiB buffer written between timed steps"},
+        "per_op": ops,
+        "e2e": {"value": round(world * n / (e2e_ms / 1e3), 1), "unit": "ciphertexts/s", "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": int(host_in.nbytes), "d2h_bytes_per_step": int(host_pr.nbytes + host_rot.nbytes)},
+        "gpu_launches": int(sum(v[1] for v in prof.values()) // args.steps),
+        "roofline": {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                     "bytes_per_launch": dbytes / dn, "ms_per_launch": per_launch,
+                     "share_of_step": round(dms / total, 3),
+                     "per_kernel": {k: {"ms": round(v[0] / args.steps, 4), "launches": v[1] // args.steps,
+                                        "GBps": round((v[2] / v[1]) / ((v[0] / v[1]) / 1e3) / 1e9, 1)}
+                                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def config1_cpu_baseline(G, W, spec, outs):
+    """The reference (oracle/_ref) on a 4-ciphertext sample, one thread: the
+    same ops, compared residue for residue with the device batch."""
+    R = _ref_module()
+    if R is None:
+        raise RuntimeError("oracle/_ref not built")
+    k = 4
+    SR, rc = config1_inputs(R, W, spec, k)
+    t0 = time.perf_counter()
+    ref = config1_ref_ops(SR, rc)
+    secs = time.perf_counter() - t0
+    got_pr = G.unstack_ciphertext(outs[2])
+    got_rot = G.unstack_ciphertext(outs[3])
+    same = all(np.array_equal(a.to_numpy(), b.to_numpy())
+               for i in range(k - 1) for a, b in zip(got_pr[i].parts, ref["pr"][i].parts))
+    same &= all(np.array_equal(a.to_numpy(), b.to_numpy())
+                for i in range(k) for a, b in zip(got_rot[i].parts, ref["rot"][i].parts))
+    return {"value": round(k / secs, 3), "unit": "ciphertexts/s", "cores": 1, "kind": "reference",
+            "sample": f"{k} ciphertexts through the reference's own ops (forward + inverse NTT of both parts, "
+                      f"mul_relin + rescale, rotate by 1; unmodified headers, g++ -O2) on one thread, {secs:.2f} s",
+            "seconds": round(secs, 2), "bit_exact_vs_reference_sample": bool(same), "host": host_cpu()}
+
+
+def config1_ref_ops(SR, rc):
+    ev, keys = SR.ev, SR.keys
+    k = len(rc)
+    for c in rc:
+        for p in c.parts:
+            e = SR.T.ntt_transform(p, SR.T.Form.eval)
+            SR.T.ntt_transform(e, SR.T.Form.coeff)
+    pr = [ev.rescale(ev.mul_relin(rc[i], rc[(i + 1) % k], keys)) for i in range(k - 1)]
+    rot = [ev.rotate(c, 1, keys) for c in rc]
+    return {"pr": pr, "rot": rot}
+
+
+def run_config1_reference(args):
+    """Reference arm, config 1: the reference's own ops on every host core
+    (one ciphertext per thread), a sample of cores ciphertexts per step."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    W = load_workloads()
+    spec = W.CONFIGS[1]
+    R = _ref_module()
+    if R is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    from concurrent.futures import ThreadPoolExecutor
+    cores = os.cpu_count() or 1
+    k = max(2, min(spec.n_cts, cores))
+    SR, rc = config1_inputs(R, W, spec, k)
+    ev, keys = SR.ev, SR.keys
+
+    def one(i):
+        c = rc[i]
+        for p in c.parts:
+            SR.T.ntt_transform(SR.T.ntt_transform(p, SR.T.Form.eval), SR.T.Form.coeff)
+        ev.rescale(ev.mul_relin(c, rc[(i + 1) % k], keys))
+        ev.rotate(c, 1, keys)
+
+    def step():
+        t = time.perf_counter()
+        with ThreadPoolExecutor(k) as ex:
+            list(ex.map(one, range(k)))
+        return time.perf_counter() - t
+
+    for _ in range(args.warmup):
+        step()
+    secs = [step() for _ in range(args.steps)]
+    s = sum(secs) / len(secs)
+    value = k / s
+    print(json.dumps({
+        "impl": "reference", "metric": CONFIG1_METRIC, "value": round(value, 3), "unit": "ciphertexts/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(s * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 (mod-q RNS residues)",
+        "data": "synthetic", "config": workload_config(spec),
+        "cpu_baseline": {"value": round(value, 3), "unit": "ciphertexts/s", "cores": k, "kind": "reference",
+                         "sample": f"each step = {k} of {spec.n_cts} ciphertexts, one per thread, through the "
+                                   f"reference's own ops (NTT fwd+inv of both parts, mul_relin + rescale, rotate by 1; "
+                                   f"unmodified headers, g++ -O2)", "host": host_cpu()},
+        "e2e": {"value": round(value, 3), "unit": "ciphertexts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_loaded": any(m.startswith("paper_2412_13269_b200") for m in sys.modules),
+    }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -981,12 +1280,14 @@ def main():
     ap.add_argument("--K", type=int, default=0, help="override the special-prime count (experiments)")
     ap.add_argument("--group", type=int, default=0, help="override the gadget group size (experiments)")
     ap.add_argument("--no-1thread", action="store_true", help="reference arm: skip the one-thread row")
-    ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=4,
+    ap.add_argument("--config", type=int, choices=[1, 2, 3, 4, 5], default=4,
                     help="BASELINE.json workload: 4 = full TETRIS statement (default), 3 = threshold count, "
-                         "5 = scale-out stress")
+                         "5 = scale-out stress, 2 = linear score, 1 = ring-op microbench")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
-    if args.impl == "reference":
+    if args.config == 1:
+        (run_config1_reference if args.impl == "reference" else run_config1)(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)

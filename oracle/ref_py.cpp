@@ -119,8 +119,8 @@ PYBIND11_MODULE(tetris_ref, m) {
         .def_static("from_numpy", &poly_from_numpy, py::arg("ring"), py::arg("data"), py::arg("level"),
                     py::arg("form"), py::arg("nspecial") = 0, py::keep_alive<0, 1>())
         .def("copy", [](const Poly& p) { return Poly(p); })
-        .def("ntt_forward", &Poly::ntt_forward)
-        .def("ntt_inverse", &Poly::ntt_inverse)
+        .def("ntt_forward", &Poly::ntt_forward, py::call_guard<py::gil_scoped_release>())
+        .def("ntt_inverse", &Poly::ntt_inverse, py::call_guard<py::gil_scoped_release>())
         .def("mul_monomial", &Poly::mul_monomial)
         .def("add_inplace", &Poly::add_inplace)
         .def("sub_inplace", &Poly::sub_inplace)
@@ -131,7 +131,7 @@ PYBIND11_MODULE(tetris_ref, m) {
         .def("mul_small_scalar_inplace", &Poly::mul_small_scalar_inplace)
         .def("drop_to_level", &Poly::drop_to_level);
 
-    m.def("ntt_transform", &ntt_transform);
+    m.def("ntt_transform", &ntt_transform, py::call_guard<py::gil_scoped_release>());
     m.def("poly_from_i64", &poly_from_i64, py::arg("ring"), py::arg("coeffs"), py::arg("level"),
           py::arg("nspecial") = 0);
     m.def("raise_level", &raise_level, py::arg("p"), py::arg("new_level"), py::arg("nspecial") = 0);

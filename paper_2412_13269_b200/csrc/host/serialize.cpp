@@ -43,6 +43,14 @@ struct Reader {
         std::memcpy(&v, take(sizeof(T)), sizeof(T));
         return v;
     }
+    std::size_t left() const { return std::size_t(end - p); }
+    // a count read from the input must fit the bytes that are left, each item
+    // taking at least `min_item` bytes, before anything is allocated for it
+    u32 count(std::size_t min_item) {
+        const u32 n = u32v();
+        if (min_item && std::size_t(n) > left() / min_item) throw TetrisError("serialize", "truncated input");
+        return n;
+    }
     uint8_t u8() { return *take(1); }
     u16 u16v() { return get<u16>(); }
     u32 u32v() { return get<u32>(); }
@@ -117,8 +125,8 @@ SwitchingKey read_switching_key_body(Reader& r, const RingParams& ring) {
     k.from_id = r.u64v();
     k.to_id = r.u64v();
     k.a_seed = r.u64v();
-    const u32 n = r.u32v();
     const int lvl = ring.max_level(), ksp = int(ring.special_count());
+    const u32 n = r.count(poly_size(ring, lvl, ksp));  // before the 2*w*n-word device block
     const std::size_t w = std::size_t(lvl + 1 + ksp) * ring.degree();
     k.block = detail::new_block(ring, 2 * w * n);  // the device layout [digit][b|a][rows][N]
     Rng ra(k.a_seed);
@@ -158,7 +166,7 @@ Ciphertext deserialize_ciphertext(const std::vector<uint8_t>& buf, const RingPar
     Reader r(buf);
     if (read_header(r, ring) != ObjectKind::ciphertext) throw TetrisError("serialize", "object kind mismatch");
     Ciphertext ct;
-    const u32 parts = r.u32v();
+    const u32 parts = r.count(poly_size(ring, 0, 0));
     ct.scale = r.f64();
     ct.domain = r.u8() ? Domain::slots : Domain::coeffs;
     ct.sk_id = r.u64v();
@@ -217,18 +225,18 @@ MinimaxChain deserialize_chain(const std::vector<uint8_t>& buf) {
     c.params.alpha = r.u32v();
     c.params.beta = r.u32v();
     c.params.epsilon = r.f64();
-    const u32 nd = r.u32v();
+    const u32 nd = r.count(4);
     for (u32 i = 0; i < nd; ++i) c.params.degrees.push_back(r.u32v());
     c.sign_error = r.f64();
     c.achieved_beta = r.f64();
-    const u32 ns = r.u32v();
+    const u32 ns = r.count(32);
     for (u32 i = 0; i < ns; ++i) {
         ChainStage st;
         st.degree = r.u32v();
         st.gamma = r.f64();
         st.upper = r.f64();
         st.error = r.f64();
-        st.cheb.resize(r.u32v());
+        st.cheb.resize(r.count(8));
         for (auto& x : st.cheb) x = r.f64();
         c.stages.push_back(std::move(st));
     }
@@ -248,7 +256,7 @@ SecretKey deserialize_secret_key(const std::vector<uint8_t>& buf, const RingPara
     Reader r(buf);
     if (read_header(r, ring) != ObjectKind::secret_key) throw TetrisError("serialize", "object kind mismatch");
     const u64 id = r.u64v();
-    std::vector<i64> c(r.u32v());
+    std::vector<i64> c(r.count(8));
     for (auto& x : c) x = r.i64v();
     return SecretKey(ring, std::move(c), id);
 }

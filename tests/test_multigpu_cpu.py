@@ -151,3 +151,25 @@ def test_sharded_statement_count_bit_exact(world):
     assert got[-1] == want.level() and got[-2] == want.scale
     for a, b in zip(got[:-2], want.parts):
         assert np.array_equal(a, b.to_numpy())
+
+
+@pytest.mark.parametrize("n_blocks,world", [(8, 1), (8, 2), (8, 4), (8, 8), (32, 8), (3, 2)])
+def test_statement_jobs_keep_batches_under_sharding(n_blocks, world):
+    """Every rank's (column, block) threshold jobs are covered exactly once,
+    batches never mix levels (the risk column runs one level lower after the
+    score's rescale), and a rank with one record block still runs its sugar
+    and pressure thresholds as ONE batch of two (batching must
+    survive sharding at 8 GPUs)."""
+    from paper_2412_13269_b200 import workloads as W
+    for rank in range(world):
+        mine = D.shard(n_blocks, world, rank)
+        batches = W.statement_jobs(len(mine), 8)
+        jobs = [j for b in batches for j in b]
+        assert sorted(jobs) == sorted((c, i) for c in W.COLUMNS for i in range(len(mine)))
+        for b in batches:
+            assert len(b) <= 8
+            assert len({c == "risk" for c, _ in b}) == 1  # one level per batch
+            assert len({W.COLUMN_NORM[c] for c, _ in b}) == 1
+        if mine:
+            sb = [b for b in batches if b[0][0] != "risk"]
+            assert min(len(b) for b in sb) >= min(2, 2 * len(mine))

@@ -61,3 +61,29 @@ def test_secret_key_bytes(G, R, pair):
     assert bg == br
     sk = G.deserialize_secret_key(br, g.ring)
     assert sk.id() == g.sk.id() and list(sk.coeffs()) == list(g.sk.coeffs())
+
+
+def test_hostile_counts_rejected_before_allocation(G):
+    """A count read from untrusted bytes must fit the bytes that follow
+    before anything is allocated (a short buffer claiming 2^32-1
+    key digits must not reserve 2*w*n device words). Runs without a GPU: the
+    check fires before the first device allocation."""
+    import struct
+    N = 64
+    moduli = list(G.find_ntt_primes(40, 3, 2 * N)) + list(G.find_ntt_primes(50, 1, 2 * N))
+    ring = G.RingParams(N, moduli, 1)
+    hdr = struct.pack("<IHHIII", 0x54545253, 1, 2, N, len(moduli), 1) + b"".join(struct.pack("<Q", q) for q in moduli)
+    body = struct.pack("<IIQQQI", 2, 0, 1, 2, 3, 0xFFFFFFFF)  # gadget, ids, a_seed, digit count
+    with pytest.raises(Exception, match="truncated input"):
+        G.deserialize_switching_key(hdr + body, ring)
+    ct_hdr = struct.pack("<IHHIII", 0x54545253, 1, 1, N, len(moduli), 1) + b"".join(struct.pack("<Q", q) for q in moduli)
+    with pytest.raises(Exception, match="truncated input"):
+        G.deserialize_ciphertext(ct_hdr + struct.pack("<I", 1 << 30) + b"\0" * 25, ring)
+    sk_hdr = struct.pack("<IHHIII", 0x54545253, 1, 7, N, len(moduli), 1) + b"".join(struct.pack("<Q", q) for q in moduli)
+    with pytest.raises(Exception, match="truncated input"):
+        G.deserialize_secret_key(sk_hdr + struct.pack("<QI", 5, 1 << 31), ring)
+    chain = G.serialize_chain(G.build_chain(G.ThresholdParams(8, 12, [15], 0.0)))
+    bad = bytearray(chain)
+    bad[24:28] = struct.pack("<I", 0xFFFFFFF0)  # the degree count (after magic, version, kind, alpha, beta, epsilon)
+    with pytest.raises(Exception, match="truncated input"):
+        G.deserialize_chain(bytes(bad))
