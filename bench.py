@@ -1022,6 +1022,7 @@ def run_config1(args):
     y = G.stack_ciphertexts(cts[1:] + cts[:1])
     x_eval = x.copy()
     x_eval.to_eval()
+    G.pool_reserve(ring, int(min(args.pool_gb, 16.0) * (1 << 30)))  # no pool growth inside timed steps
     ext = torch.cuda.ExternalStream(ring.stream_handle(), device=torch.device("cuda", local))
     flush = torch.empty(64 << 22, dtype=torch.int32, device="cuda")
 

@@ -148,11 +148,16 @@ extern "C" int tg_context_create(tg_context** out, int device, uint32_t degree, 
             const double qd = double(moduli[i]);
             const u64* t = tables + size_t(4) * i * degree;
             double* o = fp.data() + size_t(4) * i * degree;
+            // centred twiddles w in (-q/2, q/2]: |fl(w/q)| < 1/2 widens the
+            // FP64 modmul's input window to |b| < 2^52 (tg_fp64.cuh), which
+            // is what lets six forward stages / two inverse stages run
+            // between reductions; w - q is exact (both < 2^53)
+            const auto centred = [&](u64 x) { return x > moduli[i] / 2 ? double(x) - qd : double(x); };
             for (u32 j = 0; j < degree; ++j) {
-                o[j] = double(t[j]);
-                o[degree + j] = double(t[j]) / qd;
-                o[2 * size_t(degree) + j] = double(t[2 * size_t(degree) + j]);
-                o[3 * size_t(degree) + j] = double(t[2 * size_t(degree) + j]) / qd;
+                o[j] = centred(t[j]);
+                o[degree + j] = o[j] / qd;
+                o[2 * size_t(degree) + j] = centred(t[2 * size_t(degree) + j]);
+                o[3 * size_t(degree) + j] = o[2 * size_t(degree) + j] / qd;
             }
             double* s = fp.data() + nt + 4 * size_t(i);
             s[0] = qd;

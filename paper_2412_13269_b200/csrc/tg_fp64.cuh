@@ -18,6 +18,13 @@ constexpr u64 kFpMaxQ = 1351079888211148ull;          // 1.2 * 2^50: FP path bou
 __device__ __forceinline__ double u2d(u64 x) {
     return __dsub_rn(__longlong_as_double(static_cast<long long>(0x4330000000000000ull | x)), kTwo52);
 }
+// canonical u64 x in [0, q) -> the exact double of its centred representative
+// in (-q/2, q/2] (the sign choice on the integer ALU, one FP64 add: 1.5 * 2^52
+// + s has s as the low bits of its mantissa for |s| < 2^51).
+__device__ __forceinline__ double c2d(u64 x, u64 q) {
+    const long long s = static_cast<long long>(x > (q >> 1) ? x - q : x);
+    return __dsub_rn(__longlong_as_double(0x4338000000000000ll + s), kRoundMagic);
+}
 // exact double integer v in [0, 2^52) -> u64
 __device__ __forceinline__ u64 d2u(double v) {
     return static_cast<u64>(__double_as_longlong(__dadd_rn(v, kTwo52))) & 0x000FFFFFFFFFFFFFull;
@@ -35,12 +42,22 @@ __device__ __forceinline__ u64 d2u(double v) {
 //       and fma(-k, q, h) = h - k q is an exact integer (|.| < 2^53),
 //       as is r = (h - k q) + l = b w - k q.
 // Bound: |r| <= q (1/2 + |b| 2^-54) when b wq < 2^51, else q (1 + |b| 2^-54).
-// NTT use (q < 1.2 * 2^50, so q 2^-54 <= 0.075): forward stage blocks start
-// from [0, q) (column phase) or |v| <= q/2 + 1 (chunk phase); three stages
-// keep every multiplier input in [-1.19q, 2.19q] resp. |b| <= 1.62q, i.e.
-// b wq > -1.95 * 2^50 > -2^51, and |v| <= 3.35q < 2^52 before the block's
-// fp_reduce. Inverse inputs stay within |b| <= 1.2q. The config primes are
-// the 50-bit NTT primes nearest 2^50 (both sides), all below the bound.
+// NTT use: the FP64 twiddle tables hold CENTRED twiddles w in (-q/2, q/2]
+// (tg_context.cu), so |wq| < 1/2, fl(w/q) errs by <= 2^-55 and the window
+// b wq in [-2^51, 2^51) holds for every |b| < 2^52; the same derivation gives
+// |r| <= q/2 + |b| q 2^-55 <= q/2 + 0.0375 |b| (q < 1.2 * 2^50).
+//  * Forward (CT, x' = x + r, y' = x - r): from |v| <= q/2 + 1 (centred
+//    inputs, c2d) the bound after s stages is B_s with B_(s+1) = 1.0375 B_s +
+//    q/2: B_5 = 3.296q < 2^52 (the sixth stage's multiplier input) and B_6 =
+//    3.92q < 2^53, so six stages run without a reduction (radix-8 blocks:
+//    fp_reduce after the second block, then after the last; N = 2^15/2^14
+//    phases of 7 stages: after the third and fourth blocks).
+//  * Inverse (GS, x' = x + y, y' = (x - y) w): inputs |v| <= 0.6q; the sum is
+//    reduced after every ODD stage (and the last one): an unreduced stage
+//    leaves |v| <= 1.2q, so the next multiplier input |x - y| <= 2.4q < 2^52
+//    and its products are <= 0.59q; after the reducing stage |v| <= 0.6q again.
+// The config primes are the 50-bit NTT primes nearest 2^50 (both sides), all
+// below the bound.
 __device__ __forceinline__ double fp_mulmod(double b, double w, double wq, double q) {
     const double h = __dmul_rn(b, w);
     const double l = __fma_rn(b, w, -h);

@@ -16,6 +16,8 @@
 #include <cstdlib>
 #include <utility>
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors; the encoder is fetched through cudaGetDriverEntryPoint)
+
 #include "tg_internal.cuh"
 #include "tg_fp64.cuh"
 

@@ -54,15 +54,15 @@ template <int E>
 __device__ __forceinline__ void wfwd_all_pair(double (&v)[2][E], double2* pr, u32 pw, u32 lane, const u64* sw,
                                               double q, double qi) {
     if constexpr (E == 8) {
-        wfwd_fp<2, 8, false, 5, 7, 5>(v, lane, sw, q, qi, 0);
+        wfwd_fp<2, 8, false, 5, 7, 5, false>(v, lane, sw, q, qi, 0);
         wxchg_pair<8>(v, pr, pw, lane, 5, 2);
         wfwd_fp<2, 8, false, 2, 4, 2>(v, lane, sw, q, qi, 0);
         wxchg_pair<8>(v, pr, pw, lane, 2, 0);
         wfwd_fp<2, 8, false, 0, 1, 0>(v, lane, sw, q, qi, 0);
     } else {
-        wfwd_fp<2, 4, false, 5, 6, 5>(v, lane, sw, q, qi, 0);
+        wfwd_fp<2, 4, false, 5, 6, 5, false>(v, lane, sw, q, qi, 0);
         wxchg_pair<4>(v, pr, pw, lane, 5, 3);
-        wfwd_fp<2, 4, false, 3, 4, 3>(v, lane, sw, q, qi, 0);
+        wfwd_fp<2, 4, false, 3, 4, 3, false>(v, lane, sw, q, qi, 0);
         wxchg_pair<4>(v, pr, pw, lane, 3, 1);
         wfwd_fp<2, 4, false, 1, 2, 1>(v, lane, sw, q, qi, 0);
         wxchg_pair<4>(v, pr, pw, lane, 1, 0);
@@ -153,6 +153,7 @@ kw_fwd_cols2(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb,
     const u32 mi = mod_index(r, level, R.q_count);
     const u64* w = reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N);
     const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+    const u64 qq = R.q[mi];
     const u32 c0 = blockIdx.x * 16;
     issue_pair_tile<E, N2>(reinterpret_cast<double2*>(dyn), src + size_t(p * rpp + r) * N + c0);
     stage_col_twiddles<E, true>(sw, nullptr, w, w + N);
@@ -179,8 +180,8 @@ kw_fwd_cols2(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb,
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const double2 t = pr[pu(lane + 32 * j, warp)];
-            v[0][j] = u2d(static_cast<u64>(__double_as_longlong(t.x)));
-            v[1][j] = u2d(static_cast<u64>(__double_as_longlong(t.y)));
+            v[0][j] = c2d(static_cast<u64>(__double_as_longlong(t.x)), qq);
+            v[1][j] = c2d(static_cast<u64>(__double_as_longlong(t.y)), qq);
         }
         wfwd_all_pair<E>(v, pr, warp, lane, sw, qd, qi);
         __syncwarp();
@@ -250,5 +251,114 @@ kw_inv_cols2(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 
         __syncthreads();
         store_pair_tile<E, N2>(tile, data + size_t(p * rpp + r) * N + c0);
         __syncthreads();  // the tile is the next prefetch target
+    }
+}
+
+// ---------------------------------------------------------------------------
+// TMA fill of the forward column-pair tile (cp.async.bulk.tensor.2d): the
+// row is viewed as a 2-D tensor [rows x 256][256] of u64 (column index
+// innermost, row stride 2 KB); one thread issues ONE 16-column x 256-row box
+// (32 KB) per tile into a 1024-byte-aligned buffer with the hardware 128-byte
+// swizzle (16-byte unit w of tile row k lands in unit 8k + (w ^ (k & 7))),
+// completion tracked by an mbarrier (expect_tx = 32 KB). Replaces the 8
+// 16-byte cp.async per thread of issue_pair_tile; the tile is read once in
+// the TMA layout (conflict-free: lanes l..l+7 read k = l + 32j, distinct
+// k & 7), after which every exchange uses the pu() layout as before.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 pu_tma(u32 k, u32 w) { return 8 * k + (w ^ (k & 7)); }
+
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+    const u32 a = static_cast<u32>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+    const u32 a = static_cast<u32>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+    const u32 a = static_cast<u32>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra LAB_WAIT;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_tile(void* smem_dst, const void* tmap, u64* bar, int c0, int row) {
+    const u32 d = static_cast<u32>(__cvta_generic_to_shared(smem_dst));
+    const u32 b = static_cast<u32>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(d),
+        "l"(tmap), "r"(c0), "r"(row), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+template <int E>
+constexpr size_t pair_tma_smem() {  // two tiles + twiddles + 2 mbarriers
+    return size_t(16) * 8 * PGeo<E>::M * 2 + size_t(8) * 2 * WGeo<E>::TW_COL + 16;
+}
+
+template <int E, int E2>
+__global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
+kw_fwd_cols2_tma(const __grid_constant__ CUtensorMap tmap, DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb,
+                 int level, u32 skip_gs, u32 row0) {
+    using Pg = PGeo<E>;
+    constexpr u32 N = 32 * E * 32 * E2, N2 = 32 * E2, M = Pg::M;
+    constexpr u32 TILE_BYTES = 16u * 8u * M;
+    const u32 r = row0 + blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
+    u32 p = next_poly(blockIdx.z * ppb, pend, r, rpp, level, skip_gs);
+    if (p >= pend) return;
+    extern __shared__ __align__(1024) u64 dyn_tma[];  // 128-byte swizzle atoms need a 1024-byte aligned tile
+    double2* tiles = reinterpret_cast<double2*>(dyn_tma);
+    u64* sw = reinterpret_cast<u64*>(tiles + 2 * 8 * M);
+    u64* bars = sw + 2 * WGeo<E>::TW_COL;
+    const u32 mi = mod_index(r, level, R.q_count);
+    const u64* w = reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N);
+    const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
+    const u64 qq = R.q[mi];
+    const u32 c0 = blockIdx.x * 16;
+    if (threadIdx.x == 0) {
+        mbar_init(bars, 1);
+        mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        mbar_expect_tx(bars, TILE_BYTES);
+        tma_load_tile(tiles, &tmap, bars, int(c0), int((p * rpp + r) * M));
+    }
+    stage_col_twiddles<E, true>(sw, nullptr, w, w + N);
+    __syncthreads();  // barrier init and twiddles visible to every thread
+    const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    u32 phase[2] = {0, 0};
+    for (u32 cur = 0; p < pend;) {
+        const u32 pn = next_poly(p + 1, pend, r, rpp, level, skip_gs);
+        double2* tile = tiles + cur * 8 * M;
+        if (threadIdx.x == 0 && pn < pend) {  // next poly's tile in flight during this transform
+            fence_proxy_async();  // the other buffer's last generic-proxy accesses precede the async write
+            mbar_expect_tx(bars + (cur ^ 1), TILE_BYTES);
+            tma_load_tile(tiles + (cur ^ 1) * 8 * M, &tmap, bars + (cur ^ 1), int(c0), int((pn * rpp + r) * M));
+        }
+        mbar_wait(bars + cur, phase[cur]);
+        phase[cur] ^= 1;
+        double2* pr = tile;
+        double v[2][E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const double2 t = pr[pu_tma(lane + 32 * j, warp)];
+            v[0][j] = c2d(static_cast<u64>(__double_as_longlong(t.x)), qq);
+            v[1][j] = c2d(static_cast<u64>(__double_as_longlong(t.y)), qq);
+        }
+        __syncthreads();  // every warp has read the TMA layout before the exchanges overwrite the tile
+        wfwd_all_pair<E>(v, pr, warp, lane, sw, qd, qi);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < E; ++j) pr[pu((lane << WGeo<E>::LOGE) | j, warp)] = make_double2(v[0][j], v[1][j]);
+        __syncthreads();
+        store_pair_tile<E, N2>(tile, data + size_t(p * rpp + r) * N + c0);
+        __syncthreads();  // the tile is the next TMA target
+        p = pn;
+        cur ^= 1;
     }
 }

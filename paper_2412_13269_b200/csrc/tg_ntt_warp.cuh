@@ -187,15 +187,15 @@ __device__ __forceinline__ void wxchg(T (&v)[E], u64* colw, u32 lane, u32 lo_fro
 
 // ---- FP64 path (q < 1.2 * 2^50; tg_fp64.cuh) ------------------------------
 // Staged twiddle pairs are (w, fl(w/q)) doubles. Forward blocks hold at most
-// 3 stages; with the bounds of tg_fp64.cuh every multiplier input stays in
-// [-1.2q, 2.2q] (column phase, inputs [0, q)) or |b| <= 1.6q (chunk phase,
-// inputs |v| <= q/2 + 1) and |v| < 3.4q < 2^53 before the block-final
-// fp_reduce to |v| <= q/2 + 1. Inverse butterflies reduce a+b every stage
-// (|a|,|b| <= 0.6q after the first stage, so |a-b| <= 1.2q).
+// 3 stages; with the centred twiddles and bounds of tg_fp64.cuh six forward
+// stages run between reductions from centred inputs (|v| <= q/2 + 1; the
+// column phase centres canonical inputs with c2d), so only the second and the
+// last radix-8 block end in fp_reduce (RED). Inverse butterflies reduce the
+// sum after odd stages only (|x - y| <= 2.4q < 2^52 in between).
 // NP independent transforms of the same modulus and position (NP polys) run
 // interleaved: each staged twiddle feeds NP butterflies and the FP64
 // dependency chains of one transform hide behind the other's.
-template <int NP, int E, bool CHUNK, int LAY, int HI, int LO>
+template <int NP, int E, bool CHUNK, int LAY, int HI, int LO, bool RED = true>
 __device__ __forceinline__ void wfwd_fp(double (&v)[NP][E], u32 lane, const u64* sw, double q, double qi, u32 c) {
     constexpr int LOGE = WGeo<E>::LOGE, LOGM = WGeo<E>::LOGM;
 #pragma unroll
@@ -215,10 +215,12 @@ __device__ __forceinline__ void wfwd_fp(double (&v)[NP][E], u32 lane, const u64*
             }
         }
     }
+    if constexpr (RED) {  // block-final reduction (skipped where tg_fp64.cuh's bound allows)
 #pragma unroll
-    for (int n = 0; n < NP; ++n)
+        for (int n = 0; n < NP; ++n)
 #pragma unroll
-        for (int j = 0; j < E; ++j) v[n][j] = fp_reduce(v[n][j], q, qi);
+            for (int j = 0; j < E; ++j) v[n][j] = fp_reduce(v[n][j], q, qi);
+    }
 }
 
 template <int NP, int E, bool CHUNK, int LAY, int LO, int HI>
@@ -235,7 +237,9 @@ __device__ __forceinline__ void winv_fp(double (&v)[NP][E], u32 lane, const u64*
 #pragma unroll
             for (int n = 0; n < NP; ++n) {
                 const double a = v[n][j], bb = v[n][j | (1 << b)];
-                v[n][j] = fp_reduce(__dadd_rn(a, bb), q, qi);
+                // sums reduced after odd stages and the last one (tg_fp64.cuh)
+                if ((p & 1) == 1 || p == LOGM - 1) v[n][j] = fp_reduce(__dadd_rn(a, bb), q, qi);
+                else v[n][j] = __dadd_rn(a, bb);
                 v[n][j | (1 << b)] = fp_mulmod(__dsub_rn(a, bb), tw.x, tw.y, q);
             }
         }
@@ -290,15 +294,15 @@ template <int NP, int E, bool CHUNK, bool PX = false>
 __device__ __forceinline__ void wfwd_all_fp(double (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double q,
                                             double qi, u32 c) {
     if constexpr (E == 8) {
-        wfwd_fp<NP, 8, CHUNK, 5, 7, 5>(v, lane, sw, q, qi, c);
+        wfwd_fp<NP, 8, CHUNK, 5, 7, 5, false>(v, lane, sw, q, qi, c);
         wxchg_any<NP, 8, PX>(v, col, cs, lane, 5, 2);
         wfwd_fp<NP, 8, CHUNK, 2, 4, 2>(v, lane, sw, q, qi, c);
         wxchg_any<NP, 8, PX>(v, col, cs, lane, 2, 0);
         wfwd_fp<NP, 8, CHUNK, 0, 1, 0>(v, lane, sw, q, qi, c);
     } else {
-        wfwd_fp<NP, 4, CHUNK, 5, 6, 5>(v, lane, sw, q, qi, c);
+        wfwd_fp<NP, 4, CHUNK, 5, 6, 5, false>(v, lane, sw, q, qi, c);
         wxchg_any<NP, 4, PX>(v, col, cs, lane, 5, 3);
-        wfwd_fp<NP, 4, CHUNK, 3, 4, 3>(v, lane, sw, q, qi, c);
+        wfwd_fp<NP, 4, CHUNK, 3, 4, 3, false>(v, lane, sw, q, qi, c);
         wxchg_any<NP, 4, PX>(v, col, cs, lane, 3, 1);
         wfwd_fp<NP, 4, CHUNK, 1, 2, 1>(v, lane, sw, q, qi, c);
         wxchg_any<NP, 4, PX>(v, col, cs, lane, 1, 0);
@@ -538,7 +542,7 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
 #pragma unroll
                 for (int n = 0; n < 2; ++n)
 #pragma unroll
-                    for (int j = 0; j < E; ++j) v[n][j] = u2d(col[n * 8 * Gm::CS + wpad(lane + 32 * j)]);
+                    for (int j = 0; j < E; ++j) v[n][j] = c2d(col[n * 8 * Gm::CS + wpad(lane + 32 * j)], q);
                 wfwd_all_fp<2, E, false>(v, col, 8 * Gm::CS, lane, sw, qd, qi, 0);
                 __syncwarp();
 #pragma unroll
@@ -550,7 +554,7 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
             } else {
                 double v[1][E];
 #pragma unroll
-                for (int j = 0; j < E; ++j) v[0][j] = u2d(col[wpad(lane + 32 * j)]);
+                for (int j = 0; j < E; ++j) v[0][j] = c2d(col[wpad(lane + 32 * j)], q);
                 wfwd_all_fp<1, E, false>(v, col, 0, lane, sw, qd, qi, 0);
                 __syncwarp();
                 double* cold = reinterpret_cast<double*>(col);
@@ -581,7 +585,7 @@ kw_fwd_cols(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, 
             const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
             double v[1][E];
 #pragma unroll
-            for (int j = 0; j < E; ++j) v[0][j] = u2d(col[wpad(lane + 32 * j)]);
+            for (int j = 0; j < E; ++j) v[0][j] = c2d(col[wpad(lane + 32 * j)], q);
             wfwd_all_fp<1, E, false>(v, col, 0, lane, sw, qd, qi, 0);
             __syncwarp();
             double* cold = reinterpret_cast<double*>(col);
@@ -652,12 +656,12 @@ __device__ __forceinline__ void chunk_fwd_fp(u64 (&v)[NP][E], u64* col, u32 cs, 
 // inverse (canonical in, doubles |v| <= 1.5q as raw bits out to phase B)
 template <int NP, int E, bool PX = false>
 __device__ __forceinline__ void chunk_inv_fp(u64 (&v)[NP][E], u64* col, u32 cs, u32 lane, const u64* sw, double qd,
-                                             double qi, u32 warp) {
+                                             double qi, u32 warp, u64 q) {
     double vd[NP][E];
 #pragma unroll
     for (int n = 0; n < NP; ++n)
 #pragma unroll
-        for (int j = 0; j < E; ++j) vd[n][j] = u2d(v[n][j]);
+        for (int j = 0; j < E; ++j) vd[n][j] = c2d(v[n][j], q);  // centred: |v| <= q/2 (tg_fp64.cuh inverse bound)
     winv_all_fp<NP, E, true, PX>(vd, col, cs, lane, sw, qd, qi, warp);
 #pragma unroll
     for (int n = 0; n < NP; ++n)
@@ -852,11 +856,11 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
             }
             cp_async_commit();
             if (pair) {
-                chunk_inv_fp<2, E, true>(v, colp, CS2, lane, sw, qd, qi, warp);
+                chunk_inv_fp<2, E, true>(v, colp, CS2, lane, sw, qd, qi, warp, q);
                 st_strided<E>(out(p), v[0], lane);
                 st_strided<E>(out(p + 1), v[1], lane);
             } else {
-                chunk_inv_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), colp, CS2, lane, sw, qd, qi, warp);
+                chunk_inv_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), colp, CS2, lane, sw, qd, qi, warp, q);
                 st_strided<E>(out(p), v[0], lane);
             }
             if (pn >= pend) break;
@@ -873,12 +877,12 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
         __syncthreads();
         while (true) {
             if (p + 1 < pend) {
-                chunk_inv_fp<2, E, true>(v, colp, CS2, lane, sw, qd, qi, warp);
+                chunk_inv_fp<2, E, true>(v, colp, CS2, lane, sw, qd, qi, warp, q);
                 st_strided<E>(out(p), v[0], lane);
                 st_strided<E>(out(p + 1), v[1], lane);
                 p += 2;
             } else {
-                chunk_inv_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), colp, CS2, lane, sw, qd, qi, warp);
+                chunk_inv_fp<1, E>(reinterpret_cast<u64(&)[1][E]>(v[0]), colp, CS2, lane, sw, qd, qi, warp, q);
                 st_strided<E>(out(p), v[0], lane);
                 p += 1;
             }
@@ -1024,6 +1028,40 @@ inline bool warp_plan(u32 logN, int& e1, int& e2) {
     }
 }
 
+// TMA descriptor of a buffer of u64 rows viewed as [rows * M1][M2] (column
+// index innermost, 2 KB row stride at N = 2^16), box 16 columns x M1 rows,
+// 128-byte swizzle. cuTensorMapEncodeTiled comes from the driver through the
+// runtime's entry-point query (no -lcuda); false if unavailable.
+inline bool encode_col_tmap(CUtensorMap* m, const void* base, u64 matrix_rows, u32 cols, u32 box_rows) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<Encode>(f);
+    }();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {cols, matrix_rows};
+    const cuuint64_t strides[1] = {cuuint64_t(cols) * 8};
+    const cuuint32_t box[2] = {16, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline bool ntt_tma_on() {
+    static const bool on = [] {
+        const char* e = getenv("TG_NTT_TMA");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 template <int E1, int E2>
 void set_smem_attrs() {
     // thread-safe one-time init (one process drives one device)
@@ -1034,6 +1072,8 @@ void set_smem_attrs() {
         cudaFuncSetAttribute(kw_inv_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
         cudaFuncSetAttribute(kw_fwd_cols2<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pair_smem<E1>()));
         cudaFuncSetAttribute(kw_inv_cols2<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pair_smem<E1>()));
+        cudaFuncSetAttribute(kw_fwd_cols2_tma<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(pair_tma_smem<E1>()));
         return true;
     }();
     (void)done;
@@ -1055,6 +1095,12 @@ void launch_fwd_cols_any(const DevRing& R, int sms, u64* data, const u64* src, u
     const u32 M2 = 32 * E2;
     if (pair && E1 == 8) {  // column pairs (tg_ntt_cols2.cuh), N = 2^16
         const u32 p1 = polys_per_block(M2 / 16, nrows, npolys, sms);
+        CUtensorMap tm;
+        if (ntt_tma_on() && encode_col_tmap(&tm, src, u64(rpp) * npolys * (32 * E1), M2, 32 * E1)) {
+            kw_fwd_cols2_tma<E1, E2><<<dim3(M2 / 16, nrows, (npolys + p1 - 1) / p1), 256, pair_tma_smem<E1>(), s>>>(
+                tm, R, data, rpp, npolys, p1, level, skip_gs, row0);
+            return;
+        }
         kw_fwd_cols2<E1, E2><<<dim3(M2 / 16, nrows, (npolys + p1 - 1) / p1), 256, pair_smem<E1>(), s>>>(
             R, data, src, rpp, npolys, p1, level, skip_gs, row0);
         return;
