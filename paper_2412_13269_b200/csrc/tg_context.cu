@@ -467,7 +467,7 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
     // the FP64 bound: [K][4] (p_s, fl(c_s/p_s), c_s, floor(p_s/2));
     // [nq][K][2] (w, fl(w/q_r)), w = -(P/p_s) P^-1 mod q_r;
     // [nq][4] (P^-1 mod q_r, fl(./q_r), q_r, fl(1/q_r)).
-    std::vector<double> mdf(size_t(K) * 4 + size_t(nq) * K * 2 + size_t(nq) * 4, 0.0);
+    std::vector<double> mdf(size_t(K) * 4 + size_t(nq) * K * 2 + size_t(nq) * 4, 0.0), mdfn;
     g->g.fp_moddown = K > 0;
     for (u32 t = 0; t < nmod; ++t) g->g.fp_moddown &= mod[t] < kFpMaxQ;
     if (const char* e = getenv("TG_INT_MODDOWN"); e && *e == '1') g->g.fp_moddown = false;  // A/B experiments
@@ -493,8 +493,27 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
             e[2] = double(q);
             e[3] = 1.0 / double(q);
         }
+        // N^-1 folded into the input constants: the fused key switch hands
+        // ModDown the accumulators' inverse transform WITHOUT its final
+        // N^-1 scaling (raw doubles, |v| <= 0.6q); every input enters ModDown
+        // only through an exact product with one of these constants, so
+        // c_s N^-1 and P^-1 N^-1 give the same canonical residues
+        mdfn = mdf;
+        const u64 n = ctx->ring.N;
+        for (u32 s = 0; s < K; ++s) {
+            const u64 ps = mod[nq + s], c = h_mul_mod(md[2 * s], h_inv_mod(n % ps, ps), ps);
+            mdfn[4 * s + 1] = double(c) / double(ps);
+            mdfn[4 * s + 2] = double(c);
+        }
+        for (u32 r = 0; r < nq; ++r) {
+            const u64 q = mod[r], pinv = md[2 * K + size_t(K) * nq * 4 + size_t(r) * 2];
+            const u64 pn = h_mul_mod(pinv, h_inv_mod(n % q, q), q);
+            double* e = &mdfn[4 * K + size_t(nq) * K * 2 + size_t(r) * 4];
+            e[0] = double(pn);
+            e[1] = double(pn) / double(q);
+        }
     }
-    size_t words = src.size() + conv.size() + md.size() + mdf.size();
+    size_t words = src.size() + conv.size() + md.size() + mdf.size() + mdfn.size();
     cudaError_t e = cudaMalloc(&g->dev_block, words * 8);
     if (e != cudaSuccess) {
         delete g;
@@ -505,10 +524,13 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
     g->g.conv = p + src.size();
     g->g.md = p + src.size() + conv.size();
     g->g.mdf = reinterpret_cast<double*>(g->g.md + md.size());
+    g->g.mdfn = mdfn.empty() ? nullptr : g->g.mdf + mdf.size();
     e = cudaMemcpy(g->g.src, src.data(), src.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g->g.conv, conv.data(), conv.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !md.empty()) e = cudaMemcpy(g->g.md, md.data(), md.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !mdf.empty()) e = cudaMemcpy(g->g.mdf, mdf.data(), mdf.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !mdfn.empty())
+        e = cudaMemcpy(g->g.mdfn, mdfn.data(), mdfn.size() * 8, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         cudaFree(g->dev_block);
         delete g;

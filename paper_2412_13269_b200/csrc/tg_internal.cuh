@@ -168,6 +168,7 @@ struct GadgetDev {
     u64* md;    // ModDown: [K][2] (P/p_s)^-1 mod p_s; [K][q_count][4] +-(P/p_s) mod q_r; [q_count][2] P^-1 mod q_r;
                 // [q_count][4] P mod q_r (u64, Shoup, FP64 value, FP64 quotient)
     double* mdf;  // FP64 ModDown (all moduli < kFpMaxQ): see k_mod_down_fp
+    double* mdfn; // the same with N^-1 folded into the input constants (raw inverse-NTT input, RAW = true)
     bool lazy_modup, lazy_moddown;  // lazy sums provably fit a word (checked on the host)
     bool fp_moddown;                // every modulus below the FP64 bound: ModDown on the FP64 pipe
     u32 base2_bits;                 // 0: RNS digits; else balanced base-2^b sub-digits (group_size 1)
@@ -262,7 +263,9 @@ int ntt_inverse_oop(tg_context* ctx, u64* dst, const u64* src, int level, int ns
 // accumulators after the inverse chunk phase (finish with ntt_inverse_cols).
 bool ks_fused_ok(const tg_context* ctx);
 int ntt_forward_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s, u32 skip_gs);
-int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s);
+int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s,
+                     bool raw = false);
+bool ntt_inverse_cols_raw_ok(const tg_context* ctx);
 int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key, int level,
                     u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s);
 struct DeviceGuard {

@@ -697,16 +697,21 @@ k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restric
 // w = -(P/p_s) P^-1 mod q_r; [nq][4] (P^-1 mod q_r, fl(./q_r), q_r, fl(1/q_r)).
 // KMAX = K exactly (dispatch in mod_down): every per-special loop is
 // compile-time, no predicated terms.
-template <int KMAX>
+// RAW: `in` holds the raw doubles of an inverse NTT without its N^-1 factor
+// (|v| <= 0.6q, kw_inv_cols2<..., true>); the input constants carry N^-1
+// (G.mdfn), so the canonical outputs are the same.
+template <int KMAX, bool RAW = false>
 __global__ void __launch_bounds__(256)
 k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict__ in, int level, u32 npolys,
               const u64* __restrict__ addend, u32 rows_per_group) {
     constexpr u32 K = KMAX;
     const u32 N = R.N, nq = R.q_count, lvl = u32(level);
     const u32 rin = lvl + 1 + K, rout = lvl + 1;
-    const double* ys_t = G.mdf;                         // [K][4]
-    const double* w_rs = G.mdf + 4 * K;                 // [nq][K][2]
+    const double* tab = RAW ? G.mdfn : G.mdf;
+    const double* ys_t = tab;                           // [K][4]
+    const double* w_rs = tab + 4 * K;                   // [nq][K][2]
     const double* p_r = w_rs + size_t(nq) * K * 2;      // [nq][4]
+    auto in_d = [](u64 x) { return RAW ? __longlong_as_double(static_cast<long long>(x)) : u2d(x); };
     extern __shared__ double2 smf[];  // [rout][K] (w, wq), then [rout][2] (pinv, pinvq | q, qi), then [rout] q (u64)
     double2* sp = smf + size_t(rout) * K;
     u64* sq64 = reinterpret_cast<u64*>(sp + 2 * rout);
@@ -731,7 +736,7 @@ k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restri
                 const u64 xs[2] = {t.x, t.y};
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
-                    double v = fp_mulmod(u2d(xs[cc]), cw, cq, ps);  // |v| <= 0.58 p
+                    double v = fp_mulmod(in_d(xs[cc]), cw, cq, ps);  // |v| <= 0.58 p
                     if (v < 0) v = __dadd_rn(v, ps);                 // canonical [0, p)
                     if (v > half) v = __dsub_rn(v, ps);              // to_centered (common.hpp:84-86)
                     y[s][cc] = v;
@@ -739,27 +744,24 @@ k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restri
             }
         }
         const u32 r_end = min(rout, (blockIdx.y + 1) * rows_per_group);
-        u64 xn[2] = {0, 0}, anx[2] = {0, 0};
-        auto load_row = [&](u32 r) {
-            const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(src + size_t(r) * N);
-            xn[0] = t.x;
-            xn[1] = t.y;
-            if (add) {
-                const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(add + size_t(r) * N);
-                anx[0] = u.x;
-                anx[1] = u.y;
-            }
+        // two rows in flight ahead of the one being reduced (ncu: the row
+        // loads' long-scoreboard stalls dominated with one row of lookahead);
+        // rows alternate between two register slots, unrolled by two so the
+        // slots stay static registers
+        const u32 r_begin = blockIdx.y * rows_per_group;
+        auto load_row = [&](u32 r, ulonglong2& xv, ulonglong2& av) {
+            if (r >= r_end) return;
+            xv = *reinterpret_cast<const ulonglong2*>(src + size_t(r) * N);
+            if (add) av = *reinterpret_cast<const ulonglong2*>(add + size_t(r) * N);
         };
-        if (blockIdx.y * rows_per_group < r_end) load_row(blockIdx.y * rows_per_group);
-        for (u32 r = blockIdx.y * rows_per_group; r < r_end; ++r) {
-            const u64 x[2] = {xn[0], xn[1]}, a[2] = {anx[0], anx[1]};
-            if (r + 1 < r_end) load_row(r + 1);
+        auto reduce_row = [&](u32 r, const ulonglong2 xv, const ulonglong2 av) {
+            const u64 x[2] = {xv.x, xv.y}, a[2] = {av.x, av.y};
             const double2 pv = sp[2 * r], qv = sp[2 * r + 1];
             const double q = qv.x, qi = qv.y;
             const double2* wr = smf + size_t(r) * K;
             double acc[2];
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) acc[cc] = fp_mulmod(u2d(x[cc]), pv.x, pv.y, q);
+            for (int cc = 0; cc < 2; ++cc) acc[cc] = fp_mulmod(in_d(x[cc]), pv.x, pv.y, q);
 #pragma unroll
             for (int s = 0; s < KMAX; ++s) {
                 if (u32(s) < K) {
@@ -779,6 +781,19 @@ k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restri
                 if (add) o[cc] = add_mod(o[cc], a[cc], qu);
             }
             *reinterpret_cast<ulonglong2*>(dst + size_t(r) * N) = make_ulonglong2(o[0], o[1]);
+        };
+        ulonglong2 x0{}, a0{}, x1{}, a1{};
+        load_row(r_begin, x0, a0);
+        load_row(r_begin + 1, x1, a1);
+        for (u32 r = r_begin; r < r_end; r += 2) {
+            const ulonglong2 cx0 = x0, ca0 = a0;
+            load_row(r + 2, x0, a0);
+            reduce_row(r, cx0, ca0);
+            if (r + 1 < r_end) {
+                const ulonglong2 cx1 = x1, ca1 = a1;
+                load_row(r + 3, x1, a1);
+                reduce_row(r + 1, cx1, ca1);
+            }
         }
     }
 }
@@ -878,7 +893,7 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
     return ntt_forward_oop(ctx, digits, digits, level, int(R.K), nd * npolys, s, skip);
 }
 
-template <int KMAX>
+template <int KMAX, bool RAW = false>
 void launch_mod_down_fp(const DevRing& R, const GadgetDev& G, int sms, u64* out, const u64* in, int level,
                         u32 npolys, const u64* addend, cudaStream_t s) {
     const u32 rout = u32(level) + 1;
@@ -887,22 +902,26 @@ void launch_mod_down_fp(const DevRing& R, const GadgetDev& G, int sms, u64* out,
     const u32 blocks = u32(std::min<u64>((work + 255) / 256, u64(sms) * 8));
     const u32 groups = row_groups(u64(blocks) * 256, rout, sms);
     const u32 rpg = (rout + groups - 1) / groups;
-    k_mod_down_fp<KMAX><<<dim3(blocks, (rout + rpg - 1) / rpg), 256, smem, s>>>(R, G, out, in, level, npolys, addend,
-                                                                               rpg);
+    k_mod_down_fp<KMAX, RAW><<<dim3(blocks, (rout + rpg - 1) / rpg), 256, smem, s>>>(R, G, out, in, level, npolys,
+                                                                                    addend, rpg);
 }
 
 int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaStream_t s,
-             const u64* addend = nullptr) {
+             const u64* addend = nullptr, bool raw = false) {
     const DevRing& R = g->ctx->ring;
     ProfScope prof(g->ctx, TG_OP_MOD_DOWN, 8.0 * R.N * npolys * (2.0 * (level + 1) + R.K + (addend ? level + 1 : 0)), s);
     const GadgetDev& G = g->g;
     const int sms = g->ctx->sms;
+    if (raw && !(G.fp_moddown && G.mdfn)) return fail(TG_E_ARG, "[rlwe] raw ModDown input needs the FP64 ModDown");
     bool done = false;
     if (G.fp_moddown) {
         done = true;
         switch (R.K) {
-#define TG_MD_CASE(k) \
-    case k: launch_mod_down_fp<k>(R, G, sms, out, in, level, npolys, addend, s); break;
+#define TG_MD_CASE(k)                                                                    \
+    case k:                                                                              \
+        if (raw) launch_mod_down_fp<k, true>(R, G, sms, out, in, level, npolys, addend, s); \
+        else launch_mod_down_fp<k>(R, G, sms, out, in, level, npolys, addend, s);       \
+        break;
             TG_MD_CASE(1) TG_MD_CASE(2) TG_MD_CASE(3) TG_MD_CASE(4) TG_MD_CASE(5) TG_MD_CASE(6) TG_MD_CASE(7)
             TG_MD_CASE(8) TG_MD_CASE(9) TG_MD_CASE(10) TG_MD_CASE(11) TG_MD_CASE(12) TG_MD_CASE(13)
             TG_MD_CASE(14) TG_MD_CASE(15) TG_MD_CASE(16)
@@ -998,14 +1017,17 @@ int ks_fused_batch(tg_gadget* g, u64* out0, u64* out1, const u64* d, const u64* 
     if (int rc = ks_fused_chunks(ctx, acc, digits, nd, npolys, key, level, own, eval_add ? add0 : nullptr,
                                  eval_add ? add1 : nullptr, pmod, s))
         return rc;
-    if (int rc = ntt_inverse_cols(ctx, acc, level, int(R.K), 2 * npolys, s)) return rc;
+    // the accumulators' inverse column phase hands ModDown raw doubles
+    // (its N^-1 folded into ModDown's constants) when both kernels allow it
+    const bool raw = g->g.fp_moddown && g->g.mdfn && ntt_inverse_cols_raw_ok(ctx);
+    if (int rc = ntt_inverse_cols(ctx, acc, level, int(R.K), 2 * npolys, s, raw)) return rc;
     const u64* m0 = eval_add ? nullptr : add0;
     const u64* m1 = eval_add ? nullptr : add1;
     const size_t qwords = size_t(level + 1) * R.N;
     if (out1 == out0 + size_t(npolys) * qwords && (m0 ? m1 == m0 + size_t(npolys) * qwords : !m1))
-        return mod_down(g, out0, acc, level, 2 * npolys, s, m0);
-    if (int rc = mod_down(g, out0, acc, level, npolys, s, m0)) return rc;
-    return mod_down(g, out1, acc + size_t(npolys) * words, level, npolys, s, m1);
+        return mod_down(g, out0, acc, level, 2 * npolys, s, m0, raw);
+    if (int rc = mod_down(g, out0, acc, level, npolys, s, m0, raw)) return rc;
+    return mod_down(g, out1, acc + size_t(npolys) * words, level, npolys, s, m1, raw);
 }
 
 }  // namespace tg

@@ -28,6 +28,18 @@
 #define KS_KEY_PREFETCH 0
 #endif
 
+#ifndef KS_L2_PREFETCH
+#define KS_L2_PREFETCH 0  // measured: 454 -> 487 us per batched level-21 key switch (slower)
+#endif
+// Bulk prefetch of a contiguous range into L2 (TMA unit, no registers, no
+// completion to wait for): the block's key chunks and digit rows of the NEXT
+// digit pair are requested while the current pair is transformed, so their
+// loads (the kernel's top stall: the key words' conversions waited on long
+// scoreboard, ncu source page) hit L2 instead of DRAM.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, u32 bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <int E>
 constexpr size_t ks_chunk_smem() {  // two exchange columns per warp + forward and inverse chunk twiddles
     return size_t(8) * (16 * WGeo<E>::CS + 4 * WGeo<E>::TW_CHUNK);
@@ -108,7 +120,22 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
 #pragma unroll
         for (int j = 0; j < E; ++j) a[0][j] = a[1][j] = 0.0;
         const u64* dig = digits + size_t(b) * nd * words + size_t(r) * N + off;
+        // the block's 8 chunks of a (digit, key half) are one contiguous 16 KB range
+        constexpr u32 kBlockBytes = 8u * Gm::M * 8u;
+        const size_t blk0 = size_t(blockIdx.x) * 8 * Gm::M;
+        auto prefetch_pair = [&](u32 bb, u32 d0) {  // digits d0, d0 + 1 of poly bb
+            if (!KS_L2_PREFETCH || threadIdx.x != 0) return;
+            for (u32 dd = d0; dd < min(nd, d0 + 2); ++dd) {
+                prefetch_l2_bulk(key + ((size_t(dd) * 2 + 0) * key_rows + m) * N + blk0, kBlockBytes);
+                prefetch_l2_bulk(key + ((size_t(dd) * 2 + 1) * key_rows + m) * N + blk0, kBlockBytes);
+                prefetch_l2_bulk(digits + size_t(bb) * nd * words + size_t(dd) * words + size_t(r) * N + blk0,
+                                 kBlockBytes);
+            }
+        };
+        if (b == b0) prefetch_pair(b, 0);
         for (u32 d = 0; d < nd; d += 2) {
+            if (d + 2 < nd) prefetch_pair(b, d + 2);
+            else if (b + 1 < b1) prefetch_pair(b + 1, 0);
             const bool pair = d + 1 < nd;
             double v[2][E];
             if (pair && own != d && own != d + 1) {  // two digits transformed together

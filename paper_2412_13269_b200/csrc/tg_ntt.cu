@@ -262,12 +262,22 @@ int ntt_forward_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 np
     return TG_OK;
 }
 
-int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s) {
+// The raw-output inverse column phase exists for the column-pair kernel (N = 2^16, every row FP64).
+bool ntt_inverse_cols_raw_ok(const tg_context* ctx) {
+    static const bool off = [] {
+        const char* e = getenv("TG_RAW_MODDOWN");
+        return e && *e == '0';
+    }();
+    return !off && ctx->ring.logN == 16 && ntt_pair_ok(ctx);
+}
+
+int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s, bool raw) {
     const DevRing& R = ctx->ring;
     const u32 rpp = u32(level + 1 + nspecial);
     ProfScope prof(ctx, TG_OP_NTT_INV, 8.0 * rpp * npolys * R.N, s);
     const bool pair = ntt_pair_ok(ctx);
-    if (R.logN == 16) launch_inv_cols_any<8, 8>(R, ctx->sms, data, rpp, npolys, level, s, 0, rpp, pair);
+    if (raw && !(R.logN == 16 && pair)) return fail(TG_E_ARG, "[ring] raw inverse column phase needs N = 2^16, all FP64");
+    if (R.logN == 16) launch_inv_cols_any<8, 8>(R, ctx->sms, data, rpp, npolys, level, s, 0, rpp, pair, raw);
     else if (R.logN == 15) launch_inv_cols_any<4, 8>(R, ctx->sms, data, rpp, npolys, level, s, 0, rpp, pair);
     else launch_inv_cols_any<4, 4>(R, ctx->sms, data, rpp, npolys, level, s, 0, rpp, pair);
     TG_LAUNCH_CHECK();

@@ -195,8 +195,10 @@ kw_fwd_cols2(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb,
     }
 }
 
-// Phase B inverse (all rows FP64): phase-A doubles in, N^-1 and canonical out.
-template <int E, int E2>
+// Phase B inverse (all rows FP64): phase-A doubles in, N^-1 and canonical out
+// (RAW: the raw doubles out, |v| <= 0.6q, for a consumer that folds N^-1 into
+// its own constants: the key switch's ModDown, k_mod_down_fp<K, true>).
+template <int E, int E2, bool RAW = false>
 __global__ void __launch_bounds__(256, NTT_MIN_BLOCKS)
 kw_inv_cols2(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 row0) {
     using Pg = PGeo<E>;
@@ -243,10 +245,14 @@ kw_inv_cols2(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32 
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < E; ++j) {
-            const u64 a = fp_canon_small(fp_mulmod(v[0][j], nd, ndq, qd), q);
-            const u64 b = fp_canon_small(fp_mulmod(v[1][j], nd, ndq, qd), q);
-            pr[pu(lane + 32 * j, warp)] = make_double2(__longlong_as_double(static_cast<long long>(a)),
-                                                   __longlong_as_double(static_cast<long long>(b)));
+            if constexpr (RAW) {
+                pr[pu(lane + 32 * j, warp)] = make_double2(v[0][j], v[1][j]);
+            } else {
+                const u64 a = fp_canon_small(fp_mulmod(v[0][j], nd, ndq, qd), q);
+                const u64 b = fp_canon_small(fp_mulmod(v[1][j], nd, ndq, qd), q);
+                pr[pu(lane + 32 * j, warp)] = make_double2(__longlong_as_double(static_cast<long long>(a)),
+                                                       __longlong_as_double(static_cast<long long>(b)));
+            }
         }
         __syncthreads();
         store_pair_tile<E, N2>(tile, data + size_t(p * rpp + r) * N + c0);

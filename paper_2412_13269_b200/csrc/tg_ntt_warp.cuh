@@ -1072,6 +1072,8 @@ void set_smem_attrs() {
         cudaFuncSetAttribute(kw_inv_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(chunk_smem<E2>()));
         cudaFuncSetAttribute(kw_fwd_cols2<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pair_smem<E1>()));
         cudaFuncSetAttribute(kw_inv_cols2<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pair_smem<E1>()));
+        cudaFuncSetAttribute(kw_inv_cols2<E1, E2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(pair_smem<E1>()));
         cudaFuncSetAttribute(kw_fwd_cols2_tma<E1, E2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(pair_tma_smem<E1>()));
         return true;
@@ -1111,13 +1113,14 @@ void launch_fwd_cols_any(const DevRing& R, int sms, u64* data, const u64* src, u
 }
 template <int E1, int E2>
 void launch_inv_cols_any(const DevRing& R, int sms, u64* data, u32 rpp, u32 npolys, int level, cudaStream_t s,
-                         u32 row0, u32 nrows, bool pair) {
+                         u32 row0, u32 nrows, bool pair, bool raw = false) {
     set_smem_attrs<E1, E2>();
     const u32 M2 = 32 * E2;
     if (pair && E1 == 8) {
         const u32 p1 = polys_per_block(M2 / 16, nrows, npolys, sms);
-        kw_inv_cols2<E1, E2><<<dim3(M2 / 16, nrows, (npolys + p1 - 1) / p1), 256, pair_smem<E1>(), s>>>(
-            R, data, rpp, npolys, p1, level, row0);
+        const dim3 grid(M2 / 16, nrows, (npolys + p1 - 1) / p1);
+        if (raw) kw_inv_cols2<E1, E2, true><<<grid, 256, pair_smem<E1>(), s>>>(R, data, rpp, npolys, p1, level, row0);
+        else kw_inv_cols2<E1, E2><<<grid, 256, pair_smem<E1>(), s>>>(R, data, rpp, npolys, p1, level, row0);
         return;
     }
     const u32 p1 = polys_per_block(M2 / 8, nrows, npolys, sms);
