@@ -646,6 +646,12 @@ def run_b200(args):
     records = spec.records
     value = records / (ms_step / 1e3)
 
+    # the same query on ONE stream, unprofiled: with the profiled replay's
+    # kernel sum below this gives the GPU idle per step of serial issue
+    barrier()
+    single_list, _ = timed(lambda: fresh_query(streams=1), args.steps)
+    single_ms = sum(single_list) / len(single_list)
+
     # profiled replay of the same steps: per-kernel-class CUDA-event times
     G.profile_enable(S.ring, True)
     barrier()
@@ -788,6 +794,12 @@ def run_b200(args):
         "e2e": {"value": round(records / (e2e_ms / 1e3), 1), "unit": "records/s", "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches // args.steps),
+        "gpu_time": {"kernel_sum_ms": round(total_prof_ms / args.steps, 3),
+                     "single_stream_ms": round(single_ms, 3), "concurrent_ms": round(ms_step, 3),
+                     "single_stream_idle_ms": round(single_ms - total_prof_ms / args.steps, 3),
+                     "note": "kernel_sum: per-op CUDA-event brackets on one stream (profiled replay); single_stream: "
+                             "the same query on one stream, unprofiled; concurrent: the timed step (--streams "
+                             "pipelines) - below kernel_sum where pipelines overlap"},
         "roofline": roofline,
         "server_encode": server_enc,
         "cpu_baseline": cpu,

@@ -391,6 +391,28 @@ PYBIND11_MODULE(_tetris_b200, m) {
              },
              py::return_value_policy::reference)
         .def("__exit__", [](PyStreamScope& s, py::args) { s.scope.reset(); });
+    // Device-side joins between the calling thread's stream and others:
+    // record() marks the current stream's position, wait() makes the current
+    // stream wait for it (no host synchronisation; run_concurrent's fork/join).
+    struct PyStreamEvent {
+        const RingParams* ring;
+        void* ev = nullptr;
+        ~PyStreamEvent() {
+            if (ev) tg_event_destroy(ring->dev(), ev);
+        }
+    };
+    py::class_<PyStreamEvent, std::unique_ptr<PyStreamEvent>>(m, "StreamEvent")
+        .def(py::init([](const RingParams& ring) {
+                 auto e = std::make_unique<PyStreamEvent>();
+                 e->ring = &ring;
+                 check_tg(tg_event_create(ring.dev(), &e->ev));
+                 return e;
+             }),
+             py::keep_alive<1, 2>())
+        .def("record", [](PyStreamEvent& e) { check_tg(tg_event_record(e.ring->dev(), e.ev, e.ring->stream())); },
+             "mark the calling thread's current stream")
+        .def("wait", [](PyStreamEvent& e) { check_tg(tg_stream_wait_event(e.ring->dev(), e.ring->stream(), e.ev)); },
+             "the calling thread's current stream waits (on the device) for the recorded mark");
     m.def(
         "stream_scope", [](const RingParams& ring, std::size_t i) { return PyStreamScope{&ring, i, nullptr}; },
         py::keep_alive<0, 1>());

@@ -192,9 +192,12 @@ def config3_query(S, chain, cts, ct_t, do_inner_sum=True):
 def run_concurrent(T, ring, fn, items, streams):
     """fn(item) for every item; with the B200 module and streams > 1 the items
     are spread round-robin over `streams` host threads, each issuing on its
-    own CUDA stream (stream_scope) and synchronising it before returning its
-    results. Results come back in item order, so every later reduction runs
-    in the reference's order."""
+    own CUDA stream (stream_scope). Fork and join are device-side events, not
+    host synchronisations: each worker stream first waits for the caller's
+    stream (the inputs it made), and the caller's stream waits for every
+    worker stream before anything later runs on it, so the host keeps issuing
+    while the GPU works. Results come back in item order, so every later
+    reduction runs in the reference's order."""
     items = list(items)
     if streams <= 1 or len(items) <= 1:
         return [fn(x) for x in items]
@@ -205,15 +208,19 @@ def run_concurrent(T, ring, fn, items, streams):
     k = min(streams, len(items))
     scoped = hasattr(T, "stream_scope")  # the CPU reference: plain threads (protocol.hpp:297-311)
     if scoped:
-        ring.synchronize()  # inputs made on the caller's stream are complete before other streams read them
+        fork = T.StreamEvent(ring)
+        fork.record()  # the caller's stream: inputs made so far
+        done = [T.StreamEvent(ring) for _ in range(k)]
 
     def worker(w):
         try:
             with (T.stream_scope(ring, w) if scoped else contextlib.nullcontext()):
+                if scoped:
+                    fork.wait()
                 for i in range(w, len(items), k):
                     out[i] = fn(items[i])
                 if scoped:
-                    ring.synchronize()
+                    done[w].record()
         except BaseException as e:  # surfaced on the caller's thread
             errs.append(e)
 
@@ -224,6 +231,9 @@ def run_concurrent(T, ring, fn, items, streams):
         t.join()
     if errs:
         raise errs[0]
+    if scoped:
+        for e in done:
+            e.wait()  # the caller's stream continues after every worker's work
     return out
 
 
