@@ -22,6 +22,7 @@
 #include "tetris/threshold.hpp"
 #include "tetris/bootstrap.hpp"
 #include "tetris/serialize.hpp"
+#include "tetris/protocol.hpp"
 
 namespace py = pybind11;
 using namespace tetris;
@@ -434,6 +435,65 @@ PYBIND11_MODULE(tetris_ref, m) {
         return ring_merge_many(ctx, ct_ptrs(cts), swk);
     });
     m.def("ring_split", &ring_split);
+    // ---- the exploration protocol (profile.hpp, protocol.hpp) ----
+    py::class_<Profile>(m, "Profile")
+        .def_static("toy_small", &Profile::toy_small)
+        .def_static("toy", &Profile::toy)
+        .def_readwrite("n_small", &Profile::n_small)
+        .def_readwrite("n_big", &Profile::n_big)
+        .def_readwrite("th_local", &Profile::th_local)
+        .def_readwrite("th_global", &Profile::th_global)
+        .def_readwrite("hw_big", &Profile::hw_big)
+        .def_readwrite("evalmod", &Profile::evalmod)
+        .def_readwrite("delta_tv", &Profile::delta_tv)
+        .def_readwrite("delta_evalmod", &Profile::delta_evalmod)
+        .def_readwrite("gadget_group", &Profile::gadget_group)
+        .def_readwrite("special_count", &Profile::special_count);
+    py::class_<ProtocolContext>(m, "ProtocolContext")
+        .def(py::init<Profile>(), py::call_guard<py::gil_scoped_release>())
+        .def("ring_small", &ProtocolContext::ring_small, py::return_value_policy::reference_internal)
+        .def("ring_big", &ProtocolContext::ring_big, py::return_value_policy::reference_internal)
+        .def("ctx_small", &ProtocolContext::ctx_small, py::return_value_policy::reference_internal)
+        .def("ctx_big", &ProtocolContext::ctx_big, py::return_value_policy::reference_internal)
+        .def("evaluator", &ProtocolContext::evaluator, py::return_value_policy::reference_internal)
+        .def("bts", &ProtocolContext::bts, py::return_value_policy::reference_internal)
+        .def("chain_local", &ProtocolContext::chain_local, py::return_value_policy::reference_internal)
+        .def("chain_global", &ProtocolContext::chain_global, py::return_value_policy::reference_internal)
+        .def("galois_manifest", &ProtocolContext::galois_manifest)
+        .def("profile", &ProtocolContext::profile, py::return_value_policy::reference_internal);
+    py::class_<Query>(m, "Query")
+        .def_readonly("t0", &Query::t0)
+        .def_readonly("t1", &Query::t1)
+        .def_readonly("norm", &Query::norm)
+        .def_readonly("small_sk_id", &Query::small_sk_id)
+        .def_readonly("big_sk_id", &Query::big_sk_id);
+    py::class_<EvalKeySet>(m, "EvalKeySet")
+        .def_readonly("merge", &EvalKeySet::merge)
+        .def_readonly("big", &EvalKeySet::big, py::return_value_policy::reference_internal)
+        .def_readonly("repack", &EvalKeySet::repack);
+    py::class_<ScientistSetup>(m, "ScientistSetup")
+        .def_readonly("sk_small", &ScientistSetup::sk_small)
+        .def_readonly("sk_big", &ScientistSetup::sk_big)
+        .def_readonly("keys", &ScientistSetup::keys, py::return_value_policy::reference_internal)
+        .def_readonly("query", &ScientistSetup::query, py::return_value_policy::reference_internal);
+    py::class_<Database>(m, "Database")
+        .def(py::init<>())
+        .def_readwrite("attribute_names", &Database::attribute_names)
+        .def_readwrite("rows", &Database::rows);
+    py::class_<SelectionMatrix>(m, "SelectionMatrix")
+        .def_static("identity", &SelectionMatrix::identity);
+    m.def("scientist_setup", &scientist_setup, py::call_guard<py::gil_scoped_release>());
+    m.def("score_and_repack", &score_and_repack, py::arg("pc"), py::arg("db"), py::arg("sel"), py::arg("query"),
+          py::arg("keys"), py::arg("threads") = 1, py::call_guard<py::gil_scoped_release>());
+    m.def("explore_from_repacked",
+          [](const ProtocolContext& pc, const std::vector<Ciphertext>& repacked, std::size_t p_total,
+             const Query& query, const EvalKeySet& keys, int threads) {
+              py::gil_scoped_release nogil;
+              return explore_from_repacked(pc, repacked, p_total, query, keys, threads);
+          },
+          py::arg("pc"), py::arg("repacked"), py::arg("p_total"), py::arg("query"), py::arg("keys"),
+          py::arg("threads") = 1);
+
     // Multi-threaded driver for the CPU baseline: evaluates the threshold on
     // each ciphertext with a std::thread pool (the reference's own granularity,
     // protocol.hpp:297-311), sums the outputs in index order and runs

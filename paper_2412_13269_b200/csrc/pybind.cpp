@@ -11,6 +11,7 @@
 #include "tetris_b200/tetris.hpp"
 #include "tetris_b200/serialize.hpp"
 #include "tetris_b200/pfe.hpp"
+#include "tetris_b200/protocol.hpp"
 
 namespace py = pybind11;
 using namespace tetris_b200;
@@ -537,6 +538,22 @@ PYBIND11_MODULE(_tetris_b200, m) {
     m.def("merge_embed", [ct_ptrs](const py::list& cts, const RingParams& big) { return merge_embed(ct_ptrs(cts), big); },
           py::keep_alive<0, 2>());
     m.def("ring_merge", &ring_merge, py::keep_alive<0, 1>());
+    // explore_from_repacked (protocol.hpp:241-328) with the ProtocolContext's
+    // members passed in: merge, Half-BTS, batched local thresholds, slot sum,
+    // global threshold
+    m.def(
+        "explore_from_repacked",
+        [](const KeyContext& ctx_big, const Evaluator& ev, const BootstrapEvaluator& bts,
+           const MinimaxChain& chain_local, const MinimaxChain& chain_global, const std::vector<Ciphertext>& repacked,
+           std::size_t p_total, const Ciphertext& t0, const Ciphertext& t1, const Ciphertext& norm, u64 small_sk_id,
+           const SwitchingKey& merge, const EvalKeys& big) {
+            py::gil_scoped_release nogil;
+            return explore_from_repacked(ctx_big, ev, bts, chain_local, chain_global, repacked, p_total, t0, t1, norm,
+                                         small_sk_id, ExploreKeys{&merge, &big});
+        },
+        py::keep_alive<0, 1>(), py::arg("ctx_big"), py::arg("ev"), py::arg("bts"), py::arg("chain_local"),
+        py::arg("chain_global"), py::arg("repacked"), py::arg("p_total"), py::arg("t0"), py::arg("t1"),
+        py::arg("norm"), py::arg("small_sk_id"), py::arg("merge"), py::arg("big"));
     m.def("ring_merge_many", [ct_ptrs](const KeyContext& ctx, const py::list& cts, const SwitchingKey& swk) {
         return ring_merge_many(ctx, ct_ptrs(cts), swk);
     }, py::keep_alive<0, 1>());
