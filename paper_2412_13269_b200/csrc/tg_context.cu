@@ -513,7 +513,102 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
             e[1] = double(pn) / double(q);
         }
     }
-    size_t words = src.size() + conv.size() + md.size() + mdf.size() + mdfn.size();
+    // int8 tensor-core base conversion operands (tg_baseconv_tc.cuh): B in
+    // the K-major core-matrix layout (byte (row n, col k) of a target block at
+    // (k / 16) * 128 + (n % 8) * 16 + k % 16), plus the epilogue constants
+    std::vector<uint8_t> tcb;
+    std::vector<u64> tcc;
+    size_t tc_mu_b_off = 0, tc_md_b_off = 0, tc_mu_c_off = 0, tc_md_c_off = 0;
+    {
+        const char* env = getenv("TG_TC_BASECONV");
+        const bool on = g->g.fp_moddown && !base2_bits && R.N % 128 == 0 && K <= u32(kMaxSpecial) &&
+                        !(env && *env == '0');
+        if (on) {
+            auto bits = [](double v) {
+                u64 b;
+                std::memcpy(&b, &v, 8);
+                return b;
+            };
+            const u32 kbm = (8 * gs + 31) / 32 * 32, kbd = (8 * K + 31) / 32 * 32, tall = K + nq + 1;
+            g->g.tc_mode = (env && *env == '2') ? 2 : 1;
+            g->g.tc_kb_mu = kbm;
+            g->g.tc_kb_md = kbd;
+            g->g.tc_tall = tall;
+            g->g.tc_mu_bstride = size_t(tall) * 8 * kbm;
+            g->g.tc_mu_cstride = size_t(tall) * 4 + size_t(gs) * 2;
+            const size_t ncombo = size_t(ng) * gs;
+            tc_mu_b_off = 0;
+            tc_md_b_off = ncombo * g->g.tc_mu_bstride;
+            tcb.assign(tc_md_b_off + size_t(nq + 1) * 8 * kbd, 0);
+            tc_mu_c_off = 0;
+            tc_md_c_off = ncombo * g->g.tc_mu_cstride;
+            tcc.assign(tc_md_c_off + size_t(nq + 1) * 8, 0);
+            // byte b of v at (target block, row b, column k)
+            auto set = [&](size_t blk_off, u32 b, u32 k, u64 v) {
+                tcb[blk_off + (k / 16) * 128 + b * 16 + k % 16] = uint8_t(v >> (8 * b));
+            };
+            auto tgt_consts = [&](u64* e, u64 q) {
+                const u64 r32 = (u64(1) << 32) % q;
+                e[0] = q;
+                e[1] = bits(1.0 / double(q));
+                e[2] = bits(double(r32));
+                e[3] = bits(double(r32) / double(q));
+            };
+            for (u32 j = 0; j < ng; ++j) {
+                const u32 first = j * gs, count = std::min(gs, nq - first);
+                for (u32 a = 1; a <= count; ++a) {
+                    const size_t combo = size_t(j) * gs + (a - 1);
+                    u64* cc = &tcc[tc_mu_c_off + combo * g->g.tc_mu_cstride];
+                    const u32 T = K + nq - a;  // targets at the top level: specials, then q rows outside the group
+                    for (u32 v = 0; v < T; ++v) {
+                        const u32 t = v < K ? nq + v : (v - K < first ? v - K : v - K + a);
+                        const u64 qt = mod[t];
+                        tgt_consts(cc + size_t(v) * 4, qt);
+                        const size_t blk = tc_mu_b_off + combo * g->g.tc_mu_bstride + size_t(v) * 8 * kbm;
+                        for (u32 i = 0; i < a; ++i) {
+                            const u64 w = conv[(((size_t(j) * gs + (a - 1)) * gs + i) * nmod + t) * 2];
+                            u64 wa = w % qt;  // w 2^(8 al) mod q_t
+                            for (u32 al = 0; al < 7; ++al) {
+                                for (u32 b = 0; b < 8; ++b) set(blk, b, 8 * i + al, wa);
+                                wa = h_mul_mod(wa, 256, qt);
+                            }
+                        }
+                    }
+                    for (u32 i = 0; i < a; ++i) {
+                        const u64 q = mod[first + i], sc = src[((size_t(j) * gs + (a - 1)) * gs + i) * 2];
+                        cc[size_t(tall) * 4 + 2 * i] = bits(double(sc));
+                        cc[size_t(tall) * 4 + 2 * i + 1] = bits(double(sc) / double(q));
+                    }
+                }
+            }
+            const u64 n = ctx->ring.N;
+            for (u32 r = 0; r < nq; ++r) {
+                const u64 q = mod[r], pinv = md[2 * K + size_t(K) * nq * 4 + size_t(r) * 2];
+                u64* e = &tcc[tc_md_c_off + size_t(r) * 8];
+                tgt_consts(e, q);
+                const u64 pn = h_mul_mod(pinv, h_inv_mod(n % q, q), q);
+                e[4] = bits(double(pinv));
+                e[5] = bits(double(pinv) / double(q));
+                e[6] = bits(double(pn));
+                e[7] = bits(double(pn) / double(q));
+                const size_t blk = tc_md_b_off + size_t(r) * 8 * kbd;
+                for (u32 s = 0; s < K; ++s) {
+                    const u64 ws = md[2 * K + (size_t(s) * nq + r) * 4];
+                    const u64 w = h_mul_mod(ws ? q - ws : 0, pinv, q);  // -(P/p_s) P^-1 mod q_r
+                    u64 wa = w;
+                    for (u32 al = 0; al < 7; ++al) {
+                        for (u32 b = 0; b < 8; ++b) set(blk, b, 8 * s + al, wa);
+                        wa = h_mul_mod(wa, 256, q);
+                    }
+                    const u64 pw = h_mul_mod(mod[nq + s] % q, w, q);  // sign column: -p_s w mod q_r
+                    const u64 neg = pw ? q - pw : 0;
+                    for (u32 b = 0; b < 8; ++b) set(blk, b, 8 * s + 7, neg);
+                }
+            }
+        }
+    }
+    const size_t tcb_words = tcb.empty() ? 0 : (tcb.size() + 15) / 16 * 2 + 1;  // + alignment slack
+    size_t words = src.size() + conv.size() + md.size() + mdf.size() + mdfn.size() + tcc.size() + tcb_words;
     cudaError_t e = cudaMalloc(&g->dev_block, words * 8);
     if (e != cudaSuccess) {
         delete g;
@@ -525,6 +620,24 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
     g->g.md = p + src.size() + conv.size();
     g->g.mdf = reinterpret_cast<double*>(g->g.md + md.size());
     g->g.mdfn = mdfn.empty() ? nullptr : g->g.mdf + mdf.size();
+    {
+        u64* tc_c = p + src.size() + conv.size() + md.size() + mdf.size() + mdfn.size();
+        const size_t off = size_t(tc_c + tcc.size() - p);
+        uint8_t* tc_b = reinterpret_cast<uint8_t*>(p + (off + 1) / 2 * 2);  // 16-byte aligned
+        g->g.tc_mu_c = tcc.empty() ? nullptr : tc_c + tc_mu_c_off;
+        g->g.tc_md_c = tcc.empty() ? nullptr : tc_c + tc_md_c_off;
+        g->g.tc_mu_b = tcb.empty() ? nullptr : tc_b + tc_mu_b_off;
+        g->g.tc_md_b = tcb.empty() ? nullptr : tc_b + tc_md_b_off;
+        if (!tcc.empty()) {
+            cudaError_t ec = cudaMemcpy(tc_c, tcc.data(), tcc.size() * 8, cudaMemcpyHostToDevice);
+            if (ec == cudaSuccess) ec = cudaMemcpy(tc_b, tcb.data(), tcb.size(), cudaMemcpyHostToDevice);
+            if (ec != cudaSuccess) {
+                cudaFree(g->dev_block);
+                delete g;
+                return cuda_fail(ec, "cudaMemcpy(gadget tc tables)");
+            }
+        }
+    }
     e = cudaMemcpy(g->g.src, src.data(), src.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g->g.conv, conv.data(), conv.size() * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !md.empty()) e = cudaMemcpy(g->g.md, md.data(), md.size() * 8, cudaMemcpyHostToDevice);

@@ -172,6 +172,17 @@ struct GadgetDev {
     bool lazy_modup, lazy_moddown;  // lazy sums provably fit a word (checked on the host)
     bool fp_moddown;                // every modulus below the FP64 bound: ModDown on the FP64 pipe
     u32 base2_bits;                 // 0: RNS digits; else balanced base-2^b sub-digits (group_size 1)
+    // Base conversions on the int8 tensor cores (tg_baseconv_tc.cuh; all-FP64
+    // rings, RNS digits, N a multiple of 128). tc_kb_mu == 0: off.
+    u32 tc_kb_mu, tc_kb_md;      // GEMM K bytes (8 per source, rounded up to 32)
+    u32 tc_mode;                 // TG_TC_BASECONV: 1 auto (where measured faster), 2 always
+    u32 tc_tall;                 // target blocks per ModUp combo (K + q_count + 1)
+    size_t tc_mu_bstride;        // bytes per ModUp (group, active count) B operand
+    size_t tc_mu_cstride;        // words per ModUp combo constant block
+    const uint8_t* tc_mu_b;      // [ngroups * group_size][tc_tall][8][tc_kb_mu] core-matrix layout
+    const u64* tc_mu_c;          // [combo]: [tc_tall][4] target (q, 1/q, 2^32 mod q, ./q), [group_size][2] source
+    const uint8_t* tc_md_b;      // [q_count + 1][8][tc_kb_md]
+    const u64* tc_md_c;          // [q_count + 1][8]: q, 1/q, 2^32 mod q, ./q, P^-1, ./q, P^-1 N^-1, ./q
 };
 
 }  // namespace tg

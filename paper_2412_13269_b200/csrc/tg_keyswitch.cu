@@ -10,6 +10,7 @@
 // One thread owns one coefficient of one digit (ModUp) / one output poly
 // (ModDown) and keeps the <=16 source residues in registers, so each source
 // word is read once and each output word written once.
+#include <algorithm>
 #include <type_traits>
 
 #include "tg_internal.cuh"
@@ -850,6 +851,8 @@ __global__ void k_mod_down_finish(DevRing R, GadgetDev G, u64* __restrict__ out,
     }
 }
 
+#include "tg_baseconv_tc.cuh"
+
 }  // namespace
 
 // ModUp of npolys coeff-form sources (level+1 rows each, back to back) into
@@ -875,8 +878,17 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
                 off += g->nsub[j];
             }
             d_eval = nullptr;
-        } else
-        if (G.lazy_modup && G.group_size <= 4)
+        } else if (G.tc_kb_mu && tc_modup_fits(R.K, level, G.group_size, nd) &&
+                   (G.tc_mode == 2 || (G.tc_kb_mu <= 64 && level >= 16 && u64(nd) * npolys * R.N >= (u64(148) << 11)))) {
+            // int8 tensor cores (tg_baseconv_tc.cuh); auto: where measured faster than k_modup_v
+            // (digit groups <= 8, high levels, large batches: config 4 level 21 batch 8 229 -> 185 us)
+            switch (G.tc_kb_mu) {
+                case 32: launch_modup_tc<32>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s); break;
+                case 64: launch_modup_tc<64>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s); break;
+                case 96: launch_modup_tc<96>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s); break;
+                default: launch_modup_tc<128>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s); break;
+            }
+        } else if (G.lazy_modup && G.group_size <= 4)
             launch_modup_v<4, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
         else if (G.lazy_modup && G.group_size <= 8)
             launch_modup_v<8, MODUP_CPT8>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
@@ -914,7 +926,21 @@ int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaS
     const int sms = g->ctx->sms;
     if (raw && !(G.fp_moddown && G.mdfn)) return fail(TG_E_ARG, "[rlwe] raw ModDown input needs the FP64 ModDown");
     bool done = false;
-    if (G.fp_moddown) {
+    // int8 tensor-core base conversion (tg_baseconv_tc.cuh); auto: batched, high
+    // levels (measured: config 5 ModDown 77.3 -> 56.5 ms per query; small or
+    // low-level launches stay on the FP64 kernel)
+    if (G.tc_kb_md && tc_mod_down_fits(level) && (G.tc_mode == 2 || (npolys >= 4 && level >= 16))) {
+        done = true;
+#define TG_MDTC(kb)                                                                                     \
+    case kb:                                                                                            \
+        done = raw ? launch_mod_down_tc<kb, true>(R, G, sms, out, in, level, npolys, addend, s)        \
+                   : launch_mod_down_tc<kb, false>(R, G, sms, out, in, level, npolys, addend, s);      \
+        break;
+        switch (G.tc_kb_md) { TG_MDTC(32) TG_MDTC(64) TG_MDTC(96) TG_MDTC(128) default: done = false; }
+#undef TG_MDTC
+    }
+    if (done) {
+    } else if (G.fp_moddown) {
         done = true;
         switch (R.K) {
 #define TG_MD_CASE(k)                                                                    \

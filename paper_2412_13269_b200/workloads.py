@@ -68,7 +68,8 @@ CONFIGS = {
             seed=0xC0F4),
     # configs[4]: scale-out stress, 2^20 records (32 record blocks), three
     # degree-63 stages (levels_required 22), L = 28, dnum = 3 (group 10:
-    # 10 x 50-bit digits under P = 9 x 60-bit specials). Count at level 3.
+    # 10 x 50-bit digits under P = 10 x 50-bit specials, so every modulus
+    # takes the FP64 path). Count at level 3.
     5: Spec("config5-stress", N=1 << 16, nq=29, q_bits=50, K=10, sp_bits=50, group=10, h=192,
             delta_log2=50, degrees=(63, 63, 63), alpha=13, epsilon=0.0, norm=1.0, n_cts=32, records=1 << 20,
             seed=0xC0F5),

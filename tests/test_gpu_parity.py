@@ -126,6 +126,30 @@ def test_keyswitch_pieces(G, R, pair64):
         assert_poly_equal(s1g, s1r, "switch_key_apply c1")
 
 
+@pytest.mark.parametrize("N,nq,K,gs", [(1024, 9, 4, 3), (1024, 22, 7, 7), (256, 20, 16, 16), (4096, 29, 10, 10),
+                                        (128, 12, 5, 4)])
+def test_keyswitch_pieces_tensor_core(G, R, gpu_available, monkeypatch, N, nq, K, gs):
+    """ModUp / ModDown / switch_key_apply on all-FP64 rings (50-bit q and
+    specials, N a multiple of 128): the int8 tensor-core base conversion
+    (tg_baseconv_tc.cuh, forced on for every launch: TG_TC_BASECONV=2 is read
+    when the gadget is built) vs the reference, at every digit shape (full and
+    partial groups, 1..16 sources, 4..16 specials)."""
+    monkeypatch.setenv("TG_TC_BASECONV", "2")
+    g, r = both(G, R, N=N, nq=nq, K=K, group_size=gs, seed=91, q_bits=50, sp_bits=50)
+    for lvl in sorted({nq - 1, nq // 2, 1, 0}, reverse=True):
+        dg = G.sample_uniform(g.ring, lvl, 0, G.Rng(500 + lvl))
+        dr = R.sample_uniform(r.ring, lvl, 0, R.Rng(500 + lvl))
+        for i, (x, y) in enumerate(zip(g.ctx.decompose(dg), r.ctx.decompose(dr))):
+            assert_poly_equal(x, y, f"modup N={N} lvl={lvl} digit {i}")
+        xg = G.sample_uniform(g.ring, lvl, K, G.Rng(600 + lvl))
+        xr = R.sample_uniform(r.ring, lvl, K, R.Rng(600 + lvl))
+        assert_poly_equal(g.ctx.mod_down_p(xg), r.ctx.mod_down_p(xr), f"moddown N={N} lvl={lvl}")
+        s0g, s1g = g.ctx.switch_key_apply(dg, g.keys.relin)
+        s0r, s1r = r.ctx.switch_key_apply(dr, r.keys.relin)
+        assert_poly_equal(s0g, s0r, f"switch_key_apply c0 N={N} lvl={lvl}")
+        assert_poly_equal(s1g, s1r, f"switch_key_apply c1 N={N} lvl={lvl}")
+
+
 def _pair_cts(g, r, n, delta=2.0 ** 45, seed=5, level=None):
     vals = [math.sin(0.37 * i) for i in range(n)]
     return (enc_slots(g, vals, delta, g.T.Rng(seed), level=level), enc_slots(r, vals, delta, r.T.Rng(seed), level=level),
