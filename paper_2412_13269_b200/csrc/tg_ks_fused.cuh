@@ -46,10 +46,23 @@ constexpr size_t ks_chunk_smem() {  // two exchange columns per warp + forward a
 }
 
 template <int E>
+__device__ __forceinline__ void ks_chunks_int_body(const DevRing& R, u64* acc, const u64* digits, u32 nd, u32 npolys,
+                                                   u32 ppb, const u64* key, int level, u32 logN1);
+
+// MIXED: rows r >= int_from (the integer special rows of a mixed ring) take
+// the 64-bit integer body; every other row the FP64 body below (a separate
+// instantiation, so the all-FP64 kernel's registers are unaffected).
+template <int E, bool MIXED = false>
 __global__ void __launch_bounds__(256, 2)
 kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb, const u64* key, int level,
-             u32 logN1, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod) {
+             u32 logN1, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, u32 int_from) {
     using Gm = WGeo<E>;
+    if constexpr (MIXED) {
+        if (blockIdx.y >= int_from) {
+            ks_chunks_int_body<E>(R, acc, digits, nd, npolys, ppb, key, level, logN1);
+            return;
+        }
+    }
     extern __shared__ u64 dyn[];
     u64* swf = dyn + 16 * Gm::CS;
     u64* swi = swf + 2 * Gm::TW_CHUNK;
@@ -212,5 +225,76 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
             o0[lane + 32 * j] = static_cast<u64>(__double_as_longlong(a[0][j]));
             o1[lane + 32 * j] = static_cast<u64>(__double_as_longlong(a[1][j]));
         }
+    }
+}
+
+// Integer rows of a mixed ring (the 60-bit special primes of config 1; every
+// q-chain row takes kw_ks_chunks): the same fusion on the 64-bit Shoup path
+// of the warp NTT -- the digits' forward chunk phase (wfwd_all, Harvey-lazy,
+// then canonical), the key inner product as exact 128-bit sums (< nd 2^120)
+// with one Barrett reduction (rlwe.hpp:514-536), the accumulators' inverse
+// chunk phase (winv_all) -- in the data formats of kw_fwd_chunks' input and
+// kw_inv_chunks' output, so the integer column phases on either side are
+// unchanged. Blocks of these rows run in the same launch as the FP64 rows
+// (kw_ks_chunks, int_from); special rows are never own-group rows and get no
+// P * c addend.
+template <int E>
+__device__ __forceinline__ void ks_chunks_int_body(const DevRing& R, u64* acc, const u64* digits, u32 nd, u32 npolys,
+                                                   u32 ppb, const u64* key, int level, u32 logN1) {
+    using Gm = WGeo<E>;
+    extern __shared__ u64 dyn[];
+    u64* swf = dyn + 16 * Gm::CS;
+    u64* swfs = swf + Gm::TW_CHUNK;
+    u64* swi = swfs + Gm::TW_CHUNK;
+    u64* swis = swi + Gm::TW_CHUNK;
+    const u32 N = R.N, rows = u32(level) + 1 + R.K;
+    const u32 r = blockIdx.y;
+    const u32 b0 = blockIdx.z * ppb, b1 = min(npolys, b0 + ppb);
+    if (b0 >= b1) return;
+    const u32 m = mod_index(r, level, R.q_count);
+    const u64 q = R.q[m], q2 = 2 * q, rlo = R.ratio[2 * m], rhi = R.ratio[2 * m + 1];
+    const u64* tw = R.tw + size_t(m) * 4 * N;
+    stage_chunk_twiddles<E, true>(swf, swfs, tw, tw + N, logN1, blockIdx.x);
+    stage_chunk_twiddles<E, false>(swi, swis, tw + 2 * size_t(N), tw + 3 * size_t(N), logN1, blockIdx.x);
+    __syncthreads();
+    const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
+    u64* col = dyn + warp * Gm::CS;
+    const size_t words = size_t(rows) * N, key_rows = R.nmod;
+    const u32 vo = lane << Gm::LOGE;  // layout 0: this lane's E contiguous eval slots
+    for (u32 b = b0; b < b1; ++b) {
+        U128 a0[E], a1[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) a0[j] = a1[j] = U128{0, 0};
+        const u64* dig = digits + size_t(b) * nd * words + size_t(r) * N + off;
+        u64 nx[E];
+        ld_strided<E>(nx, dig, lane);
+        for (u32 d = 0; d < nd; ++d) {
+            u64 v[E];
+#pragma unroll
+            for (int j = 0; j < E; ++j) v[j] = nx[j];
+            if (d + 1 < nd) ld_strided<E>(nx, dig + size_t(d + 1) * words, lane);  // in flight during the stages
+            wfwd_all<E, true, false>(v, col, lane, swf, swfs, q, warp);
+            const u64* kb = key + ((size_t(d) * 2 + 0) * key_rows + m) * N + off + vo;
+            const u64* ka = key + ((size_t(d) * 2 + 1) * key_rows + m) * N + off + vo;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                u64 t = v[j];
+                if (t >= q2) t -= q2;
+                if (t >= q) t -= q;
+                mac128(a0[j], t, kb[j]);
+                mac128(a1[j], t, ka[j]);
+            }
+        }
+        u64 x0[E], x1[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            x0[j] = barrett128(a0[j].lo, a0[j].hi, q, rlo, rhi);
+            x1[j] = barrett128(a1[j].lo, a1[j].hi, q, rlo, rhi);
+        }
+        winv_all<E, true, false>(x0, col, lane, swi, swis, q, warp);
+        winv_all<E, true, false>(x1, col, lane, swi, swis, q, warp);
+        st_strided<E>(acc + (size_t(b) * rows + r) * N + off, x0, lane);
+        st_strided<E>(acc + (size_t(npolys + b) * rows + r) * N + off, x1, lane);
     }
 }

@@ -203,7 +203,8 @@ k_inv_cols(DevRing R, u64* __restrict__ data, u32 row_base, u32 rows_per_poly, i
 
 template <int E1, int E2>
 void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key,
-                     int level, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s) {
+                     int level, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s,
+                     bool all_fp) {
     static const bool attr = [] {
         cudaFuncSetAttribute(kw_ks_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ks_chunk_smem<E2>()));
         return true;
@@ -220,8 +221,23 @@ void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32
     if (zf > 0) z = std::min<u32>(npolys, u32(zf));
     if (z < 1) z = 1;
     const u32 ppb = (npolys + z - 1) / z;
-    kw_ks_chunks<E2><<<dim3(M1 / 8, rows, (npolys + ppb - 1) / ppb), 256, ks_chunk_smem<E2>(), s>>>(
-        R, acc, digits, nd, npolys, ppb, key, level, WGeo<E1>::LOGM, own_gs, add0, add1, pmod);
+    // rows on the FP64 path: all of them, or (mixed ring, ks_fused_ok) the
+    // q-chain, with the integer special rows' blocks in the same launch
+    const dim3 grid(M1 / 8, rows, (npolys + ppb - 1) / ppb);
+    if (all_fp) {
+        kw_ks_chunks<E2><<<grid, 256, ks_chunk_smem<E2>(), s>>>(R, acc, digits, nd, npolys, ppb, key, level,
+                                                                 WGeo<E1>::LOGM, own_gs, add0, add1, pmod, rows);
+        return;
+    }
+    static const bool attr_m = [] {
+        cudaFuncSetAttribute(kw_ks_chunks<E2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(ks_chunk_smem<E2>()));
+        return true;
+    }();
+    (void)attr_m;
+    kw_ks_chunks<E2, true><<<grid, 256, ks_chunk_smem<E2>(), s>>>(R, acc, digits, nd, npolys, ppb, key, level,
+                                                                   WGeo<E1>::LOGM, own_gs, add0, add1, pmod,
+                                                                   u32(level) + 1);
 }
 
 // every modulus on the FP64 path and no integer-row knob: column-pair kernels
@@ -238,16 +254,28 @@ bool ntt_pair_ok(const tg_context* ctx) {
 
 }  // namespace
 
+// Every q-chain modulus on the FP64 path (kw_ks_chunks); special rows either
+// FP64 too or -- the mixed rings of config 1 -- on the 64-bit integer path
+// (kw_ks_chunks_int; TG_KS_FUSED_MIXED=0 keeps those rings on the unfused
+// pipeline). The integer-row knob must be off: each row's class is fixed.
 bool ks_fused_ok(const tg_context* ctx) {
     static const bool off = [] {
         const char* e = getenv("TG_KS_FUSED");
         return e && *e == '0';
     }();
+    static const bool mixed_off = [] {
+        const char* e = getenv("TG_KS_FUSED_MIXED");
+        return e && *e == '0';
+    }();
     int e1 = 0, e2 = 0;
-    if (off || !warp_plan(ctx->ring.logN, e1, e2)) return false;
-    for (u64 q : ctx->h_q)
-        if (q >= kFpMaxQ) return false;
-    return true;
+    if (off || !warp_plan(ctx->ring.logN, e1, e2) || ctx->ring.int_every != 0) return false;
+    bool specials_fp = true;
+    for (u32 i = 0; i < ctx->h_q.size(); ++i) {
+        if (ctx->h_q[i] < kFpMaxQ) continue;
+        if (i < ctx->ring.q_count) return false;
+        specials_fp = false;
+    }
+    return specials_fp || !mixed_off;
 }
 
 int ntt_forward_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s, u32 skip_gs) {
@@ -292,11 +320,14 @@ int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 np
     ProfScope prof(ctx, TG_OP_KS_FUSED,
                    8.0 * R.N * (rows * (npolys * (nd + 2.0) + 2.0 * nd) + (add0 ? 2.0 * npolys * (level + 1) : 0.0)),
                    s);
+    bool all_fp = true;
+    for (u64 q : ctx->h_q) all_fp &= q < kFpMaxQ;
     if (R.logN == 16)
-        launch_ks_fused<8, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s);
+        launch_ks_fused<8, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp);
     else if (R.logN == 15)
-        launch_ks_fused<4, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s);
-    else launch_ks_fused<4, 4>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s);
+        launch_ks_fused<4, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp);
+    else
+        launch_ks_fused<4, 4>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

@@ -31,9 +31,12 @@ def _cts(S, n, level, seed):
     return out
 
 
-@pytest.mark.parametrize("N,nq,K,gs", [(1 << 14, 9, 4, 3), (1 << 15, 8, 3, 3), (1 << 16, 7, 3, 3)])
-def test_fused_keyswitch_bit_exact(G, R, gpu_available, N, nq, K, gs):
-    kw = dict(N=N, nq=nq, K=K, group_size=gs, seed=11, q_bits=50, sp_bits=50, h=192, rotations=(1, 5))
+@pytest.mark.parametrize("N,nq,K,gs,sp_bits", [(1 << 14, 9, 4, 3, 50), (1 << 15, 8, 3, 3, 50), (1 << 16, 7, 3, 3, 50),
+                                                (1 << 14, 8, 2, 2, 60), (1 << 15, 7, 3, 3, 60), (1 << 16, 6, 2, 3, 60)])
+def test_fused_keyswitch_bit_exact(G, R, gpu_available, N, nq, K, gs, sp_bits):
+    """sp_bits 60: mixed rings (config 1's shape) -- FP64 q-chain rows in
+    kw_ks_chunks, the 60-bit special rows in kw_ks_chunks_int."""
+    kw = dict(N=N, nq=nq, K=K, group_size=gs, seed=11, q_bits=50, sp_bits=sp_bits, h=192, rotations=(1, 5))
     g, r = make_setup(G, **kw), make_setup(R, **kw)
     top = g.ring.max_level()
     for level in (top, 4, 2):  # full, partial (own row in the last digit) and small digit counts
@@ -47,9 +50,9 @@ def test_fused_keyswitch_bit_exact(G, R, gpu_available, N, nq, K, gs):
                             f"rotate {k} N={N} level={level}")
 
 
-@pytest.mark.parametrize("batch", [3, 8])
-def test_fused_keyswitch_batched(G, R, gpu_available, batch):
-    kw = dict(N=1 << 14, nq=8, K=3, group_size=3, seed=13, q_bits=50, sp_bits=50, h=192)
+@pytest.mark.parametrize("batch,sp_bits", [(3, 50), (8, 50), (8, 60)])
+def test_fused_keyswitch_batched(G, R, gpu_available, batch, sp_bits):
+    kw = dict(N=1 << 14, nq=8, K=3, group_size=3, seed=13, q_bits=50, sp_bits=sp_bits, h=192)
     g, r = make_setup(G, **kw), make_setup(R, **kw)
     level = g.ring.max_level()
     xs_g, ys_g = _cts(g, batch, level, 7), _cts(g, batch, level, 8)
