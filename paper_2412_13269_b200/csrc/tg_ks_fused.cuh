@@ -40,6 +40,40 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, u32 bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// L2 eviction-priority hints (createpolicy + ld.global.L2::cache_hint): the
+// key chunks are re-read for every poly of the batch, the digit rows exactly
+// once; without hints the ~120 MB key set (level 21, dnum 4) is evicted by the
+// streaming digits and accumulators (ncu: DRAM reads ~2x the algorithmic
+// bytes).
+#ifndef KS_L2_HINTS
+#define KS_L2_HINTS 1
+#endif
+__device__ __forceinline__ u64 l2_policy_last() {
+    u64 p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ u64 l2_policy_first() {
+    u64 p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ ulonglong2 ld_v2_hint(const ulonglong2* a, u64 pol) {
+    ulonglong2 r;
+    asm volatile("ld.global.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;\n" : "=l"(r.x), "=l"(r.y) : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ u64 ld_hint(const u64* a, u64 pol) {
+    u64 r;
+    asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;\n" : "=l"(r) : "l"(a), "l"(pol));
+    return r;
+}
+template <int E>
+__device__ __forceinline__ void ld_strided_hint(u64 (&v)[E], const u64* x, u32 lane, u64 pol) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = KS_L2_HINTS ? ld_hint(x + lane + 32 * j, pol) : x[lane + 32 * j];
+}
+
 template <int E>
 constexpr size_t ks_chunk_smem() {  // two exchange columns per warp + forward and inverse chunk twiddles
     return size_t(8) * (16 * WGeo<E>::CS + 4 * WGeo<E>::TW_CHUNK);
@@ -116,12 +150,14 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
         }
     };
 #endif
+    const u64 pol_key = l2_policy_last(), pol_dig = l2_policy_first();
     auto mac = [&](double (&a0)[E], double (&a1)[E], const double (&v)[E], u32 d) {
         const ulonglong2* kb = kptr(d, 0);
         const ulonglong2* ka = kptr(d, 1);
 #pragma unroll
         for (int j = 0; j < E / 2; ++j) {
-            const ulonglong2 tb = kb[j], ta = ka[j];
+            const ulonglong2 tb = KS_L2_HINTS ? ld_v2_hint(kb + j, pol_key) : kb[j];
+            const ulonglong2 ta = KS_L2_HINTS ? ld_v2_hint(ka + j, pol_key) : ka[j];
             a0[2 * j] = __dadd_rn(a0[2 * j], fp_mulmod_qi(v[2 * j], u2d(tb.x), qd, qi));
             a0[2 * j + 1] = __dadd_rn(a0[2 * j + 1], fp_mulmod_qi(v[2 * j + 1], u2d(tb.y), qd, qi));
             a1[2 * j] = __dadd_rn(a1[2 * j], fp_mulmod_qi(v[2 * j], u2d(ta.x), qd, qi));
@@ -155,7 +191,7 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
 #pragma unroll
                 for (int n = 0; n < 2; ++n) {
                     u64 t[E];
-                    ld_strided<E>(t, dig + size_t(d + n) * words, lane);
+                    ld_strided_hint<E>(t, dig + size_t(d + n) * words, lane, pol_dig);
 #pragma unroll
                     for (int j = 0; j < E; ++j) v[n][j] = __longlong_as_double(static_cast<long long>(t[j]));
                 }
@@ -181,7 +217,7 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
 #pragma unroll
                         for (int j = 0; j < E; ++j) vn[0][j] = u2d(t[j]);
                     } else {
-                        ld_strided<E>(t, dig + size_t(dd) * words, lane);
+                        ld_strided_hint<E>(t, dig + size_t(dd) * words, lane, pol_dig);
 #pragma unroll
                         for (int j = 0; j < E; ++j) vn[0][j] = __longlong_as_double(static_cast<long long>(t[j]));
                         wfwd_all_fp<1, E, true>(vn, col, CS2, lane, swf, qd, qi, warp);
