@@ -141,6 +141,21 @@ class _CAI:
 FP64_PEAK_OPS = 18.3e12  # DP ops/s, tools/diag/fp64_peak.cu on this pool's B200 (61-63 ops/clk/SM at 1965 MHz)
 
 
+def fp64_roofline_class(prof, name):
+    """FP64-pipe roofline of one kernel class whose algorithmic FP64 op count
+    the profiler records (tg_profile_read_ops: the fused key-switch core, 8 ops
+    per chunk-phase butterfly and 7 per key-inner-product term) against the
+    measured FP64 peak; None when not modelled."""
+    v = prof.get(name)
+    if not v or len(v) < 4 or v[3] <= 0 or v[0] <= 0:
+        return None
+    ach = v[3] / (v[0] / 1e3)
+    return {"kernel": name, "achieved": round(ach / 1e12, 3), "peak": FP64_PEAK_OPS / 1e12,
+            "unit": "TFLOP/s (FP64 DP ops, algorithmic: 8 per butterfly, 7 per key MAC term)",
+            "frac": round(ach / FP64_PEAK_OPS, 4), "ops_per_launch": v[3] / v[1],
+            "peak_kind": "measured (tools/diag/fp64_peak.cu: DADD/DMUL/DFMA throughput probe)"}
+
+
 def fp64_roofline(prof, N):
     """FP64-pipe roofline of the NTT classes: algorithmic ops (8 per
     butterfly) per second vs the measured FP64 peak."""
@@ -720,7 +735,7 @@ def run_b200(args):
     # roofline: dominant kernel class by device time
     peak, peak_kind = measured_peaks()
     dom = max(prof.items(), key=lambda kv: kv[1][0])
-    dname, (dms, dn, dbytes) = dom[0], dom[1]
+    dname, (dms, dn, dbytes) = dom[0], dom[1][:3]
     per_launch_ms = dms / dn
     achieved = (dbytes / dn) / (per_launch_ms / 1e3) / 1e9
     total_prof_ms = sum(v[0] for v in prof.values())
@@ -745,7 +760,7 @@ def run_b200(args):
                 # the NTT's actual bound is the FP64 pipe: algorithmic
                 # FP64 ops = 8 per butterfly (exact modmul 6 + add/sub 2), N/2 log N
                 # butterflies per row = bytes * log N / 4, against the measured pipe peak
-                "fp64": fp64_roofline(prof, spec.N) if dname.startswith("ntt") else None,
+                "fp64": fp64_roofline(prof, spec.N) if dname.startswith("ntt") else fp64_roofline_class(prof, dname),
                 "per_kernel": {k: {"ms": round(v[0] / args.steps, 4), "launches": v[1] // args.steps,
                                    "GBps": round((v[2] / v[1]) / ((v[0] / v[1]) / 1e3) / 1e9, 1)}
                                for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}}
@@ -1140,7 +1155,7 @@ def run_config1(args):
             return
 
     peak, peak_kind = measured_peaks()
-    dname, (dms, dn, dbytes) = max(prof.items(), key=lambda kv: kv[1][0])
+    dname, (dms, dn, dbytes) = (lambda kv: (kv[0], kv[1][:3]))(max(prof.items(), key=lambda kv: kv[1][0]))
     per_launch = dms / dn
     achieved = (dbytes / dn) / (per_launch / 1e3) / 1e9
     total = sum(v[0] for v in prof.values())

@@ -124,6 +124,10 @@ enum {
 };
 int tg_profile_enable(tg_context* ctx, int on);
 int tg_profile_read(tg_context* ctx, double* ms, uint64_t* launches, double* bytes);
+/* As tg_profile_read, plus the algorithmic FP64 operation count per class
+ * where the op models it (the fused key-switch core: 8 per NTT butterfly, 7
+ * per key-inner-product term; 0 elsewhere); any output may be NULL. */
+int tg_profile_read_ops(tg_context* ctx, double* ms, uint64_t* launches, double* bytes, double* fp64_ops);
 const char* tg_profile_op_name(int op);
 
 /* ---- ring layer --------------------------------------------------------- */
@@ -254,6 +258,12 @@ int tg_mul_plain(tg_context* ctx, uint64_t* out, const uint64_t* ct_part, const 
 #define TG_PLAIN_SUM_MAX_TERMS 256
 int tg_mul_plain_sum(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* cts,
                      const uint64_t* const* plains, int level, uint32_t nparts, void* stream);
+/* As tg_mul_plain_sum with term t's parts part_strides[t] words apart
+ * (>= (level+1) N; NULL: contiguous), so the part-major views of a ciphertext
+ * batch (stack_ciphertexts) are read in place. */
+int tg_mul_plain_sum_strided(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* cts,
+                             const uint64_t* part_strides, const uint64_t* const* plains, int level,
+                             uint32_t nparts, void* stream);
 
 /* ---- slot encoder ------------------------------------------------------- */
 /* Encoder::encode_slots (ckks.hpp:59-86) for `batch` slot vectors of n slots:

@@ -33,6 +33,7 @@ Ciphertext Evaluator::mul_plain_sum(const std::vector<Ciphertext>& cts, const st
     double noise = 0;
     std::vector<Poly> keep;
     std::vector<const u64*> cp, pp;
+    std::vector<u64> ps;  // words between each term's two parts
     for (std::size_t j = 0; j < ev.size(); ++j) {
         Ciphertext& c = ev[j];
         if (c.degree() != 1 || c.batch != 1) throw TetrisError("ckks", "mul_plain_sum expects single degree-1 ciphertexts");
@@ -41,13 +42,24 @@ Ciphertext Evaluator::mul_plain_sum(const std::vector<Ciphertext>& cts, const st
         c.to_eval();
         if (plains_eval[j].level() < lvl || plains_eval[j].nspecial() != 0)
             throw TetrisError("ckks", "plaintext has fewer rows than the ciphertext");
-        cp.push_back(detail::group_data(c.parts, 0, 2, keep));
+        // parts on a uniform stride (a ciphertext, or the part-major views of
+        // a batch from stack_ciphertexts) are read in place, others gathered
+        const Poly &q0 = c.parts[0], &q1 = c.parts[1];
+        const std::size_t S = q1.offset() > q0.offset() ? q1.offset() - q0.offset() : 0;
+        if (q0.storage() == q1.storage() && S >= std::size_t(lvl + 1) * R.degree() && q0.level() == lvl &&
+            q1.level() == lvl) {
+            cp.push_back(c.parts[0].data());
+            ps.push_back(u64(S));
+        } else {
+            cp.push_back(detail::group_data(c.parts, 0, 2, keep));
+            ps.push_back(u64(lvl + 1) * R.degree());
+        }
         pp.push_back(plains_eval[j].data());
         noise += c.noise_bound * plain_scale;
     }
     std::vector<Poly> out = fresh_parts(R, 2, lvl, Form::eval);
-    check_tg(tg_mul_plain_sum(R.dev(), const_cast<u64*>(out[0].data()), u32(ev.size()), cp.data(), pp.data(), lvl, 2,
-                              R.stream()));
+    check_tg(tg_mul_plain_sum_strided(R.dev(), const_cast<u64*>(out[0].data()), u32(ev.size()), cp.data(), ps.data(),
+                                      pp.data(), lvl, 2, R.stream()));
     Ciphertext r;
     r.parts = std::move(out);
     r.scale = ev[0].scale * plain_scale;

@@ -564,15 +564,15 @@ PYBIND11_MODULE(_tetris_b200, m) {
     // ---- kernel timing, end-to-end transfer helpers --------------------------
     m.def("profile_enable", [](const RingParams& r, bool on) { check_tg(tg_profile_enable(r.dev(), on ? 1 : 0)); });
     m.def("profile_read", [](const RingParams& r) {
-        std::vector<double> ms(TG_OP_COUNT), bytes(TG_OP_COUNT);
+        std::vector<double> ms(TG_OP_COUNT), bytes(TG_OP_COUNT), ops(TG_OP_COUNT);
         std::vector<uint64_t> n(TG_OP_COUNT);
         {
             py::gil_scoped_release nogil;
-            check_tg(tg_profile_read(r.dev(), ms.data(), n.data(), bytes.data()));
+            check_tg(tg_profile_read_ops(r.dev(), ms.data(), n.data(), bytes.data(), ops.data()));
         }
-        py::dict d;
+        py::dict d;  // class -> (ms, launches, algorithmic bytes, algorithmic FP64 ops or 0)
         for (int i = 0; i < TG_OP_COUNT; ++i)
-            if (n[i]) d[tg_profile_op_name(i)] = py::make_tuple(ms[i], n[i], bytes[i]);
+            if (n[i]) d[tg_profile_op_name(i)] = py::make_tuple(ms[i], n[i], bytes[i], ops[i]);
         return d;
     });
     m.def("pool_reserve", [](const RingParams& r, uint64_t bytes) {

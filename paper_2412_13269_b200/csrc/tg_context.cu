@@ -280,6 +280,11 @@ extern "C" int tg_profile_enable(tg_context* ctx, int on) {
 }
 
 extern "C" int tg_profile_read(tg_context* ctx, double* ms, uint64_t* launches, double* bytes) {
+    return tg_profile_read_ops(ctx, ms, launches, bytes, nullptr);
+}
+
+extern "C" int tg_profile_read_ops(tg_context* ctx, double* ms, uint64_t* launches, double* bytes,
+                                   double* fp64_ops) {
     if (!ctx) return fail(TG_E_ARG, "[gpu] null context");
     DeviceGuard guard(ctx->device);
     std::lock_guard<std::mutex> lock(ctx->prof_mu);
@@ -287,6 +292,7 @@ extern "C" int tg_profile_read(tg_context* ctx, double* ms, uint64_t* launches, 
         if (ms) ms[i] = 0;
         if (launches) launches[i] = 0;
         if (bytes) bytes[i] = 0;
+        if (fp64_ops) fp64_ops[i] = 0;
     }
     for (auto& r : ctx->prof_recs) {
         TG_CUDA(cudaEventSynchronize(r.stop));
@@ -295,6 +301,7 @@ extern "C" int tg_profile_read(tg_context* ctx, double* ms, uint64_t* launches, 
         if (ms) ms[r.op] += t;
         if (launches) launches[r.op] += u64(r.kernels);
         if (bytes) bytes[r.op] += r.bytes;
+        if (fp64_ops) fp64_ops[r.op] += r.fp64_ops;
         ctx->prof_free.push_back(r.start);
         ctx->prof_free.push_back(r.stop);
     }

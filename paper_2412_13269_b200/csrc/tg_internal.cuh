@@ -192,6 +192,7 @@ struct ProfRecord {
     int op;
     int kernels;  // kernel launches in the scope
     double bytes;
+    double fp64_ops;  // algorithmic FP64 operations (0: not modelled for this op)
     cudaEvent_t start, stop;
 };
 }  // namespace tg
@@ -218,11 +219,13 @@ struct ProfScope {
     tg_context* ctx;
     ProfRecord rec{};
     bool on;
-    ProfScope(tg_context* c, int op, double bytes, cudaStream_t s, int kernels = 1) : ctx(c), on(c && c->prof_on) {
+    ProfScope(tg_context* c, int op, double bytes, cudaStream_t s, int kernels = 1, double fp64_ops = 0)
+        : ctx(c), on(c && c->prof_on) {
         if (!on) return;
         rec.op = op;
         rec.kernels = kernels;
         rec.bytes = bytes;
+        rec.fp64_ops = fp64_ops;
         {
             std::lock_guard<std::mutex> g(ctx->prof_mu);
             rec.start = take_event();

@@ -316,10 +316,21 @@ int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 np
                     u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s) {
     const DevRing& R = ctx->ring;
     const double rows = double(level + 1 + R.K);
+    // algorithmic FP64 work: the chunk-phase butterflies of every transformed
+    // digit row (an own-group row is read as it is) and of both accumulators
+    // (8 ops each: exact modmul 6 + add/sub 2), the key inner product (7 per
+    // term: exact modmul + add), P * c on the Q rows when adding
+    int e1 = 0, e2 = 0;
+    warp_plan(R.logN, e1, e2);
+    const double l2 = double(WGeo<8>::LOGM) - (e2 == 8 ? 0.0 : 1.0);  // log2 of the chunk length
+    const double bfly = double(R.N) / 2 * l2 * 8, own_rows = own_gs ? double(level + 1) : 0.0;
+    const double fp64_ops =
+        npolys * ((rows * nd - own_rows) * bfly + rows * nd * 2.0 * R.N * 7 + rows * 2 * bfly +
+                  (add0 ? 2.0 * (level + 1) * R.N * 7 : 0.0));
     // algorithmic: digits (phase-1 form) read, key once per batch, P*c addends, accumulators written
     ProfScope prof(ctx, TG_OP_KS_FUSED,
                    8.0 * R.N * (rows * (npolys * (nd + 2.0) + 2.0 * nd) + (add0 ? 2.0 * npolys * (level + 1) : 0.0)),
-                   s);
+                   s, 1, fp64_ops);
     bool all_fp = true;
     for (u64 q : ctx->h_q) all_fp &= q < kFpMaxQ;
     if (R.logN == 16)

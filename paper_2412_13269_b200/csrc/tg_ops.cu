@@ -344,20 +344,21 @@ struct PlainSum {
     u32 nterms;
     const u64* ct[TG_PLAIN_SUM_MAX_TERMS];
     const u64* plain[TG_PLAIN_SUM_MAX_TERMS];
+    u64 pstride[TG_PLAIN_SUM_MAX_TERMS];  // words between a term's parts (level+1 rows: contiguous)
 };
 
 __global__ void k_mul_plain_sum(DevRing R, u64* __restrict__ out, const PlainSum P, int level, u32 nparts) {
     const u32 N = R.N, rows = u32(level) + 1;
     const u64 per = u64(rows) * N, total = per * nparts;
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
-        const u64 w = i % per;
+        const u64 w = i % per, part = i / per;
         const u32 m = u32(w >> R.logN);
         const u64 q = R.q[m], rl = R.ratio[2 * m], rh = R.ratio[2 * m + 1];
         if (q < kFpMaxQ) {  // exact FP64 products, reduced every 4 terms (|sum| < q/2 + 1 + 4 * 0.81q < 2^53)
             const double qd = R.qd[4 * m], qi = R.qd[4 * m + 1];
             double s = 0.0;
             for (u32 t = 0; t < P.nterms; ++t) {
-                s = __dadd_rn(s, fp_mulmod_qi(u2d(P.ct[t][i]), u2d(P.plain[t][w]), qd, qi));
+                s = __dadd_rn(s, fp_mulmod_qi(u2d(P.ct[t][part * P.pstride[t] + w]), u2d(P.plain[t][w]), qd, qi));
                 if ((t & 3) == 3) s = fp_reduce(s, qd, qi);
             }
             out[i] = fp_canonical(fp_reduce(s, qd, qi), qd);
@@ -366,7 +367,7 @@ __global__ void k_mul_plain_sum(DevRing R, u64* __restrict__ out, const PlainSum
         U128 acc{0, 0};
         u32 pending = 0;
         for (u32 t = 0; t < P.nterms; ++t) {
-            mac128(acc, P.ct[t][i], P.plain[t][w]);
+            mac128(acc, P.ct[t][part * P.pstride[t] + w], P.plain[t][w]);
             if (++pending == 15 && t + 1 < P.nterms) {
                 acc = U128{barrett128(acc.lo, acc.hi, q, rl, rh), 0};
                 pending = 0;
@@ -632,15 +633,24 @@ extern "C" int tg_poly_reduce(tg_context* ctx, uint64_t* data, int level, int ns
 
 extern "C" int tg_mul_plain_sum(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* cts,
                                 const uint64_t* const* plains, int level, uint32_t nparts, void* stream) {
+    return tg_mul_plain_sum_strided(ctx, out, nterms, cts, nullptr, plains, level, nparts, stream);
+}
+
+extern "C" int tg_mul_plain_sum_strided(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* cts,
+                                        const uint64_t* part_strides, const uint64_t* const* plains, int level,
+                                        uint32_t nparts, void* stream) {
     if (int rc = check_shape(ctx, level, 0)) return rc;
     if (nterms == 0 || nterms > TG_PLAIN_SUM_MAX_TERMS) return fail(TG_E_ARG, "[ckks] plain sum: 1..256 terms");
     if (nparts == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     PlainSum P{};
     P.nterms = nterms;
+    const u64 per = u64(level + 1) * ctx->ring.N;
     for (u32 t = 0; t < nterms; ++t) {
         P.ct[t] = cts[t];
         P.plain[t] = plains[t];
+        P.pstride[t] = part_strides ? part_strides[t] : per;
+        if (P.pstride[t] < per && nparts > 1) return fail(TG_E_ARG, "[ckks] plain sum: parts overlap");
     }
     const size_t words = size_t(level + 1) * ctx->ring.N * nparts;
     PROF(TG_OP_MUL_PLAIN, 8.0 * words * (nterms + 1) + 8.0 * words / nparts * nterms);

@@ -13,6 +13,8 @@ import math
 from dataclasses import dataclass, field
 from types import SimpleNamespace
 
+import os
+
 import numpy as np
 
 
@@ -278,6 +280,21 @@ def encrypt_many(S, vectors, level, labels):
             for m, lab in zip(ms, labels)]
 
 
+def weights_eval(S, ct_w):
+    """B200 module: the query's 8 weight ciphertexts -- shared by every record
+    block's linear score -- forward-transformed ONCE per query as one stacked
+    batch (one batched NTT; mul_plain_sum reads the batch's part-major views
+    in place). Otherwise (or with a single weight) unchanged: per-ciphertext
+    to_eval inside mul_plain_sum, memoised on the first block."""
+    T = S.T
+    ct_w = list(ct_w)
+    if not hasattr(T, "stack_ciphertexts") or len(ct_w) < 2 or os.environ.get("TG_WEIGHTS_EVAL") == "0":
+        return ct_w
+    st = T.stack_ciphertexts(ct_w)
+    st.to_eval()
+    return T.unstack_ciphertext(st)
+
+
 def linear_score(S, ct_w, pts, plain_scale):
     """score = rescale(sum_j mul_plain(ct_w_j, pt_j)), summed in j order
     (config 2's pt x ct MAC)."""
@@ -304,7 +321,8 @@ def config2_inputs(S, attrs=None, w=None):
 
 
 def config2_query(S, inp, streams=1):
-    return run_concurrent(S.T, S.ring, lambda pts: linear_score(S, inp.ct_w, pts, inp.plain_scale),
+    ct_w = weights_eval(S, inp.ct_w)
+    return run_concurrent(S.T, S.ring, lambda pts: linear_score(S, ct_w, pts, inp.plain_scale),
                           inp.blocks, streams)
 
 
@@ -430,10 +448,11 @@ def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8, 
     keep (optional list): receives every block's output before the sum."""
     T, ev, keys = S.T, S.ev, S.keys
     wait = ready or (lambda name: None)
+    wait("w")
+    ct_w = weights_eval(S, q.ct_w)
 
     def score(blk):
-        wait("w")
-        return linear_score(S, q.ct_w, blk.pt_attr, blk.attr_scale)
+        return linear_score(S, ct_w, blk.pt_attr, blk.attr_scale)
 
     risks = run_concurrent(T, S.ring, score, blocks, streams)
     batches = statement_jobs(len(blocks), max_blocks)
