@@ -248,6 +248,7 @@ int tg_lincomb_batch(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint
 int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const uint64_t* x0,
               const uint64_t* x1, const uint64_t* y0, const uint64_t* y1, int level,
               uint32_t npolys, void* stream);
+/* (p0 and p1 both NULL: only p2 = x1 y1 is formed; x0, y0 unused.) */
 /* Evaluator::mul_plain residue step (ckks.hpp:257-265): every part row r
  * (modulus index m) times plain row m; plain holds >= level+1 rows. */
 int tg_mul_plain(tg_context* ctx, uint64_t* out, const uint64_t* ct_part, const uint64_t* plain,
@@ -348,6 +349,17 @@ int tg_relinearize_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uin
 int tg_keyswitch_add_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* d,
                            const uint64_t* d_eval, const uint64_t* key, uint32_t key_digits, int level,
                            const uint64_t* add0, const uint64_t* add1, uint32_t npolys, void* stream);
+/* mul + relinearize (ckks.hpp:229-237, rlwe.hpp:601-620) of npolys degree-1
+ * products x * y with the tensor's c0 = x0 y0 and c1 = x0 y1 + x1 y0 formed
+ * inside the fused key-switch core from the EVAL-form operand parts (x0, x1,
+ * y0, y1: npolys polys of level+1 rows each) instead of through HBM; c2 (its
+ * coefficient form and, optional, eval form) as for tg_relinearize_batch.
+ * Identical residues to tg_tensor + tg_relinearize_batch. Rings without the
+ * fused core take exactly that pair. */
+int tg_relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* c2,
+                                const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits, int level,
+                                const uint64_t* x0, const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
+                                uint32_t npolys, void* stream);
 
 #ifdef __cplusplus
 }

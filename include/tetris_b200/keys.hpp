@@ -150,6 +150,11 @@ public:
     // accumulators' special rows are inverse transformed. to_coeff() of the
     // result equals relinearize(ct, rlk) residue for residue.
     Ciphertext relinearize_eval(const Ciphertext& ct, const SwitchingKey& rlk) const;
+    // relinearize(mul(x, y)) for EVAL-form, level-aligned degree-1 operands
+    // (B200 extension, Evaluator::mul_relin): only c2 of the tensor goes
+    // through HBM; c0 / c1 are formed inside the fused key-switch core
+    // (tg_relinearize_tensor_batch). Residue for residue the same.
+    Ciphertext relinearize_tensor(const Ciphertext& x, const Ciphertext& y, const SwitchingKey& rlk) const;
     SwitchingKey galois_key_gen(const SecretKey& sk, u64 exponent, Rng& rng) const;
     Ciphertext apply_galois(const Ciphertext& ct, u64 exponent, const SwitchingKey& swk) const;
     // Hoisted automorphisms (Evaluator::apply_galois_many, ckks.hpp:338-367):

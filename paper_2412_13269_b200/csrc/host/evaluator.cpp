@@ -6,6 +6,8 @@
 #include <cmath>
 #include <thread>
 
+#include <cstdlib>
+
 #include "internal.hpp"
 #include "tetris_b200/evaluator.hpp"
 
@@ -306,8 +308,24 @@ Ciphertext Evaluator::mul(const Ciphertext& a, const Ciphertext& b) const {
     return out;
 }
 
+// mul then relinearize (ckks.hpp:301-303); with the tensor's c0 / c1 formed
+// inside the key-switch core (KeyContext::relinearize_tensor) -- the same
+// checks in the same order as mul + relinearize, the same residues.
 Ciphertext Evaluator::mul_relin(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys) const {
-    return ctx_->relinearize(mul(a, b), keys.relin);
+    static const bool off = [] {
+        const char* e = std::getenv("TG_RELIN_TENSOR");
+        return e && *e == '0';
+    }();
+    if (off) return ctx_->relinearize(mul(a, b), keys.relin);
+    if (a.domain != b.domain) throw TetrisError("ckks", "domain tag mismatch in mul");
+    if (a.degree() != 1 || b.degree() != 1) throw TetrisError("ckks", "mul expects degree-1 operands");
+    if (a.batch != b.batch) throw TetrisError("ckks", "batch size mismatch in mul");
+    Ciphertext x = a, y = b;
+    align_levels(x, y);
+    if (x.level() == 0) throw TetrisError("ckks", "exhausted ciphertext: no level left to rescale");
+    x.to_eval();
+    y.to_eval();
+    return ctx_->relinearize_tensor(x, y, keys.relin);
 }
 
 Ciphertext Evaluator::mul_relin_eval(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys) const {

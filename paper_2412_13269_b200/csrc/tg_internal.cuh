@@ -281,7 +281,8 @@ int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 np
                      bool raw = false);
 bool ntt_inverse_cols_raw_ok(const tg_context* ctx);
 int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key, int level,
-                    u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s);
+                    u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s,
+                    const u64* ty0 = nullptr, const u64* ty1 = nullptr);
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {

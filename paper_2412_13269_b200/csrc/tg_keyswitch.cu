@@ -1031,7 +1031,7 @@ int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd
 // of level+1+K rows (digits, then both accumulators).
 int ks_fused_batch(tg_gadget* g, u64* out0, u64* out1, const u64* d, const u64* d_eval, u32 nd, u32 npolys,
                    const u64* key, int level, u64* scratch, cudaStream_t s, const u64* add0, const u64* add1,
-                   bool eval_add) {
+                   bool eval_add, const u64* ty0 = nullptr, const u64* ty1 = nullptr) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const size_t words = size_t(level + 1 + R.K) * R.N;
@@ -1041,7 +1041,8 @@ int ks_fused_batch(tg_gadget* g, u64* out0, u64* out1, const u64* d, const u64* 
     const u64* pmod = g->g.md + 2 * R.K + size_t(R.K) * R.q_count * 4 + size_t(R.q_count) * 2;
     const u32 own = (d_eval && !g->g.base2_bits) ? g->g.group_size : 0u;
     if (int rc = ks_fused_chunks(ctx, acc, digits, nd, npolys, key, level, own, eval_add ? add0 : nullptr,
-                                 eval_add ? add1 : nullptr, pmod, s))
+                                 eval_add ? add1 : nullptr, pmod, s, eval_add ? ty0 : nullptr,
+                                 eval_add ? ty1 : nullptr))
         return rc;
     // the accumulators' inverse column phase hands ModDown raw doubles
     // (its N^-1 folded into ModDown's constants) when both kernels allow it
@@ -1184,6 +1185,40 @@ extern "C" int tg_relinearize_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1
             rc = ks_inner_batch(g, out0, out1, digits, nd, npolys, key, level, digits + size_t(npolys) * nd * words,
                                 s, c0_eval, c1_eval, true);
     }
+    cudaFreeAsync(scratch, s);
+    return rc;
+}
+
+extern "C" int tg_relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* c2,
+                                           const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits,
+                                           int level, const uint64_t* x0, const uint64_t* x1, const uint64_t* y0,
+                                           const uint64_t* y1, uint32_t npolys, void* stream) {
+    if (int rc = check_ks(g, level)) return rc;
+    if (npolys == 0) return TG_OK;
+    if (!x0 || !x1 || !y0 || !y1) return fail(TG_E_ARG, "[rlwe] relinearize needs both operands' eval parts");
+    tg_context* ctx = g->ctx;
+    const u32 nd = tg_gadget_digit_count(g, level);
+    if (nd > key_digits) return fail(TG_E_ARG, "[rlwe] switching key has too few digits");
+    if (nd > 15) return fail(TG_E_ARG, "[rlwe] batched key switch supports at most 15 digits");
+    DeviceGuard guard(ctx->device);
+    cudaStream_t s = as_stream(stream);
+    if (!ks_fused_ok(ctx)) {  // the tensor's c0 / c1 through HBM, then the plain batched relinearisation
+        const size_t qw = size_t(level + 1) * ctx->ring.N * npolys;
+        void* cc = nullptr;
+        TG_CUDA(cudaMallocFromPoolAsync(&cc, 3 * qw * 8, ctx->pool, s));
+        u64* c0 = static_cast<u64*>(cc);  // (c2 recomputed into the third slot, unused)
+        int rc = tg_tensor(ctx, c0, c0 + qw, c0 + 2 * qw, x0, x1, y0, y1, level, npolys, stream);
+        if (rc == TG_OK)
+            rc = tg_relinearize_batch(g, out0, out1, c2, c2_eval, key, key_digits, level, c0, c0 + qw, npolys,
+                                      stream);
+        cudaFreeAsync(cc, s);
+        return rc;
+    }
+    const size_t words = size_t(level + 1 + ctx->ring.K) * ctx->ring.N;
+    void* scratch = nullptr;
+    TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
+    const int rc = ks_fused_batch(g, out0, out1, c2, c2_eval, nd, npolys, key, level, static_cast<u64*>(scratch), s,
+                                  x0, x1, true, y0, y1);
     cudaFreeAsync(scratch, s);
     return rc;
 }

@@ -86,10 +86,15 @@ __device__ __forceinline__ void ks_chunks_int_body(const DevRing& R, u64* acc, c
 // MIXED: rows r >= int_from (the integer special rows of a mixed ring) take
 // the 64-bit integer body; every other row the FP64 body below (a separate
 // instantiation, so the all-FP64 kernel's registers are unaffected).
+// ty0/ty1 (tensor mode, tg_relinearize_tensor_batch): add0/add1 are the
+// operand x's eval parts and ty0/ty1 y's; c0 = x0 y0, c1 = x0 y1 + x1 y0 are
+// formed here (exact FP64 products, |c0| < 0.81q, |c1| < 1.62q) and folded
+// as P * c like the eval-form addends.
 template <int E, bool MIXED = false>
 __global__ void __launch_bounds__(256, 2)
 kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb, const u64* key, int level,
-             u32 logN1, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, u32 int_from) {
+             u32 logN1, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, u32 int_from,
+             const u64* ty0, const u64* ty1) {
     using Gm = WGeo<E>;
     if constexpr (MIXED) {
         if (blockIdx.y >= int_from) {
@@ -168,6 +173,40 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
         double a[2][E];
 #pragma unroll
         for (int j = 0; j < E; ++j) a[0][j] = a[1][j] = 0.0;
+        // P * c first (the accumulators start from it): its loads are in
+        // flight with the first digits' instead of exposed after the last
+        if (addq) {  // + P * c on the Q rows (|.| <= q/2 + 2^-15 q; the digit sums reduce every 4 as before)
+            const size_t qw = size_t(level + 1) * N, po = size_t(b) * qw + size_t(r) * N + off + vo;
+            const ulonglong2* c0 = reinterpret_cast<const ulonglong2*>(add0 + po);
+            const ulonglong2* c1 = reinterpret_cast<const ulonglong2*>(add1 + po);
+            if (ty0) {  // tensor mode: c0 = x0 y0, c1 = x0 y1 + x1 y0 from the operands
+                const ulonglong2* d0 = reinterpret_cast<const ulonglong2*>(ty0 + po);
+                const ulonglong2* d1 = reinterpret_cast<const ulonglong2*>(ty1 + po);
+#pragma unroll
+                for (int j = 0; j < E / 2; ++j) {
+                    const ulonglong2 x0 = c0[j], x1 = c1[j], y0 = d0[j], y1 = d1[j];
+                    const double xa[2] = {u2d(x0.x), u2d(x0.y)}, xb[2] = {u2d(x1.x), u2d(x1.y)};
+                    const double ya[2] = {u2d(y0.x), u2d(y0.y)}, yb[2] = {u2d(y1.x), u2d(y1.y)};
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const double t0 = fp_mulmod_qi(xa[h], ya[h], qd, qi);
+                        const double t1 =
+                            __dadd_rn(fp_mulmod_qi(xa[h], yb[h], qd, qi), fp_mulmod_qi(xb[h], ya[h], qd, qi));
+                        a[0][2 * j + h] = __dadd_rn(a[0][2 * j + h], fp_mulmod(t0, pmd, pmq, qd));
+                        a[1][2 * j + h] = __dadd_rn(a[1][2 * j + h], fp_mulmod(t1, pmd, pmq, qd));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < E / 2; ++j) {
+                    const ulonglong2 x0 = c0[j], x1 = c1[j];
+                    a[0][2 * j] = __dadd_rn(a[0][2 * j], fp_mulmod(u2d(x0.x), pmd, pmq, qd));
+                    a[0][2 * j + 1] = __dadd_rn(a[0][2 * j + 1], fp_mulmod(u2d(x0.y), pmd, pmq, qd));
+                    a[1][2 * j] = __dadd_rn(a[1][2 * j], fp_mulmod(u2d(x1.x), pmd, pmq, qd));
+                    a[1][2 * j + 1] = __dadd_rn(a[1][2 * j + 1], fp_mulmod(u2d(x1.y), pmd, pmq, qd));
+                }
+            }
+        }
         const u64* dig = digits + size_t(b) * nd * words + size_t(r) * N + off;
         // the block's 8 chunks of a (digit, key half) are one contiguous 16 KB range
         constexpr u32 kBlockBytes = 8u * Gm::M * 8u;
@@ -231,19 +270,6 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
                     a[0][j] = fp_reduce(a[0][j], qd, qi);
                     a[1][j] = fp_reduce(a[1][j], qd, qi);
                 }
-            }
-        }
-        if (addq) {  // + P * c on the Q rows
-            const size_t qw = size_t(level + 1) * N;
-            const ulonglong2* c0 = reinterpret_cast<const ulonglong2*>(add0 + size_t(b) * qw + size_t(r) * N + off + vo);
-            const ulonglong2* c1 = reinterpret_cast<const ulonglong2*>(add1 + size_t(b) * qw + size_t(r) * N + off + vo);
-#pragma unroll
-            for (int j = 0; j < E / 2; ++j) {
-                const ulonglong2 x0 = c0[j], x1 = c1[j];
-                a[0][2 * j] = __dadd_rn(a[0][2 * j], fp_mulmod(u2d(x0.x), pmd, pmq, qd));
-                a[0][2 * j + 1] = __dadd_rn(a[0][2 * j + 1], fp_mulmod(u2d(x0.y), pmd, pmq, qd));
-                a[1][2 * j] = __dadd_rn(a[1][2 * j], fp_mulmod(u2d(x1.x), pmd, pmq, qd));
-                a[1][2 * j + 1] = __dadd_rn(a[1][2 * j + 1], fp_mulmod(u2d(x1.y), pmd, pmq, qd));
             }
         }
 #pragma unroll

@@ -204,7 +204,7 @@ k_inv_cols(DevRing R, u64* __restrict__ data, u32 row_base, u32 rows_per_poly, i
 template <int E1, int E2>
 void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key,
                      int level, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s,
-                     bool all_fp) {
+                     bool all_fp, const u64* ty0, const u64* ty1) {
     static const bool attr = [] {
         cudaFuncSetAttribute(kw_ks_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ks_chunk_smem<E2>()));
         return true;
@@ -226,7 +226,8 @@ void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32
     const dim3 grid(M1 / 8, rows, (npolys + ppb - 1) / ppb);
     if (all_fp) {
         kw_ks_chunks<E2><<<grid, 256, ks_chunk_smem<E2>(), s>>>(R, acc, digits, nd, npolys, ppb, key, level,
-                                                                 WGeo<E1>::LOGM, own_gs, add0, add1, pmod, rows);
+                                                                 WGeo<E1>::LOGM, own_gs, add0, add1, pmod, rows,
+                                                                 ty0, ty1);
         return;
     }
     static const bool attr_m = [] {
@@ -237,7 +238,7 @@ void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32
     (void)attr_m;
     kw_ks_chunks<E2, true><<<grid, 256, ks_chunk_smem<E2>(), s>>>(R, acc, digits, nd, npolys, ppb, key, level,
                                                                    WGeo<E1>::LOGM, own_gs, add0, add1, pmod,
-                                                                   u32(level) + 1);
+                                                                   u32(level) + 1, ty0, ty1);
 }
 
 // every modulus on the FP64 path and no integer-row knob: column-pair kernels
@@ -313,7 +314,8 @@ int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 np
 }
 
 int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key, int level,
-                    u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s) {
+                    u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s, const u64* ty0,
+                    const u64* ty1) {
     const DevRing& R = ctx->ring;
     const double rows = double(level + 1 + R.K);
     // algorithmic FP64 work: the chunk-phase butterflies of every transformed
@@ -326,19 +328,20 @@ int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 np
     const double bfly = double(R.N) / 2 * l2 * 8, own_rows = own_gs ? double(level + 1) : 0.0;
     const double fp64_ops =
         npolys * ((rows * nd - own_rows) * bfly + rows * nd * 2.0 * R.N * 7 + rows * 2 * bfly +
-                  (add0 ? 2.0 * (level + 1) * R.N * 7 : 0.0));
+                  (add0 ? 2.0 * (level + 1) * R.N * 7 : 0.0) + (ty0 ? 3.0 * (level + 1) * R.N * 6.5 : 0.0));
     // algorithmic: digits (phase-1 form) read, key once per batch, P*c addends, accumulators written
     ProfScope prof(ctx, TG_OP_KS_FUSED,
-                   8.0 * R.N * (rows * (npolys * (nd + 2.0) + 2.0 * nd) + (add0 ? 2.0 * npolys * (level + 1) : 0.0)),
+                   8.0 * R.N * (rows * (npolys * (nd + 2.0) + 2.0 * nd) +
+                                (add0 ? (ty0 ? 4.0 : 2.0) * npolys * (level + 1) : 0.0)),
                    s, 1, fp64_ops);
     bool all_fp = true;
     for (u64 q : ctx->h_q) all_fp &= q < kFpMaxQ;
     if (R.logN == 16)
-        launch_ks_fused<8, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp);
+        launch_ks_fused<8, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp, ty0, ty1);
     else if (R.logN == 15)
-        launch_ks_fused<4, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp);
+        launch_ks_fused<4, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp, ty0, ty1);
     else
-        launch_ks_fused<4, 4>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp);
+        launch_ks_fused<4, 4>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp, ty0, ty1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

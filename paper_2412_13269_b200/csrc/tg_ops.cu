@@ -335,6 +335,21 @@ __global__ void k_tensor(DevRing R, Shape S, u64* p0, u64* p1, u64* p2, const u6
     }
 }
 
+// c2 = x1 y1 only (relinearisation through the fused key switch forms c0 and
+// c1 from the operands inside the key-switch core: tg_relinearize_tensor_batch)
+__global__ void k_tensor_c2(DevRing R, Shape S, u64* p2, const u64* x1, const u64* y1) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u32 m = row_mod(R, S, i);
+        const u64 q = R.q[m];
+        if (q < kFpMaxQ) {
+            const double qd = R.qd[4 * m], qi = R.qd[4 * m + 1];
+            p2[i] = fp_canonical1(fp_mulmod_qi(u2d(x1[i]), u2d(y1[i]), qd, qi), qd);
+            continue;
+        }
+        p2[i] = mul_mod(x1[i], y1[i], q, R.ratio[2 * m], R.ratio[2 * m + 1]);
+    }
+}
+
 // LinearTransformPlan::apply giant bucket (ckks.hpp:455-476):
 // out[p][r][i] = sum_t ct_t[p][r][i] * plain_t[r][i] mod q_r, 128-bit lazy
 // accumulation (reduced every 15 terms: products < 2^124), one Barrett per
@@ -601,6 +616,12 @@ extern "C" int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* 
     if (npolys == 0) return TG_OK;
     DeviceGuard guard(ctx->device);
     Shape S = shape_of(ctx, level, 0, npolys);
+    if (!p0 && !p1) {  // c2 only
+        PROF(TG_OP_TENSOR, 24 * S.words);
+        k_tensor_c2<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, p2, x1, y1);
+        TG_LAUNCH_CHECK();
+        return TG_OK;
+    }
     PROF(TG_OP_TENSOR, 56 * S.words);
     k_tensor<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, p0, p1, p2, x0, x1, y0, y1);
     TG_LAUNCH_CHECK();
