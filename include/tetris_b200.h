@@ -249,6 +249,12 @@ int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const u
               const uint64_t* x1, const uint64_t* y0, const uint64_t* y1, int level,
               uint32_t npolys, void* stream);
 /* (p0 and p1 both NULL: only p2 = x1 y1 is formed; x0, y0 unused.) */
+/* The tensor's c2 = x1 y1 (eval form, written to c2_eval) and its inverse NTT
+ * into c2 (coefficient form), npolys polys of level+1 rows: on all-FP64
+ * rings the product is formed inside the first inverse phase (c2 read once
+ * from HBM less); identical residues to tg_tensor + tg_ntt_inverse_oop. */
+int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
+                         const uint64_t* y1, int level, uint32_t npolys, void* stream);
 /* Evaluator::mul_plain residue step (ckks.hpp:257-265): every part row r
  * (modulus index m) times plain row m; plain holds >= level+1 rows. */
 int tg_mul_plain(tg_context* ctx, uint64_t* out, const uint64_t* ct_part, const uint64_t* plain,

@@ -517,11 +517,9 @@ Ciphertext KeyContext::relinearize_tensor(const Ciphertext& x, const Ciphertext&
     const u64* y0 = detail::group_data(y.parts, 0, B, keep);
     const u64* y1 = detail::group_data(y.parts, B, B, keep);
     std::vector<Poly> c2e = fresh_parts(*ring_, int(B), lvl, Form::eval);
-    check_tg(tg_tensor(ring_->dev(), nullptr, nullptr, const_cast<u64*>(c2e[0].data()), x0, x1, y0, y1, lvl, B,
-                       ring_->stream()));
     std::vector<Poly> c2 = fresh_parts(*ring_, int(B), lvl, Form::coeff);
-    check_tg(tg_ntt_inverse_oop(ring_->dev(), const_cast<u64*>(c2[0].data()), c2e[0].data(), lvl, 0, B,
-                                ring_->stream()));
+    check_tg(tg_tensor_c2_inverse(ring_->dev(), const_cast<u64*>(c2[0].data()), const_cast<u64*>(c2e[0].data()), x1,
+                                  y1, lvl, B, ring_->stream()));
     std::vector<Poly> dst = fresh_parts(*ring_, int(2 * B), lvl, Form::coeff);
     check_tg(tg_relinearize_tensor_batch(plan_->dev(), const_cast<u64*>(dst[0].data()),
                                          const_cast<u64*>(dst[B].data()), c2[0].data(), c2e[0].data(), key_base(rlk),

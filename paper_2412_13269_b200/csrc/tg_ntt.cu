@@ -434,6 +434,37 @@ int ntt_inverse_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
 
 using namespace tg;
 
+extern "C" int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
+                                    const uint64_t* y1, int level, uint32_t npolys, void* stream) {
+    if (!ctx) return fail(TG_E_ARG, "[ring] null context");
+    if (level < 0 || u32(level) >= ctx->ring.q_count) return fail(TG_E_ARG, "[ring] poly level out of range");
+    if (npolys == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    const DevRing& R = ctx->ring;
+    cudaStream_t s = as_stream(stream);
+    int e1 = 0, e2 = 0;
+    static const bool off = [] {
+        const char* e = getenv("TG_C2_FUSED");
+        return e && *e == '0';
+    }();
+    // the fused chunk phase needs every row on the FP64 path, a warp plan and
+    // the unstaged chunk kernel; otherwise the two separate passes
+    if (off || NTT_CHUNK_STAGE || !ntt_pair_ok(ctx) || !warp_plan(R.logN, e1, e2) || npolys > 65535) {
+        if (int rc = tg_tensor(ctx, nullptr, nullptr, c2_eval, x1, x1, y1, y1, level, npolys, stream)) return rc;
+        return tg_ntt_inverse_oop(ctx, c2, c2_eval, level, 0, npolys, stream);
+    }
+    {
+        const size_t words = size_t(level + 1) * R.N * npolys;
+        ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * words + 24.0 * words, s, 2);  // + the tensor's 2 reads, 1 write
+        const bool pair = true;
+        if (e1 == 8) launch_inv_tensor_w<8, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair);
+        else if (e2 == 8) launch_inv_tensor_w<4, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair);
+        else launch_inv_tensor_w<4, 4>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair);
+    }
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
 static int check_shape(tg_context* ctx, int level, int nspecial) {
     if (!ctx) return fail(TG_E_ARG, "[ring] null context");
     if (level < 0 || u32(level) >= ctx->ring.q_count) return fail(TG_E_ARG, "[ring] poly level out of range");

@@ -796,10 +796,14 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
 }
 
 // Phase A inverse: one warp per contiguous chunk (stages t = 1 .. M2/2).
+// Tensor mode (tx != nullptr; FP64 rows, unstaged path): the source chunk is
+// the product tx * ty (Evaluator::mul's c2 = x1 y1, eval form, ckks.hpp:236),
+// written to c2e (ModUp's own-group rows) and transformed straight away --
+// c2 makes one trip through HBM instead of two (tg_tensor_c2_inverse).
 template <int E>
 __global__ void __launch_bounds__(256, NTT_CHUNK_MIN_BLOCKS)
 kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, int level, u32 logN1,
-              u32 row0) {
+              u32 row0, const u64* tx = nullptr, const u64* ty = nullptr, u64* c2e = nullptr) {
     using Gm = WGeo<E>;
     // row r of every poly (rows [row0, row0 + gridDim.y) are transformed)
     const u32 r = row0 + blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
@@ -871,8 +875,23 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
     if (fp) {
         const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
         u64 v[2][E];
-        ld_vec<E>(v[0], in(p), lane);
-        if (p + 1 < pend) ld_vec<E>(v[1], in(p + 1), lane);
+        // (tensor mode) chunk of c2 = x1 y1: exact FP64 product, canonical,
+        // stored for ModUp's own rows
+        auto tload = [&](u64 (&t)[E], u32 pp) {
+            const size_t o = size_t(pp * rpp + r) * N + off;
+            u64 yv[E];
+            ld_vec<E>(t, tx + o, lane);
+            ld_vec<E>(yv, ty + o, lane);
+#pragma unroll
+            for (int j = 0; j < E; ++j) t[j] = fp_canonical1(fp_mulmod_qi(u2d(t[j]), u2d(yv[j]), qd, qi), qd);
+            st_vec<E>(c2e + o, t, lane);
+        };
+        auto load = [&](u64 (&t)[E], u32 pp) {
+            if (tx) tload(t, pp);
+            else ld_vec<E>(t, in(pp), lane);
+        };
+        load(v[0], p);
+        if (p + 1 < pend) load(v[1], p + 1);
         stage_chunk_twiddles<E, false>(sw, sws, w, w + N, logN1, blockIdx.x);
         __syncthreads();
         while (true) {
@@ -887,8 +906,8 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
                 p += 1;
             }
             if (p >= pend) break;
-            ld_vec<E>(v[0], in(p), lane);
-            if (p + 1 < pend) ld_vec<E>(v[1], in(p + 1), lane);
+            load(v[0], p);
+            if (p + 1 < pend) load(v[1], p + 1);
         }
         return;
     }
@@ -1137,6 +1156,19 @@ void launch_fwd_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp,
     launch_fwd_cols_any<E1, E2>(R, sms, data, src, rpp, npolys, level, s, skip_gs, row0, nrows, pair);
     kw_fwd_chunks<E2><<<dim3(M1 / 8, nrows, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
         R, data, rpp, npolys, p2, level, WGeo<E1>::LOGM, skip_gs, row0);
+}
+
+// c2 = x1 y1 (written to c2e) and its inverse transform into data (level+1
+// rows per poly; every row FP64, unstaged chunk phase)
+template <int E1, int E2>
+void launch_inv_tensor_w(const DevRing& R, int sms, u64* data, u64* c2e, const u64* x1, const u64* y1, u32 npolys,
+                         int level, cudaStream_t s, bool pair) {
+    set_smem_attrs<E1, E2>();
+    const u32 M1 = 32 * E1, rpp = u32(level) + 1;
+    const u32 p2 = polys_per_block(M1 / 8, rpp, npolys, sms);
+    kw_inv_chunks<E2><<<dim3(M1 / 8, rpp, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
+        R, data, nullptr, rpp, npolys, p2, level, WGeo<E1>::LOGM, 0, x1, y1, c2e);
+    launch_inv_cols_any<E1, E2>(R, sms, data, rpp, npolys, level, s, 0, rpp, pair);
 }
 
 template <int E1, int E2>
