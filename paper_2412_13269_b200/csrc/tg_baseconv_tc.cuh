@@ -216,7 +216,7 @@ __device__ __forceinline__ void tc_store_a_row(uint8_t* at, u32 m, u32 kc, u64 y
 // digit, changes only with the digit). Writes every digit's level+1+K rows:
 // own-group rows copied (eval form when d_eval is given), the others
 // converted.
-template <int KB>
+template <int KB, bool RAW = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_modup_tc(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict__ d, int level,
            const u64* __restrict__ d_eval, u32 nd, u32 npolys, u32 per_cta, u32 npad_max) {
@@ -378,7 +378,9 @@ k_modup_tc(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restri
                     const double q52 = __longlong_as_double(static_cast<long long>(0x4330000000000000ull | c01.x));
                     const double q = __dsub_rn(q52, kTwo52), qi = __longlong_as_double(static_cast<long long>(c01.y));
                     const double acc = tc::recon(r + 8 * k, q, qi, c23.x, c23.y);
-                    *reinterpret_cast<u64*>(reinterpret_cast<char*>(dig) + sr[v]) = tc::canon_fp(fp_reduce(acc, q, qi), q52);
+                    const double red = fp_reduce(acc, q, qi);  // |.| <= q/2 + 1
+                    *reinterpret_cast<u64*>(reinterpret_cast<char*>(dig) + sr[v]) =
+                        RAW ? static_cast<u64>(__double_as_longlong(red)) : tc::canon_fp(red, q52);
                 }
             }
             tc::fence_before();
@@ -582,18 +584,23 @@ inline bool tc_mod_down_fits(int level) { return level + 1 <= 32; }
 
 template <int KB>
 void launch_modup_tc(const DevRing& R, const GadgetDev& G, int sms, u64* digits, const u64* d, int level, u32 nd,
-                     const u64* d_eval, u32 npolys, cudaStream_t s) {
+                     const u64* d_eval, u32 npolys, cudaStream_t s, bool raw = false) {
     const u32 gs = G.group_size, amin = std::min(gs, u32(level) + 1 - (nd - 1) * gs);
     const u32 npad_max = (R.K + u32(level) + 2 - amin) / 2 * 16;
     const TcPlan<KB> P{npad_max, npad_max / 2};
     static const bool attr = [] {  // thread-safe one-time init per instantiation
         cudaFuncSetAttribute(k_modup_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_modup_tc<KB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         return true;
     }();
     (void)attr;
     const u32 total = nd * npolys * (R.N / 128), per = tc_items_per_cta(total, sms);
-    k_modup_tc<KB><<<(total + per - 1) / per, kTcThreads, P.bytes(), s>>>(R, G, digits, d, level, d_eval, nd, npolys,
-                                                                          per, npad_max);
+    if (raw)
+        k_modup_tc<KB, true><<<(total + per - 1) / per, kTcThreads, P.bytes(), s>>>(R, G, digits, d, level, d_eval,
+                                                                                    nd, npolys, per, npad_max);
+    else
+        k_modup_tc<KB><<<(total + per - 1) / per, kTcThreads, P.bytes(), s>>>(R, G, digits, d, level, d_eval, nd,
+                                                                              npolys, per, npad_max);
 }
 
 // false: the plan does not fit shared memory (the caller falls back)

@@ -48,6 +48,11 @@ struct DevRing {
     u32 int_every;  // NTT: one FP64-eligible row in int_every takes the integer path (0: none)
 };
 
+// NTT skip word (own-group digit rows): group size (bits 0-15), digits per
+// poly of a batch (16-30), and this flag: the transformed digit rows hold
+// ModUp's centred doubles, not canonical words (column-pair phase only).
+constexpr u32 kTgRawDigits = 0x80000000u;
+
 // Row r of a poly at (level, nspecial) -> modulus index (ring.hpp:227-229).
 __host__ __device__ __forceinline__ u32 mod_index(u32 r, int level, u32 q_count) {
     return r <= u32(level) ? r : q_count + (r - u32(level) - 1);

@@ -40,7 +40,9 @@ inline u32 grid_for(size_t work) {
 // compile time: no per-term predicates or branches in the row loop (ncu: the
 // generic loop spent ~60 integer/branch instructions per row around ~90 FP64
 // ones). Same terms, same bounds, same order as the generic FP64 path.
-template <int A, int CPT, int GMAX, class Y>
+// RAW: the converted rows are written as centred doubles (the reduced sum,
+// |v| <= q/2 + 1) for the digits' column-pair NTT phase (kTgRawDigits).
+template <int A, int CPT, int GMAX, bool RAW, class Y>
 __device__ __forceinline__ void modup_rows_fp(const Y (&yd)[GMAX][CPT], const ulonglong2* smw, const u64* sq,
                                               u32 nrest, u32 v_begin, u32 v_end, u32 first, u64* out, u32 N) {
     for (u32 v = v_begin; v < v_end; ++v) {
@@ -67,7 +69,10 @@ __device__ __forceinline__ void modup_rows_fp(const Y (&yd)[GMAX][CPT], const ul
         }
         u64 o[CPT];
 #pragma unroll
-        for (int cc = 0; cc < CPT; ++cc) o[cc] = fp_canon_small(fp_reduce(acc[cc], qd, qi), q);
+        for (int cc = 0; cc < CPT; ++cc) {
+            const double v = fp_reduce(acc[cc], qd, qi);
+            o[cc] = RAW ? static_cast<u64>(__double_as_longlong(v)) : fp_canon_small(v, q);
+        }
         if constexpr (CPT == 2) *reinterpret_cast<ulonglong2*>(out + size_t(r) * N) = make_ulonglong2(o[0], o[1]);
         else out[size_t(r) * N] = o[0];
     }
@@ -410,7 +415,7 @@ k_mod_down(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict_
 // owns), the source residues stay in registers sized by a compile-time bound
 // (GMAX / KMAX), and every global access is a 16-byte vector.
 
-template <int GMAX, int CPT>
+template <int GMAX, int CPT, bool RAW = false>
 __global__ void __launch_bounds__(kMUThreads)
 k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict__ d, int level,
           const u64* __restrict__ d_eval, u32 rows_per_group, u32 nd) {
@@ -507,8 +512,8 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
 #define TG_MU_CASE(A)                                                                                 \
     case A:                                                                                           \
         if constexpr (A <= GMAX) {                                                                    \
-            if constexpr (kHoist) modup_rows_fp<A, CPT, GMAX>(yd, smw, sq, nrest, vb, ve, first, o, N); \
-            else modup_rows_fp<A, CPT, GMAX>(y, smw, sq, nrest, vb, ve, first, o, N);                 \
+            if constexpr (kHoist) modup_rows_fp<A, CPT, GMAX, RAW>(yd, smw, sq, nrest, vb, ve, first, o, N); \
+            else modup_rows_fp<A, CPT, GMAX, RAW>(y, smw, sq, nrest, vb, ve, first, o, N);                 \
         }                                                                                             \
         return;
             TG_MU_CASE(1) TG_MU_CASE(2) TG_MU_CASE(3) TG_MU_CASE(4)
@@ -808,7 +813,7 @@ inline u32 row_groups(u64 threads, u32 rows, int sms) {
 
 template <int GMAX, int CPT>
 void launch_modup_v(const DevRing& R, const GadgetDev& G, int sms, u64* digits, const u64* d, int level, u32 nd,
-                    const u64* d_eval, cudaStream_t s, u32 npolys = 1) {
+                    const u64* d_eval, cudaStream_t s, u32 npolys = 1, bool raw = false) {
     // worst-case table over the digits (the last digit may be partial)
     const u32 gs = G.group_size, rows_out = u32(level) + 1 + R.K;
     const size_t smem = size_t(rows_out) * gs * 16 + size_t(rows_out) * 16;
@@ -816,7 +821,8 @@ void launch_modup_v(const DevRing& R, const GadgetDev& G, int sms, u64* digits, 
     const u32 groups = row_groups(u64(bx) * nd * npolys * kMUThreads, rows_out, sms);
     const u32 rpg = (rows_out + groups - 1) / groups;
     const dim3 grid(bx, nd * npolys, (rows_out + rpg - 1) / rpg);
-    k_modup_v<GMAX, CPT><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg, nd);
+    if (raw) k_modup_v<GMAX, CPT, true><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg, nd);
+    else k_modup_v<GMAX, CPT><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg, nd);
 }
 
 template <int KMAX, int CPT, bool CONV = false>
@@ -858,6 +864,14 @@ __global__ void k_mod_down_finish(DevRing R, GadgetDev G, u64* __restrict__ out,
 // ModUp of npolys coeff-form sources (level+1 rows each, back to back) into
 // digits [npolys][nd][level+1+K][N], then one batched forward NTT of all
 // digits (own-group rows skipped when the eval form d_eval is supplied).
+inline bool raw_digits_on() {
+    static const bool on = [] {
+        const char* e = getenv("TG_RAW_DIGITS");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, const u64* d_eval = nullptr,
           u32 npolys = 1, bool cols_only = false) {
     tg_context* ctx = g->ctx;
@@ -865,6 +879,10 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
     const u32 nd = tg_gadget_digit_count(g, level);
     const size_t in_words = size_t(level + 1) * R.N, dig_words = size_t(nd) * (level + 1 + R.K) * R.N;
     dim3 grid((R.N + kMUThreads - 1) / kMUThreads, nd);
+    // converted rows as centred doubles straight into the column-pair phase
+    // (own rows skipped there: eval form given); N = 2^16, every row FP64
+    const bool raw = cols_only && d_eval && !g->g.base2_bits && R.logN == 16 && ntt_inverse_cols_raw_ok(ctx) &&
+                     g->g.lazy_modup && g->g.group_size <= 16 && raw_digits_on();
     {
         ProfScope prof(ctx, TG_OP_MODUP,
                        8.0 * R.N * npolys * (double(level + 1) + double(nd) * (level + 1 + R.K)), s);
@@ -883,24 +901,24 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
             // int8 tensor cores (tg_baseconv_tc.cuh); auto: where measured faster than k_modup_v
             // (digit groups <= 8, high levels, large batches: config 4 level 21 batch 8 229 -> 185 us)
             switch (G.tc_kb_mu) {
-                case 32: launch_modup_tc<32>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s); break;
-                case 64: launch_modup_tc<64>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s); break;
-                case 96: launch_modup_tc<96>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s); break;
-                default: launch_modup_tc<128>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s); break;
+                case 32: launch_modup_tc<32>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw); break;
+                case 64: launch_modup_tc<64>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw); break;
+                case 96: launch_modup_tc<96>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw); break;
+                default: launch_modup_tc<128>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw); break;
             }
         } else if (G.lazy_modup && G.group_size <= 4)
-            launch_modup_v<4, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
+            launch_modup_v<4, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys, raw);
         else if (G.lazy_modup && G.group_size <= 8)
-            launch_modup_v<8, MODUP_CPT8>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
+            launch_modup_v<8, MODUP_CPT8>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys, raw);
         else if (G.lazy_modup && G.group_size <= 16)
-            launch_modup_v<16, MODUP_CPT16>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys);
+            launch_modup_v<16, MODUP_CPT16>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys, raw);
         else
             for (u32 b = 0; b < npolys; ++b)
                 k_modup<<<grid, kMUThreads, 0, s>>>(R, G, digits + b * dig_words, d + b * in_words, level,
                                                     d_eval ? d_eval + b * in_words : nullptr);
     }
     TG_LAUNCH_CHECK();
-    const u32 skip = d_eval ? (g->g.group_size | (npolys > 1 ? nd << 16 : 0u)) : 0u;
+    const u32 skip = d_eval ? (g->g.group_size | (npolys > 1 ? nd << 16 : 0u) | (raw ? kTgRawDigits : 0u)) : 0u;
     if (cols_only) return ntt_forward_cols(ctx, digits, level, int(R.K), nd * npolys, s, skip);
     return ntt_forward_oop(ctx, digits, digits, level, int(R.K), nd * npolys, s, skip);
 }

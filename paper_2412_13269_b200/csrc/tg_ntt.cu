@@ -33,6 +33,7 @@ constexpr u32 kLogTile = 11;
 // skip = group_size | (digits per source poly << 16): poly p is digit
 // p % digits of source p / digits (digits = 0: one source, digit p).
 __device__ __forceinline__ bool ntt_row_skipped(u32 row, u32 rpp, int level, u32 skip) {
+    skip &= ~kTgRawDigits;
     if (!skip) return false;
     const u32 gs = skip & 0xFFFFu, nd = skip >> 16;
     const u32 r = row % rpp, p = row / rpp;

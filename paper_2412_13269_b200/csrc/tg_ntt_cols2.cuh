@@ -154,6 +154,7 @@ kw_fwd_cols2(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb,
     const u64* w = reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N);
     const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
     const u64 qq = R.q[mi];
+    const bool raw = (skip_gs & kTgRawDigits) != 0;
     const u32 c0 = blockIdx.x * 16;
     issue_pair_tile<E, N2>(reinterpret_cast<double2*>(dyn), src + size_t(p * rpp + r) * N + c0);
     stage_col_twiddles<E, true>(sw, nullptr, w, w + N);
@@ -180,8 +181,13 @@ kw_fwd_cols2(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb,
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const double2 t = pr[pu(lane + 32 * j, warp)];
-            v[0][j] = c2d(static_cast<u64>(__double_as_longlong(t.x)), qq);
-            v[1][j] = c2d(static_cast<u64>(__double_as_longlong(t.y)), qq);
+            if (raw) {  // ModUp's centred doubles (|v| <= q/2 + 1, the bound c2d gives)
+                v[0][j] = t.x;
+                v[1][j] = t.y;
+            } else {
+                v[0][j] = c2d(static_cast<u64>(__double_as_longlong(t.x)), qq);
+                v[1][j] = c2d(static_cast<u64>(__double_as_longlong(t.y)), qq);
+            }
         }
         wfwd_all_pair<E>(v, pr, warp, lane, sw, qd, qi);
         __syncwarp();
@@ -326,6 +332,7 @@ kw_fwd_cols2_tma(const __grid_constant__ CUtensorMap tmap, DevRing R, u64* data,
     const u64* w = reinterpret_cast<const u64*>(R.twd + size_t(mi) * 4 * N);
     const double qd = R.qd[4 * mi], qi = R.qd[4 * mi + 1];
     const u64 qq = R.q[mi];
+    const bool raw = (skip_gs & kTgRawDigits) != 0;
     const u32 c0 = blockIdx.x * 16;
     if (threadIdx.x == 0) {
         mbar_init(bars, 1);
@@ -353,8 +360,13 @@ kw_fwd_cols2_tma(const __grid_constant__ CUtensorMap tmap, DevRing R, u64* data,
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const double2 t = pr[pu_tma(lane + 32 * j, warp)];
-            v[0][j] = c2d(static_cast<u64>(__double_as_longlong(t.x)), qq);
-            v[1][j] = c2d(static_cast<u64>(__double_as_longlong(t.y)), qq);
+            if (raw) {  // ModUp's centred doubles (|v| <= q/2 + 1, the bound c2d gives)
+                v[0][j] = t.x;
+                v[1][j] = t.y;
+            } else {
+                v[0][j] = c2d(static_cast<u64>(__double_as_longlong(t.x)), qq);
+                v[1][j] = c2d(static_cast<u64>(__double_as_longlong(t.y)), qq);
+            }
         }
         __syncthreads();  // every warp has read the TMA layout before the exchanges overwrite the tile
         wfwd_all_pair<E>(v, pr, warp, lane, sw, qd, qi);
