@@ -254,7 +254,11 @@ int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const u
  * rings the product is formed inside the first inverse phase (c2 read once
  * from HBM less); identical residues to tg_tensor + tg_ntt_inverse_oop. */
 int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
-                         const uint64_t* y1, int level, uint32_t npolys, void* stream);
+                         const uint64_t* y1, int level, uint32_t npolys, int* raw, void* stream);
+/* raw (in/out, may be NULL): non-NULL lets the call leave c2 as the inverse
+ * transform's raw doubles without the N^-1 factor (|v| <= 0.6q) when the
+ * fused key switch can consume them; *raw reports whether it did (pass it on
+ * as tg_relinearize_tensor_batch's c2_raw). */
 /* Evaluator::mul_plain residue step (ckks.hpp:257-265): every part row r
  * (modulus index m) times plain row m; plain holds >= level+1 rows. */
 int tg_mul_plain(tg_context* ctx, uint64_t* out, const uint64_t* ct_part, const uint64_t* plain,
@@ -365,7 +369,7 @@ int tg_keyswitch_add_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const u
 int tg_relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* c2,
                                 const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits, int level,
                                 const uint64_t* x0, const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
-                                uint32_t npolys, void* stream);
+                                uint32_t npolys, int c2_raw, void* stream);
 
 #ifdef __cplusplus
 }

@@ -518,12 +518,13 @@ Ciphertext KeyContext::relinearize_tensor(const Ciphertext& x, const Ciphertext&
     const u64* y1 = detail::group_data(y.parts, B, B, keep);
     std::vector<Poly> c2e = fresh_parts(*ring_, int(B), lvl, Form::eval);
     std::vector<Poly> c2 = fresh_parts(*ring_, int(B), lvl, Form::coeff);
+    int raw = 1;  // c2 may stay the inverse transform's raw doubles (ModUp folds N^-1)
     check_tg(tg_tensor_c2_inverse(ring_->dev(), const_cast<u64*>(c2[0].data()), const_cast<u64*>(c2e[0].data()), x1,
-                                  y1, lvl, B, ring_->stream()));
+                                  y1, lvl, B, &raw, ring_->stream()));
     std::vector<Poly> dst = fresh_parts(*ring_, int(2 * B), lvl, Form::coeff);
     check_tg(tg_relinearize_tensor_batch(plan_->dev(), const_cast<u64*>(dst[0].data()),
                                          const_cast<u64*>(dst[B].data()), c2[0].data(), c2e[0].data(), key_base(rlk),
-                                         rlk.digits(), lvl, x0, x1, y0, y1, B, ring_->stream()));
+                                         rlk.digits(), lvl, x0, x1, y0, y1, B, raw, ring_->stream()));
     Ciphertext out;
     out.batch = B;
     out.parts = std::move(dst);

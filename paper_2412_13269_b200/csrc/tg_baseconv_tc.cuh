@@ -216,7 +216,7 @@ __device__ __forceinline__ void tc_store_a_row(uint8_t* at, u32 m, u32 kc, u64 y
 // digit, changes only with the digit). Writes every digit's level+1+K rows:
 // own-group rows copied (eval form when d_eval is given), the others
 // converted.
-template <int KB, bool RAW = false>
+template <int KB, bool RAW = false, bool RAWIN = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_modup_tc(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict__ d, int level,
            const u64* __restrict__ d_eval, u32 nd, u32 npolys, u32 per_cta, u32 npad_max) {
@@ -273,7 +273,9 @@ k_modup_tc(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restri
         for (u32 it = 0; it < nitems; ++it) {
             const u32 as = it % kTcAStages, ause = it / kTcAStages;
             const u32 first = j * gs, A = min(gs, lvl + 1 - first);
-            const u64* sconst = G.tc_mu_c + size_t(j * gs + A - 1) * G.tc_mu_cstride + size_t(G.tc_tall) * 4;
+            // source constants (x N^-1 for raw inverse-NTT sources, RAWIN)
+            const u64* sconst = G.tc_mu_c + size_t(j * gs + A - 1) * G.tc_mu_cstride + size_t(G.tc_tall) * 4 +
+                                (RAWIN ? size_t(gs) * 2 : 0);
             const size_t off = (size_t(bs) * nd + j) * dig_words + tl * 128 + m;
             tc::bar_wait(&bars->a_empty[as], (ause & 1) ^ 1);
             uint8_t* at = sa + as * TcPlan<KB>::A_BYTES;
@@ -293,7 +295,8 @@ k_modup_tc(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restri
                             : kPE   ? xe[kPE ? u : 0]
                                     : d_eval[size_t(bs) * in_words + size_t(s) * N + tl * 128 + m];
                         const double q = u2d(R.q[s]);
-                        double v = fp_mulmod(u2d(xs[u]), __longlong_as_double(static_cast<long long>(__ldg(sconst + 2 * i))),
+                        const double xv = RAWIN ? __longlong_as_double(static_cast<long long>(xs[u])) : u2d(xs[u]);
+                        double v = fp_mulmod(xv, __longlong_as_double(static_cast<long long>(__ldg(sconst + 2 * i))),
                                              __longlong_as_double(static_cast<long long>(__ldg(sconst + 2 * i + 1))), q);
                         if (v < 0) v = __dadd_rn(v, q);
                         y[s2] = d2u(v);
@@ -584,18 +587,27 @@ inline bool tc_mod_down_fits(int level) { return level + 1 <= 32; }
 
 template <int KB>
 void launch_modup_tc(const DevRing& R, const GadgetDev& G, int sms, u64* digits, const u64* d, int level, u32 nd,
-                     const u64* d_eval, u32 npolys, cudaStream_t s, bool raw = false) {
+                     const u64* d_eval, u32 npolys, cudaStream_t s, bool raw = false, bool raw_in = false) {
     const u32 gs = G.group_size, amin = std::min(gs, u32(level) + 1 - (nd - 1) * gs);
     const u32 npad_max = (R.K + u32(level) + 2 - amin) / 2 * 16;
     const TcPlan<KB> P{npad_max, npad_max / 2};
     static const bool attr = [] {  // thread-safe one-time init per instantiation
         cudaFuncSetAttribute(k_modup_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(k_modup_tc<KB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_modup_tc<KB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_modup_tc<KB, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         return true;
     }();
     (void)attr;
     const u32 total = nd * npolys * (R.N / 128), per = tc_items_per_cta(total, sms);
-    if (raw)
+    const u32 nb = (total + per - 1) / per;
+    if (raw_in && raw)
+        k_modup_tc<KB, true, true><<<nb, kTcThreads, P.bytes(), s>>>(R, G, digits, d, level, d_eval, nd, npolys, per,
+                                                                     npad_max);
+    else if (raw_in)
+        k_modup_tc<KB, false, true><<<nb, kTcThreads, P.bytes(), s>>>(R, G, digits, d, level, d_eval, nd, npolys, per,
+                                                                      npad_max);
+    else if (raw)
         k_modup_tc<KB, true><<<(total + per - 1) / per, kTcThreads, P.bytes(), s>>>(R, G, digits, d, level, d_eval,
                                                                                     nd, npolys, per, npad_max);
     else

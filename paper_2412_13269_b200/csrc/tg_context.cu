@@ -542,7 +542,7 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
             g->g.tc_kb_md = kbd;
             g->g.tc_tall = tall;
             g->g.tc_mu_bstride = size_t(tall) * 8 * kbm;
-            g->g.tc_mu_cstride = size_t(tall) * 4 + size_t(gs) * 2;
+            g->g.tc_mu_cstride = size_t(tall) * 4 + size_t(gs) * 4;  // + sources, then sources x N^-1
             const size_t ncombo = size_t(ng) * gs;
             tc_mu_b_off = 0;
             tc_md_b_off = ncombo * g->g.tc_mu_bstride;
@@ -585,6 +585,9 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
                         const u64 q = mod[first + i], sc = src[((size_t(j) * gs + (a - 1)) * gs + i) * 2];
                         cc[size_t(tall) * 4 + 2 * i] = bits(double(sc));
                         cc[size_t(tall) * 4 + 2 * i + 1] = bits(double(sc) / double(q));
+                        const u64 scn = h_mul_mod(sc, h_inv_mod(ctx->ring.N % q, q), q);
+                        cc[size_t(tall) * 4 + size_t(gs) * 2 + 2 * i] = bits(double(scn));
+                        cc[size_t(tall) * 4 + size_t(gs) * 2 + 2 * i + 1] = bits(double(scn) / double(q));
                     }
                 }
             }
@@ -615,7 +618,25 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
         }
     }
     const size_t tcb_words = tcb.empty() ? 0 : (tcb.size() + 15) / 16 * 2 + 1;  // + alignment slack
-    size_t words = src.size() + conv.size() + md.size() + mdf.size() + mdfn.size() + tcc.size() + tcb_words;
+    // ModUp source constants times N^-1 as FP64 pairs (raw inverse-NTT sources;
+    // every modulus below the FP64 bound)
+    std::vector<u64> srcn;
+    if (g->g.fp_moddown) {
+        srcn.assign(src.size(), 0);
+        for (u32 j = 0; j < ng; ++j) {
+            const u32 first = j * gs, count = std::min(gs, nq - first);
+            for (u32 a = 1; a <= count; ++a)
+                for (u32 i = 0; i < a; ++i) {
+                    const size_t e = ((size_t(j) * gs + (a - 1)) * gs + i) * 2;
+                    const u64 q = mod[first + i], scn = h_mul_mod(src[e], h_inv_mod(ctx->ring.N % q, q), q);
+                    const double v = double(scn), vq = double(scn) / double(q);
+                    std::memcpy(&srcn[e], &v, 8);
+                    std::memcpy(&srcn[e + 1], &vq, 8);
+                }
+        }
+    }
+    size_t words = src.size() + conv.size() + md.size() + mdf.size() + mdfn.size() + tcc.size() + tcb_words +
+                   srcn.size();
     cudaError_t e = cudaMalloc(&g->dev_block, words * 8);
     if (e != cudaSuccess) {
         delete g;
@@ -631,6 +652,16 @@ extern "C" int tg_gadget_create(tg_gadget** out, tg_context* ctx, uint32_t group
         u64* tc_c = p + src.size() + conv.size() + md.size() + mdf.size() + mdfn.size();
         const size_t off = size_t(tc_c + tcc.size() - p);
         uint8_t* tc_b = reinterpret_cast<uint8_t*>(p + (off + 1) / 2 * 2);  // 16-byte aligned
+        u64* srcn_p = p + words - srcn.size();
+        g->g.srcn = srcn.empty() ? nullptr : srcn_p;
+        if (!srcn.empty()) {
+            cudaError_t es = cudaMemcpy(srcn_p, srcn.data(), srcn.size() * 8, cudaMemcpyHostToDevice);
+            if (es != cudaSuccess) {
+                cudaFree(g->dev_block);
+                delete g;
+                return cuda_fail(es, "cudaMemcpy(gadget srcn)");
+            }
+        }
         g->g.tc_mu_c = tcc.empty() ? nullptr : tc_c + tc_mu_c_off;
         g->g.tc_md_c = tcc.empty() ? nullptr : tc_c + tc_md_c_off;
         g->g.tc_mu_b = tcb.empty() ? nullptr : tc_b + tc_mu_b_off;

@@ -169,6 +169,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 struct GadgetDev {
     u32 group_size, ngroups;
     u64* src;   // [ngroups][group_size(active-1)][group_size(i)][2]
+    const u64* srcn;  // the same constants times N^-1 as FP64 (value, fl(./q)) bits: raw inverse-NTT sources
     u64* conv;  // [ngroups][group_size][group_size][nmod][2]
     u64* md;    // ModDown: [K][2] (P/p_s)^-1 mod p_s; [K][q_count][4] +-(P/p_s) mod q_r; [q_count][2] P^-1 mod q_r;
                 // [q_count][4] P mod q_r (u64, Shoup, FP64 value, FP64 quotient)

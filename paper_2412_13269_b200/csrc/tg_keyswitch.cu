@@ -415,7 +415,10 @@ k_mod_down(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict_
 // owns), the source residues stay in registers sized by a compile-time bound
 // (GMAX / KMAX), and every global access is a 16-byte vector.
 
-template <int GMAX, int CPT, bool RAW = false>
+// RAWIN: d holds raw inverse-NTT doubles (|v| <= 0.6q, no N^-1) -- the
+// sources are formed on the FP64 pipe with N^-1 folded into their constants
+// (G.srcn); the own-group rows then come from d_eval (required).
+template <int GMAX, int CPT, bool RAW = false, bool RAWIN = false>
 __global__ void __launch_bounds__(kMUThreads)
 k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restrict__ d, int level,
           const u64* __restrict__ d_eval, u32 rows_per_group, u32 nd) {
@@ -491,8 +494,21 @@ k_modup_v(DevRing R, GadgetDev G, u64* __restrict__ digits, const u64* __restric
                 x[0] = d[size_t(s) * N + c0];
                 if (copy) out[size_t(s) * N] = d_eval ? d_eval[size_t(s) * N + c0] : x[0];
             }
+            if constexpr (RAWIN) {
+                const u64* sn = G.srcn + ((size_t(j) * gs + (active - 1)) * gs + i) * 2;
+                const double wd = __longlong_as_double(static_cast<long long>(sn[0]));
+                const double wq = __longlong_as_double(static_cast<long long>(sn[1]));
+                const double qd = u2d(q);
 #pragma unroll
-            for (int cc = 0; cc < CPT; ++cc) y[i][cc] = shoup(x[cc], w, ws, q);
+                for (int cc = 0; cc < CPT; ++cc) {
+                    double v = fp_mulmod(__longlong_as_double(static_cast<long long>(x[cc])), wd, wq, qd);
+                    if (v < 0) v = __dadd_rn(v, qd);
+                    y[i][cc] = d2u(v);
+                }
+            } else {
+#pragma unroll
+                for (int cc = 0; cc < CPT; ++cc) y[i][cc] = shoup(x[cc], w, ws, q);
+            }
         }
     }
     // sources as exact doubles once (FP64 targets), not per target row; the
@@ -813,7 +829,7 @@ inline u32 row_groups(u64 threads, u32 rows, int sms) {
 
 template <int GMAX, int CPT>
 void launch_modup_v(const DevRing& R, const GadgetDev& G, int sms, u64* digits, const u64* d, int level, u32 nd,
-                    const u64* d_eval, cudaStream_t s, u32 npolys = 1, bool raw = false) {
+                    const u64* d_eval, cudaStream_t s, u32 npolys = 1, bool raw = false, bool raw_in = false) {
     // worst-case table over the digits (the last digit may be partial)
     const u32 gs = G.group_size, rows_out = u32(level) + 1 + R.K;
     const size_t smem = size_t(rows_out) * gs * 16 + size_t(rows_out) * 16;
@@ -821,7 +837,11 @@ void launch_modup_v(const DevRing& R, const GadgetDev& G, int sms, u64* digits, 
     const u32 groups = row_groups(u64(bx) * nd * npolys * kMUThreads, rows_out, sms);
     const u32 rpg = (rows_out + groups - 1) / groups;
     const dim3 grid(bx, nd * npolys, (rows_out + rpg - 1) / rpg);
-    if (raw) k_modup_v<GMAX, CPT, true><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg, nd);
+    if (raw_in && raw)
+        k_modup_v<GMAX, CPT, true, true><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg, nd);
+    else if (raw_in)
+        k_modup_v<GMAX, CPT, false, true><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg, nd);
+    else if (raw) k_modup_v<GMAX, CPT, true><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg, nd);
     else k_modup_v<GMAX, CPT><<<grid, kMUThreads, smem, s>>>(R, G, digits, d, level, d_eval, rpg, nd);
 }
 
@@ -873,12 +893,14 @@ inline bool raw_digits_on() {
 }
 
 int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, const u64* d_eval = nullptr,
-          u32 npolys = 1, bool cols_only = false) {
+          u32 npolys = 1, bool cols_only = false, bool raw_in = false) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const u32 nd = tg_gadget_digit_count(g, level);
     const size_t in_words = size_t(level + 1) * R.N, dig_words = size_t(nd) * (level + 1 + R.K) * R.N;
     dim3 grid((R.N + kMUThreads - 1) / kMUThreads, nd);
+    if (raw_in && !(d_eval && g->g.srcn && !g->g.base2_bits && g->g.lazy_modup && g->g.group_size <= 16))
+        return fail(TG_E_ARG, "[rlwe] raw ModUp sources need the FP64 gadget tables and the eval form");
     // converted rows as centred doubles straight into the column-pair phase
     // (own rows skipped there: eval form given); N = 2^16, every row FP64
     const bool raw = cols_only && d_eval && !g->g.base2_bits && R.logN == 16 && ntt_inverse_cols_raw_ok(ctx) &&
@@ -901,17 +923,17 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
             // int8 tensor cores (tg_baseconv_tc.cuh); auto: where measured faster than k_modup_v
             // (digit groups <= 8, high levels, large batches: config 4 level 21 batch 8 229 -> 185 us)
             switch (G.tc_kb_mu) {
-                case 32: launch_modup_tc<32>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw); break;
-                case 64: launch_modup_tc<64>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw); break;
-                case 96: launch_modup_tc<96>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw); break;
-                default: launch_modup_tc<128>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw); break;
+                case 32: launch_modup_tc<32>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw, raw_in); break;
+                case 64: launch_modup_tc<64>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw, raw_in); break;
+                case 96: launch_modup_tc<96>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw, raw_in); break;
+                default: launch_modup_tc<128>(R, G, ctx->sms, digits, d, level, nd, d_eval, npolys, s, raw, raw_in); break;
             }
         } else if (G.lazy_modup && G.group_size <= 4)
-            launch_modup_v<4, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys, raw);
+            launch_modup_v<4, 2>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys, raw, raw_in);
         else if (G.lazy_modup && G.group_size <= 8)
-            launch_modup_v<8, MODUP_CPT8>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys, raw);
+            launch_modup_v<8, MODUP_CPT8>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys, raw, raw_in);
         else if (G.lazy_modup && G.group_size <= 16)
-            launch_modup_v<16, MODUP_CPT16>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys, raw);
+            launch_modup_v<16, MODUP_CPT16>(R, G, ctx->sms, digits, d, level, nd, d_eval, s, npolys, raw, raw_in);
         else
             for (u32 b = 0; b < npolys; ++b)
                 k_modup<<<grid, kMUThreads, 0, s>>>(R, G, digits + b * dig_words, d + b * in_words, level,
@@ -1049,13 +1071,13 @@ int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd
 // of level+1+K rows (digits, then both accumulators).
 int ks_fused_batch(tg_gadget* g, u64* out0, u64* out1, const u64* d, const u64* d_eval, u32 nd, u32 npolys,
                    const u64* key, int level, u64* scratch, cudaStream_t s, const u64* add0, const u64* add1,
-                   bool eval_add, const u64* ty0 = nullptr, const u64* ty1 = nullptr) {
+                   bool eval_add, const u64* ty0 = nullptr, const u64* ty1 = nullptr, bool raw_in = false) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const size_t words = size_t(level + 1 + R.K) * R.N;
     u64* digits = scratch;
     u64* acc = scratch + size_t(npolys) * nd * words;
-    if (int rc = modup(g, digits, d, level, s, d_eval, npolys, true)) return rc;
+    if (int rc = modup(g, digits, d, level, s, d_eval, npolys, true, raw_in)) return rc;
     const u64* pmod = g->g.md + 2 * R.K + size_t(R.K) * R.q_count * 4 + size_t(R.q_count) * 2;
     const u32 own = (d_eval && !g->g.base2_bits) ? g->g.group_size : 0u;
     if (int rc = ks_fused_chunks(ctx, acc, digits, nd, npolys, key, level, own, eval_add ? add0 : nullptr,
@@ -1210,10 +1232,12 @@ extern "C" int tg_relinearize_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1
 extern "C" int tg_relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* c2,
                                            const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits,
                                            int level, const uint64_t* x0, const uint64_t* x1, const uint64_t* y0,
-                                           const uint64_t* y1, uint32_t npolys, void* stream) {
+                                           const uint64_t* y1, uint32_t npolys, int c2_raw, void* stream) {
     if (int rc = check_ks(g, level)) return rc;
     if (npolys == 0) return TG_OK;
     if (!x0 || !x1 || !y0 || !y1) return fail(TG_E_ARG, "[rlwe] relinearize needs both operands' eval parts");
+    if (c2_raw && !(c2_eval && ks_fused_ok(g->ctx)))
+        return fail(TG_E_ARG, "[rlwe] a raw c2 needs its eval form and the fused key switch");
     tg_context* ctx = g->ctx;
     const u32 nd = tg_gadget_digit_count(g, level);
     if (nd > key_digits) return fail(TG_E_ARG, "[rlwe] switching key has too few digits");
@@ -1236,7 +1260,7 @@ extern "C" int tg_relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_
     void* scratch = nullptr;
     TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
     const int rc = ks_fused_batch(g, out0, out1, c2, c2_eval, nd, npolys, key, level, static_cast<u64*>(scratch), s,
-                                  x0, x1, true, y0, y1);
+                                  x0, x1, true, y0, y1, c2_raw != 0);
     cudaFreeAsync(scratch, s);
     return rc;
 }

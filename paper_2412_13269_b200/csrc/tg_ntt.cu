@@ -436,7 +436,8 @@ int ntt_inverse_oop(tg_context* ctx, u64* data, const u64* src, int level, int n
 using namespace tg;
 
 extern "C" int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
-                                    const uint64_t* y1, int level, uint32_t npolys, void* stream) {
+                                    const uint64_t* y1, int level, uint32_t npolys, int* raw, void* stream) {
+    if (raw) *raw = 0;
     if (!ctx) return fail(TG_E_ARG, "[ring] null context");
     if (level < 0 || u32(level) >= ctx->ring.q_count) return fail(TG_E_ARG, "[ring] poly level out of range");
     if (npolys == 0) return TG_OK;
@@ -454,14 +455,23 @@ extern "C" int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_
         if (int rc = tg_tensor(ctx, nullptr, nullptr, c2_eval, x1, x1, y1, y1, level, npolys, stream)) return rc;
         return tg_ntt_inverse_oop(ctx, c2, c2_eval, level, 0, npolys, stream);
     }
+    // raw output (the inverse column phase's doubles, no N^-1: ModUp folds it
+    // into its source constants) when the caller accepts it and the key
+    // switch will take the fused path
+    static const bool raw_off = [] {
+        const char* e = getenv("TG_RAW_C2");
+        return e && *e == '0';
+    }();
+    const bool out_raw = raw && !raw_off && ntt_inverse_cols_raw_ok(ctx) && ks_fused_ok(ctx);
     {
         const size_t words = size_t(level + 1) * R.N * npolys;
         ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * words + 24.0 * words, s, 2);  // + the tensor's 2 reads, 1 write
         const bool pair = true;
-        if (e1 == 8) launch_inv_tensor_w<8, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair);
+        if (e1 == 8) launch_inv_tensor_w<8, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, out_raw);
         else if (e2 == 8) launch_inv_tensor_w<4, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair);
         else launch_inv_tensor_w<4, 4>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair);
     }
+    if (raw) *raw = (out_raw && e1 == 8) ? 1 : 0;
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

@@ -1162,13 +1162,13 @@ void launch_fwd_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp,
 // rows per poly; every row FP64, unstaged chunk phase)
 template <int E1, int E2>
 void launch_inv_tensor_w(const DevRing& R, int sms, u64* data, u64* c2e, const u64* x1, const u64* y1, u32 npolys,
-                         int level, cudaStream_t s, bool pair) {
+                         int level, cudaStream_t s, bool pair, bool raw = false) {
     set_smem_attrs<E1, E2>();
     const u32 M1 = 32 * E1, rpp = u32(level) + 1;
     const u32 p2 = polys_per_block(M1 / 8, rpp, npolys, sms);
     kw_inv_chunks<E2><<<dim3(M1 / 8, rpp, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
         R, data, nullptr, rpp, npolys, p2, level, WGeo<E1>::LOGM, 0, x1, y1, c2e);
-    launch_inv_cols_any<E1, E2>(R, sms, data, rpp, npolys, level, s, 0, rpp, pair);
+    launch_inv_cols_any<E1, E2>(R, sms, data, rpp, npolys, level, s, 0, rpp, pair, raw);
 }
 
 template <int E1, int E2>
