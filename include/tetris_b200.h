@@ -370,6 +370,20 @@ int tg_relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, co
                                 const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits, int level,
                                 const uint64_t* x0, const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
                                 uint32_t npolys, int c2_raw, void* stream);
+/* rescale(mul_relin(x, y)) and rescale_add(mul_relin(x, y), add)
+ * (ckks.hpp:229-237, rlwe.hpp:601-620, ckks.hpp:315-324, :195-210): the
+ * relinearised product's ModDown rows are rescaled (and added) in the same
+ * pass, so the level+1-row product never reaches HBM. out: 2*npolys polys
+ * packed (c0 of every product, then c1) of `level` rows, or out_level+1 rows
+ * with an addend (poly p of the 2*npolys at add + p*add_stride words,
+ * out_level <= level-1). Every q-chain row 0..level must be FP64-eligible
+ * (TG_E_ARG otherwise). Identical residues to tg_relinearize_tensor_batch
+ * followed by tg_rescale / tg_rescale_add, which small batches take. */
+int tg_relinearize_tensor_rescale_batch(tg_gadget* g, uint64_t* out, const uint64_t* c2,
+                                        const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits,
+                                        int level, const uint64_t* x0, const uint64_t* x1, const uint64_t* y0,
+                                        const uint64_t* y1, uint32_t npolys, int c2_raw, const uint64_t* add,
+                                        uint64_t add_stride, int out_level, void* stream);
 
 #ifdef __cplusplus
 }

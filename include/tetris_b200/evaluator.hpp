@@ -87,6 +87,12 @@ public:
     // then :195-210), one pass when every row is FP64-eligible and both are
     // coefficient-form degree-1 batches of the same shape.
     Ciphertext rescale_add(const Ciphertext& prod, const Ciphertext& y) const;
+    // Extension: rescale(mul_relin(a, b)) (add == nullptr) or
+    // rescale_add(mul_relin(a, b), *add), identical results and metadata; the
+    // product's ModDown rows are rescaled (and added) in the same pass when
+    // every row is FP64-eligible (KeyContext::relinearize_tensor_rescale).
+    Ciphertext mul_relin_rescale(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys,
+                                 const Ciphertext* add = nullptr) const;
     Ciphertext rotate(const Ciphertext& ct, u32 k, const EvalKeys& keys) const;
     Ciphertext conjugate(const Ciphertext& ct, const EvalKeys& keys) const;
     // Extension: sum_j mul_plain(cts[j], plains[j], plain_scale) in one

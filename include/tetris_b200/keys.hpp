@@ -155,6 +155,12 @@ public:
     // through HBM; c0 / c1 are formed inside the fused key-switch core
     // (tg_relinearize_tensor_batch). Residue for residue the same.
     Ciphertext relinearize_tensor(const Ciphertext& x, const Ciphertext& y, const SwitchingKey& rlk) const;
+    // relinearize_tensor then rescale_round (+ add of `add`'s rows 0..out_level)
+    // in the same ModDown pass (tg_relinearize_tensor_rescale_batch): parts of
+    // level-1 (or out_level) rows; scale / noise_bound are the PRODUCT's, the
+    // caller (Evaluator::mul_relin_rescale) applies rescale / add's metadata.
+    Ciphertext relinearize_tensor_rescale(const Ciphertext& x, const Ciphertext& y, const SwitchingKey& rlk,
+                                          const Ciphertext* add, int out_level) const;
     SwitchingKey galois_key_gen(const SecretKey& sk, u64 exponent, Rng& rng) const;
     Ciphertext apply_galois(const Ciphertext& ct, u64 exponent, const SwitchingKey& swk) const;
     // Hoisted automorphisms (Evaluator::apply_galois_many, ckks.hpp:338-367):

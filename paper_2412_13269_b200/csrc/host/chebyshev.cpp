@@ -360,8 +360,8 @@ Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const s
         std::optional<Ciphertext> Rr = rec(r, target);
         if (!Q) return Rr;
         if (!L.eval) {  // add(rescale(Q T_n), R) in one pass (Evaluator::rescale_add)
-            if (!Rr) return ev.rescale(ev.mul_relin(*Q, L.get(n), keys));
-            return ev.rescale_add(ev.mul_relin(*Q, L.get(n), keys), *Rr);
+            if (!Rr) return ev.mul_relin_rescale(*Q, L.get(n), keys);
+            return ev.mul_relin_rescale(*Q, L.get(n), keys, &*Rr);
         }
         Ciphertext P = ev.rescale_eval(ev.mul_relin_eval(*Q, L.get(n), keys));
         if (!Rr) return P;

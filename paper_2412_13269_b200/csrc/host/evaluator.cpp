@@ -328,6 +328,56 @@ Ciphertext Evaluator::mul_relin(const Ciphertext& a, const Ciphertext& b, const 
     return ctx_->relinearize_tensor(x, y, keys.relin);
 }
 
+Ciphertext Evaluator::mul_relin_rescale(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys,
+                                        const Ciphertext* add) const {
+    static const bool off = [] {
+        const char* e = std::getenv("TG_RELIN_TENSOR");
+        const char* f = std::getenv("TG_FUSED_RESCALE");
+        return (e && *e == '0') || (f && *f == '0');
+    }();
+    auto two_ops = [&] { return add ? rescale_add(mul_relin(a, b, keys), *add) : rescale(mul_relin(a, b, keys)); };
+    if (off) return two_ops();
+    // mul's checks in mul's order
+    if (a.domain != b.domain) throw TetrisError("ckks", "domain tag mismatch in mul");
+    if (a.degree() != 1 || b.degree() != 1) throw TetrisError("ckks", "mul expects degree-1 operands");
+    if (a.batch != b.batch) throw TetrisError("ckks", "batch size mismatch in mul");
+    Ciphertext x = a, y = b;
+    align_levels(x, y);
+    if (x.level() == 0) throw TetrisError("ckks", "exhausted ciphertext: no level left to rescale");
+    const RingParams& R = ring();
+    const int lvl = x.level();
+    for (int r = 0; r <= lvl; ++r)
+        if (R.modulus(u32(r)) >= 1351079888211148ull) return two_ops();  // kFpMaxQ (tg_fp64.cuh)
+    // rescale_add's one-pass conditions (otherwise add(rescale(prod), y))
+    if (add) {
+        if (add->form() != Form::coeff || add->degree() != 1 || add->batch != x.batch || add->domain != x.domain)
+            return two_ops();
+        for (const auto& p : add->parts)
+            if (p.nspecial() != 0) return two_ops();
+        if (!contiguous(add->parts, 0, add->parts.size()) && detail::uniform_stride(add->parts) == 0)
+            return two_ops();
+    }
+    for (const auto& p : x.parts)
+        if (p.nspecial() != 0) return two_ops();
+    for (const auto& p : y.parts)
+        if (p.nspecial() != 0) return two_ops();
+    // the product's metadata (mul, relinearize), then rescale's (ckks.hpp:321-323)
+    const u64 ql = R.modulus(u32(lvl));
+    const double pscale = (x.scale * y.scale) / double(ql);
+    const double pnoise = ((x.noise_bound * y.scale + y.noise_bound * x.scale) + ctx_->ks_noise_estimate()) / double(ql) + 1.0;
+    int out_level = lvl - 1;
+    if (add) {  // rescale_add: level alignment, scale check on the rescaled product first
+        out_level = std::min(lvl - 1, add->level());
+        check_scales_match(pscale, add->scale);
+    }
+    x.to_eval();
+    y.to_eval();
+    Ciphertext out = ctx_->relinearize_tensor_rescale(x, y, keys.relin, add, out_level);
+    out.scale = pscale;
+    out.noise_bound = add ? pnoise + add->noise_bound : pnoise;
+    return out;
+}
+
 Ciphertext Evaluator::mul_relin_eval(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys) const {
     return ctx_->relinearize_eval(mul(a, b), keys.relin);
 }

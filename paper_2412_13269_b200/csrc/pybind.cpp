@@ -310,6 +310,12 @@ PYBIND11_MODULE(_tetris_b200, m) {
              py::call_guard<py::gil_scoped_release>())
         .def("mul_relin_eval", &Evaluator::mul_relin_eval, py::keep_alive<0, 1>(),
              py::call_guard<py::gil_scoped_release>())
+        .def(
+            "mul_relin_rescale",
+            [](const Evaluator& ev, const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys,
+               const Ciphertext* add) { return ev.mul_relin_rescale(a, b, keys, add); },
+            py::arg("a"), py::arg("b"), py::arg("keys"), py::arg("add") = nullptr, py::keep_alive<0, 1>(),
+            py::call_guard<py::gil_scoped_release>())
         .def("rotate", &Evaluator::rotate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("conjugate", &Evaluator::conjugate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("mul_plain_sum", &Evaluator::mul_plain_sum, py::keep_alive<0, 1>(),

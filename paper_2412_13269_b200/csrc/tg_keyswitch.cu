@@ -722,10 +722,17 @@ k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restric
 // RAW: `in` holds the raw doubles of an inverse NTT without its N^-1 factor
 // (|v| <= 0.6q, kw_inv_cols2<..., true>); the input constants carry N^-1
 // (G.mdfn), so the canonical outputs are the same.
-template <int KMAX, bool RAW = false>
+// RESCALE (relinearisation followed by rescale / rescale_add, ckks.hpp:315-324):
+// every thread owns all rows of its coefficients; the last row is reduced
+// first, centred exactly as rescale_round does (ring.hpp:493-518), and rows
+// 0..nout-1 leave as (v_r - x_l) q_l^-1 mod q_r (+ radd's row: Evaluator::add
+// of the rescaled product and y, k_rescale_fp's arithmetic) -- the ModDown
+// output never goes through HBM. addend must be null.
+template <int KMAX, bool RAW = false, bool RESCALE = false>
 __global__ void __launch_bounds__(256)
 k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict__ in, int level, u32 npolys,
-              const u64* __restrict__ addend, u32 rows_per_group) {
+              const u64* __restrict__ addend, u32 rows_per_group, const u64* __restrict__ radd = nullptr,
+              u64 astride = 0, u32 nout = 0) {
     constexpr u32 K = KMAX;
     const u32 N = R.N, nq = R.q_count, lvl = u32(level);
     const u32 rin = lvl + 1 + K, rout = lvl + 1;
@@ -764,6 +771,63 @@ k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restri
                     y[s][cc] = v;
                 }
             }
+        }
+        if constexpr (RESCALE) {
+            // the reduced ModDown value of row r (|v| <= q/2 + 1) for both coefficients
+            auto rowval = [&](u32 r, const ulonglong2 xv, double (&v)[2]) {
+                const u64 x[2] = {xv.x, xv.y};
+                const double2 pv = sp[2 * r], qv = sp[2 * r + 1];
+                const double q = qv.x, qi = qv.y;
+                const double2* wr = smf + size_t(r) * K;
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    double acc = fp_mulmod(in_d(x[cc]), pv.x, pv.y, q);
+#pragma unroll
+                    for (int s = 0; s < KMAX; ++s) {
+                        if (u32(s) < K) {
+                            const double2 w = wr[s];
+                            acc = __dadd_rn(acc, fp_mulmod(y[s][cc], w.x, w.y, q));
+                            if ((s & 7) == 6 && u32(s + 1) < K) acc = fp_reduce(acc, q, qi);
+                        }
+                    }
+                    v[cc] = fp_reduce(acc, q, qi);
+                }
+            };
+            const u64 ql = sq64[lvl], hl = ql >> 1;
+            const double qld = u2d(ql);
+            double xl[2];
+            {
+                double v[2];
+                rowval(lvl, *reinterpret_cast<const ulonglong2*>(src + size_t(lvl) * N), v);
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {  // canonical, then centred as rescale_round does
+                    const u64 cv = fp_canon_small(v[cc], ql);
+                    xl[cc] = cv > hl ? __dsub_rn(u2d(cv), qld) : u2d(cv);
+                }
+            }
+            const double* rsd = R.rsd + size_t(lvl) * nq * 2;
+            u64* dr = out + size_t(p) * nout * N + c0;
+            const u64* ar = radd ? radd + size_t(p) * astride + c0 : nullptr;
+            ulonglong2 xn = *reinterpret_cast<const ulonglong2*>(src);
+            for (u32 r = 0; r < nout; ++r) {
+                const ulonglong2 xc = xn;
+                if (r + 1 < nout) xn = *reinterpret_cast<const ulonglong2*>(src + size_t(r + 1) * N);
+                double v[2];
+                rowval(r, xc, v);
+                const double q = sp[2 * r + 1].x, w = rsd[2 * r], wq = rsd[2 * r + 1];
+                const u64 qu = sq64[r];
+                u64 o[2];
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc)  // |v - x_l| <= q_r/2 + 1 + q_l/2 < 2^51: exact product
+                    o[cc] = fp_canon_small(fp_mulmod(__dsub_rn(v[cc], xl[cc]), w, wq, q), qu);
+                if (ar) {
+                    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(ar + size_t(r) * N);
+                    o[0] = add_mod(o[0], a.x, qu);
+                    o[1] = add_mod(o[1], a.y, qu);
+                }
+                *reinterpret_cast<ulonglong2*>(dr + size_t(r) * N) = make_ulonglong2(o[0], o[1]);
+            }
+            continue;
         }
         const u32 r_end = min(rout, (blockIdx.y + 1) * rows_per_group);
         // two rows in flight ahead of the one being reduced (ncu: the row
@@ -892,6 +956,15 @@ inline bool raw_digits_on() {
     return on;
 }
 
+// TG_FUSED_RESCALE=0: relinearise-then-rescale as two passes (A/B switch)
+inline bool fused_rescale_on() {
+    static const bool on = [] {
+        const char* e = getenv("TG_FUSED_RESCALE");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, const u64* d_eval = nullptr,
           u32 npolys = 1, bool cols_only = false, bool raw_in = false) {
     tg_context* ctx = g->ctx;
@@ -945,13 +1018,27 @@ int modup(tg_gadget* g, u64* digits, const u64* d, int level, cudaStream_t s, co
     return ntt_forward_oop(ctx, digits, digits, level, int(R.K), nd * npolys, s, skip);
 }
 
+// ModDown followed by rescale_round (+ add): out holds npolys polys of nout
+// rows (nout = level without an addend, out_level + 1 with one); poly p's
+// addend at radd + p * astride (k_mod_down_fp's RESCALE).
+struct RescaleSpec {
+    const u64* radd;
+    u64 astride;
+    u32 nout;
+};
+
 template <int KMAX, bool RAW = false>
 void launch_mod_down_fp(const DevRing& R, const GadgetDev& G, int sms, u64* out, const u64* in, int level,
-                        u32 npolys, const u64* addend, cudaStream_t s) {
+                        u32 npolys, const u64* addend, cudaStream_t s, const RescaleSpec* rs = nullptr) {
     const u32 rout = u32(level) + 1;
     const size_t smem = size_t(rout) * R.K * 16 + size_t(rout) * 40;
     const u64 work = u64(npolys) * R.N / 2;
     const u32 blocks = u32(std::min<u64>((work + 255) / 256, u64(sms) * 8));
+    if (rs) {  // every thread owns all rows of its coefficients
+        k_mod_down_fp<KMAX, RAW, true><<<blocks, 256, smem, s>>>(R, G, out, in, level, npolys, nullptr, rout,
+                                                                 rs->radd, rs->astride, rs->nout);
+        return;
+    }
     const u32 groups = row_groups(u64(blocks) * 256, rout, sms);
     const u32 rpg = (rout + groups - 1) / groups;
     k_mod_down_fp<KMAX, RAW><<<dim3(blocks, (rout + rpg - 1) / rpg), 256, smem, s>>>(R, G, out, in, level, npolys,
@@ -959,17 +1046,23 @@ void launch_mod_down_fp(const DevRing& R, const GadgetDev& G, int sms, u64* out,
 }
 
 int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaStream_t s,
-             const u64* addend = nullptr, bool raw = false) {
+             const u64* addend = nullptr, bool raw = false, const RescaleSpec* rs = nullptr) {
     const DevRing& R = g->ctx->ring;
-    ProfScope prof(g->ctx, TG_OP_MOD_DOWN, 8.0 * R.N * npolys * (2.0 * (level + 1) + R.K + (addend ? level + 1 : 0)), s);
+    ProfScope prof(g->ctx, TG_OP_MOD_DOWN,
+                   8.0 * R.N * npolys *
+                       (rs ? (level + 1.0 + R.K + rs->nout * (rs->radd ? 2.0 : 1.0))
+                           : (2.0 * (level + 1) + R.K + (addend ? level + 1 : 0))),
+                   s);
     const GadgetDev& G = g->g;
     const int sms = g->ctx->sms;
     if (raw && !(G.fp_moddown && G.mdfn)) return fail(TG_E_ARG, "[rlwe] raw ModDown input needs the FP64 ModDown");
+    if (rs && (addend || !G.fp_moddown || R.K > 16))
+        return fail(TG_E_ARG, "[rlwe] ModDown + rescale needs the FP64 ModDown and no ModDown addend");
     bool done = false;
     // int8 tensor-core base conversion (tg_baseconv_tc.cuh); auto: batched, high
     // levels (measured: config 5 ModDown 77.3 -> 56.5 ms per query; small or
     // low-level launches stay on the FP64 kernel)
-    if (G.tc_kb_md && tc_mod_down_fits(level) && (G.tc_mode == 2 || (npolys >= 4 && level >= 16))) {
+    if (!rs && G.tc_kb_md && tc_mod_down_fits(level) && (G.tc_mode == 2 || (npolys >= 4 && level >= 16))) {
         done = true;
 #define TG_MDTC(kb)                                                                                     \
     case kb:                                                                                            \
@@ -985,8 +1078,8 @@ int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaS
         switch (R.K) {
 #define TG_MD_CASE(k)                                                                    \
     case k:                                                                              \
-        if (raw) launch_mod_down_fp<k, true>(R, G, sms, out, in, level, npolys, addend, s); \
-        else launch_mod_down_fp<k>(R, G, sms, out, in, level, npolys, addend, s);       \
+        if (raw) launch_mod_down_fp<k, true>(R, G, sms, out, in, level, npolys, addend, s, rs); \
+        else launch_mod_down_fp<k>(R, G, sms, out, in, level, npolys, addend, s, rs);       \
         break;
             TG_MD_CASE(1) TG_MD_CASE(2) TG_MD_CASE(3) TG_MD_CASE(4) TG_MD_CASE(5) TG_MD_CASE(6) TG_MD_CASE(7)
             TG_MD_CASE(8) TG_MD_CASE(9) TG_MD_CASE(10) TG_MD_CASE(11) TG_MD_CASE(12) TG_MD_CASE(13)
@@ -1071,7 +1164,8 @@ int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd
 // of level+1+K rows (digits, then both accumulators).
 int ks_fused_batch(tg_gadget* g, u64* out0, u64* out1, const u64* d, const u64* d_eval, u32 nd, u32 npolys,
                    const u64* key, int level, u64* scratch, cudaStream_t s, const u64* add0, const u64* add1,
-                   bool eval_add, const u64* ty0 = nullptr, const u64* ty1 = nullptr, bool raw_in = false) {
+                   bool eval_add, const u64* ty0 = nullptr, const u64* ty1 = nullptr, bool raw_in = false,
+                   const RescaleSpec* rs = nullptr) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const size_t words = size_t(level + 1 + R.K) * R.N;
@@ -1088,6 +1182,10 @@ int ks_fused_batch(tg_gadget* g, u64* out0, u64* out1, const u64* d, const u64* 
     // (its N^-1 folded into ModDown's constants) when both kernels allow it
     const bool raw = g->g.fp_moddown && g->g.mdfn && ntt_inverse_cols_raw_ok(ctx);
     if (int rc = ntt_inverse_cols(ctx, acc, level, int(R.K), 2 * npolys, s, raw)) return rc;
+    if (rs) {  // out0/out1 back to back, nout rows per poly
+        if (!eval_add) return fail(TG_E_ARG, "[rlwe] ModDown + rescale takes eval-form addends only");
+        return mod_down(g, out0, acc, level, 2 * npolys, s, nullptr, raw, rs);
+    }
     const u64* m0 = eval_add ? nullptr : add0;
     const u64* m1 = eval_add ? nullptr : add1;
     const size_t qwords = size_t(level + 1) * R.N;
@@ -1261,6 +1359,55 @@ extern "C" int tg_relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_
     TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
     const int rc = ks_fused_batch(g, out0, out1, c2, c2_eval, nd, npolys, key, level, static_cast<u64*>(scratch), s,
                                   x0, x1, true, y0, y1, c2_raw != 0);
+    cudaFreeAsync(scratch, s);
+    return rc;
+}
+
+extern "C" int tg_relinearize_tensor_rescale_batch(tg_gadget* g, uint64_t* out, const uint64_t* c2,
+                                                   const uint64_t* c2_eval, const uint64_t* key,
+                                                   uint32_t key_digits, int level, const uint64_t* x0,
+                                                   const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
+                                                   uint32_t npolys, int c2_raw, const uint64_t* add,
+                                                   uint64_t add_stride, int out_level, void* stream) {
+    if (int rc = check_ks(g, level)) return rc;
+    if (level < 1) return fail(TG_E_ARG, "[ring] cannot rescale at level 0");
+    if (add && (out_level < 0 || out_level > level - 1)) return fail(TG_E_ARG, "[ring] rescale_add level out of range");
+    if (npolys == 0) return TG_OK;
+    if (!x0 || !x1 || !y0 || !y1) return fail(TG_E_ARG, "[rlwe] relinearize needs both operands' eval parts");
+    tg_context* ctx = g->ctx;
+    const DevRing& R = ctx->ring;
+    for (int r = 0; r <= level; ++r)
+        if (ctx->h_q[r] >= kFpMaxQ) return fail(TG_E_ARG, "[ring] fused rescale needs FP64 q-chain rows");
+    const u32 nd = tg_gadget_digit_count(g, level);
+    if (nd > key_digits) return fail(TG_E_ARG, "[rlwe] switching key has too few digits");
+    if (nd > 15) return fail(TG_E_ARG, "[rlwe] batched key switch supports at most 15 digits");
+    DeviceGuard guard(ctx->device);
+    cudaStream_t s = as_stream(stream);
+    const u32 nout = add ? u32(out_level) + 1 : u32(level);
+    // fused while the batch alone fills the GPU (every thread walks all rows)
+    const bool fuse = ks_fused_ok(ctx) && g->g.fp_moddown && R.K <= 16 && fused_rescale_on() &&
+                      u64(npolys) * R.N >= u64(ctx->sms) * 512;
+    if (!fuse) {  // relinearise into scratch, then rescale(_add)
+        if (c2_raw && !ks_fused_ok(ctx))
+            return fail(TG_E_ARG, "[rlwe] a raw c2 needs its eval form and the fused key switch");
+        const size_t qw = size_t(level + 1) * R.N * npolys;
+        void* tmp = nullptr;
+        TG_CUDA(cudaMallocFromPoolAsync(&tmp, 2 * qw * 8, ctx->pool, s));
+        u64* t = static_cast<u64*>(tmp);
+        int rc = tg_relinearize_tensor_batch(g, t, t + qw, c2, c2_eval, key, key_digits, level, x0, x1, y0, y1,
+                                             npolys, c2_raw, stream);
+        if (rc == TG_OK)
+            rc = add ? tg_rescale_add(ctx, out, t, level, 2 * npolys, add, add_stride, out_level, stream)
+                     : tg_rescale(ctx, out, t, level, 2 * npolys, stream);
+        cudaFreeAsync(tmp, s);
+        return rc;
+    }
+    const size_t words = size_t(level + 1 + R.K) * R.N;
+    void* scratch = nullptr;
+    TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
+    const RescaleSpec rs{add, add_stride, nout};
+    const int rc = ks_fused_batch(g, out, out + size_t(npolys) * nout * R.N, c2, c2_eval, nd, npolys, key, level,
+                                  static_cast<u64*>(scratch), s, x0, x1, true, y0, y1, c2_raw != 0, &rs);
     cudaFreeAsync(scratch, s);
     return rc;
 }

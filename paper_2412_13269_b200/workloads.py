@@ -385,6 +385,13 @@ def statement_block_inputs(S, d, b):
                            pt_flag=flag[0], flag_scale=fscale)
 
 
+def mul_relin_rescale(ev, a, b, keys):
+    """rescale(mul_relin(a, b)); one ModDown + rescale pass where the evaluator
+    has it (Evaluator::mul_relin_rescale, identical residues and metadata)."""
+    f = getattr(ev, "mul_relin_rescale", None)
+    return f(a, b, keys) if f is not None else ev.rescale(ev.mul_relin(a, b, keys))
+
+
 def statement_block(S, q, blk, threshold):
     """One block of the statement in the reference API's op order:
     linear risk score, three private thresholds (threshold(x, t, norm)),
@@ -496,8 +503,8 @@ def statement_partial_batched(S, q, blocks, threshold, streams=2, max_blocks=8, 
     for c0 in range(0, len(blocks), max_blocks):
         chunk = list(range(c0, min(len(blocks), c0 + max_blocks)))
         b1, b2, b3 = column_batch("sugar", chunk), column_batch("bp", chunk), column_batch("risk", chunk)
-        a = ev.rescale(ev.mul_relin(b1, b2, keys))
-        a = ev.rescale(ev.mul_relin(a, b3, keys))
+        a = mul_relin_rescale(ev, b1, b2, keys)
+        a = mul_relin_rescale(ev, a, b3, keys)
         for i, ct in zip(chunk, T.unstack_ciphertext(a) if a.batch > 1 else [a]):
             o = ev.rescale(ev.mul_plain(ct, blocks[i].pt_flag, blocks[i].flag_scale))
             if keep is not None:

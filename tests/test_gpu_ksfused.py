@@ -94,3 +94,60 @@ def test_rescale_add_matches_add_of_rescale(G, R, gpu_available, N):
     for i in range(3):
         want = r.ev.add(r.ev.rescale(r.ev.mul_relin(xs_r[i], xs_r[i], r.keys)), ys_r[i])
         assert_ct_equal(got[i], want, f"rescale_add batch block {i}")
+
+
+@pytest.mark.parametrize("N,batch", [(1 << 14, 8), (1 << 16, 1), (1 << 16, 8)])
+def test_mul_relin_rescale_matches_reference(G, R, gpu_available, N, batch):
+    """Evaluator::mul_relin_rescale (ModDown + rescale_round (+ add) in one
+    pass, tg_relinearize_tensor_rescale_batch) == rescale(mul_relin) and
+    add(rescale(mul_relin), y) of the reference: residues, scale and noise
+    bound. Batches that fill the GPU take the fused ModDown (N=2^16 x 8,
+    2^14 x 8), a single 2^16 product the relinearise-then-rescale fallback;
+    y at lower / equal level, a level-dropped view and an eval-form y."""
+    kw = dict(N=N, nq=7, K=3, group_size=3, seed=19, q_bits=50, sp_bits=50, h=192)
+    g, r = make_setup(G, **kw), make_setup(R, **kw)
+    top = g.ring.max_level()
+
+    def stack(T, cts):
+        return cts[0] if len(cts) == 1 else T.stack_ciphertexts(cts)
+
+    def unstack(T, ct):
+        return T.unstack_ciphertext(ct) if ct.batch > 1 else [ct]
+
+    for level in (top, 3):
+        xs_g, ys_g = _cts(g, batch, level, 41 + level), _cts(g, batch, level, 42 + level)
+        xs_r, ys_r = _cts(r, batch, level, 41 + level), _cts(r, batch, level, 42 + level)
+        got = g.ev.mul_relin_rescale(stack(G, xs_g), stack(G, ys_g), g.keys)
+        two = g.ev.rescale(g.ev.mul_relin(stack(G, xs_g), stack(G, ys_g), g.keys))
+        assert got.noise_bound == two.noise_bound
+        for i, c in enumerate(unstack(G, got)):
+            want = r.ev.rescale(r.ev.mul_relin(xs_r[i], ys_r[i], r.keys))
+            assert_ct_equal(c, want, f"mul_relin_rescale level {level} block {i}")
+            assert c.noise_bound == want.noise_bound
+        for ylvl in sorted({level - 2, level - 1}):
+            if ylvl < 0:
+                continue
+            ad_g, ad_r = _cts(g, batch, ylvl, 50 + ylvl), _cts(r, batch, ylvl, 50 + ylvl)
+            got = g.ev.mul_relin_rescale(stack(G, xs_g), stack(G, ys_g), g.keys, stack(G, ad_g))
+            for i, c in enumerate(unstack(G, got)):
+                want = r.ev.add(r.ev.rescale(r.ev.mul_relin(xs_r[i], ys_r[i], r.keys)), ad_r[i])
+                assert_ct_equal(c, want, f"mul_relin_rescale add level {level} y {ylvl} block {i}")
+                assert c.noise_bound == want.noise_bound
+    # a level-dropped view of y (strided parts) and an eval-form y (two-op path)
+    xs_g, ys_g = _cts(g, batch, top, 61), _cts(g, batch, top, 62)
+    xs_r, ys_r = _cts(r, batch, top, 61), _cts(r, batch, top, 62)
+    ad_g, ad_r = _cts(g, batch, top, 63), _cts(r, batch, top, 63)
+    yv = stack(G, ad_g).copy()
+    yv.drop_to_level(top - 2)
+    ye = stack(G, ad_g).copy()
+    ye.to_eval()
+    for y, what in ((yv, "view"), (ye, "eval y")):
+        got = unstack(G, g.ev.mul_relin_rescale(stack(G, xs_g), stack(G, ys_g), g.keys, y))
+        for i, c in enumerate(got):
+            yr = ad_r[i].copy()
+            if what == "view":
+                yr.drop_to_level(top - 2)
+            else:
+                yr.to_eval()
+            want = r.ev.add(r.ev.rescale(r.ev.mul_relin(xs_r[i], ys_r[i], r.keys)), yr)
+            assert_ct_equal(c, want, f"mul_relin_rescale {what} block {i}")
