@@ -93,6 +93,15 @@ public:
     // every row is FP64-eligible (KeyContext::relinearize_tensor_rescale).
     Ciphertext mul_relin_rescale(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys,
                                  const Ciphertext* add = nullptr) const;
+    // Extension (lazy relinearisation): rescale(relinearize(add(mul(a, b),
+    // mul(c, d)))) (+ add(., *add)) -- the reference's mul (ckks.hpp:220-245),
+    // add (:201-208), relinearize (rlwe.hpp:601-620) and rescale (:315-324) in
+    // that order, identical residues and metadata, with ONE key switch for the
+    // two products. mul(c, d)'s level must not be below mul(a, b)'s for the
+    // fast path (the second tensor is formed at the first's level: the tensor
+    // is row-wise, so dropping operands first equals add's drop afterwards).
+    Ciphertext mul2_relin_rescale(const Ciphertext& a, const Ciphertext& b, const Ciphertext& c,
+                                  const Ciphertext& d, const EvalKeys& keys, const Ciphertext* add = nullptr) const;
     Ciphertext rotate(const Ciphertext& ct, u32 k, const EvalKeys& keys) const;
     Ciphertext conjugate(const Ciphertext& ct, const EvalKeys& keys) const;
     // Extension: sum_j mul_plain(cts[j], plains[j], plain_scale) in one
@@ -150,6 +159,13 @@ Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const s
 // BSGS shapes measured, see chebyshev.cpp). Results are identical either way.
 void set_eval_pipeline(bool on);
 bool eval_pipeline_enabled();
+// Lazy relinearisation in eval_chebyshev_bsgs (default on; TG_LAZY_RELIN=0 or
+// set_lazy_relin(false) restores one key switch per product): a node whose
+// remainder is itself a giant-step node, Q T_n + (Q' T_n' + R'), adds the two
+// degree-2 products before ONE relinearisation (Evaluator::mul2_relin_rescale).
+// oracle/bsgs_ref.py (lazy=) restates both orders over reference primitives.
+void set_lazy_relin(bool on);
+bool lazy_relin_enabled();
 // Which Chebyshev evaluator the threshold stages use.
 enum class PolyEval { ladder, bsgs };
 std::vector<double> power_to_chebyshev(const std::vector<double>& pow_coeffs);

@@ -23,10 +23,26 @@ Algorithm (depth = ceil(log2 d) + 1, the same level budget as the ladder):
   quotient Q at target * q_lp / scale(T_n) so Q * T_n rescales onto target.
   Without this the giant-step products drift from Delta by scale(T_n)/q per
   level and deep chains (config 5, degree 63) fail the 1e-4 scale check.
+
+Lazy relinearisation (LAZY_RELIN, the product's default): where the remainder
+of a node is itself a giant-step node, p = Q T_n + (Q' T_n' + R'), the two
+degree-2 products are added BEFORE relinearisation,
+      rescale( relinearize( mul(Q, T_n) + mul(Q', T_n') ) ) + R',
+with Q' evaluated at the scale that makes both tensors' scales equal
+(target * q_lp / scale(T_n')) and the second tensor dropped to the first's
+level by Evaluator::add's own level alignment: one key switch and one rescale
+instead of two of each. Every step is still a reference primitive
+(Evaluator::mul ckks.hpp:220-245, add :201-208, KeyContext::relinearize
+rlwe.hpp:601-620, rescale ckks.hpp:315-324).
 """
 from __future__ import annotations
 
 import math
+import os
+
+# module default (the product's: TG_LAZY_RELIN=0 switches both to one key
+# switch per product); eval_chebyshev_bsgs(..., lazy=...) overrides it
+LAZY_RELIN = os.environ.get("TG_LAZY_RELIN", "1") != "0"
 
 
 def _trim(c):
@@ -36,7 +52,8 @@ def _trim(c):
     return c
 
 
-def eval_chebyshev_bsgs(T, ev, x, coeffs, keys):
+def eval_chebyshev_bsgs(T, ev, x, coeffs, keys, lazy=None):
+    lazy = LAZY_RELIN if lazy is None else lazy
     c = _trim(coeffs)
     d = len(c) - 1
     if d == 0:
@@ -141,6 +158,17 @@ def eval_chebyshev_bsgs(T, ev, x, coeffs, keys):
             tn = get(n)
             lp = min(lq, tn.level())
             Q = rec(q, target * float(ev.ring().modulus(lp)) / tn.scale)
+            rt = _trim(r)
+            if lazy and len(rt) - 1 >= b:  # the remainder is a giant-step node too
+                n2, q2, r2 = split(rt)
+                lq2 = level_of(q2)
+                if lq2 is not None and min(lq2, get(n2).level()) >= lp:
+                    tn2 = get(n2)
+                    Q2 = rec(q2, target * float(ev.ring().modulus(lp)) / tn2.scale)
+                    R2 = rec(r2, target)
+                    both = ev.add(ev.mul(Q, tn), ev.mul(Q2, tn2))
+                    P = ev.rescale(ev.key_context().relinearize(both, keys.relin))
+                    return P if R2 is None else ev.add(P, R2)
         Rr = rec(r, target)
         if Q is None:
             return Rr
@@ -153,7 +181,7 @@ def eval_chebyshev_bsgs(T, ev, x, coeffs, keys):
     return out
 
 
-def threshold_plain_norm_bsgs(T, ev, ct_scores, ct_t, norm, chain, keys):
+def threshold_plain_norm_bsgs(T, ev, ct_scores, ct_t, norm, chain, keys, lazy=None):
     """eval_private_threshold_plain_norm (threshold.hpp:146-157) with every
     stage evaluated by eval_chebyshev_bsgs."""
     if ct_scores.level() < chain.levels_required():
@@ -163,5 +191,5 @@ def threshold_plain_norm_bsgs(T, ev, ct_scores, ct_t, norm, chain, keys):
     ql = ev.ring().modulus(diff.level())
     u = ev.rescale(ev.mul_scalar(diff, norm, float(ql)))
     for i in range(len(chain.stages)):
-        u = eval_chebyshev_bsgs(T, ev, u, chain.eval_coeffs(i), keys)
+        u = eval_chebyshev_bsgs(T, ev, u, chain.eval_coeffs(i), keys, lazy)
     return ev.add_scalar(u, 0.5)

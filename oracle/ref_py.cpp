@@ -273,6 +273,7 @@ PYBIND11_MODULE(tetris_ref, m) {
     py::class_<Evaluator>(m, "Evaluator")
         .def(py::init<const KeyContext&>(), py::keep_alive<1, 2>())
         .def("ring", &Evaluator::ring, py::return_value_policy::reference_internal)
+        .def("key_context", &Evaluator::key_context, py::return_value_policy::reference_internal)
         .def("add", &Evaluator::add, py::call_guard<py::gil_scoped_release>())
         .def("sub", &Evaluator::sub, py::call_guard<py::gil_scoped_release>())
         .def("mul", &Evaluator::mul, py::call_guard<py::gil_scoped_release>())

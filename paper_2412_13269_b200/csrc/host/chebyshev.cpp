@@ -6,7 +6,9 @@
 //                            (oracle/bsgs_ref.py over the reference's own
 //                            Evaluator primitives), same level budget,
 //                            7/11/16 instead of 11/20/47 relinearised products
-//                            for d = 15/27/63.
+//                            for d = 15/27/63; with lazy relinearisation
+//                            (default) one key switch fewer per node whose
+//                            remainder is a giant-step node too.
 // Every ladder step and every combination step runs as ONE fused residue pass
 // (tg_lincomb) after the relinearised product; scales and noise bounds follow
 // the reference's add_inplace / mul_scalar / sub_inplace / add_scalar /
@@ -60,6 +62,18 @@ bool eval_pipeline() {
         const char* e = std::getenv("TG_EVAL_PIPELINE");
         v = (e && e[0] == '1') ? 1 : 0;
         g_eval_pipeline.store(v);
+    }
+    return v != 0;
+}
+
+std::atomic<int> g_lazy_relin{-1};
+
+bool lazy_relin() {
+    int v = g_lazy_relin.load();
+    if (v < 0) {
+        const char* e = std::getenv("TG_LAZY_RELIN");
+        v = (e && e[0] == '0') ? 0 : 1;
+        g_lazy_relin.store(v);
     }
     return v != 0;
 }
@@ -250,6 +264,8 @@ std::vector<double> trimmed(const std::vector<double>& c) {
 
 void set_eval_pipeline(bool on) { g_eval_pipeline.store(on ? 1 : 0); }
 bool eval_pipeline_enabled() { return eval_pipeline(); }
+void set_lazy_relin(bool on) { g_lazy_relin.store(on ? 1 : 0); }
+bool lazy_relin_enabled() { return lazy_relin(); }
 
 Ciphertext eval_chebyshev(const Evaluator& ev, const Ciphertext& x, const std::vector<double>& cheb_coeffs,
                           const EvalKeys& keys) {
@@ -285,6 +301,7 @@ Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const s
     const int lb = int(std::ceil(std::log2(double(d + 1)) / 2.0));
     const std::size_t b = std::size_t(1) << lb;
     Ladder L(ev, x, keys);
+    const bool lazy = lazy_relin();
 
     auto base_terms = [&](const std::vector<double>& cs) {
         std::vector<std::size_t> ks;
@@ -356,6 +373,21 @@ Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const s
             const Ciphertext& tn = L.get(n);
             const int lp = std::min(lq, tn.level());
             Q = rec(q, target * double(L.R.modulus(u32(lp))) / tn.scale);
+            // lazy relinearisation: the remainder is a giant-step node too,
+            // Q T_n + (Q2 T_n2 + R2): both tensors at one scale and level, one
+            // key switch and one rescale for the pair (oracle/bsgs_ref.py)
+            const std::vector<double> rt = trimmed(r);
+            if (lazy && !L.eval && rt.size() - 1 >= b) {
+                std::vector<double> q2, r2;
+                const std::size_t n2 = split(rt, q2, r2);
+                const int lq2 = level_of(q2);
+                if (lq2 >= 0 && std::min(lq2, L.get(n2).level()) >= lp) {
+                    const Ciphertext& tn2 = L.get(n2);
+                    std::optional<Ciphertext> Q2 = rec(q2, target * double(L.R.modulus(u32(lp))) / tn2.scale);
+                    std::optional<Ciphertext> R2 = rec(r2, target);
+                    return ev.mul2_relin_rescale(*Q, L.get(n), *Q2, tn2, keys, R2 ? &*R2 : nullptr);
+                }
+            }
         }
         std::optional<Ciphertext> Rr = rec(r, target);
         if (!Q) return Rr;

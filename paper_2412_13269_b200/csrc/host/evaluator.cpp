@@ -378,6 +378,37 @@ Ciphertext Evaluator::mul_relin_rescale(const Ciphertext& a, const Ciphertext& b
     return out;
 }
 
+// rescale(relinearize(add(mul(a, b), mul(c, d)))) [+ add]: the reference's
+// primitives in that order (ckks.hpp:220-245, :201-208, rlwe.hpp:601-620,
+// ckks.hpp:315-324) with one key switch for both products.
+Ciphertext Evaluator::mul2_relin_rescale(const Ciphertext& a, const Ciphertext& b, const Ciphertext& c,
+                                         const Ciphertext& d, const EvalKeys& keys, const Ciphertext* add) const {
+    Ciphertext t1 = mul(a, b);
+    // mul(c, d)'s checks in mul's order
+    if (c.domain != d.domain) throw TetrisError("ckks", "domain tag mismatch in mul");
+    if (c.degree() != 1 || d.degree() != 1) throw TetrisError("ckks", "mul expects degree-1 operands");
+    if (c.batch != d.batch) throw TetrisError("ckks", "batch size mismatch in mul");
+    Ciphertext x = c, y = d;
+    align_levels(x, y);
+    if (x.level() == 0) throw TetrisError("ckks", "exhausted ciphertext: no level left to rescale");
+    Ciphertext sum;
+    if (x.level() >= t1.level() && x.form() == Form::coeff && y.form() == Form::coeff) {
+        // add() would drop mul(c, d) to t1's level (align_levels); every step of
+        // the tensor is row-wise, so the operands are dropped first instead:
+        // the same rows, without the dropped rows' products and transforms
+        x.drop_to_level(t1.level());
+        y.drop_to_level(t1.level());
+        Ciphertext t2 = mul(x, y);
+        check_scales_match(t1.scale, t2.scale);
+        t1.add_inplace(t2);  // both in eval form; relinearize brings c2 back
+        sum = std::move(t1);
+    } else {
+        sum = this->add(t1, mul(c, d));
+    }
+    Ciphertext r = ctx_->relinearize(sum, keys.relin);
+    return add ? rescale_add(r, *add) : rescale(r);
+}
+
 Ciphertext Evaluator::mul_relin_eval(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys) const {
     return ctx_->relinearize_eval(mul(a, b), keys.relin);
 }

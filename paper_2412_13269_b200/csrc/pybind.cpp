@@ -316,6 +316,14 @@ PYBIND11_MODULE(_tetris_b200, m) {
                const Ciphertext* add) { return ev.mul_relin_rescale(a, b, keys, add); },
             py::arg("a"), py::arg("b"), py::arg("keys"), py::arg("add") = nullptr, py::keep_alive<0, 1>(),
             py::call_guard<py::gil_scoped_release>())
+        .def(
+            "mul2_relin_rescale",
+            [](const Evaluator& ev, const Ciphertext& a, const Ciphertext& b, const Ciphertext& c,
+               const Ciphertext& d, const EvalKeys& keys,
+               const Ciphertext* add) { return ev.mul2_relin_rescale(a, b, c, d, keys, add); },
+            py::arg("a"), py::arg("b"), py::arg("c"), py::arg("d"), py::arg("keys"), py::arg("add") = nullptr,
+            py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
+        .def("key_context", &Evaluator::key_context, py::return_value_policy::reference_internal)
         .def("rotate", &Evaluator::rotate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("conjugate", &Evaluator::conjugate, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>())
         .def("mul_plain_sum", &Evaluator::mul_plain_sum, py::keep_alive<0, 1>(),
@@ -341,6 +349,8 @@ PYBIND11_MODULE(_tetris_b200, m) {
 
     m.def("eval_chebyshev", &eval_chebyshev, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>());
     m.def("set_eval_pipeline", &set_eval_pipeline);
+    m.def("set_lazy_relin", &set_lazy_relin);
+    m.def("lazy_relin_enabled", &lazy_relin_enabled);
     m.def("eval_pipeline_enabled", &eval_pipeline_enabled);
     m.def("eval_chebyshev_bsgs", &eval_chebyshev_bsgs, py::keep_alive<0, 1>(), py::call_guard<py::gil_scoped_release>());
     py::enum_<PolyEval>(m, "PolyEval").value("ladder", PolyEval::ladder).value("bsgs", PolyEval::bsgs);

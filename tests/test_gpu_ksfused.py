@@ -151,3 +151,39 @@ def test_mul_relin_rescale_matches_reference(G, R, gpu_available, N, batch):
                 yr.to_eval()
             want = r.ev.add(r.ev.rescale(r.ev.mul_relin(xs_r[i], ys_r[i], r.keys)), yr)
             assert_ct_equal(c, want, f"mul_relin_rescale {what} block {i}")
+
+
+@pytest.mark.parametrize("N,batch", [(1 << 16, 8), (1 << 14, 3), (1 << 16, 1)])
+def test_mul2_relin_rescale_matches_reference(G, R, gpu_available, N, batch):
+    """Evaluator::mul2_relin_rescale (lazy relinearisation of a giant-step
+    pair) on the fused key-switch path and as ciphertext batches:
+    rescale(relinearize(add(mul(a, b), mul(c, d)))) [+ add] of the reference
+    (ckks.hpp:220-245, :201-208, rlwe.hpp:601-620, ckks.hpp:315-324), with
+    the second product above the first's level (level-dropped operand views)
+    and at it."""
+    kw = dict(N=N, nq=7, K=3, group_size=3, seed=23, q_bits=50, sp_bits=50, h=192)
+    g, r = make_setup(G, **kw), make_setup(R, **kw)
+    top = g.ring.max_level()
+
+    def stack(T, cts):
+        return cts[0] if len(cts) == 1 else T.stack_ciphertexts(cts)
+
+    def unstack(T, ct):
+        return T.unstack_ciphertext(ct) if ct.batch > 1 else [ct]
+
+    for (la, lc, ld, ladd) in [(top - 1, top, top - 1, top - 3), (top, top, top, None), (3, 5, 4, 2)]:
+        lv = (la, la, lc, ld)
+        ops_g = [_cts(g, batch, l, 80 + 7 * i + l) for i, l in enumerate(lv)]
+        ops_r = [_cts(r, batch, l, 80 + 7 * i + l) for i, l in enumerate(lv)]
+        ad_g = ad_r = None
+        if ladd is not None:
+            ad_g, ad_r = _cts(g, batch, ladd, 99), _cts(r, batch, ladd, 99)
+        got = g.ev.mul2_relin_rescale(*(stack(G, o) for o in ops_g), g.keys, stack(G, ad_g) if ad_g else None)
+        for i, c in enumerate(unstack(G, got)):
+            a, b, cc, d = (o[i] for o in ops_r)
+            want = r.ev.rescale(r.ev.key_context().relinearize(r.ev.add(r.ev.mul(a, b), r.ev.mul(cc, d)),
+                                                               r.keys.relin))
+            if ad_r:
+                want = r.ev.add(want, ad_r[i])
+            assert_ct_equal(c, want, f"mul2_relin_rescale N={N} levels {lv} block {i}")
+            assert c.noise_bound == want.noise_bound
