@@ -249,12 +249,24 @@ int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const u
               const uint64_t* x1, const uint64_t* y0, const uint64_t* y1, int level,
               uint32_t npolys, void* stream);
 /* (p0 and p1 both NULL: only p2 = x1 y1 is formed; x0, y0 unused.) */
+/* Sum of two tensors, add(mul(x, y), mul(u, v)) (ckks.hpp:229-237 twice, then
+ * Ciphertext::add_inplace rlwe.hpp:300-305), in one pass: p0 = x0 y0 + u0 v0,
+ * p1 = x0 y1 + x1 y0 + u0 v1 + u1 v0, p2 = x1 y1 + u1 v1 (lazy
+ * relinearisation of a pair of products). u*, v* all NULL: tg_tensor. */
+int tg_tensor2(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const uint64_t* x0,
+               const uint64_t* x1, const uint64_t* y0, const uint64_t* y1, const uint64_t* u0,
+               const uint64_t* u1, const uint64_t* v0, const uint64_t* v1, int level, uint32_t npolys,
+               void* stream);
 /* The tensor's c2 = x1 y1 (eval form, written to c2_eval) and its inverse NTT
  * into c2 (coefficient form), npolys polys of level+1 rows: on all-FP64
  * rings the product is formed inside the first inverse phase (c2 read once
  * from HBM less); identical residues to tg_tensor + tg_ntt_inverse_oop. */
 int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
                          const uint64_t* y1, int level, uint32_t npolys, int* raw, void* stream);
+/* The same for c2 = x1 y1 + u1 v1 (u1, v1 NULL: one product). */
+int tg_tensor2_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
+                          const uint64_t* y1, const uint64_t* u1, const uint64_t* v1, int level,
+                          uint32_t npolys, int* raw, void* stream);
 /* raw (in/out, may be NULL): non-NULL lets the call leave c2 as the inverse
  * transform's raw doubles without the N^-1 factor (|v| <= 0.6q) when the
  * fused key switch can consume them; *raw reports whether it did (pass it on
@@ -384,6 +396,18 @@ int tg_relinearize_tensor_rescale_batch(tg_gadget* g, uint64_t* out, const uint6
                                         int level, const uint64_t* x0, const uint64_t* x1, const uint64_t* y0,
                                         const uint64_t* y1, uint32_t npolys, int c2_raw, const uint64_t* add,
                                         uint64_t add_stride, int out_level, void* stream);
+/* Lazy relinearisation of two products: rescale(relinearize(add(mul(x, y),
+ * mul(u, v)))) [+ add] (ckks.hpp:229-237, rlwe.hpp:300-305, :601-620,
+ * ckks.hpp:315-324) with ONE key switch: c2 = x1 y1 + u1 v1 (from
+ * tg_tensor2_c2_inverse), c0 / c1 of both tensors formed inside the fused
+ * key-switch core. u0, u1, v0, v1 (npolys polys of level+1 rows, eval form)
+ * all NULL: tg_relinearize_tensor_rescale_batch. */
+int tg_relinearize_tensor2_rescale_batch(tg_gadget* g, uint64_t* out, const uint64_t* c2,
+                                         const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits,
+                                         int level, const uint64_t* x0, const uint64_t* x1, const uint64_t* y0,
+                                         const uint64_t* y1, const uint64_t* u0, const uint64_t* u1,
+                                         const uint64_t* v0, const uint64_t* v1, uint32_t npolys, int c2_raw,
+                                         const uint64_t* add, uint64_t add_stride, int out_level, void* stream);
 
 #ifdef __cplusplus
 }

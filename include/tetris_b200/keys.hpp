@@ -159,8 +159,11 @@ public:
     // in the same ModDown pass (tg_relinearize_tensor_rescale_batch): parts of
     // level-1 (or out_level) rows; scale / noise_bound are the PRODUCT's, the
     // caller (Evaluator::mul_relin_rescale) applies rescale / add's metadata.
+    // u, v (both or neither): a second product of the same level and batch,
+    // added before the one relinearisation (tg_relinearize_tensor2_rescale_batch).
     Ciphertext relinearize_tensor_rescale(const Ciphertext& x, const Ciphertext& y, const SwitchingKey& rlk,
-                                          const Ciphertext* add, int out_level) const;
+                                          const Ciphertext* add, int out_level, const Ciphertext* u = nullptr,
+                                          const Ciphertext* v = nullptr) const;
     SwitchingKey galois_key_gen(const SecretKey& sk, u64 exponent, Rng& rng) const;
     Ciphertext apply_galois(const Ciphertext& ct, u64 exponent, const SwitchingKey& swk) const;
     // Hoisted automorphisms (Evaluator::apply_galois_many, ckks.hpp:338-367):

@@ -383,30 +383,87 @@ Ciphertext Evaluator::mul_relin_rescale(const Ciphertext& a, const Ciphertext& b
 // ckks.hpp:315-324) with one key switch for both products.
 Ciphertext Evaluator::mul2_relin_rescale(const Ciphertext& a, const Ciphertext& b, const Ciphertext& c,
                                          const Ciphertext& d, const EvalKeys& keys, const Ciphertext* add) const {
-    Ciphertext t1 = mul(a, b);
-    // mul(c, d)'s checks in mul's order
-    if (c.domain != d.domain) throw TetrisError("ckks", "domain tag mismatch in mul");
-    if (c.degree() != 1 || d.degree() != 1) throw TetrisError("ckks", "mul expects degree-1 operands");
-    if (c.batch != d.batch) throw TetrisError("ckks", "batch size mismatch in mul");
-    Ciphertext x = c, y = d;
-    align_levels(x, y);
-    if (x.level() == 0) throw TetrisError("ckks", "exhausted ciphertext: no level left to rescale");
-    Ciphertext sum;
-    if (x.level() >= t1.level() && x.form() == Form::coeff && y.form() == Form::coeff) {
-        // add() would drop mul(c, d) to t1's level (align_levels); every step of
-        // the tensor is row-wise, so the operands are dropped first instead:
-        // the same rows, without the dropped rows' products and transforms
-        x.drop_to_level(t1.level());
-        y.drop_to_level(t1.level());
-        Ciphertext t2 = mul(x, y);
-        check_scales_match(t1.scale, t2.scale);
-        t1.add_inplace(t2);  // both in eval form; relinearize brings c2 back
-        sum = std::move(t1);
-    } else {
-        sum = this->add(t1, mul(c, d));
+    // the reference's primitives one after the other (any ring, any levels)
+    auto composed = [&] {
+        Ciphertext t1 = mul(a, b);
+        if (c.domain != d.domain) throw TetrisError("ckks", "domain tag mismatch in mul");
+        if (c.degree() != 1 || d.degree() != 1) throw TetrisError("ckks", "mul expects degree-1 operands");
+        if (c.batch != d.batch) throw TetrisError("ckks", "batch size mismatch in mul");
+        Ciphertext x = c, y = d;
+        align_levels(x, y);
+        if (x.level() == 0) throw TetrisError("ckks", "exhausted ciphertext: no level left to rescale");
+        Ciphertext sum;
+        if (x.level() >= t1.level() && x.form() == Form::coeff && y.form() == Form::coeff) {
+            // add() would drop mul(c, d) to t1's level (align_levels); every step of
+            // the tensor is row-wise, so the operands are dropped first instead:
+            // the same rows, without the dropped rows' products and transforms
+            x.drop_to_level(t1.level());
+            y.drop_to_level(t1.level());
+            Ciphertext t2 = mul(x, y);
+            check_scales_match(t1.scale, t2.scale);
+            t1.add_inplace(t2);  // both in eval form; relinearize brings c2 back
+            sum = std::move(t1);
+        } else {
+            sum = this->add(t1, mul(c, d));
+        }
+        Ciphertext r = ctx_->relinearize(sum, keys.relin);
+        return add ? rescale_add(r, *add) : rescale(r);
+    };
+    static const bool off = [] {
+        const char* e = std::getenv("TG_RELIN_TENSOR");
+        const char* f = std::getenv("TG_FUSED_RESCALE");
+        const char* g = std::getenv("TG_LAZY_FUSED");
+        return (e && *e == '0') || (f && *f == '0') || (g && *g == '0');
+    }();
+    if (off) return composed();
+    // one-pass conditions (mul_relin_rescale's, for both products): same
+    // batch and domain, coefficient-form degree-1 operands without special
+    // rows, the second product not below the first's level, FP64 q rows
+    for (const Ciphertext* t : {&a, &b, &c, &d}) {
+        if (t->degree() != 1 || t->batch != a.batch || t->domain != a.domain || t->form() != Form::coeff)
+            return composed();
+        for (const auto& p : t->parts)
+            if (p.nspecial() != 0) return composed();
     }
-    Ciphertext r = ctx_->relinearize(sum, keys.relin);
-    return add ? rescale_add(r, *add) : rescale(r);
+    Ciphertext x = a, y = b, u = c, v = d;
+    align_levels(x, y);
+    align_levels(u, v);
+    const int lvl = x.level();
+    if (lvl == 0 || u.level() < lvl) return composed();
+    const RingParams& R = ring();
+    for (int r = 0; r <= lvl; ++r)
+        if (R.modulus(u32(r)) >= 1351079888211148ull) return composed();  // kFpMaxQ (tg_fp64.cuh)
+    if (add) {
+        if (add->form() != Form::coeff || add->degree() != 1 || add->batch != x.batch || add->domain != x.domain)
+            return composed();
+        for (const auto& p : add->parts)
+            if (p.nspecial() != 0) return composed();
+        if (!contiguous(add->parts, 0, add->parts.size()) && detail::uniform_stride(add->parts) == 0)
+            return composed();
+    }
+    // metadata of mul, mul, add, relinearize, rescale (, add) in that order
+    const double s1 = x.scale * y.scale, s2 = u.scale * v.scale;
+    const double n1 = x.noise_bound * y.scale + y.noise_bound * x.scale;
+    const double n2 = u.noise_bound * v.scale + v.noise_bound * u.scale;
+    check_scales_match(s1, s2);
+    const u64 ql = R.modulus(u32(lvl));
+    const double pscale = s1 / double(ql);
+    const double pnoise = ((n1 + n2) + ctx_->ks_noise_estimate()) / double(ql) + 1.0;
+    int out_level = lvl - 1;
+    if (add) {
+        out_level = std::min(lvl - 1, add->level());
+        check_scales_match(pscale, add->scale);
+    }
+    u.drop_to_level(lvl);  // add()'s alignment, applied to the operands (row-wise tensor)
+    v.drop_to_level(lvl);
+    x.to_eval();
+    y.to_eval();
+    u.to_eval();
+    v.to_eval();
+    Ciphertext out = ctx_->relinearize_tensor_rescale(x, y, keys.relin, add, out_level, &u, &v);
+    out.scale = pscale;
+    out.noise_bound = add ? pnoise + add->noise_bound : pnoise;
+    return out;
 }
 
 Ciphertext Evaluator::mul_relin_eval(const Ciphertext& a, const Ciphertext& b, const EvalKeys& keys) const {

@@ -286,9 +286,18 @@ int ntt_forward_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 np
 int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 npolys, cudaStream_t s,
                      bool raw = false);
 bool ntt_inverse_cols_raw_ok(const tg_context* ctx);
+// Second operand pair of a lazily relinearised sum of two products
+// (Evaluator::mul2_relin_rescale): eval-form parts u0, u1, v0, v1 laid out
+// like the first pair's; all null when there is one product.
+struct Tensor2 {
+    const u64* u0 = nullptr;
+    const u64* u1 = nullptr;
+    const u64* v0 = nullptr;
+    const u64* v1 = nullptr;
+};
 int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key, int level,
                     u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s,
-                    const u64* ty0 = nullptr, const u64* ty1 = nullptr);
+                    const u64* ty0 = nullptr, const u64* ty1 = nullptr, Tensor2 t2 = Tensor2{});
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {

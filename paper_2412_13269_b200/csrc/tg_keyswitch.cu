@@ -1165,7 +1165,7 @@ int ks_inner_batch(tg_gadget* g, u64* out0, u64* out1, const u64* digits, u32 nd
 int ks_fused_batch(tg_gadget* g, u64* out0, u64* out1, const u64* d, const u64* d_eval, u32 nd, u32 npolys,
                    const u64* key, int level, u64* scratch, cudaStream_t s, const u64* add0, const u64* add1,
                    bool eval_add, const u64* ty0 = nullptr, const u64* ty1 = nullptr, bool raw_in = false,
-                   const RescaleSpec* rs = nullptr) {
+                   const RescaleSpec* rs = nullptr, Tensor2 t2 = Tensor2{}) {
     tg_context* ctx = g->ctx;
     const DevRing& R = ctx->ring;
     const size_t words = size_t(level + 1 + R.K) * R.N;
@@ -1176,7 +1176,7 @@ int ks_fused_batch(tg_gadget* g, u64* out0, u64* out1, const u64* d, const u64* 
     const u32 own = (d_eval && !g->g.base2_bits) ? g->g.group_size : 0u;
     if (int rc = ks_fused_chunks(ctx, acc, digits, nd, npolys, key, level, own, eval_add ? add0 : nullptr,
                                  eval_add ? add1 : nullptr, pmod, s, eval_add ? ty0 : nullptr,
-                                 eval_add ? ty1 : nullptr))
+                                 eval_add ? ty1 : nullptr, eval_add ? t2 : Tensor2{}))
         return rc;
     // the accumulators' inverse column phase hands ModDown raw doubles
     // (its N^-1 folded into ModDown's constants) when both kernels allow it
@@ -1327,11 +1327,33 @@ extern "C" int tg_relinearize_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1
     return rc;
 }
 
+static bool tensor2_given(const Tensor2& t2, bool& bad) {
+    const int n = (t2.u0 != nullptr) + (t2.u1 != nullptr) + (t2.v0 != nullptr) + (t2.v1 != nullptr);
+    bad = n != 0 && n != 4;
+    return n == 4;
+}
+
+static int relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* c2,
+                                    const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits, int level,
+                                    const uint64_t* x0, const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
+                                    const Tensor2& t2, uint32_t npolys, int c2_raw, void* stream);
+
 extern "C" int tg_relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* c2,
                                            const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits,
                                            int level, const uint64_t* x0, const uint64_t* x1, const uint64_t* y0,
                                            const uint64_t* y1, uint32_t npolys, int c2_raw, void* stream) {
+    return relinearize_tensor_batch(g, out0, out1, c2, c2_eval, key, key_digits, level, x0, x1, y0, y1, Tensor2{},
+                                    npolys, c2_raw, stream);
+}
+
+static int relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1, const uint64_t* c2,
+                                    const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits, int level,
+                                    const uint64_t* x0, const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
+                                    const Tensor2& t2, uint32_t npolys, int c2_raw, void* stream) {
     if (int rc = check_ks(g, level)) return rc;
+    bool bad = false;
+    const bool two = tensor2_given(t2, bad);
+    if (bad) return fail(TG_E_ARG, "[rlwe] the second product needs all four operand parts");
     if (npolys == 0) return TG_OK;
     if (!x0 || !x1 || !y0 || !y1) return fail(TG_E_ARG, "[rlwe] relinearize needs both operands' eval parts");
     if (c2_raw && !(c2_eval && ks_fused_ok(g->ctx)))
@@ -1347,7 +1369,9 @@ extern "C" int tg_relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_
         void* cc = nullptr;
         TG_CUDA(cudaMallocFromPoolAsync(&cc, 3 * qw * 8, ctx->pool, s));
         u64* c0 = static_cast<u64*>(cc);  // (c2 recomputed into the third slot, unused)
-        int rc = tg_tensor(ctx, c0, c0 + qw, c0 + 2 * qw, x0, x1, y0, y1, level, npolys, stream);
+        int rc = two ? tg_tensor2(ctx, c0, c0 + qw, c0 + 2 * qw, x0, x1, y0, y1, t2.u0, t2.u1, t2.v0, t2.v1, level,
+                                  npolys, stream)
+                     : tg_tensor(ctx, c0, c0 + qw, c0 + 2 * qw, x0, x1, y0, y1, level, npolys, stream);
         if (rc == TG_OK)
             rc = tg_relinearize_batch(g, out0, out1, c2, c2_eval, key, key_digits, level, c0, c0 + qw, npolys,
                                       stream);
@@ -1358,7 +1382,7 @@ extern "C" int tg_relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_
     void* scratch = nullptr;
     TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
     const int rc = ks_fused_batch(g, out0, out1, c2, c2_eval, nd, npolys, key, level, static_cast<u64*>(scratch), s,
-                                  x0, x1, true, y0, y1, c2_raw != 0);
+                                  x0, x1, true, y0, y1, c2_raw != 0, nullptr, t2);
     cudaFreeAsync(scratch, s);
     return rc;
 }
@@ -1369,7 +1393,25 @@ extern "C" int tg_relinearize_tensor_rescale_batch(tg_gadget* g, uint64_t* out, 
                                                    const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
                                                    uint32_t npolys, int c2_raw, const uint64_t* add,
                                                    uint64_t add_stride, int out_level, void* stream) {
+    return tg_relinearize_tensor2_rescale_batch(g, out, c2, c2_eval, key, key_digits, level, x0, x1, y0, y1, nullptr,
+                                                nullptr, nullptr, nullptr, npolys, c2_raw, add, add_stride,
+                                                out_level, stream);
+}
+
+extern "C" int tg_relinearize_tensor2_rescale_batch(tg_gadget* g, uint64_t* out, const uint64_t* c2,
+                                                    const uint64_t* c2_eval, const uint64_t* key,
+                                                    uint32_t key_digits, int level, const uint64_t* x0,
+                                                    const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
+                                                    const uint64_t* u0, const uint64_t* u1, const uint64_t* v0,
+                                                    const uint64_t* v1, uint32_t npolys, int c2_raw,
+                                                    const uint64_t* add, uint64_t add_stride, int out_level,
+                                                    void* stream) {
     if (int rc = check_ks(g, level)) return rc;
+    Tensor2 t2;
+    t2.u0 = u0, t2.u1 = u1, t2.v0 = v0, t2.v1 = v1;
+    bool bad = false;
+    tensor2_given(t2, bad);
+    if (bad) return fail(TG_E_ARG, "[rlwe] the second product needs all four operand parts");
     if (level < 1) return fail(TG_E_ARG, "[ring] cannot rescale at level 0");
     if (add && (out_level < 0 || out_level > level - 1)) return fail(TG_E_ARG, "[ring] rescale_add level out of range");
     if (npolys == 0) return TG_OK;
@@ -1394,8 +1436,8 @@ extern "C" int tg_relinearize_tensor_rescale_batch(tg_gadget* g, uint64_t* out, 
         void* tmp = nullptr;
         TG_CUDA(cudaMallocFromPoolAsync(&tmp, 2 * qw * 8, ctx->pool, s));
         u64* t = static_cast<u64*>(tmp);
-        int rc = tg_relinearize_tensor_batch(g, t, t + qw, c2, c2_eval, key, key_digits, level, x0, x1, y0, y1,
-                                             npolys, c2_raw, stream);
+        int rc = relinearize_tensor_batch(g, t, t + qw, c2, c2_eval, key, key_digits, level, x0, x1, y0, y1, t2,
+                                          npolys, c2_raw, stream);
         if (rc == TG_OK)
             rc = add ? tg_rescale_add(ctx, out, t, level, 2 * npolys, add, add_stride, out_level, stream)
                      : tg_rescale(ctx, out, t, level, 2 * npolys, stream);
@@ -1407,7 +1449,7 @@ extern "C" int tg_relinearize_tensor_rescale_batch(tg_gadget* g, uint64_t* out, 
     TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
     const RescaleSpec rs{add, add_stride, nout};
     const int rc = ks_fused_batch(g, out, out + size_t(npolys) * nout * R.N, c2, c2_eval, nd, npolys, key, level,
-                                  static_cast<u64*>(scratch), s, x0, x1, true, y0, y1, c2_raw != 0, &rs);
+                                  static_cast<u64*>(scratch), s, x0, x1, true, y0, y1, c2_raw != 0, &rs, t2);
     cudaFreeAsync(scratch, s);
     return rc;
 }

@@ -89,12 +89,15 @@ __device__ __forceinline__ void ks_chunks_int_body(const DevRing& R, u64* acc, c
 // ty0/ty1 (tensor mode, tg_relinearize_tensor_batch): add0/add1 are the
 // operand x's eval parts and ty0/ty1 y's; c0 = x0 y0, c1 = x0 y1 + x1 y0 are
 // formed here (exact FP64 products, |c0| < 0.81q, |c1| < 1.62q) and folded
-// as P * c like the eval-form addends.
+// as P * c like the eval-form addends. t2 (lazy relinearisation of two
+// products, tg_relinearize_tensor2_rescale_batch): c0 += u0 v0, c1 += u0 v1 +
+// u1 v0 (|c0| < 1.62q, |c1| < 3.24q, brought back to |.| <= q/2 + 1 by
+// fp_reduce before the P product).
 template <int E, bool MIXED = false>
 __global__ void __launch_bounds__(256, 2)
 kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb, const u64* key, int level,
              u32 logN1, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, u32 int_from,
-             const u64* ty0, const u64* ty1) {
+             const u64* ty0, const u64* ty1, const Tensor2 t2) {
     using Gm = WGeo<E>;
     if constexpr (MIXED) {
         if (blockIdx.y >= int_from) {
@@ -187,13 +190,31 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
                     const ulonglong2 x0 = c0[j], x1 = c1[j], y0 = d0[j], y1 = d1[j];
                     const double xa[2] = {u2d(x0.x), u2d(x0.y)}, xb[2] = {u2d(x1.x), u2d(x1.y)};
                     const double ya[2] = {u2d(y0.x), u2d(y0.y)}, yb[2] = {u2d(y1.x), u2d(y1.y)};
+                    double s0[2], s1[2];
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const double t0 = fp_mulmod_qi(xa[h], ya[h], qd, qi);
-                        const double t1 =
-                            __dadd_rn(fp_mulmod_qi(xa[h], yb[h], qd, qi), fp_mulmod_qi(xb[h], ya[h], qd, qi));
-                        a[0][2 * j + h] = __dadd_rn(a[0][2 * j + h], fp_mulmod(t0, pmd, pmq, qd));
-                        a[1][2 * j + h] = __dadd_rn(a[1][2 * j + h], fp_mulmod(t1, pmd, pmq, qd));
+                        s0[h] = fp_mulmod_qi(xa[h], ya[h], qd, qi);
+                        s1[h] = __dadd_rn(fp_mulmod_qi(xa[h], yb[h], qd, qi), fp_mulmod_qi(xb[h], ya[h], qd, qi));
+                    }
+                    if (t2.u0) {  // + the second product's c0 / c1
+                        const ulonglong2 u0 = reinterpret_cast<const ulonglong2*>(t2.u0 + po)[j];
+                        const ulonglong2 u1 = reinterpret_cast<const ulonglong2*>(t2.u1 + po)[j];
+                        const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(t2.v0 + po)[j];
+                        const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(t2.v1 + po)[j];
+                        const double ua[2] = {u2d(u0.x), u2d(u0.y)}, ub[2] = {u2d(u1.x), u2d(u1.y)};
+                        const double va[2] = {u2d(v0.x), u2d(v0.y)}, vb[2] = {u2d(v1.x), u2d(v1.y)};
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            s0[h] = fp_reduce(__dadd_rn(s0[h], fp_mulmod_qi(ua[h], va[h], qd, qi)), qd, qi);
+                            s1[h] = fp_reduce(__dadd_rn(s1[h], __dadd_rn(fp_mulmod_qi(ua[h], vb[h], qd, qi),
+                                                                         fp_mulmod_qi(ub[h], va[h], qd, qi))),
+                                              qd, qi);
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        a[0][2 * j + h] = __dadd_rn(a[0][2 * j + h], fp_mulmod(s0[h], pmd, pmq, qd));
+                        a[1][2 * j + h] = __dadd_rn(a[1][2 * j + h], fp_mulmod(s1[h], pmd, pmq, qd));
                     }
                 }
             } else {

@@ -205,7 +205,7 @@ k_inv_cols(DevRing R, u64* __restrict__ data, u32 row_base, u32 rows_per_poly, i
 template <int E1, int E2>
 void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key,
                      int level, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s,
-                     bool all_fp, const u64* ty0, const u64* ty1) {
+                     bool all_fp, const u64* ty0, const u64* ty1, const Tensor2& t2) {
     static const bool attr = [] {
         cudaFuncSetAttribute(kw_ks_chunks<E2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ks_chunk_smem<E2>()));
         return true;
@@ -228,7 +228,7 @@ void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32
     if (all_fp) {
         kw_ks_chunks<E2><<<grid, 256, ks_chunk_smem<E2>(), s>>>(R, acc, digits, nd, npolys, ppb, key, level,
                                                                  WGeo<E1>::LOGM, own_gs, add0, add1, pmod, rows,
-                                                                 ty0, ty1);
+                                                                 ty0, ty1, t2);
         return;
     }
     static const bool attr_m = [] {
@@ -239,7 +239,7 @@ void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32
     (void)attr_m;
     kw_ks_chunks<E2, true><<<grid, 256, ks_chunk_smem<E2>(), s>>>(R, acc, digits, nd, npolys, ppb, key, level,
                                                                    WGeo<E1>::LOGM, own_gs, add0, add1, pmod,
-                                                                   u32(level) + 1, ty0, ty1);
+                                                                   u32(level) + 1, ty0, ty1, t2);
 }
 
 // every modulus on the FP64 path and no integer-row knob: column-pair kernels
@@ -316,7 +316,9 @@ int ntt_inverse_cols(tg_context* ctx, u64* data, int level, int nspecial, u32 np
 
 int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key, int level,
                     u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s, const u64* ty0,
-                    const u64* ty1) {
+                    const u64* ty1, Tensor2 t2) {
+    if (t2.u0 && !(ty0 && ty1 && t2.u1 && t2.v0 && t2.v1))
+        return fail(TG_E_ARG, "[rlwe] a second product needs the first pair and all four of its parts");
     const DevRing& R = ctx->ring;
     const double rows = double(level + 1 + R.K);
     // algorithmic FP64 work: the chunk-phase butterflies of every transformed
@@ -329,20 +331,21 @@ int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 np
     const double bfly = double(R.N) / 2 * l2 * 8, own_rows = own_gs ? double(level + 1) : 0.0;
     const double fp64_ops =
         npolys * ((rows * nd - own_rows) * bfly + rows * nd * 2.0 * R.N * 7 + rows * 2 * bfly +
-                  (add0 ? 2.0 * (level + 1) * R.N * 7 : 0.0) + (ty0 ? 3.0 * (level + 1) * R.N * 6.5 : 0.0));
+                  (add0 ? 2.0 * (level + 1) * R.N * 7 : 0.0) + (ty0 ? 3.0 * (level + 1) * R.N * 6.5 : 0.0) +
+                  (t2.u0 ? 3.0 * (level + 1) * R.N * 8.5 : 0.0));
     // algorithmic: digits (phase-1 form) read, key once per batch, P*c addends, accumulators written
     ProfScope prof(ctx, TG_OP_KS_FUSED,
                    8.0 * R.N * (rows * (npolys * (nd + 2.0) + 2.0 * nd) +
-                                (add0 ? (ty0 ? 4.0 : 2.0) * npolys * (level + 1) : 0.0)),
+                                (add0 ? (t2.u0 ? 8.0 : ty0 ? 4.0 : 2.0) * npolys * (level + 1) : 0.0)),
                    s, 1, fp64_ops);
     bool all_fp = true;
     for (u64 q : ctx->h_q) all_fp &= q < kFpMaxQ;
     if (R.logN == 16)
-        launch_ks_fused<8, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp, ty0, ty1);
+        launch_ks_fused<8, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp, ty0, ty1, t2);
     else if (R.logN == 15)
-        launch_ks_fused<4, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp, ty0, ty1);
+        launch_ks_fused<4, 8>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp, ty0, ty1, t2);
     else
-        launch_ks_fused<4, 4>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp, ty0, ty1);
+        launch_ks_fused<4, 4>(R, ctx->sms, acc, digits, nd, npolys, key, level, own_gs, add0, add1, pmod, s, all_fp, ty0, ty1, t2);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -437,7 +440,14 @@ using namespace tg;
 
 extern "C" int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
                                     const uint64_t* y1, int level, uint32_t npolys, int* raw, void* stream) {
+    return tg_tensor2_c2_inverse(ctx, c2, c2_eval, x1, y1, nullptr, nullptr, level, npolys, raw, stream);
+}
+
+extern "C" int tg_tensor2_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
+                                     const uint64_t* y1, const uint64_t* u1, const uint64_t* v1, int level,
+                                     uint32_t npolys, int* raw, void* stream) {
     if (raw) *raw = 0;
+    if ((u1 == nullptr) != (v1 == nullptr)) return fail(TG_E_ARG, "[ckks] the second product needs both operands");
     if (!ctx) return fail(TG_E_ARG, "[ring] null context");
     if (level < 0 || u32(level) >= ctx->ring.q_count) return fail(TG_E_ARG, "[ring] poly level out of range");
     if (npolys == 0) return TG_OK;
@@ -452,7 +462,8 @@ extern "C" int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_
     // the fused chunk phase needs every row on the FP64 path, a warp plan and
     // the unstaged chunk kernel; otherwise the two separate passes
     if (off || NTT_CHUNK_STAGE || !ntt_pair_ok(ctx) || !warp_plan(R.logN, e1, e2) || npolys > 65535) {
-        if (int rc = tg_tensor(ctx, nullptr, nullptr, c2_eval, x1, x1, y1, y1, level, npolys, stream)) return rc;
+        if (int rc = tg_tensor2(ctx, nullptr, nullptr, c2_eval, x1, x1, y1, y1, u1, u1, v1, v1, level, npolys, stream))
+            return rc;
         return tg_ntt_inverse_oop(ctx, c2, c2_eval, level, 0, npolys, stream);
     }
     // raw output (the inverse column phase's doubles, no N^-1: ModUp folds it
@@ -465,11 +476,12 @@ extern "C" int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_
     const bool out_raw = raw && !raw_off && ntt_inverse_cols_raw_ok(ctx) && ks_fused_ok(ctx);
     {
         const size_t words = size_t(level + 1) * R.N * npolys;
-        ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * words + 24.0 * words, s, 2);  // + the tensor's 2 reads, 1 write
+        // + the tensor's 2 (4) reads, 1 write
+        ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * words + (u1 ? 40.0 : 24.0) * words, s, 2);
         const bool pair = true;
-        if (e1 == 8) launch_inv_tensor_w<8, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, out_raw);
-        else if (e2 == 8) launch_inv_tensor_w<4, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair);
-        else launch_inv_tensor_w<4, 4>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair);
+        if (e1 == 8) launch_inv_tensor_w<8, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, out_raw, u1, v1);
+        else if (e2 == 8) launch_inv_tensor_w<4, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, false, u1, v1);
+        else launch_inv_tensor_w<4, 4>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, false, u1, v1);
     }
     if (raw) *raw = (out_raw && e1 == 8) ? 1 : 0;
     TG_LAUNCH_CHECK();

@@ -799,11 +799,14 @@ kw_fwd_chunks(DevRing R, u64* data, u32 rpp, u32 npolys, u32 ppb, int level, u32
 // Tensor mode (tx != nullptr; FP64 rows, unstaged path): the source chunk is
 // the product tx * ty (Evaluator::mul's c2 = x1 y1, eval form, ckks.hpp:236),
 // written to c2e (ModUp's own-group rows) and transformed straight away --
-// c2 makes one trip through HBM instead of two (tg_tensor_c2_inverse).
+// c2 makes one trip through HBM instead of two (tg_tensor_c2_inverse). With a
+// second pair (tu, tv: lazy relinearisation of two products) the chunk is
+// tx * ty + tu * tv.
 template <int E>
 __global__ void __launch_bounds__(256, NTT_CHUNK_MIN_BLOCKS)
 kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, int level, u32 logN1,
-              u32 row0, const u64* tx = nullptr, const u64* ty = nullptr, u64* c2e = nullptr) {
+              u32 row0, const u64* tx = nullptr, const u64* ty = nullptr, u64* c2e = nullptr,
+              const u64* tu = nullptr, const u64* tv = nullptr) {
     using Gm = WGeo<E>;
     // row r of every poly (rows [row0, row0 + gridDim.y) are transformed)
     const u32 r = row0 + blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
@@ -882,8 +885,19 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
             u64 yv[E];
             ld_vec<E>(t, tx + o, lane);
             ld_vec<E>(yv, ty + o, lane);
+            if (tu) {  // x1 y1 + u1 v1: |sum| < 1.62q
+                u64 uv[E], vv[E];
+                ld_vec<E>(uv, tu + o, lane);
+                ld_vec<E>(vv, tv + o, lane);
 #pragma unroll
-            for (int j = 0; j < E; ++j) t[j] = fp_canonical1(fp_mulmod_qi(u2d(t[j]), u2d(yv[j]), qd, qi), qd);
+                for (int j = 0; j < E; ++j)
+                    t[j] = fp_canonical(__dadd_rn(fp_mulmod_qi(u2d(t[j]), u2d(yv[j]), qd, qi),
+                                                  fp_mulmod_qi(u2d(uv[j]), u2d(vv[j]), qd, qi)),
+                                        qd);
+            } else {
+#pragma unroll
+                for (int j = 0; j < E; ++j) t[j] = fp_canonical1(fp_mulmod_qi(u2d(t[j]), u2d(yv[j]), qd, qi), qd);
+            }
             st_vec<E>(c2e + o, t, lane);
         };
         auto load = [&](u64 (&t)[E], u32 pp) {
@@ -1162,12 +1176,13 @@ void launch_fwd_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp,
 // rows per poly; every row FP64, unstaged chunk phase)
 template <int E1, int E2>
 void launch_inv_tensor_w(const DevRing& R, int sms, u64* data, u64* c2e, const u64* x1, const u64* y1, u32 npolys,
-                         int level, cudaStream_t s, bool pair, bool raw = false) {
+                         int level, cudaStream_t s, bool pair, bool raw = false, const u64* u1 = nullptr,
+                         const u64* v1 = nullptr) {
     set_smem_attrs<E1, E2>();
     const u32 M1 = 32 * E1, rpp = u32(level) + 1;
     const u32 p2 = polys_per_block(M1 / 8, rpp, npolys, sms);
     kw_inv_chunks<E2><<<dim3(M1 / 8, rpp, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
-        R, data, nullptr, rpp, npolys, p2, level, WGeo<E1>::LOGM, 0, x1, y1, c2e);
+        R, data, nullptr, rpp, npolys, p2, level, WGeo<E1>::LOGM, 0, x1, y1, c2e, u1, v1);
     launch_inv_cols_any<E1, E2>(R, sms, data, rpp, npolys, level, s, 0, rpp, pair, raw);
 }
 

@@ -335,6 +335,47 @@ __global__ void k_tensor(DevRing R, Shape S, u64* p0, u64* p1, u64* p2, const u6
     }
 }
 
+// Sum of two tensors (lazy relinearisation, Evaluator::mul2_relin_rescale:
+// add(mul(x, y), mul(u, v)), ckks.hpp:229-237 twice then :201-208) in one
+// pass; p0 / p1 null: only c2 = x1 y1 + u1 v1.
+__global__ void k_tensor2(DevRing R, Shape S, u64* p0, u64* p1, u64* p2, const u64* x0, const u64* x1,
+                          const u64* y0, const u64* y1, const u64* u0, const u64* u1, const u64* v0,
+                          const u64* v1) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < S.words; i += u64(gridDim.x) * blockDim.x) {
+        const u32 m = row_mod(R, S, i);
+        const u64 q = R.q[m], rl = R.ratio[2 * m], rh = R.ratio[2 * m + 1];
+        const u64 a1 = x1[i], b1 = y1[i], c1 = u1[i], d1 = v1[i];
+        if (q < kFpMaxQ) {  // exact FP64 products (|r| < 0.81q each), sums < 3.24q < 2^53
+            const double qd = R.qd[4 * m], qi = R.qd[4 * m + 1];
+            const double da1 = u2d(a1), db1 = u2d(b1), dc1 = u2d(c1), dd1 = u2d(d1);
+            p2[i] = fp_canonical(__dadd_rn(fp_mulmod_qi(da1, db1, qd, qi), fp_mulmod_qi(dc1, dd1, qd, qi)), qd);
+            if (!p0) continue;
+            const double da0 = u2d(x0[i]), db0 = u2d(y0[i]), dc0 = u2d(u0[i]), dd0 = u2d(v0[i]);
+            p0[i] = fp_canonical(__dadd_rn(fp_mulmod_qi(da0, db0, qd, qi), fp_mulmod_qi(dc0, dd0, qd, qi)), qd);
+            const double s1 = __dadd_rn(__dadd_rn(fp_mulmod_qi(da0, db1, qd, qi), fp_mulmod_qi(da1, db0, qd, qi)),
+                                        __dadd_rn(fp_mulmod_qi(dc0, dd1, qd, qi), fp_mulmod_qi(dc1, dd0, qd, qi)));
+            p1[i] = fp_canonical(fp_reduce(s1, qd, qi), qd);
+            continue;
+        }
+        U128 acc{0, 0};  // 128-bit lazy sums (< 2^126), one reduction each
+        mac128(acc, a1, b1);
+        mac128(acc, c1, d1);
+        p2[i] = barrett128(acc.lo, acc.hi, q, rl, rh);
+        if (!p0) continue;
+        const u64 a0 = x0[i], b0 = y0[i], c0 = u0[i], d0 = v0[i];
+        acc = U128{0, 0};
+        mac128(acc, a0, b0);
+        mac128(acc, c0, d0);
+        p0[i] = barrett128(acc.lo, acc.hi, q, rl, rh);
+        acc = U128{0, 0};
+        mac128(acc, a0, b1);
+        mac128(acc, a1, b0);
+        mac128(acc, c0, d1);
+        mac128(acc, c1, d0);
+        p1[i] = barrett128(acc.lo, acc.hi, q, rl, rh);
+    }
+}
+
 // c2 = x1 y1 only (relinearisation through the fused key switch forms c0 and
 // c1 from the operands inside the key-switch core: tg_relinearize_tensor_batch)
 __global__ void k_tensor_c2(DevRing R, Shape S, u64* p2, const u64* x1, const u64* y1) {
@@ -624,6 +665,25 @@ extern "C" int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* 
     }
     PROF(TG_OP_TENSOR, 56 * S.words);
     k_tensor<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, p0, p1, p2, x0, x1, y0, y1);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_tensor2(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* p2, const uint64_t* x0,
+                          const uint64_t* x1, const uint64_t* y0, const uint64_t* y1, const uint64_t* u0,
+                          const uint64_t* u1, const uint64_t* v0, const uint64_t* v1, int level, uint32_t npolys,
+                          void* stream) {
+    if (!u0 && !u1 && !v0 && !v1) return tg_tensor(ctx, p0, p1, p2, x0, x1, y0, y1, level, npolys, stream);
+    if (int rc = check_shape(ctx, level, 0)) return rc;
+    if (npolys == 0) return TG_OK;
+    if (!p2 || (p0 == nullptr) != (p1 == nullptr)) return fail(TG_E_ARG, "[ckks] tensor2: p2 and both or none of p0 / p1");
+    if (!x1 || !y1 || !u1 || !v1 || (p0 && (!x0 || !y0 || !u0 || !v0)))
+        return fail(TG_E_ARG, "[ckks] tensor2: missing operand part");
+    DeviceGuard guard(ctx->device);
+    Shape S = shape_of(ctx, level, 0, npolys);
+    PROF(TG_OP_TENSOR, (p0 ? 88 : 40) * S.words);
+    k_tensor2<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, p0, p1, p2, x0, x1, y0, y1, u0, u1,
+                                                                     v0, v1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
