@@ -396,6 +396,22 @@ int tg_relinearize_tensor_rescale_batch(tg_gadget* g, uint64_t* out, const uint6
                                         int level, const uint64_t* x0, const uint64_t* x1, const uint64_t* y0,
                                         const uint64_t* y1, uint32_t npolys, int c2_raw, const uint64_t* add,
                                         uint64_t add_stride, int out_level, void* stream);
+/* mul_relin followed by the Chebyshev ladder step of eval_chebyshev
+ * (ckks.hpp:532-555: T_k = rescale(2 T_a T_b - mul_scalar(T_{b-a}, 1, ratio))
+ * or rescale(add_scalar(2 T_a^2, -1))): out = rescale_round( 2 relinearize(x
+ * (x) y) - sub_coef[r] * sub (+ add_const[r] at coefficient 0 of the part-0
+ * polys) ), 2*npolys polys of `level` rows. sub: coefficient-form ciphertext
+ * batch (poly p of the 2*npolys at sub + p*sub_stride words, >= level+1 rows)
+ * with its per-row multipliers sub_coef (host, level+1 words), or both NULL;
+ * add_const: host, level+1 words, or NULL. Large batches on all-FP64 rings
+ * apply the step inside ModDown (the product never reaches HBM); identical
+ * residues to tg_relinearize_tensor_batch + tg_lincomb_batch(rescale). */
+int tg_relinearize_tensor_ladder_batch(tg_gadget* g, uint64_t* out, const uint64_t* c2,
+                                       const uint64_t* c2_eval, const uint64_t* key, uint32_t key_digits,
+                                       int level, const uint64_t* x0, const uint64_t* x1, const uint64_t* y0,
+                                       const uint64_t* y1, uint32_t npolys, int c2_raw, const uint64_t* sub,
+                                       uint64_t sub_stride, const uint64_t* sub_coef,
+                                       const uint64_t* add_const, void* stream);
 /* Lazy relinearisation of two products: rescale(relinearize(add(mul(x, y),
  * mul(u, v)))) [+ add] (ckks.hpp:229-237, rlwe.hpp:300-305, :601-620,
  * ckks.hpp:315-324) with ONE key switch: c2 = x1 y1 + u1 v1 (from

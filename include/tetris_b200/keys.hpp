@@ -159,6 +159,15 @@ public:
     // in the same ModDown pass (tg_relinearize_tensor_rescale_batch): parts of
     // level-1 (or out_level) rows; scale / noise_bound are the PRODUCT's, the
     // caller (Evaluator::mul_relin_rescale) applies rescale / add's metadata.
+    // relinearize_tensor followed by the Chebyshev ladder step
+    // (ckks.hpp:532-555) in the same ModDown pass
+    // (tg_relinearize_tensor_ladder_batch): parts of level-1 rows holding
+    // rescale(2 prod - sub_coef * sub (+ add_const at coefficient 0 of part
+    // 0)); sub (coefficient form, level >= x's, uniformly strided parts) may
+    // be null. Metadata is the PRODUCT's; the caller applies the step's.
+    Ciphertext relinearize_tensor_ladder(const Ciphertext& x, const Ciphertext& y, const SwitchingKey& rlk,
+                                         const Ciphertext* sub, const std::vector<u64>& sub_coef,
+                                         const std::vector<u64>& add_const) const;
     // u, v (both or neither): a second product of the same level and batch,
     // added before the one relinearisation (tg_relinearize_tensor2_rescale_batch).
     Ciphertext relinearize_tensor_rescale(const Ciphertext& x, const Ciphertext& y, const SwitchingKey& rlk,

@@ -141,12 +141,70 @@ struct Ladder {
         return c;
     }
 
+    // The product and its ladder step in one ModDown pass
+    // (KeyContext::relinearize_tensor_ladder): coefficient-form degree-1
+    // operands of one batch and domain, FP64-eligible q rows.
+    bool fused_ladder_ok(const Ciphertext& ta, const Ciphertext& tb) const {
+        static const bool off = [] {
+            const char* e = std::getenv("TG_RELIN_TENSOR");
+            const char* f = std::getenv("TG_FUSED_LADDER");
+            return (e && *e == '0') || (f && *f == '0');
+        }();
+        if (off || ta.domain != tb.domain || ta.degree() != 1 || tb.degree() != 1 || ta.batch != tb.batch) return false;
+        const int lvl = std::min(ta.level(), tb.level());
+        if (lvl < 1 || lvl + 1 > 32) return false;
+        for (const Ciphertext* t : {&ta, &tb})
+            for (const auto& p : t->parts)
+                if (p.nspecial() != 0) return false;
+        for (int r = 0; r <= lvl; ++r)
+            if (R.modulus(u32(r)) >= 1351079888211148ull) return false;  // kFpMaxQ (tg_fp64.cuh)
+        return true;
+    }
+    // mul_relin, add_inplace, [mul_scalar, sub_inplace | add_scalar], rescale
+    // (ckks.hpp:532-555): the same checks and metadata in the same order
+    Ciphertext fused_step(const Ciphertext& ta, const Ciphertext& tb, const Ciphertext* tc) {
+        Ciphertext x = ta, y = tb;
+        ev.align_levels(x, y);
+        const int lvl = x.level();
+        const double pscale = x.scale * y.scale;
+        const double pnoise = (x.noise_bound * y.scale + y.noise_bound * x.scale) + ev.key_context().ks_noise_estimate();
+        const double two_noise = pnoise + pnoise;
+        const u64 ql = R.modulus(u32(lvl));
+        std::vector<u64> coef, add;
+        Ciphertext tc0;
+        double noise;
+        if (!tc) {
+            add.resize(lvl + 1);
+            for (int r = 0; r <= lvl; ++r) add[r] = Evaluator::scaled_residue(-1.0 * pscale, R.modulus(u32(r)));
+            noise = two_noise / double(ql) + 1.0;
+        } else {
+            tc0 = *tc;
+            tc0.to_coeff();
+            const double ratio = pscale / tc0.scale;
+            if (std::abs(1.0) * ratio >= 9.0e18)
+                throw TetrisError("ckks", "scalar multiplier exceeds the integer range");
+            const i64 v = round_half_away(1.0 * ratio);
+            const double tc_scale = tc0.scale * ratio;
+            Evaluator::check_scales_match(tc_scale, pscale);
+            coef.resize(lvl + 1);
+            for (int r = 0; r <= lvl; ++r) coef[r] = from_centered(v, R.modulus(u32(r)));
+            noise = (two_noise + tc0.noise_bound) / double(ql) + 1.0;
+        }
+        x.to_eval();
+        y.to_eval();
+        Ciphertext res = ev.key_context().relinearize_tensor_ladder(x, y, keys.relin, tc ? &tc0 : nullptr, coef, add);
+        res.noise_bound = noise;
+        res.scale = pscale / double(ql);
+        return res;
+    }
+
     const Ciphertext& get(std::size_t k) {
         auto hit = T.find(k);
         if (hit != T.end()) return hit->second;
         const std::size_t a = k / 2, b = k - a;
         const Ciphertext& ta = get(a);
         const Ciphertext& tb = get(b);
+        if (!eval && fused_ladder_ok(ta, tb)) return T.emplace(k, fused_step(ta, tb, a == b ? nullptr : &get(b - a))).first->second;
         Ciphertext prod = eval ? ev.mul_relin_eval(ta, tb, keys) : ev.mul_relin(ta, tb, keys);
         to_form(prod);
         const int lvl = prod.level();

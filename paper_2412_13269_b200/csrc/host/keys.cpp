@@ -582,6 +582,54 @@ Ciphertext KeyContext::relinearize_tensor_rescale(const Ciphertext& x, const Cip
     return out;
 }
 
+Ciphertext KeyContext::relinearize_tensor_ladder(const Ciphertext& x, const Ciphertext& y, const SwitchingKey& rlk,
+                                                 const Ciphertext* sub, const std::vector<u64>& sub_coef,
+                                                 const std::vector<u64>& add_const) const {
+    if (rlk.to_id != x.sk_id) throw TetrisError("rlwe", "relinearization key mismatch");
+    const u32 B = x.batch;
+    const int lvl = x.level();
+    if (lvl < 1) throw TetrisError("ckks", "cannot rescale at level 0");
+    std::vector<Poly> keep;
+    const u64* x0 = detail::group_data(x.parts, 0, B, keep);
+    const u64* x1 = detail::group_data(x.parts, B, B, keep);
+    const u64* y0 = detail::group_data(y.parts, 0, B, keep);
+    const u64* y1 = detail::group_data(y.parts, B, B, keep);
+    const u64* sp = nullptr;
+    std::size_t ss = 0;
+    if (sub) {
+        if (sub->form() != Form::coeff || sub->parts.size() != 2 * B || sub->level() < lvl ||
+            sub_coef.size() != std::size_t(lvl) + 1)
+            throw TetrisError("ckks", "ladder step: subtrahend shape");
+        ss = contiguous(sub->parts, 0, 2 * B) ? sub->parts[0].words() : detail::uniform_stride(sub->parts);
+        if (ss == 0) {  // parts of different blocks: gather them
+            sp = detail::group_data(sub->parts, 0, 2 * B, keep);
+            ss = sub->parts[0].words();
+        } else {
+            sp = sub->parts[0].data();
+        }
+    }
+    if (!add_const.empty() && add_const.size() != std::size_t(lvl) + 1)
+        throw TetrisError("ckks", "ladder step: constant per row");
+    std::vector<Poly> c2e = fresh_parts(*ring_, int(B), lvl, Form::eval);
+    std::vector<Poly> c2 = fresh_parts(*ring_, int(B), lvl, Form::coeff);
+    int raw = 1;
+    check_tg(tg_tensor_c2_inverse(ring_->dev(), const_cast<u64*>(c2[0].data()), const_cast<u64*>(c2e[0].data()), x1,
+                                  y1, lvl, B, &raw, ring_->stream()));
+    std::vector<Poly> dst = fresh_parts(*ring_, int(2 * B), lvl - 1, Form::coeff);
+    check_tg(tg_relinearize_tensor_ladder_batch(plan_->dev(), const_cast<u64*>(dst[0].data()), c2[0].data(),
+                                                c2e[0].data(), key_base(rlk), rlk.digits(), lvl, x0, x1, y0, y1, B, raw,
+                                                sp, ss, sub ? sub_coef.data() : nullptr,
+                                                add_const.empty() ? nullptr : add_const.data(), ring_->stream()));
+    Ciphertext out;
+    out.batch = B;
+    out.parts = std::move(dst);
+    out.scale = x.scale * y.scale;  // the product's metadata; the caller applies the ladder step's
+    out.domain = x.domain;
+    out.sk_id = x.sk_id;
+    out.noise_bound = (x.noise_bound * y.scale + y.noise_bound * x.scale) + ks_noise_estimate();
+    return out;
+}
+
 Ciphertext KeyContext::relinearize_eval(const Ciphertext& ct, const SwitchingKey& rlk) const {
     if (ct.degree() != 2) throw TetrisError("rlwe", "relinearize expects a degree-2 ciphertext");
     if (rlk.to_id != ct.sk_id) throw TetrisError("rlwe", "relinearization key mismatch");

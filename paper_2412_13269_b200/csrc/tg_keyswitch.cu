@@ -707,6 +707,22 @@ k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restric
     }
 }
 
+// The Chebyshev ladder step on the relinearised product, before its rescale
+// (ckks.hpp:532-555: rescale(2 prod - mul_scalar(T_c, 1, ratio)) or
+// rescale(add_scalar(2 prod, -1))): row r of the ModDown value v becomes
+// 2 v - m_r S_r (+ e_r at coefficient 0 of the part-0 polys). m_r, e_r are
+// canonical residues mod q_r; S is a coefficient-form ciphertext batch (poly
+// p at sub + p * stride). on = 0: plain rescale.
+constexpr int kLadderRows = 32;
+struct LadderPre {
+    int on = 0;
+    const u64* sub = nullptr;  // null: no subtrahend (the a == b step)
+    u64 stride = 0;
+    int has_e = 0;
+    double m[kLadderRows], mq[kLadderRows];
+    double e[kLadderRows];     // centred doubles of e_r
+};
+
 // FP64 ModDown (every special and q-chain prime below kFpMaxQ, tg_fp64.cuh):
 // y_s = centered([x_s (P/p_s)^-1]_{p_s}) exactly as doubles, then
 // out_r = x_r P^-1 + sum_s y_s (-(P/p_s) P^-1 mod q_r)  (mod q_r), which is
@@ -727,12 +743,13 @@ k_mod_down_v(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restric
 // first, centred exactly as rescale_round does (ring.hpp:493-518), and rows
 // 0..nout-1 leave as (v_r - x_l) q_l^-1 mod q_r (+ radd's row: Evaluator::add
 // of the rescaled product and y, k_rescale_fp's arithmetic) -- the ModDown
-// output never goes through HBM. addend must be null.
+// output never goes through HBM. addend must be null. pre (LadderPre): the
+// ladder step's linear part applied to every row before the rescale.
 template <int KMAX, bool RAW = false, bool RESCALE = false>
 __global__ void __launch_bounds__(256)
 k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restrict__ in, int level, u32 npolys,
               const u64* __restrict__ addend, u32 rows_per_group, const u64* __restrict__ radd = nullptr,
-              u64 astride = 0, u32 nout = 0) {
+              u64 astride = 0, u32 nout = 0, const LadderPre pre = LadderPre{}) {
     constexpr u32 K = KMAX;
     const u32 N = R.N, nq = R.q_count, lvl = u32(level);
     const u32 rin = lvl + 1 + K, rout = lvl + 1;
@@ -791,6 +808,19 @@ k_mod_down_fp(DevRing R, GadgetDev G, u64* __restrict__ out, const u64* __restri
                         }
                     }
                     v[cc] = fp_reduce(acc, q, qi);
+                }
+                if (pre.on) {  // 2 v - m_r S_r (+ e_r): |.| <= q + 2 + 0.58q + q/2 < 2^53
+                    double t0 = __dadd_rn(v[0], v[0]), t1 = __dadd_rn(v[1], v[1]);
+                    if (pre.sub) {
+                        const ulonglong2 sv =
+                            *reinterpret_cast<const ulonglong2*>(pre.sub + size_t(p) * pre.stride + size_t(r) * N + c0);
+                        const double m = pre.m[r], mq = pre.mq[r];
+                        t0 = __dsub_rn(t0, fp_mulmod(u2d(sv.x), m, mq, q));
+                        t1 = __dsub_rn(t1, fp_mulmod(u2d(sv.y), m, mq, q));
+                    }
+                    if (pre.has_e && c0 == 0 && 2 * p < npolys) t0 = __dadd_rn(t0, pre.e[r]);
+                    v[0] = fp_reduce(t0, q, qi);
+                    v[1] = fp_reduce(t1, q, qi);
                 }
             };
             const u64 ql = sq64[lvl], hl = ql >> 1;
@@ -1025,6 +1055,7 @@ struct RescaleSpec {
     const u64* radd;
     u64 astride;
     u32 nout;
+    const LadderPre* pre = nullptr;  // the ladder step before the rescale
 };
 
 template <int KMAX, bool RAW = false>
@@ -1036,7 +1067,8 @@ void launch_mod_down_fp(const DevRing& R, const GadgetDev& G, int sms, u64* out,
     const u32 blocks = u32(std::min<u64>((work + 255) / 256, u64(sms) * 8));
     if (rs) {  // every thread owns all rows of its coefficients
         k_mod_down_fp<KMAX, RAW, true><<<blocks, 256, smem, s>>>(R, G, out, in, level, npolys, nullptr, rout,
-                                                                 rs->radd, rs->astride, rs->nout);
+                                                                 rs->radd, rs->astride, rs->nout,
+                                                                 rs->pre ? *rs->pre : LadderPre{});
         return;
     }
     const u32 groups = row_groups(u64(blocks) * 256, rout, sms);
@@ -1050,7 +1082,8 @@ int mod_down(tg_gadget* g, u64* out, const u64* in, int level, u32 npolys, cudaS
     const DevRing& R = g->ctx->ring;
     ProfScope prof(g->ctx, TG_OP_MOD_DOWN,
                    8.0 * R.N * npolys *
-                       (rs ? (level + 1.0 + R.K + rs->nout * (rs->radd ? 2.0 : 1.0))
+                       (rs ? (level + 1.0 + R.K + rs->nout * (rs->radd ? 2.0 : 1.0) +
+                              ((rs->pre && rs->pre->sub) ? level + 1.0 : 0.0))
                            : (2.0 * (level + 1) + R.K + (addend ? level + 1 : 0))),
                    s);
     const GadgetDev& G = g->g;
@@ -1450,6 +1483,84 @@ extern "C" int tg_relinearize_tensor2_rescale_batch(tg_gadget* g, uint64_t* out,
     const RescaleSpec rs{add, add_stride, nout};
     const int rc = ks_fused_batch(g, out, out + size_t(npolys) * nout * R.N, c2, c2_eval, nd, npolys, key, level,
                                   static_cast<u64*>(scratch), s, x0, x1, true, y0, y1, c2_raw != 0, &rs, t2);
+    cudaFreeAsync(scratch, s);
+    return rc;
+}
+
+// mul_relin followed by the Chebyshev ladder step (ckks.hpp:532-555):
+// out = rescale( 2 relinearize(x (x) y) - sub_coef_r * sub (+ add_const_r at
+// coefficient 0 of the part-0 polys) ), `level` rows per poly. Large batches
+// on all-FP64 rings take the whole step inside ModDown (k_mod_down_fp RESCALE
+// with LadderPre); everything else relinearises, then tg_lincomb_batch.
+extern "C" int tg_relinearize_tensor_ladder_batch(tg_gadget* g, uint64_t* out, const uint64_t* c2,
+                                                  const uint64_t* c2_eval, const uint64_t* key,
+                                                  uint32_t key_digits, int level, const uint64_t* x0,
+                                                  const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
+                                                  uint32_t npolys, int c2_raw, const uint64_t* sub,
+                                                  uint64_t sub_stride, const uint64_t* sub_coef,
+                                                  const uint64_t* add_const, void* stream) {
+    if (int rc = check_ks(g, level)) return rc;
+    if (level < 1) return fail(TG_E_ARG, "[ring] cannot rescale at level 0");
+    if (npolys == 0) return TG_OK;
+    if (!x0 || !x1 || !y0 || !y1) return fail(TG_E_ARG, "[rlwe] relinearize needs both operands' eval parts");
+    if ((sub == nullptr) != (sub_coef == nullptr)) return fail(TG_E_ARG, "[ckks] ladder step: subtrahend without its constants");
+    tg_context* ctx = g->ctx;
+    const DevRing& R = ctx->ring;
+    const u32 nd = tg_gadget_digit_count(g, level);
+    if (nd > key_digits) return fail(TG_E_ARG, "[rlwe] switching key has too few digits");
+    if (nd > 15) return fail(TG_E_ARG, "[rlwe] batched key switch supports at most 15 digits");
+    DeviceGuard guard(ctx->device);
+    cudaStream_t s = as_stream(stream);
+    bool all_fp = true;
+    for (int r = 0; r <= level; ++r) all_fp &= ctx->h_q[r] < kFpMaxQ;
+    static const bool off = [] {
+        const char* e = getenv("TG_FUSED_LADDER");
+        return e && *e == '0';
+    }();
+    const bool fuse = !off && all_fp && ks_fused_ok(ctx) && g->g.fp_moddown && R.K <= 16 && fused_rescale_on() &&
+                      level + 1 <= kLadderRows && u64(npolys) * R.N >= u64(ctx->sms) * 512;
+    if (!fuse) {  // relinearise into scratch, then the ladder step as one lincomb pass
+        if (c2_raw && !ks_fused_ok(ctx))
+            return fail(TG_E_ARG, "[rlwe] a raw c2 needs its eval form and the fused key switch");
+        const size_t pw = size_t(level + 1) * R.N, qw = pw * npolys;
+        void* tmp = nullptr;
+        TG_CUDA(cudaMallocFromPoolAsync(&tmp, 2 * qw * 8, ctx->pool, s));
+        u64* t = static_cast<u64*>(tmp);
+        int rc = tg_relinearize_tensor_batch(g, t, t + qw, c2, c2_eval, key, key_digits, level, x0, x1, y0, y1,
+                                             npolys, c2_raw, stream);
+        if (rc == TG_OK) {
+            const uint64_t* terms[2] = {t, sub};
+            const uint64_t strides[2] = {pw, sub_stride};
+            std::vector<u64> coef(size_t(2) * (level + 1));
+            for (int r = 0; r <= level; ++r) {
+                coef[r] = 2 % ctx->h_q[r];
+                if (sub) coef[size_t(level + 1) + r] = (ctx->h_q[r] - sub_coef[r] % ctx->h_q[r]) % ctx->h_q[r];
+            }
+            rc = tg_lincomb_batch(ctx, out, sub ? 2 : 1, terms, strides, coef.data(), add_const, 0, level,
+                                  2 * npolys, npolys, 1, stream);
+        }
+        cudaFreeAsync(tmp, s);
+        return rc;
+    }
+    LadderPre pre;
+    pre.on = 1;
+    pre.sub = sub;
+    pre.stride = sub_stride;
+    pre.has_e = add_const ? 1 : 0;
+    for (int r = 0; r <= level; ++r) {
+        const u64 q = ctx->h_q[r];
+        const u64 m = sub ? sub_coef[r] % q : 0;
+        pre.m[r] = double(m);
+        pre.mq[r] = double(m) / double(q);
+        const u64 e = add_const ? add_const[r] % q : 0;
+        pre.e[r] = e > q / 2 ? -double(q - e) : double(e);
+    }
+    const size_t words = size_t(level + 1 + R.K) * R.N;
+    void* scratch = nullptr;
+    TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
+    const RescaleSpec rs{nullptr, 0, u32(level), &pre};
+    const int rc = ks_fused_batch(g, out, out + size_t(npolys) * level * R.N, c2, c2_eval, nd, npolys, key, level,
+                                  static_cast<u64*>(scratch), s, x0, x1, true, y0, y1, c2_raw != 0, &rs);
     cudaFreeAsync(scratch, s);
     return rc;
 }

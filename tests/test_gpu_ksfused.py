@@ -187,3 +187,27 @@ def test_mul2_relin_rescale_matches_reference(G, R, gpu_available, N, batch):
                 want = r.ev.add(want, ad_r[i])
             assert_ct_equal(c, want, f"mul2_relin_rescale N={N} levels {lv} block {i}")
             assert c.noise_bound == want.noise_bound
+
+
+@pytest.mark.parametrize("N,batch", [(1 << 16, 3), (1 << 14, 2), (1 << 14, 8)])
+def test_ladder_step_in_moddown_matches_reference(G, R, gpu_available, N, batch):
+    """The Chebyshev ladder (ckks.hpp:532-555) with each step's linear part
+    and rescale applied inside the product's ModDown
+    (tg_relinearize_tensor_ladder_batch: N=2^16 x 3 and 2^14 x 8 fill the GPU
+    and take the fused pass, 2^14 x 2 the relinearise-then-lincomb fallback):
+    eval_chebyshev of degree 6 (T_2 = 2 T_1^2 - 1, T_3 = 2 T_1 T_2 - T_1 with a
+    level-dropped T_1, T_4, T_5, T_6) on a ciphertext batch vs the unmodified
+    reference per block, residues and metadata."""
+    kw = dict(N=N, nq=7, K=3, group_size=3, seed=29, q_bits=50, sp_bits=50, h=192)
+    g, r = make_setup(G, **kw), make_setup(R, **kw)
+    from common import enc_slots
+    import numpy as np
+    coeffs = [0.11, -0.32, 0.27, 0.19, -0.08, 0.21, -0.13]
+    vals = [np.linspace(-0.9, 0.9, 64) * (1.0 - 0.1 * i) for i in range(batch)]
+    cg = [enc_slots(g, v, 2.0 ** 50, G.Rng(70 + i)) for i, v in enumerate(vals)]
+    cr = [enc_slots(r, v, 2.0 ** 50, R.Rng(70 + i)) for i, v in enumerate(vals)]
+    got = G.eval_chebyshev(g.ev, G.stack_ciphertexts(cg) if batch > 1 else cg[0], coeffs, g.keys)
+    for i, c in enumerate(G.unstack_ciphertext(got) if batch > 1 else [got]):
+        want = R.eval_chebyshev(r.ev, cr[i], coeffs, r.keys)
+        assert_ct_equal(c, want, f"ladder N={N} block {i}")
+        assert c.noise_bound == want.noise_bound
