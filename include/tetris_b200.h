@@ -242,6 +242,19 @@ int tg_lincomb_batch(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint
                      const uint64_t* part_strides, const uint64_t* coeffs, const uint64_t* add_per_row,
                      int add_all, int level, uint32_t nparts, uint32_t add_polys, int rescale, void* stream);
 
+/* nouts (2..4) rescaled combinations of the SAME nterms (1..4) terms in one
+ * pass: outs[o] = rescale_round( sum_t coeffs[o][t][r] * term_t (+
+ * add_per_row[o][r] at coefficient 0 of the first add_polys parts) ), `level`
+ * rows each (the combination steps of eval_chebyshev, ckks.hpp:556-578, for
+ * the base blocks of one BSGS polynomial, which share their baby steps).
+ * coeffs: nouts x nterms x (level+1) host words, add_per_row: nouts x
+ * (level+1) or NULL. Coefficient form, every row 0..level FP64-eligible
+ * (TG_E_ARG otherwise). Identical residues to nouts tg_lincomb_batch calls. */
+int tg_lincomb_multi(tg_context* ctx, uint32_t nouts, uint64_t* const* outs, uint32_t nterms,
+                     const uint64_t* const* terms, const uint64_t* part_strides, const uint64_t* coeffs,
+                     const uint64_t* add_per_row, int level, uint32_t nparts, uint32_t add_polys,
+                     void* stream);
+
 /* ---- CKKS products ------------------------------------------------------ */
 /* Evaluator::mul tensor step (ckks.hpp:229-237), eval form inputs:
  * p0 = x0*y0, p1 = x0*y1 + x1*y0, p2 = x1*y1. Outputs must not alias inputs. */

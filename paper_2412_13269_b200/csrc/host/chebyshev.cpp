@@ -25,6 +25,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
+#include <deque>
 #include <functional>
 #include <map>
 #include <optional>
@@ -76,6 +77,14 @@ bool lazy_relin() {
         g_lazy_relin.store(v);
     }
     return v != 0;
+}
+
+bool multi_base() {
+    static const bool off = [] {
+        const char* e = std::getenv("TG_MULTI_BASE");
+        return e && *e == '0';
+    }();
+    return !off;
 }
 
 std::vector<Poly> fused_lincomb(const RingParams& R, const std::vector<LinTerm>& terms,
@@ -244,48 +253,75 @@ struct Ladder {
 // rescale( sum_k mul_scalar(T_k, c_k, q_lvl) + add_scalar(c_0) ).
 // target > 0 (BSGS blocks): the combination scale becomes
 // q_lvl * target / scale(T_first), so the rescaled block lands on `target`.
-Ciphertext combine(Ladder& L, const Ciphertext& x, const std::vector<std::size_t>& ks, const std::vector<double>& cs,
-                   double c0, double target = 0.0) {
+// CombPlan: the checks, integer constants and metadata of one such step
+// (everything but the residue pass).
+struct CombPlan {
+    int lvl = 0;
+    std::vector<std::size_t> ks;
+    std::vector<LinTerm> terms;
+    std::vector<Ciphertext> conv;  // copies of terms in the ladder's form
+    std::vector<u64> add;
+    double acc_scale = 0, acc_noise = 0;
+};
+
+void plan_combine(CombPlan& P, Ladder& L, const Ciphertext& x, const std::vector<std::size_t>& ks,
+                  const std::vector<double>& cs, double c0, double target) {
     const RingParams& R = L.R;
     int lvl = x.level();
     for (std::size_t k : ks) lvl = std::min(lvl, L.get(k).level());
     double comb_scale = double(R.modulus(u32(lvl)));
     if (target > 0.0) comb_scale = comb_scale * (target / L.get(ks[0]).scale);
-    std::vector<LinTerm> terms;
-    std::vector<Ciphertext> conv;  // copies of terms in the ladder's form
-    conv.reserve(ks.size());
+    P.lvl = lvl;
+    P.ks = ks;
+    P.conv.reserve(ks.size());
     const Form f = L.eval ? Form::eval : Form::coeff;
-    double acc_scale = 0, acc_noise = 0;
     bool first = true;
     for (std::size_t k : ks) {
         const Ciphertext* tk = &L.get(k);
         if (tk->form() != f) {
-            conv.push_back(*tk);
-            L.to_form(conv.back());
-            tk = &conv.back();
+            P.conv.push_back(*tk);
+            L.to_form(P.conv.back());
+            tk = &P.conv.back();
         }
         const double c = cs[k];
         if (std::abs(c) * comb_scale >= 9.0e18) throw TetrisError("ckks", "scalar multiplier exceeds the integer range");
         const double term_scale = tk->scale * comb_scale;
         if (first) {
-            acc_scale = term_scale;
-            acc_noise = tk->noise_bound;
+            P.acc_scale = term_scale;
+            P.acc_noise = tk->noise_bound;
             first = false;
         } else {
-            Evaluator::check_scales_match(acc_scale, term_scale);
-            acc_noise += tk->noise_bound;
+            Evaluator::check_scales_match(P.acc_scale, term_scale);
+            P.acc_noise += tk->noise_bound;
         }
-        terms.push_back(LinTerm{tk, residues_of(R, round_half_away(c * comb_scale), lvl)});
+        P.terms.push_back(LinTerm{tk, residues_of(R, round_half_away(c * comb_scale), lvl)});
     }
-    std::vector<u64> add;
     if (c0 != 0.0) {
-        add.resize(lvl + 1);
-        for (int r = 0; r <= lvl; ++r) add[r] = Evaluator::scaled_residue(c0 * acc_scale, R.modulus(u32(r)));
+        P.add.resize(lvl + 1);
+        for (int r = 0; r <= lvl; ++r) P.add[r] = Evaluator::scaled_residue(c0 * P.acc_scale, R.modulus(u32(r)));
     }
     if (lvl == 0) throw TetrisError("ckks", "cannot rescale at level 0");
+}
+
+Ciphertext finish_combine(const CombPlan& P, const RingParams& R, const Ciphertext& x, std::vector<Poly> parts) {
+    const u64 ql = R.modulus(u32(P.lvl));
     Ciphertext out;
+    out.parts = std::move(parts);
+    out.batch = x.batch;
+    out.scale = P.acc_scale / double(ql);
+    out.noise_bound = P.acc_noise / double(ql) + 1.0;
+    out.domain = x.domain;
+    out.sk_id = x.sk_id;
+    return out;
+}
+
+Ciphertext run_combine(const CombPlan& P, Ladder& L, const Ciphertext& x) {
+    const RingParams& R = L.R;
+    const int lvl = P.lvl;
+    const std::vector<LinTerm>& terms = P.terms;
+    std::vector<Poly> parts;
     if (terms.size() <= TG_LINCOMB_MAX_TERMS) {
-        out.parts = fused_lincomb(R, terms, add, lvl, true);
+        parts = fused_lincomb(R, terms, P.add, lvl, true);
     } else {  // more terms than one pass holds: accumulate in chunks, rescale at the end
         Ciphertext partial;
         const std::vector<u64> one = residues_of(R, 1, lvl);
@@ -297,19 +333,70 @@ Ciphertext combine(Ladder& L, const Ciphertext& x, const std::vector<std::size_t
             const bool last = i + step >= terms.size();
             Ciphertext next;
             next.batch = x.batch;
-            next.parts = fused_lincomb(R, chunk, last ? add : std::vector<u64>{}, lvl, last);
-            next.scale = acc_scale;
+            next.parts = fused_lincomb(R, chunk, last ? P.add : std::vector<u64>{}, lvl, last);
+            next.scale = P.acc_scale;
             partial = std::move(next);
         }
-        out.parts = partial.parts;
+        parts = partial.parts;
     }
-    const u64 ql = R.modulus(u32(lvl));
-    out.batch = x.batch;
-    out.scale = acc_scale / double(ql);
-    out.noise_bound = acc_noise / double(ql) + 1.0;
-    out.domain = x.domain;
-    out.sk_id = x.sk_id;
-    return out;
+    return finish_combine(P, R, x, std::move(parts));
+}
+
+Ciphertext combine(Ladder& L, const Ciphertext& x, const std::vector<std::size_t>& ks, const std::vector<double>& cs,
+                   double c0, double target = 0.0) {
+    CombPlan P;
+    plan_combine(P, L, x, ks, cs, c0, target);
+    return run_combine(P, L, x);
+}
+
+// Several combination steps over the SAME terms at one level (the base blocks
+// of one BSGS polynomial) in one residue pass: each term word is read once
+// for all outputs (tg_lincomb_multi). Coefficient form, FP64-eligible rows,
+// 1..4 uniformly strided terms; 2..4 plans per call.
+bool multi_ok(const RingParams& R, const CombPlan& a, const CombPlan& b) {
+    if (a.lvl != b.lvl || a.ks != b.ks || a.terms.size() > 4 || !a.conv.empty() || !b.conv.empty()) return false;
+    for (int r = 0; r <= a.lvl; ++r)
+        if (R.modulus(u32(r)) >= 1351079888211148ull) return false;  // kFpMaxQ (tg_fp64.cuh)
+    for (const LinTerm& t : a.terms) {
+        const Ciphertext& c = *t.ct;
+        if (c.form() != Form::coeff || !uniform_parts(c.parts) || c.parts[0].nspecial() != 0) return false;
+    }
+    return true;
+}
+
+std::vector<Ciphertext> run_combine_multi(const std::vector<const CombPlan*>& plans, Ladder& L, const Ciphertext& x) {
+    const RingParams& R = L.R;
+    const CombPlan& P0 = *plans[0];
+    const int lvl = P0.lvl;
+    const u32 nt = u32(P0.terms.size()), no = u32(plans.size()), B = x.batch;
+    const std::size_t rows = std::size_t(lvl) + 1;
+    std::vector<const u64*> ptrs(nt);
+    std::vector<u64> strides(nt), coeffs(std::size_t(no) * nt * rows), adds(std::size_t(no) * rows, 0);
+    for (u32 t = 0; t < nt; ++t) {
+        const Ciphertext& c = *P0.terms[t].ct;
+        if (c.batch != B || c.parts.size() != 2 * B) throw TetrisError("ckks", "fused combination expects degree-1 terms");
+        ptrs[t] = c.parts[0].data();
+        strides[t] = u64(c.parts[1].data()) / 8 - u64(c.parts[0].data()) / 8;
+    }
+    bool any_add = false;
+    std::vector<std::vector<Poly>> outs(no);
+    std::vector<u64*> optr(no);
+    for (u32 o = 0; o < no; ++o) {
+        const CombPlan& P = *plans[o];
+        for (u32 t = 0; t < nt; ++t)
+            for (std::size_t r = 0; r < rows; ++r) coeffs[(std::size_t(o) * nt + t) * rows + r] = P.terms[t].coef[r];
+        if (!P.add.empty()) {
+            any_add = true;
+            for (std::size_t r = 0; r < rows; ++r) adds[std::size_t(o) * rows + r] = P.add[r];
+        }
+        outs[o] = fresh_parts(R, int(2 * B), lvl - 1, Form::coeff);
+        optr[o] = const_cast<u64*>(outs[o][0].data());
+    }
+    check_tg(tg_lincomb_multi(R.dev(), no, optr.data(), nt, ptrs.data(), strides.data(), coeffs.data(),
+                              any_add ? adds.data() : nullptr, lvl, 2 * B, B, R.stream()));
+    std::vector<Ciphertext> res;
+    for (u32 o = 0; o < no; ++o) res.push_back(finish_combine(*plans[o], R, x, std::move(outs[o])));
+    return res;
 }
 
 std::vector<double> trimmed(const std::vector<double>& c) {
@@ -403,15 +490,33 @@ Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const s
         return lr < 0 ? lp : std::min(lp, lr);
     };
 
-    auto base = [&](const std::vector<double>& cs, double target) {
+    // Two passes over the same recursion when base blocks are batched
+    // (multi_base): the PLAN pass walks the tree without evaluating any
+    // product and records every base block's combination step (its constants
+    // depend only on the ladder's scales and levels); the blocks sharing
+    // their terms and level are then evaluated together, one read of the baby
+    // steps for up to four blocks (tg_lincomb_multi); the EXEC pass consumes
+    // them in the same order.
+    bool plan = false;
+    std::deque<CombPlan> plans;
+    std::vector<Ciphertext> ready;
+    std::size_t next_ready = 0;
+    const Ciphertext dummy;
+    auto base = [&](const std::vector<double>& cs, double target) -> Ciphertext {
+        if (!plan && next_ready < ready.size()) return ready[next_ready++];
         std::vector<std::size_t> ks = base_terms(cs);
+        std::vector<double> z = cs;
         if (ks.empty()) {  // constant block: carried by 0 * T_1
-            std::vector<double> z = {cs[0], 0.0};
-            L.get(1);
-            return combine(L, x, {1}, z, cs[0], target);
+            z = {cs[0], 0.0};
+            ks = {1};
         }
         for (std::size_t k : ks) L.get(k);
-        return combine(L, x, ks, cs, cs[0], target);
+        if (plan) {
+            plans.emplace_back();
+            plan_combine(plans.back(), L, x, ks, z, cs[0], target);
+            return dummy;
+        }
+        return combine(L, x, ks, z, cs[0], target);
     };
 
     // the block evaluated at output scale `target`: blocks land exactly on the
@@ -443,12 +548,14 @@ Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const s
                     const Ciphertext& tn2 = L.get(n2);
                     std::optional<Ciphertext> Q2 = rec(q2, target * double(L.R.modulus(u32(lp))) / tn2.scale);
                     std::optional<Ciphertext> R2 = rec(r2, target);
+                    if (plan) return dummy;
                     return ev.mul2_relin_rescale(*Q, L.get(n), *Q2, tn2, keys, R2 ? &*R2 : nullptr);
                 }
             }
         }
         std::optional<Ciphertext> Rr = rec(r, target);
         if (!Q) return Rr;
+        if (plan) return dummy;
         if (!L.eval) {  // add(rescale(Q T_n), R) in one pass (Evaluator::rescale_add)
             if (!Rr) return ev.mul_relin_rescale(*Q, L.get(n), keys);
             return ev.mul_relin_rescale(*Q, L.get(n), keys, &*Rr);
@@ -464,6 +571,32 @@ Ciphertext eval_chebyshev_bsgs(const Evaluator& ev, const Ciphertext& x, const s
         P.add_inplace(y);
         return P;
     };
+    if (!L.eval && multi_base()) {
+        plan = true;
+        rec(c, x.scale);
+        plan = false;
+        // groups of up to four blocks over the same terms and level
+        ready.resize(plans.size());
+        std::vector<char> done(plans.size(), 0);
+        for (std::size_t i = 0; i < plans.size(); ++i) {
+            if (done[i]) continue;
+            std::vector<std::size_t> grp = {i};
+            for (std::size_t j = i + 1; j < plans.size() && grp.size() < 4; ++j)
+                if (!done[j] && multi_ok(L.R, plans[i], plans[j])) grp.push_back(j);
+            if (grp.size() == 1) {
+                ready[i] = run_combine(plans[i], L, x);
+                done[i] = 1;
+                continue;
+            }
+            std::vector<const CombPlan*> ps;
+            for (std::size_t j : grp) ps.push_back(&plans[j]);
+            std::vector<Ciphertext> outs = run_combine_multi(ps, L, x);
+            for (std::size_t k = 0; k < grp.size(); ++k) {
+                ready[grp[k]] = std::move(outs[k]);
+                done[grp[k]] = 1;
+            }
+        }
+    }
     std::optional<Ciphertext> out = rec(c, x.scale);
     if (!out) return ev.add_scalar(ev.mul_scalar(x, 0.0, 1.0), 0.0);
     return L.finish(*out);

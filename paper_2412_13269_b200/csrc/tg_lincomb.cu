@@ -303,10 +303,157 @@ __global__ void __launch_bounds__(kThreads) k_lincomb_fp2(DevRing R, LinComb L, 
     }
 }
 
+// Several combinations of the SAME terms in one pass (the BSGS base blocks of
+// one polynomial: q, r, q', r' are all sum_k c_k T_k over the same baby steps
+// with different constants): every term word is read once for all NO outputs
+// instead of once per output. Rescaled coefficient-form outputs only, every
+// row FP64 (k_lincomb_fp2's arithmetic per output).
+constexpr int kMultiTerms = 4, kMultiOuts = 4;
+struct MultiLin {
+    u32 nparts, add_polys;
+    int level;
+    const u64* ptr[kMultiTerms];
+    u64 pstride[kMultiTerms];
+    u64* out[kMultiOuts];
+    double c[kMultiOuts][kMultiTerms][TG_LINCOMB_MAX_ROWS];
+    double cs[kMultiOuts][kMultiTerms][TG_LINCOMB_MAX_ROWS];
+    double add[kMultiOuts][TG_LINCOMB_MAX_ROWS];  // centred constant (coefficient 0 of the first add_polys parts)
+};
+
+template <int NT, int NO>
+__global__ void __launch_bounds__(kThreads) k_lincomb_multi(DevRing R, MultiLin L) {
+    const u32 N = R.N, lvl = u32(L.level), half = N / 2;
+    const u64 total = u64(L.nparts) * half;
+    for (u64 i = blockIdx.x * u64(kThreads) + threadIdx.x; i < total; i += u64(gridDim.x) * kThreads) {
+        const u32 p = u32(i / half), c = u32(i - u64(p) * half) * 2;
+        const bool add0 = p < L.add_polys && c == 0;
+        const u64* base[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) base[t] = L.ptr[t] + p * L.pstride[t] + c;
+        auto load = [&](u32 r, ulonglong2 (&x)[NT]) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) x[t] = *reinterpret_cast<const ulonglong2*>(base[t] + size_t(r) * N);
+        };
+        // output o's sum_t c_t x_t (+ const) for both coefficients, |.| <= q/2 + 1
+        // (NT <= 4 terms of |.| <= 0.58q plus |const| <= q/2: < 2^53)
+        auto comb = [&](u32 r, const double (&xd)[NT][2], int o, double& o0, double& o1) {
+            const double qd = R.qd[4 * r], qi = R.qd[4 * r + 1];
+            double a0 = add0 ? L.add[o][r] : 0.0, a1 = 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const double w = L.c[o][t][r], wq = L.cs[o][t][r];
+                a0 = __dadd_rn(a0, fp_mulmod(xd[t][0], w, wq, qd));
+                a1 = __dadd_rn(a1, fp_mulmod(xd[t][1], w, wq, qd));
+            }
+            o0 = fp_reduce(a0, qd, qi);
+            o1 = fp_reduce(a1, qd, qi);
+        };
+        auto to_d = [&](const ulonglong2 (&x)[NT], double (&xd)[NT][2]) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                xd[t][0] = u2d(x[t].x);
+                xd[t][1] = u2d(x[t].y);
+            }
+        };
+        // rescale_round (ring.hpp:493-518) per output: centred last row, then
+        // (v_r - x) * ql^-1 per row
+        const double ql = R.qd[4 * lvl], hl = double(R.q[lvl] >> 1);
+        ulonglong2 xa[NT], xb[NT];
+        double xd[NT][2];
+        load(lvl, xa);
+        load(0, xb);
+        to_d(xa, xd);
+        double x0[NO], x1[NO];
+#pragma unroll
+        for (int o = 0; o < NO; ++o) {
+            comb(lvl, xd, o, x0[o], x1[o]);
+            if (x0[o] > hl) x0[o] = __dsub_rn(x0[o], ql);
+            if (x0[o] < -hl) x0[o] = __dadd_rn(x0[o], ql);
+            if (x1[o] > hl) x1[o] = __dsub_rn(x1[o], ql);
+            if (x1[o] < -hl) x1[o] = __dadd_rn(x1[o], ql);
+        }
+        const double* rsd = R.rsd + size_t(lvl) * R.q_count * 2;
+        const size_t po = size_t(p) * lvl * N + c;
+        for (u32 r = 0; r < lvl; ++r) {  // row r's words are in xb (r even) / xa (r odd)
+            if (r + 1 < lvl) load(r + 1, (r & 1) ? xb : xa);
+            to_d((r & 1) ? xa : xb, xd);
+            const double qd = R.qd[4 * r], w = rsd[2 * r], wq = rsd[2 * r + 1];
+            const u64 q = R.q[r];
+#pragma unroll
+            for (int o = 0; o < NO; ++o) {
+                double v0, v1;
+                comb(r, xd, o, v0, v1);
+                *reinterpret_cast<ulonglong2*>(L.out[o] + po + size_t(r) * N) =
+                    make_ulonglong2(fp_canon_small(fp_mulmod(__dsub_rn(v0, x0[o]), w, wq, qd), q),
+                                    fp_canon_small(fp_mulmod(__dsub_rn(v1, x1[o]), w, wq, qd), q));
+            }
+        }
+    }
+}
+
+template <int NT>
+void launch_multi(const DevRing& R, const MultiLin& L, u32 nouts, u32 grid, cudaStream_t st) {
+    switch (nouts) {
+        case 2: k_lincomb_multi<NT, 2><<<grid, kThreads, 0, st>>>(R, L); break;
+        case 3: k_lincomb_multi<NT, 3><<<grid, kThreads, 0, st>>>(R, L); break;
+        default: k_lincomb_multi<NT, 4><<<grid, kThreads, 0, st>>>(R, L); break;
+    }
+}
+
 }  // namespace
 }  // namespace tg
 
 using namespace tg;
+
+extern "C" int tg_lincomb_multi(tg_context* ctx, uint32_t nouts, uint64_t* const* outs, uint32_t nterms,
+                                const uint64_t* const* terms, const uint64_t* part_strides, const uint64_t* coeffs,
+                                const uint64_t* add_per_row, int level, uint32_t nparts, uint32_t add_polys,
+                                void* stream) {
+    if (!ctx) return fail(TG_E_ARG, "[ring] null context");
+    const DevRing& R = ctx->ring;
+    if (level < 1 || u32(level) >= R.q_count) return fail(TG_E_ARG, "[ring] lincomb_multi: level out of range");
+    if (nterms == 0 || nterms > u32(kMultiTerms) || nouts < 2 || nouts > u32(kMultiOuts))
+        return fail(TG_E_ARG, "[ring] lincomb_multi: 1..4 terms, 2..4 outputs");
+    if (u32(level) + 1 > TG_LINCOMB_MAX_ROWS) return fail(TG_E_ARG, "[ring] lincomb: too many rows");
+    for (int r = 0; r <= level; ++r)
+        if (ctx->h_q[r] >= kFpMaxQ) return fail(TG_E_ARG, "[ring] lincomb_multi needs FP64 q-chain rows");
+    if (nparts == 0) return TG_OK;
+    DeviceGuard guard(ctx->device);
+    MultiLin L{};
+    L.nparts = nparts;
+    L.add_polys = add_polys;
+    L.level = level;
+    for (u32 t = 0; t < nterms; ++t) {
+        L.ptr[t] = terms[t];
+        L.pstride[t] = part_strides[t];
+    }
+    const size_t rows = size_t(level) + 1;
+    for (u32 o = 0; o < nouts; ++o) {
+        L.out[o] = outs[o];
+        for (u32 t = 0; t < nterms; ++t)
+            for (int r = 0; r <= level; ++r) {
+                const u64 q = ctx->h_q[r], v = coeffs[(size_t(o) * nterms + t) * rows + r] % q;
+                L.c[o][t][r] = double(v);
+                L.cs[o][t][r] = double(v) / double(q);
+            }
+        for (int r = 0; r <= level; ++r) {
+            const u64 q = ctx->h_q[r], e = add_per_row ? add_per_row[size_t(o) * rows + r] % q : 0;
+            L.add[o][r] = e > q / 2 ? -double(q - e) : double(e);
+        }
+    }
+    ProfScope prof(ctx, TG_OP_LINCOMB, 8.0 * nparts * R.N * (double(rows) * nterms + double(nouts) * level),
+                   as_stream(stream));
+    cudaStream_t st = as_stream(stream);
+    const u32 grid = grid_for(size_t(nparts) * R.N / 2);
+    switch (nterms) {
+        case 1: launch_multi<1>(R, L, nouts, grid, st); break;
+        case 2: launch_multi<2>(R, L, nouts, grid, st); break;
+        case 3: launch_multi<3>(R, L, nouts, grid, st); break;
+        default: launch_multi<4>(R, L, nouts, grid, st); break;
+    }
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
 
 extern "C" int tg_lincomb(tg_context* ctx, uint64_t* out, uint32_t nterms, const uint64_t* const* terms,
                           const uint64_t* part_strides, const uint64_t* coeffs, const uint64_t* add_per_row,
