@@ -74,9 +74,9 @@ __device__ __forceinline__ void ld_strided_hint(u64 (&v)[E], const u64* x, u32 l
     for (int j = 0; j < E; ++j) v[j] = KS_L2_HINTS ? ld_hint(x + lane + 32 * j, pol) : x[lane + 32 * j];
 }
 
-template <int E, int NW = 8>
+template <int E>
 constexpr size_t ks_chunk_smem() {  // two exchange columns per warp + forward and inverse chunk twiddles
-    return size_t(8) * (2 * NW * WGeo<E>::CS + 4 * WGeo<E>::TW_CHUNK);
+    return size_t(8) * (16 * WGeo<E>::CS + 4 * WGeo<E>::TW_CHUNK);
 }
 
 template <int E>
@@ -93,13 +93,8 @@ __device__ __forceinline__ void ks_chunks_int_body(const DevRing& R, u64* acc, c
 // products, tg_relinearize_tensor2_rescale_batch): c0 += u0 v0, c1 += u0 v1 +
 // u1 v0 (|c0| < 1.62q, |c1| < 3.24q, brought back to |.| <= q/2 + 1 by
 // fp_reduce before the P product).
-// NW = 16 (experiment, TG_KS_W16=1): one 512-thread block per SM, warps 0-7
-// and 8-15 work on two polys of the batch side by side over the SAME eight
-// chunks -- the staged twiddles are shared (half the staging per poly, 65 KB
-// of shared memory left to L1) and both halves read the same key words close
-// in time.
-template <int E, bool MIXED = false, int NW = 8>
-__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
+template <int E, bool MIXED = false>
+__global__ void __launch_bounds__(256, 2)
 kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb, const u64* key, int level,
              u32 logN1, u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, u32 int_from,
              const u64* ty0, const u64* ty1, const Tensor2 t2) {
@@ -110,10 +105,8 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
             return;
         }
     }
-    static_assert(NW == 8 || (NW == 16 && !MIXED), "16-warp blocks: all-FP64 rings only");
-    constexpr u32 NS = NW / 8;  // polys side by side
     extern __shared__ u64 dyn[];
-    u64* swf = dyn + 2 * NW * Gm::CS;
+    u64* swf = dyn + 16 * Gm::CS;
     u64* swi = swf + 2 * Gm::TW_CHUNK;
     const u32 N = R.N, rows = u32(level) + 1 + R.K;
     const u32 r = blockIdx.y;
@@ -122,19 +115,12 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
     const u32 m = mod_index(r, level, R.q_count);
     const double qd = R.qd[4 * m], qi = R.qd[4 * m + 1];
     const u64* tw = reinterpret_cast<const u64*>(R.twd + size_t(m) * 4 * N);
-    if constexpr (NW == 8) {
-        stage_chunk_twiddles<E, true>(swf, nullptr, tw, tw + N, logN1, blockIdx.x);
-        stage_chunk_twiddles<E, false>(swi, nullptr, tw + 2 * size_t(N), tw + 3 * size_t(N), logN1, blockIdx.x);
-    } else {  // each half of the block stages one table
-        if (threadIdx.x < 256) stage_chunk_twiddles<E, true>(swf, nullptr, tw, tw + N, logN1, blockIdx.x, threadIdx.x);
-        else
-            stage_chunk_twiddles<E, false>(swi, nullptr, tw + 2 * size_t(N), tw + 3 * size_t(N), logN1, blockIdx.x,
-                                           threadIdx.x - 256);
-    }
+    stage_chunk_twiddles<E, true>(swf, nullptr, tw, tw + N, logN1, blockIdx.x);
+    stage_chunk_twiddles<E, false>(swi, nullptr, tw + 2 * size_t(N), tw + 3 * size_t(N), logN1, blockIdx.x);
     __syncthreads();
-    const u32 wfull = threadIdx.x >> 5, warp = wfull & 7, slot = wfull >> 3, lane = threadIdx.x & 31;
+    const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t off = size_t(blockIdx.x * 8 + warp) * Gm::M;
-    u64* col = dyn + wfull * 2 * Gm::CS;  // the warp's contiguous pair-exchange region
+    u64* col = dyn + warp * 2 * Gm::CS;  // the warp's contiguous pair-exchange region
     constexpr u32 CS2 = 8 * Gm::CS;
     const size_t words = size_t(rows) * N, key_rows = R.nmod;
     const bool addq = add0 && r <= u32(level);
@@ -186,10 +172,7 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
             a1[2 * j + 1] = __dadd_rn(a1[2 * j + 1], fp_mulmod_qi(v[2 * j + 1], u2d(ta.y), qd, qi));
         }
     };
-    for (u32 bi = b0; bi < b1; bi += NS) {
-        const u32 b = bi + slot;
-        if (NS > 1 && bi != b0) __syncthreads();  // the two halves stay on neighbouring polys (shared key words in L1)
-        if (b >= b1) continue;
+    for (u32 b = b0; b < b1; ++b) {
         double a[2][E];
 #pragma unroll
         for (int j = 0; j < E; ++j) a[0][j] = a[1][j] = 0.0;

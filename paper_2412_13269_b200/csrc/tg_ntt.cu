@@ -225,21 +225,6 @@ void launch_ks_fused(const DevRing& R, int sms, u64* acc, const u64* digits, u32
     // rows on the FP64 path: all of them, or (mixed ring, ks_fused_ok) the
     // q-chain, with the integer special rows' blocks in the same launch
     const dim3 grid(M1 / 8, rows, (npolys + ppb - 1) / ppb);
-    static const bool w16 = [] {  // experiment: 16-warp blocks, two polys side by side (see kw_ks_chunks)
-        const char* e = getenv("TG_KS_W16");
-        return e && *e == '1';
-    }();
-    if (all_fp && w16 && ppb >= 2) {
-        static const bool attr16 = [] {
-            cudaFuncSetAttribute(kw_ks_chunks<E2, false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(ks_chunk_smem<E2, 16>()));
-            return true;
-        }();
-        (void)attr16;
-        kw_ks_chunks<E2, false, 16><<<grid, 512, ks_chunk_smem<E2, 16>(), s>>>(
-            R, acc, digits, nd, npolys, ppb, key, level, WGeo<E1>::LOGM, own_gs, add0, add1, pmod, rows, ty0, ty1, t2);
-        return;
-    }
     if (all_fp) {
         kw_ks_chunks<E2><<<grid, 256, ks_chunk_smem<E2>(), s>>>(R, acc, digits, nd, npolys, ppb, key, level,
                                                                  WGeo<E1>::LOGM, own_gs, add0, add1, pmod, rows,

@@ -374,9 +374,7 @@ __device__ __forceinline__ void winv_all(u64 (&v)[E], u64* col, u32 lane, const 
 // sw[8(2^u-1) + t] = tab[2^(logN1+u) + 8 bx 2^u + t], t < 8*2^u.
 template <int E, bool FWD>
 __device__ __forceinline__ void stage_chunk_twiddles(u64* sw, u64* sws, const u64* __restrict__ w,
-                                                     const u64* __restrict__ ws, u32 logN1, u32 bx,
-                                                     u32 tid = 0xFFFFFFFFu) {
-    if (tid == 0xFFFFFFFFu) tid = threadIdx.x;  // 256 staging threads (tid < 256)
+                                                     const u64* __restrict__ ws, u32 logN1, u32 bx) {
     // flattened slot e -> (u, t): all of a thread's loads are issued before
     // any store, so the staging costs one memory latency, not LOGM of them
     constexpr int TOT = WGeo<E>::TW_CHUNK;
@@ -386,7 +384,7 @@ __device__ __forceinline__ void stage_chunk_twiddles(u64* sw, u64* sws, const u6
     constexpr u32 NJ = tw_nj_mask<E, FWD>();
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
-        const u32 e = tid + 256u * k;
+        const u32 e = threadIdx.x + 256u * k;
         d[k] = u32(TOT);
         if (e < u32(TOT)) {
             const u32 u = 31 - __clz((e >> 3) + 1);  // e in [8(2^u - 1), 8(2^(u+1) - 1))
