@@ -280,6 +280,13 @@ int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const
 int tg_tensor2_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
                           const uint64_t* y1, const uint64_t* u1, const uint64_t* v1, int level,
                           uint32_t npolys, int* raw, void* stream);
+/* op_strides (here and in the *_strided entry points below): NULL, or 4 host
+ * words = the distance in words between consecutive polys of the x, y, u, v
+ * operand parts (0 = tight, (level+1)*N): level-dropped views of a
+ * higher-level ciphertext batch are read in place instead of being gathered. */
+int tg_tensor2_c2_inverse_strided(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
+                                  const uint64_t* y1, const uint64_t* u1, const uint64_t* v1,
+                                  const uint64_t* op_strides, int level, uint32_t npolys, int* raw, void* stream);
 /* raw (in/out, may be NULL): non-NULL lets the call leave c2 as the inverse
  * transform's raw doubles without the N^-1 factor (|v| <= 0.6q) when the
  * fused key switch can consume them; *raw reports whether it did (pass it on
@@ -425,6 +432,13 @@ int tg_relinearize_tensor_ladder_batch(tg_gadget* g, uint64_t* out, const uint64
                                        const uint64_t* y1, uint32_t npolys, int c2_raw, const uint64_t* sub,
                                        uint64_t sub_stride, const uint64_t* sub_coef,
                                        const uint64_t* add_const, void* stream);
+int tg_relinearize_tensor_ladder_batch_strided(tg_gadget* g, uint64_t* out, const uint64_t* c2,
+                                               const uint64_t* c2_eval, const uint64_t* key,
+                                               uint32_t key_digits, int level, const uint64_t* x0,
+                                               const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
+                                               const uint64_t* op_strides, uint32_t npolys, int c2_raw,
+                                               const uint64_t* sub, uint64_t sub_stride, const uint64_t* sub_coef,
+                                               const uint64_t* add_const, void* stream);
 /* Lazy relinearisation of two products: rescale(relinearize(add(mul(x, y),
  * mul(u, v)))) [+ add] (ckks.hpp:229-237, rlwe.hpp:300-305, :601-620,
  * ckks.hpp:315-324) with ONE key switch: c2 = x1 y1 + u1 v1 (from
@@ -437,6 +451,14 @@ int tg_relinearize_tensor2_rescale_batch(tg_gadget* g, uint64_t* out, const uint
                                          const uint64_t* y1, const uint64_t* u0, const uint64_t* u1,
                                          const uint64_t* v0, const uint64_t* v1, uint32_t npolys, int c2_raw,
                                          const uint64_t* add, uint64_t add_stride, int out_level, void* stream);
+int tg_relinearize_tensor2_rescale_batch_strided(tg_gadget* g, uint64_t* out, const uint64_t* c2,
+                                                 const uint64_t* c2_eval, const uint64_t* key,
+                                                 uint32_t key_digits, int level, const uint64_t* x0,
+                                                 const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
+                                                 const uint64_t* u0, const uint64_t* u1, const uint64_t* v0,
+                                                 const uint64_t* v1, const uint64_t* op_strides, uint32_t npolys,
+                                                 int c2_raw, const uint64_t* add, uint64_t add_stride,
+                                                 int out_level, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,6 +1,7 @@
 // Host-internal helpers: ciphertext-part blocks (several polys of one shape
 // back to back in one HBM allocation) so that per-part ops launch once.
 #pragma once
+#include <cstdlib>
 
 #include "tetris_b200/keys.hpp"
 
@@ -59,6 +60,53 @@ inline const u64* group_data(const std::vector<Poly>& parts, std::size_t first, 
     }
     keep.insert(keep.end(), g.begin(), g.end());
     return g[0].data();
+}
+
+// parts[first..first+n) as one group for a kernel that reads poly i at
+// base + i * stride words: a contiguous group is tight (stride = words), the
+// polys of a level-dropped batch view keep their block's stride and are read
+// in place; anything else is gathered (tight copies kept alive in `keep`).
+inline const u64* strided_group(const std::vector<Poly>& parts, std::size_t first, std::size_t n,
+                                std::vector<Poly>& keep, u64& stride) {
+    const Poly& p0 = parts[first];
+    stride = p0.words();
+    if (n == 1 || contiguous(parts, first, n)) return p0.data();
+    bool uniform = true;
+    const std::size_t d = parts[first + 1].offset() - p0.offset();
+    for (std::size_t i = 0; i < n && uniform; ++i) {
+        const Poly& p = parts[first + i];
+        uniform = p.storage() == p0.storage() && p.level() == p0.level() && p.nspecial() == p0.nspecial() &&
+                  p.form() == p0.form() && p.offset() == p0.offset() + i * d;
+    }
+    if (uniform && d >= p0.words()) {
+        stride = d;
+        return p0.data();
+    }
+    return group_data(parts, first, n, keep);
+}
+
+// Both part groups (c0 polys, c1 polys) of a degree-1 batch with ONE poly
+// stride for the tensor entry points (op_strides); TG_OPERAND_STRIDES=0, or
+// groups whose strides differ, fall back to tight gathered copies.
+inline void operand_groups(const Ciphertext& c, u32 B, std::vector<Poly>& keep, const u64*& g0, const u64*& g1,
+                           u64& stride) {
+    static const bool off = [] {
+        const char* e = std::getenv("TG_OPERAND_STRIDES");
+        return e && *e == '0';
+    }();
+    u64 s0 = 0, s1 = 0;
+    if (!off) {
+        std::vector<Poly> k0;
+        g0 = strided_group(c.parts, 0, B, k0, s0);
+        g1 = strided_group(c.parts, B, B, k0, s1);
+        if (s0 == s1 && k0.empty()) {
+            stride = s0;
+            return;
+        }
+    }
+    g0 = group_data(c.parts, 0, B, keep);
+    g1 = group_data(c.parts, B, B, keep);
+    stride = c.parts[0].words();
 }
 
 // Applies a per-part kernel `fn(dst, src, npolys)` to all parts, writing one

@@ -545,16 +545,14 @@ Ciphertext KeyContext::relinearize_tensor_rescale(const Ciphertext& x, const Cip
     if (u && (u->level() != lvl || v->level() != lvl || u->batch != B || v->batch != B))
         throw TetrisError("rlwe", "the second product must share the first's level and batch");
     std::vector<Poly> keep;
-    const u64* x0 = detail::group_data(x.parts, 0, B, keep);
-    const u64* x1 = detail::group_data(x.parts, B, B, keep);
-    const u64* y0 = detail::group_data(y.parts, 0, B, keep);
-    const u64* y1 = detail::group_data(y.parts, B, B, keep);
+    u64 st[4] = {0, 0, 0, 0};  // poly strides of x, y, u, v (level-dropped batch views are read in place)
+    const u64 *x0, *x1, *y0, *y1;
+    detail::operand_groups(x, B, keep, x0, x1, st[0]);
+    detail::operand_groups(y, B, keep, y0, y1, st[1]);
     const u64 *u0 = nullptr, *u1 = nullptr, *v0 = nullptr, *v1 = nullptr;
     if (u) {
-        u0 = detail::group_data(u->parts, 0, B, keep);
-        u1 = detail::group_data(u->parts, B, B, keep);
-        v0 = detail::group_data(v->parts, 0, B, keep);
-        v1 = detail::group_data(v->parts, B, B, keep);
+        detail::operand_groups(*u, B, keep, u0, u1, st[2]);
+        detail::operand_groups(*v, B, keep, v0, v1, st[3]);
     }
     const u64* ad = nullptr;
     std::size_t as = 0;
@@ -566,12 +564,14 @@ Ciphertext KeyContext::relinearize_tensor_rescale(const Ciphertext& x, const Cip
     std::vector<Poly> c2e = fresh_parts(*ring_, int(B), lvl, Form::eval);
     std::vector<Poly> c2 = fresh_parts(*ring_, int(B), lvl, Form::coeff);
     int raw = 1;
-    check_tg(tg_tensor2_c2_inverse(ring_->dev(), const_cast<u64*>(c2[0].data()), const_cast<u64*>(c2e[0].data()), x1,
-                                   y1, u1, v1, lvl, B, &raw, ring_->stream()));
+    check_tg(tg_tensor2_c2_inverse_strided(ring_->dev(), const_cast<u64*>(c2[0].data()),
+                                           const_cast<u64*>(c2e[0].data()), x1, y1, u1, v1, st, lvl, B, &raw,
+                                           ring_->stream()));
     std::vector<Poly> dst = fresh_parts(*ring_, int(2 * B), add ? out_level : lvl - 1, Form::coeff);
-    check_tg(tg_relinearize_tensor2_rescale_batch(plan_->dev(), const_cast<u64*>(dst[0].data()), c2[0].data(),
-                                                  c2e[0].data(), key_base(rlk), rlk.digits(), lvl, x0, x1, y0, y1, u0,
-                                                  u1, v0, v1, B, raw, ad, as, add ? out_level : 0, ring_->stream()));
+    check_tg(tg_relinearize_tensor2_rescale_batch_strided(plan_->dev(), const_cast<u64*>(dst[0].data()), c2[0].data(),
+                                                          c2e[0].data(), key_base(rlk), rlk.digits(), lvl, x0, x1, y0,
+                                                          y1, u0, u1, v0, v1, st, B, raw, ad, as,
+                                                          add ? out_level : 0, ring_->stream()));
     Ciphertext out;
     out.batch = B;
     out.parts = std::move(dst);
@@ -590,10 +590,10 @@ Ciphertext KeyContext::relinearize_tensor_ladder(const Ciphertext& x, const Ciph
     const int lvl = x.level();
     if (lvl < 1) throw TetrisError("ckks", "cannot rescale at level 0");
     std::vector<Poly> keep;
-    const u64* x0 = detail::group_data(x.parts, 0, B, keep);
-    const u64* x1 = detail::group_data(x.parts, B, B, keep);
-    const u64* y0 = detail::group_data(y.parts, 0, B, keep);
-    const u64* y1 = detail::group_data(y.parts, B, B, keep);
+    u64 st[4] = {0, 0, 0, 0};
+    const u64 *x0, *x1, *y0, *y1;
+    detail::operand_groups(x, B, keep, x0, x1, st[0]);
+    detail::operand_groups(y, B, keep, y0, y1, st[1]);
     const u64* sp = nullptr;
     std::size_t ss = 0;
     if (sub) {
@@ -613,13 +613,15 @@ Ciphertext KeyContext::relinearize_tensor_ladder(const Ciphertext& x, const Ciph
     std::vector<Poly> c2e = fresh_parts(*ring_, int(B), lvl, Form::eval);
     std::vector<Poly> c2 = fresh_parts(*ring_, int(B), lvl, Form::coeff);
     int raw = 1;
-    check_tg(tg_tensor_c2_inverse(ring_->dev(), const_cast<u64*>(c2[0].data()), const_cast<u64*>(c2e[0].data()), x1,
-                                  y1, lvl, B, &raw, ring_->stream()));
+    check_tg(tg_tensor2_c2_inverse_strided(ring_->dev(), const_cast<u64*>(c2[0].data()),
+                                           const_cast<u64*>(c2e[0].data()), x1, y1, nullptr, nullptr, st, lvl, B, &raw,
+                                           ring_->stream()));
     std::vector<Poly> dst = fresh_parts(*ring_, int(2 * B), lvl - 1, Form::coeff);
-    check_tg(tg_relinearize_tensor_ladder_batch(plan_->dev(), const_cast<u64*>(dst[0].data()), c2[0].data(),
-                                                c2e[0].data(), key_base(rlk), rlk.digits(), lvl, x0, x1, y0, y1, B, raw,
-                                                sp, ss, sub ? sub_coef.data() : nullptr,
-                                                add_const.empty() ? nullptr : add_const.data(), ring_->stream()));
+    check_tg(tg_relinearize_tensor_ladder_batch_strided(plan_->dev(), const_cast<u64*>(dst[0].data()), c2[0].data(),
+                                                        c2e[0].data(), key_base(rlk), rlk.digits(), lvl, x0, x1, y0,
+                                                        y1, st, B, raw, sp, ss, sub ? sub_coef.data() : nullptr,
+                                                        add_const.empty() ? nullptr : add_const.data(),
+                                                        ring_->stream()));
     Ciphertext out;
     out.batch = B;
     out.parts = std::move(dst);

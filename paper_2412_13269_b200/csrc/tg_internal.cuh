@@ -289,11 +289,15 @@ bool ntt_inverse_cols_raw_ok(const tg_context* ctx);
 // Second operand pair of a lazily relinearised sum of two products
 // (Evaluator::mul2_relin_rescale): eval-form parts u0, u1, v0, v1 laid out
 // like the first pair's; all null when there is one product.
+// sx, sy, su, sv: words between consecutive polys of a part of x, y, u, v
+// (0: tight, (level+1) * N) -- level-dropped views of a higher-level batch
+// are read in place instead of being gathered first.
 struct Tensor2 {
     const u64* u0 = nullptr;
     const u64* u1 = nullptr;
     const u64* v0 = nullptr;
     const u64* v1 = nullptr;
+    u64 sx = 0, sy = 0, su = 0, sv = 0;
 };
 int ks_fused_chunks(tg_context* ctx, u64* acc, const u64* digits, u32 nd, u32 npolys, const u64* key, int level,
                     u32 own_gs, const u64* add0, const u64* add1, const u64* pmod, cudaStream_t s,

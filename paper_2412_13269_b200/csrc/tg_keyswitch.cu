@@ -1360,6 +1360,38 @@ extern "C" int tg_relinearize_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1
     return rc;
 }
 
+// Operand strides of the tensor entry points: op_strides = NULL or 4 host
+// words (words between consecutive polys of the x, y, u, v parts; 0 = tight).
+static int set_op_strides(Tensor2& t2, const uint64_t* op_strides, size_t tight, bool& strided) {
+    strided = false;
+    if (!op_strides) return TG_OK;
+    u64* dst[4] = {&t2.sx, &t2.sy, &t2.su, &t2.sv};
+    for (int i = 0; i < 4; ++i)
+        if (op_strides[i] && op_strides[i] != tight) {
+            if (op_strides[i] < tight) return fail(TG_E_ARG, "[ckks] operand stride below the poly size");
+            *dst[i] = op_strides[i];
+            strided = true;
+        }
+    return TG_OK;
+}
+
+// Tight copies of strided operand parts for the paths that need them (rings
+// without the fused core): ops = {x0, x1, y0, y1, u0, u1, v0, v1}.
+static int gather_ops(tg_context* ctx, const u64* (&ops)[8], Tensor2& t2, u32 npolys, size_t tight, void** tmp,
+                      cudaStream_t s) {
+    const u64 st[4] = {t2.sx, t2.sy, t2.su, t2.sv};
+    TG_CUDA(cudaMallocFromPoolAsync(tmp, 8 * tight * npolys * 8, ctx->pool, s));
+    for (int i = 0; i < 8; ++i)
+        if (ops[i] && st[i / 2]) {
+            u64* d = static_cast<u64*>(*tmp) + size_t(i) * tight * npolys;
+            TG_CUDA(cudaMemcpy2DAsync(d, tight * 8, ops[i], st[i / 2] * 8, tight * 8, npolys, cudaMemcpyDeviceToDevice,
+                                      s));
+            ops[i] = d;
+        }
+    t2.sx = t2.sy = t2.su = t2.sv = 0;
+    return TG_OK;
+}
+
 static bool tensor2_given(const Tensor2& t2, bool& bad) {
     const int n = (t2.u0 != nullptr) + (t2.u1 != nullptr) + (t2.v0 != nullptr) + (t2.v1 != nullptr);
     bad = n != 0 && n != 4;
@@ -1398,17 +1430,23 @@ static int relinearize_tensor_batch(tg_gadget* g, uint64_t* out0, uint64_t* out1
     DeviceGuard guard(ctx->device);
     cudaStream_t s = as_stream(stream);
     if (!ks_fused_ok(ctx)) {  // the tensor's c0 / c1 through HBM, then the plain batched relinearisation
-        const size_t qw = size_t(level + 1) * ctx->ring.N * npolys;
+        const size_t tight = size_t(level + 1) * ctx->ring.N, qw = tight * npolys;
+        Tensor2 tt = t2;
+        const u64* ops[8] = {x0, x1, y0, y1, tt.u0, tt.u1, tt.v0, tt.v1};
+        void* gt = nullptr;
+        if (tt.sx || tt.sy || tt.su || tt.sv)
+            if (int rc = gather_ops(ctx, ops, tt, npolys, tight, &gt, s)) return rc;
         void* cc = nullptr;
         TG_CUDA(cudaMallocFromPoolAsync(&cc, 3 * qw * 8, ctx->pool, s));
         u64* c0 = static_cast<u64*>(cc);  // (c2 recomputed into the third slot, unused)
-        int rc = two ? tg_tensor2(ctx, c0, c0 + qw, c0 + 2 * qw, x0, x1, y0, y1, t2.u0, t2.u1, t2.v0, t2.v1, level,
-                                  npolys, stream)
-                     : tg_tensor(ctx, c0, c0 + qw, c0 + 2 * qw, x0, x1, y0, y1, level, npolys, stream);
+        int rc = two ? tg_tensor2(ctx, c0, c0 + qw, c0 + 2 * qw, ops[0], ops[1], ops[2], ops[3], ops[4], ops[5], ops[6],
+                                  ops[7], level, npolys, stream)
+                     : tg_tensor(ctx, c0, c0 + qw, c0 + 2 * qw, ops[0], ops[1], ops[2], ops[3], level, npolys, stream);
         if (rc == TG_OK)
             rc = tg_relinearize_batch(g, out0, out1, c2, c2_eval, key, key_digits, level, c0, c0 + qw, npolys,
                                       stream);
         cudaFreeAsync(cc, s);
+        if (gt) cudaFreeAsync(gt, s);
         return rc;
     }
     const size_t words = size_t(level + 1 + ctx->ring.K) * ctx->ring.N;
@@ -1439,12 +1477,24 @@ extern "C" int tg_relinearize_tensor2_rescale_batch(tg_gadget* g, uint64_t* out,
                                                     const uint64_t* v1, uint32_t npolys, int c2_raw,
                                                     const uint64_t* add, uint64_t add_stride, int out_level,
                                                     void* stream) {
+    return tg_relinearize_tensor2_rescale_batch_strided(g, out, c2, c2_eval, key, key_digits, level, x0, x1, y0, y1,
+                                                        u0, u1, v0, v1, nullptr, npolys, c2_raw, add, add_stride,
+                                                        out_level, stream);
+}
+
+extern "C" int tg_relinearize_tensor2_rescale_batch_strided(
+    tg_gadget* g, uint64_t* out, const uint64_t* c2, const uint64_t* c2_eval, const uint64_t* key,
+    uint32_t key_digits, int level, const uint64_t* x0, const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
+    const uint64_t* u0, const uint64_t* u1, const uint64_t* v0, const uint64_t* v1, const uint64_t* op_strides,
+    uint32_t npolys, int c2_raw, const uint64_t* add, uint64_t add_stride, int out_level, void* stream) {
     if (int rc = check_ks(g, level)) return rc;
     Tensor2 t2;
     t2.u0 = u0, t2.u1 = u1, t2.v0 = v0, t2.v1 = v1;
     bool bad = false;
     tensor2_given(t2, bad);
     if (bad) return fail(TG_E_ARG, "[rlwe] the second product needs all four operand parts");
+    bool strided = false;
+    if (int rc = set_op_strides(t2, op_strides, size_t(level + 1) * g->ctx->ring.N, strided)) return rc;
     if (level < 1) return fail(TG_E_ARG, "[ring] cannot rescale at level 0");
     if (add && (out_level < 0 || out_level > level - 1)) return fail(TG_E_ARG, "[ring] rescale_add level out of range");
     if (npolys == 0) return TG_OK;
@@ -1499,7 +1549,22 @@ extern "C" int tg_relinearize_tensor_ladder_batch(tg_gadget* g, uint64_t* out, c
                                                   uint32_t npolys, int c2_raw, const uint64_t* sub,
                                                   uint64_t sub_stride, const uint64_t* sub_coef,
                                                   const uint64_t* add_const, void* stream) {
+    return tg_relinearize_tensor_ladder_batch_strided(g, out, c2, c2_eval, key, key_digits, level, x0, x1, y0, y1,
+                                                      nullptr, npolys, c2_raw, sub, sub_stride, sub_coef, add_const,
+                                                      stream);
+}
+
+extern "C" int tg_relinearize_tensor_ladder_batch_strided(
+    tg_gadget* g, uint64_t* out, const uint64_t* c2, const uint64_t* c2_eval, const uint64_t* key,
+    uint32_t key_digits, int level, const uint64_t* x0, const uint64_t* x1, const uint64_t* y0, const uint64_t* y1,
+    const uint64_t* op_strides, uint32_t npolys, int c2_raw, const uint64_t* sub, uint64_t sub_stride,
+    const uint64_t* sub_coef, const uint64_t* add_const, void* stream) {
     if (int rc = check_ks(g, level)) return rc;
+    Tensor2 t2;
+    {
+        bool strided = false;
+        if (int rc = set_op_strides(t2, op_strides, size_t(level + 1) * g->ctx->ring.N, strided)) return rc;
+    }
     if (level < 1) return fail(TG_E_ARG, "[ring] cannot rescale at level 0");
     if (npolys == 0) return TG_OK;
     if (!x0 || !x1 || !y0 || !y1) return fail(TG_E_ARG, "[rlwe] relinearize needs both operands' eval parts");
@@ -1526,8 +1591,8 @@ extern "C" int tg_relinearize_tensor_ladder_batch(tg_gadget* g, uint64_t* out, c
         void* tmp = nullptr;
         TG_CUDA(cudaMallocFromPoolAsync(&tmp, 2 * qw * 8, ctx->pool, s));
         u64* t = static_cast<u64*>(tmp);
-        int rc = tg_relinearize_tensor_batch(g, t, t + qw, c2, c2_eval, key, key_digits, level, x0, x1, y0, y1,
-                                             npolys, c2_raw, stream);
+        int rc = relinearize_tensor_batch(g, t, t + qw, c2, c2_eval, key, key_digits, level, x0, x1, y0, y1, t2,
+                                          npolys, c2_raw, stream);
         if (rc == TG_OK) {
             const uint64_t* terms[2] = {t, sub};
             const uint64_t strides[2] = {pw, sub_stride};
@@ -1560,7 +1625,7 @@ extern "C" int tg_relinearize_tensor_ladder_batch(tg_gadget* g, uint64_t* out, c
     TG_CUDA(cudaMallocFromPoolAsync(&scratch, size_t(npolys) * (nd + 2) * words * 8, ctx->pool, s));
     const RescaleSpec rs{nullptr, 0, u32(level), &pre};
     const int rc = ks_fused_batch(g, out, out + size_t(npolys) * level * R.N, c2, c2_eval, nd, npolys, key, level,
-                                  static_cast<u64*>(scratch), s, x0, x1, true, y0, y1, c2_raw != 0, &rs);
+                                  static_cast<u64*>(scratch), s, x0, x1, true, y0, y1, c2_raw != 0, &rs, t2);
     cudaFreeAsync(scratch, s);
     return rc;
 }

@@ -179,12 +179,14 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
         // P * c first (the accumulators start from it): its loads are in
         // flight with the first digits' instead of exposed after the last
         if (addq) {  // + P * c on the Q rows (|.| <= q/2 + 2^-15 q; the digit sums reduce every 4 as before)
-            const size_t qw = size_t(level + 1) * N, po = size_t(b) * qw + size_t(r) * N + off + vo;
+            const size_t qw = size_t(level + 1) * N, ro = size_t(r) * N + off + vo;
+            const size_t po = size_t(b) * (t2.sx ? t2.sx : qw) + ro;  // operand polys may be strided views
             const ulonglong2* c0 = reinterpret_cast<const ulonglong2*>(add0 + po);
             const ulonglong2* c1 = reinterpret_cast<const ulonglong2*>(add1 + po);
             if (ty0) {  // tensor mode: c0 = x0 y0, c1 = x0 y1 + x1 y0 from the operands
-                const ulonglong2* d0 = reinterpret_cast<const ulonglong2*>(ty0 + po);
-                const ulonglong2* d1 = reinterpret_cast<const ulonglong2*>(ty1 + po);
+                const size_t py = size_t(b) * (t2.sy ? t2.sy : qw) + ro;
+                const ulonglong2* d0 = reinterpret_cast<const ulonglong2*>(ty0 + py);
+                const ulonglong2* d1 = reinterpret_cast<const ulonglong2*>(ty1 + py);
 #pragma unroll
                 for (int j = 0; j < E / 2; ++j) {
                     const ulonglong2 x0 = c0[j], x1 = c1[j], y0 = d0[j], y1 = d1[j];
@@ -197,10 +199,12 @@ kw_ks_chunks(DevRing R, u64* acc, const u64* digits, u32 nd, u32 npolys, u32 ppb
                         s1[h] = __dadd_rn(fp_mulmod_qi(xa[h], yb[h], qd, qi), fp_mulmod_qi(xb[h], ya[h], qd, qi));
                     }
                     if (t2.u0) {  // + the second product's c0 / c1
-                        const ulonglong2 u0 = reinterpret_cast<const ulonglong2*>(t2.u0 + po)[j];
-                        const ulonglong2 u1 = reinterpret_cast<const ulonglong2*>(t2.u1 + po)[j];
-                        const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(t2.v0 + po)[j];
-                        const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(t2.v1 + po)[j];
+                        const size_t pu = size_t(b) * (t2.su ? t2.su : qw) + ro;
+                        const size_t pv = size_t(b) * (t2.sv ? t2.sv : qw) + ro;
+                        const ulonglong2 u0 = reinterpret_cast<const ulonglong2*>(t2.u0 + pu)[j];
+                        const ulonglong2 u1 = reinterpret_cast<const ulonglong2*>(t2.u1 + pu)[j];
+                        const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(t2.v0 + pv)[j];
+                        const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(t2.v1 + pv)[j];
                         const double ua[2] = {u2d(u0.x), u2d(u0.y)}, ub[2] = {u2d(u1.x), u2d(u1.y)};
                         const double va[2] = {u2d(v0.x), u2d(v0.y)}, vb[2] = {u2d(v1.x), u2d(v1.y)};
 #pragma unroll

@@ -446,6 +446,19 @@ extern "C" int tg_tensor_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_
 extern "C" int tg_tensor2_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
                                      const uint64_t* y1, const uint64_t* u1, const uint64_t* v1, int level,
                                      uint32_t npolys, int* raw, void* stream) {
+    return tg_tensor2_c2_inverse_strided(ctx, c2, c2_eval, x1, y1, u1, v1, nullptr, level, npolys, raw, stream);
+}
+
+// Tight copies of npolys polys `stride` words apart (one 2-D copy).
+static int gather_polys(u64* dst, const u64* src, u64 stride, u32 npolys, size_t words, cudaStream_t s) {
+    TG_CUDA(cudaMemcpy2DAsync(dst, words * 8, src, stride * 8, words * 8, npolys, cudaMemcpyDeviceToDevice, s));
+    return TG_OK;
+}
+
+extern "C" int tg_tensor2_c2_inverse_strided(tg_context* ctx, uint64_t* c2, uint64_t* c2_eval, const uint64_t* x1,
+                                             const uint64_t* y1, const uint64_t* u1, const uint64_t* v1,
+                                             const uint64_t* op_strides, int level, uint32_t npolys, int* raw,
+                                             void* stream) {
     if (raw) *raw = 0;
     if ((u1 == nullptr) != (v1 == nullptr)) return fail(TG_E_ARG, "[ckks] the second product needs both operands");
     if (!ctx) return fail(TG_E_ARG, "[ring] null context");
@@ -461,9 +474,33 @@ extern "C" int tg_tensor2_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2
     }();
     // the fused chunk phase needs every row on the FP64 path, a warp plan and
     // the unstaged chunk kernel; otherwise the two separate passes
+    const size_t tight = size_t(level + 1) * R.N;
+    u64 st[4] = {tight, tight, tight, tight};  // words between the polys of x1, y1, u1, v1
+    bool strided = false;
+    if (op_strides)
+        for (int i = 0; i < 4; ++i)
+            if (op_strides[i] && op_strides[i] != tight) {
+                if (op_strides[i] < tight) return fail(TG_E_ARG, "[ckks] operand stride below the poly size");
+                st[i] = op_strides[i];
+                strided = true;
+            }
     if (off || NTT_CHUNK_STAGE || !ntt_pair_ok(ctx) || !warp_plan(R.logN, e1, e2) || npolys > 65535) {
-        if (int rc = tg_tensor2(ctx, nullptr, nullptr, c2_eval, x1, x1, y1, y1, u1, u1, v1, v1, level, npolys, stream))
-            return rc;
+        // two separate passes over tight operands (strided views gathered first)
+        const u64* ops[4] = {x1, y1, u1, v1};
+        void* tmp = nullptr;
+        if (strided) {
+            TG_CUDA(cudaMallocFromPoolAsync(&tmp, 4 * tight * npolys * 8, ctx->pool, s));
+            for (int i = 0; i < 4; ++i)
+                if (ops[i] && st[i] != tight) {
+                    u64* d = static_cast<u64*>(tmp) + size_t(i) * tight * npolys;
+                    if (int rc = gather_polys(d, ops[i], st[i], npolys, tight, s)) return rc;
+                    ops[i] = d;
+                }
+        }
+        int rc = tg_tensor2(ctx, nullptr, nullptr, c2_eval, ops[0], ops[0], ops[1], ops[1], ops[2], ops[2], ops[3],
+                            ops[3], level, npolys, stream);
+        if (tmp) cudaFreeAsync(tmp, s);
+        if (rc) return rc;
         return tg_ntt_inverse_oop(ctx, c2, c2_eval, level, 0, npolys, stream);
     }
     // raw output (the inverse column phase's doubles, no N^-1: ModUp folds it
@@ -479,9 +516,9 @@ extern "C" int tg_tensor2_c2_inverse(tg_context* ctx, uint64_t* c2, uint64_t* c2
         // + the tensor's 2 (4) reads, 1 write
         ProfScope prof(ctx, TG_OP_NTT_INV, 16.0 * words + (u1 ? 40.0 : 24.0) * words, s, 2);
         const bool pair = true;
-        if (e1 == 8) launch_inv_tensor_w<8, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, out_raw, u1, v1);
-        else if (e2 == 8) launch_inv_tensor_w<4, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, false, u1, v1);
-        else launch_inv_tensor_w<4, 4>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, false, u1, v1);
+        if (e1 == 8) launch_inv_tensor_w<8, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, out_raw, u1, v1, st);
+        else if (e2 == 8) launch_inv_tensor_w<4, 8>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, false, u1, v1, st);
+        else launch_inv_tensor_w<4, 4>(R, ctx->sms, c2, c2_eval, x1, y1, npolys, level, s, pair, false, u1, v1, st);
     }
     if (raw) *raw = (out_raw && e1 == 8) ? 1 : 0;
     TG_LAUNCH_CHECK();

@@ -806,7 +806,7 @@ template <int E>
 __global__ void __launch_bounds__(256, NTT_CHUNK_MIN_BLOCKS)
 kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb, int level, u32 logN1,
               u32 row0, const u64* tx = nullptr, const u64* ty = nullptr, u64* c2e = nullptr,
-              const u64* tu = nullptr, const u64* tv = nullptr) {
+              const u64* tu = nullptr, const u64* tv = nullptr, u64 sx = 0, u64 sy = 0, u64 su = 0, u64 sv = 0) {
     using Gm = WGeo<E>;
     // row r of every poly (rows [row0, row0 + gridDim.y) are transformed)
     const u32 r = row0 + blockIdx.y, pend = min(npolys, (blockIdx.z + 1) * ppb);
@@ -881,14 +881,14 @@ kw_inv_chunks(DevRing R, u64* data, const u64* src, u32 rpp, u32 npolys, u32 ppb
         // (tensor mode) chunk of c2 = x1 y1: exact FP64 product, canonical,
         // stored for ModUp's own rows
         auto tload = [&](u64 (&t)[E], u32 pp) {
-            const size_t o = size_t(pp * rpp + r) * N + off;
-            u64 yv[E];
-            ld_vec<E>(t, tx + o, lane);
-            ld_vec<E>(yv, ty + o, lane);
+            const size_t o = size_t(pp * rpp + r) * N + off, ro = size_t(r) * N + off;
+            u64 yv[E];  // operand polys: sx .. sv words apart (level-dropped views read in place)
+            ld_vec<E>(t, tx + size_t(pp) * sx + ro, lane);
+            ld_vec<E>(yv, ty + size_t(pp) * sy + ro, lane);
             if (tu) {  // x1 y1 + u1 v1: |sum| < 1.62q
                 u64 uv[E], vv[E];
-                ld_vec<E>(uv, tu + o, lane);
-                ld_vec<E>(vv, tv + o, lane);
+                ld_vec<E>(uv, tu + size_t(pp) * su + ro, lane);
+                ld_vec<E>(vv, tv + size_t(pp) * sv + ro, lane);
 #pragma unroll
                 for (int j = 0; j < E; ++j)
                     t[j] = fp_canonical(__dadd_rn(fp_mulmod_qi(u2d(t[j]), u2d(yv[j]), qd, qi),
@@ -1177,12 +1177,13 @@ void launch_fwd_w(const DevRing& R, int sms, u64* data, const u64* src, u32 rpp,
 template <int E1, int E2>
 void launch_inv_tensor_w(const DevRing& R, int sms, u64* data, u64* c2e, const u64* x1, const u64* y1, u32 npolys,
                          int level, cudaStream_t s, bool pair, bool raw = false, const u64* u1 = nullptr,
-                         const u64* v1 = nullptr) {
+                         const u64* v1 = nullptr, const u64* st = nullptr) {
     set_smem_attrs<E1, E2>();
     const u32 M1 = 32 * E1, rpp = u32(level) + 1;
     const u32 p2 = polys_per_block(M1 / 8, rpp, npolys, sms);
     kw_inv_chunks<E2><<<dim3(M1 / 8, rpp, (npolys + p2 - 1) / p2), 256, chunk_smem<E2>(), s>>>(
-        R, data, nullptr, rpp, npolys, p2, level, WGeo<E1>::LOGM, 0, x1, y1, c2e, u1, v1);
+        R, data, nullptr, rpp, npolys, p2, level, WGeo<E1>::LOGM, 0, x1, y1, c2e, u1, v1, st ? st[0] : u64(rpp) * R.N,
+        st ? st[1] : u64(rpp) * R.N, st ? st[2] : u64(rpp) * R.N, st ? st[3] : u64(rpp) * R.N);
     launch_inv_cols_any<E1, E2>(R, sms, data, rpp, npolys, level, s, 0, rpp, pair, raw);
 }
 
