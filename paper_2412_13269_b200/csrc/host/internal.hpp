@@ -71,8 +71,8 @@ inline const u64* strided_group(const std::vector<Poly>& parts, std::size_t firs
     const Poly& p0 = parts[first];
     stride = p0.words();
     if (n == 1 || contiguous(parts, first, n)) return p0.data();
-    bool uniform = true;
-    const std::size_t d = parts[first + 1].offset() - p0.offset();
+    bool uniform = parts[first + 1].storage() == p0.storage() && parts[first + 1].offset() > p0.offset();
+    const std::size_t d = uniform ? parts[first + 1].offset() - p0.offset() : 0;
     for (std::size_t i = 0; i < n && uniform; ++i) {
         const Poly& p = parts[first + i];
         uniform = p.storage() == p0.storage() && p.level() == p0.level() && p.nspecial() == p0.nspecial() &&
