@@ -9,10 +9,14 @@
 //                            for d = 15/27/63; with lazy relinearisation
 //                            (default) one key switch fewer per node whose
 //                            remainder is a giant-step node too.
-// Every ladder step and every combination step runs as ONE fused residue pass
-// (tg_lincomb) after the relinearised product; scales and noise bounds follow
-// the reference's add_inplace / mul_scalar / sub_inplace / add_scalar /
-// rescale sequence exactly.
+// Every ladder step T_k = rescale(2 T_a T_b - v T_c | - 1) leaves its
+// product's key switch in one pass (Ladder::fused_step: the linear step and
+// the rescale inside ModDown, KeyContext::relinearize_tensor_ladder; rings
+// with 60-bit rows and small launches relinearise, then one tg_lincomb pass);
+// every combination step is ONE fused residue pass (tg_lincomb), and the base
+// blocks of one BSGS polynomial share a multi-output pass (tg_lincomb_multi).
+// Scales and noise bounds follow the reference's add_inplace / mul_scalar /
+// sub_inplace / add_scalar / rescale sequence exactly.
 // Eval-form pipeline (opt-in: TG_EVAL_PIPELINE=1 or set_eval_pipeline):
 // products, combinations and rescales stay in evaluation form
 // (relinearize_eval / tg_rescale_eval); the result is converted to
