@@ -37,7 +37,8 @@ def lazy(G, request):
     G.set_lazy_relin(was)
 
 
-@pytest.mark.parametrize("deg,odd", [(7, False), (15, False), (15, True), (27, True), (31, False), (63, True)])
+@pytest.mark.parametrize("deg,odd", [(3, False), (5, True), (7, False), (15, False), (15, True), (27, True),
+                                     (31, False), (63, True)])
 def test_bsgs_bit_exact_vs_oracle(G, R, pair, deg, odd, lazy):
     g, r = pair
     rng = R.Rng(1000 + deg)
