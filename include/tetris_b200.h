@@ -255,6 +255,12 @@ int tg_lincomb_multi(tg_context* ctx, uint32_t nouts, uint64_t* const* outs, uin
                      const uint64_t* add_per_row, int level, uint32_t nparts, uint32_t add_polys,
                      void* stream);
 
+/* dst[i*words .. (i+1)*words) = srcs[i][0 .. words) for i < npolys (device
+ * pointers in a host array): stacking single ciphertexts' parts into one
+ * part-major batch block with one launch (stack_ciphertexts). words even. */
+int tg_gather_polys(tg_context* ctx, uint64_t* dst, const uint64_t* const* srcs, uint32_t npolys,
+                    uint64_t words, void* stream);
+
 /* ---- CKKS products ------------------------------------------------------ */
 /* Evaluator::mul tensor step (ckks.hpp:229-237), eval form inputs:
  * p0 = x0*y0, p1 = x0*y1 + x1*y0, p2 = x1*y1. Outputs must not alias inputs. */

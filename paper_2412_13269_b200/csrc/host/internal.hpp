@@ -53,11 +53,13 @@ inline const u64* group_data(const std::vector<Poly>& parts, std::size_t first, 
     const Poly& p0 = parts[first];
     const RingParams& ring = p0.ring();
     std::vector<Poly> g = fresh_parts(ring, int(n), p0.level(), p0.form(), p0.nspecial());
+    std::vector<const u64*> srcs(n);
     for (std::size_t i = 0; i < n; ++i) {
         parts[first + i].check_shape(p0);
-        check_tg(tg_memcpy_d2d(ring.dev(), const_cast<u64*>(g[i].data()), parts[first + i].data(), g[i].words() * 8,
-                               ring.stream()));
+        srcs[i] = parts[first + i].data();
     }
+    check_tg(tg_gather_polys(ring.dev(), const_cast<u64*>(g[0].data()), srcs.data(), u32(n), g[0].words(),
+                             ring.stream()));  // one launch for the group
     keep.insert(keep.end(), g.begin(), g.end());
     return g[0].data();
 }

@@ -799,10 +799,12 @@ Ciphertext stack_ciphertexts(const std::vector<Ciphertext>& cts) {
     const Poly& p0 = c0.parts[0];
     const RingParams& ring = p0.ring();
     std::vector<Poly> out = fresh_parts(ring, int(deg1 * B), p0.level(), p0.form(), p0.nspecial());
+    // one gather launch for the whole part-major block (was one copy per poly)
+    std::vector<const u64*> srcs(deg1 * B);
     for (std::size_t k = 0; k < deg1; ++k)
-        for (u32 i = 0; i < B; ++i)
-            check_tg(tg_memcpy_d2d(ring.dev(), const_cast<u64*>(out[k * B + i].data()), cts[i].parts[k].data(),
-                                   out[k * B + i].words() * 8, ring.stream()));
+        for (u32 i = 0; i < B; ++i) srcs[k * B + i] = cts[i].parts[k].data();
+    check_tg(tg_gather_polys(ring.dev(), const_cast<u64*>(out[0].data()), srcs.data(), u32(srcs.size()), p0.words(),
+                             ring.stream()));
     Ciphertext r;
     r.parts = std::move(out);
     r.batch = B;

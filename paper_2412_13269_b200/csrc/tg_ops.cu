@@ -335,6 +335,21 @@ __global__ void k_tensor(DevRing R, Shape S, u64* p0, u64* p1, u64* p2, const u6
     }
 }
 
+// npolys polys from scattered sources into one contiguous block (stacking
+// single ciphertexts into a part-major batch): one launch instead of one
+// device-to-device copy per poly.
+constexpr int kGatherMax = 64;
+struct GatherSrc {
+    const u64* p[kGatherMax];
+};
+__global__ void k_gather_polys(u64* __restrict__ dst, GatherSrc S, u64 words) {
+    const u64* __restrict__ src = S.p[blockIdx.y];
+    u64* out = dst + u64(blockIdx.y) * words;
+    const u64 n2 = words / 2;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n2; i += u64(gridDim.x) * blockDim.x)
+        reinterpret_cast<ulonglong2*>(out)[i] = reinterpret_cast<const ulonglong2*>(src)[i];
+}
+
 // Sum of two tensors (lazy relinearisation, Evaluator::mul2_relin_rescale:
 // add(mul(x, y), mul(u, v)), ckks.hpp:229-237 twice then :201-208) in one
 // pass; p0 / p1 null: only c2 = x1 y1 + u1 v1.
@@ -666,6 +681,27 @@ extern "C" int tg_tensor(tg_context* ctx, uint64_t* p0, uint64_t* p1, uint64_t* 
     PROF(TG_OP_TENSOR, 56 * S.words);
     k_tensor<<<grid_for(S.words), kThreads, 0, as_stream(stream)>>>(ctx->ring, S, p0, p1, p2, x0, x1, y0, y1);
     TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+extern "C" int tg_gather_polys(tg_context* ctx, uint64_t* dst, const uint64_t* const* srcs, uint32_t npolys,
+                               uint64_t words, void* stream) {
+    if (!ctx) return fail(TG_E_ARG, "[ring] null context");
+    if (npolys == 0 || words == 0) return TG_OK;
+    if (words % 2) return fail(TG_E_ARG, "[ring] gather: odd word count");
+    DeviceGuard guard(ctx->device);
+    cudaStream_t s = as_stream(stream);
+    for (uint32_t first = 0; first < npolys; first += kGatherMax) {
+        const uint32_t n = std::min<uint32_t>(kGatherMax, npolys - first);
+        GatherSrc S{};
+        for (uint32_t i = 0; i < n; ++i) {
+            if (!srcs[first + i]) return fail(TG_E_ARG, "[ring] gather: null source");
+            S.p[i] = srcs[first + i];
+        }
+        const u32 bx = u32(std::min<u64>((words / 2 + kThreads - 1) / kThreads, 148u * 8u / std::max(1u, n / 4) + 1));
+        k_gather_polys<<<dim3(bx, n), kThreads, 0, s>>>(dst + u64(first) * words, S, words);
+        TG_LAUNCH_CHECK();
+    }
     return TG_OK;
 }
 
